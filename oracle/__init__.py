@@ -1,0 +1,1 @@
+"""Parity oracle — TEST INFRASTRUCTURE ONLY (see moe_oracle.py header)."""
