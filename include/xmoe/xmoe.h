@@ -1,0 +1,179 @@
+/*
+ * xmoe — B200-native (sm_100a) MoE-block hot path of X-MoE (arXiv 2508.13337).
+ *
+ * C-ABI drop-in boundary.  Plain pointers and sizes only; every operator is
+ * stream-ordered on caller-owned DEVICE buffers and returns a status code.
+ * Each entry point replaces one operator of the reference simulator's C++ API
+ * (namespace moesim, /root/reference/proj/include/moesim/*.hpp); the citation
+ * sits above each declaration.  The reference-shaped C++ adapter
+ * (include/xmoe/moesim_compat.hpp) is built on these calls.
+ *
+ * Conventions
+ *   - ids are int32; combine weights are float64 (the reference's `double`);
+ *   - XMOE_F64 operands use the reference layouts and reproduce its
+ *     arithmetic order bit for bit (parity mode);
+ *   - XMOE_BF16 operands are the performance path: bf16 storage, fp32
+ *     accumulation on tcgen05 tensor cores, weights in the K-major B200
+ *     layout documented per call;
+ *   - errors: the status codes below map 1:1 onto the reference's exception
+ *     types (error.hpp:10-38); xmoe_last_error() returns the reference's
+ *     message text (thread-local).
+ */
+#ifndef XMOE_XMOE_H_
+#define XMOE_XMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XMOE_ABI_VERSION 1
+
+/* status codes — moesim::ParseError .. PlanMismatch (error.hpp:10-38) */
+#define XMOE_OK 0
+#define XMOE_ERR_PARSE 1
+#define XMOE_ERR_VALIDATION 2
+#define XMOE_ERR_DIMENSION 3
+#define XMOE_ERR_INDEX 4
+#define XMOE_ERR_COUNT_MISMATCH 5
+#define XMOE_ERR_PLAN_MISMATCH 6
+#define XMOE_ERR_CUDA 10
+#define XMOE_ERR_NCCL 11
+#define XMOE_ERR_INTERNAL 99
+
+/* element types */
+#define XMOE_F64 0
+#define XMOE_BF16 1
+
+/* expert-parallel dispatch modes */
+#define XMOE_DISPATCH_NAIVE 0 /* pf_dispatch/pf_combine (pf_pipeline.cpp:12-135) */
+#define XMOE_DISPATCH_RBD 1   /* per-GPU redundancy bypass (rbd.cpp:26-358, node_of = rank) */
+
+typedef struct xmoe_ctx xmoe_ctx;
+typedef struct xmoe_layer xmoe_layer;
+
+int xmoe_abi_version(void);
+const char* xmoe_last_error(void);
+
+/* ------------------------------------------------------------------ context
+ * One context per process and device.  world/rank describe the expert-
+ * parallel group (moesim::Comm / WorkerGroup, collectives.hpp:71-76):
+ *   rank >= 0 : this process is rank `rank` of `world` processes, one GPU
+ *               each; the exchange runs over NCCL on NVLink.  nccl_id is the
+ *               128-byte ncclUniqueId from xmoe_nccl_unique_id() on rank 0
+ *               (NULL when world == 1).
+ *   rank == -1: this process drives all `world` workers itself on `device`
+ *               (the reference's SPMD "all ranks in one call" shape,
+ *               SURVEY §8(b)); the exchange is an on-device row move.      */
+int xmoe_nccl_unique_id(void* out_128_bytes);
+int xmoe_ctx_create(int device, int world, int rank, const void* nccl_id, xmoe_ctx** out);
+int xmoe_ctx_destroy(xmoe_ctx* ctx);
+
+/* ------------------------------------------------------------------ operators */
+
+/* moesim::gate_forward (gating.hpp:35, gating.cpp:14-57).
+ * x [S,H]; F64: wg [H,E] (reference layout); BF16: wg [E,H] (K-major).
+ * Outputs top_experts [S,k] (descending prob, ties -> lower id) and the raw
+ * softmax probabilities weights [S,k]; renorm != 0 divides by their sum
+ * (restated beyond the reference).  logits [S,E] fp64 is optional. */
+int xmoe_gate_forward(xmoe_ctx* ctx, int dtype, const void* x, const void* wg, int64_t S,
+                      int64_t H, int64_t E, int64_t k, int renorm, int32_t* top_experts,
+                      double* weights, double* logits, void* stream);
+
+/* moesim::pft_construct (pft.hpp:32-38, pft.cpp:12-60).
+ * top [S,k], w [S,k] -> expert-major packed ERI arrays of B <= S*k rows:
+ * token_ids[B], expert_ids[B], cw[B], tokens_per_expert[E]; B is written to
+ * *B_dev (device int32).  slot_pos [S,k] (optional) receives, per token, the
+ * packed rows of its kept copies ascending, padded with -1.  validate != 0
+ * checks id range/distinctness (synchronises the stream). */
+int xmoe_pft_construct(xmoe_ctx* ctx, const int32_t* top, const double* w, int64_t S, int64_t k,
+                       int64_t E, int64_t cap, int32_t* token_ids, int32_t* expert_ids,
+                       double* cw, int32_t* tokens_per_expert, int32_t* slot_pos,
+                       int32_t* B_dev, int validate, void* stream);
+
+/* moesim::gather_rows (pft.hpp:41, pft.cpp:68-77): out[i] = src[ids[i]]. */
+int xmoe_gather_rows(xmoe_ctx* ctx, int dtype, const void* src, int64_t rows, int64_t cols,
+                     const int32_t* ids, int64_t n, void* out, int validate, void* stream);
+
+/* moesim::scatter_combine (pft.hpp:45-46, pft.cpp:79-91): out [S,cols] =
+ * sum over i ascending of weights[i] * rows[i] into token_ids[i].
+ * Deterministic gather-reduce (no atomics); F64 is bit-exact. */
+int xmoe_scatter_combine(xmoe_ctx* ctx, int dtype, const void* rows, int64_t n, int64_t cols,
+                         const int32_t* token_ids, const double* weights, int64_t S, void* out,
+                         int validate, void* stream);
+
+/* moesim::grouped_expert_mlp (pf_pipeline.hpp:38-39, pf_pipeline.cpp:83-105).
+ * in [rows,H]; rows_per_expert [G] (device); expert i covers the next
+ * rows_per_expert[i] rows.  `rows` bounds the buffer; the real total is
+ * sum(rows_per_expert).  F64: w1 [G,H,F], w2 [G,F,H] (reference layout).
+ * BF16: w1 [G,F,H], w2 [G,H,F] (K-major; tcgen05 grouped GEMM). */
+int xmoe_grouped_mlp(xmoe_ctx* ctx, int dtype, const void* in, int64_t rows,
+                     const int32_t* rows_per_expert, int64_t G, const void* w1, const void* w2,
+                     int64_t H, int64_t F, void* out, void* stream);
+
+/* The tcgen05 grouped GEMM itself (BF16): D[rows,N] = A[rows,K] . B_g[N,K]^T
+ * per group, optional ReLU epilogue.  Exposed for the numerics tests. */
+int xmoe_grouped_gemm_bf16(xmoe_ctx* ctx, const void* A, int64_t rows, int64_t K,
+                           const int32_t* rows_per_group, int64_t G, const void* B, int64_t N,
+                           void* D, int relu, void* stream);
+
+/* ------------------------------------------------------------------ layer
+ * One MoE layer's weights resident in HBM in the B200 layout, plus the
+ * workspace of its forward pass.  Weights are DEVICE pointers in the
+ * reference layouts (moe_instance.hpp:17-21) and dtype: gate [H,E],
+ * w1 [E_local,H,F], w2 [E_local,F,H], where E_local = E/world experts owned
+ * by this rank (all E when rank == -1); shared experts sw1 [n_shared,H,Fs],
+ * sw2 [n_shared,Fs,H] (restated beyond the reference; may be NULL). */
+typedef struct {
+    int64_t num_experts;     /* E */
+    int64_t model_dim;       /* H */
+    int64_t ffn_dim;         /* F */
+    int64_t top_k;           /* k */
+    int64_t max_token_count; /* capacity per expert per source rank */
+    int64_t n_shared;        /* shared experts (0 = none) */
+    int64_t shared_ffn_dim;  /* Fs */
+    int64_t max_tokens;      /* S bound per rank (workspace sizing) */
+    int32_t dtype;           /* XMOE_F64 | XMOE_BF16 */
+    int32_t renorm;          /* top-k renormalisation (0 = reference) */
+    int32_t dispatch_mode;   /* XMOE_DISPATCH_NAIVE | XMOE_DISPATCH_RBD */
+    int32_t reserved;
+    uint64_t seed;           /* RBD pilot seed (salted per rank: salt_seed(seed, w, 0)) */
+} xmoe_layer_desc;
+
+int xmoe_layer_create(xmoe_ctx* ctx, const xmoe_layer_desc* desc, const void* gate,
+                      const void* w1, const void* w2, const void* sw1, const void* sw2,
+                      xmoe_layer** out);
+int xmoe_layer_destroy(xmoe_layer* layer);
+
+/* moesim::pf_moe_forward / rbd_moe_forward (pf_pipeline.hpp:48-49, rbd.hpp:92)
+ * selected by desc->dispatch_mode.  x/out: [n_local, S, H] where n_local = 1
+ * for a rank >= 0 context and world for rank == -1.  Device buffers. */
+int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S, void* out,
+                     void* stream);
+
+/* moesim::ssmb_forward (ssmb.hpp:23-26, ssmb.cpp:12-46): x_full [S,H] is the
+ * whole sequence on every rank; rank g runs rows [g*(S/G), ...) (last rank
+ * takes the remainder) through the layer with every expert local
+ * (the layer must hold all E experts), then an all-gather restores
+ * out_full [S,H] on every rank.  G == world. */
+int xmoe_ssmb_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x_full, int64_t S,
+                      void* out_full, void* stream);
+
+/* Byte ledger of the last forward on this layer (collectives.hpp:31-49):
+ * out[0..n) = { dispatch_rows_self, dispatch_rows_offrank,
+ *               dispatch_meta_offrank, combine_rows_self,
+ *               combine_rows_offrank, routed_copies, unique_rows_offrank,
+ *               copies_offrank } summed over this context's ranks. */
+int xmoe_layer_ledger(xmoe_layer* layer, uint64_t* out, int n);
+
+/* Per-stage device time of the last forward (ms, CUDA events), order:
+ * gate, pft, dispatch, gemm, combine, total.  Requires timing enabled. */
+int xmoe_layer_set_timing(xmoe_layer* layer, int enable);
+int xmoe_layer_stage_ms(xmoe_layer* layer, float* out, int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XMOE_XMOE_H_ */

@@ -334,7 +334,11 @@ def _ordered_axpy(out, dst_ids, weights, rows):
 # ---------------------------------------------------------------------------
 
 def grouped_expert_mlp(inp: np.ndarray, rows_per_expert, w: LayerWeights,
-                       first_expert: int) -> np.ndarray:
+                       first_expert: int, exact: bool = True) -> np.ndarray:
+    """``exact=False`` swaps the ordered matmul for BLAS (same maths, last-ulp
+    differences) — only for comparisons against the bf16 path, whose
+    tolerance is ~1e-2."""
+    mm = matmul if exact else (lambda a, b: np.asarray(a, np.float64) @ np.asarray(b, np.float64))
     inp = np.asarray(inp, dtype=np.float64)
     out = np.zeros_like(inp)
     off = 0
@@ -346,8 +350,8 @@ def grouped_expert_mlp(inp: np.ndarray, rows_per_expert, w: LayerWeights,
         w2 = w.w2[first_expert + i]
         if inp.shape[1] != w1.shape[0]:
             raise DimensionError("grouped_expert_mlp: activation width mismatch")
-        mid = relu(matmul(inp[off:off + n], w1))
-        out[off:off + n] = matmul(mid, w2)
+        mid = relu(mm(inp[off:off + n], w1))
+        out[off:off + n] = mm(mid, w2)
         off += n
     if off != inp.shape[0]:
         raise CountMismatch("grouped_expert_mlp: segment counts disagree with input rows")
@@ -464,7 +468,7 @@ def pf_combine(node_of, disp: PfDispatch, expert_out, pfts, seq_lens,
 
 def pf_moe_forward(tokens_per_worker, w: LayerWeights, num_experts: int, top_k: int,
                    cap: int, node_of=None, ledger: Ledger | None = None, renorm=False,
-                   return_pfts=False):
+                   return_pfts=False, exact=True):
     """pf_pipeline.cpp:137-169."""
     W = len(tokens_per_worker)
     node_of = list(range(W)) if node_of is None else list(node_of)
@@ -478,7 +482,7 @@ def pf_moe_forward(tokens_per_worker, w: LayerWeights, num_experts: int, top_k: 
         p.x = gather_rows(x, p.token_ids)
         pfts.append(p)
     disp = pf_dispatch(node_of, pfts, num_experts, ledger)
-    eo = [grouped_expert_mlp(disp.expert_input[j], disp.recv_per_expert[j], w, j * el)
+    eo = [grouped_expert_mlp(disp.expert_input[j], disp.recv_per_expert[j], w, j * el, exact)
           for j in range(W)]
     out = pf_combine(node_of, disp, eo, pfts, [x.shape[0] for x in tokens_per_worker], ledger)
     return (out, pfts, disp, eo) if return_pfts else out
@@ -652,28 +656,27 @@ def ssmb_shards(S: int, G: int):
 # Shared experts — restatement beyond the reference (parity unpinned by it)
 # ---------------------------------------------------------------------------
 
-def shared_expert_forward(x: np.ndarray, sw1: np.ndarray, sw2: np.ndarray) -> np.ndarray:
-    """Each shared expert s is the reference's expert FFN applied to every
-    token (grouped_expert_mlp over one segment of S rows,
-    pf_pipeline.cpp:83-105) and combined with weight 1.0
-    (scatter_combine with identity token ids, pft.cpp:79-91).  Shared experts
-    are added after the routed copies, in shared-expert order."""
-    S = x.shape[0]
-    acc = np.zeros((S, x.shape[1]))
-    for s in range(sw1.shape[0]):
-        y = matmul(relu(matmul(x, sw1[s])), sw2[s])
-        acc = acc + 1.0 * y
-    return acc
+def shared_expert_forward(x: np.ndarray, sw1: np.ndarray, sw2: np.ndarray,
+                          exact: bool = True) -> np.ndarray:
+    """n_shared shared experts of width Fs, each the reference's expert FFN
+    applied to every token (grouped_expert_mlp over one segment of S rows,
+    pf_pipeline.cpp:83-105).  As in DeepSeek-MoE they run as ONE FFN of width
+    n_shared*Fs (W1 concatenated along F, W2 along its rows): the sum over
+    shared experts is one ascending accumulation chain over the concatenated
+    inner dimension.  sw1 [ns, H, Fs], sw2 [ns, Fs, H]."""
+    ns, H, Fs = sw1.shape
+    w1c = np.concatenate([sw1[s] for s in range(ns)], axis=1)  # [H, ns*Fs]
+    w2c = np.concatenate([sw2[s] for s in range(ns)], axis=0)  # [ns*Fs, H]
+    mm = matmul if exact else (lambda a, b: np.asarray(a, np.float64) @ np.asarray(b, np.float64))
+    return mm(relu(mm(x, w1c)), w2c)
 
 
-def moe_layer_with_shared(x, w: LayerWeights, num_experts, top_k, cap, sw1, sw2):
-    """Routed (pf_moe_forward, W=1) then shared experts added token-wise."""
-    routed = pf_moe_forward([x], w, num_experts, top_k, cap)[0]
-    out = routed.copy()
-    for s in range(sw1.shape[0]):
-        y = matmul(relu(matmul(x, sw1[s])), sw2[s])
-        out = out + 1.0 * y
-    return out
+def moe_layer_with_shared(x, w: LayerWeights, num_experts, top_k, cap, sw1, sw2, exact=True):
+    """Routed copies combined first (pf_moe_forward, W=1; ascending expert),
+    then the shared-expert output added with weight 1.0 (axpy,
+    kernels_scalar.cpp:29-31)."""
+    routed = pf_moe_forward([x], w, num_experts, top_k, cap, exact=exact)[0]
+    return routed + 1.0 * shared_expert_forward(x, sw1, sw2, exact)
 
 
 # ---------------------------------------------------------------------------

@@ -1,0 +1,259 @@
+"""ctypes binding of the xmoe C-ABI (include/xmoe/xmoe.h) for tests and the
+bench driver.  Device memory and streams come from torch; every call goes
+straight to libxmoe.so.  There is no fallback: if the library is missing or
+the device is not an sm_100 part, construction raises."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+import torch
+
+from . import build as _build
+
+_LIB = None
+
+F64 = 0
+BF16 = 1
+NAIVE = 0
+RBD = 1
+
+ERROR_KINDS = {1: "ParseError", 2: "ValidationError", 3: "DimensionError", 4: "IndexError",
+               5: "CountMismatch", 6: "PlanMismatch", 10: "CudaError", 11: "NcclError",
+               99: "InternalError"}
+
+
+class XmoeError(RuntimeError):
+    """Status code + the reference's message text (error.hpp:10-38)."""
+
+    def __init__(self, code: int, msg: str):
+        self.code = code
+        self.kind = ERROR_KINDS.get(code, "Error")
+        self.msg = msg
+        super().__init__(f"{self.kind}: {msg}")
+
+
+class LayerDesc(C.Structure):
+    _fields_ = [("num_experts", C.c_int64), ("model_dim", C.c_int64), ("ffn_dim", C.c_int64),
+                ("top_k", C.c_int64), ("max_token_count", C.c_int64), ("n_shared", C.c_int64),
+                ("shared_ffn_dim", C.c_int64), ("max_tokens", C.c_int64), ("dtype", C.c_int32),
+                ("renorm", C.c_int32), ("dispatch_mode", C.c_int32), ("reserved", C.c_int32),
+                ("seed", C.c_uint64)]
+
+
+def header_symbols() -> list[str]:
+    """Every function the C-ABI header declares."""
+    hdr = os.path.join(_build.ROOT, "include", "xmoe", "xmoe.h")
+    txt = open(hdr).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(xmoe_\w+)\(", txt, re.M)))
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(_build.LIB):
+            raise ImportError(f"{_build.LIB} is not built (run __graft_entry__.build())")
+        L = C.CDLL(_build.LIB)
+        p, i64, i32 = C.c_void_p, C.c_int64, C.c_int
+        L.xmoe_last_error.restype = C.c_char_p
+        L.xmoe_abi_version.restype = C.c_int
+        L.xmoe_ctx_create.argtypes = [i32, i32, i32, p, C.POINTER(p)]
+        L.xmoe_ctx_destroy.argtypes = [p]
+        L.xmoe_nccl_unique_id.argtypes = [p]
+        L.xmoe_gate_forward.argtypes = [p, i32, p, p, i64, i64, i64, i64, i32, p, p, p, p]
+        L.xmoe_pft_construct.argtypes = [p, p, p, i64, i64, i64, i64, p, p, p, p, p, p, i32, p]
+        L.xmoe_gather_rows.argtypes = [p, i32, p, i64, i64, p, i64, p, i32, p]
+        L.xmoe_scatter_combine.argtypes = [p, i32, p, i64, i64, p, p, i64, p, i32, p]
+        L.xmoe_grouped_mlp.argtypes = [p, i32, p, i64, p, i64, p, p, i64, i64, p, p]
+        L.xmoe_grouped_gemm_bf16.argtypes = [p, p, i64, i64, p, i64, p, i64, p, i32, p]
+        L.xmoe_layer_create.argtypes = [p, C.POINTER(LayerDesc), p, p, p, p, p, C.POINTER(p)]
+        L.xmoe_layer_destroy.argtypes = [p]
+        L.xmoe_moe_forward.argtypes = [p, p, p, i64, p, p]
+        L.xmoe_ssmb_forward.argtypes = [p, p, p, i64, p, p]
+        L.xmoe_layer_ledger.argtypes = [p, C.POINTER(C.c_uint64), i32]
+        L.xmoe_layer_set_timing.argtypes = [p, i32]
+        L.xmoe_layer_stage_ms.argtypes = [p, C.POINTER(C.c_float), i32]
+        _LIB = L
+    return _LIB
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise XmoeError(rc, lib().xmoe_last_error().decode())
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float64:
+        return F64
+    if t.dtype == torch.bfloat16:
+        return BF16
+    raise XmoeError(2, f"unsupported dtype {t.dtype}")
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check(lib().xmoe_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class Context:
+    """xmoe_ctx: rank == -1 drives all `world` workers on this device."""
+
+    def __init__(self, device: int = 0, world: int = 1, rank: int = -1, nccl_id: bytes | None = None):
+        self.device = device
+        self.world = world
+        self.rank = rank
+        h = C.c_void_p()
+        idbuf = None if nccl_id is None else C.create_string_buffer(nccl_id, 128)
+        _check(lib().xmoe_ctx_create(device, world, rank, idbuf, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().xmoe_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ operators
+    def gate_forward(self, x, wg, k, renorm=False, want_logits=False):
+        S, H = x.shape
+        E = wg.shape[1] if x.dtype == torch.float64 else wg.shape[0]
+        top = torch.empty((S, k), dtype=torch.int32, device=x.device)
+        w = torch.empty((S, k), dtype=torch.float64, device=x.device)
+        lg = torch.empty((S, E), dtype=torch.float64, device=x.device) if want_logits else None
+        _check(lib().xmoe_gate_forward(self.h, _dtype_code(x), _ptr(x), _ptr(wg), S, H, E, k,
+                                       int(renorm), _ptr(top), _ptr(w), _ptr(lg), _stream()))
+        return (top, w, lg) if want_logits else (top, w)
+
+    def pft_construct(self, top, w, E, cap, validate=True):
+        S, k = top.shape
+        n = max(S * k, 1)
+        dev = top.device
+        tid = torch.empty(n, dtype=torch.int32, device=dev)
+        eid = torch.empty(n, dtype=torch.int32, device=dev)
+        cw = torch.empty(n, dtype=torch.float64, device=dev)
+        tpe = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
+        slot = torch.empty((S, k), dtype=torch.int32, device=dev)
+        B = torch.zeros(1, dtype=torch.int32, device=dev)
+        _check(lib().xmoe_pft_construct(self.h, _ptr(top), _ptr(w), S, k, E, cap, _ptr(tid),
+                                        _ptr(eid), _ptr(cw), _ptr(tpe), _ptr(slot), _ptr(B),
+                                        int(validate), _stream()))
+        b = int(B.item())
+        return tid[:b], eid[:b], cw[:b], tpe[:E], slot
+
+    def gather_rows(self, src, ids, validate=True):
+        n = ids.shape[0]
+        out = torch.empty((n, src.shape[1]), dtype=src.dtype, device=src.device)
+        _check(lib().xmoe_gather_rows(self.h, _dtype_code(src), _ptr(src), src.shape[0],
+                                      src.shape[1], _ptr(ids), n, _ptr(out), int(validate),
+                                      _stream()))
+        return out
+
+    def scatter_combine(self, rows, token_ids, weights, S, validate=True):
+        out = torch.empty((S, rows.shape[1]), dtype=rows.dtype, device=rows.device)
+        _check(lib().xmoe_scatter_combine(self.h, _dtype_code(rows), _ptr(rows), rows.shape[0],
+                                          rows.shape[1], _ptr(token_ids), _ptr(weights), S,
+                                          _ptr(out), int(validate), _stream()))
+        return out
+
+    def grouped_mlp(self, inp, rows_per_expert, w1, w2):
+        """F64: w1 [G,H,F], w2 [G,F,H]; BF16: w1 [G,F,H], w2 [G,H,F] (K-major)."""
+        rows, H = inp.shape
+        G = rows_per_expert.shape[0]
+        F = w1.shape[2] if inp.dtype == torch.float64 else w1.shape[1]
+        out = torch.empty_like(inp)
+        _check(lib().xmoe_grouped_mlp(self.h, _dtype_code(inp), _ptr(inp), rows,
+                                      _ptr(rows_per_expert), G, _ptr(w1), _ptr(w2), H, F,
+                                      _ptr(out), _stream()))
+        return out
+
+    def grouped_gemm_bf16(self, A, rows_per_group, B, N, relu=False, out=None):
+        rows, K = A.shape
+        G = rows_per_group.shape[0]
+        D = out if out is not None else torch.empty((rows, N), dtype=torch.bfloat16, device=A.device)
+        _check(lib().xmoe_grouped_gemm_bf16(self.h, _ptr(A), rows, K, _ptr(rows_per_group), G,
+                                            _ptr(B), N, _ptr(D), int(relu), _stream()))
+        return D
+
+
+class Layer:
+    """xmoe_layer: weights resident in HBM in the B200 layout + workspace.
+
+    gate [H,E], w1 [E_held,H,F], w2 [E_held,F,H] (reference layouts, device
+    tensors of the layer dtype); sw1 [ns,H,Fs], sw2 [ns,Fs,H] optional."""
+
+    def __init__(self, ctx: Context, *, num_experts, model_dim, ffn_dim, top_k, max_token_count,
+                 max_tokens, dtype, gate, w1, w2, sw1=None, sw2=None, renorm=False,
+                 dispatch_mode=NAIVE, seed=0):
+        self.ctx = ctx
+        ns = 0 if sw1 is None else sw1.shape[0]
+        fs = 0 if sw1 is None else sw1.shape[2]
+        self.desc = LayerDesc(num_experts, model_dim, ffn_dim, top_k, max_token_count, ns, fs,
+                              max_tokens, dtype, int(renorm), dispatch_mode, 0, seed)
+        self.dtype = dtype
+        self.H = model_dim
+        h = C.c_void_p()
+        _check(lib().xmoe_layer_create(ctx.h, C.byref(self.desc), _ptr(gate), _ptr(w1), _ptr(w2),
+                                       _ptr(sw1), _ptr(sw2), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().xmoe_layer_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def forward(self, x, out=None):
+        """x: [n_local, S, H] (or [S, H] when n_local == 1)."""
+        S = x.shape[-2]
+        out = torch.empty_like(x) if out is None else out
+        _check(lib().xmoe_moe_forward(self.ctx.h, self.h, _ptr(x), S, _ptr(out), _stream()))
+        return out
+
+    def ssmb_forward(self, x_full, out=None):
+        S = x_full.shape[0]
+        out = torch.empty_like(x_full) if out is None else out
+        _check(lib().xmoe_ssmb_forward(self.ctx.h, self.h, _ptr(x_full), S, _ptr(out), _stream()))
+        return out
+
+    LEDGER_KEYS = ["dispatch_rows_self", "dispatch_rows_offrank", "dispatch_meta_offrank",
+                   "combine_rows_self", "combine_rows_offrank", "routed_copies",
+                   "unique_rows_offrank", "copies_offrank"]
+
+    def ledger(self) -> dict:
+        buf = (C.c_uint64 * 8)()
+        _check(lib().xmoe_layer_ledger(self.h, buf, 8))
+        return dict(zip(self.LEDGER_KEYS, [int(v) for v in buf]))
+
+    def set_timing(self, on: bool):
+        _check(lib().xmoe_layer_set_timing(self.h, int(on)))
+
+    STAGES = ["gate", "pft", "dispatch", "experts", "shared", "combine", "total"]
+
+    def stage_ms(self) -> dict:
+        buf = (C.c_float * 7)()
+        _check(lib().xmoe_layer_stage_ms(self.h, buf, 7))
+        return dict(zip(self.STAGES, [float(v) for v in buf]))

@@ -1,0 +1,448 @@
+// Variable-length grouped GEMM on the 5th-generation tensor cores (sm_100a):
+// the fine-grained expert FFN of moesim::grouped_expert_mlp
+// (/root/reference/proj/src/pf_pipeline.cpp:83-105) as a bf16 tcgen05 kernel.
+//
+//   D[r, n] = act( sum_k A[r, k] * B_g[n, k] )   for rows r of group g
+//
+// A [rows, K] is the grouped expert input (K-major), B [G*N, K] the stacked
+// per-expert weights in K-major layout (W1^T / W2^T), D [rows, N].  Groups are
+// contiguous row segments whose sizes live in device memory, so the kernel
+// needs no host synchronisation and empty or oversized groups cost nothing
+// special.
+//
+// Structure (persistent, one CTA per SM, 6 warps):
+//   warp 0      TMA producer: 128x64 A box + 256x64 B box per stage,
+//               128B swizzle, 4-stage mbarrier ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (M=128, N<=256, K=16 per instruction, fp32 accumulate)
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> ReLU -> bf16/fp32 -> global,
+//               rows past the group end masked
+// Accumulators are double-buffered in TMEM (2 x 256 columns), so the epilogue
+// of tile i overlaps the MMAs of tile i+1.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace xmoe {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;
+constexpr int UK = 16;
+constexpr int kStages = 4;
+constexpr int kAccBufs = 2;
+constexpr int kTmemCols = 512;
+constexpr int kThreads = 192;
+constexpr int kMaxGroups = 1024;
+constexpr uint32_t kABytes = BM * BK * 2;
+constexpr uint32_t kBBytes = BN * BK * 2;
+constexpr uint32_t kStageBytes = kABytes + kBBytes;
+constexpr size_t kSmemBytes = 1024 /*align*/ + kStages * kStageBytes + 1024 /*barriers*/ +
+                              sizeof(int32_t) * 2 * (kMaxGroups + 1);
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                            int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor: K-major, 128B swizzle, 8-row core groups
+// 1024 B apart (SBO), LBO unused (1), descriptor version 1 (sm_100).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(1) << 16;
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+
+// Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major.
+__device__ __forceinline__ uint32_t make_idesc(int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+           (static_cast<uint32_t>(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+          "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- scheduler
+struct TileInfo {
+    int g, row0, rows_left, n0;
+};
+
+__device__ __forceinline__ TileInfo tile_of(int t, const int32_t* tile_start,
+                                            const int32_t* row_off, int G, int ntn) {
+    int lo = 0, hi = G - 1;  // last g with tile_start[g] <= t (skips empty groups)
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tile_start[mid] <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    const int local = t - tile_start[lo];
+    const int mb = local / ntn, nb = local % ntn;
+    TileInfo ti;
+    ti.g = lo;
+    ti.row0 = row_off[lo] + mb * BM;
+    ti.rows_left = (row_off[lo + 1] - row_off[lo]) - mb * BM;
+    ti.n0 = nb * BN;
+    return ti;
+}
+
+// ---------------------------------------------------------------- kernel
+template <typename OutT>
+__global__ void __launch_bounds__(kThreads, 1)
+    grouped_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                           const __grid_constant__ CUtensorMap tmap_b,
+                           const int32_t* __restrict__ rows_per_group, int G, int N, int K,
+                           OutT* __restrict__ D, int relu) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* smem_a = smem;
+    uint8_t* smem_b = smem + kStages * kABytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* full_bar = bars;
+    uint64_t* empty_bar = bars + kStages;
+    uint64_t* tfull_bar = bars + 2 * kStages;
+    uint64_t* tempty_bar = bars + 2 * kStages + kAccBufs;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * kAccBufs);
+    int32_t* tile_start = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 1024);
+    int32_t* row_off = tile_start + kMaxGroups + 1;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int ntn = (N + BN - 1) / BN;
+    const int nkb = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        int t = 0, r = 0;
+        for (int g = 0; g < G; ++g) {
+            tile_start[g] = t;
+            row_off[g] = r;
+            const int m = rows_per_group[g];
+            t += ((m + BM - 1) / BM) * ntn;
+            r += m;
+        }
+        tile_start[G] = t;
+        row_off[G] = r;
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int b = 0; b < kAccBufs; ++b) {
+            mbar_init(&tfull_bar[b], 1);
+            mbar_init(&tempty_bar[b], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmap_a);
+        prefetch_tmap(&tmap_b);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int num_tiles = tile_start[G];
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                const TileInfo ti = tile_of(t, tile_start, row_off, G, ntn);
+                const int brow = ti.g * N + ti.n0;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&empty_bar[stage], phase ^ 1);
+                    mbar_expect_tx(&full_bar[stage], kStageBytes);
+                    tma_load_2d(&tmap_a, &full_bar[stage], smem_a + stage * kABytes, kb * BK, ti.row0);
+                    tma_load_2d(&tmap_b, &full_bar[stage], smem_b + stage * kBBytes, kb * BK, brow);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            const TileInfo ti = tile_of(t, tile_start, row_off, G, ntn);
+            const int nw = min(BN, N - ti.n0);
+            const int n_mma = (nw + 15) & ~15;
+            const uint32_t idesc = make_idesc(n_mma);
+            const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
+            mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+            tc_fence_after();
+            for (int kb = 0; kb < nkb; ++kb) {
+                mbar_wait(&full_bar[stage], phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint64_t da = make_desc(smem_u32(smem_a + stage * kABytes));
+                    const uint64_t db = make_desc(smem_u32(smem_b + stage * kBBytes));
+#pragma unroll
+                    for (int kk = 0; kk < BK / UK; ++kk) {
+                        // +32 bytes along K inside the 128B swizzle atom
+                        mma_bf16(tmem_d, da + static_cast<uint64_t>(kk * 2),
+                                 db + static_cast<uint64_t>(kk * 2), idesc,
+                                 (kb > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    mma_commit(&empty_bar[stage]);
+                    if (kb == nkb - 1) mma_commit(&tfull_bar[acc]);
+                }
+                __syncwarp();
+                if (++stage == kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (++acc == kAccBufs) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    } else {
+        // ===================== epilogue (warps 2..5) =====================
+        const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            const TileInfo ti = tile_of(t, tile_start, row_off, G, ntn);
+            const int nw = min(BN, N - ti.n0);
+            mbar_wait(&tfull_bar[acc], acc_phase);
+            tc_fence_after();
+            const int r = quarter * 32 + lane;
+            const bool row_ok = r < ti.rows_left;
+            OutT* drow = D + static_cast<size_t>(ti.row0 + r) * N + ti.n0;
+            for (int c0 = 0; c0 < nw; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                              static_cast<uint32_t>(acc * BN + c0),
+                          v);
+                if (!row_ok) continue;
+                float f[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    f[i] = __uint_as_float(v[i]);
+                    if (relu) f[i] = fmaxf(f[i], 0.f);
+                }
+                const int cn = min(32, nw - c0);
+                if constexpr (sizeof(OutT) == 2) {
+                    if (cn == 32 && (N & 7) == 0) {
+                        int4* dst = reinterpret_cast<int4*>(drow + c0);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            int4 o;
+                            o.x = static_cast<int>(pack_bf16(f[8 * q + 0], f[8 * q + 1]));
+                            o.y = static_cast<int>(pack_bf16(f[8 * q + 2], f[8 * q + 3]));
+                            o.z = static_cast<int>(pack_bf16(f[8 * q + 4], f[8 * q + 5]));
+                            o.w = static_cast<int>(pack_bf16(f[8 * q + 6], f[8 * q + 7]));
+                            dst[q] = o;
+                        }
+                    } else {
+                        for (int i = 0; i < cn; ++i) drow[c0 + i] = __float2bfloat16_rn(f[i]);
+                    }
+                } else {
+                    if (cn == 32 && (N & 3) == 0) {
+                        float4* dst = reinterpret_cast<float4*>(drow + c0);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            dst[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+                    } else {
+                        for (int i = 0; i < cn; ++i) drow[c0 + i] = f[i];
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+            if (++acc == kAccBufs) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(kTmemCols)
+                     : "memory");
+    }
+}
+
+}  // namespace tc
+
+// ---------------------------------------------------------------- host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        XMOE_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        require(p != nullptr && q == cudaDriverEntryPointSuccess, XMOE_ERR_CUDA,
+                "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeFn>(p);
+    }
+    return fn;
+}
+
+// 2D bf16 K-major tensor [rows, K] with a (box_rows x 64) 128B-swizzled box.
+static CUtensorMap make_tmap(const void* base, long long rows, long long K, int box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(K) * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(tc::BK), static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                    const_cast<void*>(base), dims, strides, box, estr,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(XMOE_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
+
+template <typename OutT>
+static void launch_tc(const void* A, long long rows, int K, const int32_t* rows_per_group, int G,
+                      const void* B, int N, OutT* D, int relu, cudaStream_t st) {
+    require(G >= 1 && G <= tc::kMaxGroups, XMOE_ERR_VALIDATION, "grouped gemm: 1 <= groups <= 1024");
+    require(K % 8 == 0 && K > 0, XMOE_ERR_VALIDATION, "bf16 path requires K % 8 == 0");
+    require(N % 16 == 0 && N > 0, XMOE_ERR_VALIDATION, "bf16 path requires N % 16 == 0");
+    require((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0,
+            XMOE_ERR_VALIDATION, "bf16 operands must be 16-byte aligned");
+    if (rows == 0) return;
+    const CUtensorMap ta = make_tmap(A, rows, K, tc::BM);
+    const CUtensorMap tb = make_tmap(B, static_cast<long long>(G) * N, K, tc::BN);
+    static bool attr_set = false;
+    if (!attr_set) {
+        XMOE_CUDA(cudaFuncSetAttribute(tc::grouped_gemm_tc_kernel<OutT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(tc::kSmemBytes)));
+        attr_set = true;
+    }
+    // Upper bound on tiles from the row bound: every group could be one row
+    // short of a tile boundary.
+    const long long max_tiles =
+        ((rows + tc::BM - 1) / tc::BM + G) * static_cast<long long>((N + tc::BN - 1) / tc::BN);
+    int sms = 0;
+    XMOE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const int grid = static_cast<int>(max_tiles < sms ? max_tiles : sms);
+    tc::grouped_gemm_tc_kernel<OutT><<<grid, tc::kThreads, tc::kSmemBytes, st>>>(
+        ta, tb, rows_per_group, G, N, K, D, relu);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_grouped_gemm_bf16(const void* A, long long rows, int K, const int32_t* rows_per_group,
+                              int G, const void* B, int N, void* D, int relu, cudaStream_t st) {
+    launch_tc<__nv_bfloat16>(A, rows, K, rows_per_group, G, B, N, static_cast<__nv_bfloat16*>(D),
+                             relu, st);
+}
+
+void launch_grouped_gemm_bf16_f32out(const void* A, long long rows, int K,
+                                     const int32_t* rows_per_group, int G, const void* B, int N,
+                                     float* D, int relu, cudaStream_t st) {
+    launch_tc<float>(A, rows, K, rows_per_group, G, B, N, D, relu, st);
+}
+
+}  // namespace xmoe

@@ -1,0 +1,68 @@
+// Launchers of the xmoe device kernels (one translation unit each).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace xmoe {
+
+// gate.cu
+void launch_gate_logits_f64(const double* x, const double* wg, int S, int H, int E,
+                            double* logits, cudaStream_t st);
+void launch_gate_logits_bf16(const __nv_bfloat16* x, const __nv_bfloat16* wgt, int S, int H,
+                             int E, double* logits, cudaStream_t st);
+void launch_softmax_topk(const double* logits, int S, int E, int k, int renorm, int32_t* top,
+                         double* weights, cudaStream_t st);
+
+// pft.cu
+size_t bucket_ws_bytes(long long n, int K);
+void launch_pft(const int32_t* top, const double* w, int S, int k, int E, int cap,
+                int32_t* token_ids, int32_t* expert_ids, double* cw, int32_t* tpe,
+                int32_t* slot_pos, int32_t* B_dev, void* ws, cudaStream_t st);
+void launch_pft_validate(const int32_t* top, int S, int k, int E, unsigned long long* first_bad,
+                         cudaStream_t st);
+void launch_stable_csr(const int32_t* keys, int n, int K, int32_t* ptr, int32_t* perm, void* ws,
+                       cudaStream_t st);
+
+// permute.cu
+void launch_gather_rows(const void* src, long long rows, int row_bytes, const int32_t* ids,
+                        long long n, const int32_t* n_dev, void* out, int* err, cudaStream_t st);
+void launch_dispatch_dest(const int32_t* tpe_all, int W, int E, int src,
+                          const int32_t* expert_ids, const int32_t* B_dev, long long max_rows,
+                          int32_t* dest_rank, int32_t* dest_row, cudaStream_t st);
+void launch_scatter_rows(const void* x, int row_bytes, const int32_t* token_ids,
+                         const int32_t* B_dev, long long max_rows, const int32_t* dest_rank,
+                         const int32_t* dest_row, char* const* dest_bufs, cudaStream_t st);
+void launch_unscatter_rows(int row_bytes, const int32_t* B_dev, long long max_rows,
+                           const int32_t* dest_rank, const int32_t* dest_row,
+                           const char* const* src_bufs, void* out, cudaStream_t st);
+
+// combine.cu — out[t] = sum over t's copies c (ascending) of w[c] * row(c)
+// (+ addend[t]); row(c) = rows[c] or, with a table, tab[drank[c]][drow[c]].
+void launch_combine(int dtype, const void* rows, int H, const int32_t* ptr, const int32_t* idx,
+                    int k, const double* w, int S, const void* addend, void* out,
+                    cudaStream_t st, const char* const* tab = nullptr,
+                    const int32_t* drank = nullptr, const int32_t* drow = nullptr);
+
+// gemm_f64.cu
+void launch_grouped_gemm_f64(const double* A, long long rows_bound, int K,
+                             const int32_t* rows_per_group, int G, const double* B, int N,
+                             double* D, int relu, cudaStream_t st);
+
+// gemm_tc.cu
+void launch_grouped_gemm_bf16(const void* A, long long rows, int K, const int32_t* rows_per_group,
+                              int G, const void* B, int N, void* D, int relu, cudaStream_t st);
+void launch_grouped_gemm_bf16_f32out(const void* A, long long rows, int K,
+                                     const int32_t* rows_per_group, int G, const void* B, int N,
+                                     float* D, int relu, cudaStream_t st);
+
+// misc.cu
+void launch_recv_counts(const int32_t* tpe_all, int W, int E, int dst, int32_t* rpe,
+                        cudaStream_t st);
+void launch_fill_i32(int32_t* p, int n, int32_t v, cudaStream_t st);
+void launch_transpose(int dtype_in, const void* in, int batch, int rows, int cols,
+                      int dtype_out, void* out, cudaStream_t st);
+
+}  // namespace xmoe

@@ -1,0 +1,85 @@
+// Host-side state behind the C-ABI handles: context and MoE layer.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "xmoe/xmoe.h"
+
+namespace xmoe {
+
+// moesim::Comm analogue (collectives.hpp:71-76): the expert-parallel group.
+struct Ctx {
+    int device = 0;
+    int world = 1;
+    int rank = -1;          // -1: this process drives every rank on `device`
+    void* nccl = nullptr;   // ncclComm_t when rank >= 0 && world > 1
+    void* ws = nullptr;     // grow-only scratch for the stateless operators
+    size_t ws_bytes = 0;
+    void* dflag = nullptr;  // device error flag
+
+    int n_local() const { return rank < 0 ? world : 1; }
+    int rank_of(int i) const { return rank < 0 ? i : rank; }
+    void* scratch(size_t bytes);
+    int* err_flag();
+    ~Ctx();
+};
+
+// Per-rank buffers of one layer forward.
+struct Worker {
+    int rank = 0;
+    double* logits = nullptr;     // [S, E]
+    int32_t* top = nullptr;       // [S, k]
+    double* wts = nullptr;        // [S, k]
+    int32_t* token_ids = nullptr; // [S*k] packed ERI arrays (pft.hpp:17-25)
+    int32_t* expert_ids = nullptr;
+    double* cw = nullptr;
+    int32_t* slot_pos = nullptr;  // [S, k] kept packed rows per token, ascending
+    int32_t* B_dev = nullptr;     // packed row count
+    int32_t* tpe = nullptr;       // [E] tokens per expert (row of tpe_all when shared)
+    void* pft_ws = nullptr;
+    int32_t* dest_rank = nullptr; // [S*k] owner of each packed row
+    int32_t* dest_row = nullptr;  // [S*k] its row in the owner's grouped buffer
+    int32_t* rpe = nullptr;       // [El] rows per local expert (recv_per_expert)
+    void* recv = nullptr;         // [R_max, H] grouped expert input (PfDispatch::expert_input)
+    void* mid = nullptr;          // [R_max, F]
+    void* eout = nullptr;         // [R_max, H]
+    void* send = nullptr;         // [S*k, H] NCCL path: packed rows
+    void* back = nullptr;         // [S*k, H] NCCL path: returned rows, packed order
+    void* smid = nullptr;         // shared experts [S, Fs]
+    void* sout = nullptr;         // [S, H]
+    int32_t* s_rows = nullptr;
+};
+
+enum { kEvStart = 0, kEvGate, kEvPft, kEvDispatch, kEvGemm, kEvShared, kEvCombine, kNumEvents };
+
+struct Layer {
+    Ctx* ctx = nullptr;
+    xmoe_layer_desc d{};
+    int W = 1, E = 0, H = 0, F = 0, k = 0, El = 0, E_held = 0, Fs = 0;
+    size_t es = 2;
+    long long R_max = 0, S_max = 0, last_S = 0;
+    void* gate = nullptr;  // F64 [H,E]; BF16 [E,H]
+    void* w1 = nullptr;    // F64 [E_held,H,F]; BF16 [E_held,F,H]
+    void* w2 = nullptr;    // F64 [E_held,F,H]; BF16 [E_held,H,F]
+    void* sw1 = nullptr;   // merged shared: F64 [H,Fs]; BF16 [Fs,H]
+    void* sw2 = nullptr;   // F64 [Fs,H]; BF16 [H,Fs]
+    int32_t* tpe_all = nullptr;  // [W, E]
+    char** recv_tab = nullptr;   // device table: rank -> recv buffer (shared-device ranks)
+    char** eout_tab = nullptr;
+    std::vector<int32_t> h_tpe;
+    std::vector<Worker> workers;
+    std::vector<void*> allocs;
+    std::vector<cudaEvent_t> events;
+    bool timing = false;
+
+    void* alloc(size_t bytes);
+    void mark(int ev, cudaStream_t st);
+    void exchange_nccl(bool forward, cudaStream_t st);
+    void ledger(uint64_t* out, int n);
+    ~Layer();
+};
+
+}  // namespace xmoe

@@ -1,0 +1,190 @@
+// Row movement kernels: the padding-free permute (moesim::gather_rows,
+// /root/reference/proj/src/pft.cpp:68-77) and the expert-parallel placement
+// of packed rows into the receiver's grouped layout (pf_dispatch regroup,
+// src/pf_pipeline.cpp:47-79, done at the sender instead of after arrival).
+//
+// One warp per row, 16-byte vectors, several vectors in flight per lane,
+// L1::no_allocate on the streaming side.  HBM-bound: algorithmic bytes per
+// row are 2 * row_bytes (+4 B index).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace xmoe {
+
+constexpr int kRowWarps = 8;
+constexpr int kUnroll = 4;
+
+// Copy one row with the whole warp.  Rows whose size is a multiple of 16 B
+// (every bf16 row with H % 8 == 0) move as int4 vectors, kUnroll in flight per
+// lane; other sizes (odd-width parity rows) fall back to 8- or 2-byte words.
+__device__ __forceinline__ void warp_copy_row(const char* __restrict__ src, char* __restrict__ dst,
+                                              int row_bytes, int lane) {
+    if ((row_bytes & 15) == 0) {
+        const int nvec = row_bytes >> 4;
+        const int4* s4 = reinterpret_cast<const int4*>(src);
+        int4* d4 = reinterpret_cast<int4*>(dst);
+        int v = lane;
+        for (; v + 32 * (kUnroll - 1) < nvec; v += 32 * kUnroll) {
+            int4 r[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) r[u] = ld_nc_v4(s4 + v + 32 * u);
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) st_na_v4(d4 + v + 32 * u, r[u]);
+        }
+        for (; v < nvec; v += 32) st_na_v4(d4 + v, ld_nc_v4(s4 + v));
+    } else if ((row_bytes & 7) == 0) {
+        const long long* s8 = reinterpret_cast<const long long*>(src);
+        long long* d8 = reinterpret_cast<long long*>(dst);
+        for (int v = lane; v < (row_bytes >> 3); v += 32) d8[v] = s8[v];
+    } else {
+        const short* s2 = reinterpret_cast<const short*>(src);
+        short* d2 = reinterpret_cast<short*>(dst);
+        for (int v = lane; v < (row_bytes >> 1); v += 32) d2[v] = s2[v];
+    }
+}
+
+// out[i] = src[ids[i]] for i < n (n read from n_dev when given).
+__global__ void __launch_bounds__(32 * kRowWarps) gather_rows_kernel(
+    const char* __restrict__ src, long long rows, int row_bytes, const int32_t* __restrict__ ids,
+    long long n, const int32_t* __restrict__ n_dev, char* __restrict__ out,
+    int* __restrict__ err) {
+    const long long total = n_dev ? *n_dev : n;
+    const int lane = threadIdx.x & 31;
+    const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    for (long long i = warp; i < total; i += nwarps) {
+        const int id = ids[i];
+        if (id < 0 || id >= rows) {
+            if (lane == 0 && err) atomicExch(err, 1);
+            continue;
+        }
+        warp_copy_row(src + static_cast<size_t>(id) * row_bytes,
+                      out + static_cast<size_t>(i) * row_bytes, row_bytes, lane);
+    }
+}
+
+// Placement map for expert-parallel dispatch.  Source rank `src` holds its
+// packed rows expert-major (tokens_per_expert tpe_src[E]); packed row r of
+// expert e lands on rank j = e / El at grouped row
+//     expert_base_j[le] + sum_{s < src} tpe_s[e] + (r - blk_src[e])
+// which is the (local expert, source, position) order of pf_dispatch
+// (pf_pipeline.cpp:47-73).  tpe_all is the all-gathered [W, E] matrix.
+__global__ void dispatch_dest_kernel(const int32_t* __restrict__ tpe_all, int W, int E, int src,
+                                     const int32_t* __restrict__ expert_ids,
+                                     const int32_t* __restrict__ B_dev,
+                                     int32_t* __restrict__ dest_rank,
+                                     int32_t* __restrict__ dest_row) {
+    extern __shared__ int32_t sh[];
+    int32_t* blk = sh;              // [E+1] packed block start of each expert at src
+    int32_t* before = sh + E + 1;   // [E] rows of expert e from sources < src
+    int32_t* ebase = before + E;    // [E] grouped base of expert e on its owner
+    const int El = E / W;
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int e = 0; e < E; ++e) {
+            blk[e] = acc;
+            acc += tpe_all[src * E + e];
+        }
+        blk[E] = acc;
+        for (int e = 0; e < E; ++e) {
+            int b = 0;
+            for (int s = 0; s < src; ++s) b += tpe_all[s * E + e];
+            before[e] = b;
+        }
+        for (int j = 0; j < W; ++j) {
+            int a = 0;
+            for (int le = 0; le < El; ++le) {
+                const int e = j * El + le;
+                ebase[e] = a;
+                for (int s = 0; s < W; ++s) a += tpe_all[s * E + e];
+            }
+        }
+    }
+    __syncthreads();
+    const int B = *B_dev;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < B; r += gridDim.x * blockDim.x) {
+        const int e = expert_ids[r];
+        dest_rank[r] = e / El;
+        dest_row[r] = ebase[e] + before[e] + (r - blk[e]);
+    }
+}
+
+// Fused permute + placement for ranks that share one device (rank == -1
+// contexts, the reference's all-workers-in-one-call shape): packed row r of
+// source `src` is read straight from the token matrix (token_ids[r]) and
+// written into the owner's grouped buffer.
+__global__ void __launch_bounds__(32 * kRowWarps) scatter_rows_kernel(
+    const char* __restrict__ x, int row_bytes, const int32_t* __restrict__ token_ids,
+    const int32_t* __restrict__ B_dev, const int32_t* __restrict__ dest_rank,
+    const int32_t* __restrict__ dest_row, char* const* __restrict__ dest_bufs) {
+    const int B = *B_dev;
+    const int lane = threadIdx.x & 31;
+    const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    for (long long r = warp; r < B; r += nwarps) {
+        const int t = token_ids[r];
+        char* dst = dest_bufs[dest_rank[r]] + static_cast<size_t>(dest_row[r]) * row_bytes;
+        warp_copy_row(x + static_cast<size_t>(t) * row_bytes, dst, row_bytes, lane);
+    }
+}
+
+// Reverse of the placement: expert outputs come back from the owners'
+// grouped buffers into the source's packed order (pf_combine un-regroup +
+// reverse exchange, pf_pipeline.cpp:118-128).
+__global__ void __launch_bounds__(32 * kRowWarps) unscatter_rows_kernel(
+    int row_bytes, const int32_t* __restrict__ B_dev, const int32_t* __restrict__ dest_rank,
+    const int32_t* __restrict__ dest_row, const char* const* __restrict__ src_bufs,
+    char* __restrict__ out) {
+    const int B = *B_dev;
+    const int lane = threadIdx.x & 31;
+    const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    for (long long r = warp; r < B; r += nwarps) {
+        const char* s = src_bufs[dest_rank[r]] + static_cast<size_t>(dest_row[r]) * row_bytes;
+        warp_copy_row(s, out + static_cast<size_t>(r) * row_bytes, row_bytes, lane);
+    }
+}
+
+static int row_grid(long long n) {
+    const long long warps = n > 0 ? n : 1;
+    const long long blocks = (warps + kRowWarps - 1) / kRowWarps;
+    return static_cast<int>(blocks < 4 * kNumSMs ? blocks : 4 * kNumSMs);
+}
+
+void launch_gather_rows(const void* src, long long rows, int row_bytes, const int32_t* ids,
+                        long long n, const int32_t* n_dev, void* out, int* err,
+                        cudaStream_t st) {
+    if (!n_dev && n == 0) return;
+    gather_rows_kernel<<<row_grid(n), 32 * kRowWarps, 0, st>>>(
+        static_cast<const char*>(src), rows, row_bytes, ids, n, n_dev, static_cast<char*>(out),
+        err);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_dispatch_dest(const int32_t* tpe_all, int W, int E, int src,
+                          const int32_t* expert_ids, const int32_t* B_dev, long long max_rows,
+                          int32_t* dest_rank, int32_t* dest_row, cudaStream_t st) {
+    const int blocks = ceil_div(max_rows > 0 ? max_rows : 1, 256);
+    dispatch_dest_kernel<<<blocks < 4 * kNumSMs ? blocks : 4 * kNumSMs, 256,
+                           sizeof(int32_t) * (3 * E + 1), st>>>(tpe_all, W, E, src, expert_ids,
+                                                               B_dev, dest_rank, dest_row);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_scatter_rows(const void* x, int row_bytes, const int32_t* token_ids,
+                         const int32_t* B_dev, long long max_rows, const int32_t* dest_rank,
+                         const int32_t* dest_row, char* const* dest_bufs, cudaStream_t st) {
+    scatter_rows_kernel<<<row_grid(max_rows), 32 * kRowWarps, 0, st>>>(
+        static_cast<const char*>(x), row_bytes, token_ids, B_dev, dest_rank, dest_row, dest_bufs);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_unscatter_rows(int row_bytes, const int32_t* B_dev, long long max_rows,
+                           const int32_t* dest_rank, const int32_t* dest_row,
+                           const char* const* src_bufs, void* out, cudaStream_t st) {
+    unscatter_rows_kernel<<<row_grid(max_rows), 32 * kRowWarps, 0, st>>>(
+        row_bytes, B_dev, dest_rank, dest_row, src_bufs, static_cast<char*>(out));
+    XMOE_LAUNCH_CHECK();
+}
+
+}  // namespace xmoe

@@ -1,0 +1,104 @@
+"""GPU parity of the whole MoE-block forward (moesim::pf_moe_forward and the
+expert-parallel exchange) through the C-ABI layer object, against the pinned
+oracle on identical inputs.
+
+F64 (parity mode) must equal the reference bit for bit, including emulated
+expert-parallel groups of W workers on one GPU.  BF16 (performance mode):
+routing bit-exact on grid inputs; outputs within normwise 1e-2 and
+max_rel_diff (floor 1, matrix.hpp:47-62) 2e-2 of the fp64 oracle."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_oracle as O
+from tests.gpu_util import bf16_round, dev, grid_gate, grid_tokens, host, max_rel_diff, norm_rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _layer(ctx, dtype, E, H, F, k, cap, S, w, sw1=None, sw2=None, mode=0, seed=0):
+    from paper_2508_13337_b200 import capi
+    tdt = torch.float64 if dtype == capi.F64 else torch.bfloat16
+    return capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=cap,
+                      max_tokens=S, dtype=dtype, gate=dev(w.gate, tdt), w1=dev(w.w1, tdt),
+                      w2=dev(w.w2, tdt), sw1=None if sw1 is None else dev(sw1, tdt),
+                      sw2=None if sw2 is None else dev(sw2, tdt), dispatch_mode=mode, seed=seed)
+
+
+@pytest.mark.parametrize("W", [1, 2, 4, 8])
+def test_pf_forward_f64_bit_exact(W):
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, W, -1)
+    rng = O.Rng(31337 + W)
+    for trial in range(4):
+        E = W * (1 + rng.below(4))
+        k = 1 + rng.below(min(E, 4))
+        H = 2 + rng.below(7)
+        F = 2 + rng.below(7)
+        S = 2 + rng.below(31)
+        cap = 1 + rng.below(4) if trial % 2 == 0 else S * k
+        w = O.make_layer_weights(rng, E, H, F)
+        toks = np.array([rng.uniform(-1.0, 1.0) for _ in range(W * S * H)]).reshape(W, S, H)
+        want = O.pf_moe_forward(list(toks), w, E, k, cap)
+        L = _layer(ctx, capi.F64, E, H, F, k, cap, S, w)
+        got = host(L.forward(dev(toks)))
+        for i in range(W):
+            assert np.array_equal(got[i], want[i]), (trial, i)
+        led = L.ledger()
+        _, pfts, _, _ = O.pf_moe_forward(list(toks), w, E, k, cap, return_pfts=True)
+        assert led["routed_copies"] == sum(p.size() for p in pfts)
+
+
+def test_pf_forward_f64_reference_scale():
+    """A wider f64 layer (E=64, k=6) still bit-exact, dropless and capped."""
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, 1, -1)
+    rng = np.random.default_rng(7)
+    E, k, H, F, S = 64, 6, 64, 48, 256
+    w = O.LayerWeights(rng.uniform(-0.1, 0.1, (H, E)), rng.uniform(-0.1, 0.1, (E, H, F)),
+                       rng.uniform(-0.1, 0.1, (E, F, H)))
+    x = rng.uniform(-1, 1, (1, S, H))
+    for cap in (S * k, int(np.ceil(1.25 * S * k / E))):
+        want = O.pf_moe_forward(list(x), w, E, k, cap)
+        got = host(_layer(ctx, capi.F64, E, H, F, k, cap, S, w).forward(dev(x)))
+        assert np.array_equal(got[0], want[0])
+
+
+def test_shared_experts_f64_bit_exact():
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, 1, -1)
+    rng = np.random.default_rng(9)
+    E, k, H, F, S, ns, Fs = 16, 4, 24, 16, 50, 2, 16
+    w = O.LayerWeights(rng.uniform(-0.1, 0.1, (H, E)), rng.uniform(-0.1, 0.1, (E, H, F)),
+                       rng.uniform(-0.1, 0.1, (E, F, H)))
+    sw1 = rng.uniform(-0.1, 0.1, (ns, H, Fs))
+    sw2 = rng.uniform(-0.1, 0.1, (ns, Fs, H))
+    x = rng.uniform(-1, 1, (S, H))
+    want = O.moe_layer_with_shared(x, w, E, k, S * k, sw1, sw2)
+    got = host(_layer(ctx, capi.F64, E, H, F, k, S * k, S, w, sw1, sw2).forward(dev(x[None])))
+    assert np.array_equal(got[0], want)
+
+
+@pytest.mark.parametrize("W,S,E,k,H,F,shared", [(1, 512, 64, 6, 256, 128, True),
+                                                 (1, 2048, 64, 6, 2048, 1408, False),
+                                                 (4, 256, 32, 4, 128, 64, False)])
+def test_forward_bf16_vs_oracle(W, S, E, k, H, F, shared):
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, W, -1)
+    rng = np.random.default_rng(S + W)
+    w = O.LayerWeights(grid_gate(rng, H, E), bf16_round(rng.uniform(-0.1, 0.1, (E, H, F))),
+                       bf16_round(rng.uniform(-0.1, 0.1, (E, F, H))))
+    x = grid_tokens(rng, W, S, H)
+    sw1 = sw2 = None
+    if shared:
+        sw1 = bf16_round(rng.uniform(-0.1, 0.1, (2, H, F)))
+        sw2 = bf16_round(rng.uniform(-0.1, 0.1, (2, F, H)))
+    L = _layer(ctx, capi.BF16, E, H, F, k, S * k, S, w, sw1, sw2)
+    got = host(L.forward(dev(x, torch.bfloat16)))
+    if shared:
+        want = [O.moe_layer_with_shared(x[0], w, E, k, S * k, sw1, sw2, exact=False)]
+    else:
+        want = O.pf_moe_forward(list(x), w, E, k, S * k, exact=False)
+    for i in range(W):
+        assert norm_rel(got[i], want[i]) < 1e-2, norm_rel(got[i], want[i])
+        assert max_rel_diff(got[i], want[i]) < 2e-2, max_rel_diff(got[i], want[i])
