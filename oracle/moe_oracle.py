@@ -468,17 +468,23 @@ def pf_combine(node_of, disp: PfDispatch, expert_out, pfts, seq_lens,
 
 def pf_moe_forward(tokens_per_worker, w: LayerWeights, num_experts: int, top_k: int,
                    cap: int, node_of=None, ledger: Ledger | None = None, renorm=False,
-                   return_pfts=False, exact=True):
-    """pf_pipeline.cpp:137-169."""
+                   return_pfts=False, exact=True, gates=None):
+    """pf_pipeline.cpp:137-169.  ``gates`` optionally supplies each worker's
+    (top_experts, combine_weights) instead of recomputing them — used to
+    isolate the one libm-dependent value (exp in the softmax) when checking a
+    device pipeline bit for bit."""
     W = len(tokens_per_worker)
     node_of = list(range(W)) if node_of is None else list(node_of)
     if num_experts % W != 0:
         raise ValidationError("num_experts must be divisible by the worker-group size")
     el = num_experts // W
     pfts = []
-    for x in tokens_per_worker:
-        g = gate_forward(x, w.gate, top_k, renorm=renorm)
-        p = pft_from_gate(cap, num_experts, g)
+    for i, x in enumerate(tokens_per_worker):
+        if gates is not None:
+            g = GateOutput(np.asarray(gates[i][0], np.int64), np.asarray(gates[i][1], np.float64), top_k)
+        else:
+            g = gate_forward(x, w.gate, top_k, renorm=renorm)
+        p = pft_construct(cap, num_experts, x.shape[0], top_k, g.top_experts, g.combine_weights)
         p.x = gather_rows(x, p.token_ids)
         pfts.append(p)
     disp = pf_dispatch(node_of, pfts, num_experts, ledger)
@@ -671,11 +677,12 @@ def shared_expert_forward(x: np.ndarray, sw1: np.ndarray, sw2: np.ndarray,
     return mm(relu(mm(x, w1c)), w2c)
 
 
-def moe_layer_with_shared(x, w: LayerWeights, num_experts, top_k, cap, sw1, sw2, exact=True):
+def moe_layer_with_shared(x, w: LayerWeights, num_experts, top_k, cap, sw1, sw2, exact=True,
+                          gates=None):
     """Routed copies combined first (pf_moe_forward, W=1; ascending expert),
     then the shared-expert output added with weight 1.0 (axpy,
     kernels_scalar.cpp:29-31)."""
-    routed = pf_moe_forward([x], w, num_experts, top_k, cap, exact=exact)[0]
+    routed = pf_moe_forward([x], w, num_experts, top_k, cap, exact=exact, gates=gates)[0]
     return routed + 1.0 * shared_expert_forward(x, sw1, sw2, exact)
 
 
