@@ -56,6 +56,8 @@ typedef struct xmoe_layer xmoe_layer;
 
 int xmoe_abi_version(void);
 const char* xmoe_last_error(void);
+/* Number of device kernels this library has launched in the process. */
+uint64_t xmoe_kernel_launches(void);
 
 /* ------------------------------------------------------------------ context
  * One context per process and device.  world/rank describe the expert-

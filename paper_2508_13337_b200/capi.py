@@ -46,7 +46,7 @@ def header_symbols() -> list[str]:
     """Every function the C-ABI header declares."""
     hdr = os.path.join(_build.ROOT, "include", "xmoe", "xmoe.h")
     txt = open(hdr).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(xmoe_\w+)\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|uint64_t)\s+(xmoe_\w+)\(", txt, re.M)))
 
 
 def lib_path() -> str:
@@ -62,6 +62,7 @@ def lib():
         p, i64, i32 = C.c_void_p, C.c_int64, C.c_int
         L.xmoe_last_error.restype = C.c_char_p
         L.xmoe_abi_version.restype = C.c_int
+        L.xmoe_kernel_launches.restype = C.c_uint64
         L.xmoe_ctx_create.argtypes = [i32, i32, i32, p, C.POINTER(p)]
         L.xmoe_ctx_destroy.argtypes = [p]
         L.xmoe_nccl_unique_id.argtypes = [p]
@@ -101,6 +102,10 @@ def _dtype_code(t: torch.Tensor) -> int:
     if t.dtype == torch.bfloat16:
         return BF16
     raise XmoeError(2, f"unsupported dtype {t.dtype}")
+
+
+def kernel_launches() -> int:
+    return int(lib().xmoe_kernel_launches())
 
 
 def nccl_unique_id() -> bytes:

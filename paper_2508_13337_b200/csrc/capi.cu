@@ -21,6 +21,7 @@
 namespace xmoe {
 
 thread_local std::string g_last_error;
+std::atomic<unsigned long long> g_kernel_launches{0};
 
 #define XMOE_NCCL(expr)                                                                \
     do {                                                                               \
@@ -403,6 +404,7 @@ struct xmoe_layer {
 extern "C" {
 
 int xmoe_abi_version(void) { return XMOE_ABI_VERSION; }
+uint64_t xmoe_kernel_launches(void) { return g_kernel_launches.load(); }
 const char* xmoe_last_error(void) { return g_last_error.c_str(); }
 
 int xmoe_nccl_unique_id(void* out) {

@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -30,7 +31,14 @@ inline void require(bool ok, int code, const char* m) {
             ::xmoe::fail(XMOE_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(_e)); \
     } while (0)
 
-#define XMOE_LAUNCH_CHECK() XMOE_CUDA(cudaGetLastError())
+// Every kernel launch of the library passes through this check, which also
+// counts it (xmoe_kernel_launches()).
+extern std::atomic<unsigned long long> g_kernel_launches;
+#define XMOE_LAUNCH_CHECK()                                              \
+    do {                                                                 \
+        ::xmoe::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \
+        XMOE_CUDA(cudaGetLastError());                                   \
+    } while (0)
 
 constexpr int kNumSMs = 148;
 
