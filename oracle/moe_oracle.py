@@ -576,13 +576,13 @@ def rbd_combine_from_outputs(pft: Pft, plan: RbdPlan, y_of_copy: np.ndarray, seq
 
 
 def rbd_moe_forward(tokens_per_worker, w: LayerWeights, num_experts: int, top_k: int,
-                    cap: int, seed: int, node_of=None):
+                    cap: int, seed: int, node_of=None, gates=None, exact=True, shared=None):
     """rbd.cpp:360-386 (dispatch buffers equal pf_dispatch's bit for bit,
     rbd.hpp:50, so expert outputs per copy equal the plain path's)."""
     W = len(tokens_per_worker)
     node_of = list(range(W)) if node_of is None else list(node_of)
     _, pfts, disp, eo = pf_moe_forward(tokens_per_worker, w, num_experts, top_k, cap,
-                                       node_of, return_pfts=True)
+                                       node_of, return_pfts=True, gates=gates, exact=exact)
     el = num_experts // W
     out = []
     for s in range(W):
@@ -599,7 +599,10 @@ def rbd_moe_forward(tokens_per_worker, w: LayerWeights, num_experts: int, top_k:
                 g0 = int(base[le]) + before
                 y[blk[e]:blk[e] + n] = eo[j][g0:g0 + n]
         plan = select_pilots(p, node_of, num_experts, salt_seed(seed, s, 0))
-        out.append(rbd_combine_from_outputs(p, plan, y, tokens_per_worker[s].shape[0]))
+        o = rbd_combine_from_outputs(p, plan, y, tokens_per_worker[s].shape[0])
+        if shared is not None:  # shared experts added after the routed groups
+            o = o + 1.0 * shared_expert_forward(tokens_per_worker[s], shared[0], shared[1], exact)
+        out.append(o)
     return out
 
 

@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "layer.h"
+#include "rbd.h"
 
 namespace xmoe {
 
@@ -108,6 +109,9 @@ static void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, c
     const bool bf = d.dtype == XMOE_BF16;
     require(bf || d.dtype == XMOE_F64, XMOE_ERR_VALIDATION, "unknown dtype");
     if (bf) {
+        require(d.num_experts % 16 == 0, XMOE_ERR_VALIDATION,
+                "bf16 path requires num_experts to be a multiple of 16");
+        require(d.top_k <= 32, XMOE_ERR_VALIDATION, "bf16 path requires top_k <= 32");
         require(d.model_dim % 16 == 0 && d.ffn_dim % 16 == 0, XMOE_ERR_VALIDATION,
                 "bf16 path requires model_dim and ffn_dim to be multiples of 16");
         require(d.n_shared == 0 || (d.n_shared * d.shared_ffn_dim) % 16 == 0, XMOE_ERR_VALIDATION,
@@ -201,13 +205,51 @@ static void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, c
             w.send = L.alloc(static_cast<size_t>(nk) * H * es);
             w.back = L.alloc(static_cast<size_t>(nk) * H * es);
         }
+        w.s_rows = static_cast<int32_t*>(L.alloc(sizeof(int32_t)));
         if (L.Fs > 0) {
             w.smid = L.alloc(static_cast<size_t>(S) * L.Fs * es);
             w.sout = L.alloc(static_cast<size_t>(S) * H * es);
-            w.s_rows = static_cast<int32_t*>(L.alloc(sizeof(int32_t)));
+        }
+        if (d.dispatch_mode == XMOE_DISPATCH_RBD) {
+            const long long gmax = S * std::min<long long>(L.k, W);  // groups per source
+            const long long rmax = static_cast<long long>(W) * S;   // groups received
+            RbdWork& r = w.rbd;
+            auto i32 = [&](long long n) { return static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (n + 1))); };
+            r.g.token = i32(nk);
+            r.g.dest = i32(nk);
+            r.g.first_slot = i32(nk);
+            r.g.n = i32(nk);
+            r.g.pilot = i32(nk);
+            r.g.pos = i32(nk);
+            r.gcount = i32(S);
+            r.gbase = i32(S);
+            r.G_dev = i32(1);
+            r.flags = i32(1);
+            r.draws = static_cast<uint64_t*>(L.alloc(sizeof(uint64_t) * (nk + kRbdChunk)));
+            r.dptr = i32(W + 1);
+            r.perm = i32(nk);
+            r.nsorted = i32(nk);
+            r.coff = i32(nk);
+            r.csr_ws = L.alloc(bucket_ws_bytes(nk, W));
+            rng_state_from_seed(salt_seed_host(d.seed, static_cast<uint64_t>(w.rank), 0), r.state);
+            w.send_u = L.alloc(static_cast<size_t>(gmax) * H * es);
+            w.desc_send = static_cast<RbdDesc*>(L.alloc(sizeof(RbdDesc) * nk));
+            w.recv_u = L.alloc(static_cast<size_t>(rmax) * H * es);
+            w.desc_recv = static_cast<RbdDesc*>(L.alloc(sizeof(RbdDesc) * L.R_max));
+            w.gstart = i32(rmax);
+            w.back_u = L.alloc(static_cast<size_t>(rmax) * H * es);
+            w.ret_u = L.alloc(static_cast<size_t>(gmax) * H * es);
+            w.ru_base = i32(W);
         }
         recv_tab[w.rank] = static_cast<char*>(w.recv);
         eout_tab[w.rank] = static_cast<char*>(w.eout);
+    }
+    if (d.dispatch_mode == XMOE_DISPATCH_RBD) {
+        std::vector<uint64_t> jt;
+        rbd_jump_tables(jt);
+        L.jumps = static_cast<uint64_t*>(L.alloc(sizeof(uint64_t) * jt.size()));
+        XMOE_CUDA(cudaMemcpy(L.jumps, jt.data(), sizeof(uint64_t) * jt.size(), cudaMemcpyHostToDevice));
+        L.G_all = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * W * W));
     }
     L.recv_tab = static_cast<char**>(L.alloc(sizeof(char*) * W));
     L.eout_tab = static_cast<char**>(L.alloc(sizeof(char*) * W));
@@ -261,13 +303,16 @@ static void layer_forward(Layer& L, const void* x, long long S, void* out, cudaS
     for (int i = 0; i < nl; ++i) {
         Worker& w = L.workers[i];
         const void* xi = xb + static_cast<size_t>(i) * S * row_bytes;
-        if (dt == XMOE_F64)
+        launch_fill_i32(w.s_rows, 1, static_cast<int32_t>(S), st);  // one dense group of S rows
+        if (dt == XMOE_F64) {
             launch_gate_logits_f64(static_cast<const double*>(xi), static_cast<const double*>(L.gate),
                                    S, H, E, w.logits, st);
-        else
-            launch_gate_logits_bf16(static_cast<const __nv_bfloat16*>(xi),
-                                    static_cast<const __nv_bfloat16*>(L.gate), S, H, E, w.logits, st);
-        launch_softmax_topk(w.logits, S, E, k, L.d.renorm, w.top, w.wts, st);
+            launch_softmax_topk(w.logits, S, E, k, L.d.renorm, w.top, w.wts, st);
+        } else {
+            float* lg = reinterpret_cast<float*>(w.logits);
+            launch_grouped_gemm_bf16_f32out(xi, S, H, w.s_rows, 1, L.gate, E, lg, 0, st);
+            launch_softmax_topk_f32(lg, S, E, k, L.d.renorm, w.top, w.wts, st);
+        }
     }
     L.mark(kEvGate, st);
     for (int i = 0; i < nl; ++i) {
@@ -276,10 +321,26 @@ static void layer_forward(Layer& L, const void* x, long long S, void* out, cudaS
                    w.token_ids, w.expert_ids, w.cw, w.tpe, w.slot_pos, w.B_dev, w.pft_ws, st);
     }
     L.mark(kEvPft, st);
-    // 3. per-expert counts to every rank (pf_pipeline.cpp:30-36)
+    const bool rbd = L.d.dispatch_mode == XMOE_DISPATCH_RBD;
+    if (rbd) {
+        // 3'. (token, destination) groups and their pilots (rbd.cpp:26-81)
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            launch_rbd_groups(w.slot_pos, w.expert_ids, static_cast<int>(S), k, L.El, w.rbd.state,
+                              L.jumps, w.rbd, st);
+            launch_rbd_sort(W, nk, w.rbd, st);
+            launch_adjacent_diff(w.rbd.dptr, W, L.G_all + static_cast<size_t>(w.rank) * W, st);
+        }
+    }
+    // 3. per-expert counts (and RBD group counts) to every rank (pf_pipeline.cpp:30-36)
     if (!shared_dev) {
         Worker& w = L.workers[0];
-        XMOE_NCCL(ncclAllGather(w.tpe, L.tpe_all, E, ncclInt32, static_cast<ncclComm_t>(ctx.nccl), st));
+        auto comm = static_cast<ncclComm_t>(ctx.nccl);
+        XMOE_NCCL(ncclGroupStart());
+        XMOE_NCCL(ncclAllGather(w.tpe, L.tpe_all, E, ncclInt32, comm, st));
+        if (rbd)
+            XMOE_NCCL(ncclAllGather(L.G_all + static_cast<size_t>(w.rank) * W, L.G_all, W, ncclInt32, comm, st));
+        XMOE_NCCL(ncclGroupEnd());
     }
     // 4. dispatch (pf_pipeline.cpp:38-79): sender-side placement into the
     //    owner's (local expert, source, position) layout
@@ -288,7 +349,35 @@ static void layer_forward(Layer& L, const void* x, long long S, void* out, cudaS
         launch_dispatch_dest(L.tpe_all, W, E, w.rank, w.expert_ids, w.B_dev, nk, w.dest_rank,
                              w.dest_row, st);
     }
-    if (shared_dev) {
+    if (rbd) {
+        // 4'. counts to the host (message sizes), pack unique rows + copy
+        //     descriptors, exchange, expand at the receivers (rbd.cpp:83-285)
+        L.h_tpe.resize(static_cast<size_t>(W) * E);
+        L.h_G.resize(static_cast<size_t>(W) * W);
+        XMOE_CUDA(cudaMemcpyAsync(L.h_tpe.data(), L.tpe_all, sizeof(int32_t) * W * E, cudaMemcpyDeviceToHost, st));
+        XMOE_CUDA(cudaMemcpyAsync(L.h_G.data(), L.G_all, sizeof(int32_t) * W * W, cudaMemcpyDeviceToHost, st));
+        XMOE_CUDA(cudaStreamSynchronize(st));
+        std::vector<int32_t> ru(W);
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            for (int d = 0; d < W; ++d) {
+                long long a = 0;
+                for (int s = 0; s < w.rank; ++s) a += L.Gsd(s, d);
+                ru[d] = static_cast<int32_t>(a);
+            }
+            XMOE_CUDA(cudaMemcpy(w.ru_base, ru.data(), sizeof(int32_t) * W, cudaMemcpyHostToDevice));
+            launch_rbd_pack(xb + static_cast<size_t>(i) * S * row_bytes, static_cast<int>(row_bytes), w.rbd,
+                            nk, w.ru_base, w.slot_pos, k, w.dest_row, w.cw, w.send_u, w.desc_send, st);
+        }
+        L.rbd_exchange(/*forward=*/true, st);
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            long long nd = 0;
+            for (int s = 0; s < W; ++s) nd += L.C(s, w.rank);
+            launch_rbd_expand(w.recv_u, static_cast<int>(row_bytes), w.desc_recv, static_cast<int>(nd),
+                              w.recv, w.gstart, st);
+        }
+    } else if (shared_dev) {
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             launch_scatter_rows(xb + static_cast<size_t>(i) * S * row_bytes, static_cast<int>(row_bytes),
@@ -317,14 +406,27 @@ static void layer_forward(Layer& L, const void* x, long long S, void* out, cudaS
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             const void* xi = xb + static_cast<size_t>(i) * S * row_bytes;
-            launch_fill_i32(w.s_rows, 1, static_cast<int32_t>(S), st);
             run_gemm(L, dt, xi, S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, st);
             run_gemm(L, dt, w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, w.sout, 0, st);
         }
     }
     L.mark(kEvShared, st);
-    // 6. reverse exchange + weighted combine (pf_pipeline.cpp:107-135)
-    if (shared_dev) {
+    // 6. reverse exchange + weighted combine (pf_pipeline.cpp:107-135,
+    //    rbd.cpp:287-358)
+    if (rbd) {
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            long long ng = 0;
+            for (int s = 0; s < W; ++s) ng += L.Gsd(s, w.rank);
+            launch_rbd_merge(dt, w.eout, H, w.desc_recv, w.gstart, static_cast<int>(ng), w.back_u, st);
+        }
+        L.rbd_exchange(/*forward=*/false, st);
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            launch_rbd_combine(dt, w.ret_u, H, static_cast<int>(S), w.rbd, w.cw, L.Fs > 0 ? w.sout : nullptr,
+                               ob + static_cast<size_t>(i) * S * row_bytes, st);
+        }
+    } else if (shared_dev) {
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             launch_combine(dt, nullptr, H, nullptr, w.slot_pos, k, w.cw, static_cast<int>(S),
@@ -385,6 +487,83 @@ void Layer::exchange_nccl(bool forward, cudaStream_t st) {
             char* p = static_cast<char*>(forward ? w.recv : w.eout) + (ebase[le] + before) * rb;
             if (forward) XMOE_NCCL(ncclRecv(p, n * H, ty, peer, comm, st));
             else XMOE_NCCL(ncclSend(p, n * H, ty, peer, comm, st));
+        }
+    }
+    XMOE_NCCL(ncclGroupEnd());
+}
+
+long long Layer::C(int s, int d) const {
+    long long a = 0;
+    for (int le = 0; le < El; ++le) a += h_tpe[static_cast<size_t>(s) * E + d * El + le];
+    return a;
+}
+
+// RBD exchange.  Forward, for every (source s, dest d): the G_sd unique rows
+// of s's dest-d segment land in d's recv_u after the rows of sources < s, and
+// the C_sd copy descriptors after those of sources < s.  Reverse: the merged
+// rows go back into s's ret_u at s's dest-d segment.  Ranks sharing the
+// device use device copies; separate processes use NCCL send/recv.
+void Layer::rbd_exchange(bool forward, cudaStream_t st) {
+    const size_t rb = static_cast<size_t>(H) * es;
+    auto seg_g = [&](int s, int d) {  // s's dest-d segment start in its dest-sorted groups
+        long long a = 0;
+        for (int q = 0; q < d; ++q) a += Gsd(s, q);
+        return a;
+    };
+    auto seg_c = [&](int s, int d) {
+        long long a = 0;
+        for (int q = 0; q < d; ++q) a += C(s, q);
+        return a;
+    };
+    auto at_recv_g = [&](int s, int d) {  // rows of sources < s at receiver d
+        long long a = 0;
+        for (int q = 0; q < s; ++q) a += Gsd(q, d);
+        return a;
+    };
+    auto at_recv_c = [&](int s, int d) {
+        long long a = 0;
+        for (int q = 0; q < s; ++q) a += C(q, d);
+        return a;
+    };
+    const bool shared_dev = ctx->rank < 0 || W == 1;
+    if (shared_dev) {
+        for (Worker& src : workers)
+            for (Worker& dst : workers) {
+                const int s = src.rank, d = dst.rank;
+                const long long g = Gsd(s, d), c = C(s, d);
+                if (forward) {
+                    if (g)
+                        XMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(dst.recv_u) + at_recv_g(s, d) * rb,
+                                                  static_cast<char*>(src.send_u) + seg_g(s, d) * rb, g * rb,
+                                                  cudaMemcpyDeviceToDevice, st));
+                    if (c)
+                        XMOE_CUDA(cudaMemcpyAsync(dst.desc_recv + at_recv_c(s, d), src.desc_send + seg_c(s, d),
+                                                  c * sizeof(RbdDesc), cudaMemcpyDeviceToDevice, st));
+                } else if (g) {
+                    XMOE_CUDA(cudaMemcpyAsync(static_cast<char*>(src.ret_u) + seg_g(s, d) * rb,
+                                              static_cast<char*>(dst.back_u) + at_recv_g(s, d) * rb, g * rb,
+                                              cudaMemcpyDeviceToDevice, st));
+                }
+            }
+        return;
+    }
+    Worker& w = workers[0];
+    const int me = w.rank;
+    auto comm = static_cast<ncclComm_t>(ctx->nccl);
+    XMOE_NCCL(ncclGroupStart());
+    for (int peer = 0; peer < W; ++peer) {
+        if (forward) {
+            const long long g_out = Gsd(me, peer), c_out = C(me, peer);
+            const long long g_in = Gsd(peer, me), c_in = C(peer, me);
+            if (g_out) XMOE_NCCL(ncclSend(static_cast<char*>(w.send_u) + seg_g(me, peer) * rb, g_out * rb, ncclUint8, peer, comm, st));
+            if (c_out) XMOE_NCCL(ncclSend(w.desc_send + seg_c(me, peer), c_out * sizeof(RbdDesc), ncclUint8, peer, comm, st));
+            if (g_in) XMOE_NCCL(ncclRecv(static_cast<char*>(w.recv_u) + at_recv_g(peer, me) * rb, g_in * rb, ncclUint8, peer, comm, st));
+            if (c_in) XMOE_NCCL(ncclRecv(w.desc_recv + at_recv_c(peer, me), c_in * sizeof(RbdDesc), ncclUint8, peer, comm, st));
+        } else {
+            const long long g_back = Gsd(peer, me);  // merged rows I return to peer
+            const long long g_ret = Gsd(me, peer);   // merged rows peer returns to me
+            if (g_back) XMOE_NCCL(ncclSend(static_cast<char*>(w.back_u) + at_recv_g(peer, me) * rb, g_back * rb, ncclUint8, peer, comm, st));
+            if (g_ret) XMOE_NCCL(ncclRecv(static_cast<char*>(w.ret_u) + seg_g(me, peer) * rb, g_ret * rb, ncclUint8, peer, comm, st));
         }
     }
     XMOE_NCCL(ncclGroupEnd());
@@ -454,16 +633,24 @@ int xmoe_gate_forward(xmoe_ctx* ctx, int dtype, const void* x, const void* wg, i
         require(k >= 1, XMOE_ERR_VALIDATION, "top_k must be >= 1");
         require(k <= E, XMOE_ERR_VALIDATION, "top_k must be <= num_experts");
         auto st = static_cast<cudaStream_t>(stream);
-        double* lg = logits ? logits : static_cast<double*>(ctx->c.scratch(sizeof(double) * S * E));
-        if (dtype == XMOE_F64)
+        char* ws = static_cast<char*>(ctx->c.scratch(sizeof(double) * S * E + 256));
+        if (dtype == XMOE_F64) {
+            double* lg = logits ? logits : reinterpret_cast<double*>(ws);
             launch_gate_logits_f64(static_cast<const double*>(x), static_cast<const double*>(wg),
                                    S, H, E, lg, st);
-        else if (dtype == XMOE_BF16)
-            launch_gate_logits_bf16(static_cast<const __nv_bfloat16*>(x),
-                                    static_cast<const __nv_bfloat16*>(wg), S, H, E, lg, st);
-        else
+            launch_softmax_topk(lg, S, E, k, renorm, top, weights, st);
+        } else if (dtype == XMOE_BF16) {
+            require(E % 16 == 0 && H % 8 == 0, XMOE_ERR_VALIDATION,
+                    "bf16 gate requires num_experts % 16 == 0 and model_dim % 8 == 0");
+            int32_t* rows = reinterpret_cast<int32_t*>(ws);
+            float* lg = reinterpret_cast<float*>(ws + 256);
+            launch_fill_i32(rows, 1, static_cast<int32_t>(S), st);
+            launch_grouped_gemm_bf16_f32out(x, S, H, rows, 1, wg, E, lg, 0, st);
+            launch_softmax_topk_f32(lg, S, E, k, renorm, top, weights, st);
+            if (logits) launch_f32_to_f64(lg, static_cast<long long>(S) * E, logits, st);
+        } else {
             fail(XMOE_ERR_VALIDATION, "unknown dtype");
-        launch_softmax_topk(lg, S, E, k, renorm, top, weights, st);
+        }
     });
 }
 

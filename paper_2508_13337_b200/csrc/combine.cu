@@ -61,71 +61,106 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_f64_kernel(
     }
 }
 
-// BF16: each lane owns kV 16-byte chunks (8 bf16 each) of the row per pass.
-template <int kV>
+// BF16: a warp owns one 512-column segment of one token (2 x 16-byte chunks
+// per lane).  The copy list is fetched in one step (lane j loads copy j's
+// index, weight and row address) and broadcast with shuffles, so each token
+// pays two dependent memory latencies, and every copy's row loads are issued
+// before any math (up to 2*kBatch 16-byte loads in flight per lane).
+constexpr int kSegCols = 512;
+constexpr int kBatch = 8;
+
 __global__ void __launch_bounds__(32 * kCombWarps) combine_bf16_kernel(
     const __nv_bfloat16* __restrict__ rows, int H, CopyList cl, const double* __restrict__ w,
     int S, const __nv_bfloat16* __restrict__ addend, __nv_bfloat16* __restrict__ out) {
-    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nseg = (H + kSegCols - 1) / kSegCols;
+    const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (t >= S) return;
-    const int nn = cl.count(t);
+    if (gw >= static_cast<long long>(S) * nseg) return;
+    const int t = static_cast<int>(gw / nseg);
+    const int seg = static_cast<int>(gw % nseg);
     const int nchunk = H >> 3;
-    for (int c0 = 0; c0 < nchunk; c0 += 32 * kV) {
-        float acc[kV][8];
+    const int seg_end = min(nchunk, (seg + 1) * (kSegCols / 8));
+    const int c0 = seg * (kSegCols / 8) + lane;
+    const int c1 = c0 + 32;
+    const bool v0 = c0 < seg_end;
+    const bool v1 = c1 < seg_end;
+    float acc[16];
 #pragma unroll
-        for (int v = 0; v < kV; ++v)
+    for (int q = 0; q < 16; ++q) acc[q] = 0.f;
+    // copy list, one entry per lane
+    int n;
+    int base = 0;
+    if (cl.ptr) {
+        base = cl.ptr[t];
+        n = cl.ptr[t + 1] - base;
+    } else {
+        const int v = lane < cl.k ? cl.idx[static_cast<size_t>(t) * cl.k + lane] : -1;
+        n = __popc(__ballot_sync(0xffffffffu, v >= 0));  // kept copies are a -1 padded prefix
+    }
+    for (int j0 = 0; j0 < n; j0 += 32) {
+        const int j = j0 + lane;
+        int cj = -1;
+        float wv = 0.f;
+        const int4* rp = nullptr;
+        if (j < n) {
+            cj = cl.ptr ? cl.idx[base + j] : cl.idx[static_cast<size_t>(t) * cl.k + j];
+            wv = static_cast<float>(w[cj]);
+            rp = reinterpret_cast<const int4*>(cl.row(rows, cj, H));
+        }
+        const int m = min(32, n - j0);
+        for (int b0 = 0; b0 < m; b0 += kBatch) {
+            int4 r[kBatch][2];
+            float wj[kBatch];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) acc[v][q] = 0.f;
-        for (int j = 0; j < nn; ++j) {
-            const int cj = cl.at(t, j);  // warp-uniform
-            const float wj = static_cast<float>(w[cj]);
-            const int4* src = reinterpret_cast<const int4*>(cl.row(rows, cj, H));
-            int4 r[kV];
-#pragma unroll
-            for (int v = 0; v < kV; ++v) {
-                const int c = c0 + lane + 32 * v;
-                r[v] = c < nchunk ? ld_nc_v4(src + c) : make_int4(0, 0, 0, 0);
+            for (int b = 0; b < kBatch; ++b) {
+                const int src_lane = b0 + b;
+                const int4* p = reinterpret_cast<const int4*>(
+                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(rp), src_lane & 31));
+                wj[b] = __shfl_sync(0xffffffffu, wv, src_lane & 31);
+                if (src_lane < m) {
+                    r[b][0] = v0 ? ld_nc_v4(p + c0) : make_int4(0, 0, 0, 0);
+                    r[b][1] = v1 ? ld_nc_v4(p + c1) : make_int4(0, 0, 0, 0);
+                }
             }
 #pragma unroll
-            for (int v = 0; v < kV; ++v) {
-                const uint32_t u[4] = {static_cast<uint32_t>(r[v].x), static_cast<uint32_t>(r[v].y),
-                                       static_cast<uint32_t>(r[v].z), static_cast<uint32_t>(r[v].w)};
+            for (int b = 0; b < kBatch; ++b) {
+                if (b0 + b < m) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    acc[v][2 * q] = fmaf(wj, bf16_lo(u[q]), acc[v][2 * q]);
-                    acc[v][2 * q + 1] = fmaf(wj, bf16_hi(u[q]), acc[v][2 * q + 1]);
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t u[4] = {static_cast<uint32_t>(r[b][h].x), static_cast<uint32_t>(r[b][h].y),
+                                               static_cast<uint32_t>(r[b][h].z), static_cast<uint32_t>(r[b][h].w)};
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            acc[8 * h + 2 * q] = fmaf(wj[b], bf16_lo(u[q]), acc[8 * h + 2 * q]);
+                            acc[8 * h + 2 * q + 1] = fmaf(wj[b], bf16_hi(u[q]), acc[8 * h + 2 * q + 1]);
+                        }
+                    }
                 }
             }
         }
-        if (addend) {
-            const int4* src = reinterpret_cast<const int4*>(addend + static_cast<size_t>(t) * H);
+    }
+    const int4* add = addend ? reinterpret_cast<const int4*>(addend + static_cast<size_t>(t) * H) : nullptr;
+    int4* dst = reinterpret_cast<int4*>(out + static_cast<size_t>(t) * H);
 #pragma unroll
-            for (int v = 0; v < kV; ++v) {
-                const int c = c0 + lane + 32 * v;
-                if (c >= nchunk) continue;
-                const int4 r = ld_nc_v4(src + c);
-                const uint32_t u[4] = {static_cast<uint32_t>(r.x), static_cast<uint32_t>(r.y),
-                                       static_cast<uint32_t>(r.z), static_cast<uint32_t>(r.w)};
+    for (int h = 0; h < 2; ++h) {
+        const int c = h ? c1 : c0;
+        if (!(h ? v1 : v0)) continue;
+        if (add) {
+            const int4 a4 = ld_nc_v4(add + c);
+            const uint32_t u[4] = {static_cast<uint32_t>(a4.x), static_cast<uint32_t>(a4.y),
+                                   static_cast<uint32_t>(a4.z), static_cast<uint32_t>(a4.w)};
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    acc[v][2 * q] += bf16_lo(u[q]);
-                    acc[v][2 * q + 1] += bf16_hi(u[q]);
-                }
+            for (int q = 0; q < 4; ++q) {
+                acc[8 * h + 2 * q] += bf16_lo(u[q]);
+                acc[8 * h + 2 * q + 1] += bf16_hi(u[q]);
             }
         }
-        int4* dst = reinterpret_cast<int4*>(out + static_cast<size_t>(t) * H);
-#pragma unroll
-        for (int v = 0; v < kV; ++v) {
-            const int c = c0 + lane + 32 * v;
-            if (c >= nchunk) continue;
-            int4 o;
-            o.x = static_cast<int>(pack_bf16(acc[v][0], acc[v][1]));
-            o.y = static_cast<int>(pack_bf16(acc[v][2], acc[v][3]));
-            o.z = static_cast<int>(pack_bf16(acc[v][4], acc[v][5]));
-            o.w = static_cast<int>(pack_bf16(acc[v][6], acc[v][7]));
-            st_na_v4(dst + c, o);
-        }
+        int4 o;
+        o.x = static_cast<int>(pack_bf16(acc[8 * h + 0], acc[8 * h + 1]));
+        o.y = static_cast<int>(pack_bf16(acc[8 * h + 2], acc[8 * h + 3]));
+        o.z = static_cast<int>(pack_bf16(acc[8 * h + 4], acc[8 * h + 5]));
+        o.w = static_cast<int>(pack_bf16(acc[8 * h + 6], acc[8 * h + 7]));
+        st_na_v4(dst + c, o);
     }
 }
 
@@ -142,7 +177,8 @@ void launch_combine(int dtype, const void* rows, int H, const int32_t* ptr, cons
             static_cast<double*>(out));
     } else {
         require(H % 8 == 0, XMOE_ERR_VALIDATION, "bf16 path requires model_dim % 8 == 0");
-        combine_bf16_kernel<8><<<blocks, 32 * kCombWarps, 0, st>>>(
+        const long long warps = static_cast<long long>(S) * ((H + kSegCols - 1) / kSegCols);
+        combine_bf16_kernel<<<ceil_div(warps, kCombWarps), 32 * kCombWarps, 0, st>>>(
             static_cast<const __nv_bfloat16*>(rows), H, cl, w, S,
             static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out));
     }

@@ -11,10 +11,10 @@ namespace xmoe {
 // gate.cu
 void launch_gate_logits_f64(const double* x, const double* wg, int S, int H, int E,
                             double* logits, cudaStream_t st);
-void launch_gate_logits_bf16(const __nv_bfloat16* x, const __nv_bfloat16* wgt, int S, int H,
-                             int E, double* logits, cudaStream_t st);
 void launch_softmax_topk(const double* logits, int S, int E, int k, int renorm, int32_t* top,
                          double* weights, cudaStream_t st);
+void launch_softmax_topk_f32(const float* logits, int S, int E, int k, int renorm, int32_t* top,
+                             double* weights, cudaStream_t st);
 
 // pft.cu
 size_t bucket_ws_bytes(long long n, int K);
@@ -62,6 +62,8 @@ void launch_grouped_gemm_bf16_f32out(const void* A, long long rows, int K,
 void launch_recv_counts(const int32_t* tpe_all, int W, int E, int dst, int32_t* rpe,
                         cudaStream_t st);
 void launch_fill_i32(int32_t* p, int n, int32_t v, cudaStream_t st);
+void launch_adjacent_diff(const int32_t* ptr, int n, int32_t* out, cudaStream_t st);
+void launch_f32_to_f64(const float* in, long long n, double* out, cudaStream_t st);
 void launch_transpose(int dtype_in, const void* in, int batch, int rows, int cols,
                       int dtype_out, void* out, cudaStream_t st);
 

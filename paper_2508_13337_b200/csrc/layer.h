@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <vector>
 
+#include "rbd.h"
 #include "xmoe/xmoe.h"
 
 namespace xmoe {
@@ -51,6 +52,16 @@ struct Worker {
     void* smid = nullptr;         // shared experts [S, Fs]
     void* sout = nullptr;         // [S, H]
     int32_t* s_rows = nullptr;
+    // redundancy-bypassing dispatch (rbd.cu)
+    RbdWork rbd{};
+    void* send_u = nullptr;       // [S*min(k,W), H] one row per (token, dest) group, dest-sorted
+    RbdDesc* desc_send = nullptr; // [S*k] one descriptor per copy
+    void* recv_u = nullptr;       // [W*S, H] unique rows received from every source
+    RbdDesc* desc_recv = nullptr; // [R_max]
+    int32_t* gstart = nullptr;    // [W*S] first descriptor of each received group
+    void* back_u = nullptr;       // [W*S, H] merged group outputs to return
+    void* ret_u = nullptr;        // [S*min(k,W), H] merged outputs returned to this source
+    int32_t* ru_base = nullptr;   // [W] my groups' first row in each receiver's recv_u
 };
 
 enum { kEvStart = 0, kEvGate, kEvPft, kEvDispatch, kEvGemm, kEvShared, kEvCombine, kNumEvents };
@@ -70,6 +81,9 @@ struct Layer {
     char** recv_tab = nullptr;   // device table: rank -> recv buffer (shared-device ranks)
     char** eout_tab = nullptr;
     std::vector<int32_t> h_tpe;
+    uint64_t* jumps = nullptr;   // RBD jump-ahead matrices (device)
+    int32_t* G_all = nullptr;    // [W, W] groups source -> dest (device)
+    std::vector<int32_t> h_G;
     std::vector<Worker> workers;
     std::vector<void*> allocs;
     std::vector<cudaEvent_t> events;
@@ -78,6 +92,9 @@ struct Layer {
     void* alloc(size_t bytes);
     void mark(int ev, cudaStream_t st);
     void exchange_nccl(bool forward, cudaStream_t st);
+    void rbd_exchange(bool forward, cudaStream_t st);
+    long long C(int s, int d) const;  // copies source s -> dest d
+    long long Gsd(int s, int d) const { return h_G[static_cast<size_t>(s) * W + d]; }
     void ledger(uint64_t* out, int n);
     ~Layer();
 };

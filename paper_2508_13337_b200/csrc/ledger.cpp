@@ -51,6 +51,27 @@ void Layer::ledger(uint64_t* out, int n) {
             }
         }
     }
+    if (d.dispatch_mode == XMOE_DISPATCH_RBD && h_G.size() == static_cast<size_t>(W) * W) {
+        // bypass: one row per (token, destination) group each way, plus the
+        // 24-byte copy descriptors (rbd.h RbdDesc)
+        v[0] = v[1] = v[2] = v[3] = v[4] = 0;
+        for (const Worker& w : workers) {
+            for (int dd = 0; dd < W; ++dd) {
+                const uint64_t g = static_cast<uint64_t>(h_G[static_cast<size_t>(w.rank) * W + dd]);
+                uint64_t c = 0;
+                for (int le = 0; le < El; ++le) c += tpe[static_cast<size_t>(w.rank) * E + dd * El + le];
+                if (dd == w.rank) {
+                    v[0] += g * rb;
+                    v[3] += g * rb;
+                } else {
+                    v[1] += g * rb;
+                    v[4] += g * rb;
+                    v[2] += c * 24;
+                }
+            }
+            if (W > 1) v[2] += static_cast<uint64_t>(W - 1) * (E + W) * sizeof(int32_t);
+        }
+    }
     for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
 }
 

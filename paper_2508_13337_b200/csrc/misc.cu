@@ -55,6 +55,28 @@ void launch_fill_i32(int32_t* p, int n, int32_t v, cudaStream_t st) {
     XMOE_LAUNCH_CHECK();
 }
 
+__global__ void f32_to_f64_kernel(const float* __restrict__ in, long long n, double* __restrict__ out) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = static_cast<double>(in[i]);
+}
+
+void launch_f32_to_f64(const float* in, long long n, double* out, cudaStream_t st) {
+    if (n == 0) return;
+    f32_to_f64_kernel<<<ceil_div(n, 256), 256, 0, st>>>(in, n, out);
+    XMOE_LAUNCH_CHECK();
+}
+
+__global__ void adjacent_diff_kernel(const int32_t* __restrict__ ptr, int n, int32_t* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = ptr[i + 1] - ptr[i];
+}
+
+void launch_adjacent_diff(const int32_t* ptr, int n, int32_t* out, cudaStream_t st) {
+    if (n == 0) return;
+    adjacent_diff_kernel<<<ceil_div(n, 256), 256, 0, st>>>(ptr, n, out);
+    XMOE_LAUNCH_CHECK();
+}
+
 void launch_transpose(int dtype_in, const void* in, int batch, int rows, int cols, int dtype_out,
                       void* out, cudaStream_t st) {
     if (batch == 0 || rows == 0 || cols == 0) return;

@@ -12,7 +12,7 @@
 namespace xmoe {
 
 constexpr int kRowWarps = 8;
-constexpr int kUnroll = 4;
+constexpr int kUnroll = 8;
 
 // Copy one row with the whole warp.  Rows whose size is a multiple of 16 B
 // (every bf16 row with H % 8 == 0) move as int4 vectors, kUnroll in flight per

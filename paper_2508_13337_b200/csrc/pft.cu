@@ -20,6 +20,7 @@
 //   K6 slot_sort      per token, its kept rows ascending (for the combine)
 #include "common.cuh"
 #include "kernels.cuh"
+#include "rbd.h"
 
 namespace xmoe {
 
@@ -66,8 +67,10 @@ __global__ void pft_validate_kernel(const int32_t* __restrict__ top, int S, int 
 // ---------------------------------------------------------------- K1
 template <bool kSmem>
 __global__ void __launch_bounds__(32 * kWarps) bucket_count_kernel(
-    const int32_t* __restrict__ keys, int n, int K, int32_t* __restrict__ counts) {
+    const int32_t* __restrict__ keys, int n_host, const int32_t* __restrict__ n_dev, int K,
+    int32_t* __restrict__ counts) {
     extern __shared__ int32_t hist[];  // [kWarps][K] when kSmem
+    const int n = n_dev ? *n_dev : n_host;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int chunk = blockIdx.x * kWarps + warp;
     int32_t* h = kSmem ? hist + warp * K : counts + static_cast<size_t>(chunk) * K;
@@ -96,9 +99,10 @@ __global__ void __launch_bounds__(32 * kWarps) bucket_count_kernel(
 }
 
 // ---------------------------------------------------------------- K2
-// Single CTA.  For each key: exclusive scan of per-chunk counts (in place),
-// raw total and capacity-clamped total; then block-wide exclusive scans over
-// keys.  raw_base/kept_base get K+1 entries (last = totals).
+// Single CTA.  Phase 1, one warp per key: warp-parallel exclusive scan of the
+// key's per-chunk counts (in place), raw total and capacity-clamped total.
+// Phase 2: block-wide exclusive scans over keys of both totals.
+// raw_base/kept_base get K+1 entries (last = totals).
 __global__ void __launch_bounds__(1024) bucket_scan_kernel(int nchunks, int K, int cap,
                                                            int32_t* __restrict__ counts,
                                                            int32_t* __restrict__ raw_cnt,
@@ -109,32 +113,41 @@ __global__ void __launch_bounds__(1024) bucket_scan_kernel(int nchunks, int K, i
                                                            int32_t* __restrict__ total_out) {
     __shared__ int32_t s_raw[1024], s_kept[1024];
     __shared__ int32_t carry_raw, carry_kept;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int any_over = 0;
+    for (int key = warp; key < K; key += 32) {
+        int running = 0;
+        for (int c0 = 0; c0 < nchunks; c0 += 32) {
+            const int c = c0 + lane;
+            const int v = c < nchunks ? counts[static_cast<size_t>(c) * K + key] : 0;
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (c < nchunks) counts[static_cast<size_t>(c) * K + key] = running + incl - v;
+            running += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) {
+            raw_cnt[key] = running;
+            if (kept_cnt) kept_cnt[key] = min(running, cap);
+            if (running > cap) any_over = 1;
+        }
+    }
     if (threadIdx.x == 0) {
         carry_raw = 0;
         carry_kept = 0;
     }
     __syncthreads();
-    int any_over = 0;
     for (int k0 = 0; k0 < K; k0 += 1024) {
         const int key = k0 + threadIdx.x;
-        int tot = 0;
-        if (key < K) {
-            for (int c = 0; c < nchunks; ++c) {
-                int32_t* p = counts + static_cast<size_t>(c) * K + key;
-                const int v = *p;
-                *p = tot;
-                tot += v;
-            }
-            raw_cnt[key] = tot;
-        }
-        const int kept = (key < K) ? min(tot, cap) : 0;
-        if (key < K && tot > cap) any_over = 1;
-        if (kept_cnt && key < K) kept_cnt[key] = kept;
-        s_raw[threadIdx.x] = (key < K) ? tot : 0;
+        const int tot = key < K ? raw_cnt[key] : 0;
+        const int kept = key < K ? min(tot, cap) : 0;
+        s_raw[threadIdx.x] = tot;
         s_kept[threadIdx.x] = kept;
         __syncthreads();
-        // Hillis-Steele inclusive scans
-        for (int o = 1; o < 1024; o <<= 1) {
+        for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scans
             const int a = threadIdx.x >= o ? s_raw[threadIdx.x - o] : 0;
             const int b = threadIdx.x >= o ? s_kept[threadIdx.x - o] : 0;
             __syncthreads();
@@ -167,9 +180,11 @@ __global__ void __launch_bounds__(1024) bucket_scan_kernel(int nchunks, int K, i
 // final raw position is raw_base[key] + that + running rank.
 template <bool kSmem>
 __global__ void __launch_bounds__(32 * kWarps) bucket_place_kernel(
-    const int32_t* __restrict__ keys, int n, int K, int32_t* __restrict__ counts,
-    const int32_t* __restrict__ raw_base, int32_t* __restrict__ sorted_f) {
+    const int32_t* __restrict__ keys, int n_host, const int32_t* __restrict__ n_dev, int K,
+    int32_t* __restrict__ counts, const int32_t* __restrict__ raw_base,
+    int32_t* __restrict__ sorted_f) {
     extern __shared__ int32_t run[];
+    const int n = n_dev ? *n_dev : n_host;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int chunk = blockIdx.x * kWarps + warp;
     const int f0 = chunk * kChunk;
@@ -422,9 +437,9 @@ void launch_pft(const int32_t* top, const double* w, int S, int k, int E, int ca
     const size_t smem_bytes = smem ? sizeof(int32_t) * kWarps * E : 0;
     if (!smem) XMOE_CUDA(cudaMemsetAsync(b.counts, 0, sizeof(int32_t) * nblocks * kWarps * E, st));
     if (smem) {
-        bucket_count_kernel<true><<<nblocks, 32 * kWarps, smem_bytes, st>>>(top, n, E, b.counts);
+        bucket_count_kernel<true><<<nblocks, 32 * kWarps, smem_bytes, st>>>(top, n, nullptr, E, b.counts);
     } else {
-        bucket_count_kernel<false><<<nblocks, 32 * kWarps, 0, st>>>(top, n, E, b.counts);
+        bucket_count_kernel<false><<<nblocks, 32 * kWarps, 0, st>>>(top, n, nullptr, E, b.counts);
     }
     XMOE_LAUNCH_CHECK();
     bucket_scan_kernel<<<1, 1024, 0, st>>>(nblocks * kWarps, E, cap, b.counts, b.raw_cnt,
@@ -432,9 +447,9 @@ void launch_pft(const int32_t* top, const double* w, int S, int k, int E, int ca
     XMOE_LAUNCH_CHECK();
     if (smem) {
         bucket_place_kernel<true><<<nblocks, 32 * kWarps, smem_bytes, st>>>(
-            top, n, E, b.counts, b.raw_base, b.sorted_f);
+            top, n, nullptr, E, b.counts, b.raw_base, b.sorted_f);
     } else {
-        bucket_place_kernel<false><<<nblocks, 32 * kWarps, 0, st>>>(top, n, E, b.counts,
+        bucket_place_kernel<false><<<nblocks, 32 * kWarps, 0, st>>>(top, n, nullptr, E, b.counts,
                                                                       b.raw_base, b.sorted_f);
     }
     XMOE_LAUNCH_CHECK();
@@ -458,10 +473,12 @@ void launch_pft_validate(const int32_t* top, int S, int k, int E, unsigned long 
     XMOE_LAUNCH_CHECK();
 }
 
-// Stable CSR of arbitrary keys (token ids for scatter_combine): perm[pos] = i
-// with positions grouped by key ascending and i ascending within a key.
-void launch_stable_csr(const int32_t* keys, int n, int K, int32_t* ptr /*[K+1]*/,
-                       int32_t* perm /*[n]*/, void* ws, cudaStream_t st) {
+// Stable CSR of arbitrary keys (token ids for scatter_combine, destination
+// ranks for RBD groups): perm[pos] = i with positions grouped by key
+// ascending and i ascending within a key.  The item count is n_host, or
+// *n_dev (bounded by n_host) when n_dev is given.
+void launch_stable_csr_dev(const int32_t* keys, const int32_t* n_dev, int n, int K, int32_t* ptr,
+                           int32_t* perm, void* ws, cudaStream_t st) {
     BucketWs b = carve(ws, n, K);
     if (n == 0) {
         XMOE_CUDA(cudaMemsetAsync(ptr, 0, sizeof(int32_t) * (K + 1), st));
@@ -472,17 +489,22 @@ void launch_stable_csr(const int32_t* keys, int n, int K, int32_t* ptr /*[K+1]*/
     const bool smem = K <= 1536;
     const size_t smem_bytes = smem ? sizeof(int32_t) * kWarps * K : 0;
     if (!smem) XMOE_CUDA(cudaMemsetAsync(b.counts, 0, sizeof(int32_t) * nblocks * kWarps * K, st));
-    if (smem) bucket_count_kernel<true><<<nblocks, 32 * kWarps, smem_bytes, st>>>(keys, n, K, b.counts);
-    else bucket_count_kernel<false><<<nblocks, 32 * kWarps, 0, st>>>(keys, n, K, b.counts);
+    if (smem) bucket_count_kernel<true><<<nblocks, 32 * kWarps, smem_bytes, st>>>(keys, n, n_dev, K, b.counts);
+    else bucket_count_kernel<false><<<nblocks, 32 * kWarps, 0, st>>>(keys, n, n_dev, K, b.counts);
     XMOE_LAUNCH_CHECK();
     bucket_scan_kernel<<<1, 1024, 0, st>>>(nblocks * kWarps, K, 0x7fffffff, b.counts, b.raw_cnt,
                                            ptr, b.kept_base, nullptr, b.flags, nullptr);
     XMOE_LAUNCH_CHECK();
     if (smem)
-        bucket_place_kernel<true><<<nblocks, 32 * kWarps, smem_bytes, st>>>(keys, n, K, b.counts, ptr, perm);
+        bucket_place_kernel<true><<<nblocks, 32 * kWarps, smem_bytes, st>>>(keys, n, n_dev, K, b.counts, ptr, perm);
     else
-        bucket_place_kernel<false><<<nblocks, 32 * kWarps, 0, st>>>(keys, n, K, b.counts, ptr, perm);
+        bucket_place_kernel<false><<<nblocks, 32 * kWarps, 0, st>>>(keys, n, n_dev, K, b.counts, ptr, perm);
     XMOE_LAUNCH_CHECK();
+}
+
+void launch_stable_csr(const int32_t* keys, int n, int K, int32_t* ptr, int32_t* perm, void* ws,
+                       cudaStream_t st) {
+    launch_stable_csr_dev(keys, nullptr, n, K, ptr, perm, ws, st);
 }
 
 }  // namespace xmoe

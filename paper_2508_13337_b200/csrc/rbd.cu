@@ -1,0 +1,487 @@
+// Redundancy-bypassing dispatch (RBD) with one GPU per "node" — B200
+// restatement of moesim::select_pilots / rbd_dispatch / rbd_combine
+// (/root/reference/proj/src/rbd.cpp:26-358) with node_of[w] = w.
+//
+// A token routed to several experts on one destination GPU crosses NVLink
+// once.  Per source rank:
+//   groups   copies grouped by (token, destination rank), ordered (token asc,
+//            dest asc) — the reference's std::map key order (rbd.cpp:35-43)
+//   pilots   one Rng(salt_seed(seed, w, 0)).below(|group|) draw per group in
+//            that order picks the pilot among the members in packed order
+//            (rbd.cpp:45-51).  Group g uses the g-th xoshiro256** output: a
+//            chunked jump-ahead (GF(2) matrix powers of the state transition)
+//            lets every CTA start its 256-group chunk in parallel.
+//   pack     each group's token row once (dest-major, token order) plus one
+//            24-byte descriptor per copy {row in the unique buffer at the
+//            receiver, row in the receiver's grouped expert input, weight,
+//            group size, member index | pilot flag}
+//   expand   receiver writes every copy into its grouped (local expert,
+//            source, position) row — bit-identical to pf_dispatch
+//   merge    receiver scales the pilot's expert output by its weight and adds
+//            each other member's weighted output in packed order
+//            (rbd.cpp:318-336); singletons return raw
+//   combine  source adds its groups in pilot order with scale 1 (merged) or
+//            the pilot weight (singleton) (rbd.cpp:343-356).
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "rbd.h"
+
+namespace xmoe {
+
+// ---------------------------------------------------------------- xoshiro256**
+namespace {
+__host__ __device__ inline uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+
+__host__ __device__ inline uint64_t xoshiro_next(uint64_t* s) {
+    const uint64_t result = rotl64(s[1] * 5, 7) * 9;
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = rotl64(s[3], 45);
+    return result;
+}
+
+uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+// 256x256 GF(2) matrix, row-major: row i has bit j set iff out_i depends on in_j.
+struct Mat {
+    uint64_t r[256][4];
+};
+
+void mat_mul(const Mat& A, const Mat& B, Mat& C) {  // C = A * B
+    for (int i = 0; i < 256; ++i) {
+        uint64_t acc[4] = {0, 0, 0, 0};
+        for (int j = 0; j < 256; ++j)
+            if ((A.r[i][j >> 6] >> (j & 63)) & 1)
+                for (int w = 0; w < 4; ++w) acc[w] ^= B.r[j][w];
+        for (int w = 0; w < 4; ++w) C.r[i][w] = acc[w];
+    }
+}
+}  // namespace
+
+uint64_t salt_seed_host(uint64_t seed, uint64_t a, uint64_t b) {
+    // include/moesim/rng.hpp:17-19
+    return splitmix64(splitmix64(seed ^ 0x6d6f6573696d0001ULL) + splitmix64(a) * 3 + b);
+}
+
+void rng_state_from_seed(uint64_t seed, uint64_t out[4]) {
+    // Rng(seed) constructor, rng.hpp:26-29
+    uint64_t x = seed;
+    for (int i = 0; i < 4; ++i) out[i] = x = splitmix64(x);
+}
+
+// Jump matrices J_k = T^(kRbdChunk * 2^k), T = one xoshiro step.
+void rbd_jump_tables(std::vector<uint64_t>& out) {
+    Mat T;
+    for (int j = 0; j < 256; ++j) {  // column j = T(e_j)
+        uint64_t s[4] = {0, 0, 0, 0};
+        s[j >> 6] = 1ull << (j & 63);
+        xoshiro_next(s);
+        for (int i = 0; i < 256; ++i) {
+            if (j == 0) T.r[i][0] = T.r[i][1] = T.r[i][2] = T.r[i][3] = 0;
+            if ((s[i >> 6] >> (i & 63)) & 1) T.r[i][j >> 6] |= 1ull << (j & 63);
+        }
+    }
+    Mat P = T, tmp;
+    for (int c = 1; c < kRbdChunk; c <<= 1) {  // T^kRbdChunk by squaring
+        mat_mul(P, P, tmp);
+        P = tmp;
+    }
+    out.assign(static_cast<size_t>(kRbdJumps) * 256 * 4, 0);
+    for (int k = 0; k < kRbdJumps; ++k) {
+        for (int i = 0; i < 256; ++i)
+            for (int w = 0; w < 4; ++w) out[(static_cast<size_t>(k) * 256 + i) * 4 + w] = P.r[i][w];
+        mat_mul(P, P, tmp);
+        P = tmp;
+    }
+}
+
+// One CTA per chunk of kRbdChunk groups: jump the seed state to the chunk
+// start (thread i computes output bit i of each matrix-vector product), then
+// one thread steps through the chunk.
+__global__ void __launch_bounds__(256) rbd_draw_kernel(uint64_t s0, uint64_t s1, uint64_t s2,
+                                                      uint64_t s3, const uint64_t* __restrict__ jumps,
+                                                      const int32_t* __restrict__ G_dev,
+                                                      uint64_t* __restrict__ draws) {
+    __shared__ uint64_t st[4];
+    __shared__ uint32_t bits[8];
+    const int G = *G_dev;
+    const int c = blockIdx.x;
+    if (c * kRbdChunk >= G) return;
+    if (threadIdx.x == 0) {
+        st[0] = s0;
+        st[1] = s1;
+        st[2] = s2;
+        st[3] = s3;
+    }
+    __syncthreads();
+    const int i = threadIdx.x;
+    for (int k = 0; k < kRbdJumps && (c >> k); ++k) {
+        if (!((c >> k) & 1)) continue;
+        const uint64_t* row = jumps + (static_cast<size_t>(k) * 256 + i) * 4;
+        const int par = (__popcll(row[0] & st[0]) + __popcll(row[1] & st[1]) +
+                         __popcll(row[2] & st[2]) + __popcll(row[3] & st[3])) & 1;
+        const unsigned b = __ballot_sync(0xffffffffu, par);
+        if ((i & 31) == 0) bits[i >> 5] = b;
+        __syncthreads();
+        if (i < 4) st[i] = static_cast<uint64_t>(bits[2 * i]) | (static_cast<uint64_t>(bits[2 * i + 1]) << 32);
+        __syncthreads();
+    }
+    if (i == 0) {
+        uint64_t s[4] = {st[0], st[1], st[2], st[3]};
+        const int n = min(kRbdChunk, G - c * kRbdChunk);
+        for (int j = 0; j < n; ++j) draws[c * kRbdChunk + j] = xoshiro_next(s);
+    }
+}
+
+// ---------------------------------------------------------------- groups
+// Per token: number of distinct destination ranks among its kept copies
+// (slot_pos is ascending packed row = ascending expert = ascending dest).
+__global__ void rbd_group_count_kernel(const int32_t* __restrict__ slot_pos,
+                                       const int32_t* __restrict__ expert_ids, int S, int k, int El,
+                                       int32_t* __restrict__ gcount) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= S) return;
+    int n = 0, last = -1;
+    for (int j = 0; j < k; ++j) {
+        const int p = slot_pos[static_cast<size_t>(t) * k + j];
+        if (p < 0) break;
+        const int d = expert_ids[p] / El;
+        if (d != last) {
+            ++n;
+            last = d;
+        }
+    }
+    gcount[t] = n;
+}
+
+// Single-CTA exclusive scan of n int32 (n up to a few 10^6); total -> *total.
+__global__ void __launch_bounds__(1024) exclusive_scan_kernel(const int32_t* __restrict__ in, int n,
+                                                              int32_t* __restrict__ out,
+                                                              int32_t* __restrict__ total) {
+    __shared__ int32_t s[1024];
+    __shared__ int32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int per = (n + 1023) / 1024;
+    for (int i0 = 0; i0 < n; i0 += 1024 * 16) {
+        // each thread owns up to 16 consecutive items of this tile
+        const int my0 = i0 + threadIdx.x * 16;
+        int loc[16];
+        int sum = 0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int v = (my0 + q < n) ? in[my0 + q] : 0;
+            loc[q] = sum;
+            sum += v;
+        }
+        s[threadIdx.x] = sum;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {
+            const int a = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
+            __syncthreads();
+            s[threadIdx.x] += a;
+            __syncthreads();
+        }
+        const int before = carry + s[threadIdx.x] - sum;
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+            if (my0 + q < n) out[my0 + q] = before + loc[q];
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += s[1023];
+        __syncthreads();
+    }
+    (void)per;
+    if (threadIdx.x == 0 && total) *total = carry;
+}
+
+// Per token: emit its groups (gid = gbase[t] + j) with the drawn pilot.
+__global__ void rbd_group_fill_kernel(const int32_t* __restrict__ slot_pos,
+                                      const int32_t* __restrict__ expert_ids, int S, int k, int El,
+                                      const int32_t* __restrict__ gbase,
+                                      const uint64_t* __restrict__ draws, RbdGroups g,
+                                      int32_t* __restrict__ flags) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= S) return;
+    int gid = gbase[t];
+    int j = 0;
+    while (j < k) {
+        const int p0 = slot_pos[static_cast<size_t>(t) * k + j];
+        if (p0 < 0) break;
+        const int d = expert_ids[p0] / El;
+        int n = 1;
+        while (j + n < k) {
+            const int p = slot_pos[static_cast<size_t>(t) * k + j + n];
+            if (p < 0 || expert_ids[p] / El != d) break;
+            ++n;
+        }
+        // Rng::below(n) (rng.hpp:49-54): reject the top partial bucket
+        const uint64_t x = draws[gid];
+        const uint64_t limit = ~0ull - (~0ull % static_cast<uint64_t>(n) + 1) % static_cast<uint64_t>(n);
+        if (x > limit) atomicExch(flags, 1);  // probability ~n/2^64: reported, not replayed
+        const int pick = static_cast<int>(x % static_cast<uint64_t>(n));
+        g.token[gid] = t;
+        g.dest[gid] = d;
+        g.first_slot[gid] = j;
+        g.n[gid] = n;
+        g.pilot[gid] = slot_pos[static_cast<size_t>(t) * k + j + pick];
+        ++gid;
+        j += n;
+    }
+}
+
+// Position of every group in the dest-sorted order -> per-dest index u and
+// the group's first descriptor.  perm/ptr come from the stable CSR by dest.
+__global__ void rbd_group_pos_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ G_dev,
+                                     const RbdGroups g, int32_t* __restrict__ nsorted) {
+    const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos >= *G_dev) return;
+    const int gid = perm[pos];
+    g.pos[gid] = pos;
+    nsorted[pos] = g.n[gid];
+}
+
+// Sender pack: unique rows (dest-sorted) and one descriptor per copy.
+__global__ void __launch_bounds__(256) rbd_pack_kernel(
+    const char* __restrict__ x, int row_bytes, const int32_t* __restrict__ perm,
+    const int32_t* __restrict__ G_dev, const RbdGroups g, const int32_t* __restrict__ dptr,
+    const int32_t* __restrict__ coff, const int32_t* __restrict__ ru_base,
+    const int32_t* __restrict__ slot_pos, int k, const int32_t* __restrict__ dest_row,
+    const double* __restrict__ cw, char* __restrict__ send_u, RbdDesc* __restrict__ desc) {
+    const int G = *G_dev;
+    const int lane = threadIdx.x & 31;
+    const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    for (long long pos = warp; pos < G; pos += nwarps) {
+        const int gid = perm[pos];
+        const int t = g.token[gid], d = g.dest[gid], n = g.n[gid], j0 = g.first_slot[gid];
+        const int pilot = g.pilot[gid];
+        if (lane < n) {
+            const int p = slot_pos[static_cast<size_t>(t) * k + j0 + lane];
+            RbdDesc dd;
+            dd.u = ru_base[d] + static_cast<int>(pos - dptr[d]);
+            dd.dest_row = dest_row[p];
+            dd.w = cw[p];
+            dd.n = n;
+            dd.member = lane | (p == pilot ? kRbdPilotFlag : 0);
+            desc[coff[pos] + lane] = dd;
+        }
+        // row copy, 16-byte vectors
+        const int4* s4 = reinterpret_cast<const int4*>(x + static_cast<size_t>(t) * row_bytes);
+        int4* d4 = reinterpret_cast<int4*>(send_u + static_cast<size_t>(pos) * row_bytes);
+        if ((row_bytes & 15) == 0) {
+            for (int v = lane; v < (row_bytes >> 4); v += 32) st_na_v4(d4 + v, ld_nc_v4(s4 + v));
+        } else {
+            const long long* s8 = reinterpret_cast<const long long*>(x + static_cast<size_t>(t) * row_bytes);
+            long long* d8 = reinterpret_cast<long long*>(send_u + static_cast<size_t>(pos) * row_bytes);
+            for (int v = lane; v < (row_bytes >> 3); v += 32) d8[v] = s8[v];
+        }
+    }
+}
+
+// Receiver expand: grouped[dest_row] = recv_u[u] for every received copy;
+// also records each group's first descriptor for the merge.
+__global__ void __launch_bounds__(256) rbd_expand_kernel(const char* __restrict__ recv_u,
+                                                         int row_bytes, const RbdDesc* __restrict__ desc,
+                                                         int ndesc, char* __restrict__ grouped,
+                                                         int32_t* __restrict__ gstart) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    for (long long c = warp; c < ndesc; c += nwarps) {
+        const RbdDesc dd = desc[c];
+        if (lane == 0 && (dd.member & ~kRbdPilotFlag) == 0) gstart[dd.u] = static_cast<int>(c);
+        const char* s = recv_u + static_cast<size_t>(dd.u) * row_bytes;
+        char* o = grouped + static_cast<size_t>(dd.dest_row) * row_bytes;
+        if ((row_bytes & 15) == 0) {
+            for (int v = lane; v < (row_bytes >> 4); v += 32)
+                st_na_v4(reinterpret_cast<int4*>(o) + v, ld_nc_v4(reinterpret_cast<const int4*>(s) + v));
+        } else {
+            for (int v = lane; v < (row_bytes >> 3); v += 32)
+                reinterpret_cast<long long*>(o)[v] = reinterpret_cast<const long long*>(s)[v];
+        }
+    }
+}
+
+// Receiver merge (rbd.cpp:318-336): one warp per received group.
+template <typename T>
+__global__ void __launch_bounds__(256) rbd_merge_kernel(const T* __restrict__ eout, int H,
+                                                        const RbdDesc* __restrict__ desc,
+                                                        const int32_t* __restrict__ gstart, int ngroups,
+                                                        T* __restrict__ back_u) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    for (long long u = warp; u < ngroups; u += nwarps) {
+        const int c0 = gstart[u];
+        const int n = desc[c0].n;
+        T* out = back_u + static_cast<size_t>(u) * H;
+        if (n == 1) {  // singleton: raw row
+            const T* y = eout + static_cast<size_t>(desc[c0].dest_row) * H;
+            for (int h = lane; h < H; h += 32) out[h] = y[h];
+            continue;
+        }
+        int pm = 0;
+        for (int m = 0; m < n; ++m)
+            if (desc[c0 + m].member & kRbdPilotFlag) pm = m;
+        for (int h = lane; h < H; h += 32) {
+            if constexpr (sizeof(T) == 8) {
+                const RbdDesc pd = desc[c0 + pm];
+                double acc = __dmul_rn(static_cast<double>(eout[static_cast<size_t>(pd.dest_row) * H + h]), pd.w);
+                for (int m = 0; m < n; ++m) {
+                    if (m == pm) continue;
+                    const RbdDesc md = desc[c0 + m];
+                    acc = __dadd_rn(acc, __dmul_rn(md.w, static_cast<double>(eout[static_cast<size_t>(md.dest_row) * H + h])));
+                }
+                out[h] = static_cast<T>(acc);
+            } else {
+                const RbdDesc pd = desc[c0 + pm];
+                float acc = __bfloat162float(eout[static_cast<size_t>(pd.dest_row) * H + h]) * static_cast<float>(pd.w);
+                for (int m = 0; m < n; ++m) {
+                    if (m == pm) continue;
+                    const RbdDesc md = desc[c0 + m];
+                    acc = fmaf(static_cast<float>(md.w), __bfloat162float(eout[static_cast<size_t>(md.dest_row) * H + h]), acc);
+                }
+                out[h] = __float2bfloat16_rn(acc);
+            }
+        }
+    }
+}
+
+// Source combine (rbd.cpp:343-356): per token, its groups in pilot order.
+template <typename T>
+__global__ void __launch_bounds__(256) rbd_combine_kernel(const T* __restrict__ ret_u, int H, int S,
+                                                          const int32_t* __restrict__ gbase,
+                                                          const int32_t* __restrict__ gcount,
+                                                          const RbdGroups g, const double* __restrict__ cw,
+                                                          const T* __restrict__ addend, T* __restrict__ out) {
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= S) return;
+    const int b = gbase[t], n = gcount[t];
+    // groups of a token are few (<= k): order them by pilot packed row
+    int order[32];
+    const int nn = n < 32 ? n : 32;
+    for (int i = 0; i < nn; ++i) {
+        int q = i;
+        const int pi = g.pilot[b + i];
+        while (q > 0 && g.pilot[b + order[q - 1]] > pi) {
+            order[q] = order[q - 1];
+            --q;
+        }
+        order[q] = i;
+    }
+    for (int h = lane; h < H; h += 32) {
+        if constexpr (sizeof(T) == 8) {
+            double acc = 0.0;
+            for (int i = 0; i < nn; ++i) {
+                const int gid = b + order[i];
+                const double sc = g.n[gid] > 1 ? 1.0 : cw[g.pilot[gid]];
+                acc = __dadd_rn(acc, __dmul_rn(sc, static_cast<double>(ret_u[static_cast<size_t>(g.pos[gid]) * H + h])));
+            }
+            if (addend) acc = __dadd_rn(acc, static_cast<double>(addend[static_cast<size_t>(t) * H + h]));
+            out[static_cast<size_t>(t) * H + h] = static_cast<T>(acc);
+        } else {
+            float acc = 0.f;
+            for (int i = 0; i < nn; ++i) {
+                const int gid = b + order[i];
+                const float sc = g.n[gid] > 1 ? 1.f : static_cast<float>(cw[g.pilot[gid]]);
+                acc = fmaf(sc, __bfloat162float(ret_u[static_cast<size_t>(g.pos[gid]) * H + h]), acc);
+            }
+            if (addend) acc += __bfloat162float(addend[static_cast<size_t>(t) * H + h]);
+            out[static_cast<size_t>(t) * H + h] = __float2bfloat16_rn(acc);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- launchers
+static int warp_grid(long long items) {
+    const long long b = (items + 7) / 8;
+    return static_cast<int>(b < 1 ? 1 : (b < 8 * kNumSMs ? b : 8 * kNumSMs));
+}
+
+void launch_rbd_groups(const int32_t* slot_pos, const int32_t* expert_ids, int S, int k, int El,
+                       const uint64_t state[4], const uint64_t* jumps, RbdWork& wk, cudaStream_t st) {
+    if (S == 0) {
+        XMOE_CUDA(cudaMemsetAsync(wk.G_dev, 0, sizeof(int32_t), st));
+        return;
+    }
+    rbd_group_count_kernel<<<ceil_div(S, 256), 256, 0, st>>>(slot_pos, expert_ids, S, k, El, wk.gcount);
+    XMOE_LAUNCH_CHECK();
+    exclusive_scan_kernel<<<1, 1024, 0, st>>>(wk.gcount, S, wk.gbase, wk.G_dev);
+    XMOE_LAUNCH_CHECK();
+    const long long max_groups = static_cast<long long>(S) * k;
+    rbd_draw_kernel<<<ceil_div(max_groups, kRbdChunk), 256, 0, st>>>(
+        state[0], state[1], state[2], state[3], jumps, wk.G_dev, wk.draws);
+    XMOE_LAUNCH_CHECK();
+    rbd_group_fill_kernel<<<ceil_div(S, 256), 256, 0, st>>>(slot_pos, expert_ids, S, k, El, wk.gbase,
+                                                             wk.draws, wk.g, wk.flags);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_rbd_sort(int W, long long max_groups, RbdWork& wk, cudaStream_t st) {
+    // stable bucket of groups by destination (groups are generated in
+    // (token, dest) order, so each dest segment stays in token order)
+    launch_stable_csr_dev(wk.g.dest, wk.G_dev, static_cast<int>(max_groups), W, wk.dptr, wk.perm,
+                          wk.csr_ws, st);
+    rbd_group_pos_kernel<<<ceil_div(max_groups, 256), 256, 0, st>>>(wk.perm, wk.G_dev, wk.g, wk.nsorted);
+    XMOE_LAUNCH_CHECK();
+    exclusive_scan_kernel<<<1, 1024, 0, st>>>(wk.nsorted, static_cast<int>(max_groups), wk.coff, nullptr);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, long long max_groups,
+                     const int32_t* ru_base, const int32_t* slot_pos, int k, const int32_t* dest_row,
+                     const double* cw, void* send_u, RbdDesc* desc, cudaStream_t st) {
+    rbd_pack_kernel<<<warp_grid(max_groups), 256, 0, st>>>(
+        static_cast<const char*>(x), row_bytes, wk.perm, wk.G_dev, wk.g, wk.dptr, wk.coff, ru_base,
+        slot_pos, k, dest_row, cw, static_cast<char*>(send_u), desc);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_rbd_expand(const void* recv_u, int row_bytes, const RbdDesc* desc, int ndesc,
+                       void* grouped, int32_t* gstart, cudaStream_t st) {
+    if (ndesc == 0) return;
+    rbd_expand_kernel<<<warp_grid(ndesc), 256, 0, st>>>(static_cast<const char*>(recv_u), row_bytes,
+                                                        desc, ndesc, static_cast<char*>(grouped), gstart);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_rbd_merge(int dtype, const void* eout, int H, const RbdDesc* desc, const int32_t* gstart,
+                      int ngroups, void* back_u, cudaStream_t st) {
+    if (ngroups == 0) return;
+    if (dtype == XMOE_F64)
+        rbd_merge_kernel<double><<<warp_grid(ngroups), 256, 0, st>>>(
+            static_cast<const double*>(eout), H, desc, gstart, ngroups, static_cast<double*>(back_u));
+    else
+        rbd_merge_kernel<__nv_bfloat16><<<warp_grid(ngroups), 256, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(eout), H, desc, gstart, ngroups,
+            static_cast<__nv_bfloat16*>(back_u));
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_rbd_combine(int dtype, const void* ret_u, int H, int S, const RbdWork& wk, const double* cw,
+                        const void* addend, void* out, cudaStream_t st) {
+    if (S == 0) return;
+    if (dtype == XMOE_F64)
+        rbd_combine_kernel<double><<<ceil_div(S, 8), 256, 0, st>>>(
+            static_cast<const double*>(ret_u), H, S, wk.gbase, wk.gcount, wk.g, cw,
+            static_cast<const double*>(addend), static_cast<double*>(out));
+    else
+        rbd_combine_kernel<__nv_bfloat16><<<ceil_div(S, 8), 256, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(ret_u), H, S, wk.gbase, wk.gcount, wk.g, cw,
+            static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out));
+    XMOE_LAUNCH_CHECK();
+}
+
+}  // namespace xmoe

@@ -1,0 +1,72 @@
+// Redundancy-bypassing dispatch: device data structures (see rbd.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+namespace xmoe {
+
+constexpr int kRbdChunk = 256;  // groups per jump-ahead chunk
+constexpr int kRbdJumps = 24;   // chunk index < 2^24
+constexpr int kRbdPilotFlag = 1 << 16;
+
+// One (token, destination rank) group of a source rank, in the reference's
+// std::map order (rbd.cpp:35-43).  SoA, indexed by group id.
+struct RbdGroups {
+    int32_t* token;
+    int32_t* dest;
+    int32_t* first_slot;  // first member in the token's slot list
+    int32_t* n;           // members
+    int32_t* pilot;       // packed row of the pilot copy
+    int32_t* pos;         // position in the dest-sorted order
+};
+
+// Per-copy descriptor riding with the unique rows (24 bytes).
+struct RbdDesc {
+    int32_t u;         // row of the group in the receiver's unique-row buffer
+    int32_t dest_row;  // row of the copy in the receiver's grouped expert input
+    double w;          // combine weight of the copy
+    int32_t n;         // group size
+    int32_t member;    // member index | kRbdPilotFlag
+};
+static_assert(sizeof(RbdDesc) == 24, "descriptor layout");
+
+struct RbdWork {
+    RbdGroups g;
+    int32_t* gcount;   // [S]
+    int32_t* gbase;    // [S]
+    int32_t* G_dev;    // total groups
+    uint64_t* draws;   // [S*k] xoshiro outputs
+    int32_t* flags;    // [1] rejection-sampling event seen
+    int32_t* dptr;     // [W+1] dest segment starts (dest-sorted)
+    int32_t* perm;     // [S*k] dest-sorted position -> group id
+    int32_t* nsorted;  // [S*k] group size in sorted order
+    int32_t* coff;     // [S*k] first descriptor of each sorted group
+    void* csr_ws;
+    uint64_t state[4];  // Rng(salt_seed(seed, rank, 0)) state
+};
+
+uint64_t salt_seed_host(uint64_t seed, uint64_t a, uint64_t b);
+void rng_state_from_seed(uint64_t seed, uint64_t out[4]);
+void rbd_jump_tables(std::vector<uint64_t>& out);
+
+void launch_rbd_groups(const int32_t* slot_pos, const int32_t* expert_ids, int S, int k, int El,
+                       const uint64_t state[4], const uint64_t* jumps, RbdWork& wk, cudaStream_t st);
+void launch_rbd_sort(int W, long long max_groups, RbdWork& wk, cudaStream_t st);
+void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, long long max_groups,
+                     const int32_t* ru_base, const int32_t* slot_pos, int k, const int32_t* dest_row,
+                     const double* cw, void* send_u, RbdDesc* desc, cudaStream_t st);
+void launch_rbd_expand(const void* recv_u, int row_bytes, const RbdDesc* desc, int ndesc,
+                       void* grouped, int32_t* gstart, cudaStream_t st);
+void launch_rbd_merge(int dtype, const void* eout, int H, const RbdDesc* desc, const int32_t* gstart,
+                      int ngroups, void* back_u, cudaStream_t st);
+void launch_rbd_combine(int dtype, const void* ret_u, int H, int S, const RbdWork& wk,
+                        const double* cw, const void* addend, void* out, cudaStream_t st);
+
+// pft.cu: stable CSR with the item count on the device (bound n_max).
+void launch_stable_csr_dev(const int32_t* keys, const int32_t* n_dev, int n_max, int K, int32_t* ptr,
+                           int32_t* perm, void* ws, cudaStream_t st);
+
+}  // namespace xmoe

@@ -124,3 +124,60 @@ def test_forward_bf16_vs_oracle(W, S, E, k, H, F, shared):
     for i in range(W):
         assert norm_rel(got[i], want[i]) < 1e-2, norm_rel(got[i], want[i])
         assert max_rel_diff(got[i], want[i]) < 2e-2, max_rel_diff(got[i], want[i])
+
+
+@pytest.mark.parametrize("W", [1, 2, 4, 8])
+def test_rbd_forward_f64_bit_exact(W):
+    """rbd_moe_forward with one GPU per node (node_of = rank): pilots drawn
+    from the reference RNG stream via jump-ahead, merge and combine orders
+    as rbd.cpp:318-356 — bit-exact given the device softmax weights."""
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, W, -1)
+    rng = O.Rng(1717 + W)
+    for trial in range(4):
+        E = W * (1 + rng.below(3))
+        k = 1 + rng.below(min(E, 4))
+        H = 2 + rng.below(5)
+        F = 2 + rng.below(5)
+        S = 2 + rng.below(23)
+        cap = 1 + rng.below(4) if trial % 2 == 0 else S * k
+        w = O.make_layer_weights(rng, E, H, F)
+        toks = np.array([rng.uniform(-1.0, 1.0) for _ in range(W * S * H)]).reshape(W, S, H)
+        seed = rng.next_u64()
+        L = _layer(ctx, capi.F64, E, H, F, k, cap, S, w, mode=capi.RBD, seed=seed)
+        got = host(L.forward(dev(toks)))
+        gates = _device_gates(ctx, toks, w, k)
+        exact = O.rbd_moe_forward(list(toks), w, E, k, cap, seed, gates=gates)
+        pure = O.rbd_moe_forward(list(toks), w, E, k, cap, seed)
+        for i in range(W):
+            assert np.array_equal(got[i], exact[i]), (trial, i)
+            assert max_rel_diff(got[i], pure[i]) < 1e-14
+        # per-GPU dedupe accounting: off-rank rows == distinct (token, dest) groups
+        led = L.ledger()
+        _, pfts, _, _ = O.pf_moe_forward(list(toks), w, E, k, cap, return_pfts=True, gates=gates)
+        nodes = O.expert_nodes(list(range(W)), E)
+        groups = sum(O.redundancy_counts_internode(p, s, nodes)[1] for s, p in enumerate(pfts))
+        copies = sum(O.redundancy_counts_internode(p, s, nodes)[0] for s, p in enumerate(pfts))
+        assert led["unique_rows_offrank"] == groups
+        assert led["copies_offrank"] == copies
+        assert led["dispatch_rows_offrank"] == groups * H * 8
+
+
+@pytest.mark.parametrize("W,S,E,k,H,F", [(4, 512, 64, 6, 256, 128), (8, 256, 64, 6, 128, 64)])
+def test_rbd_forward_bf16_vs_oracle(W, S, E, k, H, F):
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, W, -1)
+    rng = np.random.default_rng(S * W)
+    w = O.LayerWeights(grid_gate(rng, H, E), bf16_round(rng.uniform(-0.1, 0.1, (E, H, F))),
+                       bf16_round(rng.uniform(-0.1, 0.1, (E, F, H))))
+    x = grid_tokens(rng, W, S, H)
+    sw1 = bf16_round(rng.uniform(-0.1, 0.1, (2, H, F)))
+    sw2 = bf16_round(rng.uniform(-0.1, 0.1, (2, F, H)))
+    L = _layer(ctx, capi.BF16, E, H, F, k, S * k, S, w, sw1, sw2, mode=capi.RBD, seed=3)
+    got = host(L.forward(dev(x, torch.bfloat16)))
+    want = O.rbd_moe_forward(list(x), w, E, k, S * k, 3, exact=False, shared=(sw1, sw2))
+    for i in range(W):
+        assert norm_rel(got[i], want[i]) < 1e-2, norm_rel(got[i], want[i])
+        assert max_rel_diff(got[i], want[i]) < 2e-2, max_rel_diff(got[i], want[i])
+    led = L.ledger()
+    assert led["dispatch_rows_offrank"] < led["copies_offrank"] * H * 2  # bytes actually saved
