@@ -40,6 +40,8 @@ def parse():
     p.add_argument("--impl", default="xmoe", choices=["xmoe", "reference"])
     p.add_argument("--mode", default="naive", choices=["rbd", "naive"])
     p.add_argument("--tokens", type=int, default=C2["S"])
+    p.add_argument("--transport", default=None, choices=["p2p", "nccl"],
+                   help="N>1 row transport: NVLink peer kernels (default) or NCCL send/recv baseline")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-tokens", type=int, default=512,
                    help="tokens per host thread for the cpu_baseline sample")
@@ -172,7 +174,7 @@ def host_threads():
         return os.cpu_count() or 1
 
 
-def run_reference(args, rank, world):
+def run_reference(args, rank, world, result_out):
     if rank != 0:
         return
     # bounded per-step sample so that K+W steps stay within a few minutes
@@ -188,17 +190,25 @@ def run_reference(args, rank, world):
                        "tokens_per_gpu": args.tokens, "parallelism": f"ep{world}"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": desc},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=result_out, flush=True)
 
 
 # ---------------------------------------------------------------- xmoe arm
 def main():
+    # Everything but the one JSON line (NCCL banners, library prints) goes to
+    # stderr: fd 1 is re-pointed at fd 2 and the result is written to a dup
+    # of the original stdout.
+    result_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    sys.stdout = sys.stderr
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.transport:
+        os.environ["XMOE_TRANSPORT"] = args.transport
     if args.impl == "reference":
-        return run_reference(args, rank, world)
+        return run_reference(args, rank, world, result_out)
 
     import torch
     import torch.distributed as dist
@@ -340,6 +350,7 @@ def main():
                                    "d_ff 1408, bf16, expert parallel, dropless (BASELINE configs[1])",
                        "tokens_per_gpu": S, "global_tokens": world * S, "parallelism": f"ep{world}",
                        "dispatch": args.mode, "pass": "forward",
+                       "transport": (os.environ.get("XMOE_TRANSPORT") or "p2p") if world > 1 else "local",
                        "l2": "working set > L2: 0.74 GB of expert weights + 64 MB tokens stream each step (126 MB L2)"},
             "e2e": {"value": world * S / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": S * H * 2, "d2h_bytes_per_step": S * H * 2},
@@ -361,7 +372,7 @@ def main():
             "clocks": clk,
             "cpu_baseline": cpu,
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=result_out, flush=True)
     if world > 1:
         dist.destroy_process_group()
 

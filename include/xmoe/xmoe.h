@@ -51,6 +51,9 @@ extern "C" {
 #define XMOE_DISPATCH_NAIVE 0 /* pf_dispatch/pf_combine (pf_pipeline.cpp:12-135) */
 #define XMOE_DISPATCH_RBD 1   /* per-GPU redundancy bypass (rbd.cpp:26-358, node_of = rank) */
 
+/* layer flags */
+#define XMOE_LAYER_SSMB 1 /* ssmb_forward layer: every rank holds all experts (ssmb.cpp:29-43) */
+
 typedef struct xmoe_ctx xmoe_ctx;
 typedef struct xmoe_layer xmoe_layer;
 
@@ -140,7 +143,7 @@ typedef struct {
     int32_t dtype;           /* XMOE_F64 | XMOE_BF16 */
     int32_t renorm;          /* top-k renormalisation (0 = reference) */
     int32_t dispatch_mode;   /* XMOE_DISPATCH_NAIVE | XMOE_DISPATCH_RBD */
-    int32_t reserved;
+    int32_t flags;           /* XMOE_LAYER_SSMB: sequence-sharded block (experts replicated) */
     uint64_t seed;           /* RBD pilot seed (salted per rank: salt_seed(seed, w, 0)) */
 } xmoe_layer_desc;
 
@@ -159,7 +162,8 @@ int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S,
  * whole sequence on every rank; rank g runs rows [g*(S/G), ...) (last rank
  * takes the remainder) through the layer with every expert local
  * (the layer must hold all E experts), then an all-gather restores
- * out_full [S,H] on every rank.  G == world. */
+ * out_full [S,H] on every rank.  G == world.  The layer is created with
+ * XMOE_LAYER_SSMB and holds every expert; max_tokens >= the largest shard. */
 int xmoe_ssmb_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x_full, int64_t S,
                       void* out_full, void* stream);
 

@@ -38,7 +38,7 @@ class LayerDesc(C.Structure):
     _fields_ = [("num_experts", C.c_int64), ("model_dim", C.c_int64), ("ffn_dim", C.c_int64),
                 ("top_k", C.c_int64), ("max_token_count", C.c_int64), ("n_shared", C.c_int64),
                 ("shared_ffn_dim", C.c_int64), ("max_tokens", C.c_int64), ("dtype", C.c_int32),
-                ("renorm", C.c_int32), ("dispatch_mode", C.c_int32), ("reserved", C.c_int32),
+                ("renorm", C.c_int32), ("dispatch_mode", C.c_int32), ("flags", C.c_int32),
                 ("seed", C.c_uint64)]
 
 
@@ -207,12 +207,12 @@ class Layer:
 
     def __init__(self, ctx: Context, *, num_experts, model_dim, ffn_dim, top_k, max_token_count,
                  max_tokens, dtype, gate, w1, w2, sw1=None, sw2=None, renorm=False,
-                 dispatch_mode=NAIVE, seed=0):
+                 dispatch_mode=NAIVE, seed=0, ssmb=False):
         self.ctx = ctx
         ns = 0 if sw1 is None else sw1.shape[0]
         fs = 0 if sw1 is None else sw1.shape[2]
         self.desc = LayerDesc(num_experts, model_dim, ffn_dim, top_k, max_token_count, ns, fs,
-                              max_tokens, dtype, int(renorm), dispatch_mode, 0, seed)
+                              max_tokens, dtype, int(renorm), dispatch_mode, int(bool(ssmb)), seed)
         self.dtype = dtype
         self.H = model_dim
         h = C.c_void_p()

@@ -1,0 +1,517 @@
+// MoE layer: weights in the B200 layout, per-rank workspace, and the forward
+// pipeline that restates moesim::pf_moe_forward (pf_pipeline.cpp:137-169),
+// rbd_moe_forward (rbd.cpp:360-386) and ssmb_forward (ssmb.cpp:12-46):
+//
+//   gate -> PFT -> [RBD groups] -> count all-gather -> dispatch
+//        -> grouped expert FFN (+ shared experts) -> [RBD merge]
+//        -> combine
+//
+// Row movement between ranks.  Ranks that share a device (rank == -1
+// contexts, or world 1) and ranks in separate processes with NVLink peer
+// access ("p2p") use the SAME kernels over device pointer tables: the
+// dispatch kernel gathers token rows and stores them straight into the
+// owner's grouped expert input (a peer address when the owner is another
+// GPU), and the combine kernel reads expert outputs straight out of the
+// owners' buffers while it reduces.  No host synchronisation: the count
+// all-gather and two 4-byte all-reduces order the ranks.  The NCCL
+// send/recv transport (XMOE_TRANSPORT=nccl, plain dispatch only) is kept as
+// the library-collective baseline it is measured against.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "layer.h"
+#include "rbd.h"
+
+namespace xmoe {
+
+#define XMOE_NCCL(expr)                                                                \
+    do {                                                                               \
+        ncclResult_t _r = (expr);                                                      \
+        if (_r != ncclSuccess)                                                         \
+            ::xmoe::fail(XMOE_ERR_NCCL, std::string(#expr ": ") + ncclGetErrorString(_r)); \
+    } while (0)
+
+static size_t elem_size_of(int dtype) { return dtype == XMOE_F64 ? 8 : 2; }
+
+Layer::~Layer() {
+    for (void* p : peer_maps) cudaIpcCloseMemHandle(p);
+    for (void* p : allocs) cudaFree(p);
+    for (auto& e : events) cudaEventDestroy(e);
+}
+
+void* Layer::alloc(size_t bytes) {
+    void* p = nullptr;
+    XMOE_CUDA(cudaMalloc(&p, bytes ? bytes : 16));
+    allocs.push_back(p);
+    return p;
+}
+
+void Layer::mark(int ev, cudaStream_t st) {
+    if (timing) XMOE_CUDA(cudaEventRecord(events[ev], st));
+}
+
+void Layer::barrier(cudaStream_t st) {
+    XMOE_NCCL(ncclAllReduce(bar, bar, 1, ncclInt32, ncclSum, static_cast<ncclComm_t>(ctx->nccl), st));
+}
+
+long long Layer::C(int s, int d) const {
+    long long a = 0;
+    for (int le = 0; le < El; ++le) a += h_tpe[static_cast<size_t>(s) * E + d * El + le];
+    return a;
+}
+
+// ---------------------------------------------------------------- creation
+void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const void* w1,
+                  const void* w2, const void* sw1, const void* sw2, Layer& L) {
+    const bool ssmb = d.flags & XMOE_LAYER_SSMB;
+    const int W = ssmb ? 1 : ctx.world;
+    require(d.num_experts >= 1, XMOE_ERR_VALIDATION, "num_experts must be >= 1");
+    require(d.top_k >= 1, XMOE_ERR_VALIDATION, "top_k must be >= 1");
+    require(d.top_k <= d.num_experts, XMOE_ERR_VALIDATION, "top_k must be <= num_experts");
+    require(d.max_token_count >= 1, XMOE_ERR_VALIDATION, "max_token_count must be >= 1");
+    require(d.num_experts % W == 0, XMOE_ERR_VALIDATION,
+            "num_experts must be divisible by the worker-group size");
+    require(d.model_dim >= 1 && d.ffn_dim >= 1, XMOE_ERR_VALIDATION, "dims must be >= 1");
+    require(d.dispatch_mode == XMOE_DISPATCH_NAIVE || d.dispatch_mode == XMOE_DISPATCH_RBD,
+            XMOE_ERR_VALIDATION, "unknown dispatch mode");
+    const bool bf = d.dtype == XMOE_BF16;
+    require(bf || d.dtype == XMOE_F64, XMOE_ERR_VALIDATION, "unknown dtype");
+    if (bf) {
+        require(d.num_experts % 16 == 0, XMOE_ERR_VALIDATION,
+                "bf16 path requires num_experts to be a multiple of 16");
+        require(d.top_k <= 32, XMOE_ERR_VALIDATION, "bf16 path requires top_k <= 32");
+        require(d.model_dim % 16 == 0 && d.ffn_dim % 16 == 0, XMOE_ERR_VALIDATION,
+                "bf16 path requires model_dim and ffn_dim to be multiples of 16");
+        require(d.n_shared == 0 || (d.n_shared * d.shared_ffn_dim) % 16 == 0, XMOE_ERR_VALIDATION,
+                "bf16 path requires n_shared*shared_ffn_dim to be a multiple of 16");
+    }
+    L.ctx = &ctx;
+    L.d = d;
+    L.ssmb = ssmb;
+    L.W = W;
+    L.nl = ssmb ? 1 : ctx.n_local();
+    L.distributed = !ssmb && ctx.rank >= 0 && W > 1;
+    L.E = static_cast<int>(d.num_experts);
+    L.H = static_cast<int>(d.model_dim);
+    L.F = static_cast<int>(d.ffn_dim);
+    L.k = static_cast<int>(d.top_k);
+    L.El = L.E / W;
+    L.E_held = L.distributed ? L.El : L.E;
+    L.Fs = static_cast<int>(d.n_shared * d.shared_ffn_dim);
+    L.es = elem_size_of(d.dtype);
+    const bool rbd = d.dispatch_mode == XMOE_DISPATCH_RBD;
+    if (L.distributed) {
+        const char* tr = std::getenv("XMOE_TRANSPORT");
+        L.p2p = !(tr && std::string(tr) == "nccl");
+        require(L.p2p || !rbd, XMOE_ERR_VALIDATION,
+                "the redundancy-bypassing dispatch runs on the NVLink peer transport");
+    }
+    const int H = L.H, F = L.F, E = L.E;
+    const size_t es = L.es;
+    cudaStream_t st = nullptr;
+
+    // ---- weights: F64 keeps the reference layouts; BF16 goes K-major
+    L.gate = L.alloc(static_cast<size_t>(H) * E * es);
+    L.w1 = L.alloc(static_cast<size_t>(L.E_held) * H * F * es);
+    L.w2 = L.alloc(static_cast<size_t>(L.E_held) * H * F * es);
+    if (!bf) {
+        XMOE_CUDA(cudaMemcpy(L.gate, gate, static_cast<size_t>(H) * E * es, cudaMemcpyDeviceToDevice));
+        XMOE_CUDA(cudaMemcpy(L.w1, w1, static_cast<size_t>(L.E_held) * H * F * es, cudaMemcpyDeviceToDevice));
+        XMOE_CUDA(cudaMemcpy(L.w2, w2, static_cast<size_t>(L.E_held) * H * F * es, cudaMemcpyDeviceToDevice));
+    } else {
+        launch_transpose(XMOE_BF16, gate, 1, H, E, XMOE_BF16, L.gate, st);       // [E,H]
+        launch_transpose(XMOE_BF16, w1, L.E_held, H, F, XMOE_BF16, L.w1, st);    // [El,F,H]
+        launch_transpose(XMOE_BF16, w2, L.E_held, F, H, XMOE_BF16, L.w2, st);    // [El,H,F]
+    }
+    if (L.Fs > 0) {
+        require(sw1 && sw2, XMOE_ERR_VALIDATION, "shared expert weights missing");
+        const int ns = static_cast<int>(d.n_shared), Fs1 = static_cast<int>(d.shared_ffn_dim);
+        L.sw1 = L.alloc(static_cast<size_t>(H) * L.Fs * es);
+        L.sw2 = L.alloc(static_cast<size_t>(H) * L.Fs * es);
+        // merged shared FFN (moe_oracle.shared_expert_forward): W1cat [H, ns*Fs], W2cat [ns*Fs, H]
+        if (!bf) {
+            for (int s = 0; s < ns; ++s)
+                XMOE_CUDA(cudaMemcpy2D(static_cast<char*>(L.sw1) + static_cast<size_t>(s) * Fs1 * es,
+                                       static_cast<size_t>(L.Fs) * es,
+                                       static_cast<const char*>(sw1) + static_cast<size_t>(s) * H * Fs1 * es,
+                                       static_cast<size_t>(Fs1) * es, static_cast<size_t>(Fs1) * es, H,
+                                       cudaMemcpyDeviceToDevice));
+            XMOE_CUDA(cudaMemcpy(L.sw2, sw2, static_cast<size_t>(H) * L.Fs * es, cudaMemcpyDeviceToDevice));
+        } else {
+            launch_transpose(XMOE_BF16, sw1, ns, H, Fs1, XMOE_BF16, L.sw1, st);  // [ns*Fs, H]
+            launch_transpose(XMOE_BF16, sw2, 1, L.Fs, H, XMOE_BF16, L.sw2, st);  // [H, ns*Fs]
+        }
+    }
+
+    // ---- per-rank workspace
+    const long long S = d.max_tokens;
+    require(S >= 1, XMOE_ERR_VALIDATION, "max_tokens must be >= 1");
+    const long long nk = S * L.k;
+    const long long per_src = S * std::min<long long>(L.k, L.El);
+    const long long cap_bound = static_cast<long long>(W) * L.El * d.max_token_count;
+    L.R_max = std::max<long long>(1, std::min<long long>(static_cast<long long>(W) * per_src, cap_bound));
+    L.S_max = S;
+    const long long gmax = S * std::min<long long>(L.k, W);  // RBD groups per source
+    const long long rmax = static_cast<long long>(W) * S;   // RBD groups received
+    L.tpe_all = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * W * E));
+    L.G_all = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * W * W));
+    L.bar = static_cast<int32_t*>(L.alloc(64));
+    // symmetric region (same offsets on every rank; exported over IPC in p2p mode)
+    auto up = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
+    const size_t off_recv = 0;
+    const size_t off_eout = off_recv + up(static_cast<size_t>(L.R_max) * H * es);
+    const size_t off_recv_u = off_eout + up(static_cast<size_t>(L.R_max) * H * es);
+    const size_t off_desc = off_recv_u + (rbd ? up(static_cast<size_t>(rmax) * H * es) : 0);
+    const size_t off_back = off_desc + (rbd ? up(sizeof(RbdDesc) * L.R_max) : 0);
+    const size_t sym_bytes = off_back + (rbd ? up(static_cast<size_t>(rmax) * H * es) : 0);
+    L.workers.resize(L.nl);
+    std::vector<char*> t_recv(W), t_eout(W), t_recv_u(W), t_desc(W), t_back(W);
+    for (int i = 0; i < L.nl; ++i) {
+        Worker& w = L.workers[i];
+        w.rank = ssmb ? 0 : ctx.rank_of(i);
+        w.logits = static_cast<double*>(L.alloc(sizeof(double) * S * E));
+        w.top = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * nk));
+        w.wts = static_cast<double*>(L.alloc(sizeof(double) * nk));
+        w.token_ids = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * nk));
+        w.expert_ids = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * nk));
+        w.cw = static_cast<double*>(L.alloc(sizeof(double) * nk));
+        w.slot_pos = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * nk));
+        w.B_dev = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * 4));
+        w.tpe = L.distributed ? static_cast<int32_t*>(L.alloc(sizeof(int32_t) * E))
+                              : L.tpe_all + static_cast<size_t>(w.rank) * E;
+        w.pft_ws = L.alloc(bucket_ws_bytes(nk, E));
+        w.dest_rank = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * nk));
+        w.dest_row = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * nk));
+        w.rpe = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * L.El));
+        w.sym = static_cast<char*>(L.alloc(sym_bytes));
+        w.recv = w.sym + off_recv;
+        w.eout = w.sym + off_eout;
+        w.mid = L.alloc(static_cast<size_t>(L.R_max) * F * es);
+        if (L.distributed && !L.p2p) {
+            w.send = L.alloc(static_cast<size_t>(nk) * H * es);
+            w.back = L.alloc(static_cast<size_t>(nk) * H * es);
+        }
+        w.s_rows = static_cast<int32_t*>(L.alloc(sizeof(int32_t)));
+        if (L.Fs > 0) {
+            w.smid = L.alloc(static_cast<size_t>(S) * L.Fs * es);
+            w.sout = L.alloc(static_cast<size_t>(S) * H * es);
+        }
+        if (rbd) {
+            RbdWork& r = w.rbd;
+            auto i32 = [&](long long n) { return static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (n + 1))); };
+            r.g.token = i32(nk);
+            r.g.dest = i32(nk);
+            r.g.first_slot = i32(nk);
+            r.g.n = i32(nk);
+            r.g.pilot = i32(nk);
+            r.g.pos = i32(nk);
+            r.gcount = i32(S);
+            r.gbase = i32(S);
+            r.G_dev = i32(1);
+            r.flags = i32(1);
+            r.draws = static_cast<uint64_t*>(L.alloc(sizeof(uint64_t) * (nk + kRbdChunk)));
+            r.dptr = i32(W + 1);
+            r.perm = i32(nk);
+            r.nsorted = i32(nk);
+            r.coff = i32(nk);
+            r.csr_ws = L.alloc(bucket_ws_bytes(nk, W));
+            r.ru_base = i32(W);
+            r.rd_base = i32(W);
+            r.cseg = i32(W);
+            r.rx = i32(2);
+            rng_state_from_seed(salt_seed_host(d.seed, static_cast<uint64_t>(w.rank), 0), r.state);
+            w.recv_u = w.sym + off_recv_u;
+            w.desc_recv = reinterpret_cast<RbdDesc*>(w.sym + off_desc);
+            w.back_u = w.sym + off_back;
+            w.gstart = i32(rmax);
+        }
+        t_recv[w.rank] = static_cast<char*>(w.recv);
+        t_eout[w.rank] = static_cast<char*>(w.eout);
+        t_recv_u[w.rank] = static_cast<char*>(w.recv_u);
+        t_desc[w.rank] = reinterpret_cast<char*>(w.desc_recv);
+        t_back[w.rank] = static_cast<char*>(w.back_u);
+    }
+    if (L.distributed && L.p2p) {
+        // export my symmetric region, import every peer's (CUDA IPC over NVLink)
+        Worker& w = L.workers[0];
+        cudaIpcMemHandle_t mine;
+        XMOE_CUDA(cudaIpcGetMemHandle(&mine, w.sym));
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+        char* hb = static_cast<char*>(L.alloc(64 * W));
+        XMOE_CUDA(cudaMemcpy(hb + 64 * w.rank, &mine, 64, cudaMemcpyHostToDevice));
+        XMOE_NCCL(ncclAllGather(hb + 64 * w.rank, hb, 64, ncclUint8, static_cast<ncclComm_t>(ctx.nccl), st));
+        std::vector<cudaIpcMemHandle_t> hs(W);
+        XMOE_CUDA(cudaMemcpy(hs.data(), hb, 64 * W, cudaMemcpyDeviceToHost));
+        for (int r = 0; r < W; ++r) {
+            if (r == w.rank) continue;
+            void* p = nullptr;
+            XMOE_CUDA(cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess));
+            L.peer_maps.push_back(p);
+            char* b = static_cast<char*>(p);
+            t_recv[r] = b + off_recv;
+            t_eout[r] = b + off_eout;
+            t_recv_u[r] = b + off_recv_u;
+            t_desc[r] = b + off_desc;
+            t_back[r] = b + off_back;
+        }
+    }
+    auto table = [&](const std::vector<char*>& v) {
+        char** t = static_cast<char**>(L.alloc(sizeof(char*) * W));
+        XMOE_CUDA(cudaMemcpy(t, v.data(), sizeof(char*) * W, cudaMemcpyHostToDevice));
+        return t;
+    };
+    L.recv_tab = table(t_recv);
+    L.eout_tab = table(t_eout);
+    if (rbd) {
+        L.recv_u_tab = table(t_recv_u);
+        L.desc_tab = reinterpret_cast<RbdDesc**>(table(t_desc));
+        L.back_tab = table(t_back);
+        std::vector<uint64_t> jt;
+        rbd_jump_tables(jt);
+        L.jumps = static_cast<uint64_t*>(L.alloc(sizeof(uint64_t) * jt.size()));
+        XMOE_CUDA(cudaMemcpy(L.jumps, jt.data(), sizeof(uint64_t) * jt.size(), cudaMemcpyHostToDevice));
+    }
+    L.events.resize(kNumEvents);
+    for (auto& e : L.events) XMOE_CUDA(cudaEventCreate(&e));
+    XMOE_CUDA(cudaDeviceSynchronize());
+}
+
+// expert weights of the worker owning rank r, inside this layer's allocation
+static const void* w1_of(const Layer& L, int r) {
+    const size_t off = L.distributed ? 0 : static_cast<size_t>(r) * L.El * L.H * L.F * L.es;
+    return static_cast<const char*>(L.w1) + off;
+}
+static const void* w2_of(const Layer& L, int r) {
+    const size_t off = L.distributed ? 0 : static_cast<size_t>(r) * L.El * L.H * L.F * L.es;
+    return static_cast<const char*>(L.w2) + off;
+}
+
+static void run_gemm(int dtype, const void* A, long long rows_bound, int K, const int32_t* rpg, int G,
+                     const void* B, int N, void* D, int relu, cudaStream_t st) {
+    if (dtype == XMOE_F64)
+        launch_grouped_gemm_f64(static_cast<const double*>(A), rows_bound, K, rpg, G,
+                                static_cast<const double*>(B), N, static_cast<double*>(D), relu, st);
+    else
+        launch_grouped_gemm_bf16(A, rows_bound, K, rpg, G, B, N, D, relu, st);
+}
+
+// ---------------------------------------------------------------- forward
+// x/out: [nl, S, H] (nl = ranks this process drives).
+void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t st) {
+    Ctx& ctx = *L.ctx;
+    require(S >= 0 && S <= L.S_max, XMOE_ERR_VALIDATION, "sequence longer than the layer's max_tokens");
+    const int W = L.W, E = L.E, H = L.H, F = L.F, k = L.k;
+    const int dt = L.d.dtype;
+    const size_t row_bytes = static_cast<size_t>(H) * L.es;
+    const int nl = L.nl;
+    const bool dist = L.distributed;
+    const bool tables = !dist || L.p2p;  // row movement by kernels over pointer tables
+    const bool rbd = L.d.dispatch_mode == XMOE_DISPATCH_RBD;
+    const char* xb = static_cast<const char*>(x);
+    char* ob = static_cast<char*>(out);
+    const long long nk = S * k;
+    auto x_of = [&](int i) { return xb + static_cast<size_t>(i) * S * row_bytes; };
+    auto o_of = [&](int i) { return ob + static_cast<size_t>(i) * S * row_bytes; };
+
+    L.mark(kEvStart, st);
+    // 1. gate (gating.cpp:14-57)
+    for (int i = 0; i < nl; ++i) {
+        Worker& w = L.workers[i];
+        launch_fill_i32(w.s_rows, 1, static_cast<int32_t>(S), st);  // one dense group of S rows
+        if (dt == XMOE_F64) {
+            launch_gate_logits_f64(reinterpret_cast<const double*>(x_of(i)), static_cast<const double*>(L.gate),
+                                   S, H, E, w.logits, st);
+            launch_softmax_topk(w.logits, S, E, k, L.d.renorm, w.top, w.wts, st);
+        } else {
+            float* lg = reinterpret_cast<float*>(w.logits);
+            launch_grouped_gemm_bf16_f32out(x_of(i), S, H, w.s_rows, 1, L.gate, E, lg, 0, st);
+            launch_softmax_topk_f32(lg, S, E, k, L.d.renorm, w.top, w.wts, st);
+        }
+    }
+    L.mark(kEvGate, st);
+    // 2. padding-free token buffer (pft.cpp:12-60) [+ RBD groups and pilots, rbd.cpp:26-81]
+    for (int i = 0; i < nl; ++i) {
+        Worker& w = L.workers[i];
+        launch_pft(w.top, w.wts, S, k, E, static_cast<int>(std::min<long long>(L.d.max_token_count, 0x7fffffff)),
+                   w.token_ids, w.expert_ids, w.cw, w.tpe, w.slot_pos, w.B_dev, w.pft_ws, st);
+        if (rbd) {
+            launch_rbd_groups(w.slot_pos, w.expert_ids, static_cast<int>(S), k, L.El, w.rbd.state, L.jumps,
+                              w.rbd, st);
+            launch_rbd_sort(W, nk, w.rbd, st);
+            launch_adjacent_diff(w.rbd.dptr, W, L.G_all + static_cast<size_t>(w.rank) * W, st);
+        }
+    }
+    L.mark(kEvPft, st);
+    // 3. per-expert (and per-destination group) counts to every rank
+    //    (pf_pipeline.cpp:30-36).  Completing it also proves every peer is
+    //    past its previous forward, so their buffers may be overwritten.
+    if (dist) {
+        Worker& w = L.workers[0];
+        auto comm = static_cast<ncclComm_t>(ctx.nccl);
+        XMOE_NCCL(ncclGroupStart());
+        XMOE_NCCL(ncclAllGather(w.tpe, L.tpe_all, E, ncclInt32, comm, st));
+        if (rbd)
+            XMOE_NCCL(ncclAllGather(L.G_all + static_cast<size_t>(w.rank) * W, L.G_all, W, ncclInt32, comm, st));
+        XMOE_NCCL(ncclGroupEnd());
+    }
+    // 4. dispatch: destination rows in the owner's (local expert, source,
+    //    position) layout (pf_pipeline.cpp:47-73), then the rows themselves
+    for (int i = 0; i < nl; ++i) {
+        Worker& w = L.workers[i];
+        launch_dispatch_dest(L.tpe_all, W, E, w.rank, w.expert_ids, w.B_dev, nk, w.dest_rank, w.dest_row, st);
+    }
+    if (rbd) {
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            launch_rbd_offsets(L.G_all, L.tpe_all, W, E, w.rank, w.rbd, st);
+            launch_rbd_pack(x_of(i), static_cast<int>(row_bytes), w.rbd, nk, w.slot_pos, k, w.dest_row, w.cw,
+                            L.recv_u_tab, L.desc_tab, st);
+        }
+        if (dist) L.barrier(st);
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            launch_rbd_expand(w.recv_u, static_cast<int>(row_bytes), w.desc_recv, w.rbd.rx, L.R_max, w.recv,
+                              w.gstart, st);
+        }
+    } else if (tables) {
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            launch_scatter_rows(x_of(i), static_cast<int>(row_bytes), w.token_ids, w.B_dev, nk, w.dest_rank,
+                                w.dest_row, L.recv_tab, st);
+        }
+        if (dist) L.barrier(st);
+    } else {
+        Worker& w = L.workers[0];
+        launch_gather_rows(xb, S, static_cast<int>(row_bytes), w.token_ids, nk, w.B_dev, w.send, nullptr, st);
+        L.h_tpe.resize(static_cast<size_t>(W) * E);
+        XMOE_CUDA(cudaMemcpyAsync(L.h_tpe.data(), L.tpe_all, sizeof(int32_t) * W * E, cudaMemcpyDeviceToHost, st));
+        XMOE_CUDA(cudaStreamSynchronize(st));
+        L.exchange_nccl(/*forward=*/true, st);
+    }
+    L.mark(kEvDispatch, st);
+    // 5. expert FFNs over each owner's contiguous segments (pf_pipeline.cpp:83-105)
+    for (int i = 0; i < nl; ++i) {
+        Worker& w = L.workers[i];
+        launch_recv_counts(L.tpe_all, W, E, w.rank, w.rpe, st);
+        run_gemm(dt, w.recv, L.R_max, H, w.rpe, L.El, w1_of(L, w.rank), F, w.mid, 1, st);
+        run_gemm(dt, w.mid, L.R_max, F, w.rpe, L.El, w2_of(L, w.rank), H, w.eout, 0, st);
+    }
+    L.mark(kEvGemm, st);
+    if (L.Fs > 0) {
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            run_gemm(dt, x_of(i), S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, st);
+            run_gemm(dt, w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, w.sout, 0, st);
+        }
+    }
+    L.mark(kEvShared, st);
+    // 6. return path + weighted combine (pf_pipeline.cpp:107-135, rbd.cpp:287-358)
+    if (rbd) {
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            launch_rbd_merge(dt, w.eout, H, w.desc_recv, w.gstart, w.rbd.rx, static_cast<long long>(W) * S, w.back_u, st);
+        }
+        if (dist) L.barrier(st);
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            launch_rbd_combine(dt, L.back_tab, H, static_cast<int>(S), w.rbd, w.cw, L.Fs > 0 ? w.sout : nullptr,
+                               o_of(i), st);
+        }
+    } else if (tables) {
+        if (dist) L.barrier(st);
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            launch_combine(dt, nullptr, H, nullptr, w.slot_pos, k, w.cw, static_cast<int>(S),
+                           L.Fs > 0 ? w.sout : nullptr, o_of(i), st, L.eout_tab, w.dest_rank, w.dest_row);
+        }
+    } else {
+        L.exchange_nccl(/*forward=*/false, st);
+        Worker& w = L.workers[0];
+        launch_combine(dt, w.back, H, nullptr, w.slot_pos, k, w.cw, static_cast<int>(S),
+                       L.Fs > 0 ? w.sout : nullptr, ob, st);
+    }
+    L.mark(kEvCombine, st);
+    L.last_S = S;
+}
+
+// NCCL alltoallv of rows (the library-collective baseline), chunked per
+// (peer, local expert) so arrivals land directly in the (local expert,
+// source, position) layout.  Forward: send -> recv; reverse (transposed
+// counts): eout -> back.
+void Layer::exchange_nccl(bool forward, cudaStream_t st) {
+    Worker& w = workers[0];
+    const int me = w.rank;
+    auto tpe = [&](int s, int e) { return h_tpe[static_cast<size_t>(s) * E + e]; };
+    const size_t rb = static_cast<size_t>(H) * es;
+    auto comm = static_cast<ncclComm_t>(ctx->nccl);
+    const ncclDataType_t ty = d.dtype == XMOE_F64 ? ncclFloat64 : ncclBfloat16;
+    std::vector<long long> blk(E + 1, 0);
+    for (int e = 0; e < E; ++e) blk[e + 1] = blk[e] + tpe(me, e);
+    std::vector<long long> ebase(El + 1, 0);
+    for (int le = 0; le < El; ++le) {
+        long long a = 0;
+        for (int s = 0; s < W; ++s) a += tpe(s, me * El + le);
+        ebase[le + 1] = ebase[le] + a;
+    }
+    XMOE_NCCL(ncclGroupStart());
+    for (int peer = 0; peer < W; ++peer) {
+        for (int le = 0; le < El; ++le) {
+            const int e = peer * El + le;
+            const long long n = tpe(me, e);
+            if (n == 0) continue;
+            if (forward) XMOE_NCCL(ncclSend(static_cast<char*>(w.send) + blk[e] * rb, n * H, ty, peer, comm, st));
+            else XMOE_NCCL(ncclRecv(static_cast<char*>(w.back) + blk[e] * rb, n * H, ty, peer, comm, st));
+        }
+        for (int le = 0; le < El; ++le) {
+            const int e = me * El + le;
+            const long long n = tpe(peer, e);
+            if (n == 0) continue;
+            long long before = 0;
+            for (int s = 0; s < peer; ++s) before += tpe(s, e);
+            char* p = static_cast<char*>(forward ? w.recv : w.eout) + (ebase[le] + before) * rb;
+            if (forward) XMOE_NCCL(ncclRecv(p, n * H, ty, peer, comm, st));
+            else XMOE_NCCL(ncclSend(p, n * H, ty, peer, comm, st));
+        }
+    }
+    XMOE_NCCL(ncclGroupEnd());
+}
+
+// ---------------------------------------------------------------- SSMB
+// moesim::ssmb_forward (ssmb.cpp:12-46): contiguous shards, the last one
+// takes the remainder; every rank routes its shard over the full (replicated)
+// expert set; then the shards are all-gathered.  With one process per GPU
+// the all-gather is a group of NCCL broadcasts (shards may differ in size).
+void ssmb_forward(Ctx& ctx, Layer& L, const void* x_full, long long S, void* out_full, cudaStream_t st) {
+    const int G = ctx.world;
+    require(L.ssmb, XMOE_ERR_VALIDATION, "ssmb_forward: layer was not created for sequence sharding");
+    require(G >= 1, XMOE_ERR_VALIDATION, "ssmb_forward: shard count must be >= 1");
+    require(G <= S, XMOE_ERR_VALIDATION, "ssmb_forward: more shards than sequence rows");
+    const long long base = S / G;
+    const size_t rb = static_cast<size_t>(L.H) * L.es;
+    auto rows_of = [&](int g) { return g == G - 1 ? S - static_cast<long long>(g) * base : base; };
+    const char* xb = static_cast<const char*>(x_full);
+    char* ob = static_cast<char*>(out_full);
+    if (ctx.rank < 0 || G == 1) {
+        for (int g = 0; g < G; ++g)
+            layer_forward(L, xb + g * base * rb, rows_of(g), ob + g * base * rb, st);
+        return;
+    }
+    const int me = ctx.rank;
+    layer_forward(L, xb + me * base * rb, rows_of(me), ob + me * base * rb, st);
+    auto comm = static_cast<ncclComm_t>(ctx.nccl);
+    XMOE_NCCL(ncclGroupStart());
+    for (int g = 0; g < G; ++g) {
+        char* p = ob + g * base * rb;
+        XMOE_NCCL(ncclBroadcast(p, p, rows_of(g) * rb, ncclUint8, g, comm, st));
+    }
+    XMOE_NCCL(ncclGroupEnd());
+}
+
+}  // namespace xmoe

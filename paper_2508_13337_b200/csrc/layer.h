@@ -52,16 +52,13 @@ struct Worker {
     void* smid = nullptr;         // shared experts [S, Fs]
     void* sout = nullptr;         // [S, H]
     int32_t* s_rows = nullptr;
+    char* sym = nullptr;          // symmetric region: recv | eout | recv_u | desc_recv | back_u
     // redundancy-bypassing dispatch (rbd.cu)
     RbdWork rbd{};
-    void* send_u = nullptr;       // [S*min(k,W), H] one row per (token, dest) group, dest-sorted
-    RbdDesc* desc_send = nullptr; // [S*k] one descriptor per copy
     void* recv_u = nullptr;       // [W*S, H] unique rows received from every source
     RbdDesc* desc_recv = nullptr; // [R_max]
     int32_t* gstart = nullptr;    // [W*S] first descriptor of each received group
-    void* back_u = nullptr;       // [W*S, H] merged group outputs to return
-    void* ret_u = nullptr;        // [S*min(k,W), H] merged outputs returned to this source
-    int32_t* ru_base = nullptr;   // [W] my groups' first row in each receiver's recv_u
+    void* back_u = nullptr;       // [W*S, H] merged group outputs, read by the sources
 };
 
 enum { kEvStart = 0, kEvGate, kEvPft, kEvDispatch, kEvGemm, kEvShared, kEvCombine, kNumEvents };
@@ -70,6 +67,12 @@ struct Layer {
     Ctx* ctx = nullptr;
     xmoe_layer_desc d{};
     int W = 1, E = 0, H = 0, F = 0, k = 0, El = 0, E_held = 0, Fs = 0;
+    int nl = 1;                // ranks driven by this process
+    bool ssmb = false;         // sequence-sharded block: experts replicated, MoE local
+    bool distributed = false;  // one process per GPU, world > 1
+    bool p2p = false;          // NVLink peer tables (else NCCL send/recv baseline)
+    int32_t* bar = nullptr;    // 4-byte all-reduce used as a cross-rank barrier
+    std::vector<void*> peer_maps;
     size_t es = 2;
     long long R_max = 0, S_max = 0, last_S = 0;
     void* gate = nullptr;  // F64 [H,E]; BF16 [E,H]
@@ -80,6 +83,9 @@ struct Layer {
     int32_t* tpe_all = nullptr;  // [W, E]
     char** recv_tab = nullptr;   // device table: rank -> recv buffer (shared-device ranks)
     char** eout_tab = nullptr;
+    char** recv_u_tab = nullptr;  // RBD tables (local or NVLink peer addresses)
+    RbdDesc** desc_tab = nullptr;
+    char** back_tab = nullptr;
     std::vector<int32_t> h_tpe;
     uint64_t* jumps = nullptr;   // RBD jump-ahead matrices (device)
     int32_t* G_all = nullptr;    // [W, W] groups source -> dest (device)
@@ -92,11 +98,15 @@ struct Layer {
     void* alloc(size_t bytes);
     void mark(int ev, cudaStream_t st);
     void exchange_nccl(bool forward, cudaStream_t st);
-    void rbd_exchange(bool forward, cudaStream_t st);
-    long long C(int s, int d) const;  // copies source s -> dest d
-    long long Gsd(int s, int d) const { return h_G[static_cast<size_t>(s) * W + d]; }
+    void barrier(cudaStream_t st);
+    long long C(int s, int d) const;  // copies source s -> dest d (needs h_tpe)
     void ledger(uint64_t* out, int n);
     ~Layer();
 };
+
+void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const void* w1,
+                  const void* w2, const void* sw1, const void* sw2, Layer& L);
+void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t st);
+void ssmb_forward(Ctx& ctx, Layer& L, const void* x_full, long long S, void* out_full, cudaStream_t st);
 
 }  // namespace xmoe

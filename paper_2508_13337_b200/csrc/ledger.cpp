@@ -51,7 +51,9 @@ void Layer::ledger(uint64_t* out, int n) {
             }
         }
     }
-    if (d.dispatch_mode == XMOE_DISPATCH_RBD && h_G.size() == static_cast<size_t>(W) * W) {
+    if (d.dispatch_mode == XMOE_DISPATCH_RBD) {
+        h_G.resize(static_cast<size_t>(W) * W);
+        XMOE_CUDA(cudaMemcpy(h_G.data(), G_all, sizeof(int32_t) * h_G.size(), cudaMemcpyDeviceToHost));
         // bypass: one row per (token, destination) group each way, plus the
         // 24-byte copy descriptors (rbd.h RbdDesc)
         v[0] = v[1] = v[2] = v[3] = v[4] = 0;

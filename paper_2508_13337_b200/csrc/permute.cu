@@ -126,6 +126,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) scatter_rows_kernel(
         char* dst = dest_bufs[dest_rank[r]] + static_cast<size_t>(dest_row[r]) * row_bytes;
         warp_copy_row(x + static_cast<size_t>(t) * row_bytes, dst, row_bytes, lane);
     }
+    __threadfence_system();  // peer (NVLink) stores complete before the rank barrier
 }
 
 // Reverse of the placement: expert outputs come back from the owners'

@@ -251,13 +251,56 @@ __global__ void rbd_group_pos_kernel(const int32_t* __restrict__ perm, const int
     nsorted[pos] = g.n[gid];
 }
 
-// Sender pack: unique rows (dest-sorted) and one descriptor per copy.
+// Per-source offsets for the table transport, all on the device (no host
+// sync): for every destination d,
+//   ru_base[d]  first row of my groups in d's unique-row buffer
+//               (groups of sources < me come first)
+//   rd_base[d]  first slot of my descriptors in d's descriptor buffer
+//   cseg[d]     first descriptor of my dest-d segment in my own order
+// and, for me as a receiver, the totals I will receive (rx[0] groups,
+// rx[1] descriptors).
+__global__ void rbd_offsets_kernel(const int32_t* __restrict__ G_all, const int32_t* __restrict__ tpe_all,
+                                   int W, int E, int me, const int32_t* __restrict__ dptr,
+                                   const int32_t* __restrict__ coff, int32_t* __restrict__ ru_base,
+                                   int32_t* __restrict__ rd_base, int32_t* __restrict__ cseg,
+                                   int32_t* __restrict__ rx) {
+    const int El = E / W;
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    auto C = [&](int s, int d) {
+        int a = 0;
+        for (int le = 0; le < El; ++le) a += tpe_all[s * E + d * El + le];
+        return a;
+    };
+    for (int d = 0; d < W; ++d) {
+        int g = 0, c = 0;
+        for (int s = 0; s < me; ++s) {
+            g += G_all[s * W + d];
+            c += C(s, d);
+        }
+        ru_base[d] = g;
+        rd_base[d] = c;
+        cseg[d] = dptr[d] < dptr[W] ? coff[dptr[d]] : 0;
+    }
+    int g = 0, c = 0;
+    for (int s = 0; s < W; ++s) {
+        g += G_all[s * W + me];
+        c += C(s, me);
+    }
+    rx[0] = g;
+    rx[1] = c;
+}
+
+// Sender pack: each group's row goes once, straight into the destination's
+// unique-row buffer, with one descriptor per copy (tables hold local or
+// NVLink-mapped peer pointers).
 __global__ void __launch_bounds__(256) rbd_pack_kernel(
     const char* __restrict__ x, int row_bytes, const int32_t* __restrict__ perm,
     const int32_t* __restrict__ G_dev, const RbdGroups g, const int32_t* __restrict__ dptr,
     const int32_t* __restrict__ coff, const int32_t* __restrict__ ru_base,
+    const int32_t* __restrict__ rd_base, const int32_t* __restrict__ cseg,
     const int32_t* __restrict__ slot_pos, int k, const int32_t* __restrict__ dest_row,
-    const double* __restrict__ cw, char* __restrict__ send_u, RbdDesc* __restrict__ desc) {
+    const double* __restrict__ cw, char* const* __restrict__ recv_u_tab,
+    RbdDesc* const* __restrict__ desc_tab) {
     const int G = *G_dev;
     const int lane = threadIdx.x & 31;
     const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -266,35 +309,38 @@ __global__ void __launch_bounds__(256) rbd_pack_kernel(
         const int gid = perm[pos];
         const int t = g.token[gid], d = g.dest[gid], n = g.n[gid], j0 = g.first_slot[gid];
         const int pilot = g.pilot[gid];
+        const int u = ru_base[d] + static_cast<int>(pos - dptr[d]);
         if (lane < n) {
             const int p = slot_pos[static_cast<size_t>(t) * k + j0 + lane];
             RbdDesc dd;
-            dd.u = ru_base[d] + static_cast<int>(pos - dptr[d]);
+            dd.u = u;
             dd.dest_row = dest_row[p];
             dd.w = cw[p];
             dd.n = n;
             dd.member = lane | (p == pilot ? kRbdPilotFlag : 0);
-            desc[coff[pos] + lane] = dd;
+            desc_tab[d][rd_base[d] + (coff[pos] - cseg[d]) + lane] = dd;
         }
-        // row copy, 16-byte vectors
-        const int4* s4 = reinterpret_cast<const int4*>(x + static_cast<size_t>(t) * row_bytes);
-        int4* d4 = reinterpret_cast<int4*>(send_u + static_cast<size_t>(pos) * row_bytes);
+        const char* src = x + static_cast<size_t>(t) * row_bytes;
+        char* dst = recv_u_tab[d] + static_cast<size_t>(u) * row_bytes;
         if ((row_bytes & 15) == 0) {
+            const int4* s4 = reinterpret_cast<const int4*>(src);
+            int4* d4 = reinterpret_cast<int4*>(dst);
             for (int v = lane; v < (row_bytes >> 4); v += 32) st_na_v4(d4 + v, ld_nc_v4(s4 + v));
         } else {
-            const long long* s8 = reinterpret_cast<const long long*>(x + static_cast<size_t>(t) * row_bytes);
-            long long* d8 = reinterpret_cast<long long*>(send_u + static_cast<size_t>(pos) * row_bytes);
-            for (int v = lane; v < (row_bytes >> 3); v += 32) d8[v] = s8[v];
+            for (int v = lane; v < (row_bytes >> 3); v += 32)
+                reinterpret_cast<long long*>(dst)[v] = reinterpret_cast<const long long*>(src)[v];
         }
     }
+    __threadfence_system();
 }
 
 // Receiver expand: grouped[dest_row] = recv_u[u] for every received copy;
 // also records each group's first descriptor for the merge.
 __global__ void __launch_bounds__(256) rbd_expand_kernel(const char* __restrict__ recv_u,
                                                          int row_bytes, const RbdDesc* __restrict__ desc,
-                                                         int ndesc, char* __restrict__ grouped,
+                                                         const int32_t* __restrict__ rx, char* __restrict__ grouped,
                                                          int32_t* __restrict__ gstart) {
+    const int ndesc = rx[1];
     const int lane = threadIdx.x & 31;
     const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
@@ -317,8 +363,10 @@ __global__ void __launch_bounds__(256) rbd_expand_kernel(const char* __restrict_
 template <typename T>
 __global__ void __launch_bounds__(256) rbd_merge_kernel(const T* __restrict__ eout, int H,
                                                         const RbdDesc* __restrict__ desc,
-                                                        const int32_t* __restrict__ gstart, int ngroups,
+                                                        const int32_t* __restrict__ gstart,
+                                                        const int32_t* __restrict__ rx,
                                                         T* __restrict__ back_u) {
+    const int ngroups = rx[0];
     const int lane = threadIdx.x & 31;
     const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
@@ -334,9 +382,9 @@ __global__ void __launch_bounds__(256) rbd_merge_kernel(const T* __restrict__ eo
         int pm = 0;
         for (int m = 0; m < n; ++m)
             if (desc[c0 + m].member & kRbdPilotFlag) pm = m;
+        const RbdDesc pd = desc[c0 + pm];
         for (int h = lane; h < H; h += 32) {
             if constexpr (sizeof(T) == 8) {
-                const RbdDesc pd = desc[c0 + pm];
                 double acc = __dmul_rn(static_cast<double>(eout[static_cast<size_t>(pd.dest_row) * H + h]), pd.w);
                 for (int m = 0; m < n; ++m) {
                     if (m == pm) continue;
@@ -345,7 +393,6 @@ __global__ void __launch_bounds__(256) rbd_merge_kernel(const T* __restrict__ eo
                 }
                 out[h] = static_cast<T>(acc);
             } else {
-                const RbdDesc pd = desc[c0 + pm];
                 float acc = __bfloat162float(eout[static_cast<size_t>(pd.dest_row) * H + h]) * static_cast<float>(pd.w);
                 for (int m = 0; m < n; ++m) {
                     if (m == pm) continue;
@@ -358,18 +405,21 @@ __global__ void __launch_bounds__(256) rbd_merge_kernel(const T* __restrict__ eo
     }
 }
 
-// Source combine (rbd.cpp:343-356): per token, its groups in pilot order.
+// Source combine (rbd.cpp:343-356): per token, its groups in pilot order;
+// each merged row is read straight from its landing rank's back_u.
 template <typename T>
-__global__ void __launch_bounds__(256) rbd_combine_kernel(const T* __restrict__ ret_u, int H, int S,
-                                                          const int32_t* __restrict__ gbase,
+__global__ void __launch_bounds__(256) rbd_combine_kernel(const char* const* __restrict__ back_tab, int H,
+                                                          int S, const int32_t* __restrict__ gbase,
                                                           const int32_t* __restrict__ gcount,
-                                                          const RbdGroups g, const double* __restrict__ cw,
+                                                          const RbdGroups g, const int32_t* __restrict__ ru_base,
+                                                          const int32_t* __restrict__ dptr,
+                                                          const double* __restrict__ cw,
                                                           const T* __restrict__ addend, T* __restrict__ out) {
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (t >= S) return;
     const int b = gbase[t], n = gcount[t];
-    // groups of a token are few (<= k): order them by pilot packed row
+    // groups of a token are few (<= min(k, W)): order them by pilot packed row
     int order[32];
     const int nn = n < 32 ? n : 32;
     for (int i = 0; i < nn; ++i) {
@@ -381,13 +431,20 @@ __global__ void __launch_bounds__(256) rbd_combine_kernel(const T* __restrict__ 
         }
         order[q] = i;
     }
+    const T* rowp[32];
+    for (int i = 0; i < nn; ++i) {
+        const int gid = b + order[i];
+        const int d = g.dest[gid];
+        rowp[i] = reinterpret_cast<const T*>(back_tab[d]) +
+                  static_cast<size_t>(ru_base[d] + g.pos[gid] - dptr[d]) * H;
+    }
     for (int h = lane; h < H; h += 32) {
         if constexpr (sizeof(T) == 8) {
             double acc = 0.0;
             for (int i = 0; i < nn; ++i) {
                 const int gid = b + order[i];
                 const double sc = g.n[gid] > 1 ? 1.0 : cw[g.pilot[gid]];
-                acc = __dadd_rn(acc, __dmul_rn(sc, static_cast<double>(ret_u[static_cast<size_t>(g.pos[gid]) * H + h])));
+                acc = __dadd_rn(acc, __dmul_rn(sc, static_cast<double>(rowp[i][h])));
             }
             if (addend) acc = __dadd_rn(acc, static_cast<double>(addend[static_cast<size_t>(t) * H + h]));
             out[static_cast<size_t>(t) * H + h] = static_cast<T>(acc);
@@ -396,7 +453,7 @@ __global__ void __launch_bounds__(256) rbd_combine_kernel(const T* __restrict__ 
             for (int i = 0; i < nn; ++i) {
                 const int gid = b + order[i];
                 const float sc = g.n[gid] > 1 ? 1.f : static_cast<float>(cw[g.pilot[gid]]);
-                acc = fmaf(sc, __bfloat162float(ret_u[static_cast<size_t>(g.pos[gid]) * H + h]), acc);
+                acc = fmaf(sc, __bfloat162float(rowp[i][h]), acc);
             }
             if (addend) acc += __bfloat162float(addend[static_cast<size_t>(t) * H + h]);
             out[static_cast<size_t>(t) * H + h] = __float2bfloat16_rn(acc);
@@ -440,46 +497,51 @@ void launch_rbd_sort(int W, long long max_groups, RbdWork& wk, cudaStream_t st) 
     XMOE_LAUNCH_CHECK();
 }
 
-void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, long long max_groups,
-                     const int32_t* ru_base, const int32_t* slot_pos, int k, const int32_t* dest_row,
-                     const double* cw, void* send_u, RbdDesc* desc, cudaStream_t st) {
-    rbd_pack_kernel<<<warp_grid(max_groups), 256, 0, st>>>(
-        static_cast<const char*>(x), row_bytes, wk.perm, wk.G_dev, wk.g, wk.dptr, wk.coff, ru_base,
-        slot_pos, k, dest_row, cw, static_cast<char*>(send_u), desc);
+void launch_rbd_offsets(const int32_t* G_all, const int32_t* tpe_all, int W, int E, int me, RbdWork& wk,
+                        cudaStream_t st) {
+    rbd_offsets_kernel<<<1, 32, 0, st>>>(G_all, tpe_all, W, E, me, wk.dptr, wk.coff, wk.ru_base,
+                                         wk.rd_base, wk.cseg, wk.rx);
     XMOE_LAUNCH_CHECK();
 }
 
-void launch_rbd_expand(const void* recv_u, int row_bytes, const RbdDesc* desc, int ndesc,
-                       void* grouped, int32_t* gstart, cudaStream_t st) {
-    if (ndesc == 0) return;
-    rbd_expand_kernel<<<warp_grid(ndesc), 256, 0, st>>>(static_cast<const char*>(recv_u), row_bytes,
-                                                        desc, ndesc, static_cast<char*>(grouped), gstart);
+void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, long long max_groups,
+                     const int32_t* slot_pos, int k, const int32_t* dest_row, const double* cw,
+                     char* const* recv_u_tab, RbdDesc* const* desc_tab, cudaStream_t st) {
+    rbd_pack_kernel<<<warp_grid(max_groups), 256, 0, st>>>(
+        static_cast<const char*>(x), row_bytes, wk.perm, wk.G_dev, wk.g, wk.dptr, wk.coff, wk.ru_base,
+        wk.rd_base, wk.cseg, slot_pos, k, dest_row, cw, recv_u_tab, desc_tab);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_rbd_expand(const void* recv_u, int row_bytes, const RbdDesc* desc, const int32_t* rx,
+                       long long max_desc, void* grouped, int32_t* gstart, cudaStream_t st) {
+    rbd_expand_kernel<<<warp_grid(max_desc), 256, 0, st>>>(static_cast<const char*>(recv_u), row_bytes,
+                                                           desc, rx, static_cast<char*>(grouped), gstart);
     XMOE_LAUNCH_CHECK();
 }
 
 void launch_rbd_merge(int dtype, const void* eout, int H, const RbdDesc* desc, const int32_t* gstart,
-                      int ngroups, void* back_u, cudaStream_t st) {
-    if (ngroups == 0) return;
+                      const int32_t* rx, long long max_groups, void* back_u, cudaStream_t st) {
     if (dtype == XMOE_F64)
-        rbd_merge_kernel<double><<<warp_grid(ngroups), 256, 0, st>>>(
-            static_cast<const double*>(eout), H, desc, gstart, ngroups, static_cast<double*>(back_u));
+        rbd_merge_kernel<double><<<warp_grid(max_groups), 256, 0, st>>>(
+            static_cast<const double*>(eout), H, desc, gstart, rx, static_cast<double*>(back_u));
     else
-        rbd_merge_kernel<__nv_bfloat16><<<warp_grid(ngroups), 256, 0, st>>>(
-            static_cast<const __nv_bfloat16*>(eout), H, desc, gstart, ngroups,
+        rbd_merge_kernel<__nv_bfloat16><<<warp_grid(max_groups), 256, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(eout), H, desc, gstart, rx,
             static_cast<__nv_bfloat16*>(back_u));
     XMOE_LAUNCH_CHECK();
 }
 
-void launch_rbd_combine(int dtype, const void* ret_u, int H, int S, const RbdWork& wk, const double* cw,
-                        const void* addend, void* out, cudaStream_t st) {
+void launch_rbd_combine(int dtype, const char* const* back_tab, int H, int S, const RbdWork& wk,
+                        const double* cw, const void* addend, void* out, cudaStream_t st) {
     if (S == 0) return;
     if (dtype == XMOE_F64)
         rbd_combine_kernel<double><<<ceil_div(S, 8), 256, 0, st>>>(
-            static_cast<const double*>(ret_u), H, S, wk.gbase, wk.gcount, wk.g, cw,
+            back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru_base, wk.dptr, cw,
             static_cast<const double*>(addend), static_cast<double*>(out));
     else
         rbd_combine_kernel<__nv_bfloat16><<<ceil_div(S, 8), 256, 0, st>>>(
-            static_cast<const __nv_bfloat16*>(ret_u), H, S, wk.gbase, wk.gcount, wk.g, cw,
+            back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru_base, wk.dptr, cw,
             static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out));
     XMOE_LAUNCH_CHECK();
 }

@@ -45,6 +45,10 @@ struct RbdWork {
     int32_t* nsorted;  // [S*k] group size in sorted order
     int32_t* coff;     // [S*k] first descriptor of each sorted group
     void* csr_ws;
+    int32_t* ru_base;  // [W] my first row in each receiver's unique-row buffer
+    int32_t* rd_base;  // [W] my first descriptor slot at each receiver
+    int32_t* cseg;     // [W] first descriptor of my dest-d segment
+    int32_t* rx;       // [2] groups / descriptors I receive
     uint64_t state[4];  // Rng(salt_seed(seed, rank, 0)) state
 };
 
@@ -55,14 +59,16 @@ void rbd_jump_tables(std::vector<uint64_t>& out);
 void launch_rbd_groups(const int32_t* slot_pos, const int32_t* expert_ids, int S, int k, int El,
                        const uint64_t state[4], const uint64_t* jumps, RbdWork& wk, cudaStream_t st);
 void launch_rbd_sort(int W, long long max_groups, RbdWork& wk, cudaStream_t st);
+void launch_rbd_offsets(const int32_t* G_all, const int32_t* tpe_all, int W, int E, int me, RbdWork& wk,
+                        cudaStream_t st);
 void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, long long max_groups,
-                     const int32_t* ru_base, const int32_t* slot_pos, int k, const int32_t* dest_row,
-                     const double* cw, void* send_u, RbdDesc* desc, cudaStream_t st);
-void launch_rbd_expand(const void* recv_u, int row_bytes, const RbdDesc* desc, int ndesc,
-                       void* grouped, int32_t* gstart, cudaStream_t st);
+                     const int32_t* slot_pos, int k, const int32_t* dest_row, const double* cw,
+                     char* const* recv_u_tab, RbdDesc* const* desc_tab, cudaStream_t st);
+void launch_rbd_expand(const void* recv_u, int row_bytes, const RbdDesc* desc, const int32_t* rx,
+                       long long max_desc, void* grouped, int32_t* gstart, cudaStream_t st);
 void launch_rbd_merge(int dtype, const void* eout, int H, const RbdDesc* desc, const int32_t* gstart,
-                      int ngroups, void* back_u, cudaStream_t st);
-void launch_rbd_combine(int dtype, const void* ret_u, int H, int S, const RbdWork& wk,
+                      const int32_t* rx, long long max_groups, void* back_u, cudaStream_t st);
+void launch_rbd_combine(int dtype, const char* const* back_tab, int H, int S, const RbdWork& wk,
                         const double* cw, const void* addend, void* out, cudaStream_t st);
 
 // pft.cu: stable CSR with the item count on the device (bound n_max).

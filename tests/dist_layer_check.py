@@ -1,0 +1,123 @@
+"""Multi-process expert-parallel parity check (one process per GPU, NCCL).
+
+Run with:  torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/dist_layer_check.py
+Every rank builds the same seeded instance, keeps its E/N experts and its
+token slice, runs the layer through the C-ABI over NCCL, and rank 0 compares
+all ranks' outputs with the oracle: F64 bit-exact given the device softmax
+weights, BF16 within the test_gpu_layer tolerances.  Exit code 0 = pass."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import moe_oracle as O  # noqa: E402
+from paper_2508_13337_b200 import capi  # noqa: E402
+from tests.gpu_util import bf16_round, grid_gate, grid_tokens, max_rel_diff, norm_rel  # noqa: E402
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    obj = [capi.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ctx = capi.Context(local, world, rank, obj[0])
+    failures = []
+    cases = [(capi.F64, capi.NAIVE, 97, 8, 3, 24, 16), (capi.F64, capi.RBD, 97, 8, 3, 24, 16),
+             (capi.BF16, capi.NAIVE, 512, 16, 6, 256, 128), (capi.BF16, capi.RBD, 512, 16, 6, 256, 128)]
+    for ci, (dt, mode, S, e_per, k, H, F) in enumerate(cases):
+        E = e_per * world
+        el = E // world
+        rng = np.random.default_rng(100 + ci)
+        if dt == capi.F64:
+            gate = rng.uniform(-0.1, 0.1, (H, E))
+            w1 = rng.uniform(-0.1, 0.1, (E, H, F))
+            w2 = rng.uniform(-0.1, 0.1, (E, F, H))
+            x = rng.uniform(-1, 1, (world, S, H))
+            tdt = torch.float64
+        else:
+            gate = grid_gate(rng, H, E)
+            w1 = bf16_round(rng.uniform(-0.1, 0.1, (E, H, F)))
+            w2 = bf16_round(rng.uniform(-0.1, 0.1, (E, F, H)))
+            x = grid_tokens(rng, world, S, H)
+            tdt = torch.bfloat16
+        cap = S * k if ci % 2 == 0 else int(np.ceil(1.5 * S * k / E))
+        seed = 4242 + ci
+        dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(tdt).cuda()  # noqa: E731
+        layer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=cap,
+                           max_tokens=S, dtype=dt, gate=dv(gate), w1=dv(w1[rank * el:(rank + 1) * el]),
+                           w2=dv(w2[rank * el:(rank + 1) * el]), dispatch_mode=mode, seed=seed)
+        out = layer.forward(dv(x[rank])).to(torch.float64).cpu().numpy()
+        led = layer.ledger()
+        gate_dev = None
+        if dt == capi.F64:
+            top, wt = ctx.gate_forward(dv(x[rank]), dv(gate), k)
+            gate_dev = (top.cpu().numpy(), wt.cpu().numpy())
+        got = [None] * world
+        dist.all_gather_object(got, (out, gate_dev, led))
+        if rank == 0:
+            W = O.LayerWeights(gate, w1, w2)
+            gates = [g[1] for g in got] if dt == capi.F64 else None
+            exact = dt == capi.F64
+            if mode == capi.NAIVE:
+                want = O.pf_moe_forward(list(x), W, E, k, cap, gates=gates, exact=exact)
+            else:
+                want = O.rbd_moe_forward(list(x), W, E, k, cap, seed, gates=gates, exact=exact)
+            for r in range(world):
+                o = got[r][0]
+                if dt == capi.F64:
+                    ok = np.array_equal(o, want[r])
+                    err = max_rel_diff(o, want[r])
+                else:
+                    err = norm_rel(o, want[r])
+                    ok = err < 1e-2 and max_rel_diff(o, want[r]) < 2e-2
+                if not ok:
+                    failures.append((ci, r, err))
+            tot = {kk: sum(g[2][kk] for g in got) for kk in got[0][2]}
+            print(f"case {ci} dtype={'f64' if dt == capi.F64 else 'bf16'} mode={'rbd' if mode else 'naive'} "
+                  f"cap={cap} ledger={tot}", flush=True)
+        del layer
+        dist.barrier()
+    # sequence-sharded block across the ranks (ssmb.cpp:12-46)
+    S, E, k, H, F = 101, 8, 2, 16, 8
+    rng = np.random.default_rng(77)
+    gate = rng.uniform(-0.1, 0.1, (H, E))
+    w1 = rng.uniform(-0.1, 0.1, (E, H, F))
+    w2 = rng.uniform(-0.1, 0.1, (E, F, H))
+    x = rng.uniform(-1, 1, (S, H))
+    bounds = O.ssmb_shards(S, world)
+    dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    layer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
+                       max_tokens=max(n for _, n in bounds), dtype=capi.F64, gate=dv(gate), w1=dv(w1),
+                       w2=dv(w2), ssmb=True)
+    out = layer.ssmb_forward(dv(x)).cpu().numpy()
+    b, n = bounds[rank]
+    top, wt = ctx.gate_forward(dv(x[b:b + n]), dv(gate), k)
+    got = [None] * world
+    dist.all_gather_object(got, (out, (top.cpu().numpy(), wt.cpu().numpy())))
+    if rank == 0:
+        Wt = O.LayerWeights(gate, w1, w2)
+        want = np.concatenate([O.pf_moe_forward([x[bb:bb + nn]], Wt, E, k, S * k, gates=[got[g][1]])[0]
+                               for g, (bb, nn) in enumerate(bounds)])
+        for r in range(world):
+            if not np.array_equal(got[r][0], want):
+                failures.append(("ssmb", r, max_rel_diff(got[r][0], want)))
+        print("ssmb checked on", world, "ranks", flush=True)
+    del layer
+    if rank == 0:
+        print("FAILURES", failures, flush=True)
+    ok = torch.tensor([0 if not failures else 1])
+    dist.broadcast(ok, 0)
+    dist.destroy_process_group()
+    sys.exit(int(ok.item()))
+
+
+if __name__ == "__main__":
+    main()

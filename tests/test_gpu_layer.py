@@ -181,3 +181,33 @@ def test_rbd_forward_bf16_vs_oracle(W, S, E, k, H, F):
         assert max_rel_diff(got[i], want[i]) < 2e-2, max_rel_diff(got[i], want[i])
     led = L.ledger()
     assert led["dispatch_rows_offrank"] < led["copies_offrank"] * H * 2  # bytes actually saved
+
+
+@pytest.mark.parametrize("G,S", [(1, 9), (2, 37), (4, 61), (8, 64)])
+def test_ssmb_forward_f64(G, S):
+    """ssmb_forward (ssmb.cpp:12-46): contiguous shards, last takes the
+    remainder, replicated experts, capacity per shard; all-gathered."""
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, G, -1)
+    rng = O.Rng(11 + G)
+    E = 4 + rng.below(5)
+    k = 1 + rng.below(3)
+    H = 3 + rng.below(4)
+    F = 2 + rng.below(5)
+    w = O.make_layer_weights(rng, E, H, F)
+    x = np.array([rng.uniform(-1.0, 1.0) for _ in range(S * H)]).reshape(S, H)
+    for cap in (S * k, 2):
+        bounds = O.ssmb_shards(S, G)
+        biggest = max(n for _, n in bounds)
+        L = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=cap,
+                       max_tokens=biggest, dtype=capi.F64, gate=dev(w.gate), w1=dev(w.w1), w2=dev(w.w2),
+                       ssmb=True)
+        got = host(L.ssmb_forward(dev(x)))
+        exact = np.concatenate([
+            O.pf_moe_forward([x[b:b + n]], w, E, k, cap, gates=_device_gates(ctx, x[None, b:b + n], w, k))[0]
+            for b, n in bounds])
+        assert np.array_equal(got, exact)
+        pure = O.ssmb_forward(x, G, w, E, k, cap)
+        assert max_rel_diff(got, pure) < 1e-14
+        if cap == S * k:  # test_ssmb.cpp:61-77: no drops => equals the unsharded layer
+            assert max_rel_diff(got, O.pf_moe_forward([x], w, E, k, S * k)[0]) < 1e-14
