@@ -461,6 +461,157 @@ __global__ void __launch_bounds__(256) rbd_combine_kernel(const char* const* __r
     }
 }
 
+// BF16 merge, vectorised: one warp per (received group, 512-column segment);
+// lane m < n holds member m's row and weight, the pilot is applied first,
+// every row moves 16 bytes per lane, fp32 math.
+__global__ void __launch_bounds__(256) rbd_merge_bf16_kernel(const __nv_bfloat16* __restrict__ eout, int H,
+                                                             const RbdDesc* __restrict__ desc,
+                                                             const int32_t* __restrict__ gstart,
+                                                             const int32_t* __restrict__ rx,
+                                                             __nv_bfloat16* __restrict__ back_u) {
+    const int ngroups = rx[0];
+    const int nseg = (H + 511) / 512;
+    const int lane = threadIdx.x & 31;
+    const int nchunk = H >> 3;
+    const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    for (long long item = warp; item < static_cast<long long>(ngroups) * nseg; item += nwarps) {
+        const int u = static_cast<int>(item / nseg), seg = static_cast<int>(item % nseg);
+        const int c0 = gstart[u];
+        const int n = desc[c0].n;
+        int my_row = 0;
+        float my_w = 0.f;
+        int is_p = 0;
+        if (lane < n) {
+            const RbdDesc md = desc[c0 + lane];
+            my_row = md.dest_row;
+            my_w = static_cast<float>(md.w);
+            is_p = (md.member & kRbdPilotFlag) ? 1 : 0;
+        }
+        const unsigned pm = __ballot_sync(0xffffffffu, is_p);
+        const int pl = pm ? __ffs(pm) - 1 : 0;
+        const int cbeg = seg * 64, cend = min(nchunk, cbeg + 64);
+        int4* dst = reinterpret_cast<int4*>(back_u + static_cast<size_t>(u) * H);
+        for (int cc = cbeg; cc < cend; cc += 32) {
+            const int c = cc + lane;
+            const bool ok = c < cend;
+            float acc[8];
+            {
+                const int r = __shfl_sync(0xffffffffu, my_row, pl);
+                const float wp = n == 1 ? 1.f : __shfl_sync(0xffffffffu, my_w, pl);
+                const int4 v = ok ? ld_nc_v4(reinterpret_cast<const int4*>(eout + static_cast<size_t>(r) * H) + c)
+                                  : make_int4(0, 0, 0, 0);
+                if (n == 1) {  // singleton: raw row (rbd.cpp:323-325)
+                    if (ok) dst[c] = v;
+                    continue;
+                }
+                const uint32_t q[4] = {static_cast<uint32_t>(v.x), static_cast<uint32_t>(v.y),
+                                       static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    acc[2 * i] = bf16_lo(q[i]) * wp;
+                    acc[2 * i + 1] = bf16_hi(q[i]) * wp;
+                }
+            }
+            for (int m = 0; m < n; ++m) {
+                if (m == pl) continue;
+                const int r = __shfl_sync(0xffffffffu, my_row, m);
+                const float wm = __shfl_sync(0xffffffffu, my_w, m);
+                const int4 v = ok ? ld_nc_v4(reinterpret_cast<const int4*>(eout + static_cast<size_t>(r) * H) + c)
+                                  : make_int4(0, 0, 0, 0);
+                const uint32_t q[4] = {static_cast<uint32_t>(v.x), static_cast<uint32_t>(v.y),
+                                       static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    acc[2 * i] = fmaf(wm, bf16_lo(q[i]), acc[2 * i]);
+                    acc[2 * i + 1] = fmaf(wm, bf16_hi(q[i]), acc[2 * i + 1]);
+                }
+            }
+            if (ok) {
+                int4 o;
+                o.x = static_cast<int>(pack_bf16(acc[0], acc[1]));
+                o.y = static_cast<int>(pack_bf16(acc[2], acc[3]));
+                o.z = static_cast<int>(pack_bf16(acc[4], acc[5]));
+                o.w = static_cast<int>(pack_bf16(acc[6], acc[7]));
+                dst[c] = o;
+            }
+        }
+    }
+}
+
+// BF16 source combine, vectorised: one warp per (token, 512-column segment).
+// Lane i < #groups resolves group i's merged-row address (peer or local);
+// the warp then permutes them into pilot order and streams the rows.
+__global__ void __launch_bounds__(256) rbd_combine_bf16_kernel(
+    const char* const* __restrict__ back_tab, int H, int S, const int32_t* __restrict__ gbase,
+    const int32_t* __restrict__ gcount, const RbdGroups g, const int32_t* __restrict__ ru_base,
+    const int32_t* __restrict__ dptr, const double* __restrict__ cw,
+    const __nv_bfloat16* __restrict__ addend, __nv_bfloat16* __restrict__ out) {
+    const int nseg = (H + 511) / 512;
+    const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= static_cast<long long>(S) * nseg) return;
+    const int t = static_cast<int>(gw / nseg), seg = static_cast<int>(gw % nseg);
+    const int b = gbase[t], n = min(gcount[t], 32);
+    int key = 0x7fffffff;
+    unsigned long long rp = 0;
+    float sc = 0.f;
+    if (lane < n) {
+        const int gid = b + lane;
+        const int d = g.dest[gid];
+        key = g.pilot[gid];
+        rp = reinterpret_cast<unsigned long long>(
+            reinterpret_cast<const __nv_bfloat16*>(back_tab[d]) +
+            static_cast<size_t>(ru_base[d] + g.pos[gid] - dptr[d]) * H);
+        sc = g.n[gid] > 1 ? 1.f : static_cast<float>(cw[key]);
+    }
+    int rank = 0;  // position of my group in pilot order (rbd.cpp:343-356)
+    for (int j = 0; j < n; ++j) rank += __shfl_sync(0xffffffffu, key, j) < key;
+    int my_src = 0;  // lane o gathers the group of rank o
+    for (int o = 0; o < n; ++o) {
+        const unsigned bm = __ballot_sync(0xffffffffu, lane < n && rank == o);
+        if (lane == o) my_src = __ffs(bm) - 1;
+    }
+    const unsigned long long orp = __shfl_sync(0xffffffffu, rp, my_src);
+    const float osc = __shfl_sync(0xffffffffu, sc, my_src);
+    const int nchunk = H >> 3;
+    const int cbeg = seg * 64, cend = min(nchunk, cbeg + 64);
+    for (int cc = cbeg; cc < cend; cc += 32) {
+        const int c = cc + lane;
+        const bool ok = c < cend;
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int o = 0; o < n; ++o) {
+            const int4* p = reinterpret_cast<const int4*>(__shfl_sync(0xffffffffu, orp, o));
+            const float s = __shfl_sync(0xffffffffu, osc, o);
+            const int4 v = ok ? ld_nc_v4(p + c) : make_int4(0, 0, 0, 0);
+            const uint32_t q[4] = {static_cast<uint32_t>(v.x), static_cast<uint32_t>(v.y),
+                                   static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                acc[2 * i] = fmaf(s, bf16_lo(q[i]), acc[2 * i]);
+                acc[2 * i + 1] = fmaf(s, bf16_hi(q[i]), acc[2 * i + 1]);
+            }
+        }
+        if (!ok) continue;
+        if (addend) {
+            const int4 v = ld_nc_v4(reinterpret_cast<const int4*>(addend + static_cast<size_t>(t) * H) + c);
+            const uint32_t q[4] = {static_cast<uint32_t>(v.x), static_cast<uint32_t>(v.y),
+                                   static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                acc[2 * i] += bf16_lo(q[i]);
+                acc[2 * i + 1] += bf16_hi(q[i]);
+            }
+        }
+        int4 o;
+        o.x = static_cast<int>(pack_bf16(acc[0], acc[1]));
+        o.y = static_cast<int>(pack_bf16(acc[2], acc[3]));
+        o.z = static_cast<int>(pack_bf16(acc[4], acc[5]));
+        o.w = static_cast<int>(pack_bf16(acc[6], acc[7]));
+        st_na_v4(reinterpret_cast<int4*>(out + static_cast<size_t>(t) * H) + c, o);
+    }
+}
+
 // ---------------------------------------------------------------- launchers
 static int warp_grid(long long items) {
     const long long b = (items + 7) / 8;
@@ -525,6 +676,9 @@ void launch_rbd_merge(int dtype, const void* eout, int H, const RbdDesc* desc, c
     if (dtype == XMOE_F64)
         rbd_merge_kernel<double><<<warp_grid(max_groups), 256, 0, st>>>(
             static_cast<const double*>(eout), H, desc, gstart, rx, static_cast<double*>(back_u));
+    else if (H % 8 == 0)
+        rbd_merge_bf16_kernel<<<warp_grid(max_groups * ((H + 511) / 512)), 256, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(eout), H, desc, gstart, rx, static_cast<__nv_bfloat16*>(back_u));
     else
         rbd_merge_kernel<__nv_bfloat16><<<warp_grid(max_groups), 256, 0, st>>>(
             static_cast<const __nv_bfloat16*>(eout), H, desc, gstart, rx,
@@ -539,6 +693,10 @@ void launch_rbd_combine(int dtype, const char* const* back_tab, int H, int S, co
         rbd_combine_kernel<double><<<ceil_div(S, 8), 256, 0, st>>>(
             back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru_base, wk.dptr, cw,
             static_cast<const double*>(addend), static_cast<double*>(out));
+    else if (H % 8 == 0)
+        rbd_combine_bf16_kernel<<<ceil_div(static_cast<long long>(S) * ((H + 511) / 512), 8), 256, 0, st>>>(
+            back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru_base, wk.dptr, cw,
+            static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out));
     else
         rbd_combine_kernel<__nv_bfloat16><<<ceil_div(S, 8), 256, 0, st>>>(
             back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru_base, wk.dptr, cw,
