@@ -165,44 +165,72 @@ __global__ void rbd_group_count_kernel(const int32_t* __restrict__ slot_pos,
     gcount[t] = n;
 }
 
-// Single-CTA exclusive scan of n int32 (n up to a few 10^6); total -> *total.
-__global__ void __launch_bounds__(1024) exclusive_scan_kernel(const int32_t* __restrict__ in, int n,
+// Single-CTA exclusive scan of n int32 (n up to a few 10^6; n_dev, when
+// given, caps n on the device); total -> *total.  Tiles of 16K items are
+// staged in shared memory with coalesced loads, each thread scans 16
+// consecutive items, a warp-shuffle scan combines the threads.
+constexpr int kScanTile = 16384;
+__global__ void __launch_bounds__(1024) exclusive_scan_kernel(const int32_t* __restrict__ in, int n_host,
+                                                              const int32_t* __restrict__ n_dev,
                                                               int32_t* __restrict__ out,
                                                               int32_t* __restrict__ total) {
-    __shared__ int32_t s[1024];
+    extern __shared__ int32_t tile[];  // [kScanTile]
+    __shared__ int32_t warp_sums[32];
     __shared__ int32_t carry;
+    const int n = n_dev ? min(*n_dev, n_host) : n_host;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    const int per = (n + 1023) / 1024;
-    for (int i0 = 0; i0 < n; i0 += 1024 * 16) {
-        // each thread owns up to 16 consecutive items of this tile
-        const int my0 = i0 + threadIdx.x * 16;
+    for (int i0 = 0; i0 < n; i0 += kScanTile) {
+        for (int q = threadIdx.x; q < kScanTile; q += 1024) tile[q] = (i0 + q < n) ? in[i0 + q] : 0;
+        __syncthreads();
         int loc[16];
         int sum = 0;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-            const int v = (my0 + q < n) ? in[my0 + q] : 0;
             loc[q] = sum;
-            sum += v;
+            sum += tile[threadIdx.x * 16 + q];
         }
-        s[threadIdx.x] = sum;
-        __syncthreads();
-        for (int o = 1; o < 1024; o <<= 1) {
-            const int a = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
-            __syncthreads();
-            s[threadIdx.x] += a;
-            __syncthreads();
-        }
-        const int before = carry + s[threadIdx.x] - sum;
+        int incl = sum;
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
-            if (my0 + q < n) out[my0 + q] = before + loc[q];
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) warp_sums[wid] = incl;
         __syncthreads();
-        if (threadIdx.x == 1023) carry += s[1023];
+        if (wid == 0) {
+            int v = warp_sums[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += y;
+            }
+            warp_sums[lane] = v;  // inclusive over warps
+        }
+        __syncthreads();
+        const int before = carry + (wid ? warp_sums[wid - 1] : 0) + incl - sum;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) tile[threadIdx.x * 16 + q] = before + loc[q];
+        __syncthreads();
+        for (int q = threadIdx.x; q < kScanTile; q += 1024)
+            if (i0 + q < n) out[i0 + q] = tile[q];
+        if (threadIdx.x == 0) carry += warp_sums[31];
         __syncthreads();
     }
-    (void)per;
     if (threadIdx.x == 0 && total) *total = carry;
+}
+
+static void scan_i32(const int32_t* in, int n, const int32_t* n_dev, int32_t* out, int32_t* total,
+                     cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        XMOE_CUDA(cudaFuncSetAttribute(exclusive_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kScanTile * 4));
+        attr = true;
+    }
+    exclusive_scan_kernel<<<1, 1024, kScanTile * 4, st>>>(in, n, n_dev, out, total);
+    XMOE_LAUNCH_CHECK();
 }
 
 // Per token: emit its groups (gid = gbase[t] + j) with the drawn pilot.
@@ -626,8 +654,7 @@ void launch_rbd_groups(const int32_t* slot_pos, const int32_t* expert_ids, int S
     }
     rbd_group_count_kernel<<<ceil_div(S, 256), 256, 0, st>>>(slot_pos, expert_ids, S, k, El, wk.gcount);
     XMOE_LAUNCH_CHECK();
-    exclusive_scan_kernel<<<1, 1024, 0, st>>>(wk.gcount, S, wk.gbase, wk.G_dev);
-    XMOE_LAUNCH_CHECK();
+    scan_i32(wk.gcount, S, nullptr, wk.gbase, wk.G_dev, st);
     const long long max_groups = static_cast<long long>(S) * k;
     rbd_draw_kernel<<<ceil_div(max_groups, kRbdChunk), 256, 0, st>>>(
         state[0], state[1], state[2], state[3], jumps, wk.G_dev, wk.draws);
@@ -644,8 +671,7 @@ void launch_rbd_sort(int W, long long max_groups, RbdWork& wk, cudaStream_t st) 
                           wk.csr_ws, st);
     rbd_group_pos_kernel<<<ceil_div(max_groups, 256), 256, 0, st>>>(wk.perm, wk.G_dev, wk.g, wk.nsorted);
     XMOE_LAUNCH_CHECK();
-    exclusive_scan_kernel<<<1, 1024, 0, st>>>(wk.nsorted, static_cast<int>(max_groups), wk.coff, nullptr);
-    XMOE_LAUNCH_CHECK();
+    scan_i32(wk.nsorted, static_cast<int>(max_groups), wk.G_dev, wk.coff, nullptr, st);
 }
 
 void launch_rbd_offsets(const int32_t* G_all, const int32_t* tpe_all, int W, int E, int me, RbdWork& wk,
