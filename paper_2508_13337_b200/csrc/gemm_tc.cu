@@ -21,6 +21,9 @@
 // of tile i overlaps the MMAs of tile i+1.
 #include <cuda.h>
 
+#include <cstdlib>
+#include <string>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -61,17 +64,25 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Waits for the phase with the given parity.  A watchdog traps after ~2^31
+// polls (tens of seconds) so a protocol bug surfaces as a launch error
+// instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(a),
-        "r"(parity)
-        : "memory");
+    uint32_t done = 0;
+    for (uint32_t it = 0;; ++it) {
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, P1;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (it == 0x7fffffffu) asm volatile("trap;");
+    }
 }
 
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
@@ -368,6 +379,321 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace tc
 
+// ============================================================================
+// 2-CTA variant (cta_group::2): a cluster of two CTAs on a TPC computes one
+// 256 x 256 tile.  Each CTA stages its own 128 rows of A and its half of the
+// 256-wide B slice (128 rows) per 64-deep K block, so per-SM shared-memory
+// and L2->SM traffic drop by a third against the 1-CTA 128x256 tile.  The
+// leader CTA issues tcgen05.mma.cta_group::2 (M=256); each CTA's TMEM holds
+// its 128 accumulator rows.  Barrier protocol:
+//   full[s]   leader only, 2 arrivals (each CTA's expect_tx) + TMA bytes
+//   empty[s]  per CTA, arrived by the leader's multicast commit
+//   tfull[b]  per CTA, arrived by the leader's multicast commit
+//   tempty[b] leader only, 8 arrivals (4 epilogue warps x 2 CTAs)
+// ============================================================================
+namespace tc2 {
+
+constexpr int BM = 256;   // rows per CTA pair
+constexpr int BMC = 128;  // rows per CTA
+constexpr int BN = 256;
+constexpr int BK = 64;
+constexpr int UK = 16;
+constexpr int kStages = 6;
+constexpr int kAccBufs = 2;
+constexpr int kTmemCols = 512;
+constexpr int kThreads = 192;
+constexpr int kMaxGroups = 1024;
+constexpr uint32_t kABytes = BMC * BK * 2;
+constexpr uint32_t kBBytes = (BN / 2) * BK * 2;
+constexpr uint32_t kStageBytes = kABytes + kBBytes;
+constexpr size_t kSmemBytes = 1024 + kStages * kStageBytes + 1024 + sizeof(int32_t) * 2 * (kMaxGroups + 1);
+
+using tc::make_desc;
+using tc::mbar_init;
+using tc::mbar_wait;
+using tc::prefetch_tmap;
+using tc::smem_u32;
+using tc::tc_fence_after;
+using tc::tc_fence_before;
+using tc::tmem_ld32;
+
+__device__ __forceinline__ uint32_t cta_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void arrive_cluster(uint32_t cl_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
+}
+__device__ __forceinline__ void expect_tx_cluster(uint32_t cl_addr, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(cl_addr), "r"(bytes)
+                 : "memory");
+}
+// TMA load into this CTA's smem, completion counted on the leader's barrier.
+__device__ __forceinline__ void tma_load_2sm(const CUtensorMap* map, uint32_t bar_cl, void* dst, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cl)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t make_idesc2(int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+           (static_cast<uint32_t>(BM >> 4) << 24);
+}
+__device__ __forceinline__ void mma2(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void commit_both(uint64_t* bar) {
+    const uint16_t mask = 0x3;
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+
+struct TileInfo {
+    int g, row0, rows_left, n0;
+};
+
+__device__ __forceinline__ TileInfo tile_of(int t, const int32_t* tile_start, const int32_t* row_off, int G,
+                                            int ntn) {
+    int lo = 0, hi = G - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tile_start[mid] <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    const int local = t - tile_start[lo];
+    const int mb = local / ntn, nb = local % ntn;
+    TileInfo ti;
+    ti.g = lo;
+    ti.row0 = row_off[lo] + mb * BM;
+    ti.rows_left = (row_off[lo + 1] - row_off[lo]) - mb * BM;
+    ti.n0 = nb * BN;
+    return ti;
+}
+
+template <typename OutT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    grouped_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                            const int32_t* __restrict__ rows_per_group, int G, int N, int K,
+                            OutT* __restrict__ D, int relu) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* smem_a = smem;
+    uint8_t* smem_b = smem + kStages * kABytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* full_bar = bars;
+    uint64_t* empty_bar = bars + kStages;
+    uint64_t* tfull_bar = bars + 2 * kStages;
+    uint64_t* tempty_bar = bars + 2 * kStages + kAccBufs;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * kAccBufs);
+    int32_t* tile_start = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 1024);
+    int32_t* row_off = tile_start + kMaxGroups + 1;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cta_rank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1;
+    const int npairs = gridDim.x >> 1;
+    const int ntn = (N + BN - 1) / BN;
+    const int nkb = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        int t = 0, r = 0;
+        for (int g = 0; g < G; ++g) {
+            tile_start[g] = t;
+            row_off[g] = r;
+            const int m = rows_per_group[g];
+            t += ((m + BM - 1) / BM) * ntn;
+            r += m;
+        }
+        tile_start[G] = t;
+        row_off[G] = r;
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full_bar[s], 2);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int b = 0; b < kAccBufs; ++b) {
+            mbar_init(&tfull_bar[b], 1);
+            mbar_init(&tempty_bar[b], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmap_a);
+        prefetch_tmap(&tmap_b);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // barrier inits and TMEM allocation visible to the peer
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int num_tiles = tile_start[G];
+
+    if (warp == 0) {
+        // ===================== TMA producer (both CTAs) =====================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = pair; t < num_tiles; t += npairs) {
+                const TileInfo ti = tile_of(t, tile_start, row_off, G, ntn);
+                const int nw = min(BN, N - ti.n0);
+                const int n_mma = (nw + 15) & ~15;
+                const int arow = ti.row0 + BMC * static_cast<int>(rank);
+                const int brow = ti.g * N + ti.n0 + (n_mma / 2) * static_cast<int>(rank);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&empty_bar[stage], phase ^ 1);
+                    const uint32_t fb = mapa(&full_bar[stage], 0);
+                    expect_tx_cluster(fb, kStageBytes);
+                    tma_load_2sm(&tmap_a, fb, smem_a + stage * kABytes, kb * BK, arow);
+                    tma_load_2sm(&tmap_b, fb, smem_b + stage * kBBytes, kb * BK, brow);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (leader CTA) =====================
+        if (leader) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = pair; t < num_tiles; t += npairs) {
+                const TileInfo ti = tile_of(t, tile_start, row_off, G, ntn);
+                const int nw = min(BN, N - ti.n0);
+                const int n_mma = (nw + 15) & ~15;
+                const uint32_t idesc = make_idesc2(n_mma);
+                const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
+                mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+                tc_fence_after();
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&full_bar[stage], phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint64_t da = make_desc(smem_u32(smem_a + stage * kABytes));
+                        const uint64_t db = make_desc(smem_u32(smem_b + stage * kBBytes));
+#pragma unroll
+                        for (int kk = 0; kk < BK / UK; ++kk)
+                            mma2(tmem_d, da + static_cast<uint64_t>(kk * 2), db + static_cast<uint64_t>(kk * 2),
+                                 idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+                        commit_both(&empty_bar[stage]);
+                        if (kb == nkb - 1) commit_both(&tfull_bar[acc]);
+                    }
+                    __syncwarp();
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                if (++acc == kAccBufs) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else {
+        // ===================== epilogue (warps 2..5, both CTAs) =====================
+        const int quarter = warp & 3;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = pair; t < num_tiles; t += npairs) {
+            const TileInfo ti = tile_of(t, tile_start, row_off, G, ntn);
+            const int nw = min(BN, N - ti.n0);
+            mbar_wait(&tfull_bar[acc], acc_phase);
+            tc_fence_after();
+            const int r = BMC * static_cast<int>(rank) + quarter * 32 + lane;
+            const bool row_ok = r < ti.rows_left;
+            OutT* drow = D + static_cast<size_t>(ti.row0 + r) * N + ti.n0;
+            for (int c0 = 0; c0 < nw; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                              static_cast<uint32_t>(acc * BN + c0),
+                          v);
+                if (!row_ok) continue;
+                float f[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    f[i] = __uint_as_float(v[i]);
+                    if (relu) f[i] = fmaxf(f[i], 0.f);
+                }
+                const int cn = min(32, nw - c0);
+                if constexpr (sizeof(OutT) == 2) {
+                    if (cn == 32 && (N & 7) == 0) {
+                        int4* dst = reinterpret_cast<int4*>(drow + c0);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            int4 o;
+                            o.x = static_cast<int>(pack_bf16(f[8 * q + 0], f[8 * q + 1]));
+                            o.y = static_cast<int>(pack_bf16(f[8 * q + 2], f[8 * q + 3]));
+                            o.z = static_cast<int>(pack_bf16(f[8 * q + 4], f[8 * q + 5]));
+                            o.w = static_cast<int>(pack_bf16(f[8 * q + 6], f[8 * q + 7]));
+                            dst[q] = o;
+                        }
+                    } else {
+                        for (int i = 0; i < cn; ++i) drow[c0 + i] = __float2bfloat16_rn(f[i]);
+                    }
+                } else {
+                    if (cn == 32 && (N & 3) == 0) {
+                        float4* dst = reinterpret_cast<float4*>(drow + c0);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) dst[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+                    } else {
+                        for (int i = 0; i < cn; ++i) drow[c0 + i] = f[i];
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_cluster(mapa(&tempty_bar[acc], 0));
+            if (++acc == kAccBufs) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // the peer is done with the pair's TMEM and barriers
+    tc_fence_after();
+    if (warp == 1) {
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
+                     : "memory");
+    }
+}
+
+}  // namespace tc2
+
 // ---------------------------------------------------------------- host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -433,10 +759,50 @@ static void launch_tc(const void* A, long long rows, int K, const int32_t* rows_
     XMOE_LAUNCH_CHECK();
 }
 
+template <typename OutT>
+static void launch_tc2(const void* A, long long rows, int K, const int32_t* rows_per_group, int G,
+                       const void* B, int N, OutT* D, int relu, cudaStream_t st) {
+    require(G >= 1 && G <= tc2::kMaxGroups, XMOE_ERR_VALIDATION, "grouped gemm: 1 <= groups <= 1024");
+    require(K % 8 == 0 && K > 0, XMOE_ERR_VALIDATION, "bf16 path requires K % 8 == 0");
+    require(N % 32 == 0 && N > 0, XMOE_ERR_VALIDATION, "bf16 2-CTA path requires N % 32 == 0");
+    require((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0,
+            XMOE_ERR_VALIDATION, "bf16 operands must be 16-byte aligned");
+    if (rows == 0) return;
+    const CUtensorMap ta = make_tmap(A, rows, K, tc2::BMC);
+    const CUtensorMap tb = make_tmap(B, static_cast<long long>(G) * N, K, tc2::BN / 2);
+    static bool attr_set = false;
+    if (!attr_set) {
+        XMOE_CUDA(cudaFuncSetAttribute(tc2::grouped_gemm_tc2_kernel<OutT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(tc2::kSmemBytes)));
+        attr_set = true;
+    }
+    const long long max_tiles =
+        ((rows + tc2::BM - 1) / tc2::BM + G) * static_cast<long long>((N + tc2::BN - 1) / tc2::BN);
+    int sms = 0;
+    XMOE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const long long pairs = max_tiles < sms / 2 ? max_tiles : sms / 2;
+    tc2::grouped_gemm_tc2_kernel<OutT><<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
+        ta, tb, rows_per_group, G, N, K, D, relu);
+    XMOE_LAUNCH_CHECK();
+}
+
+// The expert FFN GEMMs run on the 2-CTA kernel; XMOE_GEMM=1cta selects the
+// single-CTA kernel (kept for A/B measurement and for N % 32 != 0).
+static bool use_2cta(int N) {
+    static const int mode = [] {
+        const char* e = std::getenv("XMOE_GEMM");
+        return (e && std::string(e) == "1cta") ? 1 : 2;
+    }();
+    return mode == 2 && N % 32 == 0;
+}
+
 void launch_grouped_gemm_bf16(const void* A, long long rows, int K, const int32_t* rows_per_group,
                               int G, const void* B, int N, void* D, int relu, cudaStream_t st) {
-    launch_tc<__nv_bfloat16>(A, rows, K, rows_per_group, G, B, N, static_cast<__nv_bfloat16*>(D),
-                             relu, st);
+    if (use_2cta(N))
+        launch_tc2<__nv_bfloat16>(A, rows, K, rows_per_group, G, B, N, static_cast<__nv_bfloat16*>(D), relu, st);
+    else
+        launch_tc<__nv_bfloat16>(A, rows, K, rows_per_group, G, B, N, static_cast<__nv_bfloat16*>(D), relu, st);
 }
 
 void launch_grouped_gemm_bf16_f32out(const void* A, long long rows, int K,
