@@ -175,7 +175,12 @@ int xmoe_ssmb_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x_full, int6
 int xmoe_layer_ledger(xmoe_layer* layer, uint64_t* out, int n);
 
 /* Per-stage device time of the last forward (ms, CUDA events), order:
- * gate, pft, dispatch, gemm, combine, total.  Requires timing enabled. */
+ * gate, pft, dispatch, experts, shared, combine, total, then the exchange
+ * split: counts (all-gather), rows_moved (dispatch kernel), dispatch_barrier,
+ * return_wait (merge/barrier before the combine), combine_kernel, and the
+ * shared-expert GEMMs, which run on a side stream concurrently with routing
+ * and the exchange ("shared" above is only the wait for them).
+ * Requires timing enabled. */
 int xmoe_layer_set_timing(xmoe_layer* layer, int enable);
 int xmoe_layer_stage_ms(xmoe_layer* layer, float* out, int n);
 

@@ -256,9 +256,11 @@ class Layer:
     def set_timing(self, on: bool):
         _check(lib().xmoe_layer_set_timing(self.h, int(on)))
 
-    STAGES = ["gate", "pft", "dispatch", "experts", "shared", "combine", "total"]
+    STAGES = ["gate", "pft", "dispatch", "experts", "shared", "combine", "total",
+              "counts", "rows_moved", "dispatch_barrier", "return_wait", "combine_kernel",
+              "shared_side_stream"]
 
     def stage_ms(self) -> dict:
-        buf = (C.c_float * 7)()
-        _check(lib().xmoe_layer_stage_ms(self.h, buf, 7))
+        buf = (C.c_float * 13)()
+        _check(lib().xmoe_layer_stage_ms(self.h, buf, 13))
         return dict(zip(self.STAGES, [float(v) for v in buf]))

@@ -309,11 +309,16 @@ int xmoe_layer_stage_ms(xmoe_layer* layer, float* out, int n) {
         Layer& L = layer->l;
         require(L.timing, XMOE_ERR_VALIDATION, "timing not enabled");
         XMOE_CUDA(cudaEventSynchronize(L.events[kEvCombine]));
-        const int pairs[][2] = {{kEvStart, kEvGate},   {kEvGate, kEvPft},    {kEvPft, kEvDispatch},
-                                {kEvDispatch, kEvGemm}, {kEvGemm, kEvShared}, {kEvShared, kEvCombine},
-                                {kEvStart, kEvCombine}};
-        for (int i = 0; i < n && i < 7; ++i)
+        const int pairs[][2] = {{kEvStart, kEvGate},    {kEvGate, kEvPft},     {kEvPft, kEvDispatch},
+                                {kEvDispatch, kEvGemm},  {kEvGemm, kEvShared},  {kEvShared, kEvCombine},
+                                {kEvStart, kEvCombine},  {kEvPft, kEvCounts},   {kEvCounts, kEvMoved},
+                                {kEvMoved, kEvDispatch}, {kEvShared, kEvReturn}, {kEvReturn, kEvCombine}};
+        for (int i = 0; i < n && i < 12; ++i)
             XMOE_CUDA(cudaEventElapsedTime(&out[i], L.events[pairs[i][0]], L.events[pairs[i][1]]));
+        if (n > 12) {  // shared-expert GEMMs on the side stream (0 when absent)
+            out[12] = 0.f;
+            if (L.Fs > 0) XMOE_CUDA(cudaEventElapsedTime(&out[12], L.ev_side0, L.ev_side1));
+        }
     });
 }
 

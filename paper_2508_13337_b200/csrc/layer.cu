@@ -41,6 +41,9 @@ namespace xmoe {
 static size_t elem_size_of(int dtype) { return dtype == XMOE_F64 ? 8 : 2; }
 
 Layer::~Layer() {
+    if (side) cudaStreamDestroy(side);
+    for (cudaEvent_t e : {ev_fork, ev_join, ev_side0, ev_side1})
+        if (e) cudaEventDestroy(e);
     for (void* p : peer_maps) cudaIpcCloseMemHandle(p);
     for (void* p : allocs) cudaFree(p);
     for (auto& e : events) cudaEventDestroy(e);
@@ -280,6 +283,11 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     }
     L.events.resize(kNumEvents);
     for (auto& e : L.events) XMOE_CUDA(cudaEventCreate(&e));
+    XMOE_CUDA(cudaStreamCreateWithFlags(&L.side, cudaStreamNonBlocking));
+    XMOE_CUDA(cudaEventCreateWithFlags(&L.ev_fork, cudaEventDisableTiming));
+    XMOE_CUDA(cudaEventCreateWithFlags(&L.ev_join, cudaEventDisableTiming));
+    XMOE_CUDA(cudaEventCreate(&L.ev_side0));
+    XMOE_CUDA(cudaEventCreate(&L.ev_side1));
     XMOE_CUDA(cudaDeviceSynchronize());
 }
 
@@ -321,10 +329,11 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     auto o_of = [&](int i) { return ob + static_cast<size_t>(i) * S * row_bytes; };
 
     L.mark(kEvStart, st);
+    for (int i = 0; i < nl; ++i)
+        launch_fill_i32(L.workers[i].s_rows, 1, static_cast<int32_t>(S), st);  // one dense group of S rows
     // 1. gate (gating.cpp:14-57)
     for (int i = 0; i < nl; ++i) {
         Worker& w = L.workers[i];
-        launch_fill_i32(w.s_rows, 1, static_cast<int32_t>(S), st);  // one dense group of S rows
         if (dt == XMOE_F64) {
             launch_gate_logits_f64(reinterpret_cast<const double*>(x_of(i)), static_cast<const double*>(L.gate),
                                    S, H, E, w.logits, st);
@@ -336,6 +345,21 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         }
     }
     L.mark(kEvGate, st);
+    // 1b. shared experts depend on x only: they run on a side stream, concurrent
+    //     with PFT and the exchange, and join before the combine.  Forked after
+    //     the gate so the two persistent GEMMs do not contend for SMs.
+    if (L.Fs > 0) {
+        XMOE_CUDA(cudaEventRecord(L.ev_fork, st));
+        XMOE_CUDA(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
+        if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side0, L.side));
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            run_gemm(dt, x_of(i), S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, L.side);
+            run_gemm(dt, w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, w.sout, 0, L.side);
+        }
+        if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side1, L.side));
+        XMOE_CUDA(cudaEventRecord(L.ev_join, L.side));
+    }
     // 2. padding-free token buffer (pft.cpp:12-60) [+ RBD groups and pilots, rbd.cpp:26-81]
     for (int i = 0; i < nl; ++i) {
         Worker& w = L.workers[i];
@@ -361,6 +385,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
             XMOE_NCCL(ncclAllGather(L.G_all + static_cast<size_t>(w.rank) * W, L.G_all, W, ncclInt32, comm, st));
         XMOE_NCCL(ncclGroupEnd());
     }
+    L.mark(kEvCounts, st);
     // 4. dispatch: destination rows in the owner's (local expert, source,
     //    position) layout (pf_pipeline.cpp:47-73), then the rows themselves
     for (int i = 0; i < nl; ++i) {
@@ -374,6 +399,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
             launch_rbd_pack(x_of(i), static_cast<int>(row_bytes), w.rbd, nk, w.slot_pos, k, w.dest_row, w.cw,
                             L.recv_u_tab, L.desc_tab, st);
         }
+        L.mark(kEvMoved, st);
         if (dist) L.barrier(st);
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
@@ -386,6 +412,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
             launch_scatter_rows(x_of(i), static_cast<int>(row_bytes), w.token_ids, w.B_dev, nk, w.dest_rank,
                                 w.dest_row, L.recv_tab, st);
         }
+        L.mark(kEvMoved, st);
         if (dist) L.barrier(st);
     } else {
         Worker& w = L.workers[0];
@@ -394,6 +421,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         XMOE_CUDA(cudaMemcpyAsync(L.h_tpe.data(), L.tpe_all, sizeof(int32_t) * W * E, cudaMemcpyDeviceToHost, st));
         XMOE_CUDA(cudaStreamSynchronize(st));
         L.exchange_nccl(/*forward=*/true, st);
+        L.mark(kEvMoved, st);
     }
     L.mark(kEvDispatch, st);
     // 5. expert FFNs over each owner's contiguous segments (pf_pipeline.cpp:83-105)
@@ -404,13 +432,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         run_gemm(dt, w.mid, L.R_max, F, w.rpe, L.El, w2_of(L, w.rank), H, w.eout, 0, st);
     }
     L.mark(kEvGemm, st);
-    if (L.Fs > 0) {
-        for (int i = 0; i < nl; ++i) {
-            Worker& w = L.workers[i];
-            run_gemm(dt, x_of(i), S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, st);
-            run_gemm(dt, w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, w.sout, 0, st);
-        }
-    }
+    if (L.Fs > 0) XMOE_CUDA(cudaStreamWaitEvent(st, L.ev_join, 0));
     L.mark(kEvShared, st);
     // 6. return path + weighted combine (pf_pipeline.cpp:107-135, rbd.cpp:287-358)
     if (rbd) {
@@ -419,6 +441,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
             launch_rbd_merge(dt, w.eout, H, w.desc_recv, w.gstart, w.rbd.rx, static_cast<long long>(W) * S, w.back_u, st);
         }
         if (dist) L.barrier(st);
+        L.mark(kEvReturn, st);
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             launch_rbd_combine(dt, L.back_tab, H, static_cast<int>(S), w.rbd, w.cw, L.Fs > 0 ? w.sout : nullptr,
@@ -426,6 +449,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         }
     } else if (tables) {
         if (dist) L.barrier(st);
+        L.mark(kEvReturn, st);
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             launch_combine(dt, nullptr, H, nullptr, w.slot_pos, k, w.cw, static_cast<int>(S),
@@ -433,6 +457,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         }
     } else {
         L.exchange_nccl(/*forward=*/false, st);
+        L.mark(kEvReturn, st);
         Worker& w = L.workers[0];
         launch_combine(dt, w.back, H, nullptr, w.slot_pos, k, w.cw, static_cast<int>(S),
                        L.Fs > 0 ? w.sout : nullptr, ob, st);

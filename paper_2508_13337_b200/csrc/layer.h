@@ -61,7 +61,8 @@ struct Worker {
     void* back_u = nullptr;       // [W*S, H] merged group outputs, read by the sources
 };
 
-enum { kEvStart = 0, kEvGate, kEvPft, kEvDispatch, kEvGemm, kEvShared, kEvCombine, kNumEvents };
+// stage boundaries; kEvCounts/kEvMoved/kEvReturn split the exchange phases
+enum { kEvStart = 0, kEvGate, kEvPft, kEvDispatch, kEvGemm, kEvShared, kEvCombine, kEvCounts, kEvMoved, kEvReturn, kNumEvents };
 
 struct Layer {
     Ctx* ctx = nullptr;
@@ -94,6 +95,8 @@ struct Layer {
     std::vector<void*> allocs;
     std::vector<cudaEvent_t> events;
     bool timing = false;
+    cudaStream_t side = nullptr;  // shared-expert GEMMs overlap routing + exchange
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_side0 = nullptr, ev_side1 = nullptr;
 
     void* alloc(size_t bytes);
     void mark(int ev, cudaStream_t st);

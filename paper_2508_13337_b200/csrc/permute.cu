@@ -6,6 +6,9 @@
 // One warp per row, 16-byte vectors, several vectors in flight per lane,
 // L1::no_allocate on the streaming side.  HBM-bound: algorithmic bytes per
 // row are 2 * row_bytes (+4 B index).
+#include <cstdlib>
+#include <string>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -129,6 +132,69 @@ __global__ void __launch_bounds__(32 * kRowWarps) scatter_rows_kernel(
     __threadfence_system();  // peer (NVLink) stores complete before the rank barrier
 }
 
+// TMA-staged variant of the fused permute + placement (XMOE_PERMUTE=tma;
+// measured on par with the warp kernel, which is the default because it
+// needs no shared memory and co-resides with the persistent GEMM CTAs): every warp owns a
+// ring of kTmaSlots row buffers in shared memory; lane 0 moves each row with
+// two bulk-async copies (global -> shared, completion on an mbarrier; then
+// shared -> global, which may be a peer GPU's memory over NVLink), keeping up
+// to kTmaSlots rows in flight per warp without touching registers.
+constexpr int kTmaSlots = 4;
+constexpr int kTmaWarps = 4;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__global__ void __launch_bounds__(32 * kTmaWarps) scatter_rows_tma_kernel(
+    const char* __restrict__ x, int row_bytes, const int32_t* __restrict__ token_ids,
+    const int32_t* __restrict__ B_dev, const int32_t* __restrict__ dest_rank,
+    const int32_t* __restrict__ dest_row, char* const* __restrict__ dest_bufs) {
+    extern __shared__ __align__(128) char ring[];  // [kTmaWarps][kTmaSlots][row_bytes]
+    __shared__ __align__(8) uint64_t bars[kTmaWarps][kTmaSlots];
+    const int B = *B_dev;
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    if (lane != 0) return;
+    char* my = ring + static_cast<size_t>(wl) * kTmaSlots * row_bytes;
+    for (int q = 0; q < kTmaSlots; ++q)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[wl][q])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    uint32_t phase_bits = 0;
+    int i = 0;
+    for (long long r = warp; r < B; r += nwarps, ++i) {
+        const int q = i % kTmaSlots;
+        char* slot = my + static_cast<size_t>(q) * row_bytes;
+        if (i >= kTmaSlots)  // the store that last read this slot must be done reading
+            asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTmaSlots - 1) : "memory");
+        const char* src = x + static_cast<size_t>(token_ids[r]) * row_bytes;
+        char* dst = dest_bufs[dest_rank[r]] + static_cast<size_t>(dest_row[r]) * row_bytes;
+        const uint32_t bar = smem_addr(&bars[wl][q]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(row_bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_addr(slot)),
+                     "l"(src), "r"(row_bytes), "r"(bar)
+                     : "memory");
+        const uint32_t par = (phase_bits >> q) & 1u;
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n.reg .pred P;\nmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\nselp.u32 %0, 1, 0, P;\n}\n"
+                : "=r"(done)
+                : "r"(bar), "r"(par)
+                : "memory");
+        }
+        phase_bits ^= 1u << q;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(slot)),
+                     "r"(row_bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __threadfence_system();
+}
+
 // Reverse of the placement: expert outputs come back from the owners'
 // grouped buffers into the source's packed order (pf_combine un-regroup +
 // reverse exchange, pf_pipeline.cpp:118-128).
@@ -172,9 +238,33 @@ void launch_dispatch_dest(const int32_t* tpe_all, int W, int E, int src,
     XMOE_LAUNCH_CHECK();
 }
 
+static bool permute_tma(int row_bytes) {
+    static const int mode = [] {
+        const char* e = std::getenv("XMOE_PERMUTE");
+        return (e && std::string(e) == "tma") ? 1 : 0;
+    }();
+    return mode == 1 && (row_bytes & 15) == 0 && row_bytes <= 16384;
+}
+
 void launch_scatter_rows(const void* x, int row_bytes, const int32_t* token_ids,
                          const int32_t* B_dev, long long max_rows, const int32_t* dest_rank,
                          const int32_t* dest_row, char* const* dest_bufs, cudaStream_t st) {
+    if (permute_tma(row_bytes)) {
+        const size_t smem = static_cast<size_t>(kTmaWarps) * kTmaSlots * row_bytes;
+        static size_t smem_set = 0;
+        if (smem > smem_set) {
+            XMOE_CUDA(cudaFuncSetAttribute(scatter_rows_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem)));
+            smem_set = smem;
+        }
+        const long long warps = max_rows > 0 ? max_rows : 1;
+        long long blocks = (warps + kTmaWarps - 1) / kTmaWarps;
+        if (blocks > 4 * kNumSMs) blocks = 4 * kNumSMs;
+        scatter_rows_tma_kernel<<<static_cast<int>(blocks), 32 * kTmaWarps, smem, st>>>(
+            static_cast<const char*>(x), row_bytes, token_ids, B_dev, dest_rank, dest_row, dest_bufs);
+        XMOE_LAUNCH_CHECK();
+        return;
+    }
     scatter_rows_kernel<<<row_grid(max_rows), 32 * kRowWarps, 0, st>>>(
         static_cast<const char*>(x), row_bytes, token_ids, B_dev, dest_rank, dest_row, dest_bufs);
     XMOE_LAUNCH_CHECK();
