@@ -124,6 +124,15 @@ int xmoe_grouped_gemm_bf16(xmoe_ctx* ctx, const void* A, int64_t rows, int64_t K
                            const int32_t* rows_per_group, int64_t G, const void* B, int64_t N,
                            void* D, int relu, void* stream);
 
+/* Exchange plan of the plain dispatch for rank `me`, from the all-gathered
+ * per-expert counts tpe_all [W, E] (HOST memory; no GPU needed):
+ * send_off [E+1]  start of expert e's block in me's packed buffer;
+ * recv_off [W*El] grouped row where source s's rows of my local expert le
+ *                 start ((local expert, source, position), pf_pipeline.cpp:47-73);
+ * recv_per_expert [El].  Any output may be NULL. */
+int xmoe_plan_dispatch(int W, int E, const int32_t* tpe_all, int me, int64_t* send_off,
+                       int64_t* recv_off, int64_t* recv_per_expert);
+
 /* ------------------------------------------------------------------ layer
  * One MoE layer's weights resident in HBM in the B200 layout, plus the
  * workspace of its forward pass.  Weights are DEVICE pointers in the

@@ -79,6 +79,7 @@ def lib():
         L.xmoe_layer_ledger.argtypes = [p, C.POINTER(C.c_uint64), i32]
         L.xmoe_layer_set_timing.argtypes = [p, i32]
         L.xmoe_layer_stage_ms.argtypes = [p, C.POINTER(C.c_float), i32]
+        L.xmoe_plan_dispatch.argtypes = [i32, i32, p, i32, p, p, p]
         _LIB = L
     return _LIB
 
@@ -102,6 +103,20 @@ def _dtype_code(t: torch.Tensor) -> int:
     if t.dtype == torch.bfloat16:
         return BF16
     raise XmoeError(2, f"unsupported dtype {t.dtype}")
+
+
+def plan_dispatch(tpe_all, me):
+    """Host exchange plan (xmoe_plan_dispatch): numpy in, numpy out, no GPU."""
+    import numpy as np
+    t = np.ascontiguousarray(tpe_all, dtype=np.int32)
+    W, E = t.shape
+    el = E // W if W and E % W == 0 else 1
+    send = np.zeros(E + 1, np.int64)
+    recv = np.zeros(W * el, np.int64)
+    rpe = np.zeros(el, np.int64)
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    _check(lib().xmoe_plan_dispatch(W, E, ptr(t), me, ptr(send), ptr(recv), ptr(rpe)))
+    return send, recv.reshape(W, el), rpe
 
 
 def kernel_launches() -> int:

@@ -473,34 +473,26 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
 void Layer::exchange_nccl(bool forward, cudaStream_t st) {
     Worker& w = workers[0];
     const int me = w.rank;
-    auto tpe = [&](int s, int e) { return h_tpe[static_cast<size_t>(s) * E + e]; };
     const size_t rb = static_cast<size_t>(H) * es;
     auto comm = static_cast<ncclComm_t>(ctx->nccl);
     const ncclDataType_t ty = d.dtype == XMOE_F64 ? ncclFloat64 : ncclBfloat16;
-    std::vector<long long> blk(E + 1, 0);
-    for (int e = 0; e < E; ++e) blk[e + 1] = blk[e] + tpe(me, e);
-    std::vector<long long> ebase(El + 1, 0);
-    for (int le = 0; le < El; ++le) {
-        long long a = 0;
-        for (int s = 0; s < W; ++s) a += tpe(s, me * El + le);
-        ebase[le + 1] = ebase[le] + a;
-    }
+    std::vector<int64_t> send_off(E + 1), recv_off(static_cast<size_t>(W) * El);
+    if (xmoe_plan_dispatch(W, E, h_tpe.data(), me, send_off.data(), recv_off.data(), nullptr) != XMOE_OK)
+        fail(XMOE_ERR_VALIDATION, "num_experts must be divisible by the worker-group size");
+    auto tpe = [&](int s, int e) { return static_cast<long long>(h_tpe[static_cast<size_t>(s) * E + e]); };
     XMOE_NCCL(ncclGroupStart());
     for (int peer = 0; peer < W; ++peer) {
-        for (int le = 0; le < El; ++le) {
+        for (int le = 0; le < El; ++le) {  // my rows for the experts peer owns
             const int e = peer * El + le;
             const long long n = tpe(me, e);
             if (n == 0) continue;
-            if (forward) XMOE_NCCL(ncclSend(static_cast<char*>(w.send) + blk[e] * rb, n * H, ty, peer, comm, st));
-            else XMOE_NCCL(ncclRecv(static_cast<char*>(w.back) + blk[e] * rb, n * H, ty, peer, comm, st));
+            if (forward) XMOE_NCCL(ncclSend(static_cast<char*>(w.send) + send_off[e] * rb, n * H, ty, peer, comm, st));
+            else XMOE_NCCL(ncclRecv(static_cast<char*>(w.back) + send_off[e] * rb, n * H, ty, peer, comm, st));
         }
-        for (int le = 0; le < El; ++le) {
-            const int e = me * El + le;
-            const long long n = tpe(peer, e);
+        for (int le = 0; le < El; ++le) {  // peer's rows for my experts
+            const long long n = tpe(peer, me * El + le);
             if (n == 0) continue;
-            long long before = 0;
-            for (int s = 0; s < peer; ++s) before += tpe(s, e);
-            char* p = static_cast<char*>(forward ? w.recv : w.eout) + (ebase[le] + before) * rb;
+            char* p = static_cast<char*>(forward ? w.recv : w.eout) + recv_off[static_cast<size_t>(peer) * El + le] * rb;
             if (forward) XMOE_NCCL(ncclRecv(p, n * H, ty, peer, comm, st));
             else XMOE_NCCL(ncclSend(p, n * H, ty, peer, comm, st));
         }

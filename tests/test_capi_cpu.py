@@ -1,0 +1,44 @@
+"""CPU-side checks of the boundary: libxmoe.so loads without a GPU, exports
+every symbol include/xmoe/xmoe.h declares plus the reference-shaped C++ API of
+include/xmoe/moesim_compat.hpp, and fails loudly (no CPU fallback) when asked
+for device work on a host without an sm_100 GPU."""
+import ctypes
+import re
+import subprocess
+
+import pytest
+import torch
+
+from paper_2508_13337_b200 import build, capi
+
+
+def test_library_exports_every_declared_symbol():
+    L = capi.lib()
+    syms = capi.header_symbols()
+    assert len(syms) >= 18
+    for s in syms:
+        assert hasattr(L, s), s
+    assert L.xmoe_abi_version() == 1
+
+
+def test_cpp_compat_api_exported():
+    out = subprocess.run(["nm", "-DC", build.LIB], capture_output=True, text=True).stdout
+    hdr = open(build.ROOT + "/include/xmoe/moesim_compat.hpp").read()
+    names = set(re.findall(r"^\w[\w:<>, ]*\s+(\w+)\(const", hdr, re.M)) | {"pf_moe_forward", "rbd_moe_forward",
+                                                                         "ssmb_forward", "pft_construct"}
+    for n in names:
+        assert f"xmoe::{n}(" in out, n
+
+
+def test_built_for_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", build.LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", build.LIB], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass and "UTMALDG" in sass  # tcgen05 MMA + TMA in the grouped GEMM
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="CPU-only host check")
+def test_no_cpu_fallback():
+    with pytest.raises(capi.XmoeError) as ei:
+        capi.Context(0, 1, -1)
+    assert ei.value.kind == "CudaError"
