@@ -164,6 +164,102 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_bf16_kernel(
     }
 }
 
+// BF16 combine over per-slot source addresses (written by the token-major
+// scatter): lane j loads copy j's expert-output address and weight — the only
+// dependent load before the rows stream.  One warp per (token, 512-column
+// segment); rows may live in a peer GPU's memory (NVLink loads).
+__global__ void __launch_bounds__(32 * kCombWarps) combine_slots_bf16_kernel(
+    const unsigned long long* __restrict__ slot_src, const float* __restrict__ slot_w, int k, int H, int S,
+    const __nv_bfloat16* __restrict__ addend, __nv_bfloat16* __restrict__ out) {
+    const int nseg = (H + kSegCols - 1) / kSegCols;
+    const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= static_cast<long long>(S) * nseg) return;
+    const int t = static_cast<int>(gw / nseg);
+    const int seg = static_cast<int>(gw % nseg);
+    const int nchunk = H >> 3;
+    const int seg_end = min(nchunk, (seg + 1) * (kSegCols / 8));
+    const int c0 = seg * (kSegCols / 8) + lane;
+    const int c1 = c0 + 32;
+    const bool v0 = c0 < seg_end, v1 = c1 < seg_end;
+    unsigned long long rp = 0;
+    float wv = 0.f;
+    if (lane < k) {
+        rp = slot_src[static_cast<size_t>(t) * k + lane];
+        wv = slot_w[static_cast<size_t>(t) * k + lane];
+    }
+    const int n = __popc(__ballot_sync(0xffffffffu, lane < k && rp != 0));  // kept copies: a prefix
+    // addend issued early: independent of the slot chain
+    int4 a4[2] = {make_int4(0, 0, 0, 0), make_int4(0, 0, 0, 0)};
+    if (addend) {
+        const int4* add = reinterpret_cast<const int4*>(addend + static_cast<size_t>(t) * H);
+        if (v0) a4[0] = ld_nc_v4(add + c0);
+        if (v1) a4[1] = ld_nc_v4(add + c1);
+    }
+    float acc[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q] = 0.f;
+    for (int b0 = 0; b0 < n; b0 += kBatch) {
+        int4 r[kBatch][2];
+        float wj[kBatch];
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            const int4* p = reinterpret_cast<const int4*>(__shfl_sync(0xffffffffu, rp, (b0 + b) & 31));
+            wj[b] = __shfl_sync(0xffffffffu, wv, (b0 + b) & 31);
+            if (b0 + b < n) {
+                r[b][0] = v0 ? ld_nc_v4(p + c0) : make_int4(0, 0, 0, 0);
+                r[b][1] = v1 ? ld_nc_v4(p + c1) : make_int4(0, 0, 0, 0);
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            if (b0 + b < n) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t u[4] = {static_cast<uint32_t>(r[b][h].x), static_cast<uint32_t>(r[b][h].y),
+                                           static_cast<uint32_t>(r[b][h].z), static_cast<uint32_t>(r[b][h].w)};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        acc[8 * h + 2 * q] = fmaf(wj[b], bf16_lo(u[q]), acc[8 * h + 2 * q]);
+                        acc[8 * h + 2 * q + 1] = fmaf(wj[b], bf16_hi(u[q]), acc[8 * h + 2 * q + 1]);
+                    }
+                }
+            }
+        }
+    }
+    int4* dst = reinterpret_cast<int4*>(out + static_cast<size_t>(t) * H);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int c = h ? c1 : c0;
+        if (!(h ? v1 : v0)) continue;
+        if (addend) {
+            const uint32_t u[4] = {static_cast<uint32_t>(a4[h].x), static_cast<uint32_t>(a4[h].y),
+                                   static_cast<uint32_t>(a4[h].z), static_cast<uint32_t>(a4[h].w)};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                acc[8 * h + 2 * q] += bf16_lo(u[q]);
+                acc[8 * h + 2 * q + 1] += bf16_hi(u[q]);
+            }
+        }
+        int4 o;
+        o.x = static_cast<int>(pack_bf16(acc[8 * h + 0], acc[8 * h + 1]));
+        o.y = static_cast<int>(pack_bf16(acc[8 * h + 2], acc[8 * h + 3]));
+        o.z = static_cast<int>(pack_bf16(acc[8 * h + 4], acc[8 * h + 5]));
+        o.w = static_cast<int>(pack_bf16(acc[8 * h + 6], acc[8 * h + 7]));
+        st_na_v4(dst + c, o);
+    }
+}
+
+void launch_combine_slots(const unsigned long long* slot_src, const float* slot_w, int k, int H, int S,
+                          const void* addend, void* out, cudaStream_t st) {
+    if (S == 0) return;
+    require(H % 8 == 0 && k <= 32, XMOE_ERR_VALIDATION, "slot combine needs model_dim % 8 == 0, k <= 32");
+    const long long warps = static_cast<long long>(S) * ((H + kSegCols - 1) / kSegCols);
+    combine_slots_bf16_kernel<<<ceil_div(warps, kCombWarps), 32 * kCombWarps, 0, st>>>(
+        slot_src, slot_w, k, H, S, static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out));
+    XMOE_LAUNCH_CHECK();
+}
+
 void launch_combine(int dtype, const void* rows, int H, const int32_t* ptr, const int32_t* idx,
                     int k, const double* w, int S, const void* addend, void* out,
                     cudaStream_t st, const char* const* tab, const int32_t* drank,

@@ -35,6 +35,12 @@ void launch_dispatch_dest(const int32_t* tpe_all, int W, int E, int src,
 void launch_scatter_rows(const void* x, int row_bytes, const int32_t* token_ids,
                          const int32_t* B_dev, long long max_rows, const int32_t* dest_rank,
                          const int32_t* dest_row, char* const* dest_bufs, cudaStream_t st);
+void launch_scatter_tokens(const void* x, int row_bytes, int S, int k, const int32_t* slot_pos,
+                           const int32_t* dest_rank, const int32_t* dest_row, const double* cw,
+                           char* const* dest_bufs, char* const* src_bufs, unsigned long long* slot_src,
+                           float* slot_w, cudaStream_t st);
+void launch_combine_slots(const unsigned long long* slot_src, const float* slot_w, int k, int H, int S,
+                          const void* addend, void* out, cudaStream_t st);
 void launch_unscatter_rows(int row_bytes, const int32_t* B_dev, long long max_rows,
                            const int32_t* dest_rank, const int32_t* dest_row,
                            const char* const* src_bufs, void* out, cudaStream_t st);

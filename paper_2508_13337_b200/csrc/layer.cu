@@ -192,6 +192,8 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         w.pft_ws = L.alloc(bucket_ws_bytes(nk, E));
         w.dest_rank = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * nk));
         w.dest_row = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * nk));
+        w.slot_src = static_cast<unsigned long long*>(L.alloc(sizeof(unsigned long long) * nk));
+        w.slot_w = static_cast<float*>(L.alloc(sizeof(float) * nk));
         w.rpe = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * L.El));
         w.sym = static_cast<char*>(L.alloc(sym_bytes));
         w.recv = w.sym + off_recv;
@@ -322,6 +324,8 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     const bool dist = L.distributed;
     const bool tables = !dist || L.p2p;  // row movement by kernels over pointer tables
     const bool rbd = L.d.dispatch_mode == XMOE_DISPATCH_RBD;
+    // bf16 rows: token-major permute (x read once) + slot-address combine
+    const bool token_major = dt == XMOE_BF16 && (row_bytes & 15) == 0 && k <= 32;
     const char* xb = static_cast<const char*>(x);
     char* ob = static_cast<char*>(out);
     const long long nk = S * k;
@@ -409,8 +413,12 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     } else if (tables) {
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
-            launch_scatter_rows(x_of(i), static_cast<int>(row_bytes), w.token_ids, w.B_dev, nk, w.dest_rank,
-                                w.dest_row, L.recv_tab, st);
+            if (token_major)
+                launch_scatter_tokens(x_of(i), static_cast<int>(row_bytes), static_cast<int>(S), k, w.slot_pos,
+                                      w.dest_rank, w.dest_row, w.cw, L.recv_tab, L.eout_tab, w.slot_src, w.slot_w, st);
+            else
+                launch_scatter_rows(x_of(i), static_cast<int>(row_bytes), w.token_ids, w.B_dev, nk, w.dest_rank,
+                                    w.dest_row, L.recv_tab, st);
         }
         L.mark(kEvMoved, st);
         if (dist) L.barrier(st);
@@ -452,8 +460,12 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         L.mark(kEvReturn, st);
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
-            launch_combine(dt, nullptr, H, nullptr, w.slot_pos, k, w.cw, static_cast<int>(S),
-                           L.Fs > 0 ? w.sout : nullptr, o_of(i), st, L.eout_tab, w.dest_rank, w.dest_row);
+            if (token_major)
+                launch_combine_slots(w.slot_src, w.slot_w, k, H, static_cast<int>(S), L.Fs > 0 ? w.sout : nullptr,
+                                     o_of(i), st);
+            else
+                launch_combine(dt, nullptr, H, nullptr, w.slot_pos, k, w.cw, static_cast<int>(S),
+                               L.Fs > 0 ? w.sout : nullptr, o_of(i), st, L.eout_tab, w.dest_rank, w.dest_row);
         }
     } else {
         L.exchange_nccl(/*forward=*/false, st);

@@ -52,6 +52,8 @@ struct Worker {
     void* smid = nullptr;         // shared experts [S, Fs]
     void* sout = nullptr;         // [S, H]
     int32_t* s_rows = nullptr;
+    unsigned long long* slot_src = nullptr;  // [S*k] address of each copy's expert output
+    float* slot_w = nullptr;                 // [S*k] its combine weight
     char* sym = nullptr;          // symmetric region: recv | eout | recv_u | desc_recv | back_u
     // redundancy-bypassing dispatch (rbd.cu)
     RbdWork rbd{};

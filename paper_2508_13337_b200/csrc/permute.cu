@@ -212,6 +212,72 @@ __global__ void __launch_bounds__(32 * kRowWarps) unscatter_rows_kernel(
     }
 }
 
+// Token-major fused permute + placement (bf16 rows, row_bytes % 16 == 0):
+// one warp per token reads the token row ONCE (up to 8 x 16 B per lane in
+// flight) and stores it to every kept copy's slot in the owners' grouped
+// buffers (peer addresses over NVLink when the owner is another GPU).  It
+// also records, per (token, slot), the address the combine will read the
+// copy's expert output from and the copy's weight, so the combine needs a
+// single dependent load before streaming rows.  Algorithmic bytes: one read
+// of x, k writes.
+constexpr int kTokWarps = 8;
+constexpr int kTokVec = 8;  // int4 per lane per pass (4 KB rows in one pass)
+
+__global__ void __launch_bounds__(32 * kTokWarps) scatter_tokens_kernel(
+    const char* __restrict__ x, int row_bytes, int S, int k, const int32_t* __restrict__ slot_pos,
+    const int32_t* __restrict__ dest_rank, const int32_t* __restrict__ dest_row, const double* __restrict__ cw,
+    char* const* __restrict__ dest_bufs, char* const* __restrict__ src_bufs,
+    unsigned long long* __restrict__ slot_src, float* __restrict__ slot_w) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    const int nvec = row_bytes >> 4;
+    for (long long t = warp; t < S; t += nwarps) {
+        // issue the row loads first; the index chain overlaps them
+        const int4* src = reinterpret_cast<const int4*>(x + static_cast<size_t>(t) * row_bytes);
+        int4 v[kTokVec];
+#pragma unroll
+        for (int u = 0; u < kTokVec; ++u) {
+            const int c = lane + 32 * u;
+            v[u] = c < nvec ? ld_nc_v4(src + c) : make_int4(0, 0, 0, 0);
+        }
+        int p = -1;
+        unsigned long long dst = 0, rd = 0;
+        float wv = 0.f;
+        if (lane < k) {
+            p = slot_pos[static_cast<size_t>(t) * k + lane];
+            if (p >= 0) {
+                const int r = dest_rank[p];
+                const size_t off = static_cast<size_t>(dest_row[p]) * row_bytes;
+                dst = reinterpret_cast<unsigned long long>(dest_bufs[r] + off);
+                rd = reinterpret_cast<unsigned long long>(src_bufs[r] + off);
+                wv = static_cast<float>(cw[p]);
+            }
+            slot_src[static_cast<size_t>(t) * k + lane] = rd;
+            slot_w[static_cast<size_t>(t) * k + lane] = wv;
+        }
+        const int n = __popc(__ballot_sync(0xffffffffu, lane < k && p >= 0));
+        for (int base = 0; base < nvec; base += 32 * kTokVec) {
+            if (base > 0) {
+#pragma unroll
+                for (int u = 0; u < kTokVec; ++u) {
+                    const int c = base + lane + 32 * u;
+                    v[u] = c < nvec ? ld_nc_v4(src + c) : make_int4(0, 0, 0, 0);
+                }
+            }
+            for (int j = 0; j < n; ++j) {
+                int4* d = reinterpret_cast<int4*>(__shfl_sync(0xffffffffu, dst, j));
+#pragma unroll
+                for (int u = 0; u < kTokVec; ++u) {
+                    const int c = base + lane + 32 * u;
+                    if (c < nvec) st_na_v4(d + c, v[u]);
+                }
+            }
+        }
+    }
+    __threadfence_system();  // peer (NVLink) stores complete before the rank barrier
+}
+
 static int row_grid(long long n) {
     const long long warps = n > 0 ? n : 1;
     const long long blocks = (warps + kRowWarps - 1) / kRowWarps;
@@ -267,6 +333,20 @@ void launch_scatter_rows(const void* x, int row_bytes, const int32_t* token_ids,
     }
     scatter_rows_kernel<<<row_grid(max_rows), 32 * kRowWarps, 0, st>>>(
         static_cast<const char*>(x), row_bytes, token_ids, B_dev, dest_rank, dest_row, dest_bufs);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_scatter_tokens(const void* x, int row_bytes, int S, int k, const int32_t* slot_pos,
+                           const int32_t* dest_rank, const int32_t* dest_row, const double* cw,
+                           char* const* dest_bufs, char* const* src_bufs, unsigned long long* slot_src,
+                           float* slot_w, cudaStream_t st) {
+    require((row_bytes & 15) == 0 && k <= 32, XMOE_ERR_VALIDATION, "token scatter needs 16-byte rows, k <= 32");
+    if (S == 0) return;
+    long long blocks = (static_cast<long long>(S) + kTokWarps - 1) / kTokWarps;
+    if (blocks > 8 * kNumSMs) blocks = 8 * kNumSMs;
+    scatter_tokens_kernel<<<static_cast<int>(blocks), 32 * kTokWarps, 0, st>>>(
+        static_cast<const char*>(x), row_bytes, S, k, slot_pos, dest_rank, dest_row, cw, dest_bufs, src_bufs,
+        slot_src, slot_w);
     XMOE_LAUNCH_CHECK();
 }
 
