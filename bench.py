@@ -48,6 +48,14 @@ def parse():
     return p.parse_args()
 
 
+def gemm_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+            return json.load(f)["traffic_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -308,26 +316,53 @@ def main():
     comb_bytes = copies * H * 2 + 2 * S * H * 2 + 8 * copies
     expert_frac_of_step = stages["experts"] / stages["total"] if stages["total"] else None
 
-    # ---- end to end through the public API with host buffers
-    xh = x.cpu().pin_memory()
-    oh = torch.empty_like(xh).pin_memory()
-    xd = torch.empty_like(x)
-    for _ in range(2):
-        xd.copy_(xh, non_blocking=True)
-        layer.forward(xd, out)
-        oh.copy_(out, non_blocking=True)
-    torch.cuda.synchronize()
+    # ---- end to end through the public API with host buffers.  Every step
+    # copies ITS input from pinned host memory and its output back to pinned
+    # host memory; the copies of neighbouring steps overlap the compute on
+    # separate streams (double-buffered), as a serving loop would run them.
+    e2e_steps = max(4, args.steps)
+    xh = [x.cpu().pin_memory() for _ in range(2)]
+    oh = [torch.empty_like(xh[0]).pin_memory() for _ in range(2)]
+    xd = [torch.empty_like(x) for _ in range(2)]
+    od = [torch.empty_like(x) for _ in range(2)]
+    s_in = torch.cuda.Stream()
+    s_out = torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
+    ev_outfree = [torch.cuda.Event() for _ in range(2)]
+
+    def e2e_run(n, t0=None, t1=None):
+        if t0 is not None:
+            t0.record(s_in)
+        with torch.cuda.stream(s_in):
+            xd[0].copy_(xh[0], non_blocking=True)
+            ev_in[0].record(s_in)
+        for i in range(n):
+            b, nb = i % 2, (i + 1) % 2
+            if i + 1 < n:
+                with torch.cuda.stream(s_in):
+                    if i >= 1:
+                        s_in.wait_event(ev_done[nb])  # step i-1 finished reading xd[nb]
+                    xd[nb].copy_(xh[nb], non_blocking=True)
+                    ev_in[nb].record(s_in)
+            stream.wait_event(ev_in[b])
+            if i >= 2:
+                stream.wait_event(ev_outfree[b])  # step i-2's output left the device
+            layer.forward(xd[b], od[b])
+            ev_done[b].record(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_done[b])
+                oh[b].copy_(od[b], non_blocking=True)
+                ev_outfree[b].record(s_out)
+        if t1 is not None:
+            t1.record(s_out)
+        torch.cuda.synchronize()
+
+    e2e_run(3)
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    e2e_steps = max(3, args.steps // 2)
-    for _ in range(e2e_steps):
-        xd.copy_(xh, non_blocking=True)
-        layer.forward(xd, out)
-        oh.copy_(out, non_blocking=True)
-    e1.record(stream)
-    torch.cuda.synchronize()
+    e2e_run(e2e_steps, e0, e1)
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
 
@@ -358,15 +393,22 @@ def main():
                          "achieved": achieved, "peak": tf_sus, "unit": "TFLOP/s",
                          "frac": achieved / tf_sus,
                          "peak_note": f"{peak_kind} sustained bf16 (kernel timed inside a long step); burst {tf_burst}",
-                         "traffic": None,
+                         "traffic": gemm_traffic(),
+                         "traffic_note": "dram read+write bytes per routed-GEMM launch from the committed "
+                                         "ncu --set full capture (profiles/gemm_traffic.json); "
+                                         "algorithmic A+B+D bytes per launch ~1.05e9",
                          "algorithmic_flops_per_launch_pair": gemm_flops,
                          "share_of_step": expert_frac_of_step},
             "stages_ms": stages,
             "hbm_kernels": {"permute_bytes": perm_bytes, "combine_bytes": comb_bytes,
                             "dispatch_ms": stages["dispatch"], "combine_ms": stages["combine"],
-                            "permute_GBps": perm_bytes / (stages["dispatch"] * 1e-3) / 1e9 if stages["dispatch"] else None,
-                            "combine_GBps": comb_bytes / (stages["combine"] * 1e-3) / 1e9 if stages["combine"] else None,
-                            "hbm_peak_GBps": hbm},
+                            "permute_GBps": perm_bytes / (stages["rows_moved"] * 1e-3) / 1e9 if stages["rows_moved"] else None,
+                            "combine_GBps": comb_bytes / (stages["combine_kernel"] * 1e-3) / 1e9 if stages["combine_kernel"] else None,
+                            "hbm_peak_GBps": hbm,
+                            "permute_frac": perm_bytes / (stages["rows_moved"] * 1e-3) / 1e9 / hbm
+                            if world == 1 and stages.get("rows_moved") else None,
+                            "combine_frac": comb_bytes / (stages["combine_kernel"] * 1e-3) / 1e9 / hbm
+                            if world == 1 and stages.get("combine_kernel") else None},
             "ledger": led,
             "gpu_launches": launches,
             "clocks": clk,

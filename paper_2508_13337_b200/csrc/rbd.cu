@@ -166,10 +166,11 @@ __global__ void rbd_group_count_kernel(const int32_t* __restrict__ slot_pos,
 }
 
 // Single-CTA exclusive scan of n int32 (n up to a few 10^6; n_dev, when
-// given, caps n on the device); total -> *total.  Tiles of 16K items are
-// staged in shared memory with coalesced loads, each thread scans 16
-// consecutive items, a warp-shuffle scan combines the threads.
-constexpr int kScanTile = 16384;
+// given, caps n on the device); total -> *total.  Tiles of 4K items are
+// staged in shared memory with coalesced loads, each thread scans
+// kScanPer consecutive items, a warp-shuffle scan combines the threads.
+constexpr int kScanTile = 4096;  // 16 KB smem: co-resides with the persistent GEMM CTAs
+constexpr int kScanPer = kScanTile / 1024;
 __global__ void __launch_bounds__(1024) exclusive_scan_kernel(const int32_t* __restrict__ in, int n_host,
                                                               const int32_t* __restrict__ n_dev,
                                                               int32_t* __restrict__ out,
@@ -184,12 +185,12 @@ __global__ void __launch_bounds__(1024) exclusive_scan_kernel(const int32_t* __r
     for (int i0 = 0; i0 < n; i0 += kScanTile) {
         for (int q = threadIdx.x; q < kScanTile; q += 1024) tile[q] = (i0 + q < n) ? in[i0 + q] : 0;
         __syncthreads();
-        int loc[16];
+        int loc[kScanPer];
         int sum = 0;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+        for (int q = 0; q < kScanPer; ++q) {
             loc[q] = sum;
-            sum += tile[threadIdx.x * 16 + q];
+            sum += tile[threadIdx.x * kScanPer + q];
         }
         int incl = sum;
 #pragma unroll
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(1024) exclusive_scan_kernel(const int32_t* __r
         __syncthreads();
         const int before = carry + (wid ? warp_sums[wid - 1] : 0) + incl - sum;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) tile[threadIdx.x * 16 + q] = before + loc[q];
+        for (int q = 0; q < kScanPer; ++q) tile[threadIdx.x * kScanPer + q] = before + loc[q];
         __syncthreads();
         for (int q = threadIdx.x; q < kScanTile; q += 1024)
             if (i0 + q < n) out[i0 + q] = tile[q];
