@@ -52,7 +52,8 @@ extern "C" {
 #define XMOE_DISPATCH_RBD 1   /* per-GPU redundancy bypass (rbd.cpp:26-358, node_of = rank) */
 
 /* layer flags */
-#define XMOE_LAYER_SSMB 1 /* ssmb_forward layer: every rank holds all experts (ssmb.cpp:29-43) */
+#define XMOE_LAYER_SSMB 1  /* ssmb_forward layer: every rank holds all experts (ssmb.cpp:29-43) */
+#define XMOE_LAYER_TRAIN 2 /* keep what xmoe_moe_backward needs (BF16 layers) */
 
 typedef struct xmoe_ctx xmoe_ctx;
 typedef struct xmoe_layer xmoe_layer;
@@ -133,6 +134,13 @@ int xmoe_grouped_gemm_bf16(xmoe_ctx* ctx, const void* A, int64_t rows, int64_t K
 int xmoe_plan_dispatch(int W, int E, const int32_t* tpe_all, int me, int64_t* send_off,
                        int64_t* recv_off, int64_t* recv_per_expert);
 
+/* Grouped weight-gradient GEMM (BF16 in, fp32 out): D_g [M,N] = X_g^T Y_g over
+ * the row segments of X [rows,M] and Y [rows,N] (transposed and zero-padded
+ * to 64-row multiples on the device, then the grouped-K tcgen05 kernel). */
+int xmoe_grouped_wgrad_bf16(xmoe_ctx* ctx, const void* X, const void* Y, int64_t rows,
+                             const int32_t* rows_per_group, int64_t G, int64_t M, int64_t N, float* D,
+                             void* stream);
+
 /* ------------------------------------------------------------------ layer
  * One MoE layer's weights resident in HBM in the B200 layout, plus the
  * workspace of its forward pass.  Weights are DEVICE pointers in the
@@ -175,6 +183,21 @@ int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S,
  * XMOE_LAYER_SSMB and holds every expert; max_tokens >= the largest shard. */
 int xmoe_ssmb_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x_full, int64_t S,
                       void* out_full, void* stream);
+
+/* Backward of the last xmoe_moe_forward (restated beyond the reference,
+ * which is forward-only).  x is the same input, dy the
+ * gradient of the output, both [S, H] bf16 on this rank; writes dx [S, H]
+ * bf16 and the layer's fp32 weight gradients, read with xmoe_layer_grads.
+ * Routing and capacity drops are constants of the forward (as in the
+ * reference's semantics); renorm layers are not supported. */
+int xmoe_moe_backward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, const void* dy, int64_t S,
+                      void* dx, void* stream);
+/* Device pointers (fp32, owned by the layer) to the gradients of the last
+ * backward, reference layouts: gate [H,E], w1 [E_local,H,F], w2 [E_local,F,H],
+ * shared merged sw1 [H, n_shared*Fs] (expert s = columns s*Fs..), sw2
+ * [n_shared*Fs, H].  Any argument may be NULL. */
+int xmoe_layer_grads(xmoe_layer* layer, float** dgate, float** dw1, float** dw2, float** dsw1,
+                     float** dsw2);
 
 /* Byte ledger of the last forward on this layer (collectives.hpp:31-49):
  * out[0..n) = { dispatch_rows_self, dispatch_rows_offrank,

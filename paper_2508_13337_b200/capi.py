@@ -80,6 +80,9 @@ def lib():
         L.xmoe_layer_set_timing.argtypes = [p, i32]
         L.xmoe_layer_stage_ms.argtypes = [p, C.POINTER(C.c_float), i32]
         L.xmoe_plan_dispatch.argtypes = [i32, i32, p, i32, p, p, p]
+        L.xmoe_moe_backward.argtypes = [p, p, p, p, i64, p, p]
+        L.xmoe_grouped_wgrad_bf16.argtypes = [p, p, p, i64, p, i64, i64, i64, p, p]
+        L.xmoe_layer_grads.argtypes = [p] + [C.POINTER(p)] * 5
         _LIB = L
     return _LIB
 
@@ -117,6 +120,16 @@ def plan_dispatch(tpe_all, me):
     ptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
     _check(lib().xmoe_plan_dispatch(W, E, ptr(t), me, ptr(send), ptr(recv), ptr(rpe)))
     return send, recv.reshape(W, el), rpe
+
+
+def grouped_wgrad_test(ctx, X, Y, rows_per_group):
+    """D_g = X_g^T Y_g (fp32) through xmoe_grouped_wgrad_bf16."""
+    G = len(rows_per_group)
+    rpg = torch.tensor(rows_per_group, dtype=torch.int32, device=X.device)
+    D = torch.empty((G, X.shape[1], Y.shape[1]), dtype=torch.float32, device=X.device)
+    _check(lib().xmoe_grouped_wgrad_bf16(ctx.h, _ptr(X), _ptr(Y), X.shape[0], _ptr(rpg), G, X.shape[1],
+                                         Y.shape[1], _ptr(D), _stream()))
+    return D
 
 
 def kernel_launches() -> int:
@@ -222,12 +235,15 @@ class Layer:
 
     def __init__(self, ctx: Context, *, num_experts, model_dim, ffn_dim, top_k, max_token_count,
                  max_tokens, dtype, gate, w1, w2, sw1=None, sw2=None, renorm=False,
-                 dispatch_mode=NAIVE, seed=0, ssmb=False):
+                 dispatch_mode=NAIVE, seed=0, ssmb=False, train=False):
         self.ctx = ctx
         ns = 0 if sw1 is None else sw1.shape[0]
         fs = 0 if sw1 is None else sw1.shape[2]
         self.desc = LayerDesc(num_experts, model_dim, ffn_dim, top_k, max_token_count, ns, fs,
-                              max_tokens, dtype, int(renorm), dispatch_mode, int(bool(ssmb)), seed)
+                              max_tokens, dtype, int(renorm), dispatch_mode,
+                              int(bool(ssmb)) | (2 if train else 0), seed)
+        self.shape = dict(E=num_experts, H=model_dim, F=ffn_dim, ns=ns, Fs=fs,
+                          E_held=w1.shape[0])
         self.dtype = dtype
         self.H = model_dim
         h = C.c_void_p()
@@ -251,6 +267,38 @@ class Layer:
         S = x.shape[-2]
         out = torch.empty_like(x) if out is None else out
         _check(lib().xmoe_moe_forward(self.ctx.h, self.h, _ptr(x), S, _ptr(out), _stream()))
+        return out
+
+    def backward(self, x, dy, dx=None):
+        """Gradient of the last forward: returns dx; weight grads via grads()."""
+        S = x.shape[-2]
+        dx = torch.empty_like(x) if dx is None else dx
+        _check(lib().xmoe_moe_backward(self.ctx.h, self.h, _ptr(x), _ptr(dy), S, _ptr(dx), _stream()))
+        return dx
+
+    def grads(self) -> dict:
+        """fp32 weight gradients in the reference layouts (views of layer memory)."""
+        ptrs = [C.c_void_p() for _ in range(5)]
+        _check(lib().xmoe_layer_grads(self.h, *[C.byref(q) for q in ptrs]))
+        sh = self.shape
+        H, E, F, El = sh["H"], sh["E"], sh["F"], sh["E_held"]
+        out = {}
+
+        def view(ptr, shape):
+            if not ptr.value:
+                return None
+
+            class _Dev:  # zero-copy view through __cuda_array_interface__
+                __cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f4",
+                                            "data": (ptr.value, False), "version": 3}
+            return torch.as_tensor(_Dev(), device="cuda").clone()
+        torch.cuda.synchronize()
+        out["gate"] = view(ptrs[0], (H, E))
+        out["w1"] = view(ptrs[1], (El, H, F))
+        out["w2"] = view(ptrs[2], (El, F, H))
+        if sh["ns"]:
+            out["sw1"] = view(ptrs[3], (H, sh["ns"] * sh["Fs"]))
+            out["sw2"] = view(ptrs[4], (sh["ns"] * sh["Fs"], H))
         return out
 
     def ssmb_forward(self, x_full, out=None):

@@ -267,6 +267,25 @@ int xmoe_grouped_gemm_bf16(xmoe_ctx* ctx, const void* A, int64_t rows, int64_t K
     });
 }
 
+int xmoe_grouped_wgrad_bf16(xmoe_ctx* ctx, const void* X, const void* Y, int64_t rows,
+                             const int32_t* rows_per_group, int64_t G, int64_t M, int64_t N, float* D,
+                             void* stream) {
+    return guarded([&] {
+        auto st = static_cast<cudaStream_t>(stream);
+        const long long Kp = (rows + 64 * G + 63) / 64 * 64;
+        char* ws = static_cast<char*>(ctx->c.scratch(2 * (M + N) * Kp + 4096 + 12 * (G + 2)));
+        int32_t* kpg = reinterpret_cast<int32_t*>(ws);
+        int32_t* koff = kpg + (G + 1);
+        int32_t* roff = koff + (G + 1);
+        char* xT = ws + 4096;
+        char* yT = xT + 2 * M * Kp;
+        launch_pad_offsets(rows_per_group, static_cast<int>(G), kpg, koff, roff, st);
+        launch_transpose_pad(X, static_cast<int>(M), rows_per_group, koff, roff, static_cast<int>(G), Kp, xT, st);
+        launch_transpose_pad(Y, static_cast<int>(N), rows_per_group, koff, roff, static_cast<int>(G), Kp, yT, st);
+        launch_grouped_wgrad_bf16(xT, static_cast<int>(M), Kp, kpg, static_cast<int>(G), yT, static_cast<int>(N), D, st);
+    });
+}
+
 int xmoe_layer_create(xmoe_ctx* ctx, const xmoe_layer_desc* desc, const void* gate,
                       const void* w1, const void* w2, const void* sw1, const void* sw2,
                       xmoe_layer** out) {
@@ -286,6 +305,26 @@ int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S,
     return guarded([&] {
         require(layer->l.ctx == &ctx->c, XMOE_ERR_VALIDATION, "layer belongs to another context");
         layer_forward(layer->l, x, S, out, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int xmoe_moe_backward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, const void* dy, int64_t S,
+                      void* dx, void* stream) {
+    return guarded([&] {
+        require(layer->l.ctx == &ctx->c, XMOE_ERR_VALIDATION, "layer belongs to another context");
+        layer_backward(layer->l, x, dy, S, dx, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int xmoe_layer_grads(xmoe_layer* layer, float** dgate, float** dw1, float** dw2, float** dsw1, float** dsw2) {
+    return guarded([&] {
+        Layer& L = layer->l;
+        require(L.train, XMOE_ERR_VALIDATION, "layer was not created with XMOE_LAYER_TRAIN");
+        if (dgate) *dgate = L.dgate;
+        if (dw1) *dw1 = L.dw1;
+        if (dw2) *dw2 = L.dw2;
+        if (dsw1) *dsw1 = L.dsw1;
+        if (dsw2) *dsw2 = L.dsw2;
     });
 }
 

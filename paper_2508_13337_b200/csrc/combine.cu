@@ -170,7 +170,8 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_bf16_kernel(
 // segment); rows may live in a peer GPU's memory (NVLink loads).
 __global__ void __launch_bounds__(32 * kCombWarps) combine_slots_bf16_kernel(
     const unsigned long long* __restrict__ slot_src, const float* __restrict__ slot_w, int k, int H, int S,
-    const __nv_bfloat16* __restrict__ addend, __nv_bfloat16* __restrict__ out) {
+    const __nv_bfloat16* __restrict__ addend, __nv_bfloat16* __restrict__ out, long long src_delta,
+    const __nv_bfloat16* __restrict__ addend2) {
     const int nseg = (H + kSegCols - 1) / kSegCols;
     const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -186,9 +187,10 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_slots_bf16_kernel(
     float wv = 0.f;
     if (lane < k) {
         rp = slot_src[static_cast<size_t>(t) * k + lane];
-        wv = slot_w[static_cast<size_t>(t) * k + lane];
+        wv = slot_w ? slot_w[static_cast<size_t>(t) * k + lane] : 1.f;
     }
     const int n = __popc(__ballot_sync(0xffffffffu, lane < k && rp != 0));  // kept copies: a prefix
+    if (rp) rp += static_cast<unsigned long long>(src_delta);
     // addend issued early: independent of the slot chain
     int4 a4[2] = {make_int4(0, 0, 0, 0), make_int4(0, 0, 0, 0)};
     if (addend) {
@@ -241,6 +243,16 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_slots_bf16_kernel(
                 acc[8 * h + 2 * q + 1] += bf16_hi(u[q]);
             }
         }
+        if (addend2) {
+            const int4 b4 = ld_nc_v4(reinterpret_cast<const int4*>(addend2 + static_cast<size_t>(t) * H) + c);
+            const uint32_t u[4] = {static_cast<uint32_t>(b4.x), static_cast<uint32_t>(b4.y),
+                                   static_cast<uint32_t>(b4.z), static_cast<uint32_t>(b4.w)};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                acc[8 * h + 2 * q] += bf16_lo(u[q]);
+                acc[8 * h + 2 * q + 1] += bf16_hi(u[q]);
+            }
+        }
         int4 o;
         o.x = static_cast<int>(pack_bf16(acc[8 * h + 0], acc[8 * h + 1]));
         o.y = static_cast<int>(pack_bf16(acc[8 * h + 2], acc[8 * h + 3]));
@@ -251,12 +263,13 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_slots_bf16_kernel(
 }
 
 void launch_combine_slots(const unsigned long long* slot_src, const float* slot_w, int k, int H, int S,
-                          const void* addend, void* out, cudaStream_t st) {
+                          const void* addend, void* out, cudaStream_t st, long long src_delta, const void* addend2) {
     if (S == 0) return;
     require(H % 8 == 0 && k <= 32, XMOE_ERR_VALIDATION, "slot combine needs model_dim % 8 == 0, k <= 32");
     const long long warps = static_cast<long long>(S) * ((H + kSegCols - 1) / kSegCols);
     combine_slots_bf16_kernel<<<ceil_div(warps, kCombWarps), 32 * kCombWarps, 0, st>>>(
-        slot_src, slot_w, k, H, S, static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out));
+        slot_src, slot_w, k, H, S, static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out),
+        src_delta, static_cast<const __nv_bfloat16*>(addend2));
     XMOE_LAUNCH_CHECK();
 }
 

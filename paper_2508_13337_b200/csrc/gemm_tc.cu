@@ -470,11 +470,15 @@ __device__ __forceinline__ void commit_both(uint64_t* bar) {
 }
 
 struct TileInfo {
-    int g, row0, rows_left, n0;
+    int g, row0, rows_left, n0, kofs, nkb;
 };
 
-__device__ __forceinline__ TileInfo tile_of(int t, const int32_t* tile_start, const int32_t* row_off, int G,
-                                            int ntn) {
+// kVarK == false: groups are row segments of A/D sharing K (forward, dgrad).
+// kVarK == true : groups are K segments (wgrad): group g reduces over its
+//                 gk[g] columns of A [M, Ktot] and B [N, Ktot] into D_g [M, N].
+template <bool kVarK>
+__device__ __forceinline__ TileInfo tile_of(int t, const int32_t* tile_start, const int32_t* off, int G, int ntn,
+                                            int M, int K) {
     int lo = 0, hi = G - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -485,17 +489,28 @@ __device__ __forceinline__ TileInfo tile_of(int t, const int32_t* tile_start, co
     const int mb = local / ntn, nb = local % ntn;
     TileInfo ti;
     ti.g = lo;
-    ti.row0 = row_off[lo] + mb * BM;
-    ti.rows_left = (row_off[lo + 1] - row_off[lo]) - mb * BM;
     ti.n0 = nb * BN;
+    if constexpr (kVarK) {
+        ti.row0 = mb * BM;
+        ti.rows_left = M - mb * BM;
+        ti.kofs = off[lo];
+        ti.nkb = (off[lo + 1] - off[lo]) / BK;
+    } else {
+        ti.row0 = off[lo] + mb * BM;
+        ti.rows_left = (off[lo + 1] - off[lo]) - mb * BM;
+        ti.kofs = 0;
+        ti.nkb = (K + BK - 1) / BK;
+    }
     return ti;
 }
 
-template <typename OutT>
+// D (+)= epilogue(A . B^T) on 256x256 pair tiles.  Epilogue options: ReLU,
+// and mask (multiply by mask[r,n] > 0 — the ReLU derivative in dgrad).
+template <typename OutT, bool kVarK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     grouped_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                            const int32_t* __restrict__ rows_per_group, int G, int N, int K,
-                            OutT* __restrict__ D, int relu) {
+                            const int32_t* __restrict__ group_sizes, int G, int M, int N, int K,
+                            OutT* __restrict__ D, int relu, const __nv_bfloat16* __restrict__ mask) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -508,7 +523,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* tempty_bar = bars + 2 * kStages + kAccBufs;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * kAccBufs);
     int32_t* tile_start = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 1024);
-    int32_t* row_off = tile_start + kMaxGroups + 1;
+    int32_t* off = tile_start + kMaxGroups + 1;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -517,19 +532,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int pair = blockIdx.x >> 1;
     const int npairs = gridDim.x >> 1;
     const int ntn = (N + BN - 1) / BN;
-    const int nkb = (K + BK - 1) / BK;
 
     if (threadIdx.x == 0) {
         int t = 0, r = 0;
         for (int g = 0; g < G; ++g) {
             tile_start[g] = t;
-            row_off[g] = r;
-            const int m = rows_per_group[g];
-            t += ((m + BM - 1) / BM) * ntn;
+            off[g] = r;
+            const int m = group_sizes[g];
+            t += (kVarK ? (M + BM - 1) / BM : (m + BM - 1) / BM) * ntn;
             r += m;
         }
         tile_start[G] = t;
-        row_off[G] = r;
+        off[G] = r;
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full_bar[s], 2);
             mbar_init(&empty_bar[s], 1);
@@ -564,17 +578,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int t = pair; t < num_tiles; t += npairs) {
-                const TileInfo ti = tile_of(t, tile_start, row_off, G, ntn);
+                const TileInfo ti = tile_of<kVarK>(t, tile_start, off, G, ntn, M, K);
                 const int nw = min(BN, N - ti.n0);
                 const int n_mma = (nw + 15) & ~15;
                 const int arow = ti.row0 + BMC * static_cast<int>(rank);
-                const int brow = ti.g * N + ti.n0 + (n_mma / 2) * static_cast<int>(rank);
-                for (int kb = 0; kb < nkb; ++kb) {
+                const int brow = (kVarK ? 0 : ti.g * N) + ti.n0 + (n_mma / 2) * static_cast<int>(rank);
+                for (int kb = 0; kb < ti.nkb; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     const uint32_t fb = mapa(&full_bar[stage], 0);
                     expect_tx_cluster(fb, kStageBytes);
-                    tma_load_2sm(&tmap_a, fb, smem_a + stage * kABytes, kb * BK, arow);
-                    tma_load_2sm(&tmap_b, fb, smem_b + stage * kBBytes, kb * BK, brow);
+                    const int kc = ti.kofs + kb * BK;
+                    tma_load_2sm(&tmap_a, fb, smem_a + stage * kABytes, kc, arow);
+                    tma_load_2sm(&tmap_b, fb, smem_b + stage * kBBytes, kc, brow);
                     if (++stage == kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -590,14 +605,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int t = pair; t < num_tiles; t += npairs) {
-                const TileInfo ti = tile_of(t, tile_start, row_off, G, ntn);
+                const TileInfo ti = tile_of<kVarK>(t, tile_start, off, G, ntn, M, K);
+                if (ti.nkb == 0) continue;  // empty reduction: the epilogue writes zeros
                 const int nw = min(BN, N - ti.n0);
                 const int n_mma = (nw + 15) & ~15;
                 const uint32_t idesc = make_idesc2(n_mma);
                 const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
                 mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
                 tc_fence_after();
-                for (int kb = 0; kb < nkb; ++kb) {
+                for (int kb = 0; kb < ti.nkb; ++kb) {
                     mbar_wait(&full_bar[stage], phase);
                     tc_fence_after();
                     if (lane == 0) {
@@ -608,7 +624,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             mma2(tmem_d, da + static_cast<uint64_t>(kk * 2), db + static_cast<uint64_t>(kk * 2),
                                  idesc, (kb > 0 || kk > 0) ? 1u : 0u);
                         commit_both(&empty_bar[stage]);
-                        if (kb == nkb - 1) commit_both(&tfull_bar[acc]);
+                        if (kb == ti.nkb - 1) commit_both(&tfull_bar[acc]);
                     }
                     __syncwarp();
                     if (++stage == kStages) {
@@ -628,13 +644,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = pair; t < num_tiles; t += npairs) {
-            const TileInfo ti = tile_of(t, tile_start, row_off, G, ntn);
+            const TileInfo ti = tile_of<kVarK>(t, tile_start, off, G, ntn, M, K);
             const int nw = min(BN, N - ti.n0);
-            mbar_wait(&tfull_bar[acc], acc_phase);
-            tc_fence_after();
             const int r = BMC * static_cast<int>(rank) + quarter * 32 + lane;
             const bool row_ok = r < ti.rows_left;
-            OutT* drow = D + static_cast<size_t>(ti.row0 + r) * N + ti.n0;
+            OutT* drow = D + (kVarK ? static_cast<size_t>(ti.g) * M * N : 0) +
+                         static_cast<size_t>(ti.row0 + r) * N + ti.n0;
+            if (ti.nkb == 0) {  // nothing to reduce: zeros, no accumulator used
+                if (row_ok)
+                    for (int c = 0; c < nw; ++c) drow[c] = static_cast<OutT>(0.f);
+                continue;
+            }
+            mbar_wait(&tfull_bar[acc], acc_phase);
+            tc_fence_after();
+            const __nv_bfloat16* mrow = mask ? mask + static_cast<size_t>(ti.row0 + r) * N + ti.n0 : nullptr;
             for (int c0 = 0; c0 < nw; c0 += 32) {
                 uint32_t v[32];
                 tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
@@ -648,6 +671,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     if (relu) f[i] = fmaxf(f[i], 0.f);
                 }
                 const int cn = min(32, nw - c0);
+                if (mrow) {
+                    if (cn == 32) {
+                        const int4* m4 = reinterpret_cast<const int4*>(mrow + c0);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int4 mv = m4[q];
+                            const uint32_t u[4] = {static_cast<uint32_t>(mv.x), static_cast<uint32_t>(mv.y),
+                                                   static_cast<uint32_t>(mv.z), static_cast<uint32_t>(mv.w)};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                if (!(bf16_lo(u[e]) > 0.f)) f[8 * q + 2 * e] = 0.f;
+                                if (!(bf16_hi(u[e]) > 0.f)) f[8 * q + 2 * e + 1] = 0.f;
+                            }
+                        }
+                    } else {
+                        for (int i = 0; i < cn; ++i)
+                            if (!(__bfloat162float(mrow[c0 + i]) > 0.f)) f[i] = 0.f;
+                    }
+                }
                 if constexpr (sizeof(OutT) == 2) {
                     if (cn == 32 && (N & 7) == 0) {
                         int4* dst = reinterpret_cast<int4*>(drow + c0);
@@ -759,32 +801,40 @@ static void launch_tc(const void* A, long long rows, int K, const int32_t* rows_
     XMOE_LAUNCH_CHECK();
 }
 
-template <typename OutT>
-static void launch_tc2(const void* A, long long rows, int K, const int32_t* rows_per_group, int G,
-                       const void* B, int N, OutT* D, int relu, cudaStream_t st) {
+template <typename OutT, bool kVarK>
+static void launch_tc2(const void* A, long long a_rows, long long a_cols, const int32_t* group_sizes, int G,
+                       const void* B, long long b_rows, int M, int N, int K, OutT* D, int relu,
+                       const __nv_bfloat16* mask, long long tile_bound, cudaStream_t st) {
     require(G >= 1 && G <= tc2::kMaxGroups, XMOE_ERR_VALIDATION, "grouped gemm: 1 <= groups <= 1024");
-    require(K % 8 == 0 && K > 0, XMOE_ERR_VALIDATION, "bf16 path requires K % 8 == 0");
+    require(a_cols % 8 == 0 && a_cols > 0, XMOE_ERR_VALIDATION, "bf16 path requires K % 8 == 0");
     require(N % 32 == 0 && N > 0, XMOE_ERR_VALIDATION, "bf16 2-CTA path requires N % 32 == 0");
     require((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0,
             XMOE_ERR_VALIDATION, "bf16 operands must be 16-byte aligned");
-    if (rows == 0) return;
-    const CUtensorMap ta = make_tmap(A, rows, K, tc2::BMC);
-    const CUtensorMap tb = make_tmap(B, static_cast<long long>(G) * N, K, tc2::BN / 2);
+    if (a_rows == 0 || tile_bound == 0) return;
+    const CUtensorMap ta = make_tmap(A, a_rows, a_cols, tc2::BMC);
+    const CUtensorMap tb = make_tmap(B, b_rows, a_cols, tc2::BN / 2);
     static bool attr_set = false;
     if (!attr_set) {
-        XMOE_CUDA(cudaFuncSetAttribute(tc2::grouped_gemm_tc2_kernel<OutT>,
+        XMOE_CUDA(cudaFuncSetAttribute(tc2::grouped_gemm_tc2_kernel<OutT, kVarK>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(tc2::kSmemBytes)));
         attr_set = true;
     }
-    const long long max_tiles =
-        ((rows + tc2::BM - 1) / tc2::BM + G) * static_cast<long long>((N + tc2::BN - 1) / tc2::BN);
     int sms = 0;
     XMOE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-    const long long pairs = max_tiles < sms / 2 ? max_tiles : sms / 2;
-    tc2::grouped_gemm_tc2_kernel<OutT><<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
-        ta, tb, rows_per_group, G, N, K, D, relu);
+    const long long pairs = tile_bound < sms / 2 ? tile_bound : sms / 2;
+    tc2::grouped_gemm_tc2_kernel<OutT, kVarK><<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
+        ta, tb, group_sizes, G, M, N, K, D, relu, mask);
     XMOE_LAUNCH_CHECK();
+}
+
+// Grouped-M: D[rows, N] over row segments (forward and dgrad).
+template <typename OutT>
+static void launch_tc2_rows(const void* A, long long rows, int K, const int32_t* rows_per_group, int G,
+                            const void* B, int N, OutT* D, int relu, const __nv_bfloat16* mask, cudaStream_t st) {
+    const long long bound = ((rows + tc2::BM - 1) / tc2::BM + G) * static_cast<long long>((N + tc2::BN - 1) / tc2::BN);
+    launch_tc2<OutT, false>(A, rows, K, rows_per_group, G, B, static_cast<long long>(G) * N, 0, N, K, D, relu, mask,
+                            bound, st);
 }
 
 // The expert FFN GEMMs run on the 2-CTA kernel; XMOE_GEMM=1cta selects the
@@ -800,9 +850,26 @@ static bool use_2cta(int N) {
 void launch_grouped_gemm_bf16(const void* A, long long rows, int K, const int32_t* rows_per_group,
                               int G, const void* B, int N, void* D, int relu, cudaStream_t st) {
     if (use_2cta(N))
-        launch_tc2<__nv_bfloat16>(A, rows, K, rows_per_group, G, B, N, static_cast<__nv_bfloat16*>(D), relu, st);
+        launch_tc2_rows<__nv_bfloat16>(A, rows, K, rows_per_group, G, B, N, static_cast<__nv_bfloat16*>(D), relu,
+                                       nullptr, st);
     else
         launch_tc<__nv_bfloat16>(A, rows, K, rows_per_group, G, B, N, static_cast<__nv_bfloat16*>(D), relu, st);
+}
+
+void launch_grouped_gemm_bf16_mask(const void* A, long long rows, int K, const int32_t* rows_per_group, int G,
+                                   const void* B, int N, void* D, const void* mask, cudaStream_t st) {
+    launch_tc2_rows<__nv_bfloat16>(A, rows, K, rows_per_group, G, B, N, static_cast<__nv_bfloat16*>(D), 0,
+                                   static_cast<const __nv_bfloat16*>(mask), st);
+}
+
+// Grouped-K (weight gradients): D_g[M, N] (fp32) = A[:, Kg] . B[:, Kg]^T where
+// A [M, Ktot] and B [N, Ktot] are K-major and group g owns the next
+// k_per_group[g] columns (multiples of 64, zero-padded).
+void launch_grouped_wgrad_bf16(const void* A, int M, long long Ktot, const int32_t* k_per_group, int G,
+                               const void* B, int N, float* D, cudaStream_t st) {
+    require(Ktot % 64 == 0, XMOE_ERR_VALIDATION, "wgrad: K segments must be padded to 64");
+    const long long bound = static_cast<long long>(G) * ((M + tc2::BM - 1) / tc2::BM) * ((N + tc2::BN - 1) / tc2::BN);
+    launch_tc2<float, true>(A, M, Ktot, k_per_group, G, B, N, M, N, 0, D, 0, nullptr, bound, st);
 }
 
 void launch_grouped_gemm_bf16_f32out(const void* A, long long rows, int K,

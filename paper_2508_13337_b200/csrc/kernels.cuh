@@ -8,6 +8,14 @@
 
 namespace xmoe {
 
+// Owner-side tables the training-mode dispatch fills: per grouped row, the
+// copy's combine weight and its home (source rank << 32 | token*k + slot).
+struct TrainTabs {
+    float* const* gw_tab = nullptr;
+    unsigned long long* const* gsrc_tab = nullptr;
+    int me = 0;
+};
+
 // gate.cu
 void launch_gate_logits_f64(const double* x, const double* wg, int S, int H, int E,
                             double* logits, cudaStream_t st);
@@ -38,9 +46,12 @@ void launch_scatter_rows(const void* x, int row_bytes, const int32_t* token_ids,
 void launch_scatter_tokens(const void* x, int row_bytes, int S, int k, const int32_t* slot_pos,
                            const int32_t* dest_rank, const int32_t* dest_row, const double* cw,
                            char* const* dest_bufs, char* const* src_bufs, unsigned long long* slot_src,
-                           float* slot_w, cudaStream_t st);
+                           float* slot_w, cudaStream_t st, TrainTabs tr = TrainTabs{});
+// out[t] = sum over t's kept copies of w * row(copy) (+ addend[t] + addend2[t]);
+// row address = slot_src + src_delta bytes; slot_w == null means weight 1.
 void launch_combine_slots(const unsigned long long* slot_src, const float* slot_w, int k, int H, int S,
-                          const void* addend, void* out, cudaStream_t st);
+                          const void* addend, void* out, cudaStream_t st, long long src_delta = 0,
+                          const void* addend2 = nullptr);
 void launch_unscatter_rows(int row_bytes, const int32_t* B_dev, long long max_rows,
                            const int32_t* dest_rank, const int32_t* dest_row,
                            const char* const* src_bufs, void* out, cudaStream_t st);
@@ -60,9 +71,23 @@ void launch_grouped_gemm_f64(const double* A, long long rows_bound, int K,
 // gemm_tc.cu
 void launch_grouped_gemm_bf16(const void* A, long long rows, int K, const int32_t* rows_per_group,
                               int G, const void* B, int N, void* D, int relu, cudaStream_t st);
+void launch_grouped_gemm_bf16_mask(const void* A, long long rows, int K, const int32_t* rows_per_group, int G,
+                                   const void* B, int N, void* D, const void* mask, cudaStream_t st);
+void launch_grouped_wgrad_bf16(const void* A, int M, long long Ktot, const int32_t* k_per_group, int G,
+                               const void* B, int N, float* D, cudaStream_t st);
 void launch_grouped_gemm_bf16_f32out(const void* A, long long rows, int K,
                                      const int32_t* rows_per_group, int G, const void* B, int N,
                                      float* D, int relu, cudaStream_t st);
+
+// backward.cu
+void launch_bwd_owner_prep(const void* dyg, const void* eout, const float* gw, const unsigned long long* gsrc,
+                           const int32_t* rpe, int El, int H, long long max_rows, float* const* slotdw_tab,
+                           void* dz, cudaStream_t st);
+void launch_pad_offsets(const int32_t* rows, int G, int32_t* kpg, int32_t* koff, int32_t* roff, cudaStream_t st);
+void launch_transpose_pad(const void* in, int C, const int32_t* rows, const int32_t* koff, const int32_t* roff,
+                          int G, long long ld, void* out, cudaStream_t st);
+void launch_gate_bwd(const float* logits, const int32_t* slot_pos, const int32_t* expert_ids, const float* slot_dw,
+                     int S, int E, int k, void* dl, cudaStream_t st);
 
 // misc.cu
 void launch_recv_counts(const int32_t* tpe_all, int W, int E, int dst, int32_t* rpe,

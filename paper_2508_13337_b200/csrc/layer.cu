@@ -173,9 +173,23 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     const size_t off_recv_u = off_eout + up(static_cast<size_t>(L.R_max) * H * es);
     const size_t off_desc = off_recv_u + (rbd ? up(static_cast<size_t>(rmax) * H * es) : 0);
     const size_t off_back = off_desc + (rbd ? up(sizeof(RbdDesc) * L.R_max) : 0);
-    const size_t sym_bytes = off_back + (rbd ? up(static_cast<size_t>(rmax) * H * es) : 0);
+    const size_t off_train = off_back + (rbd ? up(static_cast<size_t>(rmax) * H * es) : 0);
+    L.train = (d.flags & XMOE_LAYER_TRAIN) != 0;
+    require(!L.train || (bf && !d.renorm && (!L.distributed || L.p2p) && L.nl == 1), XMOE_ERR_VALIDATION,
+            "training layers need bf16, no renorm, one rank per process (or world 1) and the NVLink peer transport");
+    require(!L.train || (H % 32 == 0 && F % 32 == 0 && E % 32 == 0 && L.Fs % 32 == 0), XMOE_ERR_VALIDATION,
+            "training layers need model_dim, ffn_dim, num_experts and shared width multiples of 32");
+    const size_t off_dyg = off_train;
+    const size_t off_dxc = off_dyg + (L.train ? up(static_cast<size_t>(L.R_max) * H * es) : 0);
+    const size_t off_gw = off_dxc + (L.train ? up(static_cast<size_t>(L.R_max) * H * es) : 0);
+    const size_t off_gsrc = off_gw + (L.train ? up(sizeof(float) * L.R_max) : 0);
+    const size_t off_sdw = off_gsrc + (L.train ? up(sizeof(unsigned long long) * L.R_max) : 0);
+    const size_t sym_bytes = off_sdw + (L.train ? up(sizeof(float) * nk) : 0);
+    L.off_eout = static_cast<long long>(off_eout);
+    L.off_dxc = static_cast<long long>(off_dxc);
     L.workers.resize(L.nl);
     std::vector<char*> t_recv(W), t_eout(W), t_recv_u(W), t_desc(W), t_back(W);
+    std::vector<char*> t_dyg(W), t_dxc(W), t_gw(W), t_gsrc(W), t_sdw(W);
     for (int i = 0; i < L.nl; ++i) {
         Worker& w = L.workers[i];
         w.rank = ssmb ? 0 : ctx.rank_of(i);
@@ -237,8 +251,45 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
             w.back_u = w.sym + off_back;
             w.gstart = i32(rmax);
         }
+        if (L.train) {
+            const long long Fs = L.Fs;
+            L.Kp = (L.R_max + 64LL * L.El + 63) / 64 * 64;
+            L.Sp = (S + 63) / 64 * 64;
+            w.dyg = w.sym + off_dyg;
+            w.dxc = w.sym + off_dxc;
+            w.gw = reinterpret_cast<float*>(w.sym + off_gw);
+            w.gsrc = reinterpret_cast<unsigned long long*>(w.sym + off_gsrc);
+            w.slot_dw = reinterpret_cast<float*>(w.sym + off_sdw);
+            w.dz = L.alloc(static_cast<size_t>(L.R_max) * H * es);
+            w.dH = L.alloc(static_cast<size_t>(L.R_max) * F * es);
+            w.xT = L.alloc(static_cast<size_t>(H) * L.Kp * es);
+            w.dHT = L.alloc(static_cast<size_t>(F) * L.Kp * es);
+            w.aT = L.alloc(static_cast<size_t>(F) * L.Kp * es);
+            w.dzT = L.alloc(static_cast<size_t>(H) * L.Kp * es);
+            w.kpg = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
+            w.koff = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
+            w.roff = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
+            w.tk = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * 8));
+            w.xTt = L.alloc(static_cast<size_t>(H) * L.Sp * es);
+            w.dyT = L.alloc(static_cast<size_t>(H) * L.Sp * es);
+            w.dlT = L.alloc(static_cast<size_t>(E) * L.Sp * es);
+            w.dl = L.alloc(static_cast<size_t>(S) * E * es);
+            w.dxg = L.alloc(static_cast<size_t>(S) * H * es);
+            if (Fs > 0) {
+                w.dHs = L.alloc(static_cast<size_t>(S) * Fs * es);
+                w.dHsT = L.alloc(static_cast<size_t>(Fs) * L.Sp * es);
+                w.asT = L.alloc(static_cast<size_t>(Fs) * L.Sp * es);
+                w.dxs = L.alloc(static_cast<size_t>(S) * H * es);
+            }
+            w.bslot_src = static_cast<unsigned long long*>(L.alloc(sizeof(unsigned long long) * nk));
+        }
         t_recv[w.rank] = static_cast<char*>(w.recv);
         t_eout[w.rank] = static_cast<char*>(w.eout);
+        t_dyg[w.rank] = static_cast<char*>(w.dyg);
+        t_dxc[w.rank] = static_cast<char*>(w.dxc);
+        t_gw[w.rank] = reinterpret_cast<char*>(w.gw);
+        t_gsrc[w.rank] = reinterpret_cast<char*>(w.gsrc);
+        t_sdw[w.rank] = reinterpret_cast<char*>(w.slot_dw);
         t_recv_u[w.rank] = static_cast<char*>(w.recv_u);
         t_desc[w.rank] = reinterpret_cast<char*>(w.desc_recv);
         t_back[w.rank] = static_cast<char*>(w.back_u);
@@ -262,6 +313,11 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
             char* b = static_cast<char*>(p);
             t_recv[r] = b + off_recv;
             t_eout[r] = b + off_eout;
+            t_dyg[r] = b + off_dyg;
+            t_dxc[r] = b + off_dxc;
+            t_gw[r] = b + off_gw;
+            t_gsrc[r] = b + off_gsrc;
+            t_sdw[r] = b + off_sdw;
             t_recv_u[r] = b + off_recv_u;
             t_desc[r] = b + off_desc;
             t_back[r] = b + off_back;
@@ -274,6 +330,38 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     };
     L.recv_tab = table(t_recv);
     L.eout_tab = table(t_eout);
+    if (L.train) {
+        L.dyg_tab = table(t_dyg);
+        L.dxc_tab = table(t_dxc);
+        L.gw_tab = reinterpret_cast<float**>(table(t_gw));
+        L.gsrc_tab = reinterpret_cast<unsigned long long**>(table(t_gsrc));
+        L.slotdw_tab = reinterpret_cast<float**>(table(t_sdw));
+        // reference-layout copies of the weights (dgrad B operands) + fp32 grads
+        const size_t ew = static_cast<size_t>(L.E_held) * H * F;
+        L.w1r = L.alloc(ew * es);
+        L.w2r = L.alloc(ew * es);
+        L.gater = L.alloc(static_cast<size_t>(H) * E * es);
+        XMOE_CUDA(cudaMemcpy(L.w1r, w1, ew * es, cudaMemcpyDeviceToDevice));
+        XMOE_CUDA(cudaMemcpy(L.w2r, w2, ew * es, cudaMemcpyDeviceToDevice));
+        XMOE_CUDA(cudaMemcpy(L.gater, gate, static_cast<size_t>(H) * E * es, cudaMemcpyDeviceToDevice));
+        L.dgate = static_cast<float*>(L.alloc(sizeof(float) * H * E));
+        L.dw1 = static_cast<float*>(L.alloc(sizeof(float) * ew));
+        L.dw2 = static_cast<float*>(L.alloc(sizeof(float) * ew));
+        if (L.Fs > 0) {
+            const int ns = static_cast<int>(d.n_shared), Fs1 = static_cast<int>(d.shared_ffn_dim);
+            L.sw1r = L.alloc(static_cast<size_t>(H) * L.Fs * es);
+            L.sw2r = L.alloc(static_cast<size_t>(H) * L.Fs * es);
+            for (int s2 = 0; s2 < ns; ++s2)  // W1cat [H, ns*Fs]
+                XMOE_CUDA(cudaMemcpy2D(static_cast<char*>(L.sw1r) + static_cast<size_t>(s2) * Fs1 * es,
+                                       static_cast<size_t>(L.Fs) * es,
+                                       static_cast<const char*>(sw1) + static_cast<size_t>(s2) * H * Fs1 * es,
+                                       static_cast<size_t>(Fs1) * es, static_cast<size_t>(Fs1) * es, H,
+                                       cudaMemcpyDeviceToDevice));
+            XMOE_CUDA(cudaMemcpy(L.sw2r, sw2, static_cast<size_t>(H) * L.Fs * es, cudaMemcpyDeviceToDevice));
+            L.dsw1 = static_cast<float*>(L.alloc(sizeof(float) * H * L.Fs));
+            L.dsw2 = static_cast<float*>(L.alloc(sizeof(float) * H * L.Fs));
+        }
+    }
     if (rbd) {
         L.recv_u_tab = table(t_recv_u);
         L.desc_tab = reinterpret_cast<RbdDesc**>(table(t_desc));
@@ -510,6 +598,78 @@ void Layer::exchange_nccl(bool forward, cudaStream_t st) {
         }
     }
     XMOE_NCCL(ncclGroupEnd());
+}
+
+// ---------------------------------------------------------------- backward
+// Gradient of the last forward (bf16, pointer-table transports).  Per rank:
+//   B1 dy rows to the owners (token-major, read once), each copy's weight and
+//      home slot recorded at the owner
+//   B2 owner: dL/dw_c = <dy_t, y_c> back to the home slot; dz = w_c dy_t
+//   B3 dgrad: dH = (dz W2^T) * [mid > 0];  dxc = dH W1^T      (grouped-M)
+//   B4 wgrad: dW1_e = x_e^T dH_e, dW2_e = a_e^T dz_e          (grouped-K)
+//   B5 shared experts (dense) and the gate: dl = softmax Jacobian of dL/dw,
+//      dx_gate = dl Wg^T, dWg = x^T dl
+//   B6 dx_t = sum of its copies' dxc rows (read from the owners) + shared
+//      + gate parts
+void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* dx, cudaStream_t st) {
+    require(L.train, XMOE_ERR_VALIDATION, "layer was not created with XMOE_LAYER_TRAIN");
+    require(S == L.last_S, XMOE_ERR_VALIDATION, "backward must follow a forward of the same sequence");
+    Ctx& ctx = *L.ctx;
+    const int W = L.W, E = L.E, H = L.H, F = L.F, k = L.k, El = L.El;
+    const size_t rb = static_cast<size_t>(H) * L.es;
+    const bool dist = L.distributed;
+    auto xo = [&](const void* b, int i) { return static_cast<const char*>(b) + static_cast<size_t>(i) * S * rb; };
+    for (int i = 0; i < L.nl; ++i) {  // B1
+        Worker& w = L.workers[i];
+        TrainTabs tr{L.gw_tab, L.gsrc_tab, w.rank};
+        launch_scatter_tokens(xo(dy, i), static_cast<int>(rb), static_cast<int>(S), k, w.slot_pos, w.dest_rank,
+                              w.dest_row, w.cw, L.dyg_tab, L.dxc_tab, w.bslot_src, nullptr, st, tr);
+    }
+    if (dist) L.barrier(st);
+    for (int i = 0; i < L.nl; ++i) {  // B2-B4 at the owner
+        Worker& w = L.workers[i];
+        const size_t eo = dist ? 0 : static_cast<size_t>(w.rank) * El * H * F * L.es;
+        launch_bwd_owner_prep(w.dyg, w.eout, w.gw, w.gsrc, w.rpe, El, H, L.R_max, L.slotdw_tab, w.dz, st);
+        launch_grouped_gemm_bf16_mask(w.dz, L.R_max, H, w.rpe, El, static_cast<const char*>(L.w2r) + eo, F, w.dH,
+                                      w.mid, st);
+        launch_grouped_gemm_bf16(w.dH, L.R_max, F, w.rpe, El, static_cast<const char*>(L.w1r) + eo, H, w.dxc, 0, st);
+        launch_pad_offsets(w.rpe, El, w.kpg, w.koff, w.roff, st);
+        launch_transpose_pad(w.recv, H, w.rpe, w.koff, w.roff, El, L.Kp, w.xT, st);
+        launch_transpose_pad(w.dH, F, w.rpe, w.koff, w.roff, El, L.Kp, w.dHT, st);
+        launch_transpose_pad(w.mid, F, w.rpe, w.koff, w.roff, El, L.Kp, w.aT, st);
+        launch_transpose_pad(w.dz, H, w.rpe, w.koff, w.roff, El, L.Kp, w.dzT, st);
+        const size_t go = dist ? 0 : static_cast<size_t>(w.rank) * El * H * F;
+        launch_grouped_wgrad_bf16(w.xT, H, L.Kp, w.kpg, El, w.dHT, F, L.dw1 + go, st);
+        launch_grouped_wgrad_bf16(w.aT, F, L.Kp, w.kpg, El, w.dzT, H, L.dw2 + go, st);
+    }
+    for (int i = 0; i < L.nl; ++i) {  // B5 token-level: transposes shared by the gate and shared experts
+        Worker& w = L.workers[i];
+        launch_fill_i32(w.tk, 1, static_cast<int32_t>(S), st);
+        launch_pad_offsets(w.tk, 1, w.tk + 1, w.tk + 2, w.tk + 4, st);
+        launch_transpose_pad(xo(x, i), H, w.tk, w.tk + 2, w.tk + 4, 1, L.Sp, w.xTt, st);
+        if (L.Fs > 0) {
+            launch_grouped_gemm_bf16_mask(xo(dy, i), S, H, w.s_rows, 1, L.sw2r, L.Fs, w.dHs, w.smid, st);
+            launch_grouped_gemm_bf16(w.dHs, S, L.Fs, w.s_rows, 1, L.sw1r, H, w.dxs, 0, st);
+            launch_transpose_pad(w.dHs, L.Fs, w.tk, w.tk + 2, w.tk + 4, 1, L.Sp, w.dHsT, st);
+            launch_transpose_pad(w.smid, L.Fs, w.tk, w.tk + 2, w.tk + 4, 1, L.Sp, w.asT, st);
+            launch_transpose_pad(xo(dy, i), H, w.tk, w.tk + 2, w.tk + 4, 1, L.Sp, w.dyT, st);
+            launch_grouped_wgrad_bf16(w.xTt, H, L.Sp, w.tk + 1, 1, w.dHsT, L.Fs, L.dsw1, st);
+            launch_grouped_wgrad_bf16(w.asT, L.Fs, L.Sp, w.tk + 1, 1, w.dyT, H, L.dsw2, st);
+        }
+    }
+    if (dist) L.barrier(st);  // every owner wrote dL/dw and dxc
+    for (int i = 0; i < L.nl; ++i) {  // B5 gate, B6 dx
+        Worker& w = L.workers[i];
+        launch_gate_bwd(reinterpret_cast<const float*>(w.logits), w.slot_pos, w.expert_ids, w.slot_dw,
+                        static_cast<int>(S), E, k, w.dl, st);
+        launch_grouped_gemm_bf16(w.dl, S, E, w.s_rows, 1, L.gater, H, w.dxg, 0, st);
+        launch_transpose_pad(w.dl, E, w.tk, w.tk + 2, w.tk + 4, 1, L.Sp, w.dlT, st);
+        launch_grouped_wgrad_bf16(w.xTt, H, L.Sp, w.tk + 1, 1, w.dlT, E, L.dgate, st);
+        launch_combine_slots(w.bslot_src, nullptr, k, H, static_cast<int>(S), L.Fs > 0 ? w.dxs : nullptr,
+                             static_cast<char*>(dx) + static_cast<size_t>(i) * S * rb, st, 0, w.dxg);
+    }
+    (void)ctx;
+    (void)W;
 }
 
 // ---------------------------------------------------------------- SSMB

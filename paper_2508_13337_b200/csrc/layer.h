@@ -61,6 +61,33 @@ struct Worker {
     RbdDesc* desc_recv = nullptr; // [R_max]
     int32_t* gstart = nullptr;    // [W*S] first descriptor of each received group
     void* back_u = nullptr;       // [W*S, H] merged group outputs, read by the sources
+    // training (XMOE_LAYER_TRAIN): symmetric-region pieces
+    void* dyg = nullptr;          // [R_max, H] dy of each received copy (grouped order)
+    void* dxc = nullptr;          // [R_max, H] dx of each received copy
+    float* gw = nullptr;          // [R_max] combine weight of each received copy
+    unsigned long long* gsrc = nullptr;  // [R_max] home (rank << 32 | token*k + slot)
+    float* slot_dw = nullptr;     // [S*k] dL/dw of my copies (written by the owners)
+    // training: local
+    void* dz = nullptr;           // [R_max, H]
+    void* dH = nullptr;           // [R_max, F]
+    void* xT = nullptr;           // [H, Kp]   transposed, zero-padded per expert
+    void* dHT = nullptr;          // [F, Kp]
+    void* aT = nullptr;           // [F, Kp]
+    void* dzT = nullptr;          // [H, Kp]
+    int32_t* kpg = nullptr;       // [El] padded rows per expert
+    int32_t* koff = nullptr;      // [El+1]
+    int32_t* roff = nullptr;      // [El+1]
+    int32_t* tk = nullptr;        // token-level (one group of S rows): kpg, koff, roff
+    void* xTt = nullptr;          // [H, Sp]
+    void* dyT = nullptr;          // [H, Sp]
+    void* dlT = nullptr;          // [E, Sp]
+    void* dl = nullptr;           // [S, E]
+    void* dxg = nullptr;          // [S, H] gate part of dx
+    void* dHs = nullptr;          // [S, Fs]
+    void* dHsT = nullptr;         // [Fs, Sp]
+    void* asT = nullptr;          // [Fs, Sp]
+    void* dxs = nullptr;          // [S, H] shared part of dx
+    unsigned long long* bslot_src = nullptr;  // [S*k] dxc row of each kept copy
 };
 
 // stage boundaries; kEvCounts/kEvMoved/kEvReturn split the exchange phases
@@ -86,6 +113,24 @@ struct Layer {
     int32_t* tpe_all = nullptr;  // [W, E]
     char** recv_tab = nullptr;   // device table: rank -> recv buffer (shared-device ranks)
     char** eout_tab = nullptr;
+    // training tables and weights in the reference layouts (dgrad B operands)
+    bool train = false;
+    long long Kp = 0, Sp = 0, off_eout = 0, off_dxc = 0;
+    char** dyg_tab = nullptr;
+    char** dxc_tab = nullptr;
+    float** gw_tab = nullptr;
+    unsigned long long** gsrc_tab = nullptr;
+    float** slotdw_tab = nullptr;
+    void* w1r = nullptr;   // [E_held, H, F]
+    void* w2r = nullptr;   // [E_held, F, H]
+    void* gater = nullptr; // [H, E]
+    void* sw1r = nullptr;  // [H, Fs] merged
+    void* sw2r = nullptr;  // [Fs, H]
+    float* dgate = nullptr;
+    float* dw1 = nullptr;
+    float* dw2 = nullptr;
+    float* dsw1 = nullptr;
+    float* dsw2 = nullptr;
     char** recv_u_tab = nullptr;  // RBD tables (local or NVLink peer addresses)
     RbdDesc** desc_tab = nullptr;
     char** back_tab = nullptr;
@@ -112,6 +157,7 @@ struct Layer {
 void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const void* w1,
                   const void* w2, const void* sw1, const void* sw2, Layer& L);
 void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t st);
+void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* dx, cudaStream_t st);
 void ssmb_forward(Ctx& ctx, Layer& L, const void* x_full, long long S, void* out_full, cudaStream_t st);
 
 }  // namespace xmoe
