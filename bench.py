@@ -43,6 +43,7 @@ def parse():
     p.add_argument("--transport", default=None, choices=["p2p", "nccl"],
                    help="N>1 row transport: NVLink peer kernels (default) or NCCL send/recv baseline")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-backward", action="store_true", help="skip the fwd+bwd measurement")
     p.add_argument("--cpu-sample-tokens", type=int, default=512,
                    help="tokens per host thread for the cpu_baseline sample")
     return p.parse_args()
@@ -248,7 +249,7 @@ def main():
     mode = capi.RBD if args.mode == "rbd" else capi.NAIVE
     layer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
                        max_tokens=S, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,
-                       dispatch_mode=mode, seed=99)
+                       dispatch_mode=mode, seed=99, train=not args.no_backward)
     del w1, w2
     g.manual_seed(100 + rank)
     x = (torch.round((torch.rand(S, H, device="cuda", generator=g) * 2 - 1) * 128) / 128).to(torch.bfloat16)
@@ -289,6 +290,32 @@ def main():
     launches = capi.kernel_launches() - launches0
     ms = max_over_ranks(t0.elapsed_time(t1) / args.steps)
     clk = clocks.stop(world) if rank == 0 else None
+
+    # ---- forward + backward (gradients w.r.t. x and every weight), same clock rules
+    fwd_bwd = None
+    if not args.no_backward:
+        g.manual_seed(300 + rank)
+        dy = ((torch.rand(S, H, device="cuda", generator=g) * 2 - 1)).to(torch.bfloat16)
+        dxb = torch.empty_like(x)
+        for _ in range(max(2, args.warmup)):
+            layer.forward(x, out)
+            layer.backward(x, dy, dxb)
+        torch.cuda.synchronize()
+        barrier()
+        b0 = torch.cuda.Event(enable_timing=True)
+        b1 = torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(args.steps):
+            layer.forward(x, out)
+            layer.backward(x, dy, dxb)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        fb_ms = max_over_ranks(b0.elapsed_time(b1) / args.steps)
+        fwd_bwd = {"metric": "MoE-layer fwd+bwd tokens/s", "value": world * S / (fb_ms * 1e-3), "unit": UNIT,
+                   "ms_per_step": fb_ms,
+                   "note": "forward + backward (dx and fp32 grads of gate, experts, shared experts); "
+                           "gradients restated beyond the forward-only reference, checked against fp64 autograd"}
 
     # ---- per-stage breakdown + roofline of the dominant kernel (grouped GEMM)
     layer.set_timing(True)
@@ -410,6 +437,7 @@ def main():
                             "combine_frac": comb_bytes / (stages["combine_kernel"] * 1e-3) / 1e9 / hbm
                             if world == 1 and stages.get("combine_kernel") else None},
             "ledger": led,
+            "fwd_bwd": fwd_bwd,
             "gpu_launches": launches,
             "clocks": clk,
             "cpu_baseline": cpu,
