@@ -272,6 +272,12 @@ int xmoe_grouped_wgrad_bf16(xmoe_ctx* ctx, const void* X, const void* Y, int64_t
                              void* stream) {
     return guarded([&] {
         auto st = static_cast<cudaStream_t>(stream);
+        if (M % 64 == 0 && N % 128 == 0) {  // MN-major kernel on the row-major operands
+            char* ws = static_cast<char*>(ctx->c.scratch(2 * 64 * G * (M + N) + 1024));
+            launch_grouped_wgrad_mn(X, static_cast<int>(M), Y, static_cast<int>(N), rows, rows_per_group,
+                                    static_cast<int>(G), ws, ws + 2 * 64 * G * M, D, st);
+            return;
+        }
         const long long Kp = (rows + 64 * G + 63) / 64 * 64;
         char* ws = static_cast<char*>(ctx->c.scratch(2 * (M + N) * Kp + 4096 + 12 * (G + 2)));
         int32_t* kpg = reinterpret_cast<int32_t*>(ws);

@@ -734,6 +734,244 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Weight-gradient GEMM with MN-major operands, straight on the grouped
+// activations (no transposes):  D_g[M, N] = sum_{r in group g} A[r, :]^T B[r, :]
+// A [rows, M], B [rows, N] row-major bf16 (M, N contiguous).  Each K block is
+// 64 rows; a group's last partial block comes from zero-padded tail copies
+// (at_tail/bt_tail: [G*64, M|N]) so other groups' rows never leak in.
+// smem per CTA and stage: two 64(MN) x 64(K) boxes of A and of B, 128B
+// swizzle; UMMA descriptors: LBO = 8 KB (next 64-wide MN atom), SBO = 1 KB
+// (next 8 K-rows), K advances 2 KB per 16-row MMA; a_major = b_major = MN.
+__device__ __forceinline__ uint64_t make_desc_mn(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(8192 >> 4) << 16;  // LBO: MN atom stride
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;  // SBO: 8-row K group stride
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+__device__ __forceinline__ uint32_t make_idesc2_mn(int n) { return make_idesc2(n) | (1u << 15) | (1u << 16); }
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    grouped_wgrad_mn_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                            const __grid_constant__ CUtensorMap tmap_at, const __grid_constant__ CUtensorMap tmap_bt,
+                            const int32_t* __restrict__ group_rows, int G, int M, int N, float* __restrict__ D) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* smem_a = smem;
+    uint8_t* smem_b = smem + kStages * kABytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* full_bar = bars;
+    uint64_t* empty_bar = bars + kStages;
+    uint64_t* tfull_bar = bars + 2 * kStages;
+    uint64_t* tempty_bar = bars + 2 * kStages + kAccBufs;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * kAccBufs);
+    int32_t* tile_start = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 1024);
+    int32_t* roff = tile_start + kMaxGroups + 1;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cta_rank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1;
+    const int npairs = gridDim.x >> 1;
+    const int ntn = (N + BN - 1) / BN;
+    const int ntm = (M + BM - 1) / BM;
+
+    if (threadIdx.x == 0) {
+        int r = 0;
+        for (int g = 0; g < G; ++g) {
+            tile_start[g] = g * ntm * ntn;
+            roff[g] = r;
+            r += group_rows[g];
+        }
+        tile_start[G] = G * ntm * ntn;
+        roff[G] = r;
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full_bar[s], 2);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int b = 0; b < kAccBufs; ++b) {
+            mbar_init(&tfull_bar[b], 1);
+            mbar_init(&tempty_bar[b], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmap_a);
+        prefetch_tmap(&tmap_b);
+        prefetch_tmap(&tmap_at);
+        prefetch_tmap(&tmap_bt);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int num_tiles = tile_start[G];
+    auto info = [&](int t, int& g, int& row0, int& n0, int& nkb, int& rows_g) {
+        g = t / (ntm * ntn);
+        const int local = t - g * ntm * ntn;
+        row0 = (local / ntn) * BM;
+        n0 = (local % ntn) * BN;
+        rows_g = roff[g + 1] - roff[g];
+        nkb = (rows_g + BK - 1) / BK;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = pair; t < num_tiles; t += npairs) {
+                int g, row0, n0, nkb, rows_g;
+                info(t, g, row0, n0, nkb, rows_g);
+                const int nw = min(BN, N - n0);
+                const int n_mma = (nw + 15) & ~15;
+                const int am = row0 + BMC * static_cast<int>(rank);
+                const int bn = n0 + (n_mma / 2) * static_cast<int>(rank);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&empty_bar[stage], phase ^ 1);
+                    const uint32_t fb = mapa(&full_bar[stage], 0);
+                    expect_tx_cluster(fb, kStageBytes);
+                    const bool tail = (kb + 1) * BK > rows_g;
+                    const CUtensorMap* ma = tail ? &tmap_at : &tmap_a;
+                    const CUtensorMap* mb = tail ? &tmap_bt : &tmap_b;
+                    const int kr = tail ? g * BK : roff[g] + kb * BK;
+                    uint8_t* sa = smem_a + stage * kABytes;
+                    uint8_t* sb = smem_b + stage * kBBytes;
+                    tma_load_2sm(ma, fb, sa, am, kr);
+                    tma_load_2sm(ma, fb, sa + 8192, am + 64, kr);
+                    tma_load_2sm(mb, fb, sb, bn, kr);
+                    tma_load_2sm(mb, fb, sb + 8192, bn + 64, kr);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = pair; t < num_tiles; t += npairs) {
+                int g, row0, n0, nkb, rows_g;
+                info(t, g, row0, n0, nkb, rows_g);
+                if (nkb == 0) continue;
+                const int nw = min(BN, N - n0);
+                const int n_mma = (nw + 15) & ~15;
+                const uint32_t idesc = make_idesc2_mn(n_mma);
+                const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
+                mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+                tc_fence_after();
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&full_bar[stage], phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint64_t da = make_desc_mn(smem_u32(smem_a + stage * kABytes));
+                        const uint64_t db = make_desc_mn(smem_u32(smem_b + stage * kBBytes));
+#pragma unroll
+                        for (int kk = 0; kk < BK / UK; ++kk)  // 16 K-rows = 2 KB
+                            mma2(tmem_d, da + static_cast<uint64_t>(kk * 128), db + static_cast<uint64_t>(kk * 128),
+                                 idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+                        commit_both(&empty_bar[stage]);
+                        if (kb == nkb - 1) commit_both(&tfull_bar[acc]);
+                    }
+                    __syncwarp();
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                if (++acc == kAccBufs) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else {
+        const int quarter = warp & 3;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = pair; t < num_tiles; t += npairs) {
+            int g, row0, n0, nkb, rows_g;
+            info(t, g, row0, n0, nkb, rows_g);
+            const int nw = min(BN, N - n0);
+            const int r = BMC * static_cast<int>(rank) + quarter * 32 + lane;
+            const bool row_ok = row0 + r < M;
+            float* drow = D + static_cast<size_t>(g) * M * N + static_cast<size_t>(row0 + r) * N + n0;
+            if (nkb == 0) {
+                if (row_ok)
+                    for (int c = 0; c < nw; ++c) drow[c] = 0.f;
+                continue;
+            }
+            mbar_wait(&tfull_bar[acc], acc_phase);
+            tc_fence_after();
+            for (int c0 = 0; c0 < nw; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN + c0),
+                          v);
+                if (!row_ok) continue;
+                const int cn = min(32, nw - c0);
+                if (cn == 32 && (N & 3) == 0) {
+                    float4* dst = reinterpret_cast<float4*>(drow + c0);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                             __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+                } else {
+                    for (int i = 0; i < cn; ++i) drow[c0 + i] = __uint_as_float(v[i]);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_cluster(mapa(&tempty_bar[acc], 0));
+            if (++acc == kAccBufs) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    if (warp == 1) {
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
+                     : "memory");
+    }
+}
+
+// Tail staging: the last (rows_g mod 64) rows of every group, zero-padded to
+// 64 rows, for A [rows, C] -> tail [G*64, C].
+__global__ void wgrad_tail_kernel(const __nv_bfloat16* __restrict__ X, int C, const int32_t* __restrict__ group_rows,
+                                  int G, __nv_bfloat16* __restrict__ tail) {
+    const int g = blockIdx.x;
+    if (g >= G) return;
+    int r0 = 0;
+    for (int q = 0; q < g; ++q) r0 += group_rows[q];
+    const int rows = group_rows[g];
+    const int rem = rows & 63;
+    const int full = rows - rem;
+    for (int i = threadIdx.x; i < 64 * C; i += blockDim.x) {
+        const int rr = i / C, c = i % C;
+        tail[(static_cast<size_t>(g) * 64 + rr) * C + c] =
+            rr < rem ? X[static_cast<size_t>(r0 + full + rr) * C + c] : __float2bfloat16_rn(0.f);
+    }
+}
+
 }  // namespace tc2
 
 // ---------------------------------------------------------------- host side
@@ -870,6 +1108,38 @@ void launch_grouped_wgrad_bf16(const void* A, int M, long long Ktot, const int32
     require(Ktot % 64 == 0, XMOE_ERR_VALIDATION, "wgrad: K segments must be padded to 64");
     const long long bound = static_cast<long long>(G) * ((M + tc2::BM - 1) / tc2::BM) * ((N + tc2::BN - 1) / tc2::BN);
     launch_tc2<float, true>(A, M, Ktot, k_per_group, G, B, N, M, N, 0, D, 0, nullptr, bound, st);
+}
+
+// MN-major grouped weight gradient straight on the grouped activations.
+void launch_grouped_wgrad_mn(const void* A, int M, const void* B, int N, long long rows,
+                             const int32_t* group_rows, int G, void* tail_a, void* tail_b, float* D,
+                             cudaStream_t st) {
+    require(G >= 1 && G <= tc2::kMaxGroups, XMOE_ERR_VALIDATION, "wgrad: 1 <= groups <= 1024");
+    require(M % 64 == 0 && N % 128 == 0, XMOE_ERR_VALIDATION, "wgrad (MN-major) needs M % 64 == 0, N % 128 == 0");
+    tc2::wgrad_tail_kernel<<<G, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(A), M, group_rows, G,
+                                              static_cast<__nv_bfloat16*>(tail_a));
+    XMOE_LAUNCH_CHECK();
+    tc2::wgrad_tail_kernel<<<G, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(B), N, group_rows, G,
+                                              static_cast<__nv_bfloat16*>(tail_b));
+    XMOE_LAUNCH_CHECK();
+    const long long r = rows > 0 ? rows : 1;
+    const CUtensorMap ta = make_tmap(A, r, M, 64);
+    const CUtensorMap tb = make_tmap(B, r, N, 64);
+    const CUtensorMap tat = make_tmap(tail_a, 64LL * G, M, 64);
+    const CUtensorMap tbt = make_tmap(tail_b, 64LL * G, N, 64);
+    static bool attr_set = false;
+    if (!attr_set) {
+        XMOE_CUDA(cudaFuncSetAttribute(tc2::grouped_wgrad_mn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(tc2::kSmemBytes)));
+        attr_set = true;
+    }
+    int sms = 0;
+    XMOE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const long long tiles = static_cast<long long>(G) * ((M + tc2::BM - 1) / tc2::BM) * ((N + tc2::BN - 1) / tc2::BN);
+    const long long pairs = tiles < sms / 2 ? tiles : sms / 2;
+    tc2::grouped_wgrad_mn_kernel<<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
+        ta, tb, tat, tbt, group_rows, G, M, N, D);
+    XMOE_LAUNCH_CHECK();
 }
 
 void launch_grouped_gemm_bf16_f32out(const void* A, long long rows, int K,

@@ -177,8 +177,8 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     L.train = (d.flags & XMOE_LAYER_TRAIN) != 0;
     require(!L.train || (bf && !d.renorm && (!L.distributed || L.p2p) && L.nl == 1), XMOE_ERR_VALIDATION,
             "training layers need bf16, no renorm, one rank per process (or world 1) and the NVLink peer transport");
-    require(!L.train || (H % 32 == 0 && F % 32 == 0 && E % 32 == 0 && L.Fs % 32 == 0), XMOE_ERR_VALIDATION,
-            "training layers need model_dim, ffn_dim, num_experts and shared width multiples of 32");
+    require(!L.train || (H % 128 == 0 && F % 128 == 0 && E % 32 == 0 && L.Fs % 128 == 0), XMOE_ERR_VALIDATION,
+            "training layers need model_dim, ffn_dim and shared width multiples of 128, num_experts of 32");
     const size_t off_dyg = off_train;
     const size_t off_dxc = off_dyg + (L.train ? up(static_cast<size_t>(L.R_max) * H * es) : 0);
     const size_t off_gw = off_dxc + (L.train ? up(static_cast<size_t>(L.R_max) * H * es) : 0);
@@ -262,23 +262,20 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
             w.slot_dw = reinterpret_cast<float*>(w.sym + off_sdw);
             w.dz = L.alloc(static_cast<size_t>(L.R_max) * H * es);
             w.dH = L.alloc(static_cast<size_t>(L.R_max) * F * es);
-            w.xT = L.alloc(static_cast<size_t>(H) * L.Kp * es);
-            w.dHT = L.alloc(static_cast<size_t>(F) * L.Kp * es);
-            w.aT = L.alloc(static_cast<size_t>(F) * L.Kp * es);
-            w.dzT = L.alloc(static_cast<size_t>(H) * L.Kp * es);
+            const size_t wide = std::max<size_t>({static_cast<size_t>(H), static_cast<size_t>(F),
+                                                  static_cast<size_t>(Fs)});
+            w.tail_a = L.alloc(64 * static_cast<size_t>(L.El + 1) * wide * es);
+            w.tail_b = L.alloc(64 * static_cast<size_t>(L.El + 1) * wide * es);
             w.kpg = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
             w.koff = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
             w.roff = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
             w.tk = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * 8));
             w.xTt = L.alloc(static_cast<size_t>(H) * L.Sp * es);
-            w.dyT = L.alloc(static_cast<size_t>(H) * L.Sp * es);
             w.dlT = L.alloc(static_cast<size_t>(E) * L.Sp * es);
             w.dl = L.alloc(static_cast<size_t>(S) * E * es);
             w.dxg = L.alloc(static_cast<size_t>(S) * H * es);
             if (Fs > 0) {
                 w.dHs = L.alloc(static_cast<size_t>(S) * Fs * es);
-                w.dHsT = L.alloc(static_cast<size_t>(Fs) * L.Sp * es);
-                w.asT = L.alloc(static_cast<size_t>(Fs) * L.Sp * es);
                 w.dxs = L.alloc(static_cast<size_t>(S) * H * es);
             }
             w.bslot_src = static_cast<unsigned long long*>(L.alloc(sizeof(unsigned long long) * nk));
@@ -606,7 +603,8 @@ void Layer::exchange_nccl(bool forward, cudaStream_t st) {
 //      home slot recorded at the owner
 //   B2 owner: dL/dw_c = <dy_t, y_c> back to the home slot; dz = w_c dy_t
 //   B3 dgrad: dH = (dz W2^T) * [mid > 0];  dxc = dH W1^T      (grouped-M)
-//   B4 wgrad: dW1_e = x_e^T dH_e, dW2_e = a_e^T dz_e          (grouped-K)
+//   B4 wgrad: dW1_e = x_e^T dH_e, dW2_e = a_e^T dz_e   (grouped-K, MN-major
+//      operands read straight from the grouped buffers)
 //   B5 shared experts (dense) and the gate: dl = softmax Jacobian of dL/dw,
 //      dx_gate = dl Wg^T, dWg = x^T dl
 //   B6 dx_t = sum of its copies' dxc rows (read from the owners) + shared
@@ -633,14 +631,10 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
         launch_grouped_gemm_bf16_mask(w.dz, L.R_max, H, w.rpe, El, static_cast<const char*>(L.w2r) + eo, F, w.dH,
                                       w.mid, st);
         launch_grouped_gemm_bf16(w.dH, L.R_max, F, w.rpe, El, static_cast<const char*>(L.w1r) + eo, H, w.dxc, 0, st);
-        launch_pad_offsets(w.rpe, El, w.kpg, w.koff, w.roff, st);
-        launch_transpose_pad(w.recv, H, w.rpe, w.koff, w.roff, El, L.Kp, w.xT, st);
-        launch_transpose_pad(w.dH, F, w.rpe, w.koff, w.roff, El, L.Kp, w.dHT, st);
-        launch_transpose_pad(w.mid, F, w.rpe, w.koff, w.roff, El, L.Kp, w.aT, st);
-        launch_transpose_pad(w.dz, H, w.rpe, w.koff, w.roff, El, L.Kp, w.dzT, st);
+        // wgrad straight on the grouped activations (MN-major tcgen05 operands)
         const size_t go = dist ? 0 : static_cast<size_t>(w.rank) * El * H * F;
-        launch_grouped_wgrad_bf16(w.xT, H, L.Kp, w.kpg, El, w.dHT, F, L.dw1 + go, st);
-        launch_grouped_wgrad_bf16(w.aT, F, L.Kp, w.kpg, El, w.dzT, H, L.dw2 + go, st);
+        launch_grouped_wgrad_mn(w.recv, H, w.dH, F, L.R_max, w.rpe, El, w.tail_a, w.tail_b, L.dw1 + go, st);
+        launch_grouped_wgrad_mn(w.mid, F, w.dz, H, L.R_max, w.rpe, El, w.tail_a, w.tail_b, L.dw2 + go, st);
     }
     for (int i = 0; i < L.nl; ++i) {  // B5 token-level: transposes shared by the gate and shared experts
         Worker& w = L.workers[i];
@@ -650,11 +644,8 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
         if (L.Fs > 0) {
             launch_grouped_gemm_bf16_mask(xo(dy, i), S, H, w.s_rows, 1, L.sw2r, L.Fs, w.dHs, w.smid, st);
             launch_grouped_gemm_bf16(w.dHs, S, L.Fs, w.s_rows, 1, L.sw1r, H, w.dxs, 0, st);
-            launch_transpose_pad(w.dHs, L.Fs, w.tk, w.tk + 2, w.tk + 4, 1, L.Sp, w.dHsT, st);
-            launch_transpose_pad(w.smid, L.Fs, w.tk, w.tk + 2, w.tk + 4, 1, L.Sp, w.asT, st);
-            launch_transpose_pad(xo(dy, i), H, w.tk, w.tk + 2, w.tk + 4, 1, L.Sp, w.dyT, st);
-            launch_grouped_wgrad_bf16(w.xTt, H, L.Sp, w.tk + 1, 1, w.dHsT, L.Fs, L.dsw1, st);
-            launch_grouped_wgrad_bf16(w.asT, L.Fs, L.Sp, w.tk + 1, 1, w.dyT, H, L.dsw2, st);
+            launch_grouped_wgrad_mn(xo(x, i), H, w.dHs, L.Fs, S, w.tk, 1, w.tail_a, w.tail_b, L.dsw1, st);
+            launch_grouped_wgrad_mn(w.smid, L.Fs, xo(dy, i), H, S, w.tk, 1, w.tail_a, w.tail_b, L.dsw2, st);
         }
     }
     if (dist) L.barrier(st);  // every owner wrote dL/dw and dxc

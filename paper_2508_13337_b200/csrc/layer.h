@@ -70,22 +70,17 @@ struct Worker {
     // training: local
     void* dz = nullptr;           // [R_max, H]
     void* dH = nullptr;           // [R_max, F]
-    void* xT = nullptr;           // [H, Kp]   transposed, zero-padded per expert
-    void* dHT = nullptr;          // [F, Kp]
-    void* aT = nullptr;           // [F, Kp]
-    void* dzT = nullptr;          // [H, Kp]
+    void* tail_a = nullptr;       // wgrad tail blocks [64*(El+1), max(H,F,Fs)]
+    void* tail_b = nullptr;
     int32_t* kpg = nullptr;       // [El] padded rows per expert
     int32_t* koff = nullptr;      // [El+1]
     int32_t* roff = nullptr;      // [El+1]
     int32_t* tk = nullptr;        // token-level (one group of S rows): kpg, koff, roff
     void* xTt = nullptr;          // [H, Sp]
-    void* dyT = nullptr;          // [H, Sp]
     void* dlT = nullptr;          // [E, Sp]
     void* dl = nullptr;           // [S, E]
     void* dxg = nullptr;          // [S, H] gate part of dx
     void* dHs = nullptr;          // [S, Fs]
-    void* dHsT = nullptr;         // [Fs, Sp]
-    void* asT = nullptr;          // [Fs, Sp]
     void* dxs = nullptr;          // [S, H] shared part of dx
     unsigned long long* bslot_src = nullptr;  // [S*k] dxc row of each kept copy
 };

@@ -88,7 +88,7 @@ def main():
     # backward over the peer transport (bf16, dropless): dx per rank, expert
     # grads of each rank's block, gate grads summed over ranks
     from oracle import moe_grad as Gr
-    S, E, k, H, F = 256, 16 * world, 4, 128, 64
+    S, E, k, H, F = 256, 16 * world, 4, 128, 128
     el = E // world
     rng = np.random.default_rng(55)
     gate = grid_gate(rng, H, E)

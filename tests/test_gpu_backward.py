@@ -13,9 +13,9 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("S,E,k,H,F,shared,cap_factor,mode", [
-    (256, 32, 4, 128, 64, False, None, 0),
+    (256, 32, 4, 128, 128, False, None, 0),
     (512, 64, 6, 256, 128, True, None, 0),
-    (384, 32, 6, 128, 96, True, 1.0, 0),
+    (384, 32, 6, 128, 256, True, 1.0, 0),
     (512, 64, 6, 256, 128, True, None, 1),
 ])
 def test_backward_bf16_vs_autograd(S, E, k, H, F, shared, cap_factor, mode):
@@ -50,14 +50,15 @@ def test_backward_bf16_vs_autograd(S, E, k, H, F, shared, cap_factor, mode):
         assert norm_rel(host(gr["sw2"]), w2c) < 3e-2
 
 
-def test_grouped_wgrad_kernel():
-    """Grouped-K tcgen05 GEMM: D_g = A[:, Kg] B[:, Kg]^T over zero-padded,
-    transposed segments, including an empty group."""
+@pytest.mark.parametrize("H,F", [(256, 128), (128, 96), (2048, 1408)])
+def test_grouped_wgrad_kernel(H, F):
+    """Weight-gradient GEMMs D_g = X_g^T Y_g: MN-major tcgen05 operands with
+    zero-padded tail blocks (F % 128 == 0) or the K-major kernel over
+    transposed, padded segments — including an empty group."""
     from paper_2508_13337_b200 import capi
     ctx = capi.Context(0, 1, 0)
     torch.manual_seed(0)
-    rows = [300, 0, 64, 1000]
-    H, F = 256, 128
+    rows = [300, 0, 64, 1000, 63]
     x = (torch.randn(sum(rows), H, device="cuda") * 0.5).to(torch.bfloat16)
     dh = (torch.randn(sum(rows), F, device="cuda") * 0.5).to(torch.bfloat16)
     out = capi.grouped_wgrad_test(ctx, x, dh, rows)
