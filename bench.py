@@ -38,7 +38,8 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="xmoe", choices=["xmoe", "reference"])
-    p.add_argument("--mode", default="naive", choices=["rbd", "naive"])
+    p.add_argument("--mode", default="auto", choices=["auto", "rbd", "naive"],
+                   help="dispatch: auto = plain at N=1, redundancy bypass at N>1")
     p.add_argument("--tokens", type=int, default=C2["S"])
     p.add_argument("--transport", default=None, choices=["p2p", "nccl"],
                    help="N>1 row transport: NVLink peer kernels (default) or NCCL send/recv baseline")
@@ -246,6 +247,8 @@ def main():
     g.manual_seed(777)
     sw1 = ((torch.rand(ns, H, Fs, device="cuda", generator=g) * 0.2 - 0.1)).to(torch.bfloat16)
     sw2 = ((torch.rand(ns, Fs, H, device="cuda", generator=g) * 0.2 - 0.1)).to(torch.bfloat16)
+    if args.mode == "auto":
+        args.mode = "rbd" if world > 1 else "naive"
     mode = capi.RBD if args.mode == "rbd" else capi.NAIVE
     layer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
                        max_tokens=S, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,

@@ -955,20 +955,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 // Tail staging: the last (rows_g mod 64) rows of every group, zero-padded to
-// 64 rows, for A [rows, C] -> tail [G*64, C].
+// 64 rows, for A [rows, C] -> tail [G*64, C].  One block per (group, row),
+// 16-byte vectors (C % 8 == 0).
 __global__ void wgrad_tail_kernel(const __nv_bfloat16* __restrict__ X, int C, const int32_t* __restrict__ group_rows,
                                   int G, __nv_bfloat16* __restrict__ tail) {
-    const int g = blockIdx.x;
-    if (g >= G) return;
-    int r0 = 0;
-    for (int q = 0; q < g; ++q) r0 += group_rows[q];
-    const int rows = group_rows[g];
-    const int rem = rows & 63;
-    const int full = rows - rem;
-    for (int i = threadIdx.x; i < 64 * C; i += blockDim.x) {
-        const int rr = i / C, c = i % C;
-        tail[(static_cast<size_t>(g) * 64 + rr) * C + c] =
-            rr < rem ? X[static_cast<size_t>(r0 + full + rr) * C + c] : __float2bfloat16_rn(0.f);
+    const int g = blockIdx.x, rr = blockIdx.y;
+    __shared__ int s_r0, s_rows;
+    if (threadIdx.x == 0) {
+        int r0 = 0;
+        for (int q = 0; q < g; ++q) r0 += group_rows[q];
+        s_r0 = r0;
+        s_rows = group_rows[g];
+    }
+    __syncthreads();
+    const int rem = s_rows & 63;
+    int4* dst = reinterpret_cast<int4*>(tail + (static_cast<size_t>(g) * 64 + rr) * C);
+    const int nv = C >> 3;
+    if (rr < rem) {
+        const int4* src = reinterpret_cast<const int4*>(X + static_cast<size_t>(s_r0 + s_rows - rem + rr) * C);
+        for (int v = threadIdx.x; v < nv; v += blockDim.x) dst[v] = src[v];
+    } else {
+        for (int v = threadIdx.x; v < nv; v += blockDim.x) dst[v] = make_int4(0, 0, 0, 0);
     }
 }
 
@@ -1116,11 +1123,11 @@ void launch_grouped_wgrad_mn(const void* A, int M, const void* B, int N, long lo
                              cudaStream_t st) {
     require(G >= 1 && G <= tc2::kMaxGroups, XMOE_ERR_VALIDATION, "wgrad: 1 <= groups <= 1024");
     require(M % 64 == 0 && N % 128 == 0, XMOE_ERR_VALIDATION, "wgrad (MN-major) needs M % 64 == 0, N % 128 == 0");
-    tc2::wgrad_tail_kernel<<<G, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(A), M, group_rows, G,
-                                              static_cast<__nv_bfloat16*>(tail_a));
+    tc2::wgrad_tail_kernel<<<dim3(G, 64), 128, 0, st>>>(static_cast<const __nv_bfloat16*>(A), M, group_rows, G,
+                                                        static_cast<__nv_bfloat16*>(tail_a));
     XMOE_LAUNCH_CHECK();
-    tc2::wgrad_tail_kernel<<<G, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(B), N, group_rows, G,
-                                              static_cast<__nv_bfloat16*>(tail_b));
+    tc2::wgrad_tail_kernel<<<dim3(G, 64), 128, 0, st>>>(static_cast<const __nv_bfloat16*>(B), N, group_rows, G,
+                                                        static_cast<__nv_bfloat16*>(tail_b));
     XMOE_LAUNCH_CHECK();
     const long long r = rows > 0 ? rows : 1;
     const CUtensorMap ta = make_tmap(A, r, M, 64);
