@@ -28,6 +28,11 @@
 #include "kernels.cuh"
 
 namespace xmoe {
+
+// SM budget of the next 2-CTA GEMM launches (0 = all SMs); the layer lowers it
+// for GEMMs that run on a side stream next to bandwidth-bound kernels.
+thread_local int g_gemm_sm_limit = 0;
+
 namespace tc {
 
 constexpr int BM = 128;
@@ -1067,7 +1072,9 @@ static void launch_tc2(const void* A, long long a_rows, long long a_cols, const 
     }
     int sms = 0;
     XMOE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-    const long long pairs = tile_bound < sms / 2 ? tile_bound : sms / 2;
+    long long cap_pairs = sms / 2;
+    if (g_gemm_sm_limit > 0 && g_gemm_sm_limit / 2 < cap_pairs) cap_pairs = g_gemm_sm_limit / 2;
+    const long long pairs = tile_bound < cap_pairs ? tile_bound : cap_pairs;
     tc2::grouped_gemm_tc2_kernel<OutT, kVarK><<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
         ta, tb, group_sizes, G, M, N, K, D, relu, mask);
     XMOE_LAUNCH_CHECK();

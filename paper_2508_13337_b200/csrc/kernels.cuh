@@ -92,6 +92,9 @@ void launch_transpose_pad(const void* in, int C, const int32_t* rows, const int3
 void launch_gate_bwd(const float* logits, const int32_t* slot_pos, const int32_t* expert_ids, const float* slot_dw,
                      int S, int E, int k, void* dl, cudaStream_t st);
 
+// gemm_tc.cu: SM budget of subsequent 2-CTA GEMM launches on this thread (0 = all)
+extern thread_local int g_gemm_sm_limit;
+
 // misc.cu
 void launch_recv_counts(const int32_t* tpe_all, int W, int E, int dst, int32_t* rpe,
                         cudaStream_t st);

@@ -171,7 +171,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     const size_t off_recv = 0;
     const size_t off_eout = off_recv + up(static_cast<size_t>(L.R_max) * H * es);
     const size_t off_recv_u = off_eout + up(static_cast<size_t>(L.R_max) * H * es);
-    const size_t off_desc = off_recv_u + (rbd ? up(static_cast<size_t>(rmax) * H * es) : 0);
+    const size_t off_desc = off_recv_u;  // RBD rows land in place (pilot slot): no unique-row buffer
     const size_t off_back = off_desc + (rbd ? up(sizeof(RbdDesc) * L.R_max) : 0);
     const size_t off_train = off_back + (rbd ? up(static_cast<size_t>(rmax) * H * es) : 0);
     L.train = (d.flags & XMOE_LAYER_TRAIN) != 0;
@@ -441,11 +441,19 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         XMOE_CUDA(cudaEventRecord(L.ev_fork, st));
         XMOE_CUDA(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
         if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side0, L.side));
+        // leave SMs to the routing / exchange kernels running beside it
+        // (multi-GPU only: at N=1 there is no exchange to overlap)
+        static const int shared_sms = [] {
+            const char* e = std::getenv("XMOE_SHARED_SMS");
+            return e ? std::atoi(e) : 104;
+        }();
+        g_gemm_sm_limit = dist ? shared_sms : 0;
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             run_gemm(dt, x_of(i), S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, L.side);
             run_gemm(dt, w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, w.sout, 0, L.side);
         }
+        g_gemm_sm_limit = 0;
         if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side1, L.side));
         XMOE_CUDA(cudaEventRecord(L.ev_join, L.side));
     }
@@ -486,7 +494,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
             Worker& w = L.workers[i];
             launch_rbd_offsets(L.G_all, L.tpe_all, W, E, w.rank, w.rbd, st);
             launch_rbd_pack(x_of(i), static_cast<int>(row_bytes), w.rbd, nk, w.slot_pos, k, w.dest_row, w.cw,
-                            L.recv_u_tab, L.desc_tab, st);
+                            L.recv_tab, L.desc_tab, st);
         }
         L.mark(kEvMoved, st);
         if (dist) L.barrier(st);

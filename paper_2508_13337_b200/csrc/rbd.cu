@@ -349,8 +349,10 @@ __global__ void __launch_bounds__(256) rbd_pack_kernel(
             dd.member = lane | (p == pilot ? kRbdPilotFlag : 0);
             desc_tab[d][rd_base[d] + (coff[pos] - cseg[d]) + lane] = dd;
         }
+        // the row lands once, at the pilot's slot of the receiver's grouped
+        // expert input; the receiver copies it to the replicas' slots
         const char* src = x + static_cast<size_t>(t) * row_bytes;
-        char* dst = recv_u_tab[d] + static_cast<size_t>(u) * row_bytes;
+        char* dst = recv_u_tab[d] + static_cast<size_t>(dest_row[pilot]) * row_bytes;
         if ((row_bytes & 15) == 0) {
             const int4* s4 = reinterpret_cast<const int4*>(src);
             int4* d4 = reinterpret_cast<int4*>(dst);
@@ -363,24 +365,33 @@ __global__ void __launch_bounds__(256) rbd_pack_kernel(
     __threadfence_system();
 }
 
-// Receiver expand: grouped[dest_row] = recv_u[u] for every received copy;
-// also records each group's first descriptor for the merge.
+// Receiver expand: every replica copies its group's row from the pilot's
+// slot (where the sender put it) into its own grouped slot; records each
+// group's first descriptor for the merge.
 __global__ void __launch_bounds__(256) rbd_expand_kernel(const char* __restrict__ recv_u,
                                                          int row_bytes, const RbdDesc* __restrict__ desc,
                                                          const int32_t* __restrict__ rx, char* __restrict__ grouped,
                                                          int32_t* __restrict__ gstart) {
+    (void)recv_u;
     const int ndesc = rx[1];
     const int lane = threadIdx.x & 31;
     const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
     for (long long c = warp; c < ndesc; c += nwarps) {
         const RbdDesc dd = desc[c];
-        if (lane == 0 && (dd.member & ~kRbdPilotFlag) == 0) gstart[dd.u] = static_cast<int>(c);
-        const char* s = recv_u + static_cast<size_t>(dd.u) * row_bytes;
+        const int m = dd.member & ~kRbdPilotFlag;
+        if (lane == 0 && m == 0) gstart[dd.u] = static_cast<int>(c);
+        if (dd.member & kRbdPilotFlag) continue;  // already in place
+        int prow = dd.dest_row;
+        for (int q = 0; q < dd.n; ++q) {
+            const RbdDesc pq = desc[c - m + q];
+            if (pq.member & kRbdPilotFlag) prow = pq.dest_row;
+        }
+        const char* s = grouped + static_cast<size_t>(prow) * row_bytes;
         char* o = grouped + static_cast<size_t>(dd.dest_row) * row_bytes;
         if ((row_bytes & 15) == 0) {
             for (int v = lane; v < (row_bytes >> 4); v += 32)
-                st_na_v4(reinterpret_cast<int4*>(o) + v, ld_nc_v4(reinterpret_cast<const int4*>(s) + v));
+                st_na_v4(reinterpret_cast<int4*>(o) + v, reinterpret_cast<const int4*>(s)[v]);
         } else {
             for (int v = lane; v < (row_bytes >> 3); v += 32)
                 reinterpret_cast<long long*>(o)[v] = reinterpret_cast<const long long*>(s)[v];
