@@ -45,6 +45,7 @@ def parse():
                    help="N>1 row transport: NVLink peer kernels (default) or NCCL send/recv baseline")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-backward", action="store_true", help="skip the fwd+bwd measurement")
+    p.add_argument("--no-graph", action="store_true", help="launch the forward kernels one by one")
     p.add_argument("--cpu-sample-tokens", type=int, default=512,
                    help="tokens per host thread for the cpu_baseline sample")
     return p.parse_args()
@@ -254,6 +255,8 @@ def main():
                        max_tokens=S, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,
                        dispatch_mode=mode, seed=99, train=not args.no_backward)
     del w1, w2
+    if not args.no_graph:
+        layer.set_graph(True)
     g.manual_seed(100 + rank)
     x = (torch.round((torch.rand(S, H, device="cuda", generator=g) * 2 - 1) * 128) / 128).to(torch.bfloat16)
     out = torch.empty_like(x)

@@ -214,6 +214,9 @@ int xmoe_layer_ledger(xmoe_layer* layer, uint64_t* out, int n);
  * and the exchange ("shared" above is only the wait for them).
  * Requires timing enabled. */
 int xmoe_layer_set_timing(xmoe_layer* layer, int enable);
+/* Capture the forward as a CUDA graph per (x, out, S) and replay it (the
+ * forward has no host synchronisation on the local and NVLink transports). */
+int xmoe_layer_set_graph(xmoe_layer* layer, int enable);
 int xmoe_layer_stage_ms(xmoe_layer* layer, float* out, int n);
 
 #ifdef __cplusplus

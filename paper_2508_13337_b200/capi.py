@@ -78,6 +78,7 @@ def lib():
         L.xmoe_ssmb_forward.argtypes = [p, p, p, i64, p, p]
         L.xmoe_layer_ledger.argtypes = [p, C.POINTER(C.c_uint64), i32]
         L.xmoe_layer_set_timing.argtypes = [p, i32]
+        L.xmoe_layer_set_graph.argtypes = [p, i32]
         L.xmoe_layer_stage_ms.argtypes = [p, C.POINTER(C.c_float), i32]
         L.xmoe_plan_dispatch.argtypes = [i32, i32, p, i32, p, p, p]
         L.xmoe_moe_backward.argtypes = [p, p, p, p, i64, p, p]
@@ -315,6 +316,9 @@ class Layer:
         buf = (C.c_uint64 * 8)()
         _check(lib().xmoe_layer_ledger(self.h, buf, 8))
         return dict(zip(self.LEDGER_KEYS, [int(v) for v in buf]))
+
+    def set_graph(self, on: bool):
+        _check(lib().xmoe_layer_set_graph(self.h, int(on)))
 
     def set_timing(self, on: bool):
         _check(lib().xmoe_layer_set_timing(self.h, int(on)))

@@ -310,8 +310,48 @@ int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S,
                      void* stream) {
     return guarded([&] {
         require(layer->l.ctx == &ctx->c, XMOE_ERR_VALIDATION, "layer belongs to another context");
-        layer_forward(layer->l, x, S, out, static_cast<cudaStream_t>(stream));
+        Layer& L = layer->l;
+        auto st = static_cast<cudaStream_t>(stream);
+        // CUDA-graph replay of the whole (host-sync-free) forward: one launch
+        // instead of ~25, keyed by the buffers and length it was captured with
+        const bool graphable = L.use_graph && !L.timing && (!L.distributed || L.p2p);
+        if (!graphable) {
+            layer_forward(L, x, S, out, st);
+            return;
+        }
+        for (auto& g : L.graphs)
+            if (g.x == x && g.out == out && g.S == S) {
+                XMOE_CUDA(cudaGraphLaunch(g.exec, st));
+                L.last_S = S;
+                return;
+            }
+        // capture on the layer's own stream (the caller's may be the legacy
+        // default stream, which cannot be captured); replay on the caller's
+        cudaGraph_t graph = nullptr;
+        cudaStream_t cs = L.cap_stream;
+        XMOE_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        try {
+            layer_forward(L, x, S, out, cs);
+        } catch (...) {
+            cudaStreamEndCapture(cs, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        XMOE_CUDA(cudaStreamEndCapture(cs, &graph));
+        cudaGraphExec_t exec = nullptr;
+        XMOE_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        XMOE_CUDA(cudaGraphDestroy(graph));
+        if (L.graphs.size() >= 4) {
+            cudaGraphExecDestroy(L.graphs.front().exec);
+            L.graphs.erase(L.graphs.begin());
+        }
+        L.graphs.push_back({x, out, S, exec});
+        XMOE_CUDA(cudaGraphLaunch(exec, st));
     });
+}
+
+int xmoe_layer_set_graph(xmoe_layer* layer, int enable) {
+    return guarded([&] { layer->l.use_graph = enable != 0; });
 }
 
 int xmoe_moe_backward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, const void* dy, int64_t S,

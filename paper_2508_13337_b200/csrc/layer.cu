@@ -41,7 +41,9 @@ namespace xmoe {
 static size_t elem_size_of(int dtype) { return dtype == XMOE_F64 ? 8 : 2; }
 
 Layer::~Layer() {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     if (side) cudaStreamDestroy(side);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     for (cudaEvent_t e : {ev_fork, ev_join, ev_side0, ev_side1})
         if (e) cudaEventDestroy(e);
     for (void* p : peer_maps) cudaIpcCloseMemHandle(p);
@@ -371,6 +373,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     L.events.resize(kNumEvents);
     for (auto& e : L.events) XMOE_CUDA(cudaEventCreate(&e));
     XMOE_CUDA(cudaStreamCreateWithFlags(&L.side, cudaStreamNonBlocking));
+    XMOE_CUDA(cudaStreamCreateWithFlags(&L.cap_stream, cudaStreamNonBlocking));
     XMOE_CUDA(cudaEventCreateWithFlags(&L.ev_fork, cudaEventDisableTiming));
     XMOE_CUDA(cudaEventCreateWithFlags(&L.ev_join, cudaEventDisableTiming));
     XMOE_CUDA(cudaEventCreate(&L.ev_side0));

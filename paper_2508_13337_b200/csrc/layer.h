@@ -137,6 +137,15 @@ struct Layer {
     std::vector<void*> allocs;
     std::vector<cudaEvent_t> events;
     bool timing = false;
+    bool use_graph = false;
+    struct GraphEntry {
+        const void* x;
+        void* out;
+        long long S;
+        cudaGraphExec_t exec;
+    };
+    std::vector<GraphEntry> graphs;  // captured forwards (xmoe_layer_set_graph)
+    cudaStream_t cap_stream = nullptr;
     cudaStream_t side = nullptr;  // shared-expert GEMMs overlap routing + exchange
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_side0 = nullptr, ev_side1 = nullptr;
 
