@@ -29,6 +29,7 @@ sys.path.insert(0, ROOT)
 
 C2 = dict(E=64, k=6, H=2048, F=1408, n_shared=2, Fs=1408, S=16384)
 METRIC = "MoE-layer fwd tokens/s"
+NVLINK_GBPS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 UNIT = "tokens/s"
 
 
@@ -46,6 +47,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-backward", action="store_true", help="skip the fwd+bwd measurement")
     p.add_argument("--no-graph", action="store_true", help="launch the forward kernels one by one")
+    p.add_argument("--chunks", type=int, default=0,
+                   help="token chunks of the pipelined forward (0 auto, 1 off)")
     p.add_argument("--cpu-sample-tokens", type=int, default=512,
                    help="tokens per host thread for the cpu_baseline sample")
     return p.parse_args()
@@ -249,12 +252,15 @@ def main():
     sw1 = ((torch.rand(ns, H, Fs, device="cuda", generator=g) * 0.2 - 0.1)).to(torch.bfloat16)
     sw2 = ((torch.rand(ns, Fs, H, device="cuda", generator=g) * 0.2 - 0.1)).to(torch.bfloat16)
     if args.mode == "auto":
-        args.mode = "rbd" if world > 1 else "naive"
+        # measured on B200: the redundancy bypass wins the step
+        # at N=2; from N=4 the chunked plain dispatch, whose all-to-all
+        # overlaps the expert GEMMs, is faster (RBD still moves fewer bytes:
+        # see dispatch_compare)
+        args.mode = "rbd" if world == 2 else "naive"
     mode = capi.RBD if args.mode == "rbd" else capi.NAIVE
     layer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
                        max_tokens=S, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,
-                       dispatch_mode=mode, seed=99, train=not args.no_backward)
-    del w1, w2
+                       dispatch_mode=mode, seed=99, chunks=args.chunks)
     if not args.no_graph:
         layer.set_graph(True)
     g.manual_seed(100 + rank)
@@ -297,6 +303,15 @@ def main():
     ms = max_over_ranks(t0.elapsed_time(t1) / args.steps)
     clk = clocks.stop(world) if rank == 0 else None
 
+    # ---- second layer object, unchunked: the training layer for fwd+bwd and
+    # the per-stage (kernel-level) breakdown behind the roofline — in the
+    # chunked forward the stages overlap and have no separate duration
+    tlayer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
+                        max_tokens=S, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,
+                        dispatch_mode=mode, seed=99, train=not args.no_backward, chunks=1)
+    if not args.no_graph:
+        tlayer.set_graph(True)
+
     # ---- forward + backward (gradients w.r.t. x and every weight), same clock rules
     fwd_bwd = None
     if not args.no_backward:
@@ -304,16 +319,16 @@ def main():
         dy = ((torch.rand(S, H, device="cuda", generator=g) * 2 - 1)).to(torch.bfloat16)
         dxb = torch.empty_like(x)
         for _ in range(max(2, args.warmup)):
-            layer.forward(x, out)
-            layer.backward(x, dy, dxb)
+            tlayer.forward(x, out)
+            tlayer.backward(x, dy, dxb)
         torch.cuda.synchronize()
         barrier()
         b0 = torch.cuda.Event(enable_timing=True)
         b1 = torch.cuda.Event(enable_timing=True)
         b0.record(stream)
         for _ in range(args.steps):
-            layer.forward(x, out)
-            layer.backward(x, dy, dxb)
+            tlayer.forward(x, out)
+            tlayer.backward(x, dy, dxb)
         b1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -324,15 +339,46 @@ def main():
                            "gradients restated beyond the forward-only reference, checked against fp64 autograd"}
 
     # ---- per-stage breakdown + roofline of the dominant kernel (grouped GEMM)
-    layer.set_timing(True)
+    tlayer.set_timing(True)
     stage_runs = []
     for _ in range(5):
-        layer.forward(x, out)
+        tlayer.forward(x, out)
         torch.cuda.synchronize()
-        stage_runs.append(layer.stage_ms())
-    layer.set_timing(False)
+        stage_runs.append(tlayer.stage_ms())
+    tlayer.set_timing(False)
     stages = {kk: statistics.median(r[kk] for r in stage_runs) for kk in stage_runs[0]}
-    led = layer.ledger()
+    led = tlayer.ledger()
+    del tlayer
+
+    # ---- plain vs redundancy-bypassing dispatch (N > 1): all-to-all bytes and
+    # isolated kernel times of both, from unchunked layers in timing mode
+    dispatch_compare = None
+    if world > 1:
+        dispatch_compare = {}
+        for name, md in (("naive", capi.NAIVE), ("rbd", capi.RBD)):
+            pl = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
+                            max_tokens=S, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,
+                            dispatch_mode=md, seed=99, chunks=1)
+            pl.set_timing(True)
+            runs = []
+            for _ in range(6):
+                pl.forward(x, out)
+                torch.cuda.synchronize()
+                runs.append(pl.stage_ms())
+            st_m = {kk: statistics.median(r[kk] for r in runs[1:]) for kk in runs[0]}
+            lg = pl.ledger()
+            del pl
+            off_d = lg["dispatch_rows_offrank"] + lg["dispatch_meta_offrank"]  # bytes (ledger.cpp)
+            off_c = lg["combine_rows_offrank"]
+            dispatch_compare[name] = {
+                "offrank_bytes_dispatch": off_d, "offrank_bytes_combine": off_c,
+                "dispatch_kernel_ms": max_over_ranks(st_m["rows_moved"]),
+                "dispatch_stage_ms": max_over_ranks(st_m["dispatch"]),
+                "combine_kernel_ms": max_over_ranks(st_m["combine_kernel"]),
+                "combine_stage_ms": max_over_ranks(st_m["combine"]),
+                "nvlink_GBps_dispatch": off_d / (st_m["rows_moved"] * 1e-3) / 1e9 if st_m["rows_moved"] else None,
+            }
+        barrier()
     copies = led["routed_copies"]
     recv_rows_here = None  # routed rows computed on this GPU
     # rows this GPU's experts process = total copies landing here; at N=1 = copies
@@ -417,7 +463,7 @@ def main():
             "config": {"workload": "C2: DeepSeek-MoE layer, 64 routed experts top-6 + 2 shared, d_model 2048, "
                                    "d_ff 1408, bf16, expert parallel, dropless (BASELINE configs[1])",
                        "tokens_per_gpu": S, "global_tokens": world * S, "parallelism": f"ep{world}",
-                       "dispatch": args.mode, "pass": "forward",
+                       "dispatch": args.mode, "pass": "forward", "chunks": layer.chunks(),
                        "transport": (os.environ.get("XMOE_TRANSPORT") or "p2p") if world > 1 else "local",
                        "l2": "working set > L2: 0.74 GB of expert weights + 64 MB tokens stream each step (126 MB L2)"},
             "e2e": {"value": world * S / (e2e_ms * 1e-3), "unit": UNIT,
@@ -443,6 +489,14 @@ def main():
                             "combine_frac": comb_bytes / (stages["combine_kernel"] * 1e-3) / 1e9 / hbm
                             if world == 1 and stages.get("combine_kernel") else None},
             "ledger": led,
+            "a2a": None if world == 1 else {
+                "bound": "nvlink", "unit": "GB/s", "peak": NVLINK_GBPS,
+                "bytes_offrank_per_gpu": dispatch_compare[args.mode]["offrank_bytes_dispatch"],
+                "achieved": dispatch_compare[args.mode]["nvlink_GBps_dispatch"],
+                "frac": (dispatch_compare[args.mode]["nvlink_GBps_dispatch"] or 0) / NVLINK_GBPS,
+                "note": "dispatch kernel, isolated (timing mode), off-rank row bytes this GPU sends over NVLink "
+                        "/ kernel time; peak = measured 770 GB/s peer copy per direction (B200_PROFILING.md)"},
+            "dispatch_compare": dispatch_compare,
             "fwd_bwd": fwd_bwd,
             "gpu_launches": launches,
             "clocks": clk,

@@ -4,7 +4,7 @@
  * C-ABI drop-in boundary.  Plain pointers and sizes only; every operator is
  * stream-ordered on caller-owned DEVICE buffers and returns a status code.
  * Each entry point replaces one operator of the reference simulator's C++ API
- * (namespace moesim, /root/reference/proj/include/moesim/*.hpp); the citation
+ * (namespace moesim, /root/reference/proj/include/moesim/ headers); the citation
  * sits above each declaration.  The reference-shaped C++ adapter
  * (include/xmoe/moesim_compat.hpp) is built on these calls.
  *
@@ -54,6 +54,12 @@ extern "C" {
 /* layer flags */
 #define XMOE_LAYER_SSMB 1  /* ssmb_forward layer: every rank holds all experts (ssmb.cpp:29-43) */
 #define XMOE_LAYER_TRAIN 2 /* keep what xmoe_moe_backward needs (BF16 layers) */
+/* token chunks of the pipelined BF16 forward (plain dispatch): chunk c's
+ * expert GEMMs overlap chunk c+1's dispatch and chunk c-1's combine.
+ * 0 = automatic, 1 = off, 2..8 = that many chunks.  Results are
+ * bit-identical for every chunk count. */
+#define XMOE_LAYER_CHUNKS(n) ((n) << 8)
+#define XMOE_LAYER_CHUNKS_OF(flags) (((flags) >> 8) & 15)
 
 typedef struct xmoe_ctx xmoe_ctx;
 typedef struct xmoe_layer xmoe_layer;
@@ -160,7 +166,7 @@ typedef struct {
     int32_t dtype;           /* XMOE_F64 | XMOE_BF16 */
     int32_t renorm;          /* top-k renormalisation (0 = reference) */
     int32_t dispatch_mode;   /* XMOE_DISPATCH_NAIVE | XMOE_DISPATCH_RBD */
-    int32_t flags;           /* XMOE_LAYER_SSMB: sequence-sharded block (experts replicated) */
+    int32_t flags;           /* XMOE_LAYER_SSMB | XMOE_LAYER_TRAIN | XMOE_LAYER_CHUNKS(n) */
     uint64_t seed;           /* RBD pilot seed (salted per rank: salt_seed(seed, w, 0)) */
 } xmoe_layer_desc;
 
@@ -210,13 +216,20 @@ int xmoe_layer_ledger(xmoe_layer* layer, uint64_t* out, int n);
  * gate, pft, dispatch, experts, shared, combine, total, then the exchange
  * split: counts (all-gather), rows_moved (dispatch kernel), dispatch_barrier,
  * return_wait (merge/barrier before the combine), combine_kernel, and the
- * shared-expert GEMMs, which run on a side stream concurrently with routing
- * and the exchange ("shared" above is only the wait for them).
- * Requires timing enabled. */
+ * shared-expert GEMMs.  Timing mode serialises the unchunked forward (the
+ * shared-expert GEMMs run in line as the "shared" stage instead of on the
+ * side stream), so every stage is an isolated kernel time and "total" is
+ * their sum, not the overlapped step.  Chunked layers append, per chunk,
+ * the ms from the start to its scatter end, GEMM start, GEMM end and
+ * combine end (n = 13 + 4 * chunks).  Requires timing enabled. */
 int xmoe_layer_set_timing(xmoe_layer* layer, int enable);
 /* Capture the forward as a CUDA graph per (x, out, S) and replay it (the
  * forward has no host synchronisation on the local and NVLink transports). */
 int xmoe_layer_set_graph(xmoe_layer* layer, int enable);
+
+/* Token chunks the BF16 forward of this layer is pipelined over (1 = not
+ * chunked); see XMOE_LAYER_CHUNKS. */
+int xmoe_layer_chunks(const xmoe_layer* layer, int32_t* out);
 int xmoe_layer_stage_ms(xmoe_layer* layer, float* out, int n);
 
 #ifdef __cplusplus

@@ -79,6 +79,7 @@ def lib():
         L.xmoe_layer_ledger.argtypes = [p, C.POINTER(C.c_uint64), i32]
         L.xmoe_layer_set_timing.argtypes = [p, i32]
         L.xmoe_layer_set_graph.argtypes = [p, i32]
+        L.xmoe_layer_chunks.argtypes = [p, p]
         L.xmoe_layer_stage_ms.argtypes = [p, C.POINTER(C.c_float), i32]
         L.xmoe_plan_dispatch.argtypes = [i32, i32, p, i32, p, p, p]
         L.xmoe_moe_backward.argtypes = [p, p, p, p, i64, p, p]
@@ -232,17 +233,19 @@ class Layer:
     """xmoe_layer: weights resident in HBM in the B200 layout + workspace.
 
     gate [H,E], w1 [E_held,H,F], w2 [E_held,F,H] (reference layouts, device
-    tensors of the layer dtype); sw1 [ns,H,Fs], sw2 [ns,Fs,H] optional."""
+    tensors of the layer dtype); sw1 [ns,H,Fs], sw2 [ns,Fs,H] optional.
+    chunks: token chunks of the pipelined BF16 forward (0 auto, 1 off; see
+    XMOE_LAYER_CHUNKS in xmoe.h)."""
 
     def __init__(self, ctx: Context, *, num_experts, model_dim, ffn_dim, top_k, max_token_count,
                  max_tokens, dtype, gate, w1, w2, sw1=None, sw2=None, renorm=False,
-                 dispatch_mode=NAIVE, seed=0, ssmb=False, train=False):
+                 dispatch_mode=NAIVE, seed=0, ssmb=False, train=False, chunks=0):
         self.ctx = ctx
         ns = 0 if sw1 is None else sw1.shape[0]
         fs = 0 if sw1 is None else sw1.shape[2]
         self.desc = LayerDesc(num_experts, model_dim, ffn_dim, top_k, max_token_count, ns, fs,
                               max_tokens, dtype, int(renorm), dispatch_mode,
-                              int(bool(ssmb)) | (2 if train else 0), seed)
+                              int(bool(ssmb)) | (2 if train else 0) | (int(chunks) << 8), seed)
         self.shape = dict(E=num_experts, H=model_dim, F=ffn_dim, ns=ns, Fs=fs,
                           E_held=w1.shape[0])
         self.dtype = dtype
@@ -317,6 +320,11 @@ class Layer:
         _check(lib().xmoe_layer_ledger(self.h, buf, 8))
         return dict(zip(self.LEDGER_KEYS, [int(v) for v in buf]))
 
+    def chunks(self) -> int:
+        v = C.c_int32()
+        _check(lib().xmoe_layer_chunks(self.h, C.byref(v)))
+        return int(v.value)
+
     def set_graph(self, on: bool):
         _check(lib().xmoe_layer_set_graph(self.h, int(on)))
 
@@ -326,6 +334,16 @@ class Layer:
     STAGES = ["gate", "pft", "dispatch", "experts", "shared", "combine", "total",
               "counts", "rows_moved", "dispatch_barrier", "return_wait", "combine_kernel",
               "shared_side_stream"]
+
+    def timeline_ms(self) -> list:
+        """Chunked forward (timing on): per chunk [scatter end, GEMM start,
+        GEMM end, combine end] in ms from the forward's start."""
+        n = self.chunks()
+        if n <= 1:
+            return []
+        buf = (C.c_float * (13 + 4 * n))()
+        _check(lib().xmoe_layer_stage_ms(self.h, buf, 13 + 4 * n))
+        return [[round(float(buf[13 + 4 * c + j]), 4) for j in range(4)] for c in range(n)]
 
     def stage_ms(self) -> dict:
         buf = (C.c_float * 13)()

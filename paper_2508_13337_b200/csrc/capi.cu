@@ -350,6 +350,13 @@ int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S,
     });
 }
 
+int xmoe_layer_chunks(const xmoe_layer* layer, int32_t* out) {
+    return guarded([&] {
+        require(out != nullptr, XMOE_ERR_VALIDATION, "null output");
+        *out = layer->l.nchunks;
+    });
+}
+
 int xmoe_layer_set_graph(xmoe_layer* layer, int enable) {
     return guarded([&] { layer->l.use_graph = enable != 0; });
 }
@@ -404,6 +411,10 @@ int xmoe_layer_stage_ms(xmoe_layer* layer, float* out, int n) {
             out[12] = 0.f;
             if (L.Fs > 0) XMOE_CUDA(cudaEventElapsedTime(&out[12], L.ev_side0, L.ev_side1));
         }
+        // chunked forward: per chunk, ms from the start to its scatter end,
+        // GEMM start, GEMM end and combine end
+        for (int i = 13; i < n && i - 13 < static_cast<int>(L.tl.size()); ++i)
+            XMOE_CUDA(cudaEventElapsedTime(&out[i], L.events[kEvStart], L.tl[i - 13]));
     });
 }
 

@@ -1,0 +1,176 @@
+// Token-chunked forward pipeline (layer.cu: layer_forward_chunked).
+//
+// The S tokens of every source are cut into C contiguous chunks
+// [floor(cS/C), floor((c+1)S/C)).  Each owner keeps one fixed region of Rc
+// rows per chunk, laid out inside it exactly like the unchunked grouped
+// buffer — (local expert, source, position), pf_pipeline.cpp:47-73 — so
+// chunk c's rows can be dispatched, run through the grouped GEMMs and
+// combined while the neighbouring chunks are in a different phase.  Every
+// row's arithmetic is unchanged (a GEMM row does not depend on its
+// neighbours, the combine sums a token's copies in slot order), so the
+// chunked forward is bit-identical to the unchunked one.
+//
+// Cross-GPU phase ordering uses epoch flags in the symmetric (IPC-mapped)
+// region instead of NCCL all-reduces: flag[phase][c][src] on every owner,
+// written with st.release.sys by the source after its phase-c work, polled
+// with ld.acquire.sys by the consumer.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace xmoe {
+
+__host__ __device__ __forceinline__ int chunk_t0(int c, int S, int C) {
+    return static_cast<int>(static_cast<long long>(c) * S / C);
+}
+__device__ __forceinline__ int chunk_of(int t, int S, int C) {
+    return static_cast<int>((static_cast<long long>(t + 1) * C - 1) / S);
+}
+
+// per (chunk c, expert e): kept copies of e whose token lies in chunk c, and
+// their offset inside e's packed segment (tokens ascend within a segment,
+// pft.cpp:35-57, so a chunk is a contiguous sub-range found by binary search)
+__global__ void chunk_counts_kernel(const int32_t* __restrict__ token_ids, const int32_t* __restrict__ tpe,
+                                    int E, int S, int C, int32_t* __restrict__ tpe_c,
+                                    int32_t* __restrict__ pfx_c, int32_t* __restrict__ seg) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= C * E) return;
+    const int c = idx / E, e = idx % E;
+    int s0 = 0;
+    for (int j = 0; j < e; ++j) s0 += tpe[j];
+    const int n = tpe[e];
+    auto lb = [&](int t) {
+        int lo = 0, hi = n;
+        while (lo < hi) {
+            const int m = (lo + hi) >> 1;
+            if (token_ids[s0 + m] < t) lo = m + 1;
+            else hi = m;
+        }
+        return lo;
+    };
+    const int a = lb(chunk_t0(c, S, C));
+    const int b = c == C - 1 ? n : lb(chunk_t0(c + 1, S, C));
+    tpe_c[idx] = b - a;
+    pfx_c[idx] = a;
+    if (c == 0) seg[e] = s0;
+}
+
+// base[c][e]: first row of (expert e, source me) in e's owner's chunk-c
+// region; rpe_c[c][le]: rows of my local expert le in my chunk-c region.
+// T = [W][C][E] per-source chunk counts.
+__global__ void chunk_bases_kernel(const int32_t* __restrict__ T, int W, int C, int E, int me, int Rc,
+                                   int32_t* __restrict__ base, int32_t* __restrict__ rpe_c) {
+    const int El = E / W;
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    auto t = [&](int s, int c, int e) { return T[(static_cast<size_t>(s) * C + c) * E + e]; };
+    if (idx < C * E) {
+        const int c = idx / E, e = idx % E;
+        const int o = e / El, le = e % El;
+        int a = c * Rc;
+        for (int l2 = 0; l2 < le; ++l2)
+            for (int s = 0; s < W; ++s) a += t(s, c, o * El + l2);
+        for (int s = 0; s < me; ++s) a += t(s, c, e);
+        base[idx] = a;
+    } else if (idx < C * E + C * El) {
+        const int j = idx - C * E;
+        const int c = j / El, le = j % El;
+        int a = 0;
+        for (int s = 0; s < W; ++s) a += t(s, c, me * El + le);
+        rpe_c[j] = a;
+    }
+}
+
+__global__ void dispatch_dest_chunked_kernel(const int32_t* __restrict__ expert_ids,
+                                             const int32_t* __restrict__ token_ids,
+                                             const int32_t* __restrict__ B_dev, int S, int C, int E, int El,
+                                             const int32_t* __restrict__ seg, const int32_t* __restrict__ pfx_c,
+                                             const int32_t* __restrict__ base, int32_t* __restrict__ dest_rank,
+                                             int32_t* __restrict__ dest_row) {
+    const int B = *B_dev;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < B; r += gridDim.x * blockDim.x) {
+        const int e = expert_ids[r];
+        const int c = chunk_of(token_ids[r], S, C);
+        dest_rank[r] = e / El;
+        dest_row[r] = base[c * E + e] + (r - seg[e]) - pfx_c[c * E + e];
+    }
+}
+
+__global__ void forward_begin_kernel(int32_t* s_rows, int S, unsigned* epoch) {
+    if (threadIdx.x == 0) {
+        *s_rows = S;
+        if (epoch) *epoch += 1u;
+    }
+}
+
+__global__ void flag_signal_kernel(unsigned* const* __restrict__ flag_tab, int W, int me, int slot,
+                                   const unsigned* __restrict__ epoch) {
+    const int p = threadIdx.x;
+    if (p >= W) return;
+    const unsigned e = *epoch;
+    unsigned* f = flag_tab[p] + static_cast<size_t>(slot) * W + me;
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(e) : "memory");
+}
+
+__global__ void flag_wait_kernel(const unsigned* __restrict__ flags, int W, int slot,
+                                 const unsigned* __restrict__ epoch) {
+    const int s = threadIdx.x;
+    if (s < W) {
+        const unsigned e = *epoch;
+        const unsigned* f = flags + static_cast<size_t>(slot) * W + s;
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+            unsigned v;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            if (static_cast<int>(v - e) >= 0) break;
+            __nanosleep(100);
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 20000000000ull) __trap();  // a peer never arrived: fail, do not hang
+        }
+    }
+    __syncthreads();
+}
+
+void launch_chunk_counts(const int32_t* token_ids, const int32_t* tpe, int E, int S, int C, int32_t* tpe_c,
+                         int32_t* pfx_c, int32_t* seg, cudaStream_t st) {
+    const int n = C * E;
+    chunk_counts_kernel<<<(n + 127) / 128, 128, 0, st>>>(token_ids, tpe, E, S, C, tpe_c, pfx_c, seg);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_chunk_bases(const int32_t* T, int W, int C, int E, int me, int Rc, int32_t* base, int32_t* rpe_c,
+                        cudaStream_t st) {
+    const int n = C * E + C * (E / W);
+    chunk_bases_kernel<<<(n + 127) / 128, 128, 0, st>>>(T, W, C, E, me, Rc, base, rpe_c);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_dispatch_dest_chunked(const int32_t* expert_ids, const int32_t* token_ids, const int32_t* B_dev,
+                                  long long max_rows, int S, int C, int E, int El, const int32_t* seg,
+                                  const int32_t* pfx_c, const int32_t* base, int32_t* dest_rank,
+                                  int32_t* dest_row, cudaStream_t st) {
+    const long long blocks = (max_rows + 255) / 256;
+    dispatch_dest_chunked_kernel<<<static_cast<int>(blocks < 4 * kNumSMs ? (blocks > 0 ? blocks : 1) : 4 * kNumSMs),
+                                   256, 0, st>>>(expert_ids, token_ids, B_dev, S, C, E, El, seg, pfx_c, base,
+                                                 dest_rank, dest_row);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_forward_begin(int32_t* s_rows, int S, unsigned* epoch, cudaStream_t st) {
+    forward_begin_kernel<<<1, 32, 0, st>>>(s_rows, S, epoch);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_flag_signal(unsigned* const* flag_tab, int W, int me, int slot, const unsigned* epoch,
+                        cudaStream_t st) {
+    flag_signal_kernel<<<1, 32 * ((W + 31) / 32), 0, st>>>(flag_tab, W, me, slot, epoch);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_flag_wait(const unsigned* flags, int W, int slot, const unsigned* epoch, cudaStream_t st) {
+    flag_wait_kernel<<<1, 32 * ((W + 31) / 32), 0, st>>>(flags, W, slot, epoch);
+    XMOE_LAUNCH_CHECK();
+}
+
+}  // namespace xmoe

@@ -73,9 +73,10 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_bf16_kernel(
     const __nv_bfloat16* __restrict__ rows, int H, CopyList cl, const double* __restrict__ w,
     int S, const __nv_bfloat16* __restrict__ addend, __nv_bfloat16* __restrict__ out) {
     const int nseg = (H + kSegCols - 1) / kSegCols;
-    const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (gw >= static_cast<long long>(S) * nseg) return;
+    const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    for (long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+         gw < static_cast<long long>(S) * nseg; gw += nw) {
     const int t = static_cast<int>(gw / nseg);
     const int seg = static_cast<int>(gw % nseg);
     const int nchunk = H >> 3;
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_bf16_kernel(
         o.w = static_cast<int>(pack_bf16(acc[8 * h + 6], acc[8 * h + 7]));
         st_na_v4(dst + c, o);
     }
+    }
 }
 
 // BF16 combine over per-slot source addresses (written by the token-major
@@ -173,9 +175,10 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_slots_bf16_kernel(
     const __nv_bfloat16* __restrict__ addend, __nv_bfloat16* __restrict__ out, long long src_delta,
     const __nv_bfloat16* __restrict__ addend2) {
     const int nseg = (H + kSegCols - 1) / kSegCols;
-    const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (gw >= static_cast<long long>(S) * nseg) return;
+    const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    for (long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+         gw < static_cast<long long>(S) * nseg; gw += nw) {
     const int t = static_cast<int>(gw / nseg);
     const int seg = static_cast<int>(gw % nseg);
     const int nchunk = H >> 3;
@@ -260,6 +263,7 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_slots_bf16_kernel(
         o.w = static_cast<int>(pack_bf16(acc[8 * h + 6], acc[8 * h + 7]));
         st_na_v4(dst + c, o);
     }
+    }
 }
 
 void launch_combine_slots(const unsigned long long* slot_src, const float* slot_w, int k, int H, int S,
@@ -267,7 +271,9 @@ void launch_combine_slots(const unsigned long long* slot_src, const float* slot_
     if (S == 0) return;
     require(H % 8 == 0 && k <= 32, XMOE_ERR_VALIDATION, "slot combine needs model_dim % 8 == 0, k <= 32");
     const long long warps = static_cast<long long>(S) * ((H + kSegCols - 1) / kSegCols);
-    combine_slots_bf16_kernel<<<ceil_div(warps, kCombWarps), 32 * kCombWarps, 0, st>>>(
+    long long blocks = ceil_div(warps, kCombWarps);
+    if (g_copy_blocks > 0 && blocks > g_copy_blocks) blocks = g_copy_blocks;
+    combine_slots_bf16_kernel<<<static_cast<int>(blocks), 32 * kCombWarps, 0, st>>>(
         slot_src, slot_w, k, H, S, static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out),
         src_delta, static_cast<const __nv_bfloat16*>(addend2));
     XMOE_LAUNCH_CHECK();

@@ -94,6 +94,11 @@ void launch_gate_bwd(const float* logits, const int32_t* slot_pos, const int32_t
 
 // gemm_tc.cu: SM budget of subsequent 2-CTA GEMM launches on this thread (0 = all)
 extern thread_local int g_gemm_sm_limit;
+// grid cap of the row-movement kernels (token scatter, slot combine; 0 =
+// their default).  The chunked forward runs them on a few SMs' worth of
+// blocks so the NVLink traffic they drive does not stall the GEMM CTAs on
+// every SM.
+extern thread_local int g_copy_blocks;
 
 // misc.cu
 void launch_recv_counts(const int32_t* tpe_all, int W, int E, int dst, int32_t* rpe,
@@ -103,5 +108,20 @@ void launch_adjacent_diff(const int32_t* ptr, int n, int32_t* out, cudaStream_t 
 void launch_f32_to_f64(const float* in, long long n, double* out, cudaStream_t st);
 void launch_transpose(int dtype_in, const void* in, int batch, int rows, int cols,
                       int dtype_out, void* out, cudaStream_t st);
+
+// chunk.cu: token-chunked pipeline (layout, counts, cross-GPU epoch flags)
+constexpr int kMaxChunks = 8;
+void launch_chunk_counts(const int32_t* token_ids, const int32_t* tpe, int E, int S, int C, int32_t* tpe_c,
+                         int32_t* pfx_c, int32_t* seg, cudaStream_t st);
+void launch_chunk_bases(const int32_t* T, int W, int C, int E, int me, int Rc, int32_t* base, int32_t* rpe_c,
+                        cudaStream_t st);
+void launch_dispatch_dest_chunked(const int32_t* expert_ids, const int32_t* token_ids, const int32_t* B_dev,
+                                  long long max_rows, int S, int C, int E, int El, const int32_t* seg,
+                                  const int32_t* pfx_c, const int32_t* base, int32_t* dest_rank,
+                                  int32_t* dest_row, cudaStream_t st);
+void launch_forward_begin(int32_t* s_rows, int S, unsigned* epoch, cudaStream_t st);
+void launch_flag_signal(unsigned* const* flag_tab, int W, int me, int slot, const unsigned* epoch,
+                        cudaStream_t st);
+void launch_flag_wait(const unsigned* flags, int W, int slot, const unsigned* epoch, cudaStream_t st);
 
 }  // namespace xmoe

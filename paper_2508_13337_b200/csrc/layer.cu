@@ -44,8 +44,12 @@ Layer::~Layer() {
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     if (side) cudaStreamDestroy(side);
     if (cap_stream) cudaStreamDestroy(cap_stream);
-    for (cudaEvent_t e : {ev_fork, ev_join, ev_side0, ev_side1})
+    if (comm) cudaStreamDestroy(comm);
+    for (cudaEvent_t e : {ev_fork, ev_join, ev_side0, ev_side1, ev_done})
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : evA) cudaEventDestroy(e);
+    for (cudaEvent_t e : evB) cudaEventDestroy(e);
+    for (cudaEvent_t e : tl) cudaEventDestroy(e);
     for (void* p : peer_maps) cudaIpcCloseMemHandle(p);
     for (void* p : allocs) cudaFree(p);
     for (auto& e : events) cudaEventDestroy(e);
@@ -163,11 +167,32 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     const long long cap_bound = static_cast<long long>(W) * L.El * d.max_token_count;
     L.R_max = std::max<long long>(1, std::min<long long>(static_cast<long long>(W) * per_src, cap_bound));
     L.S_max = S;
+    // token-chunked pipeline (chunk.cu): BF16 plain dispatch over pointer tables
+    L.train = (d.flags & XMOE_LAYER_TRAIN) != 0;
+    {
+        const int req = XMOE_LAYER_CHUNKS_OF(d.flags);
+        require(req <= kMaxChunks, XMOE_ERR_VALIDATION, "at most 8 token chunks");
+        const bool can = bf && !L.train && (!L.distributed || L.p2p) && L.k <= 32;
+        int C = req > 0 ? req : (S >= 4096 && L.distributed && !rbd ? std::min(4, W) : 1);
+        if (const char* e = std::getenv("XMOE_CHUNKS")) C = std::max(1, std::min(kMaxChunks, std::atoi(e)));
+        L.nchunks = can ? static_cast<int>(std::max<long long>(1, std::min<long long>(C, S))) : 1;
+        if (L.nchunks > 1) {
+            const long long cs = (S + L.nchunks - 1) / L.nchunks;
+            const long long rc = std::min<long long>(static_cast<long long>(W) * cs * std::min<long long>(L.k, L.El),
+                                                     static_cast<long long>(W) * L.El *
+                                                         std::min<long long>(d.max_token_count, cs));
+            require(rc * L.nchunks < (1LL << 31), XMOE_ERR_VALIDATION, "chunk regions exceed 2^31 rows");
+            L.Rc = static_cast<int>(std::max<long long>(1, rc));
+            L.R_max = std::max<long long>(L.R_max, static_cast<long long>(L.Rc) * L.nchunks);
+        }
+    }
     const long long gmax = S * std::min<long long>(L.k, W);  // RBD groups per source
     const long long rmax = static_cast<long long>(W) * S;   // RBD groups received
     L.tpe_all = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * W * E));
     L.G_all = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * W * W));
     L.bar = static_cast<int32_t*>(L.alloc(64));
+    if (L.nchunks > 1) L.tpe_c_all = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * W * L.nchunks * E));
+    if (rbd) L.gd_all = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * 2 * W * W * L.nchunks));
     // symmetric region (same offsets on every rank; exported over IPC in p2p mode)
     auto up = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
     const size_t off_recv = 0;
@@ -176,7 +201,6 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     const size_t off_desc = off_recv_u;  // RBD rows land in place (pilot slot): no unique-row buffer
     const size_t off_back = off_desc + (rbd ? up(sizeof(RbdDesc) * L.R_max) : 0);
     const size_t off_train = off_back + (rbd ? up(static_cast<size_t>(rmax) * H * es) : 0);
-    L.train = (d.flags & XMOE_LAYER_TRAIN) != 0;
     require(!L.train || (bf && !d.renorm && (!L.distributed || L.p2p) && L.nl == 1), XMOE_ERR_VALIDATION,
             "training layers need bf16, no renorm, one rank per process (or world 1) and the NVLink peer transport");
     require(!L.train || (H % 128 == 0 && F % 128 == 0 && E % 32 == 0 && L.Fs % 128 == 0), XMOE_ERR_VALIDATION,
@@ -186,12 +210,14 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     const size_t off_gw = off_dxc + (L.train ? up(static_cast<size_t>(L.R_max) * H * es) : 0);
     const size_t off_gsrc = off_gw + (L.train ? up(sizeof(float) * L.R_max) : 0);
     const size_t off_sdw = off_gsrc + (L.train ? up(sizeof(unsigned long long) * L.R_max) : 0);
-    const size_t sym_bytes = off_sdw + (L.train ? up(sizeof(float) * nk) : 0);
+    const size_t off_flags = off_sdw + (L.train ? up(sizeof(float) * nk) : 0);
+    const size_t flag_bytes = sizeof(unsigned) * 2 * kMaxChunks * W;
+    const size_t sym_bytes = off_flags + up(flag_bytes);
     L.off_eout = static_cast<long long>(off_eout);
     L.off_dxc = static_cast<long long>(off_dxc);
     L.workers.resize(L.nl);
     std::vector<char*> t_recv(W), t_eout(W), t_recv_u(W), t_desc(W), t_back(W);
-    std::vector<char*> t_dyg(W), t_dxc(W), t_gw(W), t_gsrc(W), t_sdw(W);
+    std::vector<char*> t_dyg(W), t_dxc(W), t_gw(W), t_gsrc(W), t_sdw(W), t_flags(W);
     for (int i = 0; i < L.nl; ++i) {
         Worker& w = L.workers[i];
         w.rank = ssmb ? 0 : ctx.rank_of(i);
@@ -212,6 +238,16 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         w.slot_w = static_cast<float*>(L.alloc(sizeof(float) * nk));
         w.rpe = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * L.El));
         w.sym = static_cast<char*>(L.alloc(sym_bytes));
+        w.flags = reinterpret_cast<unsigned*>(w.sym + off_flags);
+        XMOE_CUDA(cudaMemset(w.flags, 0, flag_bytes));
+        if (L.nchunks > 1) {
+            const int CE = L.nchunks * E;
+            w.tpe_c = L.distributed ? static_cast<int32_t*>(L.alloc(sizeof(int32_t) * CE)) : nullptr;
+            w.pfx_c = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * CE));
+            w.seg = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * E));
+            w.cbase = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * CE));
+            w.rpe_c = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * L.nchunks * L.El));
+        }
         w.recv = w.sym + off_recv;
         w.eout = w.sym + off_eout;
         w.mid = L.alloc(static_cast<size_t>(L.R_max) * F * es);
@@ -243,10 +279,14 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
             r.nsorted = i32(nk);
             r.coff = i32(nk);
             r.csr_ws = L.alloc(bucket_ws_bytes(nk, W));
-            r.ru_base = i32(W);
-            r.rd_base = i32(W);
-            r.cseg = i32(W);
-            r.rx = i32(2);
+            r.C = L.nchunks;
+            r.gpos = i32(static_cast<long long>(W) * (r.C + 1));
+            r.gd_own = L.distributed ? i32(2LL * W * r.C)
+                                     : L.gd_all + static_cast<size_t>(w.rank) * 2 * W * r.C;
+            r.ru = i32(static_cast<long long>(W) * r.C);
+            r.rd = i32(static_cast<long long>(W) * r.C);
+            r.cs = i32(static_cast<long long>(W) * r.C);
+            r.rx = i32(4LL * r.C);
             rng_state_from_seed(salt_seed_host(d.seed, static_cast<uint64_t>(w.rank), 0), r.state);
             w.recv_u = w.sym + off_recv_u;
             w.desc_recv = reinterpret_cast<RbdDesc*>(w.sym + off_desc);
@@ -282,6 +322,8 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
             }
             w.bslot_src = static_cast<unsigned long long*>(L.alloc(sizeof(unsigned long long) * nk));
         }
+        if (L.nchunks > 1 && !L.distributed) w.tpe_c = L.tpe_c_all + static_cast<size_t>(w.rank) * L.nchunks * E;
+        t_flags[w.rank] = reinterpret_cast<char*>(w.flags);
         t_recv[w.rank] = static_cast<char*>(w.recv);
         t_eout[w.rank] = static_cast<char*>(w.eout);
         t_dyg[w.rank] = static_cast<char*>(w.dyg);
@@ -320,6 +362,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
             t_recv_u[r] = b + off_recv_u;
             t_desc[r] = b + off_desc;
             t_back[r] = b + off_back;
+            t_flags[r] = b + off_flags;
         }
     }
     auto table = [&](const std::vector<char*>& v) {
@@ -328,6 +371,9 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         return t;
     };
     L.recv_tab = table(t_recv);
+    L.flag_tab = reinterpret_cast<unsigned**>(table(t_flags));
+    L.epoch = static_cast<unsigned*>(L.alloc(sizeof(unsigned)));
+    XMOE_CUDA(cudaMemset(L.epoch, 0, sizeof(unsigned)));
     L.eout_tab = table(t_eout);
     if (L.train) {
         L.dyg_tab = table(t_dyg);
@@ -378,6 +424,16 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     XMOE_CUDA(cudaEventCreateWithFlags(&L.ev_join, cudaEventDisableTiming));
     XMOE_CUDA(cudaEventCreate(&L.ev_side0));
     XMOE_CUDA(cudaEventCreate(&L.ev_side1));
+    if (L.nchunks > 1) {
+        XMOE_CUDA(cudaStreamCreateWithFlags(&L.comm, cudaStreamNonBlocking));
+        L.evA.resize(L.nchunks);
+        L.evB.resize(L.nchunks);
+        for (auto* v : {&L.evA, &L.evB})
+            for (auto& e : *v) XMOE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        XMOE_CUDA(cudaEventCreateWithFlags(&L.ev_done, cudaEventDisableTiming));
+        L.tl.resize(4 * L.nchunks);
+        for (auto& e : L.tl) XMOE_CUDA(cudaEventCreate(&e));
+    }
     XMOE_CUDA(cudaDeviceSynchronize());
 }
 
@@ -400,11 +456,190 @@ static void run_gemm(int dtype, const void* A, long long rows_bound, int K, cons
         launch_grouped_gemm_bf16(A, rows_bound, K, rpg, G, B, N, D, relu, st);
 }
 
+// ---------------------------------------------------------------- chunked forward
+// BF16 plain dispatch, cut into L.nchunks token chunks (chunk.cu).  Streams:
+//   st   gate | shared-expert GEMMs | per chunk: [wait A_c] GEMM1, GEMM2 [signal B_c]
+//   comm       PFT, counts, destinations | per chunk: scatter [signal A_c] | per chunk: [wait B_c] combine
+// so chunk c's expert GEMMs run while chunk c+1's rows are still moving and
+// chunk c-1's outputs are being combined; the row-movement kernels need no
+// shared memory and co-reside with the persistent GEMM CTAs.  A_c / B_c are
+// local events plus, across GPUs, epoch flags in the peers' symmetric
+// regions.  Every row's arithmetic equals the unchunked forward's.
+static void layer_forward_chunked(Layer& L, const void* x, long long S, void* out, cudaStream_t st) {
+    Ctx& ctx = *L.ctx;
+    const int W = L.W, E = L.E, H = L.H, F = L.F, k = L.k, El = L.El, C = L.nchunks;
+    const size_t rb = static_cast<size_t>(H) * L.es;
+    const int nl = L.nl;
+    const bool dist = L.distributed;
+    const long long nk = S * k;
+    cudaStream_t cm = L.comm;
+    const char* xb = static_cast<const char*>(x);
+    char* ob = static_cast<char*>(out);
+    auto x_of = [&](int i) { return xb + static_cast<size_t>(i) * S * rb; };
+    auto o_of = [&](int i) { return ob + static_cast<size_t>(i) * S * rb; };
+    auto t0_of = [&](int c) { return static_cast<int>(static_cast<long long>(c) * S / C); };
+    const int me = L.workers[0].rank;
+    const bool rbd = L.d.dispatch_mode == XMOE_DISPATCH_RBD;
+    // row-movement kernels run on a bounded grid beside the GEMMs
+    static const int blk_scatter = [] {
+        const char* e = std::getenv("XMOE_COPY_BLOCKS");
+        return e ? std::max(1, std::atoi(e)) : 64;
+    }();
+    static const int blk_combine = [] {
+        const char* e = std::getenv("XMOE_COPY_BLOCKS");
+        const char* c = e ? std::strchr(e, ',') : nullptr;
+        return c ? std::max(1, std::atoi(c + 1)) : 64;
+    }();
+    auto slot_A = [](int c) { return c; };
+    auto slot_B = [](int c) { return kMaxChunks + c; };
+
+    L.mark(kEvStart, st);
+    for (int i = 0; i < nl; ++i)
+        launch_forward_begin(L.workers[i].s_rows, static_cast<int>(S), i == 0 ? L.epoch : nullptr, st);
+    for (int i = 0; i < nl; ++i) {  // 1. gate (gating.cpp:14-57)
+        Worker& w = L.workers[i];
+        float* lg = reinterpret_cast<float*>(w.logits);
+        launch_grouped_gemm_bf16_f32out(x_of(i), S, H, w.s_rows, 1, L.gate, E, lg, 0, st);
+        launch_softmax_topk_f32(lg, S, E, k, L.d.renorm, w.top, w.wts, st);
+    }
+    L.mark(kEvGate, st);
+    XMOE_CUDA(cudaEventRecord(L.ev_fork, st));
+    XMOE_CUDA(cudaStreamWaitEvent(cm, L.ev_fork, 0));
+    // 2. comm stream: PFT (pft.cpp:12-60), chunk counts, count all-gather,
+    //    destinations, then every chunk's rows
+    for (int i = 0; i < nl; ++i) {
+        Worker& w = L.workers[i];
+        launch_pft(w.top, w.wts, S, k, E, static_cast<int>(std::min<long long>(L.d.max_token_count, 0x7fffffff)),
+                   w.token_ids, w.expert_ids, w.cw, w.tpe, w.slot_pos, w.B_dev, w.pft_ws, cm);
+        launch_chunk_counts(w.token_ids, w.tpe, E, static_cast<int>(S), C, w.tpe_c, w.pfx_c, w.seg, cm);
+        if (rbd) {  // groups, pilots (rbd.cpp:26-81), per (dest, chunk) counts
+            launch_rbd_groups(w.slot_pos, w.expert_ids, static_cast<int>(S), k, El, w.rbd.state, L.jumps, w.rbd,
+                              cm);
+            launch_rbd_sort(W, nk, w.rbd, cm);
+            launch_adjacent_diff(w.rbd.dptr, W, L.G_all + static_cast<size_t>(w.rank) * W, cm);
+            launch_rbd_chunk_counts(W, static_cast<int>(S), w.rbd, cm);
+        }
+    }
+    L.mark(kEvPft, cm);
+    if (dist) {
+        Worker& w = L.workers[0];
+        auto comm = static_cast<ncclComm_t>(ctx.nccl);
+        XMOE_NCCL(ncclGroupStart());
+        XMOE_NCCL(ncclAllGather(w.tpe, L.tpe_all, E, ncclInt32, comm, cm));
+        XMOE_NCCL(ncclAllGather(w.tpe_c, L.tpe_c_all, static_cast<size_t>(C) * E, ncclInt32, comm, cm));
+        if (rbd) {
+            XMOE_NCCL(ncclAllGather(L.G_all + static_cast<size_t>(w.rank) * W, L.G_all, W, ncclInt32, comm, cm));
+            XMOE_NCCL(ncclAllGather(w.rbd.gd_own, L.gd_all, static_cast<size_t>(2) * W * C, ncclInt32, comm, cm));
+        }
+        XMOE_NCCL(ncclGroupEnd());
+    }
+    L.mark(kEvCounts, cm);
+    for (int i = 0; i < nl; ++i) {
+        Worker& w = L.workers[i];
+        launch_chunk_bases(L.tpe_c_all, W, C, E, w.rank, L.Rc, w.cbase, w.rpe_c, cm);
+        launch_dispatch_dest_chunked(w.expert_ids, w.token_ids, w.B_dev, nk, static_cast<int>(S), C, E, El, w.seg,
+                                     w.pfx_c, w.cbase, w.dest_rank, w.dest_row, cm);
+        if (rbd) launch_rbd_offsets(L.gd_all, W, w.rank, w.rbd, cm);
+    }
+    for (int c = 0; c < C; ++c) {
+        // chunk 0 gates the first expert GEMM: full grid; later chunks run
+        // beside the GEMMs on a bounded grid
+        g_copy_blocks = c == 0 ? 0 : blk_scatter;
+        const int t0 = t0_of(c), n = t0_of(c + 1) - t0;
+        if (rbd)  // each (token, dest) group's row once + a descriptor per copy
+            for (int i = 0; i < nl; ++i) {
+                Worker& w = L.workers[i];
+                launch_rbd_pack(x_of(i), static_cast<int>(rb), w.rbd, W, c, nk, w.slot_pos, k, w.dest_row, w.cw,
+                                L.recv_tab, L.desc_tab, cm);
+            }
+        else if (n > 0)
+            for (int i = 0; i < nl; ++i) {
+                Worker& w = L.workers[i];
+                launch_scatter_tokens(x_of(i) + static_cast<size_t>(t0) * rb, static_cast<int>(rb), n, k,
+                                      w.slot_pos + static_cast<size_t>(t0) * k, w.dest_rank, w.dest_row, w.cw,
+                                      L.recv_tab, L.eout_tab, w.slot_src + static_cast<size_t>(t0) * k,
+                                      w.slot_w + static_cast<size_t>(t0) * k, cm);
+            }
+        if (dist) launch_flag_signal(L.flag_tab, W, me, slot_A(c), L.epoch, cm);
+        if (L.timing) XMOE_CUDA(cudaEventRecord(L.tl[4 * c], cm));
+        XMOE_CUDA(cudaEventRecord(L.evA[c], cm));
+    }
+    g_copy_blocks = 0;
+    L.mark(kEvMoved, cm);
+    L.mark(kEvDispatch, cm);
+    // 3. st: shared experts (x only), then the routed experts chunk by chunk
+    //    (pf_pipeline.cpp:83-105)
+    if (L.Fs > 0) {
+        if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side0, st));
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            launch_grouped_gemm_bf16(x_of(i), S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, st);
+            launch_grouped_gemm_bf16(w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, w.sout, 0, st);
+        }
+        if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side1, st));
+    }
+    for (int c = 0; c < C; ++c) {
+        XMOE_CUDA(cudaStreamWaitEvent(st, L.evA[c], 0));
+        if (dist) launch_flag_wait(L.workers[0].flags, W, slot_A(c), L.epoch, st);
+        if (L.timing) XMOE_CUDA(cudaEventRecord(L.tl[4 * c + 1], st));
+        const size_t r0 = static_cast<size_t>(c) * L.Rc;
+        g_copy_blocks = 0;
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            if (rbd)  // replicas copy the row from their pilot's slot
+                launch_rbd_expand(static_cast<int>(rb), w.desc_recv, w.rbd, c, L.R_max, w.recv, w.gstart, st);
+            launch_grouped_gemm_bf16(static_cast<char*>(w.recv) + r0 * rb, L.Rc, H, w.rpe_c + c * El, El,
+                                     w1_of(L, w.rank), F, static_cast<char*>(w.mid) + r0 * F * L.es, 1, st);
+            launch_grouped_gemm_bf16(static_cast<char*>(w.mid) + r0 * F * L.es, L.Rc, F, w.rpe_c + c * El, El,
+                                     w2_of(L, w.rank), H, static_cast<char*>(w.eout) + r0 * rb, 0, st);
+            if (rbd)  // weighted sum of each group's outputs, pilot first (rbd.cpp:318-336)
+                launch_rbd_merge(XMOE_BF16, w.eout, H, w.desc_recv, w.gstart, w.rbd, c,
+                                 static_cast<long long>(W) * S, w.back_u, st);
+        }
+        if (L.timing) XMOE_CUDA(cudaEventRecord(L.tl[4 * c + 2], st));
+        if (dist) launch_flag_signal(L.flag_tab, W, me, slot_B(c), L.epoch, st);
+        XMOE_CUDA(cudaEventRecord(L.evB[c], st));
+    }
+    L.mark(kEvGemm, st);
+    L.mark(kEvShared, st);
+    // 4. comm: each chunk's weighted combine as soon as every owner finished
+    //    it (pf_pipeline.cpp:107-135)
+    for (int c = 0; c < C; ++c) {
+        g_copy_blocks = c == C - 1 ? 0 : blk_combine;  // the last combine runs alone
+        XMOE_CUDA(cudaStreamWaitEvent(cm, L.evB[c], 0));
+        if (dist) launch_flag_wait(L.workers[0].flags, W, slot_B(c), L.epoch, cm);
+        if (c == C - 1) L.mark(kEvReturn, cm);
+        const int t0 = t0_of(c), n = t0_of(c + 1) - t0;
+        if (n == 0) continue;
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            if (rbd) {  // one merged row per group, in pilot order (rbd.cpp:343-356)
+                launch_rbd_combine(XMOE_BF16, L.back_tab, H, static_cast<int>(S), w.rbd, c, w.cw,
+                                   L.Fs > 0 ? w.sout : nullptr, o_of(i), cm);
+                continue;
+            }
+            launch_combine_slots(w.slot_src + static_cast<size_t>(t0) * k, w.slot_w + static_cast<size_t>(t0) * k,
+                                 k, H, n, L.Fs > 0 ? static_cast<const char*>(w.sout) + t0 * rb : nullptr,
+                                 o_of(i) + static_cast<size_t>(t0) * rb, cm);
+        }
+        if (L.timing) XMOE_CUDA(cudaEventRecord(L.tl[4 * c + 3], cm));
+    }
+    g_copy_blocks = 0;
+    XMOE_CUDA(cudaEventRecord(L.ev_done, cm));
+    XMOE_CUDA(cudaStreamWaitEvent(st, L.ev_done, 0));
+    L.mark(kEvCombine, st);
+    L.last_S = S;
+}
+
 // ---------------------------------------------------------------- forward
 // x/out: [nl, S, H] (nl = ranks this process drives).
 void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t st) {
     Ctx& ctx = *L.ctx;
     require(S >= 0 && S <= L.S_max, XMOE_ERR_VALIDATION, "sequence longer than the layer's max_tokens");
+    if (L.nchunks > 1 && S > 0) {
+        layer_forward_chunked(L, x, S, out, st);
+        return;
+    }
     const int W = L.W, E = L.E, H = L.H, F = L.F, k = L.k;
     const int dt = L.d.dtype;
     const size_t row_bytes = static_cast<size_t>(H) * L.es;
@@ -439,11 +674,19 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     L.mark(kEvGate, st);
     // 1b. shared experts depend on x only: they run on a side stream, concurrent
     //     with PFT and the exchange, and join before the combine.  Forked after
-    //     the gate so the two persistent GEMMs do not contend for SMs.
-    if (L.Fs > 0) {
+    //     the gate so the two persistent GEMMs do not contend for SMs.  Timing
+    //     mode issues them in line at the join instead, so that every stage
+    //     (and "shared") is an isolated kernel time.
+    auto issue_shared = [&](cudaStream_t ss) {
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            run_gemm(dt, x_of(i), S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, ss);
+            run_gemm(dt, w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, w.sout, 0, ss);
+        }
+    };
+    if (L.Fs > 0 && !L.timing) {
         XMOE_CUDA(cudaEventRecord(L.ev_fork, st));
         XMOE_CUDA(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
-        if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side0, L.side));
         // leave SMs to the routing / exchange kernels running beside it
         // (multi-GPU only: at N=1 there is no exchange to overlap)
         static const int shared_sms = [] {
@@ -451,13 +694,8 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
             return e ? std::atoi(e) : 104;
         }();
         g_gemm_sm_limit = dist ? shared_sms : 0;
-        for (int i = 0; i < nl; ++i) {
-            Worker& w = L.workers[i];
-            run_gemm(dt, x_of(i), S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, L.side);
-            run_gemm(dt, w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, w.sout, 0, L.side);
-        }
+        issue_shared(L.side);
         g_gemm_sm_limit = 0;
-        if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side1, L.side));
         XMOE_CUDA(cudaEventRecord(L.ev_join, L.side));
     }
     // 2. padding-free token buffer (pft.cpp:12-60) [+ RBD groups and pilots, rbd.cpp:26-81]
@@ -470,6 +708,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
                               w.rbd, st);
             launch_rbd_sort(W, nk, w.rbd, st);
             launch_adjacent_diff(w.rbd.dptr, W, L.G_all + static_cast<size_t>(w.rank) * W, st);
+            launch_rbd_chunk_counts(W, static_cast<int>(S), w.rbd, st);
         }
     }
     L.mark(kEvPft, st);
@@ -481,8 +720,10 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         auto comm = static_cast<ncclComm_t>(ctx.nccl);
         XMOE_NCCL(ncclGroupStart());
         XMOE_NCCL(ncclAllGather(w.tpe, L.tpe_all, E, ncclInt32, comm, st));
-        if (rbd)
+        if (rbd) {
             XMOE_NCCL(ncclAllGather(L.G_all + static_cast<size_t>(w.rank) * W, L.G_all, W, ncclInt32, comm, st));
+            XMOE_NCCL(ncclAllGather(w.rbd.gd_own, L.gd_all, 2 * W, ncclInt32, comm, st));
+        }
         XMOE_NCCL(ncclGroupEnd());
     }
     L.mark(kEvCounts, st);
@@ -495,16 +736,15 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     if (rbd) {
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
-            launch_rbd_offsets(L.G_all, L.tpe_all, W, E, w.rank, w.rbd, st);
-            launch_rbd_pack(x_of(i), static_cast<int>(row_bytes), w.rbd, nk, w.slot_pos, k, w.dest_row, w.cw,
-                            L.recv_tab, L.desc_tab, st);
+            launch_rbd_offsets(L.gd_all, W, w.rank, w.rbd, st);
+            launch_rbd_pack(x_of(i), static_cast<int>(row_bytes), w.rbd, W, 0, nk, w.slot_pos, k, w.dest_row,
+                            w.cw, L.recv_tab, L.desc_tab, st);
         }
         L.mark(kEvMoved, st);
         if (dist) L.barrier(st);
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
-            launch_rbd_expand(w.recv_u, static_cast<int>(row_bytes), w.desc_recv, w.rbd.rx, L.R_max, w.recv,
-                              w.gstart, st);
+            launch_rbd_expand(static_cast<int>(row_bytes), w.desc_recv, w.rbd, 0, L.R_max, w.recv, w.gstart, st);
         }
     } else if (tables) {
         for (int i = 0; i < nl; ++i) {
@@ -536,20 +776,29 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         run_gemm(dt, w.mid, L.R_max, F, w.rpe, L.El, w2_of(L, w.rank), H, w.eout, 0, st);
     }
     L.mark(kEvGemm, st);
-    if (L.Fs > 0) XMOE_CUDA(cudaStreamWaitEvent(st, L.ev_join, 0));
+    if (L.Fs > 0) {
+        if (L.timing) {
+            XMOE_CUDA(cudaEventRecord(L.ev_side0, st));
+            issue_shared(st);
+            XMOE_CUDA(cudaEventRecord(L.ev_side1, st));
+        } else {
+            XMOE_CUDA(cudaStreamWaitEvent(st, L.ev_join, 0));
+        }
+    }
     L.mark(kEvShared, st);
     // 6. return path + weighted combine (pf_pipeline.cpp:107-135, rbd.cpp:287-358)
     if (rbd) {
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
-            launch_rbd_merge(dt, w.eout, H, w.desc_recv, w.gstart, w.rbd.rx, static_cast<long long>(W) * S, w.back_u, st);
+            launch_rbd_merge(dt, w.eout, H, w.desc_recv, w.gstart, w.rbd, 0, static_cast<long long>(W) * S,
+                             w.back_u, st);
         }
         if (dist) L.barrier(st);
         L.mark(kEvReturn, st);
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
-            launch_rbd_combine(dt, L.back_tab, H, static_cast<int>(S), w.rbd, w.cw, L.Fs > 0 ? w.sout : nullptr,
-                               o_of(i), st);
+            launch_rbd_combine(dt, L.back_tab, H, static_cast<int>(S), w.rbd, 0, w.cw,
+                               L.Fs > 0 ? w.sout : nullptr, o_of(i), st);
         }
     } else if (tables) {
         if (dist) L.barrier(st);

@@ -83,6 +83,13 @@ struct Worker {
     void* dHs = nullptr;          // [S, Fs]
     void* dxs = nullptr;          // [S, H] shared part of dx
     unsigned long long* bslot_src = nullptr;  // [S*k] dxc row of each kept copy
+    // token-chunked pipeline (chunk.cu)
+    int32_t* tpe_c = nullptr;     // [C, E] my kept copies per (chunk, expert)
+    int32_t* pfx_c = nullptr;     // [C, E] their offset inside the expert's packed segment
+    int32_t* seg = nullptr;       // [E] packed segment start of each expert
+    int32_t* cbase = nullptr;     // [C, E] first destination row of (chunk, expert) at its owner
+    int32_t* rpe_c = nullptr;     // [C, El] rows per local expert in my chunk regions
+    unsigned* flags = nullptr;    // [2, kMaxChunks, W] epoch flags (symmetric region)
 };
 
 // stage boundaries; kEvCounts/kEvMoved/kEvReturn split the exchange phases
@@ -148,6 +155,18 @@ struct Layer {
     cudaStream_t cap_stream = nullptr;
     cudaStream_t side = nullptr;  // shared-expert GEMMs overlap routing + exchange
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_side0 = nullptr, ev_side1 = nullptr;
+    // token-chunked pipeline: C chunks of Rc rows per owner, comm stream for
+    // the row movement, per-chunk events and cross-GPU epoch flags
+    int nchunks = 1;
+    int Rc = 0;
+    int32_t* tpe_c_all = nullptr;  // [W, C, E]
+    int32_t* gd_all = nullptr;     // RBD [W_src, 2, W, C] groups / copies per (dest, chunk)
+    unsigned** flag_tab = nullptr; // rank -> its flags (peer addresses)
+    unsigned* epoch = nullptr;     // forwards issued (device)
+    cudaStream_t comm = nullptr;
+    std::vector<cudaEvent_t> evA, evB;
+    std::vector<cudaEvent_t> tl;   // timing: per chunk scatter end, GEMM start, GEMM end, combine end
+    cudaEvent_t ev_done = nullptr;
 
     void* alloc(size_t bytes);
     void mark(int ev, cudaStream_t st);

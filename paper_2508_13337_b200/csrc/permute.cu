@@ -14,6 +14,8 @@
 
 namespace xmoe {
 
+thread_local int g_copy_blocks = 0;
+
 constexpr int kRowWarps = 8;
 constexpr int kUnroll = 8;
 
@@ -348,7 +350,8 @@ void launch_scatter_tokens(const void* x, int row_bytes, int S, int k, const int
     require((row_bytes & 15) == 0 && k <= 32, XMOE_ERR_VALIDATION, "token scatter needs 16-byte rows, k <= 32");
     if (S == 0) return;
     long long blocks = (static_cast<long long>(S) + kTokWarps - 1) / kTokWarps;
-    if (blocks > 8 * kNumSMs) blocks = 8 * kNumSMs;
+    const long long cap = g_copy_blocks > 0 ? g_copy_blocks : 8LL * kNumSMs;
+    if (blocks > cap) blocks = cap;
     scatter_tokens_kernel<<<static_cast<int>(blocks), 32 * kTokWarps, 0, st>>>(
         static_cast<const char*>(x), row_bytes, S, k, slot_pos, dest_rank, dest_row, cw, dest_bufs, src_bufs,
         slot_src, slot_w, tr);

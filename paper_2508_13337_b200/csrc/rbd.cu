@@ -280,86 +280,145 @@ __global__ void rbd_group_pos_kernel(const int32_t* __restrict__ perm, const int
     nsorted[pos] = g.n[gid];
 }
 
-// Per-source offsets for the table transport, all on the device (no host
-// sync): for every destination d,
-//   ru_base[d]  first row of my groups in d's unique-row buffer
-//               (groups of sources < me come first)
-//   rd_base[d]  first slot of my descriptors in d's descriptor buffer
-//   cseg[d]     first descriptor of my dest-d segment in my own order
-// and, for me as a receiver, the totals I will receive (rx[0] groups,
-// rx[1] descriptors).
-__global__ void rbd_offsets_kernel(const int32_t* __restrict__ G_all, const int32_t* __restrict__ tpe_all,
-                                   int W, int E, int me, const int32_t* __restrict__ dptr,
-                                   const int32_t* __restrict__ coff, int32_t* __restrict__ ru_base,
-                                   int32_t* __restrict__ rd_base, int32_t* __restrict__ cseg,
-                                   int32_t* __restrict__ rx) {
-    const int El = E / W;
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    auto C = [&](int s, int d) {
-        int a = 0;
-        for (int le = 0; le < El; ++le) a += tpe_all[s * E + d * El + le];
-        return a;
-    };
-    for (int d = 0; d < W; ++d) {
-        int g = 0, c = 0;
-        for (int s = 0; s < me; ++s) {
-            g += G_all[s * W + d];
-            c += C(s, d);
+__device__ __forceinline__ int rbd_chunk_t0(int c, int S, int C) {
+    return static_cast<int>(static_cast<long long>(c) * S / C);
+}
+
+// first descriptor (my order) of sorted position p; p == G gives the total
+__device__ __forceinline__ int rbd_coff_at(const int32_t* coff, const int32_t* nsorted, int G, int p) {
+    return p < G ? coff[p] : (G > 0 ? coff[G - 1] + nsorted[G - 1] : 0);
+}
+
+// Sender side, before the count all-gather: chunk boundaries inside every
+// dest segment (binary search on the token; segments are token-ordered) and
+// the groups / copies per (dest, chunk).
+__global__ void rbd_chunk_counts_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ G_dev,
+                                        const int32_t* __restrict__ gtoken, const int32_t* __restrict__ dptr,
+                                        const int32_t* __restrict__ coff, const int32_t* __restrict__ nsorted,
+                                        int W, int S, int C, int32_t* __restrict__ gpos,
+                                        int32_t* __restrict__ gd_own) {
+    const int G = *G_dev;
+    for (int idx = threadIdx.x; idx < W * (C + 1); idx += blockDim.x) {
+        const int d = idx / (C + 1), c = idx % (C + 1);
+        const int b = dptr[d], n = dptr[d + 1] - b;
+        int v;
+        if (c == 0) v = 0;
+        else if (c == C) v = n;
+        else {
+            const int t0 = rbd_chunk_t0(c, S, C);
+            int lo = 0, hi = n;
+            while (lo < hi) {
+                const int m = (lo + hi) >> 1;
+                if (gtoken[perm[b + m]] < t0) lo = m + 1;
+                else hi = m;
+            }
+            v = lo;
         }
-        ru_base[d] = g;
-        rd_base[d] = c;
-        cseg[d] = dptr[d] < dptr[W] ? coff[dptr[d]] : 0;
+        gpos[idx] = v;
     }
-    int g = 0, c = 0;
-    for (int s = 0; s < W; ++s) {
-        g += G_all[s * W + me];
-        c += C(s, me);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < W * C; idx += blockDim.x) {
+        const int d = idx / C, c = idx % C;
+        const int p0 = dptr[d] + gpos[d * (C + 1) + c], p1 = dptr[d] + gpos[d * (C + 1) + c + 1];
+        gd_own[idx] = p1 - p0;  // groups
+        gd_own[W * C + idx] = rbd_coff_at(coff, nsorted, G, p1) - rbd_coff_at(coff, nsorted, G, p0);  // copies
     }
-    rx[0] = g;
-    rx[1] = c;
+}
+
+// Offsets, all on the device (no host sync).  Receivers keep groups and
+// descriptors in (chunk, source, sender order):
+//   ru[d][c]  first row of my chunk-c groups in d's merged-row buffer
+//   rd[d][c]  first slot of my chunk-c descriptors in d's descriptor buffer
+//   cs[d][c]  first descriptor of my (d, c) segment in my own order
+//   rx[.][c]  what I receive in chunk c: group base / count, descriptor base / count
+__global__ void rbd_offsets_kernel(const int32_t* __restrict__ gd_all, int W, int C, int me,
+                                   const int32_t* __restrict__ gpos, const int32_t* __restrict__ dptr,
+                                   const int32_t* __restrict__ coff, const int32_t* __restrict__ nsorted,
+                                   const int32_t* __restrict__ G_dev, int32_t* __restrict__ ru,
+                                   int32_t* __restrict__ rd, int32_t* __restrict__ cs,
+                                   int32_t* __restrict__ rx) {
+    auto GD = [&](int s, int which, int d, int c) {
+        return gd_all[((static_cast<size_t>(s) * 2 + which) * W + d) * C + c];
+    };
+    const int G = *G_dev;
+    for (int idx = threadIdx.x; idx < W * C; idx += blockDim.x) {
+        const int d = idx / C, c = idx % C;
+        int g = 0, q = 0;
+        for (int c2 = 0; c2 < c; ++c2)
+            for (int s = 0; s < W; ++s) {
+                g += GD(s, 0, d, c2);
+                q += GD(s, 1, d, c2);
+            }
+        for (int s = 0; s < me; ++s) {
+            g += GD(s, 0, d, c);
+            q += GD(s, 1, d, c);
+        }
+        ru[idx] = g;
+        rd[idx] = q;
+        cs[idx] = rbd_coff_at(coff, nsorted, G, dptr[d] + gpos[d * (C + 1) + c]);
+    }
+    if (threadIdx.x == 0) {
+        int gb = 0, qb = 0;
+        for (int c = 0; c < C; ++c) {
+            int g = 0, q = 0;
+            for (int s = 0; s < W; ++s) {
+                g += GD(s, 0, me, c);
+                q += GD(s, 1, me, c);
+            }
+            rx[c] = gb;
+            rx[C + c] = g;
+            rx[2 * C + c] = qb;
+            rx[3 * C + c] = q;
+            gb += g;
+            qb += q;
+        }
+    }
 }
 
 // Sender pack: each group's row goes once, straight into the destination's
 // unique-row buffer, with one descriptor per copy (tables hold local or
 // NVLink-mapped peer pointers).
 __global__ void __launch_bounds__(256) rbd_pack_kernel(
-    const char* __restrict__ x, int row_bytes, const int32_t* __restrict__ perm,
-    const int32_t* __restrict__ G_dev, const RbdGroups g, const int32_t* __restrict__ dptr,
-    const int32_t* __restrict__ coff, const int32_t* __restrict__ ru_base,
-    const int32_t* __restrict__ rd_base, const int32_t* __restrict__ cseg,
-    const int32_t* __restrict__ slot_pos, int k, const int32_t* __restrict__ dest_row,
-    const double* __restrict__ cw, char* const* __restrict__ recv_u_tab,
-    RbdDesc* const* __restrict__ desc_tab) {
-    const int G = *G_dev;
+    const char* __restrict__ x, int row_bytes, const int32_t* __restrict__ perm, const RbdGroups g,
+    const int32_t* __restrict__ dptr, const int32_t* __restrict__ coff, const int32_t* __restrict__ gpos,
+    const int32_t* __restrict__ ru, const int32_t* __restrict__ rd, const int32_t* __restrict__ cs, int W,
+    int C, int c, const int32_t* __restrict__ slot_pos, int k, const int32_t* __restrict__ dest_row,
+    const double* __restrict__ cw, char* const* __restrict__ recv_u_tab, RbdDesc* const* __restrict__ desc_tab) {
     const int lane = threadIdx.x & 31;
     const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-    for (long long pos = warp; pos < G; pos += nwarps) {
-        const int gid = perm[pos];
-        const int t = g.token[gid], d = g.dest[gid], n = g.n[gid], j0 = g.first_slot[gid];
-        const int pilot = g.pilot[gid];
-        const int u = ru_base[d] + static_cast<int>(pos - dptr[d]);
-        if (lane < n) {
-            const int p = slot_pos[static_cast<size_t>(t) * k + j0 + lane];
-            RbdDesc dd;
-            dd.u = u;
-            dd.dest_row = dest_row[p];
-            dd.w = cw[p];
-            dd.n = n;
-            dd.member = lane | (p == pilot ? kRbdPilotFlag : 0);
-            desc_tab[d][rd_base[d] + (coff[pos] - cseg[d]) + lane] = dd;
-        }
-        // the row lands once, at the pilot's slot of the receiver's grouped
-        // expert input; the receiver copies it to the replicas' slots
-        const char* src = x + static_cast<size_t>(t) * row_bytes;
-        char* dst = recv_u_tab[d] + static_cast<size_t>(dest_row[pilot]) * row_bytes;
-        if ((row_bytes & 15) == 0) {
-            const int4* s4 = reinterpret_cast<const int4*>(src);
-            int4* d4 = reinterpret_cast<int4*>(dst);
-            for (int v = lane; v < (row_bytes >> 4); v += 32) st_na_v4(d4 + v, ld_nc_v4(s4 + v));
-        } else {
-            for (int v = lane; v < (row_bytes >> 3); v += 32)
-                reinterpret_cast<long long*>(dst)[v] = reinterpret_cast<const long long*>(src)[v];
+    for (int d = 0; d < W; ++d) {
+        const int beg = dptr[d] + gpos[d * (C + 1) + c];
+        const int cnt = dptr[d] + gpos[d * (C + 1) + c + 1] - beg;
+        const int ub = ru[d * C + c], db = rd[d * C + c], cb = cs[d * C + c];
+        for (long long i = warp; i < cnt; i += nwarps) {
+            const int pos = beg + static_cast<int>(i);
+            const int gid = perm[pos];
+            const int t = g.token[gid], n = g.n[gid], j0 = g.first_slot[gid];
+            const int pilot = g.pilot[gid];
+            const int u = ub + static_cast<int>(i);
+            if (lane < n) {
+                const int p = slot_pos[static_cast<size_t>(t) * k + j0 + lane];
+                RbdDesc dd;
+                dd.u = u;
+                dd.dest_row = dest_row[p];
+                dd.w = cw[p];
+                dd.n = n;
+                dd.member = lane | (p == pilot ? kRbdPilotFlag : 0);
+                desc_tab[d][db + (coff[pos] - cb) + lane] = dd;
+            }
+            // the row lands once, at the pilot's slot of the receiver's grouped
+            // expert input; the receiver copies it to the replicas' slots
+            const char* src = x + static_cast<size_t>(t) * row_bytes;
+            char* dst = recv_u_tab[d] + static_cast<size_t>(dest_row[pilot]) * row_bytes;
+            if ((row_bytes & 15) == 0) {
+                const int4* s4 = reinterpret_cast<const int4*>(src);
+                int4* d4 = reinterpret_cast<int4*>(dst);
+                for (int v = lane; v < (row_bytes >> 4); v += 32) st_na_v4(d4 + v, ld_nc_v4(s4 + v));
+            } else {
+                for (int v = lane; v < (row_bytes >> 3); v += 32)
+                    reinterpret_cast<long long*>(dst)[v] = reinterpret_cast<const long long*>(src)[v];
+            }
         }
     }
     __threadfence_system();
@@ -370,14 +429,15 @@ __global__ void __launch_bounds__(256) rbd_pack_kernel(
 // group's first descriptor for the merge.
 __global__ void __launch_bounds__(256) rbd_expand_kernel(const char* __restrict__ recv_u,
                                                          int row_bytes, const RbdDesc* __restrict__ desc,
-                                                         const int32_t* __restrict__ rx, char* __restrict__ grouped,
+                                                         const int32_t* __restrict__ rx, int C, int ck,
+                                                         char* __restrict__ grouped,
                                                          int32_t* __restrict__ gstart) {
     (void)recv_u;
-    const int ndesc = rx[1];
+    const int dbeg = rx[2 * C + ck], dend = dbeg + rx[3 * C + ck];
     const int lane = threadIdx.x & 31;
     const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-    for (long long c = warp; c < ndesc; c += nwarps) {
+    for (long long c = dbeg + warp; c < dend; c += nwarps) {
         const RbdDesc dd = desc[c];
         const int m = dd.member & ~kRbdPilotFlag;
         if (lane == 0 && m == 0) gstart[dd.u] = static_cast<int>(c);
@@ -404,13 +464,13 @@ template <typename T>
 __global__ void __launch_bounds__(256) rbd_merge_kernel(const T* __restrict__ eout, int H,
                                                         const RbdDesc* __restrict__ desc,
                                                         const int32_t* __restrict__ gstart,
-                                                        const int32_t* __restrict__ rx,
+                                                        const int32_t* __restrict__ rx, int C, int ck,
                                                         T* __restrict__ back_u) {
-    const int ngroups = rx[0];
+    const int ubeg = rx[ck], uend = ubeg + rx[C + ck];
     const int lane = threadIdx.x & 31;
     const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-    for (long long u = warp; u < ngroups; u += nwarps) {
+    for (long long u = ubeg + warp; u < uend; u += nwarps) {
         const int c0 = gstart[u];
         const int n = desc[c0].n;
         T* out = back_u + static_cast<size_t>(u) * H;
@@ -451,13 +511,14 @@ template <typename T>
 __global__ void __launch_bounds__(256) rbd_combine_kernel(const char* const* __restrict__ back_tab, int H,
                                                           int S, const int32_t* __restrict__ gbase,
                                                           const int32_t* __restrict__ gcount,
-                                                          const RbdGroups g, const int32_t* __restrict__ ru_base,
+                                                          const RbdGroups g, const int32_t* __restrict__ ru,
+                                                          const int32_t* __restrict__ gpos, int C, int ck,
                                                           const int32_t* __restrict__ dptr,
                                                           const double* __restrict__ cw,
                                                           const T* __restrict__ addend, T* __restrict__ out) {
-    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int t = rbd_chunk_t0(ck, S, C) + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
-    if (t >= S) return;
+    if (t >= rbd_chunk_t0(ck + 1, S, C)) return;
     const int b = gbase[t], n = gcount[t];
     // groups of a token are few (<= min(k, W)): order them by pilot packed row
     int order[32];
@@ -476,7 +537,7 @@ __global__ void __launch_bounds__(256) rbd_combine_kernel(const char* const* __r
         const int gid = b + order[i];
         const int d = g.dest[gid];
         rowp[i] = reinterpret_cast<const T*>(back_tab[d]) +
-                  static_cast<size_t>(ru_base[d] + g.pos[gid] - dptr[d]) * H;
+                  static_cast<size_t>(ru[d * C + ck] + g.pos[gid] - dptr[d] - gpos[d * (C + 1) + ck]) * H;
     }
     for (int h = lane; h < H; h += 32) {
         if constexpr (sizeof(T) == 8) {
@@ -507,16 +568,16 @@ __global__ void __launch_bounds__(256) rbd_combine_kernel(const char* const* __r
 __global__ void __launch_bounds__(256) rbd_merge_bf16_kernel(const __nv_bfloat16* __restrict__ eout, int H,
                                                              const RbdDesc* __restrict__ desc,
                                                              const int32_t* __restrict__ gstart,
-                                                             const int32_t* __restrict__ rx,
+                                                             const int32_t* __restrict__ rx, int C, int ck,
                                                              __nv_bfloat16* __restrict__ back_u) {
-    const int ngroups = rx[0];
+    const int ubeg = rx[ck], ngroups = rx[C + ck];
     const int nseg = (H + 511) / 512;
     const int lane = threadIdx.x & 31;
     const int nchunk = H >> 3;
     const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
     for (long long item = warp; item < static_cast<long long>(ngroups) * nseg; item += nwarps) {
-        const int u = static_cast<int>(item / nseg), seg = static_cast<int>(item % nseg);
+        const int u = ubeg + static_cast<int>(item / nseg), seg = static_cast<int>(item % nseg);
         const int c0 = gstart[u];
         const int n = desc[c0].n;
         int my_row = 0;
@@ -584,14 +645,15 @@ __global__ void __launch_bounds__(256) rbd_merge_bf16_kernel(const __nv_bfloat16
 // the warp then permutes them into pilot order and streams the rows.
 __global__ void __launch_bounds__(256) rbd_combine_bf16_kernel(
     const char* const* __restrict__ back_tab, int H, int S, const int32_t* __restrict__ gbase,
-    const int32_t* __restrict__ gcount, const RbdGroups g, const int32_t* __restrict__ ru_base,
-    const int32_t* __restrict__ dptr, const double* __restrict__ cw,
-    const __nv_bfloat16* __restrict__ addend, __nv_bfloat16* __restrict__ out) {
+    const int32_t* __restrict__ gcount, const RbdGroups g, const int32_t* __restrict__ ru,
+    const int32_t* __restrict__ gpos, int C, int ck, const int32_t* __restrict__ dptr,
+    const double* __restrict__ cw, const __nv_bfloat16* __restrict__ addend, __nv_bfloat16* __restrict__ out) {
     const int nseg = (H + 511) / 512;
+    const int t0 = rbd_chunk_t0(ck, S, C), nt = rbd_chunk_t0(ck + 1, S, C) - t0;
     const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (gw >= static_cast<long long>(S) * nseg) return;
-    const int t = static_cast<int>(gw / nseg), seg = static_cast<int>(gw % nseg);
+    if (gw >= static_cast<long long>(nt) * nseg) return;
+    const int t = t0 + static_cast<int>(gw / nseg), seg = static_cast<int>(gw % nseg);
     const int b = gbase[t], n = min(gcount[t], 32);
     int key = 0x7fffffff;
     unsigned long long rp = 0;
@@ -602,7 +664,7 @@ __global__ void __launch_bounds__(256) rbd_combine_bf16_kernel(
         key = g.pilot[gid];
         rp = reinterpret_cast<unsigned long long>(
             reinterpret_cast<const __nv_bfloat16*>(back_tab[d]) +
-            static_cast<size_t>(ru_base[d] + g.pos[gid] - dptr[d]) * H);
+            static_cast<size_t>(ru[d * C + ck] + g.pos[gid] - dptr[d] - gpos[d * (C + 1) + ck]) * H);
         sc = g.n[gid] > 1 ? 1.f : static_cast<float>(cw[key]);
     }
     int rank = 0;  // position of my group in pilot order (rbd.cpp:343-356)
@@ -686,58 +748,71 @@ void launch_rbd_sort(int W, long long max_groups, RbdWork& wk, cudaStream_t st) 
     scan_i32(wk.nsorted, static_cast<int>(max_groups), wk.G_dev, wk.coff, nullptr, st);
 }
 
-void launch_rbd_offsets(const int32_t* G_all, const int32_t* tpe_all, int W, int E, int me, RbdWork& wk,
-                        cudaStream_t st) {
-    rbd_offsets_kernel<<<1, 32, 0, st>>>(G_all, tpe_all, W, E, me, wk.dptr, wk.coff, wk.ru_base,
-                                         wk.rd_base, wk.cseg, wk.rx);
+void launch_rbd_chunk_counts(int W, int S, RbdWork& wk, cudaStream_t st) {
+    rbd_chunk_counts_kernel<<<1, 256, 0, st>>>(wk.perm, wk.G_dev, wk.g.token, wk.dptr, wk.coff, wk.nsorted, W,
+                                               S, wk.C, wk.gpos, wk.gd_own);
     XMOE_LAUNCH_CHECK();
 }
 
-void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, long long max_groups,
+void launch_rbd_offsets(const int32_t* gd_all, int W, int me, RbdWork& wk, cudaStream_t st) {
+    rbd_offsets_kernel<<<1, 256, 0, st>>>(gd_all, W, wk.C, me, wk.gpos, wk.dptr, wk.coff, wk.nsorted, wk.G_dev,
+                                          wk.ru, wk.rd, wk.cs, wk.rx);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, int W, int c, long long max_groups,
                      const int32_t* slot_pos, int k, const int32_t* dest_row, const double* cw,
                      char* const* recv_u_tab, RbdDesc* const* desc_tab, cudaStream_t st) {
-    rbd_pack_kernel<<<warp_grid(max_groups), 256, 0, st>>>(
-        static_cast<const char*>(x), row_bytes, wk.perm, wk.G_dev, wk.g, wk.dptr, wk.coff, wk.ru_base,
-        wk.rd_base, wk.cseg, slot_pos, k, dest_row, cw, recv_u_tab, desc_tab);
+    int grid = warp_grid(max_groups / wk.C + 1);
+    if (g_copy_blocks > 0 && grid > g_copy_blocks) grid = g_copy_blocks;
+    rbd_pack_kernel<<<grid, 256, 0, st>>>(static_cast<const char*>(x), row_bytes, wk.perm, wk.g, wk.dptr, wk.coff,
+                                          wk.gpos, wk.ru, wk.rd, wk.cs, W, wk.C, c, slot_pos, k, dest_row, cw,
+                                          recv_u_tab, desc_tab);
     XMOE_LAUNCH_CHECK();
 }
 
-void launch_rbd_expand(const void* recv_u, int row_bytes, const RbdDesc* desc, const int32_t* rx,
-                       long long max_desc, void* grouped, int32_t* gstart, cudaStream_t st) {
-    rbd_expand_kernel<<<warp_grid(max_desc), 256, 0, st>>>(static_cast<const char*>(recv_u), row_bytes,
-                                                           desc, rx, static_cast<char*>(grouped), gstart);
+void launch_rbd_expand(int row_bytes, const RbdDesc* desc, const RbdWork& wk, int c, long long max_desc,
+                       void* grouped, int32_t* gstart, cudaStream_t st) {
+    int grid = warp_grid(max_desc / wk.C + 1);
+    if (g_copy_blocks > 0 && grid > g_copy_blocks) grid = g_copy_blocks;
+    rbd_expand_kernel<<<grid, 256, 0, st>>>(nullptr, row_bytes, desc, wk.rx, wk.C, c,
+                                            static_cast<char*>(grouped), gstart);
     XMOE_LAUNCH_CHECK();
 }
 
 void launch_rbd_merge(int dtype, const void* eout, int H, const RbdDesc* desc, const int32_t* gstart,
-                      const int32_t* rx, long long max_groups, void* back_u, cudaStream_t st) {
+                      const RbdWork& wk, int c, long long max_groups, void* back_u, cudaStream_t st) {
+    const long long per = max_groups / wk.C + 1;
+    auto cap = [](int g) { return g_copy_blocks > 0 && g > g_copy_blocks ? g_copy_blocks : g; };
     if (dtype == XMOE_F64)
-        rbd_merge_kernel<double><<<warp_grid(max_groups), 256, 0, st>>>(
-            static_cast<const double*>(eout), H, desc, gstart, rx, static_cast<double*>(back_u));
+        rbd_merge_kernel<double><<<cap(warp_grid(per)), 256, 0, st>>>(
+            static_cast<const double*>(eout), H, desc, gstart, wk.rx, wk.C, c, static_cast<double*>(back_u));
     else if (H % 8 == 0)
-        rbd_merge_bf16_kernel<<<warp_grid(max_groups * ((H + 511) / 512)), 256, 0, st>>>(
-            static_cast<const __nv_bfloat16*>(eout), H, desc, gstart, rx, static_cast<__nv_bfloat16*>(back_u));
+        rbd_merge_bf16_kernel<<<cap(warp_grid(per * ((H + 511) / 512))), 256, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(eout), H, desc, gstart, wk.rx, wk.C, c,
+            static_cast<__nv_bfloat16*>(back_u));
     else
-        rbd_merge_kernel<__nv_bfloat16><<<warp_grid(max_groups), 256, 0, st>>>(
-            static_cast<const __nv_bfloat16*>(eout), H, desc, gstart, rx,
+        rbd_merge_kernel<__nv_bfloat16><<<cap(warp_grid(per)), 256, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(eout), H, desc, gstart, wk.rx, wk.C, c,
             static_cast<__nv_bfloat16*>(back_u));
     XMOE_LAUNCH_CHECK();
 }
 
-void launch_rbd_combine(int dtype, const char* const* back_tab, int H, int S, const RbdWork& wk,
+void launch_rbd_combine(int dtype, const char* const* back_tab, int H, int S, const RbdWork& wk, int c,
                         const double* cw, const void* addend, void* out, cudaStream_t st) {
-    if (S == 0) return;
+    const int nt = static_cast<int>(static_cast<long long>(c + 1) * S / wk.C - static_cast<long long>(c) * S / wk.C);
+    if (nt == 0) return;
     if (dtype == XMOE_F64)
-        rbd_combine_kernel<double><<<ceil_div(S, 8), 256, 0, st>>>(
-            back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru_base, wk.dptr, cw,
+        rbd_combine_kernel<double><<<ceil_div(nt, 8), 256, 0, st>>>(
+            back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru, wk.gpos, wk.C, c, wk.dptr, cw,
             static_cast<const double*>(addend), static_cast<double*>(out));
     else if (H % 8 == 0)
-        rbd_combine_bf16_kernel<<<ceil_div(static_cast<long long>(S) * ((H + 511) / 512), 8), 256, 0, st>>>(
-            back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru_base, wk.dptr, cw,
+        rbd_combine_bf16_kernel<<<ceil_div(static_cast<long long>(nt) * ((H + 511) / 512), 8), 256, 0, st>>>(
+            back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru, wk.gpos, wk.C, c, wk.dptr, cw,
             static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out));
     else
-        rbd_combine_kernel<__nv_bfloat16><<<ceil_div(S, 8), 256, 0, st>>>(
-            back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru_base, wk.dptr, cw,
+        rbd_combine_kernel<__nv_bfloat16><<<ceil_div(nt, 8), 256, 0, st>>>(
+            back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru, wk.gpos, wk.C, c, wk.dptr, cw,
             static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out));
     XMOE_LAUNCH_CHECK();
 }

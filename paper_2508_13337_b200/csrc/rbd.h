@@ -45,10 +45,17 @@ struct RbdWork {
     int32_t* nsorted;  // [S*k] group size in sorted order
     int32_t* coff;     // [S*k] first descriptor of each sorted group
     void* csr_ws;
-    int32_t* ru_base;  // [W] my first row in each receiver's unique-row buffer
-    int32_t* rd_base;  // [W] my first descriptor slot at each receiver
-    int32_t* cseg;     // [W] first descriptor of my dest-d segment
-    int32_t* rx;       // [2] groups / descriptors I receive
+    // token chunks (chunk.cu; C = 1 when the forward is not chunked).  The
+    // receiver keeps its groups and descriptors in (chunk, source, sender
+    // order); a dest segment of the sender is token-ordered, so chunk c of
+    // it is the sub-range [gpos[d][c], gpos[d][c+1]).
+    int C;
+    int32_t* gpos;     // [W, C+1] chunk starts inside each dest segment
+    int32_t* gd_own;   // [2, W, C] my groups / copies per (dest, chunk)
+    int32_t* ru;       // [W, C] my first group row at receiver d for chunk c
+    int32_t* rd;       // [W, C] my first descriptor slot at receiver d for chunk c
+    int32_t* cs;       // [W, C] first descriptor (my order) of my (d, c) segment
+    int32_t* rx;       // [4, C] receiver: group base, groups, descriptor base, descriptors
     uint64_t state[4];  // Rng(salt_seed(seed, rank, 0)) state
 };
 
@@ -59,16 +66,19 @@ void rbd_jump_tables(std::vector<uint64_t>& out);
 void launch_rbd_groups(const int32_t* slot_pos, const int32_t* expert_ids, int S, int k, int El,
                        const uint64_t state[4], const uint64_t* jumps, RbdWork& wk, cudaStream_t st);
 void launch_rbd_sort(int W, long long max_groups, RbdWork& wk, cudaStream_t st);
-void launch_rbd_offsets(const int32_t* G_all, const int32_t* tpe_all, int W, int E, int me, RbdWork& wk,
-                        cudaStream_t st);
-void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, long long max_groups,
+// per (dest, chunk) group / copy counts of this sender (before the all-gather)
+void launch_rbd_chunk_counts(int W, int S, RbdWork& wk, cudaStream_t st);
+// offsets from every sender's counts gd_all [W_src, 2, W, C]
+void launch_rbd_offsets(const int32_t* gd_all, int W, int me, RbdWork& wk, cudaStream_t st);
+// chunk c (tokens [floor(cS/C), floor((c+1)S/C)))
+void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, int W, int c, long long max_groups,
                      const int32_t* slot_pos, int k, const int32_t* dest_row, const double* cw,
                      char* const* recv_u_tab, RbdDesc* const* desc_tab, cudaStream_t st);
-void launch_rbd_expand(const void* recv_u, int row_bytes, const RbdDesc* desc, const int32_t* rx,
-                       long long max_desc, void* grouped, int32_t* gstart, cudaStream_t st);
+void launch_rbd_expand(int row_bytes, const RbdDesc* desc, const RbdWork& wk, int c, long long max_desc,
+                       void* grouped, int32_t* gstart, cudaStream_t st);
 void launch_rbd_merge(int dtype, const void* eout, int H, const RbdDesc* desc, const int32_t* gstart,
-                      const int32_t* rx, long long max_groups, void* back_u, cudaStream_t st);
-void launch_rbd_combine(int dtype, const char* const* back_tab, int H, int S, const RbdWork& wk,
+                      const RbdWork& wk, int c, long long max_groups, void* back_u, cudaStream_t st);
+void launch_rbd_combine(int dtype, const char* const* back_tab, int H, int S, const RbdWork& wk, int c,
                         const double* cw, const void* addend, void* out, cudaStream_t st);
 
 // pft.cu: stable CSR with the item count on the device (bound n_max).

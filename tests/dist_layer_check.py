@@ -85,6 +85,50 @@ def main():
                   f"cap={cap} ledger={tot}", flush=True)
         del layer
         dist.barrier()
+    # token-chunked pipelined forward (epoch flags over NVLink): bit-identical
+    # to the unchunked layer, eager and graph-replayed, over repeated forwards
+    for ci, (S, cap_f, chunks, mode) in enumerate([(1000, None, 3, capi.NAIVE), (777, 0.6, 4, capi.NAIVE),
+                                                   (4096, None, 0, capi.NAIVE), (1000, None, 3, capi.RBD),
+                                                   (777, 0.6, 4, capi.RBD), (4096, None, 0, capi.RBD)]):
+        E, k, H, F = 16 * world, 6, 256, 128
+        el = E // world
+        rng = np.random.default_rng(300 + ci)
+        gate = grid_gate(rng, H, E)
+        w1 = bf16_round(rng.uniform(-0.1, 0.1, (E, H, F)))
+        w2 = bf16_round(rng.uniform(-0.1, 0.1, (E, F, H)))
+        sw1 = bf16_round(rng.uniform(-0.1, 0.1, (2, H, 128)))
+        sw2 = bf16_round(rng.uniform(-0.1, 0.1, (2, 128, H)))
+        x = grid_tokens(rng, world, S, H)
+        cap = S * k if cap_f is None else int(cap_f * S * k / E)
+        bv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).cuda()  # noqa: E731
+        outs = []
+        for c in (1, chunks):
+            layer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=cap,
+                               max_tokens=S, dtype=capi.BF16, gate=bv(gate), w1=bv(w1[rank * el:(rank + 1) * el]),
+                               w2=bv(w2[rank * el:(rank + 1) * el]), sw1=bv(sw1), sw2=bv(sw2), chunks=c,
+                               dispatch_mode=mode, seed=11)
+            xd = bv(x[rank])
+            o = [layer.forward(xd).clone() for _ in range(3)]
+            layer.set_graph(True)
+            ob = torch.empty_like(xd)
+            for _ in range(3):
+                layer.forward(xd, ob)
+            torch.cuda.synchronize()
+            o.append(ob.clone())
+            outs.append(o)
+            del layer
+            dist.barrier()
+        same = all(torch.equal(outs[0][0], t) for t in outs[0] + outs[1])
+        got = [None] * world
+        dist.all_gather_object(got, (same, outs[1][0].float().cpu().numpy()))
+        if rank == 0:
+            Wt = O.LayerWeights(gate, w1, w2)
+            want = [O.moe_layer_with_shared(x[r], Wt, E, k, cap, sw1, sw2, exact=False) for r in range(world)]
+            errs = [norm_rel(got[r][1], want[r]) for r in range(world)]
+            print(f"chunked case {ci} mode={mode} S={S} chunks={chunks} bit-identical={[g[0] for g in got]} err={max(errs):.2e}",
+                  flush=True)
+            if not all(g[0] for g in got) or max(errs) > 1e-2:
+                failures.append(("chunked", ci, [g[0] for g in got], errs))
     # backward over the peer transport (bf16, dropless): dx per rank, expert
     # grads of each rank's block, gate grads summed over ranks
     from oracle import moe_grad as Gr

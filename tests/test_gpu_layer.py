@@ -236,3 +236,47 @@ def test_graph_replay_matches_eager(mode):
         L.forward(xb, ob)
     torch.cuda.synchronize()
     assert torch.equal(oa, eager_a) and torch.equal(ob, eager_b)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("W,S,chunks,cap_factor,shared", [(1, 1000, 2, None, True), (1, 4096, 8, None, True),
+                                                          (4, 333, 3, None, False), (4, 512, 4, 0.5, True),
+                                                          (2, 3, 4, None, False), (8, 700, 5, None, True)])
+def test_chunked_forward_bit_identical(W, S, chunks, cap_factor, shared, mode):
+    """The token-chunked pipelined forward (chunk.cu), plain and
+    redundancy-bypassing, is bit-identical to the unchunked one — ragged
+    chunks, capacity drops, more chunks than tokens — and matches the fp64
+    oracle at the bf16 tolerance."""
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, W, -1)
+    rng = np.random.default_rng(S + 17 * W)
+    E, k, H, F = 32, 4, 256, 128
+    w = O.LayerWeights(grid_gate(rng, H, E), bf16_round(rng.uniform(-0.1, 0.1, (E, H, F))),
+                       bf16_round(rng.uniform(-0.1, 0.1, (E, F, H))))
+    sw1 = bf16_round(rng.uniform(-0.1, 0.1, (2, H, 64))) if shared else None
+    sw2 = bf16_round(rng.uniform(-0.1, 0.1, (2, 64, H))) if shared else None
+    cap = S * k if cap_factor is None else max(1, int(cap_factor * S * k / E))
+    x = grid_tokens(rng, W, S, H)
+    xd = dev(x, torch.bfloat16)
+    outs = []
+    for c in (1, chunks):
+        L = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=cap, max_tokens=S,
+                       dtype=capi.BF16, gate=dev(w.gate, torch.bfloat16), w1=dev(w.w1, torch.bfloat16),
+                       w2=dev(w.w2, torch.bfloat16), sw1=None if sw1 is None else dev(sw1, torch.bfloat16),
+                       sw2=None if sw2 is None else dev(sw2, torch.bfloat16), chunks=c, dispatch_mode=mode,
+                       seed=5)
+        assert L.chunks() == min(c, S)
+        outs.append(L.forward(xd).clone())
+        outs.append(L.forward(xd).clone())  # second forward: epochs / reused regions
+        led = L.ledger()
+    assert torch.equal(outs[0], outs[2]) and torch.equal(outs[1], outs[3]) and torch.equal(outs[0], outs[1])
+    got = host(outs[2])
+    if shared:
+        want = [O.moe_layer_with_shared(x[i], w, E, k, cap, sw1, sw2, exact=False) for i in range(W)]
+    else:
+        want = O.pf_moe_forward(list(x), w, E, k, cap, exact=False)
+    for i in range(W):
+        assert norm_rel(got[i], want[i]) < 1e-2, norm_rel(got[i], want[i])
+    assert led["routed_copies"] > 0
+    if mode == 1 and W > 1:
+        assert led["unique_rows_offrank"] <= led["copies_offrank"]
