@@ -550,7 +550,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
             for (int i = 0; i < nl; ++i) {
                 Worker& w = L.workers[i];
                 launch_rbd_pack(x_of(i), static_cast<int>(rb), w.rbd, W, c, nk, w.slot_pos, k, w.dest_row, w.cw,
-                                L.recv_tab, L.desc_tab, cm);
+                                L.recv_tab, L.desc_tab, cm, static_cast<int>(S), w.expert_ids, El);
             }
         else if (n > 0)
             for (int i = 0; i < nl; ++i) {
@@ -738,7 +738,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
             Worker& w = L.workers[i];
             launch_rbd_offsets(L.gd_all, W, w.rank, w.rbd, st);
             launch_rbd_pack(x_of(i), static_cast<int>(row_bytes), w.rbd, W, 0, nk, w.slot_pos, k, w.dest_row,
-                            w.cw, L.recv_tab, L.desc_tab, st);
+                            w.cw, L.recv_tab, L.desc_tab, st, static_cast<int>(S), w.expert_ids, L.El);
         }
         L.mark(kEvMoved, st);
         if (dist) L.barrier(st);

@@ -424,6 +424,92 @@ __global__ void __launch_bounds__(256) rbd_pack_kernel(
     __threadfence_system();
 }
 
+// Token-major sender pack: one warp per token of chunk c loads the token's
+// row once and stores it to each of its (token, dest) groups' pilot slot;
+// lane l < kept(t) writes slot l's descriptor.  Same bytes as the
+// group-major pack, k-fold fewer dependent row loads per warp.
+constexpr int kPackVec = 8;  // int4 per lane per pass (4 KB rows in one pass)
+__global__ void __launch_bounds__(256) rbd_pack_tokens_kernel(
+    const char* __restrict__ x, int row_bytes, int S, int C, int c, int k, int El,
+    const int32_t* __restrict__ slot_pos, const int32_t* __restrict__ expert_ids,
+    const int32_t* __restrict__ dest_row, const double* __restrict__ cw, const int32_t* __restrict__ gbase,
+    const int32_t* __restrict__ gcount, const RbdGroups g, const int32_t* __restrict__ dptr,
+    const int32_t* __restrict__ coff, const int32_t* __restrict__ gpos, const int32_t* __restrict__ ru,
+    const int32_t* __restrict__ rd, const int32_t* __restrict__ cs, char* const* __restrict__ recv_u_tab,
+    RbdDesc* const* __restrict__ desc_tab) {
+    const int lane = threadIdx.x & 31;
+    const int t_beg = rbd_chunk_t0(c, S, C), t_end = rbd_chunk_t0(c + 1, S, C);
+    const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    const int nvec = row_bytes >> 4;
+    for (long long tt = t_beg + warp; tt < t_end; tt += nwarps) {
+        const int t = static_cast<int>(tt);
+        const int4* src = reinterpret_cast<const int4*>(x + static_cast<size_t>(t) * row_bytes);
+        int4 v[kPackVec];
+#pragma unroll
+        for (int q = 0; q < kPackVec; ++q) {
+            const int col = lane + 32 * q;
+            v[q] = col < nvec ? ld_nc_v4(src + col) : make_int4(0, 0, 0, 0);
+        }
+        const int ng = gcount[t], b = gbase[t];
+        // lane j < ng: group j of the token (dest ascending)
+        unsigned long long dst = 0;
+        int gn = 0, gpilot = -1, gdesc = 0, gu = 0, gd = 0;
+        if (lane < ng) {
+            const int gid = b + lane;
+            gd = g.dest[gid];
+            gn = g.n[gid];
+            gpilot = g.pilot[gid];
+            const int pos = g.pos[gid];
+            gu = ru[gd * C + c] + pos - dptr[gd] - gpos[gd * (C + 1) + c];
+            gdesc = rd[gd * C + c] + (coff[pos] - cs[gd * C + c]);
+            dst = reinterpret_cast<unsigned long long>(recv_u_tab[gd] +
+                                                       static_cast<size_t>(dest_row[gpilot]) * row_bytes);
+        }
+        // lane l < kept(t): descriptor of slot l (groups are runs of equal dest)
+        const int p = lane < k ? slot_pos[static_cast<size_t>(t) * k + lane] : -1;
+        const int dl = p >= 0 ? expert_ids[p] / El : -1;
+        const int dprev = __shfl_up_sync(0xffffffffu, dl, 1);
+        const unsigned starts = __ballot_sync(0xffffffffu, p >= 0 && (lane == 0 || dl != dprev));
+        const unsigned le = starts & (0xffffffffu >> (31 - lane));
+        const int gj = __popc(le) - 1;
+        const int m = le ? lane - (31 - __clz(le)) : 0;
+        const int jd = gj < 0 ? 0 : gj;
+        const int n_j = __shfl_sync(0xffffffffu, gn, jd);
+        const int pil_j = __shfl_sync(0xffffffffu, gpilot, jd);
+        const int desc_j = __shfl_sync(0xffffffffu, gdesc, jd);
+        const int u_j = __shfl_sync(0xffffffffu, gu, jd);
+        const int d_j = __shfl_sync(0xffffffffu, gd, jd);
+        if (p >= 0) {
+            RbdDesc dd;
+            dd.u = u_j;
+            dd.dest_row = dest_row[p];
+            dd.w = cw[p];
+            dd.n = n_j;
+            dd.member = m | (p == pil_j ? kRbdPilotFlag : 0);
+            desc_tab[d_j][desc_j + m] = dd;
+        }
+        for (int base = 0; base < nvec; base += 32 * kPackVec) {
+            if (base > 0) {
+#pragma unroll
+                for (int q = 0; q < kPackVec; ++q) {
+                    const int col = base + lane + 32 * q;
+                    v[q] = col < nvec ? ld_nc_v4(src + col) : make_int4(0, 0, 0, 0);
+                }
+            }
+            for (int j = 0; j < ng; ++j) {
+                int4* d = reinterpret_cast<int4*>(__shfl_sync(0xffffffffu, dst, j));
+#pragma unroll
+                for (int q = 0; q < kPackVec; ++q) {
+                    const int col = base + lane + 32 * q;
+                    if (col < nvec) st_na_v4(d + col, v[q]);
+                }
+            }
+        }
+    }
+    __threadfence_system();
+}
+
 // Receiver expand: every replica copies its group's row from the pilot's
 // slot (where the sender put it) into its own grouped slot; records each
 // group's first descriptor for the merge.
@@ -762,9 +848,20 @@ void launch_rbd_offsets(const int32_t* gd_all, int W, int me, RbdWork& wk, cudaS
 
 void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, int W, int c, long long max_groups,
                      const int32_t* slot_pos, int k, const int32_t* dest_row, const double* cw,
-                     char* const* recv_u_tab, RbdDesc* const* desc_tab, cudaStream_t st) {
+                     char* const* recv_u_tab, RbdDesc* const* desc_tab, cudaStream_t st, int S,
+                     const int32_t* expert_ids, int El) {
     int grid = warp_grid(max_groups / wk.C + 1);
     if (g_copy_blocks > 0 && grid > g_copy_blocks) grid = g_copy_blocks;
+    if ((row_bytes & 15) == 0 && k <= 32 && S > 0 && expert_ids) {
+        const int nt = static_cast<int>(static_cast<long long>(c + 1) * S / wk.C - static_cast<long long>(c) * S / wk.C);
+        int tg = warp_grid(nt);
+        if (g_copy_blocks > 0 && tg > g_copy_blocks) tg = g_copy_blocks;
+        rbd_pack_tokens_kernel<<<tg, 256, 0, st>>>(
+            static_cast<const char*>(x), row_bytes, S, wk.C, c, k, El, slot_pos, expert_ids, dest_row, cw, wk.gbase,
+            wk.gcount, wk.g, wk.dptr, wk.coff, wk.gpos, wk.ru, wk.rd, wk.cs, recv_u_tab, desc_tab);
+        XMOE_LAUNCH_CHECK();
+        return;
+    }
     rbd_pack_kernel<<<grid, 256, 0, st>>>(static_cast<const char*>(x), row_bytes, wk.perm, wk.g, wk.dptr, wk.coff,
                                           wk.gpos, wk.ru, wk.rd, wk.cs, W, wk.C, c, slot_pos, k, dest_row, cw,
                                           recv_u_tab, desc_tab);

@@ -73,7 +73,8 @@ void launch_rbd_offsets(const int32_t* gd_all, int W, int me, RbdWork& wk, cudaS
 // chunk c (tokens [floor(cS/C), floor((c+1)S/C)))
 void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, int W, int c, long long max_groups,
                      const int32_t* slot_pos, int k, const int32_t* dest_row, const double* cw,
-                     char* const* recv_u_tab, RbdDesc* const* desc_tab, cudaStream_t st);
+                     char* const* recv_u_tab, RbdDesc* const* desc_tab, cudaStream_t st, int S = 0,
+                     const int32_t* expert_ids = nullptr, int El = 1);
 void launch_rbd_expand(int row_bytes, const RbdDesc* desc, const RbdWork& wk, int c, long long max_desc,
                        void* grouped, int32_t* gstart, cudaStream_t st);
 void launch_rbd_merge(int dtype, const void* eout, int H, const RbdDesc* desc, const int32_t* gstart,
