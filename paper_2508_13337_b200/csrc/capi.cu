@@ -322,6 +322,7 @@ int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S,
         for (auto& g : L.graphs)
             if (g.x == x && g.out == out && g.S == S) {
                 XMOE_CUDA(cudaGraphLaunch(g.exec, st));
+                g_kernel_launches.fetch_add(g.kernels, std::memory_order_relaxed);  // our kernel nodes
                 L.last_S = S;
                 return;
             }
@@ -329,6 +330,7 @@ int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S,
         // default stream, which cannot be captured); replay on the caller's
         cudaGraph_t graph = nullptr;
         cudaStream_t cs = L.cap_stream;
+        const unsigned long long before = g_kernel_launches.load();
         XMOE_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
         try {
             layer_forward(L, x, S, out, cs);
@@ -338,6 +340,9 @@ int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S,
             throw;
         }
         XMOE_CUDA(cudaStreamEndCapture(cs, &graph));
+        // captured launches did not run: count them when the graph does
+        const unsigned long long kernels = g_kernel_launches.load() - before;
+        g_kernel_launches.fetch_sub(kernels, std::memory_order_relaxed);
         cudaGraphExec_t exec = nullptr;
         XMOE_CUDA(cudaGraphInstantiate(&exec, graph, 0));
         XMOE_CUDA(cudaGraphDestroy(graph));
@@ -345,8 +350,9 @@ int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S,
             cudaGraphExecDestroy(L.graphs.front().exec);
             L.graphs.erase(L.graphs.begin());
         }
-        L.graphs.push_back({x, out, S, exec});
+        L.graphs.push_back({x, out, S, exec, kernels});
         XMOE_CUDA(cudaGraphLaunch(exec, st));
+        g_kernel_launches.fetch_add(kernels, std::memory_order_relaxed);
     });
 }
 

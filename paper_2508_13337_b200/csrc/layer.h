@@ -150,6 +150,7 @@ struct Layer {
         void* out;
         long long S;
         cudaGraphExec_t exec;
+        unsigned long long kernels;  // our kernel nodes in it (xmoe_kernel_launches)
     };
     std::vector<GraphEntry> graphs;  // captured forwards (xmoe_layer_set_graph)
     cudaStream_t cap_stream = nullptr;

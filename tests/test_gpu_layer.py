@@ -228,7 +228,10 @@ def test_graph_replay_matches_eager(mode):
     L = _layer(ctx, capi.BF16, E, H, F, k, S * k, S, w, sw1, sw2, mode=mode, seed=7)
     xa = dev(grid_tokens(rng, S, H), torch.bfloat16)
     xb = dev(grid_tokens(rng, S, H), torch.bfloat16)
+    n0 = capi.kernel_launches()
     eager_a, eager_b = L.forward(xa).clone(), L.forward(xb).clone()
+    per_forward = (capi.kernel_launches() - n0) // 2
+    assert per_forward > 10
     L.set_graph(True)
     oa, ob = torch.empty_like(xa), torch.empty_like(xb)
     for _ in range(3):
@@ -236,6 +239,9 @@ def test_graph_replay_matches_eager(mode):
         L.forward(xb, ob)
     torch.cuda.synchronize()
     assert torch.equal(oa, eager_a) and torch.equal(ob, eager_b)
+    n1 = capi.kernel_launches()  # a replay counts the kernels it runs
+    L.forward(xa, oa)
+    assert capi.kernel_launches() - n1 == per_forward
 
 
 @pytest.mark.parametrize("mode", [0, 1])
