@@ -333,8 +333,17 @@ def main():
         torch.cuda.synchronize()
         barrier()
         fb_ms = max_over_ranks(b0.elapsed_time(b1) / args.steps)
+        tlayer.set_timing(True)  # per-stage backward breakdown (eager launches)
+        bst = []
+        for _ in range(4):
+            tlayer.forward(x, out)
+            tlayer.backward(x, dy, dxb)
+            torch.cuda.synchronize()
+            bst.append(tlayer.bwd_stage_ms())
+        tlayer.set_timing(False)
+        bwd_stages = {kk: statistics.median(r[kk] for r in bst[1:]) for kk in bst[0]}
         fwd_bwd = {"metric": "MoE-layer fwd+bwd tokens/s", "value": world * S / (fb_ms * 1e-3), "unit": UNIT,
-                   "ms_per_step": fb_ms,
+                   "ms_per_step": fb_ms, "bwd_stages_ms": bwd_stages,
                    "note": "forward + backward (dx and fp32 grads of gate, experts, shared experts); "
                            "gradients restated beyond the forward-only reference, checked against fp64 autograd"}
 

@@ -214,7 +214,7 @@ int xmoe_layer_ledger(xmoe_layer* layer, uint64_t* out, int n);
 
 /* Per-stage device time of the last forward (ms, CUDA events), order:
  * gate, pft, dispatch, experts, shared, combine, total, then the exchange
- * split: counts (all-gather), rows_moved (dispatch kernel), dispatch_barrier,
+ * split: counts (all-gather + destination rows), rows_moved (the row kernel), dispatch_barrier,
  * return_wait (merge/barrier before the combine), combine_kernel, and the
  * shared-expert GEMMs.  Timing mode serialises the unchunked forward (the
  * shared-expert GEMMs run in line as the "shared" stage instead of on the
@@ -231,6 +231,10 @@ int xmoe_layer_set_graph(xmoe_layer* layer, int enable);
  * chunked); see XMOE_LAYER_CHUNKS. */
 int xmoe_layer_chunks(const xmoe_layer* layer, int32_t* out);
 int xmoe_layer_stage_ms(xmoe_layer* layer, float* out, int n);
+/* Per-stage device time of the last backward (ms; timing enabled, training
+ * layer), order: dy scatter (+barrier), owner prep (dL/dw, dz), dgrad GEMMs,
+ * wgrad GEMMs, token level (transposes + shared experts), gate + dx combine. */
+int xmoe_layer_bwd_stage_ms(xmoe_layer* layer, float* out, int n);
 
 #ifdef __cplusplus
 }

@@ -80,6 +80,7 @@ def lib():
         L.xmoe_layer_set_timing.argtypes = [p, i32]
         L.xmoe_layer_set_graph.argtypes = [p, i32]
         L.xmoe_layer_chunks.argtypes = [p, p]
+        L.xmoe_layer_bwd_stage_ms.argtypes = [p, p, i32]
         L.xmoe_layer_stage_ms.argtypes = [p, C.POINTER(C.c_float), i32]
         L.xmoe_plan_dispatch.argtypes = [i32, i32, p, i32, p, p, p]
         L.xmoe_moe_backward.argtypes = [p, p, p, p, i64, p, p]
@@ -334,6 +335,13 @@ class Layer:
     STAGES = ["gate", "pft", "dispatch", "experts", "shared", "combine", "total",
               "counts", "rows_moved", "dispatch_barrier", "return_wait", "combine_kernel",
               "shared_side_stream"]
+
+    BWD_STAGES = ["scatter_dy", "owner_prep", "dgrad", "wgrad", "token_level", "gate_and_dx"]
+
+    def bwd_stage_ms(self) -> dict:
+        buf = (C.c_float * 6)()
+        _check(lib().xmoe_layer_bwd_stage_ms(self.h, buf, 6))
+        return dict(zip(self.BWD_STAGES, [float(v) for v in buf]))
 
     def timeline_ms(self) -> list:
         """Chunked forward (timing on): per chunk [scatter end, GEMM start,

@@ -356,6 +356,16 @@ int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S,
     });
 }
 
+int xmoe_layer_bwd_stage_ms(xmoe_layer* layer, float* out, int n) {
+    return guarded([&] {
+        Layer& L = layer->l;
+        require(L.timing && L.train, XMOE_ERR_VALIDATION, "timing not enabled on a training layer");
+        XMOE_CUDA(cudaEventSynchronize(L.bev[kBwEnd]));
+        for (int i = 0; i < n && i < kBwdEvents - 1; ++i)
+            XMOE_CUDA(cudaEventElapsedTime(&out[i], L.bev[i], L.bev[i + 1]));
+    });
+}
+
 int xmoe_layer_chunks(const xmoe_layer* layer, int32_t* out) {
     return guarded([&] {
         require(out != nullptr, XMOE_ERR_VALIDATION, "null output");

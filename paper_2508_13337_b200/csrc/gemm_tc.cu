@@ -411,7 +411,9 @@ constexpr int kMaxGroups = 1024;
 constexpr uint32_t kABytes = BMC * BK * 2;
 constexpr uint32_t kBBytes = (BN / 2) * BK * 2;
 constexpr uint32_t kStageBytes = kABytes + kBBytes;
-constexpr size_t kSmemBytes = 1024 + kStages * kStageBytes + 1024 + sizeof(int32_t) * 2 * (kMaxGroups + 1);
+constexpr size_t kGroupTabBytes = sizeof(int32_t) * 2 * (kMaxGroups + 1);
+constexpr size_t kEpiWarpWords = 32 * 33;  // per epilogue warp: a 32 x 32 transpose tile (+1 pad)
+constexpr size_t kSmemBytes = 1024 + kStages * kStageBytes + 1024 + kGroupTabBytes + 4 * kEpiWarpWords * 4;
 
 using tc::make_desc;
 using tc::mbar_init;
@@ -511,11 +513,43 @@ __device__ __forceinline__ TileInfo tile_of(int t, const int32_t* tile_start, co
 
 // D (+)= epilogue(A . B^T) on 256x256 pair tiles.  Epilogue options: ReLU,
 // and mask (multiply by mask[r,n] > 0 — the ReLU derivative in dgrad).
+// Epilogue store of one 32-column chunk: lane l holds row l's 32 fp32
+// values; they go through a per-warp [32][33] shared tile so that each
+// store instruction writes whole 128-byte row segments (fp32: one row per
+// instruction; bf16: two 64-byte row segments) instead of 32 scattered
+// 16-byte pieces.  rows_valid: rows of this warp inside the output.
+template <typename OutT>
+__device__ __forceinline__ void store_chunk_coalesced(uint32_t* tile, const float* f, OutT* D, size_t ldd,
+                                                      size_t row_base, int rows_valid, int col0, int cn,
+                                                      int lane) {
+    if constexpr (sizeof(OutT) == 4) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) tile[lane * 33 + i] = __float_as_uint(f[i]);
+        __syncwarp();
+        const int rmax = min(32, rows_valid);
+        for (int rr = 0; rr < rmax; ++rr)
+            if (lane < cn) D[(row_base + rr) * ldd + col0 + lane] = __uint_as_float(tile[rr * 33 + lane]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) tile[lane * 33 + i] = pack_bf16(f[2 * i], f[2 * i + 1]);
+        __syncwarp();
+        const int rmax = min(32, rows_valid);
+        const int ci = lane & 15;
+        uint32_t* D32 = reinterpret_cast<uint32_t*>(D);
+        for (int rr = 0; rr < rmax; rr += 2) {
+            const int r = rr + (lane >> 4);
+            if (r < rmax && 2 * ci < cn) D32[((row_base + r) * ldd + col0) / 2 + ci] = tile[r * 33 + ci];
+        }
+    }
+    __syncwarp();
+}
+
 template <typename OutT, bool kVarK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     grouped_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                             const int32_t* __restrict__ group_sizes, int G, int M, int N, int K,
-                            OutT* __restrict__ D, int relu, const __nv_bfloat16* __restrict__ mask) {
+                            OutT* __restrict__ D, int relu, const __nv_bfloat16* __restrict__ mask,
+                            int coalesced) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -663,11 +697,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
             const __nv_bfloat16* mrow = mask ? mask + static_cast<size_t>(ti.row0 + r) * N + ti.n0 : nullptr;
+            uint32_t* etile = reinterpret_cast<uint32_t*>(smem + kStages * kStageBytes + 1024 + kGroupTabBytes) +
+                              (warp - 2) * kEpiWarpWords;
+            const int wrow = BMC * static_cast<int>(rank) + quarter * 32;  // first row of this warp in the tile
             for (int c0 = 0; c0 < nw; c0 += 32) {
                 uint32_t v[32];
                 tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                               static_cast<uint32_t>(acc * BN + c0),
                           v);
+                if (coalesced) {
+                    float f[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        f[i] = __uint_as_float(v[i]);
+                        if (relu) f[i] = fmaxf(f[i], 0.f);
+                    }
+                    const int cn = min(32, nw - c0);
+                    if (mrow && row_ok) {
+                        if (cn == 32) {
+                            const int4* m4 = reinterpret_cast<const int4*>(mrow + c0);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const int4 mv = m4[q];
+                                const uint32_t u[4] = {static_cast<uint32_t>(mv.x), static_cast<uint32_t>(mv.y),
+                                                       static_cast<uint32_t>(mv.z), static_cast<uint32_t>(mv.w)};
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    if (!(bf16_lo(u[e]) > 0.f)) f[8 * q + 2 * e] = 0.f;
+                                    if (!(bf16_hi(u[e]) > 0.f)) f[8 * q + 2 * e + 1] = 0.f;
+                                }
+                            }
+                        } else {
+                            for (int i = 0; i < cn; ++i)
+                                if (!(__bfloat162float(mrow[c0 + i]) > 0.f)) f[i] = 0.f;
+                        }
+                    }
+                    store_chunk_coalesced<OutT>(etile, f, D + (kVarK ? static_cast<size_t>(ti.g) * M * N : 0),
+                                                static_cast<size_t>(N), static_cast<size_t>(ti.row0 + wrow),
+                                                ti.rows_left - wrow, ti.n0 + c0, cn, lane);
+                    continue;
+                }
                 if (!row_ok) continue;
                 float f[32];
 #pragma unroll
@@ -762,7 +831,8 @@ __device__ __forceinline__ uint32_t make_idesc2_mn(int n) { return make_idesc2(n
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     grouped_wgrad_mn_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                             const __grid_constant__ CUtensorMap tmap_at, const __grid_constant__ CUtensorMap tmap_bt,
-                            const int32_t* __restrict__ group_rows, int G, int M, int N, float* __restrict__ D) {
+                            const int32_t* __restrict__ group_rows, int G, int M, int N, float* __restrict__ D,
+                            int coalesced) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -924,10 +994,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
+            uint32_t* etile = reinterpret_cast<uint32_t*>(smem + kStages * kStageBytes + 1024 + kGroupTabBytes) +
+                              (warp - 2) * kEpiWarpWords;
+            const int wrow = BMC * static_cast<int>(rank) + quarter * 32;
             for (int c0 = 0; c0 < nw; c0 += 32) {
                 uint32_t v[32];
                 tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN + c0),
                           v);
+                if (coalesced) {
+                    float f[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+                    store_chunk_coalesced<float>(etile, f, D + static_cast<size_t>(g) * M * N, static_cast<size_t>(N),
+                                                 static_cast<size_t>(row0 + wrow), M - (row0 + wrow), n0 + c0,
+                                                 min(32, nw - c0), lane);
+                    continue;
+                }
                 if (!row_ok) continue;
                 const int cn = min(32, nw - c0);
                 if (cn == 32 && (N & 3) == 0) {
@@ -987,6 +1069,18 @@ __global__ void wgrad_tail_kernel(const __nv_bfloat16* __restrict__ X, int C, co
 }  // namespace tc2
 
 // ---------------------------------------------------------------- host side
+// fp32 outputs (weight gradients) leave the epilogue through a per-warp
+// shared-memory transpose as whole-row segments (measured: wgrad 1.59 ->
+// 1.23 ms); bf16 outputs keep the direct per-row 16-byte stores, which
+// measured faster.  XMOE_EPI=0 selects the direct stores everywhere.
+static int epi_coalesced() {
+    static const int v = [] {
+        const char* e = std::getenv("XMOE_EPI");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -1076,7 +1170,7 @@ static void launch_tc2(const void* A, long long a_rows, long long a_cols, const 
     if (g_gemm_sm_limit > 0 && g_gemm_sm_limit / 2 < cap_pairs) cap_pairs = g_gemm_sm_limit / 2;
     const long long pairs = tile_bound < cap_pairs ? tile_bound : cap_pairs;
     tc2::grouped_gemm_tc2_kernel<OutT, kVarK><<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
-        ta, tb, group_sizes, G, M, N, K, D, relu, mask);
+        ta, tb, group_sizes, G, M, N, K, D, relu, mask, sizeof(OutT) == 4 ? epi_coalesced() : 0);
     XMOE_LAUNCH_CHECK();
 }
 
@@ -1152,7 +1246,7 @@ void launch_grouped_wgrad_mn(const void* A, int M, const void* B, int N, long lo
     const long long tiles = static_cast<long long>(G) * ((M + tc2::BM - 1) / tc2::BM) * ((N + tc2::BN - 1) / tc2::BN);
     const long long pairs = tiles < sms / 2 ? tiles : sms / 2;
     tc2::grouped_wgrad_mn_kernel<<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
-        ta, tb, tat, tbt, group_rows, G, M, N, D);
+        ta, tb, tat, tbt, group_rows, G, M, N, D, epi_coalesced());
     XMOE_LAUNCH_CHECK();
 }
 

@@ -50,6 +50,7 @@ Layer::~Layer() {
     for (cudaEvent_t e : evA) cudaEventDestroy(e);
     for (cudaEvent_t e : evB) cudaEventDestroy(e);
     for (cudaEvent_t e : tl) cudaEventDestroy(e);
+    for (cudaEvent_t e : bev) cudaEventDestroy(e);
     for (void* p : peer_maps) cudaIpcCloseMemHandle(p);
     for (void* p : allocs) cudaFree(p);
     for (auto& e : events) cudaEventDestroy(e);
@@ -308,6 +309,8 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
                                                   static_cast<size_t>(Fs)});
             w.tail_a = L.alloc(64 * static_cast<size_t>(L.El + 1) * wide * es);
             w.tail_b = L.alloc(64 * static_cast<size_t>(L.El + 1) * wide * es);
+            w.tail_sa = L.alloc(64 * 2 * wide * es);  // side-stream (shared-expert wgrad) copies
+            w.tail_sb = L.alloc(64 * 2 * wide * es);
             w.kpg = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
             w.koff = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
             w.roff = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
@@ -418,6 +421,10 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     }
     L.events.resize(kNumEvents);
     for (auto& e : L.events) XMOE_CUDA(cudaEventCreate(&e));
+    if (L.train) {
+        L.bev.resize(kBwdEvents);
+        for (auto& e : L.bev) XMOE_CUDA(cudaEventCreate(&e));
+    }
     XMOE_CUDA(cudaStreamCreateWithFlags(&L.side, cudaStreamNonBlocking));
     XMOE_CUDA(cudaStreamCreateWithFlags(&L.cap_stream, cudaStreamNonBlocking));
     XMOE_CUDA(cudaEventCreateWithFlags(&L.ev_fork, cudaEventDisableTiming));
@@ -726,17 +733,17 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         }
         XMOE_NCCL(ncclGroupEnd());
     }
-    L.mark(kEvCounts, st);
     // 4. dispatch: destination rows in the owner's (local expert, source,
     //    position) layout (pf_pipeline.cpp:47-73), then the rows themselves
     for (int i = 0; i < nl; ++i) {
         Worker& w = L.workers[i];
         launch_dispatch_dest(L.tpe_all, W, E, w.rank, w.expert_ids, w.B_dev, nk, w.dest_rank, w.dest_row, st);
+        if (rbd) launch_rbd_offsets(L.gd_all, W, w.rank, w.rbd, st);
     }
+    L.mark(kEvCounts, st);  // counts + destinations; rows_moved is the row kernel alone
     if (rbd) {
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
-            launch_rbd_offsets(L.gd_all, W, w.rank, w.rbd, st);
             launch_rbd_pack(x_of(i), static_cast<int>(row_bytes), w.rbd, W, 0, nk, w.slot_pos, k, w.dest_row,
                             w.cw, L.recv_tab, L.desc_tab, st, static_cast<int>(S), w.expert_ids, L.El);
         }
@@ -877,6 +884,43 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
     const size_t rb = static_cast<size_t>(H) * L.es;
     const bool dist = L.distributed;
     auto xo = [&](const void* b, int i) { return static_cast<const char*>(b) + static_cast<size_t>(i) * S * rb; };
+    auto bmark = [&](int e) {
+        if (L.timing) XMOE_CUDA(cudaEventRecord(L.bev[e], st));
+    };
+    bmark(kBwStart);
+    for (int i = 0; i < L.nl; ++i) {  // token-level group descriptors (one group of S rows)
+        Worker& w = L.workers[i];
+        launch_fill_i32(w.tk, 1, static_cast<int32_t>(S), st);
+        launch_pad_offsets(w.tk, 1, w.tk + 1, w.tk + 2, w.tk + 4, st);
+    }
+    // B5a token-level work that needs only x, dy and the forward's shared
+    // activations (x transpose for the gate, shared-expert dgrad + wgrad):
+    // on the side stream, overlapping the routed backward (own tail
+    // scratch).  Timing mode runs it in line as the "token_level" stage.
+    auto token_level = [&](cudaStream_t ss) {
+        for (int i = 0; i < L.nl; ++i) {
+            Worker& w = L.workers[i];
+            launch_transpose_pad(xo(x, i), H, w.tk, w.tk + 2, w.tk + 4, 1, L.Sp, w.xTt, ss);
+            if (L.Fs > 0) {
+                launch_grouped_gemm_bf16_mask(xo(dy, i), S, H, w.s_rows, 1, L.sw2r, L.Fs, w.dHs, w.smid, ss);
+                launch_grouped_gemm_bf16(w.dHs, S, L.Fs, w.s_rows, 1, L.sw1r, H, w.dxs, 0, ss);
+                launch_grouped_wgrad_mn(xo(x, i), H, w.dHs, L.Fs, S, w.tk, 1, w.tail_sa, w.tail_sb, L.dsw1, ss);
+                launch_grouped_wgrad_mn(w.smid, L.Fs, xo(dy, i), H, S, w.tk, 1, w.tail_sa, w.tail_sb, L.dsw2, ss);
+            }
+        }
+    };
+    if (!L.timing) {
+        XMOE_CUDA(cudaEventRecord(L.ev_fork, st));
+        XMOE_CUDA(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
+        static const int side_sms = [] {
+            const char* e = std::getenv("XMOE_BWD_SIDE_SMS");
+            return e ? std::atoi(e) : 0;
+        }();
+        g_gemm_sm_limit = side_sms;
+        token_level(L.side);
+        g_gemm_sm_limit = 0;
+        XMOE_CUDA(cudaEventRecord(L.ev_join, L.side));
+    }
     for (int i = 0; i < L.nl; ++i) {  // B1
         Worker& w = L.workers[i];
         TrainTabs tr{L.gw_tab, L.gsrc_tab, w.rank};
@@ -884,30 +928,24 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
                               w.dest_row, w.cw, L.dyg_tab, L.dxc_tab, w.bslot_src, nullptr, st, tr);
     }
     if (dist) L.barrier(st);
+    bmark(kBwScatter);
     for (int i = 0; i < L.nl; ++i) {  // B2-B4 at the owner
         Worker& w = L.workers[i];
         const size_t eo = dist ? 0 : static_cast<size_t>(w.rank) * El * H * F * L.es;
         launch_bwd_owner_prep(w.dyg, w.eout, w.gw, w.gsrc, w.rpe, El, H, L.R_max, L.slotdw_tab, w.dz, st);
+        bmark(kBwPrep);
         launch_grouped_gemm_bf16_mask(w.dz, L.R_max, H, w.rpe, El, static_cast<const char*>(L.w2r) + eo, F, w.dH,
                                       w.mid, st);
         launch_grouped_gemm_bf16(w.dH, L.R_max, F, w.rpe, El, static_cast<const char*>(L.w1r) + eo, H, w.dxc, 0, st);
+        bmark(kBwDgrad);
         // wgrad straight on the grouped activations (MN-major tcgen05 operands)
         const size_t go = dist ? 0 : static_cast<size_t>(w.rank) * El * H * F;
         launch_grouped_wgrad_mn(w.recv, H, w.dH, F, L.R_max, w.rpe, El, w.tail_a, w.tail_b, L.dw1 + go, st);
         launch_grouped_wgrad_mn(w.mid, F, w.dz, H, L.R_max, w.rpe, El, w.tail_a, w.tail_b, L.dw2 + go, st);
     }
-    for (int i = 0; i < L.nl; ++i) {  // B5 token-level: transposes shared by the gate and shared experts
-        Worker& w = L.workers[i];
-        launch_fill_i32(w.tk, 1, static_cast<int32_t>(S), st);
-        launch_pad_offsets(w.tk, 1, w.tk + 1, w.tk + 2, w.tk + 4, st);
-        launch_transpose_pad(xo(x, i), H, w.tk, w.tk + 2, w.tk + 4, 1, L.Sp, w.xTt, st);
-        if (L.Fs > 0) {
-            launch_grouped_gemm_bf16_mask(xo(dy, i), S, H, w.s_rows, 1, L.sw2r, L.Fs, w.dHs, w.smid, st);
-            launch_grouped_gemm_bf16(w.dHs, S, L.Fs, w.s_rows, 1, L.sw1r, H, w.dxs, 0, st);
-            launch_grouped_wgrad_mn(xo(x, i), H, w.dHs, L.Fs, S, w.tk, 1, w.tail_a, w.tail_b, L.dsw1, st);
-            launch_grouped_wgrad_mn(w.smid, L.Fs, xo(dy, i), H, S, w.tk, 1, w.tail_a, w.tail_b, L.dsw2, st);
-        }
-    }
+    bmark(kBwWgrad);
+    if (L.timing) token_level(st);
+    bmark(kBwToken);
     if (dist) L.barrier(st);  // every owner wrote dL/dw and dxc
     for (int i = 0; i < L.nl; ++i) {  // B5 gate, B6 dx
         Worker& w = L.workers[i];
@@ -915,10 +953,12 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
                         static_cast<int>(S), E, k, w.dl, st);
         launch_grouped_gemm_bf16(w.dl, S, E, w.s_rows, 1, L.gater, H, w.dxg, 0, st);
         launch_transpose_pad(w.dl, E, w.tk, w.tk + 2, w.tk + 4, 1, L.Sp, w.dlT, st);
+        if (i == 0 && !L.timing) XMOE_CUDA(cudaStreamWaitEvent(st, L.ev_join, 0));  // xTt, dxs
         launch_grouped_wgrad_bf16(w.xTt, H, L.Sp, w.tk + 1, 1, w.dlT, E, L.dgate, st);
         launch_combine_slots(w.bslot_src, nullptr, k, H, static_cast<int>(S), L.Fs > 0 ? w.dxs : nullptr,
                              static_cast<char*>(dx) + static_cast<size_t>(i) * S * rb, st, 0, w.dxg);
     }
+    bmark(kBwEnd);
     (void)ctx;
     (void)W;
 }

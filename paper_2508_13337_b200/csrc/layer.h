@@ -72,6 +72,8 @@ struct Worker {
     void* dH = nullptr;           // [R_max, F]
     void* tail_a = nullptr;       // wgrad tail blocks [64*(El+1), max(H,F,Fs)]
     void* tail_b = nullptr;
+    void* tail_sa = nullptr;      // the same for the side-stream (shared-expert) wgrad
+    void* tail_sb = nullptr;
     int32_t* kpg = nullptr;       // [El] padded rows per expert
     int32_t* koff = nullptr;      // [El+1]
     int32_t* roff = nullptr;      // [El+1]
@@ -93,6 +95,9 @@ struct Worker {
 };
 
 // stage boundaries; kEvCounts/kEvMoved/kEvReturn split the exchange phases
+// backward stage boundaries: start, dy scattered, owner prep, dgrad GEMMs,
+// wgrad GEMMs, token-level (transpose + shared experts), gate + dx combine
+enum { kBwStart = 0, kBwScatter, kBwPrep, kBwDgrad, kBwWgrad, kBwToken, kBwEnd, kBwdEvents };
 enum { kEvStart = 0, kEvGate, kEvPft, kEvDispatch, kEvGemm, kEvShared, kEvCombine, kEvCounts, kEvMoved, kEvReturn, kNumEvents };
 
 struct Layer {
@@ -167,6 +172,7 @@ struct Layer {
     cudaStream_t comm = nullptr;
     std::vector<cudaEvent_t> evA, evB;
     std::vector<cudaEvent_t> tl;   // timing: per chunk scatter end, GEMM start, GEMM end, combine end
+    std::vector<cudaEvent_t> bev;  // timing: backward stage boundaries (kBwdEvents)
     cudaEvent_t ev_done = nullptr;
 
     void* alloc(size_t bytes);
