@@ -60,6 +60,12 @@ extern "C" {
  * bit-identical for every chunk count. */
 #define XMOE_LAYER_CHUNKS(n) ((n) << 8)
 #define XMOE_LAYER_CHUNKS_OF(flags) (((flags) >> 8) & 15)
+/* Redundancy-bypassing dispatch over nodes of n GPUs (node_of[w] = w / n,
+ * the reference's two-tier form, rbd.cpp:83-358): one row per (token,
+ * destination node), forwarded inside the node to the replicas' owners.
+ * 0 or 1 = one GPU per node. */
+#define XMOE_LAYER_GPUS_PER_NODE(n) ((n) << 12)
+#define XMOE_LAYER_GPUS_PER_NODE_OF(flags) (((flags) >> 12) & 255)
 
 typedef struct xmoe_ctx xmoe_ctx;
 typedef struct xmoe_layer xmoe_layer;
@@ -211,6 +217,44 @@ int xmoe_layer_grads(xmoe_layer* layer, float** dgate, float** dw1, float** dw2,
  *               combine_rows_offrank, routed_copies, unique_rows_offrank,
  *               copies_offrank } summed over this context's ranks. */
 int xmoe_layer_ledger(xmoe_layer* layer, uint64_t* out, int n);
+
+/* Topology for the reference-schema ledger (moesim::Topology,
+ * config.hpp:30-40): node_of[w] = w / gpus_per_node classifies every
+ * message as self, intra-node or inter-node; the alpha-beta model
+ * (collectives.cpp:56-76) charges latency + bytes / bandwidth per message
+ * to its sender.  dtype_bytes: wire bytes per element (0 = the layer's). */
+typedef struct xmoe_topology {
+    int64_t gpus_per_node;
+    double bw_intra, bw_inter;           /* bytes / s */
+    double latency_intra, latency_inter; /* s per message */
+    int64_t dtype_bytes;
+} xmoe_topology;
+
+/* One collective of the last forward, as moesim::LedgerEntry
+ * (collectives.hpp:31-41): the exchanges the reference's pf_moe_forward /
+ * rbd_moe_forward / ssmb_forward perform, in its order and with its kinds
+ * ("dispatch_counts", "dispatch_rows", "combine_rows", "rbd_dispatch_counts",
+ * "rbd_dispatch_meta", "rbd_dispatch_rows1", "rbd_dispatch_meta2",
+ * "rbd_dispatch_rows2", "rbd_combine_rows2", "rbd_combine_rows1",
+ * "ssmb_gather_rows"), bytes from this layer's actual routing. */
+typedef struct xmoe_ledger_entry {
+    int64_t id;
+    char kind[32];
+    uint64_t self_bytes, intra_bytes, inter_bytes, intra_msgs, inter_msgs;
+    double time_s;
+} xmoe_ledger_entry;
+
+/* Entries of the last forward (topo NULL = the reference defaults:
+ * gpus_per_node 8, 200e9 / 25e9 B/s, zero latency).  *n receives the entry
+ * count; at most cap are written.  With one process per GPU the per-rank
+ * contributions are summed over the group (collective: every rank calls). */
+int xmoe_layer_ledger_entries(xmoe_layer* layer, const xmoe_topology* topo, xmoe_ledger_entry* out, int cap,
+                              int* n);
+/* The same as CostLedger::write_csv (collectives.cpp:26-34):
+ * "collective_id,kind,intra_bytes,inter_bytes,modeled_time_s" rows.
+ * *len receives the full length; at most cap bytes (NUL-terminated) are
+ * written. */
+int xmoe_layer_ledger_csv(xmoe_layer* layer, const xmoe_topology* topo, char* buf, int64_t cap, int64_t* len);
 
 /* Per-stage device time of the last forward (ms, CUDA events), order:
  * gate, pft, dispatch, experts, shared, combine, total, then the exchange

@@ -12,6 +12,7 @@
 //   5 CountMismatch 6 PlanMismatch 99 other.
 #include <cstdint>
 #include <cstring>
+#include <cstdio>
 #include <exception>
 #include <string>
 #include <vector>
@@ -106,7 +107,20 @@ const char* const kKinds[] = {"dispatch_counts",    "dispatch_rows",      "combi
                               "rbd_combine_rows1",  "ssmb_gather_rows"};
 constexpr int kNumKinds = sizeof(kKinds) / sizeof(kKinds[0]);
 
+// The last forward's ledger in CostLedger::write_csv's format
+// (collectives.cpp:26-34), formatted here from led.entries() with the same
+// "%.12g": the reference's ostream writer is not called across the
+// libstdc++ the host process loads.
+std::string g_last_csv;
+
 void dump_ledger(const CostLedger& led, std::uint64_t* out) {
+    g_last_csv = "collective_id,kind,intra_bytes,inter_bytes,modeled_time_s\n";
+    char buf[64];
+    for (const auto& e : led.entries()) {
+        std::snprintf(buf, sizeof buf, "%.12g", e.time_s);
+        g_last_csv += std::to_string(e.id) + ',' + e.kind + ',' + std::to_string(e.intra_bytes) + ',' +
+                      std::to_string(e.inter_bytes) + ',' + buf + '\n';
+    }
     if (!out) return;
     for (int i = 0; i < kNumKinds; ++i) {
         std::uint64_t s = 0, a = 0, r = 0;
@@ -138,6 +152,7 @@ std::vector<Pft> build_pfts(const MoeInstance& inst) {
 extern "C" {
 
 const char* ref_last_error(void) { return g_err.c_str(); }
+const char* ref_last_ledger_csv(void) { return g_last_csv.c_str(); }
 int ref_num_ledger_kinds(void) { return kNumKinds; }
 const char* ref_ledger_kind(int i) { return (i >= 0 && i < kNumKinds) ? kKinds[i] : ""; }
 const char* ref_kernel_backend(void) { return kernels::active().name; }

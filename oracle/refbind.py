@@ -56,6 +56,7 @@ def lib():
             raise FileNotFoundError(f"{LIB_PATH} not built (run make -C oracle)")
         L = C.CDLL(LIB_PATH)
         L.ref_last_error.restype = C.c_char_p
+        L.ref_last_ledger_csv.restype = C.c_char_p
         L.ref_kernel_backend.restype = C.c_char_p
         L.ref_salt_seed.restype = _u64
         L.ref_salt_seed.argtypes = [_u64, _u64, _u64]
@@ -244,3 +245,8 @@ def select_pilots(token_ids, expert_ids, cw, tpe, E, node_of, seed):
 def sample_redundancy(seed, tokens, k, expert_node):
     en = _i64a(expert_node)
     return float(lib().ref_sample_redundancy(seed, tokens, k, en.shape[0], _ptr(en)))
+
+
+def last_ledger_csv() -> str:
+    """CostLedger::write_csv of the last reference forward (collectives.cpp:26-34)."""
+    return lib().ref_last_ledger_csv().decode()

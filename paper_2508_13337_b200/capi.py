@@ -42,6 +42,22 @@ class LayerDesc(C.Structure):
                 ("seed", C.c_uint64)]
 
 
+class Topology(C.Structure):
+    """xmoe_topology (moesim::Topology, config.hpp:30-40)."""
+    _fields_ = [("gpus_per_node", C.c_int64), ("bw_intra", C.c_double), ("bw_inter", C.c_double),
+                ("latency_intra", C.c_double), ("latency_inter", C.c_double), ("dtype_bytes", C.c_int64)]
+
+    @classmethod
+    def reference_defaults(cls, gpus_per_node=8, dtype_bytes=0):
+        return cls(gpus_per_node, 200e9, 25e9, 0.0, 0.0, dtype_bytes)
+
+
+class LedgerEntry(C.Structure):
+    _fields_ = [("id", C.c_int64), ("kind", C.c_char * 32), ("self_bytes", C.c_uint64),
+                ("intra_bytes", C.c_uint64), ("inter_bytes", C.c_uint64), ("intra_msgs", C.c_uint64),
+                ("inter_msgs", C.c_uint64), ("time_s", C.c_double)]
+
+
 def header_symbols() -> list[str]:
     """Every function the C-ABI header declares."""
     hdr = os.path.join(_build.ROOT, "include", "xmoe", "xmoe.h")
@@ -80,6 +96,8 @@ def lib():
         L.xmoe_layer_set_timing.argtypes = [p, i32]
         L.xmoe_layer_set_graph.argtypes = [p, i32]
         L.xmoe_layer_chunks.argtypes = [p, p]
+        L.xmoe_layer_ledger_entries.argtypes = [p, p, p, i32, p]
+        L.xmoe_layer_ledger_csv.argtypes = [p, p, p, i64, p]
         L.xmoe_layer_bwd_stage_ms.argtypes = [p, p, i32]
         L.xmoe_layer_stage_ms.argtypes = [p, C.POINTER(C.c_float), i32]
         L.xmoe_plan_dispatch.argtypes = [i32, i32, p, i32, p, p, p]
@@ -240,13 +258,14 @@ class Layer:
 
     def __init__(self, ctx: Context, *, num_experts, model_dim, ffn_dim, top_k, max_token_count,
                  max_tokens, dtype, gate, w1, w2, sw1=None, sw2=None, renorm=False,
-                 dispatch_mode=NAIVE, seed=0, ssmb=False, train=False, chunks=0):
+                 dispatch_mode=NAIVE, seed=0, ssmb=False, train=False, chunks=0, gpus_per_node=1):
         self.ctx = ctx
         ns = 0 if sw1 is None else sw1.shape[0]
         fs = 0 if sw1 is None else sw1.shape[2]
         self.desc = LayerDesc(num_experts, model_dim, ffn_dim, top_k, max_token_count, ns, fs,
                               max_tokens, dtype, int(renorm), dispatch_mode,
-                              int(bool(ssmb)) | (2 if train else 0) | (int(chunks) << 8), seed)
+                              int(bool(ssmb)) | (2 if train else 0) | (int(chunks) << 8) |
+                              (int(gpus_per_node) << 12), seed)
         self.shape = dict(E=num_experts, H=model_dim, F=ffn_dim, ns=ns, Fs=fs,
                           E_held=w1.shape[0])
         self.dtype = dtype
@@ -325,6 +344,26 @@ class Layer:
         v = C.c_int32()
         _check(lib().xmoe_layer_chunks(self.h, C.byref(v)))
         return int(v.value)
+
+    def ledger_entries(self, topo: "Topology | None" = None) -> list[dict]:
+        """The last forward's collectives in the reference's CostLedger schema."""
+        n = C.c_int32()
+        tp = C.byref(topo) if topo is not None else None
+        _check(lib().xmoe_layer_ledger_entries(self.h, tp, None, 0, C.byref(n)))
+        buf = (LedgerEntry * max(1, n.value))()
+        _check(lib().xmoe_layer_ledger_entries(self.h, tp, buf, n.value, C.byref(n)))
+        return [{"id": e.id, "kind": e.kind.decode(), "self_bytes": e.self_bytes, "intra_bytes": e.intra_bytes,
+                 "inter_bytes": e.inter_bytes, "intra_msgs": e.intra_msgs, "inter_msgs": e.inter_msgs,
+                 "time_s": e.time_s} for e in buf[:n.value]]
+
+    def ledger_csv(self, topo: "Topology | None" = None) -> str:
+        """CostLedger::write_csv of the last forward (collectives.cpp:26-34)."""
+        n = C.c_int64()
+        tp = C.byref(topo) if topo is not None else None
+        _check(lib().xmoe_layer_ledger_csv(self.h, tp, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(lib().xmoe_layer_ledger_csv(self.h, tp, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
 
     def set_graph(self, on: bool):
         _check(lib().xmoe_layer_set_graph(self.h, int(on)))

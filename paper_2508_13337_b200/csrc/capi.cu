@@ -14,6 +14,10 @@
 #include <string>
 #include <vector>
 
+#include <cstdio>
+#include <cstring>
+#include <string>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "layer.h"
@@ -401,6 +405,47 @@ int xmoe_ssmb_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x_full, int6
                       void* out_full, void* stream) {
     return guarded([&] {
         ssmb_forward(ctx->c, layer->l, x_full, S, out_full, static_cast<cudaStream_t>(stream));
+    });
+}
+
+static xmoe_topology topo_or_default(const xmoe_topology* t) {
+    if (t) return *t;
+    xmoe_topology d{};  // moesim::Topology defaults (config.hpp:30-37)
+    d.gpus_per_node = 8;
+    d.bw_intra = 200e9;
+    d.bw_inter = 25e9;
+    return d;
+}
+
+int xmoe_layer_ledger_entries(xmoe_layer* layer, const xmoe_topology* topo, xmoe_ledger_entry* out, int cap,
+                              int* n) {
+    return guarded([&] {
+        require(n != nullptr, XMOE_ERR_VALIDATION, "null output");
+        std::vector<xmoe_ledger_entry> v;
+        layer->l.ledger_entries(topo_or_default(topo), v);
+        *n = static_cast<int>(v.size());
+        for (int i = 0; i < cap && i < *n; ++i) out[i] = v[i];
+    });
+}
+
+int xmoe_layer_ledger_csv(xmoe_layer* layer, const xmoe_topology* topo, char* buf, int64_t cap, int64_t* len) {
+    return guarded([&] {
+        require(len != nullptr, XMOE_ERR_VALIDATION, "null output");
+        std::vector<xmoe_ledger_entry> v;
+        layer->l.ledger_entries(topo_or_default(topo), v);
+        std::string csv = "collective_id,kind,intra_bytes,inter_bytes,modeled_time_s\n";
+        char tb[64];
+        for (const auto& e : v) {
+            std::snprintf(tb, sizeof tb, "%.12g", e.time_s);
+            csv += std::to_string(e.id) + ',' + e.kind + ',' + std::to_string(e.intra_bytes) + ',' +
+                   std::to_string(e.inter_bytes) + ',' + tb + '\n';
+        }
+        *len = static_cast<int64_t>(csv.size());
+        if (buf && cap > 0) {
+            const size_t m = std::min<size_t>(csv.size(), static_cast<size_t>(cap - 1));
+            std::memcpy(buf, csv.data(), m);
+            buf[m] = '\0';
+        }
     });
 }
 

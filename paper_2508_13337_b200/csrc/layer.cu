@@ -123,6 +123,9 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         require(L.p2p || !rbd, XMOE_ERR_VALIDATION,
                 "the redundancy-bypassing dispatch runs on the NVLink peer transport");
     }
+    L.gpn = std::max(1, XMOE_LAYER_GPUS_PER_NODE_OF(d.flags));
+    require(W % L.gpn == 0, XMOE_ERR_VALIDATION, "the worker group must be whole nodes (world % gpus_per_node)");
+    require(L.gpn == 1 || rbd, XMOE_ERR_VALIDATION, "gpus_per_node applies to the redundancy-bypassing dispatch");
     const int H = L.H, F = L.F, E = L.E;
     const size_t es = L.es;
     cudaStream_t st = nullptr;
@@ -173,7 +176,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     {
         const int req = XMOE_LAYER_CHUNKS_OF(d.flags);
         require(req <= kMaxChunks, XMOE_ERR_VALIDATION, "at most 8 token chunks");
-        const bool can = bf && !L.train && (!L.distributed || L.p2p) && L.k <= 32;
+        const bool can = bf && !L.train && (!L.distributed || L.p2p) && L.k <= 32 && L.gpn == 1;
         int C = req > 0 ? req : (S >= 4096 && L.distributed && !rbd ? std::min(4, W) : 1);
         if (const char* e = std::getenv("XMOE_CHUNKS")) C = std::max(1, std::min(kMaxChunks, std::atoi(e)));
         L.nchunks = can ? static_cast<int>(std::max<long long>(1, std::min<long long>(C, S))) : 1;
@@ -281,6 +284,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
             r.coff = i32(nk);
             r.csr_ws = L.alloc(bucket_ws_bytes(nk, W));
             r.C = L.nchunks;
+            r.gpn = L.gpn;
             r.gpos = i32(static_cast<long long>(W) * (r.C + 1));
             r.gd_own = L.distributed ? i32(2LL * W * r.C)
                                      : L.gd_all + static_cast<size_t>(w.rank) * 2 * W * r.C;
@@ -594,13 +598,14 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             if (rbd)  // replicas copy the row from their pilot's slot
-                launch_rbd_expand(static_cast<int>(rb), w.desc_recv, w.rbd, c, L.R_max, w.recv, w.gstart, st);
+                launch_rbd_expand(static_cast<int>(rb), w.desc_recv, w.rbd, c, L.R_max, w.recv, L.recv_tab, w.gstart,
+                                  st);
             launch_grouped_gemm_bf16(static_cast<char*>(w.recv) + r0 * rb, L.Rc, H, w.rpe_c + c * El, El,
                                      w1_of(L, w.rank), F, static_cast<char*>(w.mid) + r0 * F * L.es, 1, st);
             launch_grouped_gemm_bf16(static_cast<char*>(w.mid) + r0 * F * L.es, L.Rc, F, w.rpe_c + c * El, El,
                                      w2_of(L, w.rank), H, static_cast<char*>(w.eout) + r0 * rb, 0, st);
             if (rbd)  // weighted sum of each group's outputs, pilot first (rbd.cpp:318-336)
-                launch_rbd_merge(XMOE_BF16, w.eout, H, w.desc_recv, w.gstart, w.rbd, c,
+                launch_rbd_merge(XMOE_BF16, L.eout_tab, H, w.desc_recv, w.gstart, w.rbd, c,
                                  static_cast<long long>(W) * S, w.back_u, st);
         }
         if (L.timing) XMOE_CUDA(cudaEventRecord(L.tl[4 * c + 2], st));
@@ -643,6 +648,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
 void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t st) {
     Ctx& ctx = *L.ctx;
     require(S >= 0 && S <= L.S_max, XMOE_ERR_VALIDATION, "sequence longer than the layer's max_tokens");
+    L.last_ssmb = false;
     if (L.nchunks > 1 && S > 0) {
         layer_forward_chunked(L, x, S, out, st);
         return;
@@ -751,8 +757,10 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         if (dist) L.barrier(st);
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
-            launch_rbd_expand(static_cast<int>(row_bytes), w.desc_recv, w.rbd, 0, L.R_max, w.recv, w.gstart, st);
+            launch_rbd_expand(static_cast<int>(row_bytes), w.desc_recv, w.rbd, 0, L.R_max, w.recv, L.recv_tab,
+                              w.gstart, st);
         }
+        if (dist && L.gpn > 1) L.barrier(st);  // stage-2 rows landed in peers' inputs
     } else if (tables) {
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
@@ -797,7 +805,8 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     if (rbd) {
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
-            launch_rbd_merge(dt, w.eout, H, w.desc_recv, w.gstart, w.rbd, 0, static_cast<long long>(W) * S,
+            if (i == 0 && dist && L.gpn > 1) L.barrier(st);  // replicas' outputs are read from their owners
+            launch_rbd_merge(dt, L.eout_tab, H, w.desc_recv, w.gstart, w.rbd, 0, static_cast<long long>(W) * S,
                              w.back_u, st);
         }
         if (dist) L.barrier(st);
@@ -978,13 +987,28 @@ void ssmb_forward(Ctx& ctx, Layer& L, const void* x_full, long long S, void* out
     auto rows_of = [&](int g) { return g == G - 1 ? S - static_cast<long long>(g) * base : base; };
     const char* xb = static_cast<const char*>(x_full);
     char* ob = static_cast<char*>(out_full);
+    if (L.ssmb_cap < G) {  // kept copies per shard, for the ledger
+        L.ssmb_B = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * G));
+        L.ssmb_cap = G;
+    }
+    XMOE_CUDA(cudaMemsetAsync(L.ssmb_B, 0, sizeof(int32_t) * G, st));
+    L.ssmb_rows.assign(G, 0);
+    for (int g = 0; g < G; ++g) L.ssmb_rows[g] = rows_of(g);
+    auto keep_count = [&](int g) {
+        XMOE_CUDA(cudaMemcpyAsync(L.ssmb_B + g, L.workers[0].B_dev, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    };
     if (ctx.rank < 0 || G == 1) {
-        for (int g = 0; g < G; ++g)
+        for (int g = 0; g < G; ++g) {
             layer_forward(L, xb + g * base * rb, rows_of(g), ob + g * base * rb, st);
+            keep_count(g);
+        }
+        L.last_ssmb = true;
         return;
     }
     const int me = ctx.rank;
     layer_forward(L, xb + me * base * rb, rows_of(me), ob + me * base * rb, st);
+    keep_count(me);
+    L.last_ssmb = true;
     auto comm = static_cast<ncclComm_t>(ctx.nccl);
     XMOE_NCCL(ncclGroupStart());
     for (int g = 0; g < G; ++g) {

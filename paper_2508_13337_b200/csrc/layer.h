@@ -105,6 +105,7 @@ struct Layer {
     xmoe_layer_desc d{};
     int W = 1, E = 0, H = 0, F = 0, k = 0, El = 0, E_held = 0, Fs = 0;
     int nl = 1;                // ranks driven by this process
+    int gpn = 1;               // RBD GPUs per node (node_of = rank / gpn)
     bool ssmb = false;         // sequence-sharded block: experts replicated, MoE local
     bool distributed = false;  // one process per GPU, world > 1
     bool p2p = false;          // NVLink peer tables (else NCCL send/recv baseline)
@@ -181,6 +182,12 @@ struct Layer {
     void barrier(cudaStream_t st);
     long long C(int s, int d) const;  // copies source s -> dest d (needs h_tpe)
     void ledger(uint64_t* out, int n);
+    // reference-schema ledger (ledger.cpp)
+    bool last_ssmb = false;             // last forward was ssmb_forward
+    std::vector<long long> ssmb_rows;   // its shard lengths
+    int32_t* ssmb_B = nullptr;          // [G] kept copies per shard (device)
+    int ssmb_cap = 0;
+    void ledger_entries(const xmoe_topology& topo, std::vector<xmoe_ledger_entry>& out);
     ~Layer();
 };
 

@@ -3,8 +3,12 @@
 // collectives.cpp:45-76).  Self traffic stays on the GPU; off-rank traffic
 // crosses NVLink.  Row bytes use the layer's real element size.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
+#include <algorithm>
+#include <cstring>
 #include <set>
+#include <string>
 #include <utility>
 #include <vector>
 
@@ -75,6 +79,174 @@ void Layer::ledger(uint64_t* out, int n) {
         }
     }
     for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
+}
+
+// ---------------------------------------------------------------- reference-schema ledger
+// Byte matrices M[i][j] (sender i -> receiver j) per collective kind, from
+// the routing of the last forward, then moesim's classification and
+// alpha-beta model (collectives.cpp:36-76, 143-202).  Each process adds the
+// contributions of the sources it drives; with one process per GPU the
+// matrices are summed over the group, so every rank gets the global ledger.
+namespace {
+
+struct Kind {
+    const char* name;
+    std::vector<uint64_t> M;  // W * W
+    bool ring = false;        // ssmb_gather_rows: synchronous ring all-gather
+};
+
+int node_of(const xmoe_topology& t, int w) { return t.gpus_per_node > 0 ? static_cast<int>(w / t.gpus_per_node) : w; }
+
+xmoe_ledger_entry finish(const Kind& k, int W, const xmoe_topology& t, const std::vector<long long>& ring_rows,
+                         uint64_t ring_row_bytes) {
+    xmoe_ledger_entry e{};
+    std::strncpy(e.kind, k.name, sizeof(e.kind) - 1);
+    auto charge = [&](int i, int j, uint64_t bytes, std::vector<double>& sender) {
+        if (i == j) {
+            e.self_bytes += bytes;
+        } else if (node_of(t, i) == node_of(t, j)) {
+            e.intra_bytes += bytes;
+            e.intra_msgs += 1;
+            sender[i] += t.latency_intra + static_cast<double>(bytes) / t.bw_intra;
+        } else {
+            e.inter_bytes += bytes;
+            e.inter_msgs += 1;
+            sender[i] += t.latency_inter + static_cast<double>(bytes) / t.bw_inter;
+        }
+    };
+    if (k.ring) {
+        if (W > 1) {
+            double total = 0.0;
+            std::vector<double> one(W, 0.0);
+            for (int step = 0; step < W - 1; ++step) {
+                double step_time = 0.0;
+                for (int i = 0; i < W; ++i) {
+                    const int j = (i + 1) % W, chunk = (i + W - step) % W;
+                    const uint64_t bytes = static_cast<uint64_t>(ring_rows[chunk]) * ring_row_bytes;
+                    if (bytes == 0) continue;
+                    one[i] = 0.0;
+                    charge(i, j, bytes, one);
+                    step_time = std::max(step_time, one[i]);
+                }
+                total += step_time;
+            }
+            e.time_s = total;
+        }
+        return e;
+    }
+    std::vector<double> sender(W, 0.0);
+    for (int i = 0; i < W; ++i)
+        for (int j = 0; j < W; ++j)
+            if (k.M[static_cast<size_t>(i) * W + j] > 0) charge(i, j, k.M[static_cast<size_t>(i) * W + j], sender);
+    e.time_s = W ? *std::max_element(sender.begin(), sender.end()) : 0.0;
+    return e;
+}
+
+}  // namespace
+
+void Layer::ledger_entries(const xmoe_topology& topo, std::vector<xmoe_ledger_entry>& out) {
+    out.clear();
+    XMOE_CUDA(cudaDeviceSynchronize());
+    const uint64_t db = topo.dtype_bytes > 0 ? static_cast<uint64_t>(topo.dtype_bytes) : es;
+    const uint64_t rbytes = static_cast<uint64_t>(H) * db;
+    auto comm_sum = [&](std::vector<uint64_t>& v) {  // one process per GPU: sum over the group
+        if (!distributed || v.empty()) return;
+        uint64_t* d = nullptr;
+        XMOE_CUDA(cudaMalloc(&d, sizeof(uint64_t) * v.size()));
+        XMOE_CUDA(cudaMemcpy(d, v.data(), sizeof(uint64_t) * v.size(), cudaMemcpyHostToDevice));
+        ncclResult_t r = ncclAllReduce(d, d, v.size(), ncclUint64, ncclSum, static_cast<ncclComm_t>(ctx->nccl), nullptr);
+        if (r != ncclSuccess) {
+            cudaFree(d);
+            fail(XMOE_ERR_NCCL, std::string("ledger all-reduce: ") + ncclGetErrorString(r));
+        }
+        XMOE_CUDA(cudaMemcpy(v.data(), d, sizeof(uint64_t) * v.size(), cudaMemcpyDeviceToHost));
+        XMOE_CUDA(cudaFree(d));
+    };
+    if (last_ssmb) {  // ssmb.cpp:12-46: G local pf forwards (W = 1 each), then the ring all-gather
+        const int G = static_cast<int>(ssmb_rows.size());
+        std::vector<int32_t> Bh(G, 0);
+        XMOE_CUDA(cudaMemcpy(Bh.data(), ssmb_B, sizeof(int32_t) * G, cudaMemcpyDeviceToHost));
+        std::vector<uint64_t> B(Bh.begin(), Bh.end());
+        comm_sum(B);
+        for (int g = 0; g < G; ++g) {
+            const char* names[3] = {"dispatch_counts", "dispatch_rows", "combine_rows"};
+            for (int q = 0; q < 3; ++q) {
+                Kind k{names[q], std::vector<uint64_t>(1, q == 0 ? 0 : B[g] * rbytes)};
+                out.push_back(finish(k, 1, topo, {}, 0));
+            }
+        }
+        Kind ring{"ssmb_gather_rows", {}, true};
+        if (G > 1) out.push_back(finish(ring, G, topo, ssmb_rows, rbytes));
+        for (size_t i = 0; i < out.size(); ++i) out[i].id = static_cast<int64_t>(i);
+        return;
+    }
+    std::vector<int32_t> tpe(static_cast<size_t>(W) * E);
+    XMOE_CUDA(cudaMemcpy(tpe.data(), tpe_all, sizeof(int32_t) * tpe.size(), cudaMemcpyDeviceToHost));
+    const size_t WW = static_cast<size_t>(W) * W;
+    const bool rbd = d.dispatch_mode == XMOE_DISPATCH_RBD;
+    std::vector<Kind> kinds;
+    if (!rbd) {
+        kinds = {{"dispatch_counts", std::vector<uint64_t>(WW, 0)},
+                 {"dispatch_rows", std::vector<uint64_t>(WW, 0)},
+                 {"combine_rows", std::vector<uint64_t>(WW, 0)}};
+    } else {
+        for (const char* n : {"rbd_dispatch_counts", "rbd_dispatch_meta", "rbd_dispatch_rows1", "rbd_dispatch_meta2",
+                              "rbd_dispatch_rows2", "rbd_combine_rows2", "rbd_combine_rows1"})
+            kinds.push_back({n, std::vector<uint64_t>(WW, 0)});
+    }
+    auto at = [&](int kind, int i, int j) -> uint64_t& { return kinds[kind].M[static_cast<size_t>(i) * W + j]; };
+    for (const Worker& w : workers) {
+        const int s = w.rank;
+        for (int j = 0; j < W; ++j)
+            if (j != s) at(0, s, j) = static_cast<uint64_t>(El) * 8;  // per-expert counts of j's block
+        if (!rbd) {  // pf_pipeline.cpp:30-40, 128
+            for (int e = 0; e < E; ++e) {
+                const uint64_t c = static_cast<uint64_t>(tpe[static_cast<size_t>(s) * E + e]) * rbytes;
+                at(1, s, e / El) += c;
+                at(2, e / El, s) += c;
+            }
+            continue;
+        }
+        // rbd.cpp:130-233, 300-345: per (token, node) group of source s
+        int32_t G = 0;
+        XMOE_CUDA(cudaMemcpy(&G, w.rbd.G_dev, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        const long long S = last_S;
+        std::vector<int32_t> tok(G), dst(G), first(G), n(G), pilot(G);
+        if (G > 0) {
+            XMOE_CUDA(cudaMemcpy(tok.data(), w.rbd.g.token, sizeof(int32_t) * G, cudaMemcpyDeviceToHost));
+            XMOE_CUDA(cudaMemcpy(dst.data(), w.rbd.g.dest, sizeof(int32_t) * G, cudaMemcpyDeviceToHost));
+            XMOE_CUDA(cudaMemcpy(first.data(), w.rbd.g.first_slot, sizeof(int32_t) * G, cudaMemcpyDeviceToHost));
+            XMOE_CUDA(cudaMemcpy(n.data(), w.rbd.g.n, sizeof(int32_t) * G, cudaMemcpyDeviceToHost));
+            XMOE_CUDA(cudaMemcpy(pilot.data(), w.rbd.g.pilot, sizeof(int32_t) * G, cudaMemcpyDeviceToHost));
+        }
+        std::vector<int32_t> slot(static_cast<size_t>(S) * k);
+        if (!slot.empty())
+            XMOE_CUDA(cudaMemcpy(slot.data(), w.slot_pos, sizeof(int32_t) * slot.size(), cudaMemcpyDeviceToHost));
+        int32_t B = 0;
+        XMOE_CUDA(cudaMemcpy(&B, w.B_dev, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        std::vector<int32_t> ex(B > 0 ? B : 1);
+        if (B > 0) XMOE_CUDA(cudaMemcpy(ex.data(), w.expert_ids, sizeof(int32_t) * B, cudaMemcpyDeviceToHost));
+        for (int g = 0; g < G; ++g) {
+            const int L = dst[g];
+            at(2, s, L) += rbytes;  // rows1: the pilot row
+            at(6, L, s) += rbytes;  // combine rows1: one merged row home
+            if (n[g] > 1) at(1, s, L) += db;  // the pilot's weight rides along
+            for (int m = 0; m < n[g]; ++m) {
+                const int p = slot[static_cast<size_t>(tok[g]) * k + first[g] + m];
+                if (p == pilot[g]) continue;
+                const int owner = ex[p] / El;
+                at(1, s, L) += 3 * 8 + db;  // replica descriptor + weight
+                at(3, L, owner) += 3 * 8;   // stage-2 descriptor
+                at(4, L, owner) += rbytes;  // stage-2 row
+                at(5, owner, L) += rbytes;  // reverse stage 2
+            }
+        }
+    }
+    for (auto& kd : kinds) {
+        comm_sum(kd.M);
+        out.push_back(finish(kd, W, topo, {}, 0));
+    }
+    for (size_t i = 0; i < out.size(); ++i) out[i].id = static_cast<int64_t>(i);
 }
 
 }  // namespace xmoe

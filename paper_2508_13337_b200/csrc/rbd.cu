@@ -17,6 +17,12 @@
 //            group size, member index | pilot flag}
 //   expand   receiver writes every copy into its grouped (local expert,
 //            source, position) row — bit-identical to pf_dispatch
+//
+// Two-tier form (gpus_per_node > 1, rbd.cpp:83-358 with node_of = rank /
+// gpus_per_node): groups are (token, destination NODE); the row lands once
+// on the pilot's owner (stage 1), which forwards it to the replicas' owners
+// on the same node (stage 2, an NVLink peer store in expand) and merges the
+// members' outputs by reading them from their owners (reverse stage 2).
 //   merge    receiver scales the pilot's expert output by its weight and adds
 //            each other member's weighted output in packed order
 //            (rbd.cpp:318-336); singletons return raw
@@ -150,6 +156,7 @@ __global__ void __launch_bounds__(256) rbd_draw_kernel(uint64_t s0, uint64_t s1,
 __global__ void rbd_group_count_kernel(const int32_t* __restrict__ slot_pos,
                                        const int32_t* __restrict__ expert_ids, int S, int k, int El,
                                        int32_t* __restrict__ gcount) {
+    // El here = experts per NODE (node key = expert / (experts per GPU x GPUs per node))
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= S) return;
     int n = 0, last = -1;
@@ -237,9 +244,11 @@ static void scan_i32(const int32_t* in, int n, const int32_t* n_dev, int32_t* ou
 // Per token: emit its groups (gid = gbase[t] + j) with the drawn pilot.
 __global__ void rbd_group_fill_kernel(const int32_t* __restrict__ slot_pos,
                                       const int32_t* __restrict__ expert_ids, int S, int k, int El,
-                                      const int32_t* __restrict__ gbase,
+                                      int El_rank, const int32_t* __restrict__ gbase,
                                       const uint64_t* __restrict__ draws, RbdGroups g,
                                       int32_t* __restrict__ flags) {
+    // groups: runs of equal node (El = experts per node); a group lands on
+    // its pilot's owner (rbd.cpp:135-150: stage 1 goes to the pilot's worker)
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= S) return;
     int gid = gbase[t];
@@ -259,11 +268,13 @@ __global__ void rbd_group_fill_kernel(const int32_t* __restrict__ slot_pos,
         const uint64_t limit = ~0ull - (~0ull % static_cast<uint64_t>(n) + 1) % static_cast<uint64_t>(n);
         if (x > limit) atomicExch(flags, 1);  // probability ~n/2^64: reported, not replayed
         const int pick = static_cast<int>(x % static_cast<uint64_t>(n));
+        const int pilot = slot_pos[static_cast<size_t>(t) * k + j + pick];
         g.token[gid] = t;
-        g.dest[gid] = d;
+        g.dest[gid] = expert_ids[pilot] / El_rank;
         g.first_slot[gid] = j;
         g.n[gid] = n;
-        g.pilot[gid] = slot_pos[static_cast<size_t>(t) * k + j + pick];
+        g.pilot[gid] = pilot;
+        (void)d;
         ++gid;
         j += n;
     }
@@ -375,55 +386,6 @@ __global__ void rbd_offsets_kernel(const int32_t* __restrict__ gd_all, int W, in
     }
 }
 
-// Sender pack: each group's row goes once, straight into the destination's
-// unique-row buffer, with one descriptor per copy (tables hold local or
-// NVLink-mapped peer pointers).
-__global__ void __launch_bounds__(256) rbd_pack_kernel(
-    const char* __restrict__ x, int row_bytes, const int32_t* __restrict__ perm, const RbdGroups g,
-    const int32_t* __restrict__ dptr, const int32_t* __restrict__ coff, const int32_t* __restrict__ gpos,
-    const int32_t* __restrict__ ru, const int32_t* __restrict__ rd, const int32_t* __restrict__ cs, int W,
-    int C, int c, const int32_t* __restrict__ slot_pos, int k, const int32_t* __restrict__ dest_row,
-    const double* __restrict__ cw, char* const* __restrict__ recv_u_tab, RbdDesc* const* __restrict__ desc_tab) {
-    const int lane = threadIdx.x & 31;
-    const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-    for (int d = 0; d < W; ++d) {
-        const int beg = dptr[d] + gpos[d * (C + 1) + c];
-        const int cnt = dptr[d] + gpos[d * (C + 1) + c + 1] - beg;
-        const int ub = ru[d * C + c], db = rd[d * C + c], cb = cs[d * C + c];
-        for (long long i = warp; i < cnt; i += nwarps) {
-            const int pos = beg + static_cast<int>(i);
-            const int gid = perm[pos];
-            const int t = g.token[gid], n = g.n[gid], j0 = g.first_slot[gid];
-            const int pilot = g.pilot[gid];
-            const int u = ub + static_cast<int>(i);
-            if (lane < n) {
-                const int p = slot_pos[static_cast<size_t>(t) * k + j0 + lane];
-                RbdDesc dd;
-                dd.u = u;
-                dd.dest_row = dest_row[p];
-                dd.w = cw[p];
-                dd.n = n;
-                dd.member = lane | (p == pilot ? kRbdPilotFlag : 0);
-                desc_tab[d][db + (coff[pos] - cb) + lane] = dd;
-            }
-            // the row lands once, at the pilot's slot of the receiver's grouped
-            // expert input; the receiver copies it to the replicas' slots
-            const char* src = x + static_cast<size_t>(t) * row_bytes;
-            char* dst = recv_u_tab[d] + static_cast<size_t>(dest_row[pilot]) * row_bytes;
-            if ((row_bytes & 15) == 0) {
-                const int4* s4 = reinterpret_cast<const int4*>(src);
-                int4* d4 = reinterpret_cast<int4*>(dst);
-                for (int v = lane; v < (row_bytes >> 4); v += 32) st_na_v4(d4 + v, ld_nc_v4(s4 + v));
-            } else {
-                for (int v = lane; v < (row_bytes >> 3); v += 32)
-                    reinterpret_cast<long long*>(dst)[v] = reinterpret_cast<const long long*>(src)[v];
-            }
-        }
-    }
-    __threadfence_system();
-}
-
 // Token-major sender pack: one warp per token of chunk c loads the token's
 // row once and stores it to each of its (token, dest) groups' pilot slot;
 // lane l < kept(t) writes slot l's descriptor.  Same bytes as the
@@ -436,8 +398,9 @@ __global__ void __launch_bounds__(256) rbd_pack_tokens_kernel(
     const int32_t* __restrict__ gcount, const RbdGroups g, const int32_t* __restrict__ dptr,
     const int32_t* __restrict__ coff, const int32_t* __restrict__ gpos, const int32_t* __restrict__ ru,
     const int32_t* __restrict__ rd, const int32_t* __restrict__ cs, char* const* __restrict__ recv_u_tab,
-    RbdDesc* const* __restrict__ desc_tab) {
+    RbdDesc* const* __restrict__ desc_tab, int gpn) {
     const int lane = threadIdx.x & 31;
+    const bool vec = (row_bytes & 15) == 0;  // else 8-byte rows (F64, odd model_dim)
     const int t_beg = rbd_chunk_t0(c, S, C), t_end = rbd_chunk_t0(c + 1, S, C);
     const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
@@ -449,7 +412,7 @@ __global__ void __launch_bounds__(256) rbd_pack_tokens_kernel(
 #pragma unroll
         for (int q = 0; q < kPackVec; ++q) {
             const int col = lane + 32 * q;
-            v[q] = col < nvec ? ld_nc_v4(src + col) : make_int4(0, 0, 0, 0);
+            v[q] = vec && col < nvec ? ld_nc_v4(src + col) : make_int4(0, 0, 0, 0);
         }
         const int ng = gcount[t], b = gbase[t];
         // lane j < ng: group j of the token (dest ascending)
@@ -468,7 +431,8 @@ __global__ void __launch_bounds__(256) rbd_pack_tokens_kernel(
         }
         // lane l < kept(t): descriptor of slot l (groups are runs of equal dest)
         const int p = lane < k ? slot_pos[static_cast<size_t>(t) * k + lane] : -1;
-        const int dl = p >= 0 ? expert_ids[p] / El : -1;
+        const int owner = p >= 0 ? expert_ids[p] / El : -1;
+        const int dl = p >= 0 ? owner / gpn : -1;  // group key: the member's node
         const int dprev = __shfl_up_sync(0xffffffffu, dl, 1);
         const unsigned starts = __ballot_sync(0xffffffffu, p >= 0 && (lane == 0 || dl != dprev));
         const unsigned le = starts & (0xffffffffu >> (31 - lane));
@@ -486,8 +450,16 @@ __global__ void __launch_bounds__(256) rbd_pack_tokens_kernel(
             dd.dest_row = dest_row[p];
             dd.w = cw[p];
             dd.n = n_j;
-            dd.member = m | (p == pil_j ? kRbdPilotFlag : 0);
+            dd.member = m | (p == pil_j ? kRbdPilotFlag : 0) | (owner << kRbdOwnerShift);
             desc_tab[d_j][desc_j + m] = dd;
+        }
+        if (!vec) {
+            const long long* s8 = reinterpret_cast<const long long*>(src);
+            for (int j = 0; j < ng; ++j) {
+                long long* d8 = reinterpret_cast<long long*>(__shfl_sync(0xffffffffu, dst, j));
+                for (int q = lane; q < (row_bytes >> 3); q += 32) d8[q] = s8[q];
+            }
+            continue;
         }
         for (int base = 0; base < nvec; base += 32 * kPackVec) {
             if (base > 0) {
@@ -513,19 +485,18 @@ __global__ void __launch_bounds__(256) rbd_pack_tokens_kernel(
 // Receiver expand: every replica copies its group's row from the pilot's
 // slot (where the sender put it) into its own grouped slot; records each
 // group's first descriptor for the merge.
-__global__ void __launch_bounds__(256) rbd_expand_kernel(const char* __restrict__ recv_u,
+__global__ void __launch_bounds__(256) rbd_expand_kernel(char* const* __restrict__ recv_tab,
                                                          int row_bytes, const RbdDesc* __restrict__ desc,
                                                          const int32_t* __restrict__ rx, int C, int ck,
-                                                         char* __restrict__ grouped,
+                                                         const char* __restrict__ grouped,
                                                          int32_t* __restrict__ gstart) {
-    (void)recv_u;
     const int dbeg = rx[2 * C + ck], dend = dbeg + rx[3 * C + ck];
     const int lane = threadIdx.x & 31;
     const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
     for (long long c = dbeg + warp; c < dend; c += nwarps) {
         const RbdDesc dd = desc[c];
-        const int m = dd.member & ~kRbdPilotFlag;
+        const int m = dd.member & kRbdMemberMask;
         if (lane == 0 && m == 0) gstart[dd.u] = static_cast<int>(c);
         if (dd.member & kRbdPilotFlag) continue;  // already in place
         int prow = dd.dest_row;
@@ -533,8 +504,10 @@ __global__ void __launch_bounds__(256) rbd_expand_kernel(const char* __restrict_
             const RbdDesc pq = desc[c - m + q];
             if (pq.member & kRbdPilotFlag) prow = pq.dest_row;
         }
+        // the pilot landed here; a replica owned by another GPU of the node
+        // gets its row over NVLink (stage 2, rbd.cpp:178-233)
         const char* s = grouped + static_cast<size_t>(prow) * row_bytes;
-        char* o = grouped + static_cast<size_t>(dd.dest_row) * row_bytes;
+        char* o = recv_tab[dd.member >> kRbdOwnerShift] + static_cast<size_t>(dd.dest_row) * row_bytes;
         if ((row_bytes & 15) == 0) {
             for (int v = lane; v < (row_bytes >> 4); v += 32)
                 st_na_v4(reinterpret_cast<int4*>(o) + v, reinterpret_cast<const int4*>(s)[v]);
@@ -547,7 +520,7 @@ __global__ void __launch_bounds__(256) rbd_expand_kernel(const char* __restrict_
 
 // Receiver merge (rbd.cpp:318-336): one warp per received group.
 template <typename T>
-__global__ void __launch_bounds__(256) rbd_merge_kernel(const T* __restrict__ eout, int H,
+__global__ void __launch_bounds__(256) rbd_merge_kernel(const char* const* __restrict__ eout_tab, int H,
                                                         const RbdDesc* __restrict__ desc,
                                                         const int32_t* __restrict__ gstart,
                                                         const int32_t* __restrict__ rx, int C, int ck,
@@ -560,8 +533,11 @@ __global__ void __launch_bounds__(256) rbd_merge_kernel(const T* __restrict__ eo
         const int c0 = gstart[u];
         const int n = desc[c0].n;
         T* out = back_u + static_cast<size_t>(u) * H;
+        auto row_of = [&](const RbdDesc& d) {
+            return reinterpret_cast<const T*>(eout_tab[d.member >> kRbdOwnerShift]) + static_cast<size_t>(d.dest_row) * H;
+        };
         if (n == 1) {  // singleton: raw row
-            const T* y = eout + static_cast<size_t>(desc[c0].dest_row) * H;
+            const T* y = row_of(desc[c0]);
             for (int h = lane; h < H; h += 32) out[h] = y[h];
             continue;
         }
@@ -571,19 +547,19 @@ __global__ void __launch_bounds__(256) rbd_merge_kernel(const T* __restrict__ eo
         const RbdDesc pd = desc[c0 + pm];
         for (int h = lane; h < H; h += 32) {
             if constexpr (sizeof(T) == 8) {
-                double acc = __dmul_rn(static_cast<double>(eout[static_cast<size_t>(pd.dest_row) * H + h]), pd.w);
+                double acc = __dmul_rn(static_cast<double>(row_of(pd)[h]), pd.w);
                 for (int m = 0; m < n; ++m) {
                     if (m == pm) continue;
                     const RbdDesc md = desc[c0 + m];
-                    acc = __dadd_rn(acc, __dmul_rn(md.w, static_cast<double>(eout[static_cast<size_t>(md.dest_row) * H + h])));
+                    acc = __dadd_rn(acc, __dmul_rn(md.w, static_cast<double>(row_of(md)[h])));
                 }
                 out[h] = static_cast<T>(acc);
             } else {
-                float acc = __bfloat162float(eout[static_cast<size_t>(pd.dest_row) * H + h]) * static_cast<float>(pd.w);
+                float acc = __bfloat162float(row_of(pd)[h]) * static_cast<float>(pd.w);
                 for (int m = 0; m < n; ++m) {
                     if (m == pm) continue;
                     const RbdDesc md = desc[c0 + m];
-                    acc = fmaf(static_cast<float>(md.w), __bfloat162float(eout[static_cast<size_t>(md.dest_row) * H + h]), acc);
+                    acc = fmaf(static_cast<float>(md.w), __bfloat162float(row_of(md)[h]), acc);
                 }
                 out[h] = __float2bfloat16_rn(acc);
             }
@@ -651,7 +627,7 @@ __global__ void __launch_bounds__(256) rbd_combine_kernel(const char* const* __r
 // BF16 merge, vectorised: one warp per (received group, 512-column segment);
 // lane m < n holds member m's row and weight, the pilot is applied first,
 // every row moves 16 bytes per lane, fp32 math.
-__global__ void __launch_bounds__(256) rbd_merge_bf16_kernel(const __nv_bfloat16* __restrict__ eout, int H,
+__global__ void __launch_bounds__(256) rbd_merge_bf16_kernel(const char* const* __restrict__ eout_tab, int H,
                                                              const RbdDesc* __restrict__ desc,
                                                              const int32_t* __restrict__ gstart,
                                                              const int32_t* __restrict__ rx, int C, int ck,
@@ -666,12 +642,13 @@ __global__ void __launch_bounds__(256) rbd_merge_bf16_kernel(const __nv_bfloat16
         const int u = ubeg + static_cast<int>(item / nseg), seg = static_cast<int>(item % nseg);
         const int c0 = gstart[u];
         const int n = desc[c0].n;
-        int my_row = 0;
+        const __nv_bfloat16* my_row = nullptr;
         float my_w = 0.f;
         int is_p = 0;
         if (lane < n) {
             const RbdDesc md = desc[c0 + lane];
-            my_row = md.dest_row;
+            my_row = reinterpret_cast<const __nv_bfloat16*>(eout_tab[md.member >> kRbdOwnerShift]) +
+                     static_cast<size_t>(md.dest_row) * H;
             my_w = static_cast<float>(md.w);
             is_p = (md.member & kRbdPilotFlag) ? 1 : 0;
         }
@@ -684,10 +661,10 @@ __global__ void __launch_bounds__(256) rbd_merge_bf16_kernel(const __nv_bfloat16
             const bool ok = c < cend;
             float acc[8];
             {
-                const int r = __shfl_sync(0xffffffffu, my_row, pl);
+                const __nv_bfloat16* r = reinterpret_cast<const __nv_bfloat16*>(
+                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), pl));
                 const float wp = n == 1 ? 1.f : __shfl_sync(0xffffffffu, my_w, pl);
-                const int4 v = ok ? ld_nc_v4(reinterpret_cast<const int4*>(eout + static_cast<size_t>(r) * H) + c)
-                                  : make_int4(0, 0, 0, 0);
+                const int4 v = ok ? ld_nc_v4(reinterpret_cast<const int4*>(r) + c) : make_int4(0, 0, 0, 0);
                 if (n == 1) {  // singleton: raw row (rbd.cpp:323-325)
                     if (ok) dst[c] = v;
                     continue;
@@ -702,10 +679,10 @@ __global__ void __launch_bounds__(256) rbd_merge_bf16_kernel(const __nv_bfloat16
             }
             for (int m = 0; m < n; ++m) {
                 if (m == pl) continue;
-                const int r = __shfl_sync(0xffffffffu, my_row, m);
+                const __nv_bfloat16* r = reinterpret_cast<const __nv_bfloat16*>(
+                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_row), m));
                 const float wm = __shfl_sync(0xffffffffu, my_w, m);
-                const int4 v = ok ? ld_nc_v4(reinterpret_cast<const int4*>(eout + static_cast<size_t>(r) * H) + c)
-                                  : make_int4(0, 0, 0, 0);
+                const int4 v = ok ? ld_nc_v4(reinterpret_cast<const int4*>(r) + c) : make_int4(0, 0, 0, 0);
                 const uint32_t q[4] = {static_cast<uint32_t>(v.x), static_cast<uint32_t>(v.y),
                                        static_cast<uint32_t>(v.z), static_cast<uint32_t>(v.w)};
 #pragma unroll
@@ -812,14 +789,15 @@ void launch_rbd_groups(const int32_t* slot_pos, const int32_t* expert_ids, int S
         XMOE_CUDA(cudaMemsetAsync(wk.G_dev, 0, sizeof(int32_t), st));
         return;
     }
-    rbd_group_count_kernel<<<ceil_div(S, 256), 256, 0, st>>>(slot_pos, expert_ids, S, k, El, wk.gcount);
+    const int El_node = El * wk.gpn;  // group key: the copy's node
+    rbd_group_count_kernel<<<ceil_div(S, 256), 256, 0, st>>>(slot_pos, expert_ids, S, k, El_node, wk.gcount);
     XMOE_LAUNCH_CHECK();
     scan_i32(wk.gcount, S, nullptr, wk.gbase, wk.G_dev, st);
     const long long max_groups = static_cast<long long>(S) * k;
     rbd_draw_kernel<<<ceil_div(max_groups, kRbdChunk), 256, 0, st>>>(
         state[0], state[1], state[2], state[3], jumps, wk.G_dev, wk.draws);
     XMOE_LAUNCH_CHECK();
-    rbd_group_fill_kernel<<<ceil_div(S, 256), 256, 0, st>>>(slot_pos, expert_ids, S, k, El, wk.gbase,
+    rbd_group_fill_kernel<<<ceil_div(S, 256), 256, 0, st>>>(slot_pos, expert_ids, S, k, El_node, El, wk.gbase,
                                                              wk.draws, wk.g, wk.flags);
     XMOE_LAUNCH_CHECK();
 }
@@ -850,48 +828,42 @@ void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, int W, int
                      const int32_t* slot_pos, int k, const int32_t* dest_row, const double* cw,
                      char* const* recv_u_tab, RbdDesc* const* desc_tab, cudaStream_t st, int S,
                      const int32_t* expert_ids, int El) {
-    int grid = warp_grid(max_groups / wk.C + 1);
-    if (g_copy_blocks > 0 && grid > g_copy_blocks) grid = g_copy_blocks;
-    if ((row_bytes & 15) == 0 && k <= 32 && S > 0 && expert_ids) {
-        const int nt = static_cast<int>(static_cast<long long>(c + 1) * S / wk.C - static_cast<long long>(c) * S / wk.C);
-        int tg = warp_grid(nt);
-        if (g_copy_blocks > 0 && tg > g_copy_blocks) tg = g_copy_blocks;
-        rbd_pack_tokens_kernel<<<tg, 256, 0, st>>>(
-            static_cast<const char*>(x), row_bytes, S, wk.C, c, k, El, slot_pos, expert_ids, dest_row, cw, wk.gbase,
-            wk.gcount, wk.g, wk.dptr, wk.coff, wk.gpos, wk.ru, wk.rd, wk.cs, recv_u_tab, desc_tab);
-        XMOE_LAUNCH_CHECK();
-        return;
-    }
-    rbd_pack_kernel<<<grid, 256, 0, st>>>(static_cast<const char*>(x), row_bytes, wk.perm, wk.g, wk.dptr, wk.coff,
-                                          wk.gpos, wk.ru, wk.rd, wk.cs, W, wk.C, c, slot_pos, k, dest_row, cw,
-                                          recv_u_tab, desc_tab);
+    (void)W;
+    (void)max_groups;
+    require((row_bytes & 7) == 0 && k <= 32 && expert_ids, XMOE_ERR_VALIDATION,
+            "rbd pack needs 8-byte rows, top_k <= 32");
+    const int nt = static_cast<int>(static_cast<long long>(c + 1) * S / wk.C - static_cast<long long>(c) * S / wk.C);
+    if (nt == 0) return;
+    int tg = warp_grid(nt);
+    if (g_copy_blocks > 0 && tg > g_copy_blocks) tg = g_copy_blocks;
+    rbd_pack_tokens_kernel<<<tg, 256, 0, st>>>(static_cast<const char*>(x), row_bytes, S, wk.C, c, k, El, slot_pos,
+                                               expert_ids, dest_row, cw, wk.gbase, wk.gcount, wk.g, wk.dptr, wk.coff,
+                                               wk.gpos, wk.ru, wk.rd, wk.cs, recv_u_tab, desc_tab, wk.gpn);
     XMOE_LAUNCH_CHECK();
 }
 
 void launch_rbd_expand(int row_bytes, const RbdDesc* desc, const RbdWork& wk, int c, long long max_desc,
-                       void* grouped, int32_t* gstart, cudaStream_t st) {
+                       void* grouped, char* const* recv_tab, int32_t* gstart, cudaStream_t st) {
     int grid = warp_grid(max_desc / wk.C + 1);
     if (g_copy_blocks > 0 && grid > g_copy_blocks) grid = g_copy_blocks;
-    rbd_expand_kernel<<<grid, 256, 0, st>>>(nullptr, row_bytes, desc, wk.rx, wk.C, c,
-                                            static_cast<char*>(grouped), gstart);
+    rbd_expand_kernel<<<grid, 256, 0, st>>>(recv_tab, row_bytes, desc, wk.rx, wk.C, c,
+                                            static_cast<const char*>(grouped), gstart);
     XMOE_LAUNCH_CHECK();
 }
 
-void launch_rbd_merge(int dtype, const void* eout, int H, const RbdDesc* desc, const int32_t* gstart,
+void launch_rbd_merge(int dtype, const char* const* eout_tab, int H, const RbdDesc* desc, const int32_t* gstart,
                       const RbdWork& wk, int c, long long max_groups, void* back_u, cudaStream_t st) {
     const long long per = max_groups / wk.C + 1;
     auto cap = [](int g) { return g_copy_blocks > 0 && g > g_copy_blocks ? g_copy_blocks : g; };
     if (dtype == XMOE_F64)
-        rbd_merge_kernel<double><<<cap(warp_grid(per)), 256, 0, st>>>(
-            static_cast<const double*>(eout), H, desc, gstart, wk.rx, wk.C, c, static_cast<double*>(back_u));
+        rbd_merge_kernel<double><<<cap(warp_grid(per)), 256, 0, st>>>(eout_tab, H, desc, gstart, wk.rx, wk.C, c,
+                                                                     static_cast<double*>(back_u));
     else if (H % 8 == 0)
         rbd_merge_bf16_kernel<<<cap(warp_grid(per * ((H + 511) / 512))), 256, 0, st>>>(
-            static_cast<const __nv_bfloat16*>(eout), H, desc, gstart, wk.rx, wk.C, c,
-            static_cast<__nv_bfloat16*>(back_u));
+            eout_tab, H, desc, gstart, wk.rx, wk.C, c, static_cast<__nv_bfloat16*>(back_u));
     else
         rbd_merge_kernel<__nv_bfloat16><<<cap(warp_grid(per)), 256, 0, st>>>(
-            static_cast<const __nv_bfloat16*>(eout), H, desc, gstart, wk.rx, wk.C, c,
-            static_cast<__nv_bfloat16*>(back_u));
+            eout_tab, H, desc, gstart, wk.rx, wk.C, c, static_cast<__nv_bfloat16*>(back_u));
     XMOE_LAUNCH_CHECK();
 }
 

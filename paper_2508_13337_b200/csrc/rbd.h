@@ -11,6 +11,8 @@ namespace xmoe {
 constexpr int kRbdChunk = 256;  // groups per jump-ahead chunk
 constexpr int kRbdJumps = 24;   // chunk index < 2^24
 constexpr int kRbdPilotFlag = 1 << 16;
+constexpr int kRbdMemberMask = 0xFFFF;
+constexpr int kRbdOwnerShift = 20;  // member's owner rank (two-tier: may differ from the landing rank)
 
 // One (token, destination rank) group of a source rank, in the reference's
 // std::map order (rbd.cpp:35-43).  SoA, indexed by group id.
@@ -29,12 +31,13 @@ struct RbdDesc {
     int32_t dest_row;  // row of the copy in the receiver's grouped expert input
     double w;          // combine weight of the copy
     int32_t n;         // group size
-    int32_t member;    // member index | kRbdPilotFlag
+    int32_t member;    // member index | kRbdPilotFlag | owner rank << kRbdOwnerShift
 };
 static_assert(sizeof(RbdDesc) == 24, "descriptor layout");
 
 struct RbdWork {
     RbdGroups g;
+    int gpn;           // GPUs per node: groups are (token, node); 1 = per-GPU bypass
     int32_t* gcount;   // [S]
     int32_t* gbase;    // [S]
     int32_t* G_dev;    // total groups
@@ -75,9 +78,12 @@ void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, int W, int
                      const int32_t* slot_pos, int k, const int32_t* dest_row, const double* cw,
                      char* const* recv_u_tab, RbdDesc* const* desc_tab, cudaStream_t st, int S = 0,
                      const int32_t* expert_ids = nullptr, int El = 1);
+// replicas copy their pilot's row (local) into their owner's grouped input
+// (recv_tab: local or NVLink peer); `grouped` is this landing rank's input
 void launch_rbd_expand(int row_bytes, const RbdDesc* desc, const RbdWork& wk, int c, long long max_desc,
-                       void* grouped, int32_t* gstart, cudaStream_t st);
-void launch_rbd_merge(int dtype, const void* eout, int H, const RbdDesc* desc, const int32_t* gstart,
+                       void* grouped, char* const* recv_tab, int32_t* gstart, cudaStream_t st);
+// each group's members' outputs read from their owners (eout_tab)
+void launch_rbd_merge(int dtype, const char* const* eout_tab, int H, const RbdDesc* desc, const int32_t* gstart,
                       const RbdWork& wk, int c, long long max_groups, void* back_u, cudaStream_t st);
 void launch_rbd_combine(int dtype, const char* const* back_tab, int H, int S, const RbdWork& wk, int c,
                         const double* cw, const void* addend, void* out, cudaStream_t st);

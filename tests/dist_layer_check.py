@@ -30,9 +30,11 @@ def main():
     dist.broadcast_object_list(obj, src=0)
     ctx = capi.Context(local, world, rank, obj[0])
     failures = []
-    cases = [(capi.F64, capi.NAIVE, 97, 8, 3, 24, 16), (capi.F64, capi.RBD, 97, 8, 3, 24, 16),
-             (capi.BF16, capi.NAIVE, 512, 16, 6, 256, 128), (capi.BF16, capi.RBD, 512, 16, 6, 256, 128)]
-    for ci, (dt, mode, S, e_per, k, H, F) in enumerate(cases):
+    cases = [(capi.F64, capi.NAIVE, 97, 8, 3, 24, 16, 1), (capi.F64, capi.RBD, 97, 8, 3, 24, 16, 1),
+             (capi.BF16, capi.NAIVE, 512, 16, 6, 256, 128, 1), (capi.BF16, capi.RBD, 512, 16, 6, 256, 128, 1)]
+    if world % 2 == 0:  # two-tier RBD: nodes of 2 GPUs, stage 2 and its reverse over NVLink
+        cases += [(capi.F64, capi.RBD, 97, 8, 5, 24, 16, 2), (capi.BF16, capi.RBD, 512, 16, 6, 256, 128, 2)]
+    for ci, (dt, mode, S, e_per, k, H, F, gpn) in enumerate(cases):
         E = e_per * world
         el = E // world
         rng = np.random.default_rng(100 + ci)
@@ -53,9 +55,12 @@ def main():
         dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(tdt).cuda()  # noqa: E731
         layer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=cap,
                            max_tokens=S, dtype=dt, gate=dv(gate), w1=dv(w1[rank * el:(rank + 1) * el]),
-                           w2=dv(w2[rank * el:(rank + 1) * el]), dispatch_mode=mode, seed=seed)
+                           w2=dv(w2[rank * el:(rank + 1) * el]), dispatch_mode=mode, seed=seed,
+                           gpus_per_node=gpn)
         out = layer.forward(dv(x[rank])).to(torch.float64).cpu().numpy()
         led = layer.ledger()
+        # reference-schema ledger: every rank contributes its sources (collective)
+        csv = layer.ledger_csv(capi.Topology.reference_defaults(gpus_per_node=gpn, dtype_bytes=2))
         gate_dev = None
         if dt == capi.F64:
             top, wt = ctx.gate_forward(dv(x[rank]), dv(gate), k)
@@ -69,7 +74,8 @@ def main():
             if mode == capi.NAIVE:
                 want = O.pf_moe_forward(list(x), W, E, k, cap, gates=gates, exact=exact)
             else:
-                want = O.rbd_moe_forward(list(x), W, E, k, cap, seed, gates=gates, exact=exact)
+                want = O.rbd_moe_forward(list(x), W, E, k, cap, seed, [r // gpn for r in range(world)],
+                                         gates=gates, exact=exact)
             for r in range(world):
                 o = got[r][0]
                 if dt == capi.F64:
@@ -80,8 +86,20 @@ def main():
                     ok = err < 1e-2 and max_rel_diff(o, want[r]) < 2e-2
                 if not ok:
                     failures.append((ci, r, err))
+            if dt == capi.F64:
+                from oracle import refbind
+                if refbind.available():
+                    rl = refbind.Layer(gate, w1, w2)
+                    if mode == capi.NAIVE:
+                        rl.pf_moe_forward(x, k, cap, [r // gpn for r in range(world)])
+                    else:
+                        rl.rbd_moe_forward(x, k, cap, seed, [r // gpn for r in range(world)])
+                    if csv != refbind.last_ledger_csv():
+                        failures.append((ci, "ledger_csv", csv, refbind.last_ledger_csv()))
+                    else:
+                        print(f"case {ci} ledger CSV identical to the reference's", flush=True)
             tot = {kk: sum(g[2][kk] for g in got) for kk in got[0][2]}
-            print(f"case {ci} dtype={'f64' if dt == capi.F64 else 'bf16'} mode={'rbd' if mode else 'naive'} "
+            print(f"case {ci} dtype={'f64' if dt == capi.F64 else 'bf16'} mode={'rbd' if mode else 'naive'} gpn={gpn} "
                   f"cap={cap} ledger={tot}", flush=True)
         del layer
         dist.barrier()

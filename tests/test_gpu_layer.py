@@ -163,6 +163,57 @@ def test_rbd_forward_f64_bit_exact(W):
         assert led["dispatch_rows_offrank"] == groups * H * 8
 
 
+@pytest.mark.parametrize("W,gpn", [(2, 2), (4, 2), (8, 2), (8, 4)])
+def test_rbd_two_tier_f64_bit_exact(W, gpn):
+    """Two-tier rbd_moe_forward (rbd.cpp:83-358, node_of = rank / gpn): one
+    row per (token, destination node) to the pilot's owner, forwarded inside
+    the node to the replicas' owners, merged at the landing rank from the
+    owners' outputs — bit-exact to the pinned oracle given the device softmax
+    weights, and to the compiled reference within the exp-ulp bound."""
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, W, -1)
+    rng = O.Rng(2929 + 10 * W + gpn)
+    node_of = [r // gpn for r in range(W)]
+    for trial in range(4):
+        E = W * (1 + rng.below(3))
+        k = 1 + rng.below(min(E, 5))
+        H = 2 + rng.below(5)
+        F = 2 + rng.below(5)
+        S = 2 + rng.below(23)
+        cap = 1 + rng.below(4) if trial % 2 == 0 else S * k
+        w = O.make_layer_weights(rng, E, H, F)
+        toks = np.array([rng.uniform(-1.0, 1.0) for _ in range(W * S * H)]).reshape(W, S, H)
+        seed = rng.next_u64()
+        L = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=cap, max_tokens=S,
+                       dtype=capi.F64, gate=dev(w.gate), w1=dev(w.w1), w2=dev(w.w2), dispatch_mode=capi.RBD,
+                       seed=seed, gpus_per_node=gpn)
+        got = host(L.forward(dev(toks)))
+        gates = _device_gates(ctx, toks, w, k)
+        exact = O.rbd_moe_forward(list(toks), w, E, k, cap, seed, node_of, gates=gates)
+        pure = O.rbd_moe_forward(list(toks), w, E, k, cap, seed, node_of)
+        for i in range(W):
+            assert np.array_equal(got[i], exact[i]), (trial, i)
+            assert max_rel_diff(got[i], pure[i]) < 1e-14
+
+
+def test_rbd_two_tier_bf16_vs_oracle():
+    from paper_2508_13337_b200 import capi
+    W, gpn, S, E, k, H, F = 8, 4, 256, 64, 6, 128, 64
+    ctx = capi.Context(0, W, -1)
+    rng = np.random.default_rng(99)
+    w = O.LayerWeights(grid_gate(rng, H, E), bf16_round(rng.uniform(-0.1, 0.1, (E, H, F))),
+                       bf16_round(rng.uniform(-0.1, 0.1, (E, F, H))))
+    x = grid_tokens(rng, W, S, H)
+    L = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k, max_tokens=S,
+                   dtype=capi.BF16, gate=dev(w.gate, torch.bfloat16), w1=dev(w.w1, torch.bfloat16),
+                   w2=dev(w.w2, torch.bfloat16), dispatch_mode=capi.RBD, seed=4, gpus_per_node=gpn)
+    assert L.chunks() == 1
+    got = host(L.forward(dev(x, torch.bfloat16)))
+    want = O.rbd_moe_forward(list(x), w, E, k, S * k, 4, [r // gpn for r in range(W)], exact=False)
+    for i in range(W):
+        assert norm_rel(got[i], want[i]) < 1e-2, norm_rel(got[i], want[i])
+
+
 @pytest.mark.parametrize("W,S,E,k,H,F", [(4, 512, 64, 6, 256, 128), (8, 256, 64, 6, 128, 64)])
 def test_rbd_forward_bf16_vs_oracle(W, S, E, k, H, F):
     from paper_2508_13337_b200 import capi
@@ -286,3 +337,54 @@ def test_chunked_forward_bit_identical(W, S, chunks, cap_factor, shared, mode):
     assert led["routed_copies"] > 0
     if mode == 1 and W > 1:
         assert led["unique_rows_offrank"] <= led["copies_offrank"]
+
+
+@pytest.mark.parametrize("mode,W,gpn", [(0, 4, 1), (0, 4, 2), (1, 4, 1), (1, 4, 2), (1, 8, 4), (0, 1, 1)])
+def test_ledger_csv_matches_reference(ref, mode, W, gpn):
+    """The reference-schema ledger of a GPU forward (xmoe_layer_ledger_csv)
+    equals CostLedger::write_csv of the UNMODIFIED reference forward on the
+    same inputs, byte for byte: kinds, ids, intra/inter bytes and the
+    alpha-beta modeled times (default Topology, node_of = rank / gpn)."""
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, W, -1)
+    rng = O.Rng(515 + 7 * W + gpn + mode)
+    E = W * 4
+    k, H, F, S = 3, 6, 5, 29
+    cap = 12
+    w = O.make_layer_weights(rng, E, H, F)
+    toks = np.array([rng.uniform(-1.0, 1.0) for _ in range(W * S * H)]).reshape(W, S, H)
+    seed = rng.next_u64()
+    node_of = [r // gpn for r in range(W)]
+    L = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=cap, max_tokens=S,
+                   dtype=capi.F64, gate=dev(w.gate), w1=dev(w.w1), w2=dev(w.w2),
+                   dispatch_mode=capi.RBD if mode else capi.NAIVE, seed=seed, gpus_per_node=gpn if mode else 1)
+    L.forward(dev(toks))
+    topo = capi.Topology.reference_defaults(gpus_per_node=gpn, dtype_bytes=2)
+    got = L.ledger_csv(topo)
+    rl = ref.Layer(w.gate, w.w1, w.w2)
+    if mode:
+        rl.rbd_moe_forward(toks, k, cap, seed, node_of)
+    else:
+        rl.pf_moe_forward(toks, k, cap, node_of)
+    want = ref.last_ledger_csv()
+    assert got == want, (got, want)
+    ents = L.ledger_entries(topo)
+    assert [e["kind"] for e in ents] == [line.split(",")[1] for line in want.strip().split("\n")[1:]]
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_ledger_csv_ssmb_matches_reference(ref, G):
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, G, -1)
+    rng = O.Rng(77 + G)
+    E, k, H, F, S = 8, 2, 5, 4, 45
+    w = O.make_layer_weights(rng, E, H, F)
+    x = np.array([rng.uniform(-1.0, 1.0) for _ in range(S * H)]).reshape(S, H)
+    bounds = O.ssmb_shards(S, G)
+    L = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
+                   max_tokens=max(n for _, n in bounds), dtype=capi.F64, gate=dev(w.gate), w1=dev(w.w1),
+                   w2=dev(w.w2), ssmb=True)
+    L.ssmb_forward(dev(x))
+    got = L.ledger_csv(capi.Topology.reference_defaults(gpus_per_node=1, dtype_bytes=2))
+    ref.Layer(w.gate, w.w1, w.w2).ssmb_forward(x, G, k, S * k)
+    assert got == ref.last_ledger_csv()
