@@ -300,6 +300,14 @@ def main():
     torch.cuda.synchronize()
     barrier()
     launches = capi.kernel_launches() - launches0
+    # the last timed forward's collectives in the reference's CostLedger schema
+    # (one node of 8 GPUs: every off-rank byte is intra-node NVLink), and the
+    # padded (GShard) comparator's for the same layer
+    topo = capi.Topology.reference_defaults(gpus_per_node=8)
+    ref_ledger = {e["kind"]: {"intra_bytes": e["intra_bytes"], "inter_bytes": e["inter_bytes"],
+                              "self_bytes": e["self_bytes"]} for e in layer.ledger_entries(topo)}
+    padded_csv = layer.ledger_csv(topo, padded=True).strip().split("\n")[1:]
+    padded_ledger = {ln.split(",")[1]: int(ln.split(",")[2]) + int(ln.split(",")[3]) for ln in padded_csv}
     ms = max_over_ranks(t0.elapsed_time(t1) / args.steps)
     clk = clocks.stop(world) if rank == 0 else None
 
@@ -506,6 +514,9 @@ def main():
                 "note": "dispatch kernel, isolated (timing mode), off-rank row bytes this GPU sends over NVLink "
                         "/ kernel time; peak = measured 770 GB/s peer copy per direction (B200_PROFILING.md)"},
             "dispatch_compare": dispatch_compare,
+            "ref_schema_ledger": {"entries": ref_ledger, "padded_offrank_bytes": padded_ledger,
+                                  "note": "xmoe_layer_ledger_entries / xmoe_layer_padded_ledger_csv of the "
+                                          "last timed forward, moesim CostLedger kinds (global, all ranks)"},
             "fwd_bwd": fwd_bwd,
             "gpu_launches": launches,
             "clocks": clk,

@@ -255,6 +255,12 @@ int xmoe_layer_ledger_entries(xmoe_layer* layer, const xmoe_topology* topo, xmoe
  * *len receives the full length; at most cap bytes (NUL-terminated) are
  * written. */
 int xmoe_layer_ledger_csv(xmoe_layer* layer, const xmoe_topology* topo, char* buf, int64_t cap, int64_t* len);
+/* The padded (GShard) comparator for this layer: the ledger the reference's
+ * padded_moe_forward (padded_pipeline.cpp:75-159) charges — every pair moves
+ * e_local * max_token_count padded rows each way, whatever the routing —
+ * in the same CSV schema ("padded_dispatch_rows", "padded_combine_rows"). */
+int xmoe_layer_padded_ledger_csv(xmoe_layer* layer, const xmoe_topology* topo, char* buf, int64_t cap,
+                                 int64_t* len);
 
 /* Per-stage device time of the last forward (ms, CUDA events), order:
  * gate, pft, dispatch, experts, shared, combine, total, then the exchange

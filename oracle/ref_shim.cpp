@@ -295,10 +295,12 @@ int ref_padded_moe_forward(void* layer, std::int64_t W, const std::int64_t* node
                            std::int64_t cap, double* out) {
     return guarded([&] {
         const auto& L = *static_cast<Layer*>(layer);
-        auto comm = make_comm(W, node_of, nullptr);
+        CostLedger led;
+        auto comm = make_comm(W, node_of, &led);
         const auto inst = make_inst(L, W, tokens, S, k, cap);
         const auto res = padded_moe_forward(inst, comm);
         for (std::int64_t w = 0; w < W; ++w) from_matrix(res[w], out + w * S * L.H);
+        dump_ledger(led, nullptr);
     });
 }
 

@@ -98,6 +98,7 @@ def lib():
         L.xmoe_layer_chunks.argtypes = [p, p]
         L.xmoe_layer_ledger_entries.argtypes = [p, p, p, i32, p]
         L.xmoe_layer_ledger_csv.argtypes = [p, p, p, i64, p]
+        L.xmoe_layer_padded_ledger_csv.argtypes = [p, p, p, i64, p]
         L.xmoe_layer_bwd_stage_ms.argtypes = [p, p, i32]
         L.xmoe_layer_stage_ms.argtypes = [p, C.POINTER(C.c_float), i32]
         L.xmoe_plan_dispatch.argtypes = [i32, i32, p, i32, p, p, p]
@@ -356,13 +357,15 @@ class Layer:
                  "inter_bytes": e.inter_bytes, "intra_msgs": e.intra_msgs, "inter_msgs": e.inter_msgs,
                  "time_s": e.time_s} for e in buf[:n.value]]
 
-    def ledger_csv(self, topo: "Topology | None" = None) -> str:
-        """CostLedger::write_csv of the last forward (collectives.cpp:26-34)."""
+    def ledger_csv(self, topo: "Topology | None" = None, padded: bool = False) -> str:
+        """CostLedger::write_csv of the last forward (collectives.cpp:26-34);
+        padded=True: the padded (GShard) comparator's ledger for this layer."""
+        fn = lib().xmoe_layer_padded_ledger_csv if padded else lib().xmoe_layer_ledger_csv
         n = C.c_int64()
         tp = C.byref(topo) if topo is not None else None
-        _check(lib().xmoe_layer_ledger_csv(self.h, tp, None, 0, C.byref(n)))
+        _check(fn(self.h, tp, None, 0, C.byref(n)))
         buf = C.create_string_buffer(n.value + 1)
-        _check(lib().xmoe_layer_ledger_csv(self.h, tp, buf, n.value + 1, C.byref(n)))
+        _check(fn(self.h, tp, buf, n.value + 1, C.byref(n)))
         return buf.value.decode()
 
     def set_graph(self, on: bool):

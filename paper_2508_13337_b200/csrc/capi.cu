@@ -428,11 +428,13 @@ int xmoe_layer_ledger_entries(xmoe_layer* layer, const xmoe_topology* topo, xmoe
     });
 }
 
-int xmoe_layer_ledger_csv(xmoe_layer* layer, const xmoe_topology* topo, char* buf, int64_t cap, int64_t* len) {
+static int ledger_csv(xmoe_layer* layer, const xmoe_topology* topo, char* buf, int64_t cap, int64_t* len,
+                      bool padded) {
     return guarded([&] {
         require(len != nullptr, XMOE_ERR_VALIDATION, "null output");
         std::vector<xmoe_ledger_entry> v;
-        layer->l.ledger_entries(topo_or_default(topo), v);
+        if (padded) layer->l.padded_ledger_entries(topo_or_default(topo), v);
+        else layer->l.ledger_entries(topo_or_default(topo), v);
         std::string csv = "collective_id,kind,intra_bytes,inter_bytes,modeled_time_s\n";
         char tb[64];
         for (const auto& e : v) {
@@ -447,6 +449,15 @@ int xmoe_layer_ledger_csv(xmoe_layer* layer, const xmoe_topology* topo, char* bu
             buf[m] = '\0';
         }
     });
+}
+
+int xmoe_layer_ledger_csv(xmoe_layer* layer, const xmoe_topology* topo, char* buf, int64_t cap, int64_t* len) {
+    return ledger_csv(layer, topo, buf, cap, len, false);
+}
+
+int xmoe_layer_padded_ledger_csv(xmoe_layer* layer, const xmoe_topology* topo, char* buf, int64_t cap,
+                                 int64_t* len) {
+    return ledger_csv(layer, topo, buf, cap, len, true);
 }
 
 int xmoe_layer_ledger(xmoe_layer* layer, uint64_t* out, int n) {

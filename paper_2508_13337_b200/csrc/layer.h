@@ -188,6 +188,7 @@ struct Layer {
     int32_t* ssmb_B = nullptr;          // [G] kept copies per shard (device)
     int ssmb_cap = 0;
     void ledger_entries(const xmoe_topology& topo, std::vector<xmoe_ledger_entry>& out);
+    void padded_ledger_entries(const xmoe_topology& topo, std::vector<xmoe_ledger_entry>& out);
     ~Layer();
 };
 

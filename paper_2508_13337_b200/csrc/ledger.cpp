@@ -249,4 +249,17 @@ void Layer::ledger_entries(const xmoe_topology& topo, std::vector<xmoe_ledger_en
     for (size_t i = 0; i < out.size(); ++i) out[i].id = static_cast<int64_t>(i);
 }
 
+// padded_pipeline.cpp:106-143: an even all-to-all of e_local * C slots per
+// pair each way (self included), independent of the routing.
+void Layer::padded_ledger_entries(const xmoe_topology& topo, std::vector<xmoe_ledger_entry>& out) {
+    out.clear();
+    const uint64_t db = topo.dtype_bytes > 0 ? static_cast<uint64_t>(topo.dtype_bytes) : es;
+    const uint64_t slot_bytes = static_cast<uint64_t>(El) * static_cast<uint64_t>(d.max_token_count) * H * db;
+    for (const char* n : {"padded_dispatch_rows", "padded_combine_rows"}) {
+        Kind kd{n, std::vector<uint64_t>(static_cast<size_t>(W) * W, slot_bytes)};
+        out.push_back(finish(kd, W, topo, {}, 0));
+    }
+    for (size_t i = 0; i < out.size(); ++i) out[i].id = static_cast<int64_t>(i);
+}
+
 }  // namespace xmoe

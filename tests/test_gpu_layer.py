@@ -370,6 +370,9 @@ def test_ledger_csv_matches_reference(ref, mode, W, gpn):
     assert got == want, (got, want)
     ents = L.ledger_entries(topo)
     assert [e["kind"] for e in ents] == [line.split(",")[1] for line in want.strip().split("\n")[1:]]
+    # the padded (GShard) comparator: what padded_moe_forward would charge
+    rl.padded_moe_forward(toks, k, cap, node_of)
+    assert L.ledger_csv(topo, padded=True) == ref.last_ledger_csv()
 
 
 @pytest.mark.parametrize("G", [2, 4])
