@@ -548,8 +548,8 @@ template <typename OutT, bool kVarK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     grouped_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                             const int32_t* __restrict__ group_sizes, int G, int M, int N, int K,
-                            OutT* __restrict__ D, int relu, const __nv_bfloat16* __restrict__ mask,
-                            int coalesced) {
+                            OutT* __restrict__ D, int relu, const uint32_t* __restrict__ mbits_in,
+                            uint32_t* __restrict__ mbits_out, int coalesced) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -696,7 +696,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
-            const __nv_bfloat16* mrow = mask ? mask + static_cast<size_t>(ti.row0 + r) * N + ti.n0 : nullptr;
+            // ReLU masks as bits: one word per (row, 32 columns), ceil(N/32) words per row
+            const int mwords = (N + 31) >> 5;
+            const uint32_t* mrow = mbits_in ? mbits_in + static_cast<size_t>(ti.row0 + r) * mwords + (ti.n0 >> 5)
+                                            : nullptr;
+            uint32_t* orow = mbits_out ? mbits_out + static_cast<size_t>(ti.row0 + r) * mwords + (ti.n0 >> 5)
+                                       : nullptr;
             uint32_t* etile = reinterpret_cast<uint32_t*>(smem + kStages * kStageBytes + 1024 + kGroupTabBytes) +
                               (warp - 2) * kEpiWarpWords;
             const int wrow = BMC * static_cast<int>(rank) + quarter * 32;  // first row of this warp in the tile
@@ -714,23 +719,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                     const int cn = min(32, nw - c0);
                     if (mrow && row_ok) {
-                        if (cn == 32) {
-                            const int4* m4 = reinterpret_cast<const int4*>(mrow + c0);
+                        const uint32_t mw = mrow[c0 >> 5];
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                const int4 mv = m4[q];
-                                const uint32_t u[4] = {static_cast<uint32_t>(mv.x), static_cast<uint32_t>(mv.y),
-                                                       static_cast<uint32_t>(mv.z), static_cast<uint32_t>(mv.w)};
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    if (!(bf16_lo(u[e]) > 0.f)) f[8 * q + 2 * e] = 0.f;
-                                    if (!(bf16_hi(u[e]) > 0.f)) f[8 * q + 2 * e + 1] = 0.f;
-                                }
-                            }
-                        } else {
-                            for (int i = 0; i < cn; ++i)
-                                if (!(__bfloat162float(mrow[c0 + i]) > 0.f)) f[i] = 0.f;
-                        }
+                        for (int i = 0; i < 32; ++i)
+                            if (!((mw >> i) & 1u)) f[i] = 0.f;
                     }
                     store_chunk_coalesced<OutT>(etile, f, D + (kVarK ? static_cast<size_t>(ti.g) * M * N : 0),
                                                 static_cast<size_t>(N), static_cast<size_t>(ti.row0 + wrow),
@@ -746,23 +738,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 const int cn = min(32, nw - c0);
                 if (mrow) {
-                    if (cn == 32) {
-                        const int4* m4 = reinterpret_cast<const int4*>(mrow + c0);
+                    const uint32_t mw = mrow[c0 >> 5];
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const int4 mv = m4[q];
-                            const uint32_t u[4] = {static_cast<uint32_t>(mv.x), static_cast<uint32_t>(mv.y),
-                                                   static_cast<uint32_t>(mv.z), static_cast<uint32_t>(mv.w)};
+                    for (int i = 0; i < 32; ++i)
+                        if (!((mw >> i) & 1u)) f[i] = 0.f;
+                }
+                if (orow) {  // ReLU mask of the bf16 output, for the dgrad (bit i: y_i != 0)
+                    uint32_t mw = 0;
 #pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                if (!(bf16_lo(u[e]) > 0.f)) f[8 * q + 2 * e] = 0.f;
-                                if (!(bf16_hi(u[e]) > 0.f)) f[8 * q + 2 * e + 1] = 0.f;
-                            }
-                        }
-                    } else {
-                        for (int i = 0; i < cn; ++i)
-                            if (!(__bfloat162float(mrow[c0 + i]) > 0.f)) f[i] = 0.f;
-                    }
+                    for (int i = 0; i < 32; ++i)
+                        mw |= (i < cn && __bfloat162float(__float2bfloat16_rn(f[i])) > 0.f ? 1u : 0u) << i;
+                    orow[c0 >> 5] = mw;
                 }
                 if constexpr (sizeof(OutT) == 2) {
                     if (cn == 32 && (N & 7) == 0) {
@@ -1148,7 +1134,7 @@ static void launch_tc(const void* A, long long rows, int K, const int32_t* rows_
 template <typename OutT, bool kVarK>
 static void launch_tc2(const void* A, long long a_rows, long long a_cols, const int32_t* group_sizes, int G,
                        const void* B, long long b_rows, int M, int N, int K, OutT* D, int relu,
-                       const __nv_bfloat16* mask, long long tile_bound, cudaStream_t st) {
+                       const uint32_t* mbits_in, uint32_t* mbits_out, long long tile_bound, cudaStream_t st) {
     require(G >= 1 && G <= tc2::kMaxGroups, XMOE_ERR_VALIDATION, "grouped gemm: 1 <= groups <= 1024");
     require(a_cols % 8 == 0 && a_cols > 0, XMOE_ERR_VALIDATION, "bf16 path requires K % 8 == 0");
     require(N % 32 == 0 && N > 0, XMOE_ERR_VALIDATION, "bf16 2-CTA path requires N % 32 == 0");
@@ -1170,17 +1156,19 @@ static void launch_tc2(const void* A, long long a_rows, long long a_cols, const 
     if (g_gemm_sm_limit > 0 && g_gemm_sm_limit / 2 < cap_pairs) cap_pairs = g_gemm_sm_limit / 2;
     const long long pairs = tile_bound < cap_pairs ? tile_bound : cap_pairs;
     tc2::grouped_gemm_tc2_kernel<OutT, kVarK><<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
-        ta, tb, group_sizes, G, M, N, K, D, relu, mask, sizeof(OutT) == 4 ? epi_coalesced() : 0);
+        ta, tb, group_sizes, G, M, N, K, D, relu, mbits_in, mbits_out,
+        sizeof(OutT) == 4 && !mbits_out ? epi_coalesced() : 0);
     XMOE_LAUNCH_CHECK();
 }
 
 // Grouped-M: D[rows, N] over row segments (forward and dgrad).
 template <typename OutT>
 static void launch_tc2_rows(const void* A, long long rows, int K, const int32_t* rows_per_group, int G,
-                            const void* B, int N, OutT* D, int relu, const __nv_bfloat16* mask, cudaStream_t st) {
+                            const void* B, int N, OutT* D, int relu, const uint32_t* mbits_in, uint32_t* mbits_out,
+                            cudaStream_t st) {
     const long long bound = ((rows + tc2::BM - 1) / tc2::BM + G) * static_cast<long long>((N + tc2::BN - 1) / tc2::BN);
-    launch_tc2<OutT, false>(A, rows, K, rows_per_group, G, B, static_cast<long long>(G) * N, 0, N, K, D, relu, mask,
-                            bound, st);
+    launch_tc2<OutT, false>(A, rows, K, rows_per_group, G, B, static_cast<long long>(G) * N, 0, N, K, D, relu,
+                            mbits_in, mbits_out, bound, st);
 }
 
 // The expert FFN GEMMs run on the 2-CTA kernel; XMOE_GEMM=1cta selects the
@@ -1194,18 +1182,19 @@ static bool use_2cta(int N) {
 }
 
 void launch_grouped_gemm_bf16(const void* A, long long rows, int K, const int32_t* rows_per_group,
-                              int G, const void* B, int N, void* D, int relu, cudaStream_t st) {
+                              int G, const void* B, int N, void* D, int relu, cudaStream_t st, uint32_t* mbits_out) {
+    require(!mbits_out || (relu && use_2cta(N)), XMOE_ERR_VALIDATION, "ReLU mask output needs the 2-CTA ReLU GEMM");
     if (use_2cta(N))
         launch_tc2_rows<__nv_bfloat16>(A, rows, K, rows_per_group, G, B, N, static_cast<__nv_bfloat16*>(D), relu,
-                                       nullptr, st);
+                                       nullptr, mbits_out, st);
     else
         launch_tc<__nv_bfloat16>(A, rows, K, rows_per_group, G, B, N, static_cast<__nv_bfloat16*>(D), relu, st);
 }
 
 void launch_grouped_gemm_bf16_mask(const void* A, long long rows, int K, const int32_t* rows_per_group, int G,
-                                   const void* B, int N, void* D, const void* mask, cudaStream_t st) {
-    launch_tc2_rows<__nv_bfloat16>(A, rows, K, rows_per_group, G, B, N, static_cast<__nv_bfloat16*>(D), 0,
-                                   static_cast<const __nv_bfloat16*>(mask), st);
+                                   const void* B, int N, void* D, const uint32_t* mbits, cudaStream_t st) {
+    launch_tc2_rows<__nv_bfloat16>(A, rows, K, rows_per_group, G, B, N, static_cast<__nv_bfloat16*>(D), 0, mbits,
+                                   nullptr, st);
 }
 
 // Grouped-K (weight gradients): D_g[M, N] (fp32) = A[:, Kg] . B[:, Kg]^T where
@@ -1215,7 +1204,7 @@ void launch_grouped_wgrad_bf16(const void* A, int M, long long Ktot, const int32
                                const void* B, int N, float* D, cudaStream_t st) {
     require(Ktot % 64 == 0, XMOE_ERR_VALIDATION, "wgrad: K segments must be padded to 64");
     const long long bound = static_cast<long long>(G) * ((M + tc2::BM - 1) / tc2::BM) * ((N + tc2::BN - 1) / tc2::BN);
-    launch_tc2<float, true>(A, M, Ktot, k_per_group, G, B, N, M, N, 0, D, 0, nullptr, bound, st);
+    launch_tc2<float, true>(A, M, Ktot, k_per_group, G, B, N, M, N, 0, D, 0, nullptr, nullptr, bound, st);
 }
 
 // MN-major grouped weight gradient straight on the grouped activations.

@@ -69,10 +69,13 @@ void launch_grouped_gemm_f64(const double* A, long long rows_bound, int K,
                              double* D, int relu, cudaStream_t st);
 
 // gemm_tc.cu
+// mbits_out (ReLU GEMMs, training layers): bit i of word [row][c/32] = (y[row][c] != 0)
 void launch_grouped_gemm_bf16(const void* A, long long rows, int K, const int32_t* rows_per_group,
-                              int G, const void* B, int N, void* D, int relu, cudaStream_t st);
+                              int G, const void* B, int N, void* D, int relu, cudaStream_t st,
+                              uint32_t* mbits_out = nullptr);
+// dgrad with the ReLU mask of the forward: D = (A B) * mask
 void launch_grouped_gemm_bf16_mask(const void* A, long long rows, int K, const int32_t* rows_per_group, int G,
-                                   const void* B, int N, void* D, const void* mask, cudaStream_t st);
+                                   const void* B, int N, void* D, const uint32_t* mbits, cudaStream_t st);
 void launch_grouped_wgrad_bf16(const void* A, int M, long long Ktot, const int32_t* k_per_group, int G,
                                const void* B, int N, float* D, cudaStream_t st);
 void launch_grouped_wgrad_mn(const void* A, int M, const void* B, int N, long long rows,

@@ -313,6 +313,9 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
                                                   static_cast<size_t>(Fs)});
             w.tail_a = L.alloc(64 * static_cast<size_t>(L.El + 1) * wide * es);
             w.tail_b = L.alloc(64 * static_cast<size_t>(L.El + 1) * wide * es);
+            // ReLU masks of the forward's first GEMMs (bits), the dgrad's masks
+            w.mbits = static_cast<uint32_t*>(L.alloc(sizeof(uint32_t) * L.R_max * ((F + 31) / 32)));
+            if (Fs > 0) w.smbits = static_cast<uint32_t*>(L.alloc(sizeof(uint32_t) * S * ((Fs + 31) / 32)));
             w.tail_sa = L.alloc(64 * 2 * wide * es);  // side-stream (shared-expert wgrad) copies
             w.tail_sb = L.alloc(64 * 2 * wide * es);
             w.kpg = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
@@ -459,12 +462,12 @@ static const void* w2_of(const Layer& L, int r) {
 }
 
 static void run_gemm(int dtype, const void* A, long long rows_bound, int K, const int32_t* rpg, int G,
-                     const void* B, int N, void* D, int relu, cudaStream_t st) {
+                     const void* B, int N, void* D, int relu, cudaStream_t st, uint32_t* mbits_out = nullptr) {
     if (dtype == XMOE_F64)
         launch_grouped_gemm_f64(static_cast<const double*>(A), rows_bound, K, rpg, G,
                                 static_cast<const double*>(B), N, static_cast<double*>(D), relu, st);
     else
-        launch_grouped_gemm_bf16(A, rows_bound, K, rpg, G, B, N, D, relu, st);
+        launch_grouped_gemm_bf16(A, rows_bound, K, rpg, G, B, N, D, relu, st, mbits_out);
 }
 
 // ---------------------------------------------------------------- chunked forward
@@ -693,7 +696,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     auto issue_shared = [&](cudaStream_t ss) {
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
-            run_gemm(dt, x_of(i), S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, ss);
+            run_gemm(dt, x_of(i), S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, ss, w.smbits);
             run_gemm(dt, w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, w.sout, 0, ss);
         }
     };
@@ -787,7 +790,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     for (int i = 0; i < nl; ++i) {
         Worker& w = L.workers[i];
         launch_recv_counts(L.tpe_all, W, E, w.rank, w.rpe, st);
-        run_gemm(dt, w.recv, L.R_max, H, w.rpe, L.El, w1_of(L, w.rank), F, w.mid, 1, st);
+        run_gemm(dt, w.recv, L.R_max, H, w.rpe, L.El, w1_of(L, w.rank), F, w.mid, 1, st, w.mbits);
         run_gemm(dt, w.mid, L.R_max, F, w.rpe, L.El, w2_of(L, w.rank), H, w.eout, 0, st);
     }
     L.mark(kEvGemm, st);
@@ -911,7 +914,7 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
             Worker& w = L.workers[i];
             launch_transpose_pad(xo(x, i), H, w.tk, w.tk + 2, w.tk + 4, 1, L.Sp, w.xTt, ss);
             if (L.Fs > 0) {
-                launch_grouped_gemm_bf16_mask(xo(dy, i), S, H, w.s_rows, 1, L.sw2r, L.Fs, w.dHs, w.smid, ss);
+                launch_grouped_gemm_bf16_mask(xo(dy, i), S, H, w.s_rows, 1, L.sw2r, L.Fs, w.dHs, w.smbits, ss);
                 launch_grouped_gemm_bf16(w.dHs, S, L.Fs, w.s_rows, 1, L.sw1r, H, w.dxs, 0, ss);
                 launch_grouped_wgrad_mn(xo(x, i), H, w.dHs, L.Fs, S, w.tk, 1, w.tail_sa, w.tail_sb, L.dsw1, ss);
                 launch_grouped_wgrad_mn(w.smid, L.Fs, xo(dy, i), H, S, w.tk, 1, w.tail_sa, w.tail_sb, L.dsw2, ss);
@@ -944,7 +947,7 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
         launch_bwd_owner_prep(w.dyg, w.eout, w.gw, w.gsrc, w.rpe, El, H, L.R_max, L.slotdw_tab, w.dz, st);
         bmark(kBwPrep);
         launch_grouped_gemm_bf16_mask(w.dz, L.R_max, H, w.rpe, El, static_cast<const char*>(L.w2r) + eo, F, w.dH,
-                                      w.mid, st);
+                                      w.mbits, st);
         launch_grouped_gemm_bf16(w.dH, L.R_max, F, w.rpe, El, static_cast<const char*>(L.w1r) + eo, H, w.dxc, 0, st);
         bmark(kBwDgrad);
         // wgrad straight on the grouped activations (MN-major tcgen05 operands)

@@ -72,6 +72,8 @@ struct Worker {
     void* dH = nullptr;           // [R_max, F]
     void* tail_a = nullptr;       // wgrad tail blocks [64*(El+1), max(H,F,Fs)]
     void* tail_b = nullptr;
+    uint32_t* mbits = nullptr;    // [R_max, ceil(F/32)] ReLU mask bits of mid (training)
+    uint32_t* smbits = nullptr;   // [S, ceil(Fs/32)] of the shared experts' mid
     void* tail_sa = nullptr;      // the same for the side-stream (shared-expert) wgrad
     void* tail_sb = nullptr;
     int32_t* kpg = nullptr;       // [El] padded rows per expert
