@@ -132,6 +132,94 @@ __global__ void flag_wait_kernel(const unsigned* __restrict__ flags, int W, int 
     __syncthreads();
 }
 
+// Count all-gather over the symmetric regions (replaces ncclAllGather of
+// the routing counts): every rank stores its rows into every peer's count
+// area (double-buffered by forward parity: a peer at most one forward
+// behind is still reading the other half), raises its flag, waits for all
+// flags, and copies the gathered area into the layer's local arrays.
+// Passing it also proves every peer finished its previous forward.
+__global__ void counts_exchange_kernel(CountSegs segs, int32_t* const* __restrict__ area_tab, int area_ints,
+                                       int me, int W, unsigned* const* __restrict__ flag_tab,
+                                       const unsigned* __restrict__ my_flags, int slot,
+                                       const unsigned* __restrict__ epoch) {
+    const unsigned e = *epoch;
+    const int par = static_cast<int>(e & 1u);
+    for (int p = 0; p < W; ++p) {
+        int32_t* area = area_tab[p] + static_cast<size_t>(par) * area_ints;
+        for (int q = 0; q < segs.n; ++q) {
+            const CountSeg& sg = segs.s[q];
+            for (int i = threadIdx.x; i < sg.row; i += blockDim.x) area[sg.off + me * sg.row + i] = sg.src[i];
+        }
+    }
+    __threadfence_system();
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < W) {
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag_tab[t] + static_cast<size_t>(slot) * W + me),
+                     "r"(e)
+                     : "memory");
+        const unsigned* f = my_flags + static_cast<size_t>(slot) * W + t;
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+            unsigned v;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            if (static_cast<int>(v - e) >= 0) break;
+            __nanosleep(64);
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 20000000000ull) __trap();
+        }
+    }
+    __syncthreads();
+    const int32_t* mine = area_tab[me] + static_cast<size_t>(par) * area_ints;
+    for (int q = 0; q < segs.n; ++q) {
+        const CountSeg& sg = segs.s[q];
+        for (int i = threadIdx.x; i < W * sg.row; i += blockDim.x) sg.local[i] = mine[sg.off + i];
+    }
+}
+
+// Cross-GPU barrier on one flag slot (every rank's previous kernels on this
+// stream are complete and their peer stores visible when it passes).
+__global__ void flag_barrier_kernel(unsigned* const* __restrict__ flag_tab, const unsigned* __restrict__ my_flags,
+                                    int W, int me, int slot, const unsigned* __restrict__ epoch) {
+    const unsigned e = *epoch;
+    const int t = threadIdx.x;
+    __threadfence_system();
+    __syncthreads();
+    if (t < W) {
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag_tab[t] + static_cast<size_t>(slot) * W + me),
+                     "r"(e)
+                     : "memory");
+        const unsigned* f = my_flags + static_cast<size_t>(slot) * W + t;
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+            unsigned v;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            if (static_cast<int>(v - e) >= 0) break;
+            __nanosleep(64);
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 20000000000ull) __trap();
+        }
+    }
+    __syncthreads();
+}
+
+void launch_counts_exchange(const CountSegs& segs, int32_t* const* area_tab, int area_ints, int me, int W,
+                            unsigned* const* flag_tab, const unsigned* my_flags, int slot, const unsigned* epoch,
+                            cudaStream_t st) {
+    counts_exchange_kernel<<<1, 256, 0, st>>>(segs, area_tab, area_ints, me, W, flag_tab, my_flags, slot, epoch);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_flag_barrier(unsigned* const* flag_tab, const unsigned* my_flags, int W, int me, int slot,
+                         const unsigned* epoch, cudaStream_t st) {
+    flag_barrier_kernel<<<1, 32 * ((W + 31) / 32), 0, st>>>(flag_tab, my_flags, W, me, slot, epoch);
+    XMOE_LAUNCH_CHECK();
+}
+
 void launch_chunk_counts(const int32_t* token_ids, const int32_t* tpe, int E, int S, int C, int32_t* tpe_c,
                          int32_t* pfx_c, int32_t* seg, cudaStream_t st) {
     const int n = C * E;

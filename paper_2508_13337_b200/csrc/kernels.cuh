@@ -126,5 +126,25 @@ void launch_forward_begin(int32_t* s_rows, int S, unsigned* epoch, cudaStream_t 
 void launch_flag_signal(unsigned* const* flag_tab, int W, int me, int slot, const unsigned* epoch,
                         cudaStream_t st);
 void launch_flag_wait(const unsigned* flags, int W, int slot, const unsigned* epoch, cudaStream_t st);
+// flag slots per rank: [0, kMaxChunks) chunk dispatch, [kMaxChunks, 2 kMaxChunks)
+// chunk combine, then the count exchange and the unchunked forward's barriers
+constexpr int kSlotCounts = 2 * kMaxChunks;
+constexpr int kSlotBar = 2 * kMaxChunks + 1;  // + 0..3
+constexpr int kFlagSlots = 2 * kMaxChunks + 5;
+struct CountSeg {
+    const int32_t* src;  // my row
+    int row;             // ints per rank row
+    int off;             // offset of the [W, row] block in the count area
+    int32_t* local;      // [W, row] gathered copy
+};
+struct CountSegs {
+    CountSeg s[4];
+    int n;
+};
+void launch_counts_exchange(const CountSegs& segs, int32_t* const* area_tab, int area_ints, int me, int W,
+                            unsigned* const* flag_tab, const unsigned* my_flags, int slot, const unsigned* epoch,
+                            cudaStream_t st);
+void launch_flag_barrier(unsigned* const* flag_tab, const unsigned* my_flags, int W, int me, int slot,
+                         const unsigned* epoch, cudaStream_t st);
 
 }  // namespace xmoe

@@ -215,13 +215,16 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     const size_t off_gsrc = off_gw + (L.train ? up(sizeof(float) * L.R_max) : 0);
     const size_t off_sdw = off_gsrc + (L.train ? up(sizeof(unsigned long long) * L.R_max) : 0);
     const size_t off_flags = off_sdw + (L.train ? up(sizeof(float) * nk) : 0);
-    const size_t flag_bytes = sizeof(unsigned) * 2 * kMaxChunks * W;
-    const size_t sym_bytes = off_flags + up(flag_bytes);
+    const size_t flag_bytes = sizeof(unsigned) * kFlagSlots * W;
+    // count all-gather area (double-buffered): tpe [W,E] | tpe_c [W,C,E] | G [W,W] | gd [W,2,W,C]
+    L.area_ints = W * E + W * L.nchunks * E + W * W + 2 * W * W * L.nchunks;
+    const size_t off_counts = off_flags + up(flag_bytes);
+    const size_t sym_bytes = off_counts + up(sizeof(int32_t) * 2 * L.area_ints);
     L.off_eout = static_cast<long long>(off_eout);
     L.off_dxc = static_cast<long long>(off_dxc);
     L.workers.resize(L.nl);
     std::vector<char*> t_recv(W), t_eout(W), t_recv_u(W), t_desc(W), t_back(W);
-    std::vector<char*> t_dyg(W), t_dxc(W), t_gw(W), t_gsrc(W), t_sdw(W), t_flags(W);
+    std::vector<char*> t_dyg(W), t_dxc(W), t_gw(W), t_gsrc(W), t_sdw(W), t_flags(W), t_counts(W);
     for (int i = 0; i < L.nl; ++i) {
         Worker& w = L.workers[i];
         w.rank = ssmb ? 0 : ctx.rank_of(i);
@@ -244,6 +247,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         w.sym = static_cast<char*>(L.alloc(sym_bytes));
         w.flags = reinterpret_cast<unsigned*>(w.sym + off_flags);
         XMOE_CUDA(cudaMemset(w.flags, 0, flag_bytes));
+        t_counts[w.rank] = w.sym + off_counts;
         if (L.nchunks > 1) {
             const int CE = L.nchunks * E;
             w.tpe_c = L.distributed ? static_cast<int32_t*>(L.alloc(sizeof(int32_t) * CE)) : nullptr;
@@ -373,6 +377,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
             t_desc[r] = b + off_desc;
             t_back[r] = b + off_back;
             t_flags[r] = b + off_flags;
+            t_counts[r] = b + off_counts;
         }
     }
     auto table = [&](const std::vector<char*>& v) {
@@ -382,6 +387,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     };
     L.recv_tab = table(t_recv);
     L.flag_tab = reinterpret_cast<unsigned**>(table(t_flags));
+    L.cnt_tab = reinterpret_cast<int32_t**>(table(t_counts));
     L.epoch = static_cast<unsigned*>(L.alloc(sizeof(unsigned)));
     XMOE_CUDA(cudaMemset(L.epoch, 0, sizeof(unsigned)));
     L.eout_tab = table(t_eout);
@@ -470,6 +476,22 @@ static void run_gemm(int dtype, const void* A, long long rows_bound, int K, cons
         launch_grouped_gemm_bf16(A, rows_bound, K, rpg, G, B, N, D, relu, st, mbits_out);
 }
 
+// Count all-gather of the routing counts over the peer tables (one process
+// per GPU): this rank's tpe row [+ chunk counts] [+ RBD group counts].
+static void exchange_counts(Layer& L, cudaStream_t st) {
+    Worker& w = L.workers[0];
+    const int W = L.W, E = L.E, C = L.nchunks;
+    const bool rbd = L.d.dispatch_mode == XMOE_DISPATCH_RBD;
+    CountSegs sg{};
+    sg.s[sg.n++] = CountSeg{w.tpe, E, 0, L.tpe_all};
+    if (C > 1) sg.s[sg.n++] = CountSeg{w.tpe_c, C * E, W * E, L.tpe_c_all};
+    if (rbd) {
+        sg.s[sg.n++] = CountSeg{L.G_all + static_cast<size_t>(w.rank) * W, W, W * E + W * C * E, L.G_all};
+        sg.s[sg.n++] = CountSeg{w.rbd.gd_own, 2 * W * C, W * E + W * C * E + W * W, L.gd_all};
+    }
+    launch_counts_exchange(sg, L.cnt_tab, L.area_ints, w.rank, W, L.flag_tab, w.flags, kSlotCounts, L.epoch, st);
+}
+
 // ---------------------------------------------------------------- chunked forward
 // BF16 plain dispatch, cut into L.nchunks token chunks (chunk.cu).  Streams:
 //   st   gate | shared-expert GEMMs | per chunk: [wait A_c] GEMM1, GEMM2 [signal B_c]
@@ -535,18 +557,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
         }
     }
     L.mark(kEvPft, cm);
-    if (dist) {
-        Worker& w = L.workers[0];
-        auto comm = static_cast<ncclComm_t>(ctx.nccl);
-        XMOE_NCCL(ncclGroupStart());
-        XMOE_NCCL(ncclAllGather(w.tpe, L.tpe_all, E, ncclInt32, comm, cm));
-        XMOE_NCCL(ncclAllGather(w.tpe_c, L.tpe_c_all, static_cast<size_t>(C) * E, ncclInt32, comm, cm));
-        if (rbd) {
-            XMOE_NCCL(ncclAllGather(L.G_all + static_cast<size_t>(w.rank) * W, L.G_all, W, ncclInt32, comm, cm));
-            XMOE_NCCL(ncclAllGather(w.rbd.gd_own, L.gd_all, static_cast<size_t>(2) * W * C, ncclInt32, comm, cm));
-        }
-        XMOE_NCCL(ncclGroupEnd());
-    }
+    if (dist) exchange_counts(L, cm);
     L.mark(kEvCounts, cm);
     for (int i = 0; i < nl; ++i) {
         Worker& w = L.workers[i];
@@ -672,8 +683,13 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     auto o_of = [&](int i) { return ob + static_cast<size_t>(i) * S * row_bytes; };
 
     L.mark(kEvStart, st);
-    for (int i = 0; i < nl; ++i)
-        launch_fill_i32(L.workers[i].s_rows, 1, static_cast<int32_t>(S), st);  // one dense group of S rows
+    for (int i = 0; i < nl; ++i)  // one dense group of S rows; the forward's epoch
+        launch_forward_begin(L.workers[i].s_rows, static_cast<int>(S), i == 0 ? L.epoch : nullptr, st);
+    const int me = L.workers[0].rank;
+    auto fbar = [&](int j) {  // cross-rank barrier of the peer transport
+        if (L.p2p) launch_flag_barrier(L.flag_tab, L.workers[0].flags, W, me, kSlotBar + j, L.epoch, st);
+        else L.barrier(st);
+    };
     // 1. gate (gating.cpp:14-57)
     for (int i = 0; i < nl; ++i) {
         Worker& w = L.workers[i];
@@ -731,15 +747,13 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     // 3. per-expert (and per-destination group) counts to every rank
     //    (pf_pipeline.cpp:30-36).  Completing it also proves every peer is
     //    past its previous forward, so their buffers may be overwritten.
-    if (dist) {
+    if (dist && L.p2p) {
+        exchange_counts(L, st);
+    } else if (dist) {  // NCCL transport baseline
         Worker& w = L.workers[0];
         auto comm = static_cast<ncclComm_t>(ctx.nccl);
         XMOE_NCCL(ncclGroupStart());
         XMOE_NCCL(ncclAllGather(w.tpe, L.tpe_all, E, ncclInt32, comm, st));
-        if (rbd) {
-            XMOE_NCCL(ncclAllGather(L.G_all + static_cast<size_t>(w.rank) * W, L.G_all, W, ncclInt32, comm, st));
-            XMOE_NCCL(ncclAllGather(w.rbd.gd_own, L.gd_all, 2 * W, ncclInt32, comm, st));
-        }
         XMOE_NCCL(ncclGroupEnd());
     }
     // 4. dispatch: destination rows in the owner's (local expert, source,
@@ -757,13 +771,13 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
                             w.cw, L.recv_tab, L.desc_tab, st, static_cast<int>(S), w.expert_ids, L.El);
         }
         L.mark(kEvMoved, st);
-        if (dist) L.barrier(st);
+        if (dist) fbar(0);
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             launch_rbd_expand(static_cast<int>(row_bytes), w.desc_recv, w.rbd, 0, L.R_max, w.recv, L.recv_tab,
                               w.gstart, st);
         }
-        if (dist && L.gpn > 1) L.barrier(st);  // stage-2 rows landed in peers' inputs
+        if (dist && L.gpn > 1) fbar(1);  // stage-2 rows landed in peers' inputs
     } else if (tables) {
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
@@ -775,7 +789,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
                                     w.dest_row, L.recv_tab, st);
         }
         L.mark(kEvMoved, st);
-        if (dist) L.barrier(st);
+        if (dist) fbar(0);
     } else {
         Worker& w = L.workers[0];
         launch_gather_rows(xb, S, static_cast<int>(row_bytes), w.token_ids, nk, w.B_dev, w.send, nullptr, st);
@@ -808,11 +822,11 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     if (rbd) {
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
-            if (i == 0 && dist && L.gpn > 1) L.barrier(st);  // replicas' outputs are read from their owners
+            if (i == 0 && dist && L.gpn > 1) fbar(2);  // replicas' outputs are read from their owners
             launch_rbd_merge(dt, L.eout_tab, H, w.desc_recv, w.gstart, w.rbd, 0, static_cast<long long>(W) * S,
                              w.back_u, st);
         }
-        if (dist) L.barrier(st);
+        if (dist) fbar(3);
         L.mark(kEvReturn, st);
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
@@ -820,7 +834,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
                                L.Fs > 0 ? w.sout : nullptr, o_of(i), st);
         }
     } else if (tables) {
-        if (dist) L.barrier(st);
+        if (dist) fbar(3);
         L.mark(kEvReturn, st);
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];

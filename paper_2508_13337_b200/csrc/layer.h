@@ -171,6 +171,8 @@ struct Layer {
     int32_t* tpe_c_all = nullptr;  // [W, C, E]
     int32_t* gd_all = nullptr;     // RBD [W_src, 2, W, C] groups / copies per (dest, chunk)
     unsigned** flag_tab = nullptr; // rank -> its flags (peer addresses)
+    int32_t** cnt_tab = nullptr;   // rank -> its count all-gather area (peer addresses)
+    int area_ints = 0;             // ints per half of the count area
     unsigned* epoch = nullptr;     // forwards issued (device)
     cudaStream_t comm = nullptr;
     std::vector<cudaEvent_t> evA, evB;
