@@ -90,8 +90,9 @@ struct ActivationCounters {
     std::vector<std::uint64_t> dispatch_out_elements;
 };
 
-// ---- placement.hpp:51-54 / collectives.hpp:71-76 (node_of = one GPU per
-// rank here; the byte ledger of the device run replaces the alpha-beta model)
+// ---- placement.hpp:51-54 / collectives.hpp:71-76 (node_of: contiguous
+// blocks of equal size; rbd_moe_forward runs the two-tier bypass when a block
+// holds several GPUs)
 struct WorkerGroup {
     std::vector<std::int64_t> node_of;
     std::size_t size() const { return node_of.size(); }

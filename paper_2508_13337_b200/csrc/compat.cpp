@@ -109,7 +109,7 @@ void make_layer(xmoe_ctx* ctx, const MoeLayerWeights& w, std::int64_t E, std::in
 }
 
 std::vector<Matrix> run_layer(const MoeInstance& inst, Comm& comm, int mode, std::uint64_t seed,
-                              const char* who) {
+                              const char* who, int flags = 0) {
     const size_t W = comm.group.size();
     if (inst.tokens.size() != W) throw DimensionError(std::string(who) + ": need one token matrix per worker");
     const std::int64_t E = inst.num_experts;
@@ -122,7 +122,8 @@ std::vector<Matrix> run_layer(const MoeInstance& inst, Comm& comm, int mode, std
     for (const auto& t : inst.tokens) x.insert(x.end(), t.data.begin(), t.data.end());
     xmoe_ctx* ctx = ctx_for(static_cast<int>(W));
     LayerHandle lh;
-    make_layer(ctx, inst.weights, E, inst.top_k, inst.max_token_count, static_cast<std::int64_t>(S), mode, seed, 0, lh);
+    make_layer(ctx, inst.weights, E, inst.top_k, inst.max_token_count, static_cast<std::int64_t>(S), mode, seed, flags,
+               lh);
     auto dx = upload(x);
     DBuf dout(x.size() * sizeof(double));
     ck(xmoe_moe_forward(ctx, lh.l, dx->p, static_cast<std::int64_t>(S), dout.p, nullptr));
@@ -257,12 +258,24 @@ std::vector<Matrix> pf_moe_forward(const MoeInstance& inst, Comm& comm, Activati
     return run_layer(inst, comm, XMOE_DISPATCH_NAIVE, 0, "pf_moe_forward");
 }
 
+// node_of must be contiguous blocks of equal size (node n = ranks
+// [n*g, (n+1)*g)); g > 1 is the two-tier bypass (rbd.cpp:83-358)
 std::vector<Matrix> rbd_moe_forward(const MoeInstance& inst, Comm& comm, std::uint64_t seed) {
-    for (size_t i = 0; i < comm.group.size(); ++i)
-        for (size_t j = 0; j < i; ++j)
-            if (comm.group.node_of[i] == comm.group.node_of[j])
-                throw ValidationError("xmoe: the redundancy bypass runs with one GPU per node (distinct node_of)");
-    return run_layer(inst, comm, XMOE_DISPATCH_RBD, seed, "rbd_moe_forward");
+    const auto& no = comm.group.node_of;
+    const size_t W = no.size();
+    size_t g = 1;
+    while (g < W && no[g] == no[0]) ++g;
+    bool blocks = W % g == 0;
+    for (size_t i = 0; blocks && i < W; ++i) {
+        if (no[i] != no[(i / g) * g]) blocks = false;
+        if (i % g == 0)
+            for (size_t j = 0; j < i; j += g)
+                if (no[j] == no[i]) blocks = false;
+    }
+    if (!blocks)
+        throw ValidationError("xmoe: node_of must be contiguous blocks of equal size (rank / gpus_per_node)");
+    return run_layer(inst, comm, XMOE_DISPATCH_RBD, seed, "rbd_moe_forward",
+                     XMOE_LAYER_GPUS_PER_NODE(static_cast<int>(g)));
 }
 
 Matrix ssmb_forward(const Matrix& tokens, std::int64_t G, const MoeLayerWeights& weights, std::int64_t E,

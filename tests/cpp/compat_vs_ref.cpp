@@ -162,6 +162,17 @@ int main() {
             const auto c = moesim::rbd_moe_forward(inst, rc, seed);
             const auto d = xmoe::rbd_moe_forward(xi, xc, seed);
             for (std::size_t w = 0; w < W; ++w) CHECK(rel(c[w].data, d[w].data) < 1e-14);
+            if (W % 2 == 0) {  // two-tier bypass: nodes of 2 GPUs
+                moesim::Comm r2;
+                xmoe::Comm x2;
+                for (std::size_t w = 0; w < W; ++w) {
+                    r2.group.node_of.push_back(static_cast<std::int64_t>(w / 2));
+                    x2.group.node_of.push_back(static_cast<std::int64_t>(w / 2));
+                }
+                const auto c2 = moesim::rbd_moe_forward(inst, r2, seed);
+                const auto d2 = xmoe::rbd_moe_forward(xi, x2, seed);
+                for (std::size_t w = 0; w < W; ++w) CHECK(rel(c2[w].data, d2[w].data) < 1e-14);
+            }
             if (W >= 2 && static_cast<std::size_t>(W) <= S) {
                 moesim::Comm sc;
                 xmoe::Comm sx;
