@@ -355,17 +355,22 @@ def main():
                    "note": "forward + backward (dx and fp32 grads of gate, experts, shared experts); "
                            "gradients restated beyond the forward-only reference, checked against fp64 autograd"}
 
-    # ---- per-stage breakdown + roofline of the dominant kernel (grouped GEMM)
-    tlayer.set_timing(True)
-    stage_runs = []
-    for _ in range(5):
-        tlayer.forward(x, out)
-        torch.cuda.synchronize()
-        stage_runs.append(tlayer.stage_ms())
-    tlayer.set_timing(False)
-    stages = {kk: statistics.median(r[kk] for r in stage_runs) for kk in stage_runs[0]}
-    led = tlayer.ledger()
+    # ---- per-stage breakdown + roofline of the dominant kernel (grouped GEMM),
+    # on a forward-only unchunked layer (kernel-level stages; the training
+    # layer's GEMM1 epilogue also stores ReLU masks)
     del tlayer
+    slayer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
+                        max_tokens=S, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,
+                        dispatch_mode=mode, seed=99, chunks=1)
+    slayer.set_timing(True)
+    stage_runs = []
+    for _ in range(6):
+        slayer.forward(x, out)
+        torch.cuda.synchronize()
+        stage_runs.append(slayer.stage_ms())
+    stages = {kk: statistics.median(r[kk] for r in stage_runs[1:]) for kk in stage_runs[0]}
+    led = slayer.ledger()
+    del slayer
 
     # ---- plain vs redundancy-bypassing dispatch (N > 1): all-to-all bytes and
     # isolated kernel times of both, from unchunked layers in timing mode

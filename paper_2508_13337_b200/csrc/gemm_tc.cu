@@ -743,27 +743,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     for (int i = 0; i < 32; ++i)
                         if (!((mw >> i) & 1u)) f[i] = 0.f;
                 }
-                if (orow) {  // ReLU mask of the bf16 output, for the dgrad (bit i: y_i != 0)
-                    uint32_t mw = 0;
-#pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        mw |= (i < cn && __bfloat162float(__float2bfloat16_rn(f[i])) > 0.f ? 1u : 0u) << i;
-                    orow[c0 >> 5] = mw;
-                }
                 if constexpr (sizeof(OutT) == 2) {
                     if (cn == 32 && (N & 7) == 0) {
                         int4* dst = reinterpret_cast<int4*>(drow + c0);
+                        uint32_t mw = 0;  // ReLU mask of the stored bf16 values (bit i: y_i != 0)
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            int4 o;
-                            o.x = static_cast<int>(pack_bf16(f[8 * q + 0], f[8 * q + 1]));
-                            o.y = static_cast<int>(pack_bf16(f[8 * q + 2], f[8 * q + 3]));
-                            o.z = static_cast<int>(pack_bf16(f[8 * q + 4], f[8 * q + 5]));
-                            o.w = static_cast<int>(pack_bf16(f[8 * q + 6], f[8 * q + 7]));
-                            dst[q] = o;
+                            uint32_t u[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                u[e] = pack_bf16(f[8 * q + 2 * e], f[8 * q + 2 * e + 1]);
+                                if (orow) {
+                                    mw |= ((u[e] & 0x7FFFu) ? 1u : 0u) << (8 * q + 2 * e);
+                                    mw |= ((u[e] & 0x7FFF0000u) ? 1u : 0u) << (8 * q + 2 * e + 1);
+                                }
+                            }
+                            dst[q] = make_int4(static_cast<int>(u[0]), static_cast<int>(u[1]), static_cast<int>(u[2]),
+                                               static_cast<int>(u[3]));
                         }
+                        if (orow) orow[c0 >> 5] = mw;
                     } else {
-                        for (int i = 0; i < cn; ++i) drow[c0 + i] = __float2bfloat16_rn(f[i]);
+                        uint32_t mw = 0;
+                        for (int i = 0; i < cn; ++i) {
+                            const __nv_bfloat16 b = __float2bfloat16_rn(f[i]);
+                            drow[c0 + i] = b;
+                            mw |= (__bfloat162float(b) != 0.f ? 1u : 0u) << i;
+                        }
+                        if (orow) orow[c0 >> 5] = mw;
                     }
                 } else {
                     if (cn == 32 && (N & 3) == 0) {
