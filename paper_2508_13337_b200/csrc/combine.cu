@@ -273,7 +273,7 @@ void launch_combine_slots(const unsigned long long* slot_src, const float* slot_
     const long long warps = static_cast<long long>(S) * ((H + kSegCols - 1) / kSegCols);
     long long blocks = ceil_div(warps, kCombWarps);
     if (g_copy_blocks > 0 && blocks > g_copy_blocks) blocks = g_copy_blocks;
-    combine_slots_bf16_kernel<<<static_cast<int>(blocks), 32 * kCombWarps, 0, st>>>(
+    combine_slots_bf16_kernel<<<static_cast<int>(blocks), 32 * kCombWarps, g_copy_smem, st>>>(
         slot_src, slot_w, k, H, S, static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out),
         src_delta, static_cast<const __nv_bfloat16*>(addend2));
     XMOE_LAUNCH_CHECK();

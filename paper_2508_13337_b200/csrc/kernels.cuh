@@ -102,6 +102,9 @@ extern thread_local int g_gemm_sm_limit;
 // blocks so the NVLink traffic they drive does not stall the GEMM CTAs on
 // every SM.
 extern thread_local int g_copy_blocks;
+// dynamic shared memory the row-movement kernels reserve (unused): large
+// enough, it keeps them off SMs that hold a GEMM CTA (SM partition)
+extern thread_local int g_copy_smem;
 
 // misc.cu
 void launch_recv_counts(const int32_t* tpe_all, int W, int E, int dst, int32_t* rpe,

@@ -526,6 +526,13 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
         const char* c = e ? std::strchr(e, ',') : nullptr;
         return c ? std::max(1, std::atoi(c + 1)) : 64;
     }();
+    // optional SM partition (XMOE_PART_SMS=n): the chunk GEMMs use n SMs and
+    // the row movement reserves enough shared memory to stay off them
+    static const int part_sms = [] {
+        const char* e = std::getenv("XMOE_PART_SMS");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int copy_smem = part_sms > 0 ? 32 * 1024 : 0;
     auto slot_A = [](int c) { return c; };
     auto slot_B = [](int c) { return kMaxChunks + c; };
 
@@ -566,6 +573,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
                                      w.pfx_c, w.cbase, w.dest_rank, w.dest_row, cm);
         if (rbd) launch_rbd_offsets(L.gd_all, W, w.rank, w.rbd, cm);
     }
+    g_copy_smem = copy_smem;
     for (int c = 0; c < C; ++c) {
         // chunk 0 gates the first expert GEMM: full grid; later chunks run
         // beside the GEMMs on a bounded grid
@@ -596,11 +604,13 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     //    (pf_pipeline.cpp:83-105)
     if (L.Fs > 0) {
         if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side0, st));
+        g_gemm_sm_limit = part_sms;
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             launch_grouped_gemm_bf16(x_of(i), S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, st);
             launch_grouped_gemm_bf16(w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, w.sout, 0, st);
         }
+        g_gemm_sm_limit = 0;
         if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side1, st));
     }
     for (int c = 0; c < C; ++c) {
@@ -609,6 +619,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
         if (L.timing) XMOE_CUDA(cudaEventRecord(L.tl[4 * c + 1], st));
         const size_t r0 = static_cast<size_t>(c) * L.Rc;
         g_copy_blocks = 0;
+        g_gemm_sm_limit = part_sms;
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             if (rbd)  // replicas copy the row from their pilot's slot
@@ -622,6 +633,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
                 launch_rbd_merge(XMOE_BF16, L.eout_tab, H, w.desc_recv, w.gstart, w.rbd, c,
                                  static_cast<long long>(W) * S, w.back_u, st);
         }
+        g_gemm_sm_limit = 0;
         if (L.timing) XMOE_CUDA(cudaEventRecord(L.tl[4 * c + 2], st));
         if (dist) launch_flag_signal(L.flag_tab, W, me, slot_B(c), L.epoch, st);
         XMOE_CUDA(cudaEventRecord(L.evB[c], st));
@@ -651,6 +663,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
         if (L.timing) XMOE_CUDA(cudaEventRecord(L.tl[4 * c + 3], cm));
     }
     g_copy_blocks = 0;
+    g_copy_smem = 0;
     XMOE_CUDA(cudaEventRecord(L.ev_done, cm));
     XMOE_CUDA(cudaStreamWaitEvent(st, L.ev_done, 0));
     L.mark(kEvCombine, st);

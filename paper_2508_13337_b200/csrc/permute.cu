@@ -15,6 +15,7 @@
 namespace xmoe {
 
 thread_local int g_copy_blocks = 0;
+thread_local int g_copy_smem = 0;
 
 constexpr int kRowWarps = 8;
 constexpr int kUnroll = 8;
@@ -352,7 +353,7 @@ void launch_scatter_tokens(const void* x, int row_bytes, int S, int k, const int
     long long blocks = (static_cast<long long>(S) + kTokWarps - 1) / kTokWarps;
     const long long cap = g_copy_blocks > 0 ? g_copy_blocks : 8LL * kNumSMs;
     if (blocks > cap) blocks = cap;
-    scatter_tokens_kernel<<<static_cast<int>(blocks), 32 * kTokWarps, 0, st>>>(
+    scatter_tokens_kernel<<<static_cast<int>(blocks), 32 * kTokWarps, g_copy_smem, st>>>(
         static_cast<const char*>(x), row_bytes, S, k, slot_pos, dest_rank, dest_row, cw, dest_bufs, src_bufs,
         slot_src, slot_w, tr);
     XMOE_LAUNCH_CHECK();
