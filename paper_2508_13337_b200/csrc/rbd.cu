@@ -807,6 +807,7 @@ void launch_rbd_sort(int W, long long max_groups, RbdWork& wk, cudaStream_t st) 
     // (token, dest) order, so each dest segment stays in token order)
     launch_stable_csr_dev(wk.g.dest, wk.G_dev, static_cast<int>(max_groups), W, wk.dptr, wk.perm,
                           wk.csr_ws, st);
+    if (max_groups == 0) return;  // empty sequence: dptr zeroed above
     rbd_group_pos_kernel<<<ceil_div(max_groups, 256), 256, 0, st>>>(wk.perm, wk.G_dev, wk.g, wk.nsorted);
     XMOE_LAUNCH_CHECK();
     scan_i32(wk.nsorted, static_cast<int>(max_groups), wk.G_dev, wk.coff, nullptr, st);

@@ -391,3 +391,50 @@ def test_ledger_csv_ssmb_matches_reference(ref, G):
     got = L.ledger_csv(capi.Topology.reference_defaults(gpus_per_node=1, dtype_bytes=2))
     ref.Layer(w.gate, w.w1, w.w2).ssmb_forward(x, G, k, S * k)
     assert got == ref.last_ledger_csv()
+
+
+@pytest.mark.parametrize("mode,dtype,chunks", [(0, "f64", 1), (1, "f64", 1), (0, "bf16", 1), (1, "bf16", 1),
+                                               (0, "bf16", 3), (1, "bf16", 2)])
+def test_layer_edge_lengths_and_errors(mode, dtype, chunks):
+    """Empty and ragged sequences through one layer object (S = 0, 1, odd, the
+    maximum), each equal to a fresh layer's result, and the layer's
+    validation errors (error.hpp status codes, reference messages)."""
+    from paper_2508_13337_b200 import capi
+    from paper_2508_13337_b200.capi import XmoeError
+    W, E, k, H, F, S_max = 2, 16, 3, 32, 32, 37
+    ctx = capi.Context(0, W, -1)
+    rng = np.random.default_rng(3)
+    dt = capi.F64 if dtype == "f64" else capi.BF16
+    tdt = torch.float64 if dtype == "f64" else torch.bfloat16
+    w = O.LayerWeights(grid_gate(rng, H, E), bf16_round(rng.uniform(-0.1, 0.1, (E, H, F))),
+                       bf16_round(rng.uniform(-0.1, 0.1, (E, F, H))))
+    mk = lambda: capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S_max * k,  # noqa: E731
+                            max_tokens=S_max, dtype=dt, gate=dev(w.gate, tdt), w1=dev(w.w1, tdt),
+                            w2=dev(w.w2, tdt), dispatch_mode=mode, seed=9, chunks=chunks)
+    L = mk()
+    for S in (0, 1, 17, S_max, 5, 0):
+        x = dev(grid_tokens(rng, W, S, H), tdt)
+        got = L.forward(x).clone()
+        want = mk().forward(x)
+        assert torch.equal(got, want), S
+        if S:
+            ref = O.pf_moe_forward(list(host(x)), w, E, k, S_max * k, exact=False) if mode == 0 else \
+                O.rbd_moe_forward(list(host(x)), w, E, k, S_max * k, 9, exact=False)
+            for i in range(W):
+                assert norm_rel(host(got[i]), ref[i]) < (1e-12 if dtype == "f64" else 1e-2)
+    with pytest.raises(XmoeError, match="longer than the layer's max_tokens"):
+        L.forward(dev(grid_tokens(rng, W, S_max + 1, H), tdt))
+    with pytest.raises(XmoeError, match="divisible"):
+        capi.Layer(ctx, num_experts=E + 1, model_dim=H, ffn_dim=F, top_k=k, max_token_count=8, max_tokens=8,
+                   dtype=capi.F64, gate=dev(rng.uniform(-1, 1, (H, E + 1))),
+                   w1=dev(rng.uniform(-1, 1, (E + 1, H, F))), w2=dev(rng.uniform(-1, 1, (E + 1, F, H))))
+    if mode == 1:
+        with pytest.raises(XmoeError, match="whole nodes"):
+            capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=8, max_tokens=8,
+                       dtype=dt, gate=dev(w.gate, tdt), w1=dev(w.w1, tdt), w2=dev(w.w2, tdt),
+                       dispatch_mode=1, gpus_per_node=4)
+    else:
+        with pytest.raises(XmoeError, match="redundancy-bypassing"):
+            capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=8, max_tokens=8,
+                       dtype=dt, gate=dev(w.gate, tdt), w1=dev(w.w1, tdt), w2=dev(w.w2, tdt),
+                       dispatch_mode=0, gpus_per_node=2)
