@@ -147,6 +147,34 @@ def main():
                   flush=True)
             if not all(g[0] for g in got) or max(errs) > 1e-2:
                 failures.append(("chunked", ci, [g[0] for g in got], errs))
+    # ragged and empty sequences through one layer (every rank the same S)
+    E, k, H, F = 8 * world, 3, 64, 32
+    el = E // world
+    rng = np.random.default_rng(808)
+    gate = grid_gate(rng, H, E)
+    w1 = bf16_round(rng.uniform(-0.1, 0.1, (E, H, F)))
+    w2 = bf16_round(rng.uniform(-0.1, 0.1, (E, F, H)))
+    bv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).cuda()  # noqa: E731
+    for mode in (capi.NAIVE, capi.RBD):
+        layer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=4096 * k,
+                           max_tokens=4096, dtype=capi.BF16, gate=bv(gate), w1=bv(w1[rank * el:(rank + 1) * el]),
+                           w2=bv(w2[rank * el:(rank + 1) * el]), dispatch_mode=mode, seed=5)
+        for S in (0, 1, 7, 4096, 0, 33):
+            x = grid_tokens(np.random.default_rng(S), world, S, H)
+            o = layer.forward(bv(x[rank])).float().cpu().numpy()
+            got = [None] * world
+            dist.all_gather_object(got, o)
+            if rank == 0 and S:
+                want = O.pf_moe_forward(list(x), O.LayerWeights(gate, w1, w2), E, k, 4096 * k, exact=False) \
+                    if mode == capi.NAIVE else \
+                    O.rbd_moe_forward(list(x), O.LayerWeights(gate, w1, w2), E, k, 4096 * k, 5, exact=False)
+                errs = [norm_rel(got[r], want[r]) for r in range(world)]
+                if max(errs) > 1e-2:
+                    failures.append(("ragged", mode, S, errs))
+        del layer
+        dist.barrier()
+    if rank == 0:
+        print("ragged / empty sequences checked", flush=True)
     # backward over the peer transport (bf16, dropless): dx per rank, expert
     # grads of each rank's block, gate grads summed over ranks
     from oracle import moe_grad as Gr
