@@ -188,6 +188,29 @@ def host_threads():
         return os.cpu_count() or 1
 
 
+def bind_to_gpu_numa(device):
+    """Pin this rank's host threads to the CPUs local to its GPU (PCIe root
+    complex), so the pinned staging buffers of the e2e loop live on that NUMA
+    node.  Best effort: returns the CPU list used, or None."""
+    import torch
+    try:
+        pr = torch.cuda.get_device_properties(device)
+        bus = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bus}/local_cpulist") as f:
+            spec = f.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return spec
+    except Exception:
+        return None
+    return None
+
+
 def run_reference(args, rank, world, result_out):
     if rank != 0:
         return
@@ -422,6 +445,7 @@ def main():
     # host memory; the copies of neighbouring steps overlap the compute on
     # separate streams (double-buffered), as a serving loop would run them.
     e2e_steps = max(50, args.steps)  # steady state: one pipeline fill + drain amortised over the run
+    numa_cpus = bind_to_gpu_numa(local_rank)
     xh = [x.cpu().pin_memory() for _ in range(2)]
     oh = [torch.empty_like(xh[0]).pin_memory() for _ in range(2)]
     xd = [torch.empty_like(x) for _ in range(2)]
@@ -490,6 +514,7 @@ def main():
                        "l2": "working set > L2: 0.74 GB of expert weights + 64 MB tokens stream each step (126 MB L2)"},
             "e2e": {"value": world * S / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": S * H * 2, "d2h_bytes_per_step": S * H * 2, "steps": e2e_steps,
+                    "host_cpus": numa_cpus,
                     "note": "pinned host x -> device, forward, device -> pinned host out, every step; copies of "
                             "neighbouring steps overlap the forward on two copy streams (double-buffered)"},
             "roofline": {"bound": "tensor", "kernel": "grouped_gemm_tc (routed experts, GEMM1+GEMM2)",
