@@ -453,6 +453,16 @@ __device__ __forceinline__ void tma_load_2sm(const CUtensorMap* map, uint32_t ba
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cl)
         : "memory");
 }
+// TMA gather of 4 arbitrary rows (box {BK, 1}) into 4 consecutive 128-byte
+// smem rows, completion counted on the leader's barrier.
+__device__ __forceinline__ void tma_gather4_2sm(const CUtensorMap* map, uint32_t bar_cl, void* dst, int c0,
+                                                int r0, int r1, int r2, int r3) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar_cl)
+        : "memory");
+}
 __device__ __forceinline__ uint32_t make_idesc2(int n) {
     return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
            (static_cast<uint32_t>(BM >> 4) << 24);
@@ -549,7 +559,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     grouped_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                             const int32_t* __restrict__ group_sizes, int G, int M, int N, int K,
                             OutT* __restrict__ D, int relu, const uint32_t* __restrict__ mbits_in,
-                            uint32_t* __restrict__ mbits_out, int coalesced) {
+                            uint32_t* __restrict__ mbits_out, int coalesced, const int32_t* __restrict__ a_idx,
+                            int a_rows) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -613,7 +624,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs) =====================
-        if (lane == 0) {
+        if (a_idx) {
+            // row-gathered A (a_idx: physical row of every logical row): lane l
+            // brings rows 4l..4l+3 of this CTA's 128 with one gather4 per k-block
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = pair; t < num_tiles; t += npairs) {
+                const TileInfo ti = tile_of<kVarK>(t, tile_start, off, G, ntn, M, K);
+                const int nw = min(BN, N - ti.n0);
+                const int n_mma = (nw + 15) & ~15;
+                const int arow = ti.row0 + BMC * static_cast<int>(rank);
+                const int brow = (kVarK ? 0 : ti.g * N) + ti.n0 + (n_mma / 2) * static_cast<int>(rank);
+                int r4[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) r4[q] = a_idx[min(arow + 4 * lane + q, a_rows - 1)];
+                for (int kb = 0; kb < ti.nkb; ++kb) {
+                    const uint32_t fb = mapa(&full_bar[stage], 0);
+                    if (lane == 0) {
+                        mbar_wait(&empty_bar[stage], phase ^ 1);
+                        expect_tx_cluster(fb, kStageBytes);
+                    }
+                    __syncwarp();
+                    const int kc = ti.kofs + kb * BK;
+                    tma_gather4_2sm(&tmap_a, fb, smem_a + stage * kABytes + lane * 512, kc, r4[0], r4[1], r4[2],
+                                    r4[3]);
+                    if (lane == 0) tma_load_2sm(&tmap_b, fb, smem_b + stage * kBBytes, kc, brow);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        } else if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
             for (int t = pair; t < num_tiles; t += npairs) {
@@ -1140,14 +1182,15 @@ static void launch_tc(const void* A, long long rows, int K, const int32_t* rows_
 template <typename OutT, bool kVarK>
 static void launch_tc2(const void* A, long long a_rows, long long a_cols, const int32_t* group_sizes, int G,
                        const void* B, long long b_rows, int M, int N, int K, OutT* D, int relu,
-                       const uint32_t* mbits_in, uint32_t* mbits_out, long long tile_bound, cudaStream_t st) {
+                       const uint32_t* mbits_in, uint32_t* mbits_out, long long tile_bound, cudaStream_t st,
+                       const int32_t* a_idx = nullptr, long long idx_rows = 0) {
     require(G >= 1 && G <= tc2::kMaxGroups, XMOE_ERR_VALIDATION, "grouped gemm: 1 <= groups <= 1024");
     require(a_cols % 8 == 0 && a_cols > 0, XMOE_ERR_VALIDATION, "bf16 path requires K % 8 == 0");
     require(N % 32 == 0 && N > 0, XMOE_ERR_VALIDATION, "bf16 2-CTA path requires N % 32 == 0");
     require((reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0,
             XMOE_ERR_VALIDATION, "bf16 operands must be 16-byte aligned");
     if (a_rows == 0 || tile_bound == 0) return;
-    const CUtensorMap ta = make_tmap(A, a_rows, a_cols, tc2::BMC);
+    const CUtensorMap ta = make_tmap(A, a_rows, a_cols, a_idx ? 1 : tc2::BMC);  // gather4: {BK, 1} boxes
     const CUtensorMap tb = make_tmap(B, b_rows, a_cols, tc2::BN / 2);
     static bool attr_set = false;
     if (!attr_set) {
@@ -1163,7 +1206,7 @@ static void launch_tc2(const void* A, long long a_rows, long long a_cols, const 
     const long long pairs = tile_bound < cap_pairs ? tile_bound : cap_pairs;
     tc2::grouped_gemm_tc2_kernel<OutT, kVarK><<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
         ta, tb, group_sizes, G, M, N, K, D, relu, mbits_in, mbits_out,
-        sizeof(OutT) == 4 && !mbits_out ? epi_coalesced() : 0);
+        sizeof(OutT) == 4 && !mbits_out ? epi_coalesced() : 0, a_idx, static_cast<int>(idx_rows));
     XMOE_LAUNCH_CHECK();
 }
 
@@ -1171,10 +1214,10 @@ static void launch_tc2(const void* A, long long a_rows, long long a_cols, const 
 template <typename OutT>
 static void launch_tc2_rows(const void* A, long long rows, int K, const int32_t* rows_per_group, int G,
                             const void* B, int N, OutT* D, int relu, const uint32_t* mbits_in, uint32_t* mbits_out,
-                            cudaStream_t st) {
+                            cudaStream_t st, const int32_t* a_idx = nullptr, long long phys_rows = 0) {
     const long long bound = ((rows + tc2::BM - 1) / tc2::BM + G) * static_cast<long long>((N + tc2::BN - 1) / tc2::BN);
-    launch_tc2<OutT, false>(A, rows, K, rows_per_group, G, B, static_cast<long long>(G) * N, 0, N, K, D, relu,
-                            mbits_in, mbits_out, bound, st);
+    launch_tc2<OutT, false>(A, a_idx ? phys_rows : rows, K, rows_per_group, G, B, static_cast<long long>(G) * N, 0, N,
+                            K, D, relu, mbits_in, mbits_out, bound, st, a_idx, rows);
 }
 
 // The expert FFN GEMMs run on the 2-CTA kernel; XMOE_GEMM=1cta selects the
@@ -1195,6 +1238,15 @@ void launch_grouped_gemm_bf16(const void* A, long long rows, int K, const int32_
                                        nullptr, mbits_out, st);
     else
         launch_tc<__nv_bfloat16>(A, rows, K, rows_per_group, G, B, N, static_cast<__nv_bfloat16*>(D), relu, st);
+}
+
+void launch_grouped_gemm_bf16_gather(const void* A, long long phys_rows, long long rows, int K,
+                                     const int32_t* rows_per_group, int G, const void* B, int N, void* D, int relu,
+                                     const int32_t* a_idx, cudaStream_t st) {
+    require(use_2cta(N), XMOE_ERR_VALIDATION, "row-gathered GEMM needs the 2-CTA kernel (N % 32 == 0)");
+    require(phys_rows < (1LL << 31) && rows >= 1, XMOE_ERR_VALIDATION, "row-gathered GEMM: 1 <= rows, phys rows < 2^31");
+    launch_tc2_rows<__nv_bfloat16>(A, rows, K, rows_per_group, G, B, N, static_cast<__nv_bfloat16*>(D), relu,
+                                   nullptr, nullptr, st, a_idx, phys_rows);
 }
 
 void launch_grouped_gemm_bf16_mask(const void* A, long long rows, int K, const int32_t* rows_per_group, int G,

@@ -73,6 +73,11 @@ void launch_grouped_gemm_f64(const double* A, long long rows_bound, int K,
 void launch_grouped_gemm_bf16(const void* A, long long rows, int K, const int32_t* rows_per_group,
                               int G, const void* B, int N, void* D, int relu, cudaStream_t st,
                               uint32_t* mbits_out = nullptr);
+// A rows gathered through a_idx: logical row r (< rows) reads A[a_idx[r]]
+// (A has phys_rows rows; TMA gather4)
+void launch_grouped_gemm_bf16_gather(const void* A, long long phys_rows, long long rows, int K,
+                                     const int32_t* rows_per_group, int G, const void* B, int N, void* D, int relu,
+                                     const int32_t* a_idx, cudaStream_t st);
 // dgrad with the ReLU mask of the forward: D = (A B) * mask
 void launch_grouped_gemm_bf16_mask(const void* A, long long rows, int K, const int32_t* rows_per_group, int G,
                                    const void* B, int N, void* D, const uint32_t* mbits, cudaStream_t st);

@@ -124,6 +124,16 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
                 "the redundancy-bypassing dispatch runs on the NVLink peer transport");
     }
     L.gpn = std::max(1, XMOE_LAYER_GPUS_PER_NODE_OF(d.flags));
+    {
+        // XMOE_RBD_GATHER=1: RBD replicas read their pilot's row through a TMA
+        // gather4 A-load in GEMM1 instead of the expand copy (training layers
+        // keep the copies: the wgrad reads them).  Bit-identical, but measured
+        // slower (GEMM1 0.97 -> 1.83 ms at N=2 for 0.05 ms of expand saved:
+        // 4-row gathers move A at a fraction of a 128-row box), so opt-in.
+        const char* e = std::getenv("XMOE_RBD_GATHER");
+        L.rbd_gather = d.dispatch_mode == XMOE_DISPATCH_RBD && d.dtype == XMOE_BF16 && L.gpn == 1 &&
+                       !(d.flags & XMOE_LAYER_TRAIN) && d.ffn_dim % 32 == 0 && e && std::atoi(e) == 1;
+    }
     require(W % L.gpn == 0, XMOE_ERR_VALIDATION, "the worker group must be whole nodes (world % gpus_per_node)");
     require(L.gpn == 1 || rbd, XMOE_ERR_VALIDATION, "gpus_per_node applies to the redundancy-bypassing dispatch");
     const int H = L.H, F = L.F, E = L.E;
@@ -289,6 +299,12 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
             r.csr_ws = L.alloc(bucket_ws_bytes(nk, W));
             r.C = L.nchunks;
             r.gpn = L.gpn;
+            if (L.rbd_gather) {  // identity until the first expand rewrites the received rows
+                std::vector<int32_t> iota(static_cast<size_t>(L.R_max));
+                for (size_t q = 0; q < iota.size(); ++q) iota[q] = static_cast<int32_t>(q);
+                w.a_idx = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * iota.size()));
+                XMOE_CUDA(cudaMemcpy(w.a_idx, iota.data(), sizeof(int32_t) * iota.size(), cudaMemcpyHostToDevice));
+            }
             r.gpos = i32(static_cast<long long>(W) * (r.C + 1));
             r.gd_own = L.distributed ? i32(2LL * W * r.C)
                                      : L.gd_all + static_cast<size_t>(w.rank) * 2 * W * r.C;
@@ -622,11 +638,15 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
         g_gemm_sm_limit = part_sms;
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
-            if (rbd)  // replicas copy the row from their pilot's slot
+            if (rbd)  // replicas read (gather) or copy the row from their pilot's slot
                 launch_rbd_expand(static_cast<int>(rb), w.desc_recv, w.rbd, c, L.R_max, w.recv, L.recv_tab, w.gstart,
-                                  st);
-            launch_grouped_gemm_bf16(static_cast<char*>(w.recv) + r0 * rb, L.Rc, H, w.rpe_c + c * El, El,
-                                     w1_of(L, w.rank), F, static_cast<char*>(w.mid) + r0 * F * L.es, 1, st);
+                                  st, L.rbd_gather ? w.a_idx : nullptr);
+            if (rbd && L.rbd_gather)
+                launch_grouped_gemm_bf16_gather(w.recv, L.R_max, L.Rc, H, w.rpe_c + c * El, El, w1_of(L, w.rank), F,
+                                                static_cast<char*>(w.mid) + r0 * F * L.es, 1, w.a_idx + r0, st);
+            else
+                launch_grouped_gemm_bf16(static_cast<char*>(w.recv) + r0 * rb, L.Rc, H, w.rpe_c + c * El, El,
+                                         w1_of(L, w.rank), F, static_cast<char*>(w.mid) + r0 * F * L.es, 1, st);
             launch_grouped_gemm_bf16(static_cast<char*>(w.mid) + r0 * F * L.es, L.Rc, F, w.rpe_c + c * El, El,
                                      w2_of(L, w.rank), H, static_cast<char*>(w.eout) + r0 * rb, 0, st);
             if (rbd)  // weighted sum of each group's outputs, pilot first (rbd.cpp:318-336)
@@ -788,7 +808,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             launch_rbd_expand(static_cast<int>(row_bytes), w.desc_recv, w.rbd, 0, L.R_max, w.recv, L.recv_tab,
-                              w.gstart, st);
+                              w.gstart, st, L.rbd_gather ? w.a_idx : nullptr);
         }
         if (dist && L.gpn > 1) fbar(1);  // stage-2 rows landed in peers' inputs
     } else if (tables) {
@@ -817,7 +837,11 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     for (int i = 0; i < nl; ++i) {
         Worker& w = L.workers[i];
         launch_recv_counts(L.tpe_all, W, E, w.rank, w.rpe, st);
-        run_gemm(dt, w.recv, L.R_max, H, w.rpe, L.El, w1_of(L, w.rank), F, w.mid, 1, st, w.mbits);
+        if (rbd && L.rbd_gather)  // replica rows come straight from their pilot's row (TMA gather4)
+            launch_grouped_gemm_bf16_gather(w.recv, L.R_max, L.R_max, H, w.rpe, L.El, w1_of(L, w.rank), F, w.mid, 1,
+                                            w.a_idx, st);
+        else
+            run_gemm(dt, w.recv, L.R_max, H, w.rpe, L.El, w1_of(L, w.rank), F, w.mid, 1, st, w.mbits);
         run_gemm(dt, w.mid, L.R_max, F, w.rpe, L.El, w2_of(L, w.rank), H, w.eout, 0, st);
     }
     L.mark(kEvGemm, st);

@@ -72,6 +72,7 @@ struct Worker {
     void* dH = nullptr;           // [R_max, F]
     void* tail_a = nullptr;       // wgrad tail blocks [64*(El+1), max(H,F,Fs)]
     void* tail_b = nullptr;
+    int32_t* a_idx = nullptr;     // [R_max] RBD gather: physical recv row of every grouped row
     uint32_t* mbits = nullptr;    // [R_max, ceil(F/32)] ReLU mask bits of mid (training)
     uint32_t* smbits = nullptr;   // [S, ceil(Fs/32)] of the shared experts' mid
     void* tail_sa = nullptr;      // the same for the side-stream (shared-expert) wgrad
@@ -108,6 +109,7 @@ struct Layer {
     int W = 1, E = 0, H = 0, F = 0, k = 0, El = 0, E_held = 0, Fs = 0;
     int nl = 1;                // ranks driven by this process
     int gpn = 1;               // RBD GPUs per node (node_of = rank / gpn)
+    bool rbd_gather = false;   // RBD GEMM1 gathers replica rows (no expand copy)
     bool ssmb = false;         // sequence-sharded block: experts replicated, MoE local
     bool distributed = false;  // one process per GPU, world > 1
     bool p2p = false;          // NVLink peer tables (else NCCL send/recv baseline)

@@ -489,7 +489,8 @@ __global__ void __launch_bounds__(256) rbd_expand_kernel(char* const* __restrict
                                                          int row_bytes, const RbdDesc* __restrict__ desc,
                                                          const int32_t* __restrict__ rx, int C, int ck,
                                                          const char* __restrict__ grouped,
-                                                         int32_t* __restrict__ gstart) {
+                                                         int32_t* __restrict__ gstart,
+                                                         int32_t* __restrict__ a_idx) {
     const int dbeg = rx[2 * C + ck], dend = dbeg + rx[3 * C + ck];
     const int lane = threadIdx.x & 31;
     const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -498,6 +499,17 @@ __global__ void __launch_bounds__(256) rbd_expand_kernel(char* const* __restrict
         const RbdDesc dd = desc[c];
         const int m = dd.member & kRbdMemberMask;
         if (lane == 0 && m == 0) gstart[dd.u] = static_cast<int>(c);
+        if (a_idx) {  // gather mode: GEMM1 reads every copy's row through a_idx
+            if (lane == 0) {
+                int prow = dd.dest_row;
+                for (int q = 0; q < dd.n; ++q) {
+                    const RbdDesc pq = desc[c - m + q];
+                    if (pq.member & kRbdPilotFlag) prow = pq.dest_row;
+                }
+                a_idx[dd.dest_row] = prow;
+            }
+            continue;
+        }
         if (dd.member & kRbdPilotFlag) continue;  // already in place
         int prow = dd.dest_row;
         for (int q = 0; q < dd.n; ++q) {
@@ -844,11 +856,11 @@ void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, int W, int
 }
 
 void launch_rbd_expand(int row_bytes, const RbdDesc* desc, const RbdWork& wk, int c, long long max_desc,
-                       void* grouped, char* const* recv_tab, int32_t* gstart, cudaStream_t st) {
+                       void* grouped, char* const* recv_tab, int32_t* gstart, cudaStream_t st, int32_t* a_idx) {
     int grid = warp_grid(max_desc / wk.C + 1);
     if (g_copy_blocks > 0 && grid > g_copy_blocks) grid = g_copy_blocks;
     rbd_expand_kernel<<<grid, 256, 0, st>>>(recv_tab, row_bytes, desc, wk.rx, wk.C, c,
-                                            static_cast<const char*>(grouped), gstart);
+                                            static_cast<const char*>(grouped), gstart, a_idx);
     XMOE_LAUNCH_CHECK();
 }
 

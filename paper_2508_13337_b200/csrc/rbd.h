@@ -80,8 +80,11 @@ void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, int W, int
                      const int32_t* expert_ids = nullptr, int El = 1);
 // replicas copy their pilot's row (local) into their owner's grouped input
 // (recv_tab: local or NVLink peer); `grouped` is this landing rank's input
+// a_idx (gather mode, one GPU per node): record each copy's pilot row for
+// the row-gathered GEMM1 instead of copying the row
 void launch_rbd_expand(int row_bytes, const RbdDesc* desc, const RbdWork& wk, int c, long long max_desc,
-                       void* grouped, char* const* recv_tab, int32_t* gstart, cudaStream_t st);
+                       void* grouped, char* const* recv_tab, int32_t* gstart, cudaStream_t st,
+                       int32_t* a_idx = nullptr);
 // each group's members' outputs read from their owners (eout_tab)
 void launch_rbd_merge(int dtype, const char* const* eout_tab, int H, const RbdDesc* desc, const int32_t* gstart,
                       const RbdWork& wk, int c, long long max_groups, void* back_u, cudaStream_t st);

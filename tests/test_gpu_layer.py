@@ -438,3 +438,29 @@ def test_layer_edge_lengths_and_errors(mode, dtype, chunks):
             capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=8, max_tokens=8,
                        dtype=dt, gate=dev(w.gate, tdt), w1=dev(w.w1, tdt), w2=dev(w.w2, tdt),
                        dispatch_mode=0, gpus_per_node=2)
+
+
+@pytest.mark.parametrize("W,chunks", [(2, 1), (4, 1), (8, 1), (4, 3)])
+def test_rbd_gather_gemm_bit_identical_to_expand(W, chunks, monkeypatch):
+    """RBD replicas read through the TMA gather4 A-load of GEMM1 (no expand
+    copy, XMOE_RBD_GATHER=1) give bit-identical outputs to the row-copying
+    expand (the default)."""
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, W, -1)
+    rng = np.random.default_rng(W * 10 + chunks)
+    E, k, H, F, S = 8 * W, 6, 256, 128, 700
+    w = O.LayerWeights(grid_gate(rng, H, E), bf16_round(rng.uniform(-0.1, 0.1, (E, H, F))),
+                       bf16_round(rng.uniform(-0.1, 0.1, (E, F, H))))
+    x = dev(grid_tokens(rng, W, S, H), torch.bfloat16)
+    outs = []
+    for gather in ("0", "1"):
+        monkeypatch.setenv("XMOE_RBD_GATHER", gather)
+        L = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k, max_tokens=S,
+                       dtype=capi.BF16, gate=dev(w.gate, torch.bfloat16), w1=dev(w.w1, torch.bfloat16),
+                       w2=dev(w.w2, torch.bfloat16), dispatch_mode=capi.RBD, seed=21, chunks=chunks)
+        outs.append(L.forward(x).clone())
+        outs.append(L.forward(x).clone())
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+    want = O.rbd_moe_forward(list(host(x)), w, E, k, S * k, 21, exact=False)
+    for i in range(W):
+        assert norm_rel(host(outs[3][i]), want[i]) < 1e-2
