@@ -696,6 +696,9 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     Ctx& ctx = *L.ctx;
     require(S >= 0 && S <= L.S_max, XMOE_ERR_VALIDATION, "sequence longer than the layer's max_tokens");
     L.last_ssmb = false;
+    g_copy_blocks = 0;  // launch-shaping globals start clean even after an aborted forward
+    g_copy_smem = 0;
+    g_gemm_sm_limit = 0;
     if (L.nchunks > 1 && S > 0) {
         layer_forward_chunked(L, x, S, out, st);
         return;
