@@ -4,7 +4,8 @@
 //   logits = X . Wg      (F64: ascending-h __dmul_rn/__dadd_rn, bit-exact to
 //                         kernels_scalar.cpp:11-23; BF16: fp32 accumulation,
 //                         exact on the bf16 grid inputs)
-//   probs  = softmax(logits - max)  in fp64, summed ascending e (gating.cpp:39-43)
+//   probs  = softmax(logits - max)  in fp64, summed ascending e (gating.cpp:39-43;
+//            the BF16 path sums as a tree)
 //   top-k  by (prob desc, id asc)   (gating.cpp:45-50), raw probs as weights.
 #include "common.cuh"
 #include "kernels.cuh"
@@ -58,12 +59,22 @@ __global__ void __launch_bounds__(256) softmax_topk_kernel(const LT* __restrict_
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
 #pragma unroll
     for (int i = 0; i < PER; ++i) p[i] = (lane + 32 * i < E) ? exp(__dsub_rn(p[i], mx)) : 0.0;
-    // Sequential ascending-e sum, exactly as the reference accumulates (gating.cpp:42).
     double sum = 0.0;
+    if constexpr (sizeof(LT) == 8) {
+        // F64 parity: sequential ascending-e sum, exactly as the reference
+        // accumulates (gating.cpp:42)
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-        const int lim = min(32, E - 32 * i);
-        for (int l = 0; l < lim; ++l) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, p[i], l));
+        for (int i = 0; i < PER; ++i) {
+            const int lim = min(32, E - 32 * i);
+            for (int l = 0; l < lim; ++l) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, p[i], l));
+        }
+    } else {
+        // BF16 path: tree sum (weights within a few fp64 ulp of the reference;
+        // the top-k order depends on the logits alone, so routing is unchanged)
+#pragma unroll
+        for (int i = 0; i < PER; ++i) sum += p[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     }
 #pragma unroll
     for (int i = 0; i < PER; ++i) p[i] = (lane + 32 * i < E) ? __ddiv_rn(p[i], sum) : -1.0;

@@ -61,7 +61,7 @@ def test_gate_bf16_routing_bit_exact(ctx, S, H, E, k):
     top, w, lg = ctx.gate_forward(dev(x, torch.bfloat16), dev(wg.T, torch.bfloat16), k, want_logits=True)
     assert np.array_equal(host(lg), g.logits)
     assert np.array_equal(host(top), g.top_experts)
-    np.testing.assert_allclose(host(w), g.combine_weights, rtol=1e-15, atol=0)
+    np.testing.assert_allclose(host(w), g.combine_weights, rtol=1e-14, atol=0)  # tree-summed softmax
 
 
 def test_gate_renorm(ctx):
