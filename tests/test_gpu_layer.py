@@ -464,3 +464,28 @@ def test_rbd_gather_gemm_bit_identical_to_expand(W, chunks, monkeypatch):
     want = O.rbd_moe_forward(list(host(x)), w, E, k, S * k, 21, exact=False)
     for i in range(W):
         assert norm_rel(host(outs[3][i]), want[i]) < 1e-2
+
+
+@pytest.mark.parametrize("W,E,k,H,F,mode,chunks", [(16, 16, 1, 16, 32, 0, 1), (16, 16, 3, 16, 32, 1, 1),
+                                                   (2, 16, 2, 64, 32, 1, 2), (8, 16, 8, 32, 64, 0, 4),
+                                                   (8, 16, 8, 32, 64, 1, 1), (1, 16, 16, 32, 32, 0, 3)])
+def test_bf16_unusual_shapes(W, E, k, H, F, mode, chunks):
+    """top_k = 1, one expert per GPU (16 workers), top_k = num_experts, the
+    smallest bf16 widths (bf16 needs num_experts % 16 == 0) — plain and RBD,
+    chunked and not — against the oracle."""
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, W, -1)
+    rng = np.random.default_rng(E * 7 + k)
+    S = 300
+    w = O.LayerWeights(grid_gate(rng, H, E), bf16_round(rng.uniform(-0.1, 0.1, (E, H, F))),
+                       bf16_round(rng.uniform(-0.1, 0.1, (E, F, H))))
+    x = grid_tokens(rng, W, S, H)
+    for cap in (S * k, max(1, S * k // (2 * E))):
+        L = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=cap, max_tokens=S,
+                       dtype=capi.BF16, gate=dev(w.gate, torch.bfloat16), w1=dev(w.w1, torch.bfloat16),
+                       w2=dev(w.w2, torch.bfloat16), dispatch_mode=mode, seed=2, chunks=chunks)
+        got = host(L.forward(dev(x, torch.bfloat16)))
+        want = O.pf_moe_forward(list(x), w, E, k, cap, exact=False) if mode == 0 else \
+            O.rbd_moe_forward(list(x), w, E, k, cap, 2, exact=False)
+        for i in range(W):
+            assert norm_rel(got[i], want[i]) < 1e-2, (cap, i, norm_rel(got[i], want[i]))
