@@ -509,16 +509,18 @@ static void exchange_counts(Layer& L, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------- chunked forward
-// BF16 plain dispatch, cut into L.nchunks token chunks (chunk.cu).  Streams:
-//   st   gate | shared-expert GEMMs | per chunk: [wait A_c] GEMM1, GEMM2 [signal B_c]
-//   comm       PFT, counts, destinations | per chunk: scatter [signal A_c] | per chunk: [wait B_c] combine
+// BF16 forward (plain or RBD dispatch), cut into L.nchunks token chunks
+// (chunk.cu).  Streams:
+//   st   gate | shared-expert GEMMs | per chunk: [wait A_c] (RBD expand) GEMM1, GEMM2 (RBD merge) [signal B_c]
+//   comm       PFT (+RBD groups), count exchange, destinations | per chunk: scatter / pack [signal A_c]
+//              | per chunk: [wait B_c] combine
 // so chunk c's expert GEMMs run while chunk c+1's rows are still moving and
 // chunk c-1's outputs are being combined; the row-movement kernels need no
-// shared memory and co-reside with the persistent GEMM CTAs.  A_c / B_c are
-// local events plus, across GPUs, epoch flags in the peers' symmetric
-// regions.  Every row's arithmetic equals the unchunked forward's.
+// shared memory and co-reside with the persistent GEMM CTAs on a bounded
+// grid.  A_c / B_c are local events plus, across GPUs, epoch flags in the
+// peers' symmetric regions.  Every row's arithmetic equals the unchunked
+// forward's.
 static void layer_forward_chunked(Layer& L, const void* x, long long S, void* out, cudaStream_t st) {
-    Ctx& ctx = *L.ctx;
     const int W = L.W, E = L.E, H = L.H, F = L.F, k = L.k, El = L.El, C = L.nchunks;
     const size_t rb = static_cast<size_t>(H) * L.es;
     const int nl = L.nl;
