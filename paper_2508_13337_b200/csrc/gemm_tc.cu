@@ -413,7 +413,10 @@ constexpr uint32_t kBBytes = (BN / 2) * BK * 2;
 constexpr uint32_t kStageBytes = kABytes + kBBytes;
 constexpr size_t kGroupTabBytes = sizeof(int32_t) * 2 * (kMaxGroups + 1);
 constexpr size_t kEpiWarpWords = 32 * 33;  // per epilogue warp: a 32 x 32 transpose tile (+1 pad)
-constexpr size_t kSmemBytes = 1024 + kStages * kStageBytes + 1024 + kGroupTabBytes + 4 * kEpiWarpWords * 4;
+constexpr size_t kEpiWarpBytes = 5120;     // per-warp staging slot (1024-aligned, >= 32*33*4)
+// epilogue staging area: 1024-aligned (the TMA-store tile uses the 128B swizzle)
+constexpr size_t kEpiOff = (kStages * kStageBytes + 1024 + kGroupTabBytes + 1023) / 1024 * 1024;
+constexpr size_t kSmemBytes = 1024 + kEpiOff + 4 * kEpiWarpBytes;
 
 using tc::make_desc;
 using tc::mbar_init;
@@ -463,6 +466,18 @@ __device__ __forceinline__ void tma_gather4_2sm(const CUtensorMap* map, uint32_t
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar_cl)
         : "memory");
 }
+// TMA store of a staged smem box to global (bulk-group completion)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(smem_u32(src))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ uint32_t make_idesc2(int n) {
     return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
            (static_cast<uint32_t>(BM >> 4) << 24);
@@ -744,8 +759,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                             : nullptr;
             uint32_t* orow = mbits_out ? mbits_out + static_cast<size_t>(ti.row0 + r) * mwords + (ti.n0 >> 5)
                                        : nullptr;
-            uint32_t* etile = reinterpret_cast<uint32_t*>(smem + kStages * kStageBytes + 1024 + kGroupTabBytes) +
-                              (warp - 2) * kEpiWarpWords;
+            uint32_t* etile = reinterpret_cast<uint32_t*>(smem + kEpiOff + (warp - 2) * kEpiWarpBytes);
             const int wrow = BMC * static_cast<int>(rank) + quarter * 32;  // first row of this warp in the tile
             for (int c0 = 0; c0 < nw; c0 += 32) {
                 uint32_t v[32];
@@ -866,7 +880,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     grouped_wgrad_mn_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                             const __grid_constant__ CUtensorMap tmap_at, const __grid_constant__ CUtensorMap tmap_bt,
                             const int32_t* __restrict__ group_rows, int G, int M, int N, float* __restrict__ D,
-                            int coalesced) {
+                            int coalesced, const __grid_constant__ CUtensorMap tmap_d, int tma_store) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -1028,13 +1042,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
-            uint32_t* etile = reinterpret_cast<uint32_t*>(smem + kStages * kStageBytes + 1024 + kGroupTabBytes) +
-                              (warp - 2) * kEpiWarpWords;
+            uint32_t* etile = reinterpret_cast<uint32_t*>(smem + kEpiOff + (warp - 2) * kEpiWarpBytes);
             const int wrow = BMC * static_cast<int>(rank) + quarter * 32;
             for (int c0 = 0; c0 < nw; c0 += 32) {
                 uint32_t v[32];
                 tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN + c0),
                           v);
+                if (tma_store) {
+                    // 32 x 32 fp32 box through 128B-swizzled smem, stored by TMA
+                    // (the D map is [G*M, N]; M % 256 == 0, so a box never
+                    // crosses into the next group)
+                    if (lane == 0) tma_store_wait_read();  // the previous box left the buffer
+                    __syncwarp();
+                    uint8_t* row = reinterpret_cast<uint8_t*>(etile) + lane * 128;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        *reinterpret_cast<uint4*>(row + ((q ^ (lane & 7)) << 4)) =
+                            make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) tma_store_2d(&tmap_d, etile, n0 + c0, g * M + row0 + wrow);
+                    continue;
+                }
                 if (coalesced) {
                     float f[32];
 #pragma unroll
@@ -1065,6 +1094,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
     }
+    if (tma_store && warp >= 2 && lane == 0) tma_store_wait_all();
     tc_fence_before();
     __syncthreads();
     cluster_sync();
@@ -1107,6 +1137,15 @@ __global__ void wgrad_tail_kernel(const __nv_bfloat16* __restrict__ X, int C, co
 // shared-memory transpose as whole-row segments (measured: wgrad 1.59 ->
 // 1.23 ms); bf16 outputs keep the direct per-row 16-byte stores, which
 // measured faster.  XMOE_EPI=0 selects the direct stores everywhere.
+// weight gradients leave through TMA stores (XMOE_WGRAD_TMA=0: the
+// shared-memory transpose + coalesced stores)
+static bool wgrad_tma_store() {
+    static const bool v = [] {
+        const char* e = std::getenv("XMOE_WGRAD_TMA");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return v;
+}
 static int epi_coalesced() {
     static const int v = [] {
         const char* e = std::getenv("XMOE_EPI");
@@ -1282,6 +1321,19 @@ void launch_grouped_wgrad_mn(const void* A, int M, const void* B, int N, long lo
     const CUtensorMap tb = make_tmap(B, r, N, 64);
     const CUtensorMap tat = make_tmap(tail_a, 64LL * G, M, 64);
     const CUtensorMap tbt = make_tmap(tail_b, 64LL * G, N, 64);
+    // fp32 D [G*M, N] for the TMA-store epilogue: boxes of 32 x 32, 128B swizzle
+    const bool tma_store = wgrad_tma_store() && M % tc2::BM == 0 && N % 32 == 0;
+    CUtensorMap td{};
+    if (tma_store) {
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(G) * M};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(N) * 4};
+        const cuuint32_t box[2] = {32, 32};
+        const cuuint32_t estr[2] = {1, 1};
+        const CUresult r = get_encode()(&td, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, D, dims, strides, box, estr,
+                                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail(XMOE_ERR_CUDA, "cuTensorMapEncodeTiled (wgrad D) failed: " + std::to_string(r));
+    }
     static bool attr_set = false;
     if (!attr_set) {
         XMOE_CUDA(cudaFuncSetAttribute(tc2::grouped_wgrad_mn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1293,7 +1345,7 @@ void launch_grouped_wgrad_mn(const void* A, int M, const void* B, int N, long lo
     const long long tiles = static_cast<long long>(G) * ((M + tc2::BM - 1) / tc2::BM) * ((N + tc2::BN - 1) / tc2::BN);
     const long long pairs = tiles < sms / 2 ? tiles : sms / 2;
     tc2::grouped_wgrad_mn_kernel<<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
-        ta, tb, tat, tbt, group_rows, G, M, N, D, epi_coalesced());
+        ta, tb, tat, tbt, group_rows, G, M, N, D, epi_coalesced(), td, tma_store ? 1 : 0);
     XMOE_LAUNCH_CHECK();
 }
 
