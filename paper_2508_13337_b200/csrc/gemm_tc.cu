@@ -575,7 +575,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             const int32_t* __restrict__ group_sizes, int G, int M, int N, int K,
                             OutT* __restrict__ D, int relu, const uint32_t* __restrict__ mbits_in,
                             uint32_t* __restrict__ mbits_out, int coalesced, const int32_t* __restrict__ a_idx,
-                            int a_rows) {
+                            int a_rows, const __grid_constant__ CUtensorMap tmap_d, int tma_d) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -761,6 +761,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                        : nullptr;
             uint32_t* etile = reinterpret_cast<uint32_t*>(smem + kEpiOff + (warp - 2) * kEpiWarpBytes);
             const int wrow = BMC * static_cast<int>(rank) + quarter * 32;  // first row of this warp in the tile
+            // bf16 output boxes of 32 rows x 64 columns leave through TMA stores when
+            // the warp's 32 rows all belong to the group (a box must not touch the
+            // next group's rows)
+            const bool use_tma = sizeof(OutT) == 2 && !kVarK && tma_d && ti.rows_left - wrow >= 32 && (nw & 63) == 0;
             for (int c0 = 0; c0 < nw; c0 += 32) {
                 uint32_t v[32];
                 tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
@@ -802,6 +806,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if constexpr (sizeof(OutT) == 2) {
                     if (cn == 32 && (N & 7) == 0) {
                         int4* dst = reinterpret_cast<int4*>(drow + c0);
+                        uint8_t* srow = reinterpret_cast<uint8_t*>(etile) + lane * 128;  // staging row (128B swizzle)
+                        if (use_tma && (c0 & 63) == 0) {
+                            if (lane == 0) tma_store_wait_read();  // the previous box left the buffer
+                            __syncwarp();
+                        }
                         uint32_t mw = 0;  // ReLU mask of the stored bf16 values (bit i: y_i != 0)
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
@@ -814,10 +823,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                     mw |= ((u[e] & 0x7FFF0000u) ? 1u : 0u) << (8 * q + 2 * e + 1);
                                 }
                             }
-                            dst[q] = make_int4(static_cast<int>(u[0]), static_cast<int>(u[1]), static_cast<int>(u[2]),
-                                               static_cast<int>(u[3]));
+                            const int4 o = make_int4(static_cast<int>(u[0]), static_cast<int>(u[1]),
+                                                     static_cast<int>(u[2]), static_cast<int>(u[3]));
+                            if (use_tma) {
+                                const int chunk = ((c0 & 32) >> 3) + q;  // 16-byte chunk in the 128-byte row
+                                *reinterpret_cast<int4*>(srow + ((chunk ^ (lane & 7)) << 4)) = o;
+                            } else {
+                                dst[q] = o;
+                            }
                         }
                         if (orow) orow[c0 >> 5] = mw;
+                        if (use_tma && (c0 & 63) == 32) {
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                            __syncwarp();
+                            if (lane == 0) tma_store_2d(&tmap_d, etile, ti.n0 + c0 - 32, ti.row0 + wrow);
+                        }
                     } else {
                         uint32_t mw = 0;
                         for (int i = 0; i < cn; ++i) {
@@ -846,6 +866,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
     }
+    if (tma_d && warp >= 2 && lane == 0) tma_store_wait_all();
     tc_fence_before();
     __syncthreads();
     cluster_sync();  // the peer is done with the pair's TMEM and barriers
@@ -1139,6 +1160,15 @@ __global__ void wgrad_tail_kernel(const __nv_bfloat16* __restrict__ X, int C, co
 // measured faster.  XMOE_EPI=0 selects the direct stores everywhere.
 // weight gradients leave through TMA stores (XMOE_WGRAD_TMA=0: the
 // shared-memory transpose + coalesced stores)
+// bf16 GEMM outputs leave through TMA stores where a warp's rows are whole
+// (XMOE_FWD_TMA=0: direct per-row stores)
+static bool fwd_tma_store() {
+    static const bool v = [] {
+        const char* e = std::getenv("XMOE_FWD_TMA");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return v;
+}
 static bool wgrad_tma_store() {
     static const bool v = [] {
         const char* e = std::getenv("XMOE_WGRAD_TMA");
@@ -1231,6 +1261,20 @@ static void launch_tc2(const void* A, long long a_rows, long long a_cols, const 
     if (a_rows == 0 || tile_bound == 0) return;
     const CUtensorMap ta = make_tmap(A, a_rows, a_cols, a_idx ? 1 : tc2::BMC);  // gather4: {BK, 1} boxes
     const CUtensorMap tb = make_tmap(B, b_rows, a_cols, tc2::BN / 2);
+    // bf16 D [rows, N] for the TMA-store epilogue (boxes of 64 columns x 32 rows, 128B swizzle)
+    const long long d_rows = a_idx ? idx_rows : a_rows;
+    const bool tma_d = sizeof(OutT) == 2 && !kVarK && fwd_tma_store() && N % 64 == 0 && d_rows > 0;
+    CUtensorMap td{};
+    if (tma_d) {
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(d_rows)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(N) * 2};
+        const cuuint32_t box[2] = {64, 32};
+        const cuuint32_t estr[2] = {1, 1};
+        const CUresult r = get_encode()(&td, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, dims, strides, box, estr,
+                                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail(XMOE_ERR_CUDA, "cuTensorMapEncodeTiled (D) failed: " + std::to_string(r));
+    }
     static bool attr_set = false;
     if (!attr_set) {
         XMOE_CUDA(cudaFuncSetAttribute(tc2::grouped_gemm_tc2_kernel<OutT, kVarK>,
@@ -1245,7 +1289,7 @@ static void launch_tc2(const void* A, long long a_rows, long long a_cols, const 
     const long long pairs = tile_bound < cap_pairs ? tile_bound : cap_pairs;
     tc2::grouped_gemm_tc2_kernel<OutT, kVarK><<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
         ta, tb, group_sizes, G, M, N, K, D, relu, mbits_in, mbits_out,
-        sizeof(OutT) == 4 && !mbits_out ? epi_coalesced() : 0, a_idx, static_cast<int>(idx_rows));
+        sizeof(OutT) == 4 && !mbits_out ? epi_coalesced() : 0, a_idx, static_cast<int>(idx_rows), td, tma_d ? 1 : 0);
     XMOE_LAUNCH_CHECK();
 }
 
