@@ -18,7 +18,7 @@ namespace xmoe {
 __global__ void __launch_bounds__(256) bwd_owner_prep_kernel(
     const __nv_bfloat16* __restrict__ dyg, const __nv_bfloat16* __restrict__ eout, const float* __restrict__ gw,
     const unsigned long long* __restrict__ gsrc, const int32_t* __restrict__ rpe, int El, int H,
-    float* const* __restrict__ slotdw_tab, __nv_bfloat16* __restrict__ dz) {
+    float* const* __restrict__ slotdw_tab, __nv_bfloat16* __restrict__ dz, int me) {
     int rows = 0;
     for (int i = 0; i < El; ++i) rows += rpe[i];
     const int lane = threadIdx.x & 31;
@@ -26,6 +26,8 @@ __global__ void __launch_bounds__(256) bwd_owner_prep_kernel(
     const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
     const int nvec = H >> 3;
     for (long long r = warp; r < rows; r += nwarps) {
+        const unsigned long long s = gsrc[r];
+        if (static_cast<int>(s >> 32) == me) continue;  // finished by bwd_scatter_dy_kernel at the source
         const int4* a = reinterpret_cast<const int4*>(dyg + static_cast<size_t>(r) * H);
         const int4* b = reinterpret_cast<const int4*>(eout + static_cast<size_t>(r) * H);
         int4* o = reinterpret_cast<int4*>(dz + static_cast<size_t>(r) * H);
@@ -53,12 +55,112 @@ __global__ void __launch_bounds__(256) bwd_owner_prep_kernel(
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
-        if (lane == 0) {
-            const unsigned long long s = gsrc[r];
-            slotdw_tab[s >> 32][static_cast<uint32_t>(s)] = dot;
-        }
+        if (lane == 0) slotdw_tab[s >> 32][static_cast<uint32_t>(s)] = dot;
     }
     __threadfence_system();
+}
+
+// B1 + B2 fused, token side, one warp per token (bf16 rows, H % 8 == 0):
+// dy_t is read once; for every kept copy c of t
+//   * owned by this rank: dw_c = <dy_t, y_c> (y_c read from the local expert
+//     output) goes straight to the home slot, and dz = w_c * dy_t is written
+//     into the grouped dz buffer — the owner-side pass never sees the row;
+//   * owned by a peer: dy_t goes to the peer's grouped dy buffer with the
+//     copy's weight and home slot, for bwd_owner_prep_kernel over there.
+// The dot product uses the owner-side pass's per-lane order (ascending 16 B
+// chunks, lo/hi halves, then the xor-shuffle tree), so both give the same
+// bits.  Algorithmic bytes at W = 1: dy once, y and dz once per copy.
+constexpr int kBsVec = 8;  // int4 per lane per pass (4 KB rows in one pass)
+
+__global__ void __launch_bounds__(256) bwd_scatter_dy_kernel(
+    const char* __restrict__ dy, int H, int S, int k, const int32_t* __restrict__ slot_pos,
+    const int32_t* __restrict__ dest_rank, const int32_t* __restrict__ dest_row, const double* __restrict__ cw,
+    int me, char* __restrict__ dz, char* const* __restrict__ eout_tab, char* const* __restrict__ dyg_tab,
+    char* const* __restrict__ dxc_tab, float* const* __restrict__ gw_tab,
+    unsigned long long* const* __restrict__ gsrc_tab, float* __restrict__ slot_dw,
+    unsigned long long* __restrict__ bslot_src) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    const size_t rb = static_cast<size_t>(H) * 2;
+    const int nvec = H >> 3;
+    const bool one_pass = nvec <= 32 * kBsVec;
+    for (long long t = warp; t < S; t += nwarps) {
+        const int4* src = reinterpret_cast<const int4*>(dy + static_cast<size_t>(t) * rb);
+        int4 v[kBsVec];
+#pragma unroll
+        for (int u = 0; u < kBsVec; ++u) {
+            const int c = lane + 32 * u;
+            v[u] = c < nvec ? ld_nc_v4(src + c) : make_int4(0, 0, 0, 0);
+        }
+        int p = -1, r = -1, row = 0;
+        float wv = 0.f;
+        if (lane < k) {
+            p = slot_pos[static_cast<size_t>(t) * k + lane];
+            if (p >= 0) {
+                r = dest_rank[p];
+                row = dest_row[p];
+                wv = static_cast<float>(cw[p]);
+                // home slot at the owner (rank == me tells its pass to skip the row)
+                gsrc_tab[r][row] = (static_cast<unsigned long long>(me) << 32) | static_cast<unsigned>(t * k + lane);
+                if (r != me) gw_tab[r][row] = wv;  // the owner finishes this copy (bwd_owner_prep_kernel)
+            }
+            bslot_src[static_cast<size_t>(t) * k + lane] =
+                p >= 0 ? reinterpret_cast<unsigned long long>(dxc_tab[r] + static_cast<size_t>(row) * rb) : 0ull;
+        }
+        const int n = __popc(__ballot_sync(0xffffffffu, lane < k && p >= 0));  // kept copies: a prefix
+        for (int j = 0; j < n; ++j) {
+            const int rj = __shfl_sync(0xffffffffu, r, j);
+            const size_t off = static_cast<size_t>(__shfl_sync(0xffffffffu, row, j)) * rb;
+            if (rj == me) {
+                const float w = __shfl_sync(0xffffffffu, wv, j);
+                const int4* y = reinterpret_cast<const int4*>(eout_tab[me] + off);
+                int4* o = reinterpret_cast<int4*>(dz + off);
+                float dot = 0.f;
+                for (int base = 0; base < nvec; base += 32 * kBsVec) {
+                    int4 e[kBsVec];
+#pragma unroll
+                    for (int u = 0; u < kBsVec; ++u) {
+                        const int c = base + lane + 32 * u;
+                        if (!one_pass) v[u] = c < nvec ? ld_nc_v4(src + c) : make_int4(0, 0, 0, 0);
+                        e[u] = c < nvec ? ld_nc_v4(y + c) : make_int4(0, 0, 0, 0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kBsVec; ++u) {
+                        const int c = base + lane + 32 * u;
+                        if (c >= nvec) continue;
+                        const uint32_t ua[4] = {static_cast<uint32_t>(v[u].x), static_cast<uint32_t>(v[u].y),
+                                                static_cast<uint32_t>(v[u].z), static_cast<uint32_t>(v[u].w)};
+                        const uint32_t ub[4] = {static_cast<uint32_t>(e[u].x), static_cast<uint32_t>(e[u].y),
+                                                static_cast<uint32_t>(e[u].z), static_cast<uint32_t>(e[u].w)};
+                        uint32_t uo[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            dot = fmaf(bf16_lo(ua[q]), bf16_lo(ub[q]), dot);
+                            dot = fmaf(bf16_hi(ua[q]), bf16_hi(ub[q]), dot);
+                            uo[q] = pack_bf16(w * bf16_lo(ua[q]), w * bf16_hi(ua[q]));
+                        }
+                        st_na_v4(o + c, make_int4(static_cast<int>(uo[0]), static_cast<int>(uo[1]),
+                                                  static_cast<int>(uo[2]), static_cast<int>(uo[3])));
+                    }
+                }
+#pragma unroll
+                for (int s = 16; s > 0; s >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, s);
+                if (lane == 0) slot_dw[static_cast<size_t>(t) * k + j] = dot;
+            } else {
+                int4* d = reinterpret_cast<int4*>(dyg_tab[rj] + off);
+                for (int base = 0; base < nvec; base += 32 * kBsVec) {
+#pragma unroll
+                    for (int u = 0; u < kBsVec; ++u) {
+                        const int c = base + lane + 32 * u;
+                        if (!one_pass) v[u] = c < nvec ? ld_nc_v4(src + c) : make_int4(0, 0, 0, 0);
+                        if (c < nvec) st_na_v4(d + c, v[u]);
+                    }
+                }
+            }
+        }
+    }
+    __threadfence_system();  // peer (NVLink) stores complete before the rank barrier
 }
 
 // Per-group K padding for the wgrad GEMMs: kpg[g] = roundup(rows_g, 64),
@@ -192,11 +294,25 @@ static int warp_grid(long long items) {
 
 void launch_bwd_owner_prep(const void* dyg, const void* eout, const float* gw, const unsigned long long* gsrc,
                            const int32_t* rpe, int El, int H, long long max_rows, float* const* slotdw_tab,
-                           void* dz, cudaStream_t st) {
+                           void* dz, int me, cudaStream_t st) {
     require(H % 8 == 0, XMOE_ERR_VALIDATION, "backward requires model_dim % 8 == 0");
     bwd_owner_prep_kernel<<<warp_grid(max_rows), 256, 0, st>>>(
         static_cast<const __nv_bfloat16*>(dyg), static_cast<const __nv_bfloat16*>(eout), gw, gsrc, rpe, El, H,
-        slotdw_tab, static_cast<__nv_bfloat16*>(dz));
+        slotdw_tab, static_cast<__nv_bfloat16*>(dz), me);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_bwd_scatter_dy(const void* dy, int H, int S, int k, const int32_t* slot_pos, const int32_t* dest_rank,
+                           const int32_t* dest_row, const double* cw, int me, void* dz, char* const* eout_tab,
+                           char* const* dyg_tab, char* const* dxc_tab, float* const* gw_tab,
+                           unsigned long long* const* gsrc_tab, float* slot_dw, unsigned long long* bslot_src,
+                           cudaStream_t st) {
+    require(H % 8 == 0 && k <= 32, XMOE_ERR_VALIDATION, "backward requires model_dim % 8 == 0, top_k <= 32");
+    if (S == 0) return;
+    const long long blocks = (static_cast<long long>(S) + 7) / 8;
+    bwd_scatter_dy_kernel<<<static_cast<int>(blocks < 8LL * kNumSMs ? blocks : 8LL * kNumSMs), 256, 0, st>>>(
+        static_cast<const char*>(dy), H, S, k, slot_pos, dest_rank, dest_row, cw, me, static_cast<char*>(dz),
+        eout_tab, dyg_tab, dxc_tab, gw_tab, gsrc_tab, slot_dw, bslot_src);
     XMOE_LAUNCH_CHECK();
 }
 

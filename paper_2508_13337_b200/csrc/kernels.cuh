@@ -93,7 +93,12 @@ void launch_grouped_gemm_bf16_f32out(const void* A, long long rows, int K,
 // backward.cu
 void launch_bwd_owner_prep(const void* dyg, const void* eout, const float* gw, const unsigned long long* gsrc,
                            const int32_t* rpe, int El, int H, long long max_rows, float* const* slotdw_tab,
-                           void* dz, cudaStream_t st);
+                           void* dz, int me, cudaStream_t st);
+void launch_bwd_scatter_dy(const void* dy, int H, int S, int k, const int32_t* slot_pos, const int32_t* dest_rank,
+                           const int32_t* dest_row, const double* cw, int me, void* dz, char* const* eout_tab,
+                           char* const* dyg_tab, char* const* dxc_tab, float* const* gw_tab,
+                           unsigned long long* const* gsrc_tab, float* slot_dw, unsigned long long* bslot_src,
+                           cudaStream_t st);
 void launch_pad_offsets(const int32_t* rows, int G, int32_t* kpg, int32_t* koff, int32_t* roff, cudaStream_t st);
 void launch_transpose_pad(const void* in, int C, const int32_t* rows, const int32_t* koff, const int32_t* roff,
                           int G, long long ld, void* out, cudaStream_t st);

@@ -936,7 +936,8 @@ void Layer::exchange_nccl(bool forward, cudaStream_t st) {
 // Gradient of the last forward (bf16, pointer-table transports).  Per rank:
 //   B1 dy rows to the owners (token-major, read once), each copy's weight and
 //      home slot recorded at the owner
-//   B2 owner: dL/dw_c = <dy_t, y_c> back to the home slot; dz = w_c dy_t
+//   B2 dL/dw_c = <dy_t, y_c> to the home slot; dz = w_c dy_t — at the source
+//      for copies this rank owns (fused into B1), at the owner for the rest
 //   B3 dgrad: dH = (dz W2^T) * [mid > 0];  dxc = dH W1^T      (grouped-M)
 //   B4 wgrad: dW1_e = x_e^T dH_e, dW2_e = a_e^T dz_e   (grouped-K, MN-major
 //      operands read straight from the grouped buffers)
@@ -991,16 +992,18 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
     }
     for (int i = 0; i < L.nl; ++i) {  // B1
         Worker& w = L.workers[i];
-        TrainTabs tr{L.gw_tab, L.gsrc_tab, w.rank};
-        launch_scatter_tokens(xo(dy, i), static_cast<int>(rb), static_cast<int>(S), k, w.slot_pos, w.dest_rank,
-                              w.dest_row, w.cw, L.dyg_tab, L.dxc_tab, w.bslot_src, nullptr, st, tr);
+        launch_bwd_scatter_dy(xo(dy, i), H, static_cast<int>(S), k, w.slot_pos, w.dest_rank, w.dest_row, w.cw,
+                              w.rank, w.dz, L.eout_tab, L.dyg_tab, L.dxc_tab, L.gw_tab, L.gsrc_tab, w.slot_dw,
+                              w.bslot_src, st);
     }
     if (dist) L.barrier(st);
     bmark(kBwScatter);
     for (int i = 0; i < L.nl; ++i) {  // B2-B4 at the owner
         Worker& w = L.workers[i];
         const size_t eo = dist ? 0 : static_cast<size_t>(w.rank) * El * H * F * L.es;
-        launch_bwd_owner_prep(w.dyg, w.eout, w.gw, w.gsrc, w.rpe, El, H, L.R_max, L.slotdw_tab, w.dz, st);
+        if (W > 1)  // copies from peers (this rank's own were finished at the source)
+            launch_bwd_owner_prep(w.dyg, w.eout, w.gw, w.gsrc, w.rpe, El, H, L.R_max, L.slotdw_tab, w.dz, w.rank,
+                                  st);
         bmark(kBwPrep);
         launch_grouped_gemm_bf16_mask(w.dz, L.R_max, H, w.rpe, El, static_cast<const char*>(L.w2r) + eo, F, w.dH,
                                       w.mbits, st);
