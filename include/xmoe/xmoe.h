@@ -153,6 +153,14 @@ int xmoe_grouped_wgrad_bf16(xmoe_ctx* ctx, const void* X, const void* Y, int64_t
                              const int32_t* rows_per_group, int64_t G, int64_t M, int64_t N, float* D,
                              void* stream);
 
+/* One weight gradient D [M,N] = X^T Y (BF16 in, fp32 out) over all `rows` of
+ * X [rows,M] and Y [rows,N], split along the rows into `splits` (1..32)
+ * segments whose fp32 partials are summed in segment order (deterministic).
+ * M % 64 == 0, N % 8 == 0 (N is padded to 128 inside; the padding reads as
+ * zeros).  This is the layer's shared-expert and gate weight gradient. */
+int xmoe_wgrad_split_bf16(xmoe_ctx* ctx, const void* X, const void* Y, int64_t rows, int64_t M, int64_t N,
+                          int64_t splits, float* D, void* stream);
+
 /* ------------------------------------------------------------------ layer
  * One MoE layer's weights resident in HBM in the B200 layout, plus the
  * workspace of its forward pass.  Weights are DEVICE pointers in the

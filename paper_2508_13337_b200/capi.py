@@ -104,6 +104,7 @@ def lib():
         L.xmoe_plan_dispatch.argtypes = [i32, i32, p, i32, p, p, p]
         L.xmoe_moe_backward.argtypes = [p, p, p, p, i64, p, p]
         L.xmoe_grouped_wgrad_bf16.argtypes = [p, p, p, i64, p, i64, i64, i64, p, p]
+        L.xmoe_wgrad_split_bf16.argtypes = [p, p, p, i64, i64, i64, i64, p, p]
         L.xmoe_layer_grads.argtypes = [p] + [C.POINTER(p)] * 5
         _LIB = L
     return _LIB
@@ -151,6 +152,14 @@ def grouped_wgrad_test(ctx, X, Y, rows_per_group):
     D = torch.empty((G, X.shape[1], Y.shape[1]), dtype=torch.float32, device=X.device)
     _check(lib().xmoe_grouped_wgrad_bf16(ctx.h, _ptr(X), _ptr(Y), X.shape[0], _ptr(rpg), G, X.shape[1],
                                          Y.shape[1], _ptr(D), _stream()))
+    return D
+
+
+def wgrad_split_test(ctx, X, Y, splits):
+    """D = X^T Y (fp32) over all rows, split-K, through xmoe_wgrad_split_bf16."""
+    D = torch.empty((X.shape[1], Y.shape[1]), dtype=torch.float32, device=X.device)
+    _check(lib().xmoe_wgrad_split_bf16(ctx.h, _ptr(X), _ptr(Y), X.shape[0], X.shape[1], Y.shape[1], splits,
+                                       _ptr(D), _stream()))
     return D
 
 

@@ -296,6 +296,23 @@ int xmoe_grouped_wgrad_bf16(xmoe_ctx* ctx, const void* X, const void* Y, int64_t
     });
 }
 
+int xmoe_wgrad_split_bf16(xmoe_ctx* ctx, const void* X, const void* Y, int64_t rows, int64_t M, int64_t N,
+                          int64_t splits, float* D, void* stream) {
+    return guarded([&] {
+        require(rows >= 0 && M > 0 && N > 0, XMOE_ERR_VALIDATION, "split wgrad: rows >= 0, M > 0, N > 0");
+        require(M % 64 == 0, XMOE_ERR_VALIDATION, "split wgrad: M % 64 == 0");
+        const long long Np = (N + 127) / 128 * 128;
+        const size_t tails = 2 * 64 * static_cast<size_t>(splits) * (M + N);
+        const size_t part = sizeof(float) * static_cast<size_t>(splits) * M * Np;
+        char* ws = static_cast<char*>(ctx->c.scratch(256 + tails + part + 1024));
+        char* ta = ws + 256;
+        char* tb = ta + 2 * 64 * splits * M;
+        float* pp = reinterpret_cast<float*>(ws + 256 + (tails + 255) / 256 * 256);
+        launch_wgrad_mn_split(X, static_cast<int>(M), Y, static_cast<int>(N), rows, static_cast<int>(splits),
+                              reinterpret_cast<int32_t*>(ws), ta, tb, pp, D, static_cast<cudaStream_t>(stream));
+    });
+}
+
 int xmoe_layer_create(xmoe_ctx* ctx, const xmoe_layer_desc* desc, const void* gate,
                       const void* w1, const void* w2, const void* sw1, const void* sw2,
                       xmoe_layer** out) {

@@ -751,12 +751,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     for (int c = 0; c < nw; ++c) drow[c] = static_cast<OutT>(0.f);
                 continue;
             }
-            mbar_wait(&tfull_bar[acc], acc_phase);
-            tc_fence_after();
-            // ReLU masks as bits: one word per (row, 32 columns), ceil(N/32) words per row
+            // ReLU masks as bits: one word per (row, 32 columns), ceil(N/32) words per row;
+            // the tile's words are loaded before the accumulator wait (off the critical path)
             const int mwords = (N + 31) >> 5;
             const uint32_t* mrow = mbits_in ? mbits_in + static_cast<size_t>(ti.row0 + r) * mwords + (ti.n0 >> 5)
                                             : nullptr;
+            uint32_t mpre[BN / 32];
+#pragma unroll
+            for (int q = 0; q < BN / 32; ++q) mpre[q] = (mrow && row_ok && 32 * q < nw) ? __ldg(mrow + q) : 0u;
+            auto mask_word = [&](int c0) {
+                uint32_t mw = mpre[0];
+#pragma unroll
+                for (int q = 1; q < BN / 32; ++q)
+                    if ((c0 >> 5) == q) mw = mpre[q];
+                return mw;
+            };
+            mbar_wait(&tfull_bar[acc], acc_phase);
+            tc_fence_after();
             uint32_t* orow = mbits_out ? mbits_out + static_cast<size_t>(ti.row0 + r) * mwords + (ti.n0 >> 5)
                                        : nullptr;
             uint32_t* etile = reinterpret_cast<uint32_t*>(smem + kEpiOff + (warp - 2) * kEpiWarpBytes);
@@ -779,7 +790,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                     const int cn = min(32, nw - c0);
                     if (mrow && row_ok) {
-                        const uint32_t mw = mrow[c0 >> 5];
+                        const uint32_t mw = mask_word(c0);
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
                             if (!((mw >> i) & 1u)) f[i] = 0.f;
@@ -798,7 +809,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 const int cn = min(32, nw - c0);
                 if (mrow) {
-                    const uint32_t mw = mrow[c0 >> 5];
+                    const uint32_t mw = mask_word(c0);
 #pragma unroll
                     for (int i = 0; i < 32; ++i)
                         if (!((mw >> i) & 1u)) f[i] = 0.f;
@@ -901,7 +912,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     grouped_wgrad_mn_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                             const __grid_constant__ CUtensorMap tmap_at, const __grid_constant__ CUtensorMap tmap_bt,
                             const int32_t* __restrict__ group_rows, int G, int M, int N, float* __restrict__ D,
-                            int coalesced, const __grid_constant__ CUtensorMap tmap_d, int tma_store) {
+                            int coalesced, const __grid_constant__ CUtensorMap tmap_d, int tma_store,
+                            int transpose_out) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -1069,6 +1081,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 uint32_t v[32];
                 tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN + c0),
                           v);
+                if (transpose_out) {
+                    // D_g^T: output row n holds the M values of column n ([G, N, M]);
+                    // lane l (row m = l of the warp) writes element (n = i, m = l)
+                    if (tma_store) {
+                        // 32 (n) x 32 (m) box, 128B-swizzled, stored by TMA (map [G*N, M])
+                        if (lane == 0) tma_store_wait_read();
+                        __syncwarp();
+                        uint8_t* tb = reinterpret_cast<uint8_t*>(etile);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            *reinterpret_cast<uint32_t*>(tb + i * 128 + ((((lane >> 2) ^ (i & 7))) << 4) +
+                                                         (lane & 3) * 4) = v[i];
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0) tma_store_2d(&tmap_d, etile, row0 + wrow, g * N + n0 + c0);
+                    } else if (row_ok) {
+                        const int cn = min(32, nw - c0);
+                        float* dt = D + static_cast<size_t>(g) * M * N + static_cast<size_t>(n0 + c0) * M + row0 + r;
+                        for (int i = 0; i < cn; ++i) dt[static_cast<size_t>(i) * M] = __uint_as_float(v[i]);
+                    }
+                    continue;
+                }
                 if (tma_store) {
                     // 32 x 32 fp32 box through 128B-swizzled smem, stored by TMA
                     // (the D map is [G*M, N]; M % 256 == 0, so a box never
@@ -1148,6 +1182,40 @@ __global__ void wgrad_tail_kernel(const __nv_bfloat16* __restrict__ X, int C, co
         for (int v = threadIdx.x; v < nv; v += blockDim.x) dst[v] = src[v];
     } else {
         for (int v = threadIdx.x; v < nv; v += blockDim.x) dst[v] = make_int4(0, 0, 0, 0);
+    }
+}
+
+// Split-K of one long reduction into `splits` row groups (each a multiple of
+// 64 rows but the last), so a single-group weight gradient with few output
+// tiles (shared experts, gate) fills every SM pair.
+__global__ void split_rows_kernel(int rows, int splits, int32_t* __restrict__ out) {
+    const int g = threadIdx.x;
+    if (g >= splits) return;
+    const int per = ((rows + splits - 1) / splits + 63) & ~63;
+    const int r0 = min(rows, g * per);
+    out[g] = min(rows, r0 + per) - r0;
+}
+
+// D[m, n] = sum over s ascending of P[s, m, n] for n < Nv (P row stride N);
+// four columns per thread (Nv % 4 == 0, N % 4 == 0).
+__global__ void __launch_bounds__(256) sum_partials_kernel(const float* __restrict__ P, int splits, int M, int N,
+                                                           int Nv, float* __restrict__ D) {
+    const int nq = Nv >> 2;
+    const long long total = static_cast<long long>(M) * nq;
+    const size_t plane = static_cast<size_t>(M) * N;
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int m = static_cast<int>(i / nq), c = static_cast<int>(i % nq) * 4;
+        const float* p = P + static_cast<size_t>(m) * N + c;
+        float4 acc = __ldg(reinterpret_cast<const float4*>(p));
+        for (int sp = 1; sp < splits; ++sp) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(p + sp * plane));
+            acc.x += v.x;
+            acc.y += v.y;
+            acc.z += v.z;
+            acc.w += v.w;
+        }
+        *reinterpret_cast<float4*>(D + static_cast<size_t>(m) * Nv + c) = acc;
     }
 }
 
@@ -1349,28 +1417,33 @@ void launch_grouped_wgrad_bf16(const void* A, int M, long long Ktot, const int32
 }
 
 // MN-major grouped weight gradient straight on the grouped activations.
-void launch_grouped_wgrad_mn(const void* A, int M, const void* B, int N, long long rows,
-                             const int32_t* group_rows, int G, void* tail_a, void* tail_b, float* D,
-                             cudaStream_t st) {
+// B has b_cols physical columns (b_cols <= N); columns past them read as
+// zeros (TMA out-of-bounds fill), so N may be padded up to a multiple of 128.
+static void wgrad_mn_impl(const void* A, int M, const void* B, int N, int b_cols, long long rows,
+                          const int32_t* group_rows, int G, void* tail_a, void* tail_b, float* D, cudaStream_t st,
+                          bool transpose_out = false) {
     require(G >= 1 && G <= tc2::kMaxGroups, XMOE_ERR_VALIDATION, "wgrad: 1 <= groups <= 1024");
     require(M % 64 == 0 && N % 128 == 0, XMOE_ERR_VALIDATION, "wgrad (MN-major) needs M % 64 == 0, N % 128 == 0");
+    require(b_cols % 8 == 0 && b_cols <= N, XMOE_ERR_VALIDATION, "wgrad (MN-major): B columns % 8 == 0, <= N");
     tc2::wgrad_tail_kernel<<<dim3(G, 64), 128, 0, st>>>(static_cast<const __nv_bfloat16*>(A), M, group_rows, G,
                                                         static_cast<__nv_bfloat16*>(tail_a));
     XMOE_LAUNCH_CHECK();
-    tc2::wgrad_tail_kernel<<<dim3(G, 64), 128, 0, st>>>(static_cast<const __nv_bfloat16*>(B), N, group_rows, G,
+    tc2::wgrad_tail_kernel<<<dim3(G, 64), 128, 0, st>>>(static_cast<const __nv_bfloat16*>(B), b_cols, group_rows, G,
                                                         static_cast<__nv_bfloat16*>(tail_b));
     XMOE_LAUNCH_CHECK();
     const long long r = rows > 0 ? rows : 1;
     const CUtensorMap ta = make_tmap(A, r, M, 64);
-    const CUtensorMap tb = make_tmap(B, r, N, 64);
+    const CUtensorMap tb = make_tmap(B, r, b_cols, 64);
     const CUtensorMap tat = make_tmap(tail_a, 64LL * G, M, 64);
-    const CUtensorMap tbt = make_tmap(tail_b, 64LL * G, N, 64);
+    const CUtensorMap tbt = make_tmap(tail_b, 64LL * G, b_cols, 64);
     // fp32 D [G*M, N] for the TMA-store epilogue: boxes of 32 x 32, 128B swizzle
+    // (transposed: D_g^T, map [G*N, M])
     const bool tma_store = wgrad_tma_store() && M % tc2::BM == 0 && N % 32 == 0;
     CUtensorMap td{};
     if (tma_store) {
-        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(G) * M};
-        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(N) * 4};
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(transpose_out ? M : N),
+                                    static_cast<cuuint64_t>(G) * (transpose_out ? N : M)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(transpose_out ? M : N) * 4};
         const cuuint32_t box[2] = {32, 32};
         const cuuint32_t estr[2] = {1, 1};
         const CUresult r = get_encode()(&td, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, D, dims, strides, box, estr,
@@ -1389,7 +1462,44 @@ void launch_grouped_wgrad_mn(const void* A, int M, const void* B, int N, long lo
     const long long tiles = static_cast<long long>(G) * ((M + tc2::BM - 1) / tc2::BM) * ((N + tc2::BN - 1) / tc2::BN);
     const long long pairs = tiles < sms / 2 ? tiles : sms / 2;
     tc2::grouped_wgrad_mn_kernel<<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
-        ta, tb, tat, tbt, group_rows, G, M, N, D, epi_coalesced(), td, tma_store ? 1 : 0);
+        ta, tb, tat, tbt, group_rows, G, M, N, D, epi_coalesced(), td, tma_store ? 1 : 0, transpose_out ? 1 : 0);
+    XMOE_LAUNCH_CHECK();
+}
+
+// D_g^T [N, M] = (A_g^T B_g)^T: the same product written transposed, so that
+// an output with few rows (M) and many columns runs as M = the long side
+// (whole 256-row tiles) — the routed W2 gradient, M = H, N = F.
+void launch_grouped_wgrad_mn_t(const void* A, int M, const void* B, int N, long long rows,
+                               const int32_t* group_rows, int G, void* tail_a, void* tail_b, float* D,
+                               cudaStream_t st) {
+    wgrad_mn_impl(A, M, B, N, N, rows, group_rows, G, tail_a, tail_b, D, st, true);
+}
+
+void launch_grouped_wgrad_mn(const void* A, int M, const void* B, int N, long long rows,
+                             const int32_t* group_rows, int G, void* tail_a, void* tail_b, float* D,
+                             cudaStream_t st) {
+    wgrad_mn_impl(A, M, B, N, N, rows, group_rows, G, tail_a, tail_b, D, st);
+}
+
+// One weight gradient D[M, Nb] = A^T B over all `rows` (A [rows, M], B
+// [rows, Nb], bf16, MN-major), split into `splits` K segments whose fp32
+// partials ([splits, M, roundup(Nb, 128)] in `partial`) are summed in order
+// (deterministic).  tails: 64 * splits rows of M and of Nb columns;
+// split_rows: `splits` ints of device scratch.
+void launch_wgrad_mn_split(const void* A, int M, const void* B, int Nb, long long rows, int splits,
+                           int32_t* split_rows, void* tail_a, void* tail_b, float* partial, float* D,
+                           cudaStream_t st) {
+    require(splits >= 1 && splits <= 32 && rows < (1LL << 31), XMOE_ERR_VALIDATION,
+            "split wgrad: 1 <= splits <= 32, rows < 2^31");
+    require(Nb % 8 == 0, XMOE_ERR_VALIDATION, "split wgrad: columns % 8 == 0");
+    const int N = (Nb + 127) / 128 * 128;
+    tc2::split_rows_kernel<<<1, 32, 0, st>>>(static_cast<int>(rows), splits, split_rows);
+    XMOE_LAUNCH_CHECK();
+    wgrad_mn_impl(A, M, B, N, Nb, rows, split_rows, splits, tail_a, tail_b, partial, st);
+    const long long quads = static_cast<long long>(M) * (Nb / 4);
+    long long blocks = (quads + 255) / 256;
+    if (blocks > 8 * kNumSMs) blocks = 8 * kNumSMs;
+    tc2::sum_partials_kernel<<<static_cast<int>(blocks < 1 ? 1 : blocks), 256, 0, st>>>(partial, splits, M, N, Nb, D);
     XMOE_LAUNCH_CHECK();
 }
 

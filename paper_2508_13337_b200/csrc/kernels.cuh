@@ -86,6 +86,12 @@ void launch_grouped_wgrad_bf16(const void* A, int M, long long Ktot, const int32
 void launch_grouped_wgrad_mn(const void* A, int M, const void* B, int N, long long rows,
                              const int32_t* group_rows, int G, void* tail_a, void* tail_b, float* D,
                              cudaStream_t st);
+void launch_grouped_wgrad_mn_t(const void* A, int M, const void* B, int N, long long rows,
+                               const int32_t* group_rows, int G, void* tail_a, void* tail_b, float* D,
+                               cudaStream_t st);
+void launch_wgrad_mn_split(const void* A, int M, const void* B, int Nb, long long rows, int splits,
+                           int32_t* split_rows, void* tail_a, void* tail_b, float* partial, float* D,
+                           cudaStream_t st);
 void launch_grouped_gemm_bf16_f32out(const void* A, long long rows, int K,
                                      const int32_t* rows_per_group, int G, const void* B, int N,
                                      float* D, int relu, cudaStream_t st);

@@ -38,6 +38,21 @@ namespace xmoe {
             ::xmoe::fail(XMOE_ERR_NCCL, std::string(#expr ": ") + ncclGetErrorString(_r)); \
     } while (0)
 
+// Split-K factor of a single-group weight gradient D[M, N] over `rows`
+// tokens: the fewest splits whose tiles fill >= 85 % of the last round of
+// the 74 SM pairs (at most 16, and at least 512 rows per split).
+static int wgrad_splits(long long M, long long N, long long rows) {
+    const long long pairs = kNumSMs / 2;
+    const long long tiles = ((M + 255) / 256) * (((N + 127) / 128 * 128 + 255) / 256);
+    int s = 1;
+    for (; s < 16; ++s) {
+        const long long t = tiles * s;
+        if (static_cast<double>(t) / (static_cast<double>((t + pairs - 1) / pairs) * pairs) >= 0.85) break;
+    }
+    while (s > 1 && rows / s < 512) --s;
+    return s;
+}
+
 static size_t elem_size_of(int dtype) { return dtype == XMOE_F64 ? 8 : 2; }
 
 Layer::~Layer() {
@@ -336,14 +351,27 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
             // ReLU masks of the forward's first GEMMs (bits), the dgrad's masks
             w.mbits = static_cast<uint32_t*>(L.alloc(sizeof(uint32_t) * L.R_max * ((F + 31) / 32)));
             if (Fs > 0) w.smbits = static_cast<uint32_t*>(L.alloc(sizeof(uint32_t) * S * ((Fs + 31) / 32)));
-            w.tail_sa = L.alloc(64 * 2 * wide * es);  // side-stream (shared-expert wgrad) copies
-            w.tail_sb = L.alloc(64 * 2 * wide * es);
+            // single-group weight gradients, split along the tokens (K) so
+            // that their few output tiles fill the SM pairs
+            L.splits_s1 = wgrad_splits(H, static_cast<int>(Fs), S);
+            L.splits_s2 = wgrad_splits(static_cast<int>(Fs), H, S);
+            L.splits_g = wgrad_splits(H, E, S);
+            const int ss = std::max(L.splits_s1, L.splits_s2);
+            w.tail_sa = L.alloc(64 * static_cast<size_t>(std::max(ss, 2)) * wide * es);  // side-stream copies
+            w.tail_sb = L.alloc(64 * static_cast<size_t>(std::max(ss, 2)) * wide * es);
+            w.split_s = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * 32));
+            w.split_g = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * 32));
+            const auto r128 = [](long long n) { return (n + 127) / 128 * 128; };
+            if (Fs > 0)
+                w.part_s = static_cast<float*>(L.alloc(sizeof(float) * ss *
+                                                       std::max(H * r128(Fs), Fs * r128(H))));
+            w.part_g = static_cast<float*>(L.alloc(sizeof(float) * L.splits_g * H * r128(E)));
+            w.tail_ga = L.alloc(64 * static_cast<size_t>(L.splits_g) * H * es);
+            w.tail_gb = L.alloc(64 * static_cast<size_t>(L.splits_g) * E * es);
             w.kpg = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
             w.koff = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
             w.roff = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
             w.tk = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * 8));
-            w.xTt = L.alloc(static_cast<size_t>(H) * L.Sp * es);
-            w.dlT = L.alloc(static_cast<size_t>(E) * L.Sp * es);
             w.dl = L.alloc(static_cast<size_t>(S) * E * es);
             w.dxg = L.alloc(static_cast<size_t>(S) * H * es);
             if (Fs > 0) {
@@ -969,12 +997,13 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
     auto token_level = [&](cudaStream_t ss) {
         for (int i = 0; i < L.nl; ++i) {
             Worker& w = L.workers[i];
-            launch_transpose_pad(xo(x, i), H, w.tk, w.tk + 2, w.tk + 4, 1, L.Sp, w.xTt, ss);
             if (L.Fs > 0) {
                 launch_grouped_gemm_bf16_mask(xo(dy, i), S, H, w.s_rows, 1, L.sw2r, L.Fs, w.dHs, w.smbits, ss);
                 launch_grouped_gemm_bf16(w.dHs, S, L.Fs, w.s_rows, 1, L.sw1r, H, w.dxs, 0, ss);
-                launch_grouped_wgrad_mn(xo(x, i), H, w.dHs, L.Fs, S, w.tk, 1, w.tail_sa, w.tail_sb, L.dsw1, ss);
-                launch_grouped_wgrad_mn(w.smid, L.Fs, xo(dy, i), H, S, w.tk, 1, w.tail_sa, w.tail_sb, L.dsw2, ss);
+                launch_wgrad_mn_split(xo(x, i), H, w.dHs, L.Fs, S, L.splits_s1, w.split_s, w.tail_sa, w.tail_sb,
+                                      w.part_s, L.dsw1, ss);
+                launch_wgrad_mn_split(w.smid, L.Fs, xo(dy, i), H, S, L.splits_s2, w.split_s, w.tail_sa, w.tail_sb,
+                                      w.part_s, L.dsw2, ss);
             }
         }
     };
@@ -1012,7 +1041,8 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
         // wgrad straight on the grouped activations (MN-major tcgen05 operands)
         const size_t go = dist ? 0 : static_cast<size_t>(w.rank) * El * H * F;
         launch_grouped_wgrad_mn(w.recv, H, w.dH, F, L.R_max, w.rpe, El, w.tail_a, w.tail_b, L.dw1 + go, st);
-        launch_grouped_wgrad_mn(w.mid, F, w.dz, H, L.R_max, w.rpe, El, w.tail_a, w.tail_b, L.dw2 + go, st);
+        // dW2_e [F, H] as (dz_e^T mid_e)^T: M = H fills whole 256-row tiles
+        launch_grouped_wgrad_mn_t(w.dz, H, w.mid, F, L.R_max, w.rpe, El, w.tail_a, w.tail_b, L.dw2 + go, st);
     }
     bmark(kBwWgrad);
     if (L.timing) token_level(st);
@@ -1023,9 +1053,9 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
         launch_gate_bwd(reinterpret_cast<const float*>(w.logits), w.slot_pos, w.expert_ids, w.slot_dw,
                         static_cast<int>(S), E, k, w.dl, st);
         launch_grouped_gemm_bf16(w.dl, S, E, w.s_rows, 1, L.gater, H, w.dxg, 0, st);
-        launch_transpose_pad(w.dl, E, w.tk, w.tk + 2, w.tk + 4, 1, L.Sp, w.dlT, st);
-        if (i == 0 && !L.timing) XMOE_CUDA(cudaStreamWaitEvent(st, L.ev_join, 0));  // xTt, dxs
-        launch_grouped_wgrad_bf16(w.xTt, H, L.Sp, w.tk + 1, 1, w.dlT, E, L.dgate, st);
+        launch_wgrad_mn_split(xo(x, i), H, w.dl, E, S, L.splits_g, w.split_g, w.tail_ga, w.tail_gb, w.part_g,
+                              L.dgate, st);
+        if (i == 0 && !L.timing) XMOE_CUDA(cudaStreamWaitEvent(st, L.ev_join, 0));  // dxs
         launch_combine_slots(w.bslot_src, nullptr, k, H, static_cast<int>(S), L.Fs > 0 ? w.dxs : nullptr,
                              static_cast<char*>(dx) + static_cast<size_t>(i) * S * rb, st, 0, w.dxg);
     }

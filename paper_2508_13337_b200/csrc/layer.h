@@ -81,8 +81,14 @@ struct Worker {
     int32_t* koff = nullptr;      // [El+1]
     int32_t* roff = nullptr;      // [El+1]
     int32_t* tk = nullptr;        // token-level (one group of S rows): kpg, koff, roff
-    void* xTt = nullptr;          // [H, Sp]
-    void* dlT = nullptr;          // [E, Sp]
+    // split-K weight gradients of the single-group (token-level) products:
+    // shared experts on the side stream (_s), the gate on the layer stream (_g)
+    int32_t* split_s = nullptr;   // [32] rows per split
+    int32_t* split_g = nullptr;
+    float* part_s = nullptr;      // [splits, M, roundup(N, 128)] fp32 partials
+    float* part_g = nullptr;
+    void* tail_ga = nullptr;      // [64*splits_g, H], [64*splits_g, E]
+    void* tail_gb = nullptr;
     void* dl = nullptr;           // [S, E]
     void* dxg = nullptr;          // [S, H] gate part of dx
     void* dHs = nullptr;          // [S, Fs]
@@ -139,6 +145,7 @@ struct Layer {
     void* sw1r = nullptr;  // [H, Fs] merged
     void* sw2r = nullptr;  // [Fs, H]
     float* dgate = nullptr;
+    int splits_s1 = 1, splits_s2 = 1, splits_g = 1;  // split-K factors (wgrad_splits)
     float* dw1 = nullptr;
     float* dw2 = nullptr;
     float* dsw1 = nullptr;

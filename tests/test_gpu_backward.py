@@ -68,3 +68,24 @@ def test_grouped_wgrad_kernel(H, F):
         err = (out[g] - ref).norm() / max(ref.norm().item(), 1e-30)
         assert (n == 0 and out[g].abs().max() == 0) or err < 1e-3, (g, float(err))
         off += n
+
+
+@pytest.mark.parametrize("rows,M,N,splits", [(16384, 2048, 64, 8), (5000, 256, 2816, 3), (777, 128, 200, 5),
+                                             (100, 64, 128, 4), (0, 64, 64, 2)])
+def test_wgrad_split_kernel(rows, M, N, splits):
+    """Split-K single-group weight gradient (shared experts, gate): zero-filled
+    column padding past N, ragged last split, splits with no rows, rows = 0."""
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, 1, 0)
+    torch.manual_seed(rows + N)
+    x = (torch.randn(rows, M, device="cuda") * 0.5).to(torch.bfloat16)
+    y = (torch.randn(rows, N, device="cuda") * 0.5).to(torch.bfloat16)
+    out = capi.wgrad_split_test(ctx, x, y, splits)
+    ref = x.float().T @ y.float()
+    if rows == 0:
+        assert out.abs().max().item() == 0
+    else:
+        err = (out - ref).norm() / ref.norm()
+        assert err < 1e-3, float(err)
+    again = capi.wgrad_split_test(ctx, x, y, splits)
+    assert torch.equal(out, again)  # deterministic (ordered partial sums)
