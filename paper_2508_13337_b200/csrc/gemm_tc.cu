@@ -492,6 +492,52 @@ __device__ __forceinline__ void mma2(uint32_t tmem_d, uint64_t da, uint64_t db, 
         "l"(da), "l"(db), "r"(idesc), "r"(acc)
         : "memory");
 }
+// One K block (BK = 64 = four K=16 MMAs) issued from ONE thread in one asm
+// block, followed by the commit that frees the smem stage in both CTAs.
+// Descriptor start addresses advance by INC (16-byte units) per MMA: 2 for
+// K-major operands (32 B per 16 K-columns), 128 for MN-major (2 KB per 16
+// K-rows).  Keeping the four MMAs and the commit in one block lets the
+// compiler move the operands to uniform registers once per K block instead
+// of electing and broadcasting per instruction (the issue loop, not the
+// tensor pipe, was the limit: ncu showed the MMA warp never waiting on data).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t e;
+    asm volatile(
+        "{\n"
+        ".reg .b32 rx;\n"
+        ".reg .pred px;\n"
+        "elect.sync rx|px, 0xffffffff;\n"
+        "selp.u32 %0, 1, 0, px;\n"
+        "}\n"
+        : "=r"(e));
+    return e != 0;
+}
+static_assert(BK / UK == 4, "mma2_kblock issues four K=16 MMAs per K block");
+template <int INC>
+__device__ __forceinline__ void mma2_kblock(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc,
+                                            uint32_t empty_bar) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, q;\n"
+        ".reg .b64 a1, a2, a3, b1, b2, b3;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "setp.eq.b32 q, 0, 0;\n"
+        "add.s64 a1, %1, %6;\n"
+        "add.s64 b1, %2, %6;\n"
+        "add.s64 a2, %1, %7;\n"
+        "add.s64 b2, %2, %7;\n"
+        "add.s64 a3, %1, %8;\n"
+        "add.s64 b3, %2, %8;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, q;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, q;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, q;\n"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], %9;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(empty_bar), "n"(INC), "n"(2 * INC), "n"(3 * INC),
+        "h"(static_cast<uint16_t>(0x3))
+        : "memory");
+}
 __device__ __forceinline__ void commit_both(uint64_t* bar) {
     const uint16_t mask = 0x3;
     asm volatile(
@@ -694,7 +740,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        // ===================== MMA issuer (leader CTA) =====================
+        // ===================== MMA issuer (leader CTA; one elected thread issues) =====================
         if (leader) {
             int stage = 0;
             uint32_t phase = 0;
@@ -712,14 +758,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int kb = 0; kb < ti.nkb; ++kb) {
                     mbar_wait(&full_bar[stage], phase);
                     tc_fence_after();
-                    if (lane == 0) {
-                        const uint64_t da = make_desc(smem_u32(smem_a + stage * kABytes));
-                        const uint64_t db = make_desc(smem_u32(smem_b + stage * kBBytes));
-#pragma unroll
-                        for (int kk = 0; kk < BK / UK; ++kk)
-                            mma2(tmem_d, da + static_cast<uint64_t>(kk * 2), db + static_cast<uint64_t>(kk * 2),
-                                 idesc, (kb > 0 || kk > 0) ? 1u : 0u);
-                        commit_both(&empty_bar[stage]);
+                    if (elect_one()) {
+                        mma2_kblock<2>(tmem_d, make_desc(smem_u32(smem_a + stage * kABytes)),
+                                       make_desc(smem_u32(smem_b + stage * kBBytes)), idesc, kb > 0 ? 1u : 0u,
+                                       smem_u32(&empty_bar[stage]));
                         if (kb == ti.nkb - 1) commit_both(&tfull_bar[acc]);
                     }
                     __syncwarp();
@@ -1035,14 +1077,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&full_bar[stage], phase);
                     tc_fence_after();
-                    if (lane == 0) {
-                        const uint64_t da = make_desc_mn(smem_u32(smem_a + stage * kABytes));
-                        const uint64_t db = make_desc_mn(smem_u32(smem_b + stage * kBBytes));
-#pragma unroll
-                        for (int kk = 0; kk < BK / UK; ++kk)  // 16 K-rows = 2 KB
-                            mma2(tmem_d, da + static_cast<uint64_t>(kk * 128), db + static_cast<uint64_t>(kk * 128),
-                                 idesc, (kb > 0 || kk > 0) ? 1u : 0u);
-                        commit_both(&empty_bar[stage]);
+                    // 16 K-rows = 2 KB per MMA
+                    if (elect_one()) {
+                        mma2_kblock<128>(tmem_d, make_desc_mn(smem_u32(smem_a + stage * kABytes)),
+                                         make_desc_mn(smem_u32(smem_b + stage * kBBytes)), idesc, kb > 0 ? 1u : 0u,
+                                         smem_u32(&empty_bar[stage]));
                         if (kb == nkb - 1) commit_both(&tfull_bar[acc]);
                     }
                     __syncwarp();
