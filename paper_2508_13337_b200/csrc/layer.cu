@@ -1017,7 +1017,6 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
         g_gemm_sm_limit = side_sms;
         token_level(L.side);
         g_gemm_sm_limit = 0;
-        XMOE_CUDA(cudaEventRecord(L.ev_join, L.side));
     }
     for (int i = 0; i < L.nl; ++i) {  // B1
         Worker& w = L.workers[i];
@@ -1027,7 +1026,7 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
     }
     if (dist) L.barrier(st);
     bmark(kBwScatter);
-    for (int i = 0; i < L.nl; ++i) {  // B2-B4 at the owner
+    for (int i = 0; i < L.nl; ++i) {  // B2-B3 at the owner
         Worker& w = L.workers[i];
         const size_t eo = dist ? 0 : static_cast<size_t>(w.rank) * El * H * F * L.es;
         if (W > 1)  // copies from peers (this rank's own were finished at the source)
@@ -1037,27 +1036,47 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
         launch_grouped_gemm_bf16_mask(w.dz, L.R_max, H, w.rpe, El, static_cast<const char*>(L.w2r) + eo, F, w.dH,
                                       w.mbits, st);
         launch_grouped_gemm_bf16(w.dH, L.R_max, F, w.rpe, El, static_cast<const char*>(L.w1r) + eo, H, w.dxc, 0, st);
-        bmark(kBwDgrad);
-        // wgrad straight on the grouped activations (MN-major tcgen05 operands)
+    }
+    bmark(kBwDgrad);
+    // B5 gate, B6 dx: need every owner's dxc rows and dL/dw home-slot writes
+    // (barrier), not the weight gradients — so outside timing mode they run
+    // on the side stream (after the token-level work queued there) while the
+    // layer stream computes the weight gradients; the dx combine's NVLink
+    // reads overlap the wgrad GEMMs.
+    auto gate_and_dx = [&](cudaStream_t gs) {
+        for (int i = 0; i < L.nl; ++i) {
+            Worker& w = L.workers[i];
+            launch_gate_bwd(reinterpret_cast<const float*>(w.logits), w.slot_pos, w.expert_ids, w.slot_dw,
+                            static_cast<int>(S), E, k, w.dl, gs);
+            launch_grouped_gemm_bf16(w.dl, S, E, w.s_rows, 1, L.gater, H, w.dxg, 0, gs);
+            launch_wgrad_mn_split(xo(x, i), H, w.dl, E, S, L.splits_g, w.split_g, w.tail_ga, w.tail_gb, w.part_g,
+                                  L.dgate, gs);
+            launch_combine_slots(w.bslot_src, nullptr, k, H, static_cast<int>(S), L.Fs > 0 ? w.dxs : nullptr,
+                                 static_cast<char*>(dx) + static_cast<size_t>(i) * S * rb, gs, 0, w.dxg);
+        }
+    };
+    if (dist) L.barrier(st);  // every owner wrote dL/dw and dxc
+    if (!L.timing) {
+        XMOE_CUDA(cudaEventRecord(L.ev_fork, st));
+        XMOE_CUDA(cudaStreamWaitEvent(L.side, L.ev_fork, 0));  // side: token level, then this
+        gate_and_dx(L.side);
+        XMOE_CUDA(cudaEventRecord(L.ev_join, L.side));
+    }
+    for (int i = 0; i < L.nl; ++i) {  // B4 wgrad straight on the grouped activations (MN-major operands)
+        Worker& w = L.workers[i];
         const size_t go = dist ? 0 : static_cast<size_t>(w.rank) * El * H * F;
         launch_grouped_wgrad_mn(w.recv, H, w.dH, F, L.R_max, w.rpe, El, w.tail_a, w.tail_b, L.dw1 + go, st);
         // dW2_e [F, H] as (dz_e^T mid_e)^T: M = H fills whole 256-row tiles
         launch_grouped_wgrad_mn_t(w.dz, H, w.mid, F, L.R_max, w.rpe, El, w.tail_a, w.tail_b, L.dw2 + go, st);
     }
     bmark(kBwWgrad);
-    if (L.timing) token_level(st);
-    bmark(kBwToken);
-    if (dist) L.barrier(st);  // every owner wrote dL/dw and dxc
-    for (int i = 0; i < L.nl; ++i) {  // B5 gate, B6 dx
-        Worker& w = L.workers[i];
-        launch_gate_bwd(reinterpret_cast<const float*>(w.logits), w.slot_pos, w.expert_ids, w.slot_dw,
-                        static_cast<int>(S), E, k, w.dl, st);
-        launch_grouped_gemm_bf16(w.dl, S, E, w.s_rows, 1, L.gater, H, w.dxg, 0, st);
-        launch_wgrad_mn_split(xo(x, i), H, w.dl, E, S, L.splits_g, w.split_g, w.tail_ga, w.tail_gb, w.part_g,
-                              L.dgate, st);
-        if (i == 0 && !L.timing) XMOE_CUDA(cudaStreamWaitEvent(st, L.ev_join, 0));  // dxs
-        launch_combine_slots(w.bslot_src, nullptr, k, H, static_cast<int>(S), L.Fs > 0 ? w.dxs : nullptr,
-                             static_cast<char*>(dx) + static_cast<size_t>(i) * S * rb, st, 0, w.dxg);
+    if (L.timing) {
+        token_level(st);
+        bmark(kBwToken);
+        gate_and_dx(st);
+    } else {
+        XMOE_CUDA(cudaStreamWaitEvent(st, L.ev_join, 0));  // dx, gate and shared-expert gradients
+        bmark(kBwToken);
     }
     bmark(kBwEnd);
     (void)ctx;
