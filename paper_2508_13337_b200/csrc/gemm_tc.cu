@@ -478,9 +478,9 @@ __device__ __forceinline__ void tma_store_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ uint32_t make_idesc2(int n) {
+__device__ __forceinline__ uint32_t make_idesc2(int n, int m = BM) {
     return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
-           (static_cast<uint32_t>(BM >> 4) << 24);
+           (static_cast<uint32_t>(m >> 4) << 24);
 }
 __device__ __forceinline__ void mma2(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
     asm volatile(
@@ -621,7 +621,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             const int32_t* __restrict__ group_sizes, int G, int M, int N, int K,
                             OutT* __restrict__ D, int relu, const uint32_t* __restrict__ mbits_in,
                             uint32_t* __restrict__ mbits_out, int coalesced, const int32_t* __restrict__ a_idx,
-                            int a_rows, const __grid_constant__ CUtensorMap tmap_d, int tma_d) {
+                            int a_rows, const __grid_constant__ CUtensorMap tmap_d, int tma_d, int half_ok) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -682,6 +682,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int num_tiles = tile_start[G];
+    // Half tiles: a group's last row tile with <= 128 rows runs as an M = 128
+    // pair MMA (64 rows per CTA; accumulator columns [0, n/2) in TMEM lanes
+    // 0-63 and [n/2, n) in lanes 64-127 of each CTA), half the tensor work
+    // of padding it to 256 rows.  Every role derives it from the tile alone.
+    auto is_half = [&](const TileInfo& ti, int nw) {
+        return !kVarK && half_ok && ti.rows_left <= BMC && (nw & 63) == 0;
+    };
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs) =====================
@@ -694,7 +701,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const TileInfo ti = tile_of<kVarK>(t, tile_start, off, G, ntn, M, K);
                 const int nw = min(BN, N - ti.n0);
                 const int n_mma = (nw + 15) & ~15;
-                const int arow = ti.row0 + BMC * static_cast<int>(rank);
+                const int arow = ti.row0 + (is_half(ti, nw) ? BMC / 2 : BMC) * static_cast<int>(rank);
                 const int brow = (kVarK ? 0 : ti.g * N) + ti.n0 + (n_mma / 2) * static_cast<int>(rank);
                 int r4[4];
 #pragma unroll
@@ -723,7 +730,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const TileInfo ti = tile_of<kVarK>(t, tile_start, off, G, ntn, M, K);
                 const int nw = min(BN, N - ti.n0);
                 const int n_mma = (nw + 15) & ~15;
-                const int arow = ti.row0 + BMC * static_cast<int>(rank);
+                const int arow = ti.row0 + (is_half(ti, nw) ? BMC / 2 : BMC) * static_cast<int>(rank);
                 const int brow = (kVarK ? 0 : ti.g * N) + ti.n0 + (n_mma / 2) * static_cast<int>(rank);
                 for (int kb = 0; kb < ti.nkb; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -751,7 +758,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (ti.nkb == 0) continue;  // empty reduction: the epilogue writes zeros
                 const int nw = min(BN, N - ti.n0);
                 const int n_mma = (nw + 15) & ~15;
-                const uint32_t idesc = make_idesc2(n_mma);
+                const uint32_t idesc = make_idesc2(n_mma, is_half(ti, nw) ? BM / 2 : BM);
                 const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
                 mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
                 tc_fence_after();
@@ -783,11 +790,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t acc_phase = 0;
         for (int t = pair; t < num_tiles; t += npairs) {
             const TileInfo ti = tile_of<kVarK>(t, tile_start, off, G, ntn, M, K);
-            const int nw = min(BN, N - ti.n0);
-            const int r = BMC * static_cast<int>(rank) + quarter * 32 + lane;
+            const int nw_tile = min(BN, N - ti.n0);
+            // this warp's rows and columns of the tile: full tiles — 32 rows of
+            // the CTA's 128, every column; half tiles — 32 rows of the CTA's 64,
+            // one half of the columns (TMEM lanes 64-127 hold the second half)
+            const bool hf = is_half(ti, nw_tile);
+            const int wrow = hf ? (BMC / 2) * static_cast<int>(rank) + (quarter & 1) * 32
+                                : BMC * static_cast<int>(rank) + quarter * 32;  // first row of this warp
+            const int cbase = hf ? (quarter >> 1) * (nw_tile / 2) : 0;           // first column of this warp
+            const int nw = hf ? nw_tile / 2 : nw_tile;                          // columns of this warp
+            const int r = wrow + lane;
             const bool row_ok = r < ti.rows_left;
             OutT* drow = D + (kVarK ? static_cast<size_t>(ti.g) * M * N : 0) +
-                         static_cast<size_t>(ti.row0 + r) * N + ti.n0;
+                         static_cast<size_t>(ti.row0 + r) * N + ti.n0 + cbase;
             if (ti.nkb == 0) {  // nothing to reduce: zeros, no accumulator used
                 if (row_ok)
                     for (int c = 0; c < nw; ++c) drow[c] = static_cast<OutT>(0.f);
@@ -796,7 +811,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // ReLU masks as bits: one word per (row, 32 columns), ceil(N/32) words per row;
             // the tile's words are loaded before the accumulator wait (off the critical path)
             const int mwords = (N + 31) >> 5;
-            const uint32_t* mrow = mbits_in ? mbits_in + static_cast<size_t>(ti.row0 + r) * mwords + (ti.n0 >> 5)
+            const uint32_t* mrow = mbits_in ? mbits_in + static_cast<size_t>(ti.row0 + r) * mwords +
+                                                  ((ti.n0 + cbase) >> 5)
                                             : nullptr;
             uint32_t mpre[BN / 32];
 #pragma unroll
@@ -810,10 +826,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             };
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
-            uint32_t* orow = mbits_out ? mbits_out + static_cast<size_t>(ti.row0 + r) * mwords + (ti.n0 >> 5)
+            uint32_t* orow = mbits_out ? mbits_out + static_cast<size_t>(ti.row0 + r) * mwords +
+                                             ((ti.n0 + cbase) >> 5)
                                        : nullptr;
             uint32_t* etile = reinterpret_cast<uint32_t*>(smem + kEpiOff + (warp - 2) * kEpiWarpBytes);
-            const int wrow = BMC * static_cast<int>(rank) + quarter * 32;  // first row of this warp in the tile
             // bf16 output boxes of 32 rows x 64 columns leave through TMA stores when
             // the warp's 32 rows all belong to the group (a box must not touch the
             // next group's rows)
@@ -839,7 +855,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                     store_chunk_coalesced<OutT>(etile, f, D + (kVarK ? static_cast<size_t>(ti.g) * M * N : 0),
                                                 static_cast<size_t>(N), static_cast<size_t>(ti.row0 + wrow),
-                                                ti.rows_left - wrow, ti.n0 + c0, cn, lane);
+                                                ti.rows_left - wrow, ti.n0 + cbase + c0, cn, lane);
                     continue;
                 }
                 if (!row_ok) continue;
@@ -889,7 +905,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         if (use_tma && (c0 & 63) == 32) {
                             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                             __syncwarp();
-                            if (lane == 0) tma_store_2d(&tmap_d, etile, ti.n0 + c0 - 32, ti.row0 + wrow);
+                            if (lane == 0) tma_store_2d(&tmap_d, etile, ti.n0 + cbase + c0 - 32, ti.row0 + wrow);
                         }
                     } else {
                         uint32_t mw = 0;
@@ -1276,6 +1292,15 @@ static bool fwd_tma_store() {
     }();
     return v;
 }
+// a group's last row tile with <= 128 rows runs as an M = 128 pair MMA
+// (XMOE_HALF_TILES=0: padded to 256 rows like every other tile)
+static bool half_tiles() {
+    static const bool v = [] {
+        const char* e = std::getenv("XMOE_HALF_TILES");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return v;
+}
 static bool wgrad_tma_store() {
     static const bool v = [] {
         const char* e = std::getenv("XMOE_WGRAD_TMA");
@@ -1396,7 +1421,8 @@ static void launch_tc2(const void* A, long long a_rows, long long a_cols, const 
     const long long pairs = tile_bound < cap_pairs ? tile_bound : cap_pairs;
     tc2::grouped_gemm_tc2_kernel<OutT, kVarK><<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
         ta, tb, group_sizes, G, M, N, K, D, relu, mbits_in, mbits_out,
-        sizeof(OutT) == 4 && !mbits_out ? epi_coalesced() : 0, a_idx, static_cast<int>(idx_rows), td, tma_d ? 1 : 0);
+        sizeof(OutT) == 4 && !mbits_out ? epi_coalesced() : 0, a_idx, static_cast<int>(idx_rows), td, tma_d ? 1 : 0,
+        half_tiles() ? 1 : 0);
     XMOE_LAUNCH_CHECK();
 }
 
