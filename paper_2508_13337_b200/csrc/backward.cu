@@ -296,7 +296,9 @@ void launch_bwd_owner_prep(const void* dyg, const void* eout, const float* gw, c
                            const int32_t* rpe, int El, int H, long long max_rows, float* const* slotdw_tab,
                            void* dz, int me, cudaStream_t st) {
     require(H % 8 == 0, XMOE_ERR_VALIDATION, "backward requires model_dim % 8 == 0");
-    bwd_owner_prep_kernel<<<warp_grid(max_rows), 256, 0, st>>>(
+    int grid = warp_grid(max_rows);
+    if (g_copy_blocks > 0 && grid > g_copy_blocks) grid = g_copy_blocks;
+    bwd_owner_prep_kernel<<<grid, 256, 0, st>>>(
         static_cast<const __nv_bfloat16*>(dyg), static_cast<const __nv_bfloat16*>(eout), gw, gsrc, rpe, El, H,
         slotdw_tab, static_cast<__nv_bfloat16*>(dz), me);
     XMOE_LAUNCH_CHECK();
@@ -309,8 +311,10 @@ void launch_bwd_scatter_dy(const void* dy, int H, int S, int k, const int32_t* s
                            cudaStream_t st) {
     require(H % 8 == 0 && k <= 32, XMOE_ERR_VALIDATION, "backward requires model_dim % 8 == 0, top_k <= 32");
     if (S == 0) return;
-    const long long blocks = (static_cast<long long>(S) + 7) / 8;
-    bwd_scatter_dy_kernel<<<static_cast<int>(blocks < 8LL * kNumSMs ? blocks : 8LL * kNumSMs), 256, 0, st>>>(
+    long long blocks = (static_cast<long long>(S) + 7) / 8;
+    if (blocks > 8LL * kNumSMs) blocks = 8LL * kNumSMs;
+    if (g_copy_blocks > 0 && blocks > g_copy_blocks) blocks = g_copy_blocks;
+    bwd_scatter_dy_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(
         static_cast<const char*>(dy), H, S, k, slot_pos, dest_rank, dest_row, cw, me, static_cast<char*>(dz),
         eout_tab, dyg_tab, dxc_tab, gw_tab, gsrc_tab, slot_dw, bslot_src);
     XMOE_LAUNCH_CHECK();

@@ -976,6 +976,8 @@ void Layer::exchange_nccl(bool forward, cudaStream_t st) {
 void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* dx, cudaStream_t st) {
     require(L.train, XMOE_ERR_VALIDATION, "layer was not created with XMOE_LAYER_TRAIN");
     require(S == L.last_S, XMOE_ERR_VALIDATION, "backward must follow a forward of the same sequence");
+    g_copy_blocks = 0;  // launch-shaping globals start clean even after an aborted call
+    g_gemm_sm_limit = 0;
     Ctx& ctx = *L.ctx;
     const int W = L.W, E = L.E, H = L.H, F = L.F, k = L.k, El = L.El;
     const size_t rb = static_cast<size_t>(H) * L.es;
@@ -1007,6 +1009,16 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
             }
         }
     };
+    // NVLink row movement beside GEMMs on the other stream runs on a bounded
+    // grid (as in the chunked forward): with every SM's worth of blocks its
+    // remote traffic stalls the GEMM CTAs.  XMOE_BWD_COPY_BLOCKS (default
+    // 128; 0 = full grid) applies when distributed, outside timing mode
+    // (N=4 fwd+bwd, M tok/s: 32 blocks 9.9, 64 11.6, 128 11.9, full 11.8).
+    static const int bwd_copy_blocks = [] {
+        const char* e = std::getenv("XMOE_BWD_COPY_BLOCKS");
+        return e ? std::max(0, std::atoi(e)) : 128;
+    }();
+    const int copy_cap = dist && !L.timing ? bwd_copy_blocks : 0;
     if (!L.timing) {
         XMOE_CUDA(cudaEventRecord(L.ev_fork, st));
         XMOE_CUDA(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
@@ -1018,6 +1030,7 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
         token_level(L.side);
         g_gemm_sm_limit = 0;
     }
+    g_copy_blocks = copy_cap;
     for (int i = 0; i < L.nl; ++i) {  // B1
         Worker& w = L.workers[i];
         launch_bwd_scatter_dy(xo(dy, i), H, static_cast<int>(S), k, w.slot_pos, w.dest_rank, w.dest_row, w.cw,
@@ -1032,6 +1045,7 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
         if (W > 1)  // copies from peers (this rank's own were finished at the source)
             launch_bwd_owner_prep(w.dyg, w.eout, w.gw, w.gsrc, w.rpe, El, H, L.R_max, L.slotdw_tab, w.dz, w.rank,
                                   st);
+        g_copy_blocks = 0;
         bmark(kBwPrep);
         launch_grouped_gemm_bf16_mask(w.dz, L.R_max, H, w.rpe, El, static_cast<const char*>(L.w2r) + eo, F, w.dH,
                                       w.mbits, st);
@@ -1051,8 +1065,10 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
             launch_grouped_gemm_bf16(w.dl, S, E, w.s_rows, 1, L.gater, H, w.dxg, 0, gs);
             launch_wgrad_mn_split(xo(x, i), H, w.dl, E, S, L.splits_g, w.split_g, w.tail_ga, w.tail_gb, w.part_g,
                                   L.dgate, gs);
+            g_copy_blocks = copy_cap;
             launch_combine_slots(w.bslot_src, nullptr, k, H, static_cast<int>(S), L.Fs > 0 ? w.dxs : nullptr,
                                  static_cast<char*>(dx) + static_cast<size_t>(i) * S * rb, gs, 0, w.dxg);
+            g_copy_blocks = 0;
         }
     };
     if (dist) L.barrier(st);  // every owner wrote dL/dw and dxc
