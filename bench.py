@@ -73,16 +73,41 @@ def peaks():
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region: NVML polled every 2 ms from a thread (a timed region of 20 steps
+    is only ~30 ms, shorter than nvidia-smi's 100 ms sampling period), with
+    `nvidia-smi -lms 100` as the fallback when NVML is unavailable."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self):
+    def __init__(self, gpus=1):
         self.proc = None
         self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons set)
+        self.stop_ev = threading.Event()
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = [int(v) for v in vis.split(",")][:gpus] if vis and all(
+                v.strip().isdigit() for v in vis.split(",")) else list(range(gpus))
+            self.handles = [pynvml.nvmlDeviceGetHandleByIndex(i) for i in idx]
+            self.bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                         "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                         "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                         "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            self.nvml = pynvml
+        except Exception:
+            self.nvml = None
 
     def start(self):
+        if self.nvml is not None:
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                                           "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
@@ -92,38 +117,56 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        nv = self.nvml
+        while not self.stop_ev.is_set():
+            for h in self.handles:
+                try:
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((float(sm), float(mx), {n for n, b in self.bits.items() if r & b}))
+                except Exception:
+                    pass
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self, gpus):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9 or not f[0].isdigit() or int(f[0]) >= gpus:
-                continue
+        if self.nvml is not None:
+            self.stop_ev.set()
+            self.t.join(timeout=1)
+            samples = self.samples
+            src = "nvml, 2 ms"
+        elif self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
             try:
-                sm.append(float(f[1]))
-                mx.append(float(f[2]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+            samples = []
+            for ln in self.lines:
+                f = [x.strip() for x in ln.split(",")]
+                if len(f) < 9 or not f[0].isdigit() or int(f[0]) >= gpus:
+                    continue
+                try:
+                    samples.append((float(f[1]), float(f[2]),
+                                    {n for n, v in zip(self.NAMES, f[5:9]) if v.lower() == "active"}))
+                except ValueError:
+                    continue
+            src = "nvidia-smi, 100 ms"
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        if not samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
-        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        sm = [x[0] for x in samples]
+        reasons = set().union(*[x[2] for x in samples])
+        busy = [v for v in sm if v > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_min_mhz": min(busy), "sm_max_mhz": max(x[1] for x in samples),
+                "reasons": sorted(reasons), "samples": len(samples), "sampler": src}
 
 
 # ---------------------------------------------------------------- CPU reference
@@ -308,7 +351,7 @@ def main():
     torch.cuda.synchronize()
 
     # ---- device-timed region (inputs resident in HBM)
-    clocks = ClockSampler()
+    clocks = ClockSampler(world)
     if rank == 0:
         clocks.start()
     launches0 = capi.kernel_launches()
