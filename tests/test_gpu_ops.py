@@ -220,7 +220,9 @@ def _torch_grouped_gemm(A, seg, B, N, relu):
 
 @pytest.mark.parametrize("seg,K,N", [([128], 64, 256), ([300, 0, 17, 1000], 2048, 1408),
                                      ([1536] * 8, 1408, 2048), ([5, 129, 0, 0, 64], 256, 64),
-                                     ([4096], 2048, 64)])
+                                     ([4096], 2048, 64),
+                                     # M=128 half tiles: tails of 1..128 rows, N tiles of 192 / 64 columns
+                                     ([200, 50, 130, 1], 128, 192), ([383, 64, 257], 256, 320)])
 def test_grouped_gemm_bf16_tcgen05(ctx, seg, K, N):
     torch.manual_seed(0)
     rows = sum(seg)
