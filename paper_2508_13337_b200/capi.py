@@ -74,7 +74,7 @@ def lib():
     if _LIB is None:
         if not os.path.exists(_build.LIB):
             raise ImportError(f"{_build.LIB} is not built (run __graft_entry__.build())")
-        L = C.CDLL(_build.LIB)
+        L = C.CDLL(os.environ.get("XMOE_LIB") or _build.LIB)  # XMOE_LIB: A/B builds
         p, i64, i32 = C.c_void_p, C.c_int64, C.c_int
         L.xmoe_last_error.restype = C.c_char_p
         L.xmoe_abi_version.restype = C.c_int

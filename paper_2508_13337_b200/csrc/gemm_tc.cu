@@ -723,7 +723,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-        } else if (lane == 0) {
+        } else {  // whole warp in the loop, one elected thread issues (see the wgrad producer)
             int stage = 0;
             uint32_t phase = 0;
             for (int t = pair; t < num_tiles; t += npairs) {
@@ -734,11 +734,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int brow = (kVarK ? 0 : ti.g * N) + ti.n0 + (n_mma / 2) * static_cast<int>(rank);
                 for (int kb = 0; kb < ti.nkb; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
-                    const uint32_t fb = mapa(&full_bar[stage], 0);
-                    expect_tx_cluster(fb, kStageBytes);
                     const int kc = ti.kofs + kb * BK;
-                    tma_load_2sm(&tmap_a, fb, smem_a + stage * kABytes, kc, arow);
-                    tma_load_2sm(&tmap_b, fb, smem_b + stage * kBBytes, kc, brow);
+                    if (elect_one()) {
+                        const uint32_t fb = mapa(&full_bar[stage], 0);
+                        expect_tx_cluster(fb, kStageBytes);
+                        tma_load_2sm(&tmap_a, fb, smem_a + stage * kABytes, kc, arow);
+                        tma_load_2sm(&tmap_b, fb, smem_b + stage * kBBytes, kc, brow);
+                    }
+                    __syncwarp();
                     if (++stage == kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -1043,34 +1046,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     };
 
     if (warp == 0) {
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int t = pair; t < num_tiles; t += npairs) {
-                int g, row0, n0, nkb, rows_g;
-                info(t, g, row0, n0, nkb, rows_g);
-                const int nw = min(BN, N - n0);
-                const int n_mma = (nw + 15) & ~15;
-                const int am = row0 + BMC * static_cast<int>(rank);
-                const int bn = n0 + (n_mma / 2) * static_cast<int>(rank);
-                for (int kb = 0; kb < nkb; ++kb) {
-                    mbar_wait(&empty_bar[stage], phase ^ 1);
+        // TMA producer: the whole warp runs the loop (uniform control flow)
+        // and one elected thread issues; a `lane == 0` branch made ptxas wrap
+        // every TMA in an elect/broadcast loop, and with four loads per stage
+        // the producer fell behind the MMAs (ncu: the MMA warp waited on full
+        // stages while the producer never waited on empty ones)
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = pair; t < num_tiles; t += npairs) {
+            int g, row0, n0, nkb, rows_g;
+            info(t, g, row0, n0, nkb, rows_g);
+            const int nw = min(BN, N - n0);
+            const int n_mma = (nw + 15) & ~15;
+            const int am = row0 + BMC * static_cast<int>(rank);
+            const int bn = n0 + (n_mma / 2) * static_cast<int>(rank);
+            const int r0 = roff[g];
+            for (int kb = 0; kb < nkb; ++kb) {
+                mbar_wait(&empty_bar[stage], phase ^ 1);
+                const bool tail = (kb + 1) * BK > rows_g;
+                const int kr = tail ? g * BK : r0 + kb * BK;
+                if (elect_one()) {
                     const uint32_t fb = mapa(&full_bar[stage], 0);
                     expect_tx_cluster(fb, kStageBytes);
-                    const bool tail = (kb + 1) * BK > rows_g;
                     const CUtensorMap* ma = tail ? &tmap_at : &tmap_a;
                     const CUtensorMap* mb = tail ? &tmap_bt : &tmap_b;
-                    const int kr = tail ? g * BK : roff[g] + kb * BK;
                     uint8_t* sa = smem_a + stage * kABytes;
                     uint8_t* sb = smem_b + stage * kBBytes;
                     tma_load_2sm(ma, fb, sa, am, kr);
                     tma_load_2sm(ma, fb, sa + 8192, am + 64, kr);
                     tma_load_2sm(mb, fb, sb, bn, kr);
                     tma_load_2sm(mb, fb, sb + 8192, bn + 64, kr);
-                    if (++stage == kStages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                }
+                __syncwarp();
+                if (++stage == kStages) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
