@@ -350,7 +350,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             dst[q] = o;
                         }
                     } else {
-                        for (int i = 0; i < cn; ++i) drow[c0 + i] = __float2bfloat16_rn(f[i]);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (i < cn) drow[c0 + i] = __float2bfloat16_rn(f[i]);
                     }
                 } else {
                     if (cn == 32 && (N & 3) == 0) {
@@ -359,7 +361,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int q = 0; q < 8; ++q)
                             dst[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
                     } else {
-                        for (int i = 0; i < cn; ++i) drow[c0 + i] = f[i];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (i < cn) drow[c0 + i] = f[i];
                     }
                 }
             }
@@ -820,13 +824,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint32_t mpre[BN / 32];
 #pragma unroll
             for (int q = 0; q < BN / 32; ++q) mpre[q] = (mrow && row_ok && 32 * q < nw) ? __ldg(mrow + q) : 0u;
-            auto mask_word = [&](int c0) {
-                uint32_t mw = mpre[0];
-#pragma unroll
-                for (int q = 1; q < BN / 32; ++q)
-                    if ((c0 >> 5) == q) mw = mpre[q];
-                return mw;
-            };
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
             uint32_t* orow = mbits_out ? mbits_out + static_cast<size_t>(ti.row0 + r) * mwords +
@@ -838,6 +835,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // next group's rows)
             const bool use_tma = sizeof(OutT) == 2 && !kVarK && tma_d && ti.rows_left - wrow >= 32 && (nw & 63) == 0;
             for (int c0 = 0; c0 < nw; c0 += 32) {
+                // this chunk's mask word; the prefetched words shift down one
+                // per chunk (constant indices keep them in registers)
+                const uint32_t mask_w = mpre[0];
+#pragma unroll
+                for (int q = 0; q + 1 < BN / 32; ++q) mpre[q] = mpre[q + 1];
                 uint32_t v[32];
                 tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                               static_cast<uint32_t>(acc * BN + c0),
@@ -851,7 +853,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                     const int cn = min(32, nw - c0);
                     if (mrow && row_ok) {
-                        const uint32_t mw = mask_word(c0);
+                        const uint32_t mw = mask_w;
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
                             if (!((mw >> i) & 1u)) f[i] = 0.f;
@@ -870,7 +872,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 const int cn = min(32, nw - c0);
                 if (mrow) {
-                    const uint32_t mw = mask_word(c0);
+                    const uint32_t mw = mask_w;
 #pragma unroll
                     for (int i = 0; i < 32; ++i)
                         if (!((mw >> i) & 1u)) f[i] = 0.f;
@@ -912,7 +914,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         }
                     } else {
                         uint32_t mw = 0;
-                        for (int i = 0; i < cn; ++i) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            if (i >= cn) continue;
                             const __nv_bfloat16 b = __float2bfloat16_rn(f[i]);
                             drow[c0 + i] = b;
                             mw |= (__bfloat162float(b) != 0.f ? 1u : 0u) << i;
@@ -925,7 +929,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int q = 0; q < 8; ++q) dst[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
                     } else {
-                        for (int i = 0; i < cn; ++i) drow[c0 + i] = f[i];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (i < cn) drow[c0 + i] = f[i];
                     }
                 }
             }
@@ -1164,7 +1170,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     } else if (row_ok) {
                         const int cn = min(32, nw - c0);
                         float* dt = D + static_cast<size_t>(g) * M * N + static_cast<size_t>(n0 + c0) * M + row0 + r;
-                        for (int i = 0; i < cn; ++i) dt[static_cast<size_t>(i) * M] = __uint_as_float(v[i]);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (i < cn) dt[static_cast<size_t>(i) * M] = __uint_as_float(v[i]);
                     }
                     continue;
                 }
@@ -1202,7 +1210,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
                                              __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
                 } else {
-                    for (int i = 0; i < cn; ++i) drow[c0 + i] = __uint_as_float(v[i]);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (i < cn) drow[c0 + i] = __uint_as_float(v[i]);
                 }
             }
             tc_fence_before();
