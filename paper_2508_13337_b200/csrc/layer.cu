@@ -310,6 +310,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
             r.dptr = i32(W + 1);
             r.perm = i32(nk);
             r.nsorted = i32(nk);
+            r.scan_ws = i32(nk / 2048 + 2);
             r.coff = i32(nk);
             r.csr_ws = L.alloc(bucket_ws_bytes(nk, W));
             r.C = L.nchunks;

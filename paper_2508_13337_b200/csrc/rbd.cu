@@ -172,72 +172,96 @@ __global__ void rbd_group_count_kernel(const int32_t* __restrict__ slot_pos,
     gcount[t] = n;
 }
 
-// Single-CTA exclusive scan of n int32 (n up to a few 10^6; n_dev, when
-// given, caps n on the device); total -> *total.  Tiles of 4K items are
-// staged in shared memory with coalesced loads, each thread scans
-// kScanPer consecutive items, a warp-shuffle scan combines the threads.
-constexpr int kScanTile = 4096;  // 16 KB smem: co-resides with the persistent GEMM CTAs
-constexpr int kScanPer = kScanTile / 1024;
-__global__ void __launch_bounds__(1024) exclusive_scan_kernel(const int32_t* __restrict__ in, int n_host,
-                                                              const int32_t* __restrict__ n_dev,
-                                                              int32_t* __restrict__ out,
-                                                              int32_t* __restrict__ total) {
-    extern __shared__ int32_t tile[];  // [kScanTile]
-    __shared__ int32_t warp_sums[32];
-    __shared__ int32_t carry;
+// Exclusive scan of n int32 (n_dev, when given, caps n on the device);
+// total -> *total.  Two launches: per-tile sums of 2048 items, then every
+// tile adds the sums of the tiles before it and scans itself (8 items per
+// thread, warp-shuffle and block combine).  Replaced a single-CTA scan
+// (27 us for the S*k = 98K group sizes of C2 on the RBD head; ncu).
+constexpr int kScanThreads = 256;
+constexpr int kScanPer = 8;
+constexpr int kScanTile = kScanThreads * kScanPer;
+
+__global__ void __launch_bounds__(kScanThreads) scan_tile_sums_kernel(const int32_t* __restrict__ in, int n_host,
+                                                                      const int32_t* __restrict__ n_dev,
+                                                                      int32_t* __restrict__ bsum) {
+    __shared__ int32_t ws[kScanThreads / 32];
     const int n = n_dev ? min(*n_dev, n_host) : n_host;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int i0 = 0; i0 < n; i0 += kScanTile) {
-        for (int q = threadIdx.x; q < kScanTile; q += 1024) tile[q] = (i0 + q < n) ? in[i0 + q] : 0;
-        __syncthreads();
-        int loc[kScanPer];
-        int sum = 0;
+    const int base = blockIdx.x * kScanTile;
+    int sum = 0;
+    if (base < n) {
 #pragma unroll
         for (int q = 0; q < kScanPer; ++q) {
-            loc[q] = sum;
-            sum += tile[threadIdx.x * kScanPer + q];
+            const int i = base + q * kScanThreads + threadIdx.x;  // coalesced
+            if (i < n) sum += in[i];
         }
-        int incl = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (lane == 31) warp_sums[wid] = incl;
-        __syncthreads();
-        if (wid == 0) {
-            int v = warp_sums[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, v, o);
-                if (lane >= o) v += y;
-            }
-            warp_sums[lane] = v;  // inclusive over warps
-        }
-        __syncthreads();
-        const int before = carry + (wid ? warp_sums[wid - 1] : 0) + incl - sum;
-#pragma unroll
-        for (int q = 0; q < kScanPer; ++q) tile[threadIdx.x * kScanPer + q] = before + loc[q];
-        __syncthreads();
-        for (int q = threadIdx.x; q < kScanTile; q += 1024)
-            if (i0 + q < n) out[i0 + q] = tile[q];
-        if (threadIdx.x == 0) carry += warp_sums[31];
-        __syncthreads();
     }
-    if (threadIdx.x == 0 && total) *total = carry;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+#pragma unroll
+        for (int w = 0; w < kScanThreads / 32; ++w) t += ws[w];
+        bsum[blockIdx.x] = t;
+    }
 }
 
-static void scan_i32(const int32_t* in, int n, const int32_t* n_dev, int32_t* out, int32_t* total,
-                     cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        XMOE_CUDA(cudaFuncSetAttribute(exclusive_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kScanTile * 4));
-        attr = true;
+__global__ void __launch_bounds__(kScanThreads) scan_tiles_kernel(const int32_t* __restrict__ in, int n_host,
+                                                                  const int32_t* __restrict__ n_dev,
+                                                                  const int32_t* __restrict__ bsum,
+                                                                  int32_t* __restrict__ out, int32_t* __restrict__ total) {
+    __shared__ int32_t ws[kScanThreads / 32];
+    __shared__ int32_t s_prefix;
+    const int n = n_dev ? min(*n_dev, n_host) : n_host;
+    const int base = blockIdx.x * kScanTile;
+    const int last = n > 0 ? (n - 1) / kScanTile : 0;
+    if (static_cast<int>(blockIdx.x) > last) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (wid == 0) {  // sum of the earlier tiles
+        int p = 0;
+        for (int b = lane; b < static_cast<int>(blockIdx.x); b += 32) p += bsum[b];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+        if (lane == 0) s_prefix = p;
     }
-    exclusive_scan_kernel<<<1, 1024, kScanTile * 4, st>>>(in, n, n_dev, out, total);
+    // thread t scans items base + t*kScanPer .. +kScanPer-1 (blocked, vector loads)
+    int v[kScanPer];
+    const int i0 = base + threadIdx.x * kScanPer;
+#pragma unroll
+    for (int q = 0; q < kScanPer; ++q) v[q] = (i0 + q < n) ? in[i0 + q] : 0;
+    int sum = 0;
+#pragma unroll
+    for (int q = 0; q < kScanPer; ++q) {
+        const int x = v[q];
+        v[q] = sum;
+        sum += x;
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) ws[wid] = incl;
+    __syncthreads();
+    int before = s_prefix + incl - sum;
+#pragma unroll
+    for (int w = 0; w < kScanThreads / 32; ++w)
+        if (w < wid) before += ws[w];
+#pragma unroll
+    for (int q = 0; q < kScanPer; ++q)
+        if (i0 + q < n) out[i0 + q] = before + v[q];
+    if (static_cast<int>(blockIdx.x) == last && threadIdx.x == kScanThreads - 1 && total)
+        *total = n > 0 ? before + sum : 0;
+}
+
+static void scan_i32(const int32_t* in, int n, const int32_t* n_dev, int32_t* out, int32_t* total, int32_t* ws,
+                     cudaStream_t st) {
+    const int nb = n > 0 ? (n + kScanTile - 1) / kScanTile : 1;
+    scan_tile_sums_kernel<<<nb, kScanThreads, 0, st>>>(in, n, n_dev, ws);
+    XMOE_LAUNCH_CHECK();
+    scan_tiles_kernel<<<nb, kScanThreads, 0, st>>>(in, n, n_dev, ws, out, total);
     XMOE_LAUNCH_CHECK();
 }
 
@@ -804,7 +828,7 @@ void launch_rbd_groups(const int32_t* slot_pos, const int32_t* expert_ids, int S
     const int El_node = El * wk.gpn;  // group key: the copy's node
     rbd_group_count_kernel<<<ceil_div(S, 256), 256, 0, st>>>(slot_pos, expert_ids, S, k, El_node, wk.gcount);
     XMOE_LAUNCH_CHECK();
-    scan_i32(wk.gcount, S, nullptr, wk.gbase, wk.G_dev, st);
+    scan_i32(wk.gcount, S, nullptr, wk.gbase, wk.G_dev, wk.scan_ws, st);
     const long long max_groups = static_cast<long long>(S) * k;
     rbd_draw_kernel<<<ceil_div(max_groups, kRbdChunk), 256, 0, st>>>(
         state[0], state[1], state[2], state[3], jumps, wk.G_dev, wk.draws);
@@ -822,7 +846,7 @@ void launch_rbd_sort(int W, long long max_groups, RbdWork& wk, cudaStream_t st) 
     if (max_groups == 0) return;  // empty sequence: dptr zeroed above
     rbd_group_pos_kernel<<<ceil_div(max_groups, 256), 256, 0, st>>>(wk.perm, wk.G_dev, wk.g, wk.nsorted);
     XMOE_LAUNCH_CHECK();
-    scan_i32(wk.nsorted, static_cast<int>(max_groups), wk.G_dev, wk.coff, nullptr, st);
+    scan_i32(wk.nsorted, static_cast<int>(max_groups), wk.G_dev, wk.coff, nullptr, wk.scan_ws, st);
 }
 
 void launch_rbd_chunk_counts(int W, int S, RbdWork& wk, cudaStream_t st) {

@@ -46,6 +46,7 @@ struct RbdWork {
     int32_t* dptr;     // [W+1] dest segment starts (dest-sorted)
     int32_t* perm;     // [S*k] dest-sorted position -> group id
     int32_t* nsorted;  // [S*k] group size in sorted order
+    int32_t* scan_ws;  // [S*k/2048 + 2] block sums of the multi-block scans
     int32_t* coff;     // [S*k] first descriptor of each sorted group
     void* csr_ws;
     // token chunks (chunk.cu; C = 1 when the forward is not chunked).  The
