@@ -8,14 +8,6 @@
 
 namespace xmoe {
 
-// Owner-side tables the training-mode dispatch fills: per grouped row, the
-// copy's combine weight and its home (source rank << 32 | token*k + slot).
-struct TrainTabs {
-    float* const* gw_tab = nullptr;
-    unsigned long long* const* gsrc_tab = nullptr;
-    int me = 0;
-};
-
 // gate.cu
 void launch_gate_logits_f64(const double* x, const double* wg, int S, int H, int E,
                             double* logits, cudaStream_t st);
@@ -46,7 +38,7 @@ void launch_scatter_rows(const void* x, int row_bytes, const int32_t* token_ids,
 void launch_scatter_tokens(const void* x, int row_bytes, int S, int k, const int32_t* slot_pos,
                            const int32_t* dest_rank, const int32_t* dest_row, const double* cw,
                            char* const* dest_bufs, char* const* src_bufs, unsigned long long* slot_src,
-                           float* slot_w, cudaStream_t st, TrainTabs tr = TrainTabs{});
+                           float* slot_w, cudaStream_t st);
 // out[t] = sum over t's kept copies of w * row(copy) (+ addend[t] + addend2[t]);
 // row address = slot_src + src_delta bytes; slot_w == null means weight 1.
 void launch_combine_slots(const unsigned long long* slot_src, const float* slot_w, int k, int H, int S,

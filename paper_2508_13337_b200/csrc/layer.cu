@@ -336,8 +336,6 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         }
         if (L.train) {
             const long long Fs = L.Fs;
-            L.Kp = (L.R_max + 64LL * L.El + 63) / 64 * 64;
-            L.Sp = (S + 63) / 64 * 64;
             w.dyg = w.sym + off_dyg;
             w.dxc = w.sym + off_dxc;
             w.gw = reinterpret_cast<float*>(w.sym + off_gw);
@@ -369,10 +367,6 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
             w.part_g = static_cast<float*>(L.alloc(sizeof(float) * L.splits_g * H * r128(E)));
             w.tail_ga = L.alloc(64 * static_cast<size_t>(L.splits_g) * H * es);
             w.tail_gb = L.alloc(64 * static_cast<size_t>(L.splits_g) * E * es);
-            w.kpg = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
-            w.koff = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
-            w.roff = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * (L.El + 1)));
-            w.tk = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * 8));
             w.dl = L.alloc(static_cast<size_t>(S) * E * es);
             w.dxg = L.alloc(static_cast<size_t>(S) * H * es);
             if (Fs > 0) {
@@ -988,11 +982,6 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
         if (L.timing) XMOE_CUDA(cudaEventRecord(L.bev[e], st));
     };
     bmark(kBwStart);
-    for (int i = 0; i < L.nl; ++i) {  // token-level group descriptors (one group of S rows)
-        Worker& w = L.workers[i];
-        launch_fill_i32(w.tk, 1, static_cast<int32_t>(S), st);
-        launch_pad_offsets(w.tk, 1, w.tk + 1, w.tk + 2, w.tk + 4, st);
-    }
     // B5a token-level work that needs only x, dy and the forward's shared
     // activations (x transpose for the gate, shared-expert dgrad + wgrad):
     // on the side stream, overlapping the routed backward (own tail

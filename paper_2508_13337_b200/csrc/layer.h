@@ -77,10 +77,6 @@ struct Worker {
     uint32_t* smbits = nullptr;   // [S, ceil(Fs/32)] of the shared experts' mid
     void* tail_sa = nullptr;      // the same for the side-stream (shared-expert) wgrad
     void* tail_sb = nullptr;
-    int32_t* kpg = nullptr;       // [El] padded rows per expert
-    int32_t* koff = nullptr;      // [El+1]
-    int32_t* roff = nullptr;      // [El+1]
-    int32_t* tk = nullptr;        // token-level (one group of S rows): kpg, koff, roff
     // split-K weight gradients of the single-group (token-level) products:
     // shared experts on the side stream (_s), the gate on the layer stream (_g)
     int32_t* split_s = nullptr;   // [32] rows per split
@@ -133,7 +129,7 @@ struct Layer {
     char** eout_tab = nullptr;
     // training tables and weights in the reference layouts (dgrad B operands)
     bool train = false;
-    long long Kp = 0, Sp = 0, off_eout = 0, off_dxc = 0;
+    long long off_eout = 0, off_dxc = 0;
     char** dyg_tab = nullptr;
     char** dxc_tab = nullptr;
     float** gw_tab = nullptr;

@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(32 * kTokWarps) scatter_tokens_kernel(
     const char* __restrict__ x, int row_bytes, int S, int k, const int32_t* __restrict__ slot_pos,
     const int32_t* __restrict__ dest_rank, const int32_t* __restrict__ dest_row, const double* __restrict__ cw,
     char* const* __restrict__ dest_bufs, char* const* __restrict__ src_bufs,
-    unsigned long long* __restrict__ slot_src, float* __restrict__ slot_w, TrainTabs tr) {
+    unsigned long long* __restrict__ slot_src, float* __restrict__ slot_w) {
     const int lane = threadIdx.x & 31;
     const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
@@ -255,11 +255,6 @@ __global__ void __launch_bounds__(32 * kTokWarps) scatter_tokens_kernel(
                 dst = reinterpret_cast<unsigned long long>(dest_bufs[r] + off);
                 if (src_bufs) rd = reinterpret_cast<unsigned long long>(src_bufs[r] + off);
                 wv = static_cast<float>(cw[p]);
-                if (tr.gw_tab) {  // training: the owner learns each row's weight and home slot
-                    tr.gw_tab[r][dest_row[p]] = wv;
-                    tr.gsrc_tab[r][dest_row[p]] =
-                        (static_cast<unsigned long long>(tr.me) << 32) | static_cast<unsigned>(t * k + lane);
-                }
             }
             if (slot_src) slot_src[static_cast<size_t>(t) * k + lane] = rd;
             if (slot_w) slot_w[static_cast<size_t>(t) * k + lane] = wv;
@@ -347,7 +342,7 @@ void launch_scatter_rows(const void* x, int row_bytes, const int32_t* token_ids,
 void launch_scatter_tokens(const void* x, int row_bytes, int S, int k, const int32_t* slot_pos,
                            const int32_t* dest_rank, const int32_t* dest_row, const double* cw,
                            char* const* dest_bufs, char* const* src_bufs, unsigned long long* slot_src,
-                           float* slot_w, cudaStream_t st, TrainTabs tr) {
+                           float* slot_w, cudaStream_t st) {
     require((row_bytes & 15) == 0 && k <= 32, XMOE_ERR_VALIDATION, "token scatter needs 16-byte rows, k <= 32");
     if (S == 0) return;
     long long blocks = (static_cast<long long>(S) + kTokWarps - 1) / kTokWarps;
@@ -355,7 +350,7 @@ void launch_scatter_tokens(const void* x, int row_bytes, int S, int k, const int
     if (blocks > cap) blocks = cap;
     scatter_tokens_kernel<<<static_cast<int>(blocks), 32 * kTokWarps, g_copy_smem, st>>>(
         static_cast<const char*>(x), row_bytes, S, k, slot_pos, dest_rank, dest_row, cw, dest_bufs, src_bufs,
-        slot_src, slot_w, tr);
+        slot_src, slot_w);
     XMOE_LAUNCH_CHECK();
 }
 
