@@ -1032,10 +1032,10 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
     for (int i = 0; i < L.nl; ++i) {  // B2-B3 at the owner
         Worker& w = L.workers[i];
         const size_t eo = dist ? 0 : static_cast<size_t>(w.rank) * El * H * F * L.es;
+        g_copy_blocks = 0;  // local HBM work: full grid
         if (W > 1)  // copies from peers (this rank's own were finished at the source)
             launch_bwd_owner_prep(w.dyg, w.eout, w.gw, w.gsrc, w.rpe, El, H, L.R_max, L.slotdw_tab, w.dz, w.rank,
                                   st);
-        g_copy_blocks = 0;
         bmark(kBwPrep);
         launch_grouped_gemm_bf16_mask(w.dz, L.R_max, H, w.rpe, El, static_cast<const char*>(L.w2r) + eo, F, w.dH,
                                       w.mbits, st);
@@ -1043,18 +1043,32 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
     }
     bmark(kBwDgrad);
     // B5 gate, B6 dx: need every owner's dxc rows and dL/dw home-slot writes
-    // (barrier), not the weight gradients — so outside timing mode they run
-    // on the side stream (after the token-level work queued there) while the
-    // layer stream computes the weight gradients; the dx combine's NVLink
-    // reads overlap the wgrad GEMMs.
-    auto gate_and_dx = [&](cudaStream_t gs) {
+    // (barrier), not the weight gradients.  Outside timing mode the gate's
+    // two small GEMMs run on the layer stream first (persistent GEMMs cannot
+    // share SMs with the wgrad GEMMs, so on the side stream they would wait
+    // for the wgrads to finish), then the dx combine — NVLink reads of every
+    // copy's dxc row — runs on the side stream beside the wgrad GEMMs.
+    auto gate_part = [&](cudaStream_t gs, bool with_wgrad) {
         for (int i = 0; i < L.nl; ++i) {
             Worker& w = L.workers[i];
             launch_gate_bwd(reinterpret_cast<const float*>(w.logits), w.slot_pos, w.expert_ids, w.slot_dw,
                             static_cast<int>(S), E, k, w.dl, gs);
             launch_grouped_gemm_bf16(w.dl, S, E, w.s_rows, 1, L.gater, H, w.dxg, 0, gs);
+            if (with_wgrad)
+                launch_wgrad_mn_split(xo(x, i), H, w.dl, E, S, L.splits_g, w.split_g, w.tail_ga, w.tail_gb,
+                                      w.part_g, L.dgate, gs);
+        }
+    };
+    auto gate_wgrad = [&](cudaStream_t gs) {
+        for (int i = 0; i < L.nl; ++i) {
+            Worker& w = L.workers[i];
             launch_wgrad_mn_split(xo(x, i), H, w.dl, E, S, L.splits_g, w.split_g, w.tail_ga, w.tail_gb, w.part_g,
                                   L.dgate, gs);
+        }
+    };
+    auto dx_combine = [&](cudaStream_t gs) {
+        for (int i = 0; i < L.nl; ++i) {
+            Worker& w = L.workers[i];
             g_copy_blocks = copy_cap;
             launch_combine_slots(w.bslot_src, nullptr, k, H, static_cast<int>(S), L.Fs > 0 ? w.dxs : nullptr,
                                  static_cast<char*>(dx) + static_cast<size_t>(i) * S * rb, gs, 0, w.dxg);
@@ -1063,10 +1077,12 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
     };
     if (dist) L.barrier(st);  // every owner wrote dL/dw and dxc
     if (!L.timing) {
+        gate_part(st, false);
         XMOE_CUDA(cudaEventRecord(L.ev_fork, st));
-        XMOE_CUDA(cudaStreamWaitEvent(L.side, L.ev_fork, 0));  // side: token level, then this
-        gate_and_dx(L.side);
+        XMOE_CUDA(cudaStreamWaitEvent(L.side, L.ev_fork, 0));  // side: token level, then the dx combine
+        dx_combine(L.side);
         XMOE_CUDA(cudaEventRecord(L.ev_join, L.side));
+        gate_wgrad(st);
     }
     for (int i = 0; i < L.nl; ++i) {  // B4 wgrad straight on the grouped activations (MN-major operands)
         Worker& w = L.workers[i];
@@ -1079,7 +1095,8 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
     if (L.timing) {
         token_level(st);
         bmark(kBwToken);
-        gate_and_dx(st);
+        gate_part(st, true);
+        dx_combine(st);
     } else {
         XMOE_CUDA(cudaStreamWaitEvent(st, L.ev_join, 0));  // dx, gate and shared-expert gradients
         bmark(kBwToken);
