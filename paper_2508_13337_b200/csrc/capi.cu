@@ -345,6 +345,7 @@ int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S,
                 XMOE_CUDA(cudaGraphLaunch(g.exec, st));
                 g_kernel_launches.fetch_add(g.kernels, std::memory_order_relaxed);  // our kernel nodes
                 L.last_S = S;
+                L.bwd_pending = true;
                 return;
             }
         // capture on the layer's own stream (the caller's may be the legacy

@@ -138,10 +138,12 @@ void launch_flag_signal(unsigned* const* flag_tab, int W, int me, int slot, cons
                         cudaStream_t st);
 void launch_flag_wait(const unsigned* flags, int W, int slot, const unsigned* epoch, cudaStream_t st);
 // flag slots per rank: [0, kMaxChunks) chunk dispatch, [kMaxChunks, 2 kMaxChunks)
-// chunk combine, then the count exchange and the unchunked forward's barriers
+// chunk combine, then the count exchange, the unchunked forward's barriers
+// and the backward's two barriers (same epoch as the forward they follow)
 constexpr int kSlotCounts = 2 * kMaxChunks;
-constexpr int kSlotBar = 2 * kMaxChunks + 1;  // + 0..3
-constexpr int kFlagSlots = 2 * kMaxChunks + 5;
+constexpr int kSlotBar = 2 * kMaxChunks + 1;     // + 0..3
+constexpr int kSlotBwdBar = 2 * kMaxChunks + 5;  // + 0..1
+constexpr int kFlagSlots = 2 * kMaxChunks + 7;
 struct CountSeg {
     const int32_t* src;  // my row
     int row;             // ints per rank row

@@ -713,6 +713,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     XMOE_CUDA(cudaStreamWaitEvent(st, L.ev_done, 0));
     L.mark(kEvCombine, st);
     L.last_S = S;
+    L.bwd_pending = true;
 }
 
 // ---------------------------------------------------------------- forward
@@ -919,6 +920,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     }
     L.mark(kEvCombine, st);
     L.last_S = S;
+    L.bwd_pending = true;
 }
 
 // NCCL alltoallv of rows (the library-collective baseline), chunked per
@@ -971,6 +973,9 @@ void Layer::exchange_nccl(bool forward, cudaStream_t st) {
 void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* dx, cudaStream_t st) {
     require(L.train, XMOE_ERR_VALIDATION, "layer was not created with XMOE_LAYER_TRAIN");
     require(S == L.last_S, XMOE_ERR_VALIDATION, "backward must follow a forward of the same sequence");
+    // one backward per forward: the cross-rank barriers are keyed by the forward's epoch
+    require(L.bwd_pending, XMOE_ERR_VALIDATION, "backward must follow a forward (one backward per forward)");
+    L.bwd_pending = false;
     g_copy_blocks = 0;  // launch-shaping globals start clean even after an aborted call
     g_gemm_sm_limit = 0;
     Ctx& ctx = *L.ctx;
@@ -1027,7 +1032,14 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
                               w.rank, w.dz, L.eout_tab, L.dyg_tab, L.dxc_tab, L.gw_tab, L.gsrc_tab, w.slot_dw,
                               w.bslot_src, st);
     }
-    if (dist) L.barrier(st);
+    // cross-rank barriers: peer flags (a one-block kernel; an NCCL kernel
+    // could not start while the side stream's persistent GEMMs hold every
+    // SM's shared memory — it waited for them, 0.1 ms at N=4)
+    const int me_rank = L.workers[0].rank;
+    auto bbar = [&](int j) {
+        launch_flag_barrier(L.flag_tab, L.workers[0].flags, W, me_rank, kSlotBwdBar + j, L.epoch, st);
+    };
+    if (dist) bbar(0);
     bmark(kBwScatter);
     for (int i = 0; i < L.nl; ++i) {  // B2-B3 at the owner
         Worker& w = L.workers[i];
@@ -1075,7 +1087,7 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
             g_copy_blocks = 0;
         }
     };
-    if (dist) L.barrier(st);  // every owner wrote dL/dw and dxc
+    if (dist) bbar(1);  // every owner wrote dL/dw and dxc
     if (!L.timing) {
         gate_part(st, false);
         XMOE_CUDA(cudaEventRecord(L.ev_fork, st));

@@ -119,6 +119,7 @@ struct Layer {
     std::vector<void*> peer_maps;
     size_t es = 2;
     long long R_max = 0, S_max = 0, last_S = 0;
+    bool bwd_pending = false;  // a forward ran since the last backward (one backward per forward)
     void* gate = nullptr;  // F64 [H,E]; BF16 [E,H]
     void* w1 = nullptr;    // F64 [E_held,H,F]; BF16 [E_held,F,H]
     void* w2 = nullptr;    // F64 [E_held,F,H]; BF16 [E_held,H,F]

@@ -38,12 +38,16 @@ for _ in range(10):
 t1.record()
 torch.cuda.synchronize()
 print(f"fwd+bwd eager {t0.elapsed_time(t1) / 10:.3f} ms/step", flush=True)
-# host enqueue cost vs device time, forward and backward separately
+# host enqueue cost vs device time (the GPU spins first so the host queues
+# everything ahead of it); backward = (forward + backward) - forward, since a
+# backward must follow its own forward
 import time  # noqa: E402
-for name, fn in (("forward", lambda: layer.forward(x, out)), ("backward", lambda: layer.backward(x, dy, dx))):
+res = {}
+for name, fn in (("forward", lambda: layer.forward(x, out)),
+                 ("fwd+bwd", lambda: (layer.forward(x, out), layer.backward(x, dy, dx)))):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda._sleep(200_000_000)  # ~0.1 s of GPU spin: the host queues everything ahead of it
+    torch.cuda._sleep(200_000_000)
     e0.record()
     h0 = time.perf_counter()
     for _ in range(10):
@@ -51,5 +55,7 @@ for name, fn in (("forward", lambda: layer.forward(x, out)), ("backward", lambda
     h1 = time.perf_counter()
     e1.record()
     torch.cuda.synchronize()
-    print(f"{name}: device {e0.elapsed_time(e1) / 10:.3f} ms/call (host queued ahead), "
-          f"host enqueue {(h1 - h0) * 100:.3f} ms/call", flush=True)
+    res[name] = e0.elapsed_time(e1) / 10
+    print(f"{name}: device {res[name]:.3f} ms/call (host queued ahead), host enqueue {(h1 - h0) * 100:.3f} ms/call",
+          flush=True)
+print(f"backward: device {res['fwd+bwd'] - res['forward']:.3f} ms/call", flush=True)
