@@ -140,6 +140,21 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t 
         : "memory");
 }
 
+// one thread of a converged warp (elect.sync): keeps the issue code on the
+// uniform datapath (see tc2::mma2_kblock)
+__device__ __forceinline__ bool elect_one_sync() {
+    uint32_t e;
+    asm volatile(
+        "{\n"
+        ".reg .b32 rx;\n"
+        ".reg .pred px;\n"
+        "elect.sync rx|px, 0xffffffff;\n"
+        "selp.u32 %0, 1, 0, px;\n"
+        "}\n"
+        : "=r"(e));
+    return e != 0;
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile(
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -251,8 +266,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int num_tiles = tile_start[G];
 
     if (warp == 0) {
-        // ===================== TMA producer =====================
-        if (lane == 0) {
+        // ===================== TMA producer (whole warp, one elected issuer) =====================
+        {
             int stage = 0;
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -260,9 +275,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int brow = ti.g * N + ti.n0;
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
-                    mbar_expect_tx(&full_bar[stage], kStageBytes);
-                    tma_load_2d(&tmap_a, &full_bar[stage], smem_a + stage * kABytes, kb * BK, ti.row0);
-                    tma_load_2d(&tmap_b, &full_bar[stage], smem_b + stage * kBBytes, kb * BK, brow);
+                    if (elect_one_sync()) {
+                        mbar_expect_tx(&full_bar[stage], kStageBytes);
+                        tma_load_2d(&tmap_a, &full_bar[stage], smem_a + stage * kABytes, kb * BK, ti.row0);
+                        tma_load_2d(&tmap_b, &full_bar[stage], smem_b + stage * kBBytes, kb * BK, brow);
+                    }
+                    __syncwarp();
                     if (++stage == kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -287,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kb = 0; kb < nkb; ++kb) {
                 mbar_wait(&full_bar[stage], phase);
                 tc_fence_after();
-                if (lane == 0) {
+                if (elect_one_sync()) {
                     const uint64_t da = make_desc(smem_u32(smem_a + stage * kABytes));
                     const uint64_t db = make_desc(smem_u32(smem_b + stage * kBBytes));
 #pragma unroll
