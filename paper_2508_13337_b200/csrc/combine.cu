@@ -201,6 +201,12 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_slots_bf16_kernel(
         if (v0) a4[0] = ld_nc_v4(add + c0);
         if (v1) a4[1] = ld_nc_v4(add + c1);
     }
+    int4 b4[2] = {make_int4(0, 0, 0, 0), make_int4(0, 0, 0, 0)};
+    if (addend2) {  // issued early too (the backward's dx adds two addends)
+        const int4* add = reinterpret_cast<const int4*>(addend2 + static_cast<size_t>(t) * H);
+        if (v0) b4[0] = ld_nc_v4(add + c0);
+        if (v1) b4[1] = ld_nc_v4(add + c1);
+    }
     float acc[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) acc[q] = 0.f;
@@ -247,9 +253,8 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_slots_bf16_kernel(
             }
         }
         if (addend2) {
-            const int4 b4 = ld_nc_v4(reinterpret_cast<const int4*>(addend2 + static_cast<size_t>(t) * H) + c);
-            const uint32_t u[4] = {static_cast<uint32_t>(b4.x), static_cast<uint32_t>(b4.y),
-                                   static_cast<uint32_t>(b4.z), static_cast<uint32_t>(b4.w)};
+            const uint32_t u[4] = {static_cast<uint32_t>(b4[h].x), static_cast<uint32_t>(b4[h].y),
+                                   static_cast<uint32_t>(b4[h].z), static_cast<uint32_t>(b4[h].w)};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 acc[8 * h + 2 * q] += bf16_lo(u[q]);
