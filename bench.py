@@ -377,9 +377,24 @@ def main():
     ms = max_over_ranks(t0.elapsed_time(t1) / args.steps)
     clk = clocks.stop(world) if rank == 0 else None
 
-    # ---- second layer object, unchunked: the training layer for fwd+bwd and
-    # the per-stage (kernel-level) breakdown behind the roofline — in the
-    # chunked forward the stages overlap and have no separate duration
+    # ---- per-stage breakdown + roofline of the dominant kernel (grouped GEMM),
+    # measured right after the timed forward (before the heavier fwd+bwd
+    # section changes the board's power/clock state),
+    # on a forward-only unchunked layer (kernel-level stages; the training
+    # layer's GEMM1 epilogue also stores ReLU masks)
+    slayer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
+                        max_tokens=S, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,
+                        dispatch_mode=mode, seed=99, chunks=1)
+    slayer.set_timing(True)
+    stage_runs = []
+    for _ in range(6):
+        slayer.forward(x, out)
+        torch.cuda.synchronize()
+        stage_runs.append(slayer.stage_ms())
+    stages = {kk: statistics.median(r[kk] for r in stage_runs[1:]) for kk in stage_runs[0]}
+    led = slayer.ledger()
+    del slayer
+    # ---- training layer (unchunked) for fwd+bwd
     tlayer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
                         max_tokens=S, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,
                         dispatch_mode=mode, seed=99, train=not args.no_backward, chunks=1)
@@ -421,22 +436,7 @@ def main():
                    "note": "forward + backward (dx and fp32 grads of gate, experts, shared experts); "
                            "gradients restated beyond the forward-only reference, checked against fp64 autograd"}
 
-    # ---- per-stage breakdown + roofline of the dominant kernel (grouped GEMM),
-    # on a forward-only unchunked layer (kernel-level stages; the training
-    # layer's GEMM1 epilogue also stores ReLU masks)
     del tlayer
-    slayer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
-                        max_tokens=S, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,
-                        dispatch_mode=mode, seed=99, chunks=1)
-    slayer.set_timing(True)
-    stage_runs = []
-    for _ in range(6):
-        slayer.forward(x, out)
-        torch.cuda.synchronize()
-        stage_runs.append(slayer.stage_ms())
-    stages = {kk: statistics.median(r[kk] for r in stage_runs[1:]) for kk in stage_runs[0]}
-    led = slayer.ledger()
-    del slayer
 
     # ---- plain vs redundancy-bypassing dispatch (N > 1): all-to-all bytes and
     # isolated kernel times of both, from unchunked layers in timing mode
