@@ -209,7 +209,9 @@ int xmoe_ssmb_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x_full, int6
  * gradient of the output, both [S, H] bf16 on this rank; writes dx [S, H]
  * bf16 and the layer's fp32 weight gradients, read with xmoe_layer_grads.
  * Routing and capacity drops are constants of the forward (as in the
- * reference's semantics); renorm layers are not supported. */
+ * reference's semantics); renorm layers are not supported.  One backward per
+ * forward: its cross-rank barriers are keyed by that forward's epoch
+ * (XMOE_ERR_VALIDATION otherwise). */
 int xmoe_moe_backward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, const void* dy, int64_t S,
                       void* dx, void* stream);
 /* Device pointers (fp32, owned by the layer) to the gradients of the last
