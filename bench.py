@@ -36,7 +36,7 @@ UNIT = "tokens/s"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="xmoe", choices=["xmoe", "reference"])
     p.add_argument("--mode", default="auto", choices=["auto", "rbd", "naive"],
@@ -258,7 +258,7 @@ def run_reference(args, rank, world, result_out):
     if rank != 0:
         return
     # bounded per-step sample so that K+W steps stay within a few minutes
-    per_step = max(32, min(512, 3000 // max(1, args.steps + args.warmup)))
+    per_step = max(16, min(512, 1500 // max(1, args.steps + args.warmup)))
     v, cores, times, desc = cpu_reference(C2, threads=host_threads(), sample_tokens=per_step,
                                           steps=args.steps, warmup=args.warmup)
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
