@@ -197,7 +197,7 @@ def cpu_reference(cfg, seconds_hint=None, threads=None, sample_tokens=48, steps=
 
     def work(i):
         try:
-            out, _ = layer.pf_moe_forward(samples[i], k, cap)
+            out = layer.pf_moe_forward_noncopy(samples[i], k, cap)
             sh = shared.grouped_expert_mlp(samples[i][0], np.array([sample_tokens]), 0)
             out[0] += 1.0 * sh
         except Exception as e:  # pragma: no cover
@@ -219,7 +219,8 @@ def cpu_reference(cfg, seconds_hint=None, threads=None, sample_tokens=48, steps=
     tok = threads * sample_tokens
     v = tok / statistics.mean(times)
     desc = (f"{threads} host threads x {sample_tokens} tokens of the C2 layer per step "
-            f"(reference pf_moe_forward W=1 + reference grouped_expert_mlp for the 2 shared experts), "
+            f"(reference pf_moe_forward composition W=1, weights by reference, + reference "
+            f"grouped_expert_mlp for the 2 shared experts), "
             f"fp64, backend {refbind.lib().ref_kernel_backend().decode()}")
     return v, threads, times, desc
 

@@ -276,6 +276,43 @@ int ref_pf_moe_forward(void* layer, std::int64_t W, const std::int64_t* node_of,
     });
 }
 
+// The same composition as moesim::pf_moe_forward (pf_pipeline.cpp:137-169),
+// step for step through the reference's own gate_forward / pft_construct /
+// gather_rows / pf_dispatch / grouped_expert_mlp / pf_combine, but with the
+// layer's weights by const reference: the MoeInstance above holds its
+// MoeLayerWeights by value, so every call through it first copies all of
+// them (2.9 GB of fp64 at C2) — shim overhead, not reference work, which
+// dominated small per-thread samples of the CPU baseline.  Identical output
+// (tests/test_oracle.py).
+int ref_pf_moe_forward_noncopy(void* layer, std::int64_t W, const std::int64_t* node_of,
+                               const double* tokens, std::int64_t S, std::int64_t k, std::int64_t cap,
+                               double* out) {
+    return guarded([&] {
+        const auto& L = *static_cast<Layer*>(layer);
+        auto comm = make_comm(W, node_of, nullptr);
+        const std::int64_t E = L.E;
+        if (E % W != 0) throw ValidationError("num_experts must be divisible by the worker-group size");
+        const std::int64_t e_local = E / W;
+        std::vector<Matrix> toks;
+        for (std::int64_t w = 0; w < W; ++w) toks.push_back(to_matrix(tokens + w * S * L.H, S, L.H));
+        std::vector<Pft> pfts(static_cast<std::size_t>(W));
+        for (std::int64_t w = 0; w < W; ++w) {
+            const auto gate = gate_forward(toks[w], L.w.gate, k);
+            pfts[w] = pft_construct(cap, E, gate);
+            pfts[w].x = gather_rows(toks[w], pfts[w].token_ids);
+        }
+        auto disp = pf_dispatch(comm, pfts, E);
+        std::vector<Matrix> expert_out(static_cast<std::size_t>(W));
+        std::vector<std::size_t> seq_lens(static_cast<std::size_t>(W));
+        for (std::int64_t w = 0; w < W; ++w) {
+            expert_out[w] = grouped_expert_mlp(disp.expert_input[w], disp.recv_per_expert[w], L.w, w * e_local);
+            seq_lens[w] = toks[w].rows;
+        }
+        const auto res = pf_combine(comm, disp, expert_out, pfts, seq_lens);
+        for (std::int64_t w = 0; w < W; ++w) from_matrix(res[w], out + w * S * L.H);
+    });
+}
+
 int ref_rbd_moe_forward(void* layer, std::int64_t W, const std::int64_t* node_of,
                         const double* tokens, std::int64_t S, std::int64_t k, std::int64_t cap,
                         std::uint64_t seed, double* out, std::uint64_t* ledger) {

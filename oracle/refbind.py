@@ -72,6 +72,7 @@ def lib():
         L.ref_layer_destroy.argtypes = [_p]
         L.ref_grouped_expert_mlp.argtypes = [_p, _p, _i64, _p, _i64, _i64, _p]
         L.ref_pf_moe_forward.argtypes = [_p, _i64, _p, _p, _i64, _i64, _i64, _p, _p]
+        L.ref_pf_moe_forward_noncopy.argtypes = [_p, _i64, _p, _p, _i64, _i64, _i64, _p]
         L.ref_rbd_moe_forward.argtypes = [_p, _i64, _p, _p, _i64, _i64, _i64, _u64, _p, _p]
         L.ref_padded_moe_forward.argtypes = [_p, _i64, _p, _p, _i64, _i64, _i64, _p]
         L.ref_dispatch.argtypes = [_p, _i64, _p, _p, _i64, _i64, _i64, C.c_int, _u64,
@@ -185,6 +186,16 @@ class Layer:
 
     def pf_moe_forward(self, tokens, k, cap, node_of=None):
         return self._fwd(lib().ref_pf_moe_forward, tokens, k, cap, node_of)
+
+    def pf_moe_forward_noncopy(self, tokens, k, cap, node_of=None):
+        """pf_moe_forward's composition with the weights by reference (no
+        per-call copy of MoeLayerWeights; see ref_shim.cpp)."""
+        tokens = _f64(tokens)
+        W, S, H = tokens.shape
+        node_of = _i64a(list(range(W)) if node_of is None else node_of)
+        out = np.zeros_like(tokens)
+        _check(lib().ref_pf_moe_forward_noncopy(self.h, W, _ptr(node_of), _ptr(tokens), S, k, cap, _ptr(out)))
+        return out
 
     def rbd_moe_forward(self, tokens, k, cap, seed, node_of=None):
         return self._fwd(lib().ref_rbd_moe_forward, tokens, k, cap, node_of, C.c_uint64(seed))

@@ -243,8 +243,10 @@ def test_pf_moe_forward_bit_exact_vs_reference(ref, W):
         got = O.pf_moe_forward(list(toks), w, E, k, cap, node_of, led)
         L = ref.Layer(w.gate, w.w1, w.w2)
         want, rled = L.pf_moe_forward(toks, k, cap, node_of)
+        nc = L.pf_moe_forward_noncopy(toks, k, cap, node_of)  # the CPU-baseline entry (bench.py)
         for i in range(W):
             assert np.array_equal(got[i], want[i])
+            assert np.array_equal(nc[i], want[i])
         for kind in ("dispatch_counts", "dispatch_rows", "combine_rows"):
             assert led.get(kind) == rled[kind], kind
         # the padded GShard path agrees within the reference's own 1e-12
