@@ -782,12 +782,17 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         XMOE_CUDA(cudaEventRecord(L.ev_fork, st));
         XMOE_CUDA(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
         // leave SMs to the routing / exchange kernels running beside it
-        // (multi-GPU only: at N=1 there is no exchange to overlap)
+        // (multi-GPU by default: at N=1 there is no exchange to overlap;
+        // XMOE_SHARED_SMS_N1 applies a limit at N=1 too, for A/B runs)
         static const int shared_sms = [] {
             const char* e = std::getenv("XMOE_SHARED_SMS");
             return e ? std::atoi(e) : 104;
         }();
-        g_gemm_sm_limit = dist ? shared_sms : 0;
+        static const int shared_sms_n1 = [] {
+            const char* e = std::getenv("XMOE_SHARED_SMS_N1");
+            return e ? std::atoi(e) : 0;
+        }();
+        g_gemm_sm_limit = dist ? shared_sms : shared_sms_n1;
         issue_shared(L.side);
         g_gemm_sm_limit = 0;
         XMOE_CUDA(cudaEventRecord(L.ev_join, L.side));
