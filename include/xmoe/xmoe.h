@@ -41,11 +41,13 @@ extern "C" {
 #define XMOE_ERR_PLAN_MISMATCH 6
 #define XMOE_ERR_CUDA 10
 #define XMOE_ERR_NCCL 11
+#define XMOE_ERR_PEER_TIMEOUT 12 /* a peer rank never reached a cross-GPU flag (XMOE_PEER_TIMEOUT_S) */
 #define XMOE_ERR_INTERNAL 99
 
 /* element types */
 #define XMOE_F64 0
 #define XMOE_BF16 1
+#define XMOE_F32 2
 
 /* expert-parallel dispatch modes */
 #define XMOE_DISPATCH_NAIVE 0 /* pf_dispatch/pf_combine (pf_pipeline.cpp:12-135) */
@@ -161,6 +163,102 @@ int xmoe_grouped_wgrad_bf16(xmoe_ctx* ctx, const void* X, const void* Y, int64_t
 int xmoe_wgrad_split_bf16(xmoe_ctx* ctx, const void* X, const void* Y, int64_t rows, int64_t M, int64_t N,
                           int64_t splits, float* D, void* stream);
 
+/* ------------------------------------------------------------------ split expert-parallel operators
+ * The reference's SPMD shape: one call takes EVERY worker's
+ * data (rank == -1 context, all W = world workers on this device).  Per-worker
+ * arguments are HOST arrays of W DEVICE pointers; counts are host int64
+ * arrays.  Packed buffers are a Pft (pft.hpp:17-25): rows x [B_w, H] in
+ * expert-major packed order with token_ids / expert_ids / combine weights,
+ * tokens_per_expert of all workers as one device [W, E] int32 matrix.  Every
+ * copy lands at its owner's grouped row in (local expert, source, position)
+ * order (pf_pipeline.cpp:47-73).  dest_rank/dest_row [B_w] receive (or may be
+ * scratch when NULL, pf_dispatch only) the owner and grouped row of each copy. */
+
+/* moesim::pf_dispatch (pf_pipeline.hpp:34, pf_pipeline.cpp:12-81).  Outputs:
+ * expert_input[j] [n_j, H] (n_j = rows owned by j, sized by the caller from
+ * tpe), recv_per_expert [W, E/W] device, arrival_to_grouped[j] [n_j]
+ * (optional; NULL entries or NULL array skip it). */
+int xmoe_pf_dispatch(xmoe_ctx* ctx, int dtype, int64_t H, int64_t E, const void* const* packed,
+                     const int32_t* const* expert_ids, const int64_t* B, const int32_t* tpe, void* const* expert_input,
+                     int32_t* recv_per_expert, int32_t* const* dest_rank, int32_t* const* dest_row,
+                     int32_t* const* arrival_to_grouped, void* stream);
+
+/* moesim::pf_combine (pf_pipeline.hpp:42-45, pf_pipeline.cpp:107-135): the
+ * return trip plus scatter_combine per source: out[w] [seq_lens[w], H] =
+ * sum over w's copies in packed order of cw * expert_out[owner][grouped row]
+ * (F64: the reference's axpy order, bit-exact). */
+int xmoe_pf_combine(xmoe_ctx* ctx, int dtype, int64_t H, int64_t E, const void* const* expert_out,
+                    const int32_t* tpe, const int32_t* const* token_ids, const int32_t* const* expert_ids,
+                    const double* const* cw, const int64_t* B, const int64_t* seq_lens, void* const* out,
+                    void* stream);
+
+/* moesim::select_pilots (rbd.hpp:46-47, rbd.cpp:26-81) for one packed buffer
+ * of B copies: groups the copies by (token, node of the expert's owner) with
+ * node = owner / gpus_per_node (contiguous blocks, placement.hpp:21-26) and
+ * draws one Rng(seed).below(|group|) per group in (token, node) order.
+ * S bounds the token ids (< S) and k the copies per token.  pilot_mask [B]
+ * (uint8, device); pilot_of [B] (optional) = packed row of each copy's pilot. */
+int xmoe_select_pilots(xmoe_ctx* ctx, int64_t B, const int32_t* token_ids, const int32_t* expert_ids, int64_t S,
+                       int64_t k, int64_t E, int64_t W, int64_t gpus_per_node, uint64_t seed, uint8_t* pilot_mask,
+                       int32_t* pilot_of, void* stream);
+
+/* moesim::rbd_dispatch (rbd.hpp:78-79, rbd.cpp:83-285): stage 1 moves each
+ * (token, node) group's pilot row to the pilot's owner (the landing worker),
+ * stage 2 re-creates the replicas there from the landed row and stores them
+ * at their owners on the same node.  expert_input is bit-identical to
+ * xmoe_pf_dispatch's (rbd.hpp:50).  pilot_mask[w] [B_w] is the plan's mask;
+ * seq_lens bound the token ids, k the copies per token.  Outputs per source:
+ * dest_rank, dest_row and pilot_of [B_w] (all required: they are the
+ * bookkeeping the reverse path and the reference's RbdDispatch are built
+ * from).  XMOE_ERR_PLAN_MISMATCH when a group has no or several pilots. */
+int xmoe_rbd_dispatch(xmoe_ctx* ctx, int dtype, int64_t H, int64_t E, int64_t gpus_per_node,
+                      const void* const* packed, const int32_t* const* token_ids, const int32_t* const* expert_ids,
+                      const int64_t* B, const int64_t* seq_lens, int64_t k, const int32_t* tpe,
+                      const uint8_t* const* pilot_mask, void* const* expert_input, int32_t* recv_per_expert,
+                      int32_t* const* dest_rank, int32_t* const* dest_row, int32_t* const* pilot_of, void* stream);
+
+/* moesim::rbd_combine (rbd.hpp:85-88, rbd.cpp:287-358) over the reference's
+ * RbdDispatch bookkeeping, flattened: P landed pilots (all landing workers),
+ * flat pilot p landed at worker land_of[p], grouped row land_pos[p], multi-copy
+ * flag and weight; its replicas' outputs are entries ent_ptr[p]..ent_ptr[p+1]
+ * (owner, grouped row, weight) in the reference's slot order.  The landing
+ * worker merges: y_p (x w_p when multi) + sum w_r y_r (kernels::scale/axpy);
+ * source w then adds, per token in pilot order, merged row f scaled by
+ * flat_scale[f] (1 for multi-copy groups, else the pilot weight):
+ * src_ptr[w] [seq_lens[w]+1] / src_flat[w] is a token CSR of flat indices.
+ * All arrays are DEVICE arrays except seq_lens. */
+int xmoe_rbd_combine(xmoe_ctx* ctx, int dtype, int64_t H, const void* const* expert_out, int64_t P,
+                     const int32_t* land_of, const int32_t* land_pos, const uint8_t* land_multi, const double* land_w,
+                     const int32_t* ent_ptr, const int32_t* ent_owner, const int32_t* ent_pos, const double* ent_w,
+                     const int32_t* const* src_ptr, const int32_t* const* src_flat, const double* flat_scale,
+                     const int64_t* seq_lens, void* const* out, void* stream);
+
+/* Distinct (token, node) pairs among n copies (moesim::redundancy_rate*,
+ * internode_redundancy_counts, rbd.cpp:390-442): node = expert_node[expert]
+ * (device [E]), tokens < `tokens`, nodes < `nodes`; copies on skip_node are
+ * ignored (-1 = none).  *copies and *groups are host outputs (synchronises). */
+int xmoe_route_pairs(xmoe_ctx* ctx, int64_t n, const int32_t* token, const int32_t* expert,
+                     const int32_t* expert_node, int64_t E, int64_t nodes, int64_t tokens, int64_t skip_node,
+                     int64_t* copies, int64_t* groups, void* stream);
+
+/* ------------------------------------------------------------------ synthetic inputs
+ * The reference's generator on the device: outputs [offset, offset+n) of
+ * Rng(seed).uniform(lo, hi) (rng.hpp:24-47, xoshiro256** + 53-bit uniform),
+ * each snapped to multiples of 1/grid (round half even; grid 0 = none) and
+ * stored as dtype (XMOE_F64 | XMOE_F32 | XMOE_BF16, round to nearest even).
+ * GF(2) jump-ahead: any offset, no host draws. */
+int xmoe_rng_uniform(xmoe_ctx* ctx, uint64_t seed, uint64_t offset, int64_t n, double lo, double hi, double grid,
+                     int dtype, void* out, void* stream);
+/* moesim::salt_seed (rng.hpp:17-19). */
+uint64_t xmoe_salt_seed(uint64_t seed, uint64_t a, uint64_t b);
+/* moesim::make_layer_weights (padded_pipeline.cpp:13-27) on the device for
+ * Rng(seed) advanced by `offset` draws: gate [H,E] (NULL = skip; snapped to
+ * gate_grid when > 0) and experts [first_expert, first_expert + n_experts) of
+ * w1 [.,H,F] / w2 [.,F,H], in the reference layouts and draw order. */
+int xmoe_make_layer_weights(xmoe_ctx* ctx, uint64_t seed, uint64_t offset, int64_t E, int64_t H, int64_t F,
+                            int64_t first_expert, int64_t n_experts, double gate_grid, int dtype, void* gate,
+                            void* w1, void* w2, void* stream);
+
 /* ------------------------------------------------------------------ layer
  * One MoE layer's weights resident in HBM in the B200 layout, plus the
  * workspace of its forward pass.  Weights are DEVICE pointers in the
@@ -187,13 +285,26 @@ typedef struct {
 int xmoe_layer_create(xmoe_ctx* ctx, const xmoe_layer_desc* desc, const void* gate,
                       const void* w1, const void* w2, const void* sw1, const void* sw2,
                       xmoe_layer** out);
+/* Collective for one-process-per-GPU layers: every rank must call it (a flag
+ * barrier keeps a peer's last NVLink reads off this rank's freed buffers). */
 int xmoe_layer_destroy(xmoe_layer* layer);
+/* XMOE_OK, or XMOE_ERR_PEER_TIMEOUT when a cross-GPU wait of an earlier pass
+ * gave up after XMOE_PEER_TIMEOUT_S seconds (default 300) because a peer never
+ * arrived.  The wait does not trap the device: the pass finishes with invalid
+ * results and every later forward/backward on the layer returns this code. */
+int xmoe_layer_status(xmoe_layer* layer);
 
 /* moesim::pf_moe_forward / rbd_moe_forward (pf_pipeline.hpp:48-49, rbd.hpp:92)
  * selected by desc->dispatch_mode.  x/out: [n_local, S, H] where n_local = 1
  * for a rank >= 0 context and world for rank == -1.  Device buffers. */
 int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S, void* out,
                      void* stream);
+
+/* The same forward with a token count per worker (moe_instance.hpp:27 allows
+ * S_w to differ): S_per_worker [n_local] (host); x/out hold the workers'
+ * [S_w, H] blocks back to back.  Runs the unchunked pipeline. */
+int xmoe_moe_forward_v(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, const int64_t* S_per_worker, void* out,
+                       void* stream);
 
 /* moesim::ssmb_forward (ssmb.hpp:23-26, ssmb.cpp:12-46): x_full [S,H] is the
  * whole sequence on every rank; rank g runs rows [g*(S/G), ...) (last rank
@@ -217,9 +328,43 @@ int xmoe_moe_backward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, const voi
 /* Device pointers (fp32, owned by the layer) to the gradients of the last
  * backward, reference layouts: gate [H,E], w1 [E_local,H,F], w2 [E_local,F,H],
  * shared merged sw1 [H, n_shared*Fs] (expert s = columns s*Fs..), sw2
- * [n_shared*Fs, H].  Any argument may be NULL. */
+ * [n_shared*Fs, H].  Any argument may be NULL.
+ * Scope with one process per GPU: dw1/dw2 are COMPLETE for this rank's
+ * experts (every rank's tokens reach them through the exchange); dgate,
+ * dsw1 and dsw2 are PARTIAL sums over this rank's tokens only — all-reduce
+ * them over the expert-parallel group before the optimizer step. */
 int xmoe_layer_grads(xmoe_layer* layer, float** dgate, float** dw1, float** dw2, float** dsw1,
                      float** dsw2);
+
+/* Replace the layer's weights in place (e.g. after an optimizer step), same
+ * layouts and dtype as xmoe_layer_create, this rank's experts only; refreshes
+ * the B200-layout copies and, for training layers, the reference-layout
+ * copies the backward reads.  Stream-ordered; captured forwards stay valid. */
+int xmoe_layer_set_weights(xmoe_layer* layer, const void* gate, const void* w1, const void* w2, const void* sw1,
+                           const void* sw2, void* stream);
+
+/* Debug view of the last forward's internal arrays (synchronises the
+ * device): *ptr = a DEVICE pointer owned by the layer, *count = elements.
+ * `worker` indexes the ranks this context drives (0 for rank >= 0).  Used by
+ * the parity tests to compare the routing, the packed order and the grouped
+ * dispatch layout bit for bit with the reference's own pf_dispatch /
+ * select_pilots. */
+#define XMOE_INSPECT_TOP_EXPERTS 0       /* int32 [S,k] (gating.hpp:15-32) */
+#define XMOE_INSPECT_WEIGHTS 1           /* f64 [S,k] */
+#define XMOE_INSPECT_TOKEN_IDS 2         /* int32 [B] (pft.hpp:17-25) */
+#define XMOE_INSPECT_EXPERT_IDS 3        /* int32 [B] */
+#define XMOE_INSPECT_COMBINE_WEIGHTS 4   /* f64 [B] */
+#define XMOE_INSPECT_TOKENS_PER_EXPERT 5 /* int32 [E] */
+#define XMOE_INSPECT_TPE_ALL 6           /* int32 [W,E] all-gathered counts */
+#define XMOE_INSPECT_EXPERT_INPUT 7      /* dtype [R_max,H]: PfDispatch::expert_input (unchunked: rows 0..n) */
+#define XMOE_INSPECT_EXPERT_OUTPUT 8     /* dtype [R_max,H] */
+#define XMOE_INSPECT_RECV_PER_EXPERT 9   /* int32 [E/W] (unchunked layers) */
+#define XMOE_INSPECT_TPE_CHUNKS 10       /* int32 [W,C,E] (chunked layers: region c holds chunk c) */
+#define XMOE_INSPECT_DEST_RANK 11        /* int32 [B] owner of each packed row */
+#define XMOE_INSPECT_DEST_ROW 12         /* int32 [B] its grouped row at the owner */
+#define XMOE_INSPECT_SLOT_POS 13         /* int32 [S,k] packed rows of each token's kept copies */
+#define XMOE_INSPECT_PILOT_MASK 14       /* uint8 [B] RbdPlan::pilot_mask (rbd.hpp:28-41) */
+int xmoe_layer_inspect(xmoe_layer* layer, int worker, int what, const void** ptr, int64_t* count);
 
 /* Byte ledger of the last forward on this layer (collectives.hpp:31-49):
  * out[0..n) = { dispatch_rows_self, dispatch_rows_offrank,

@@ -16,12 +16,22 @@ _LIB = None
 
 F64 = 0
 BF16 = 1
+F32 = 2
 NAIVE = 0
 RBD = 1
 
 ERROR_KINDS = {1: "ParseError", 2: "ValidationError", 3: "DimensionError", 4: "IndexError",
                5: "CountMismatch", 6: "PlanMismatch", 10: "CudaError", 11: "NcclError",
-               99: "InternalError"}
+               12: "PeerTimeout", 99: "InternalError"}
+
+# xmoe_layer_inspect items (xmoe.h)
+INSPECT = {"top_experts": (0, torch.int32), "weights": (1, torch.float64), "token_ids": (2, torch.int32),
+           "expert_ids": (3, torch.int32), "combine_weights": (4, torch.float64),
+           "tokens_per_expert": (5, torch.int32), "tpe_all": (6, torch.int32), "expert_input": (7, None),
+           "expert_output": (8, None), "recv_per_expert": (9, torch.int32), "tpe_chunks": (10, torch.int32),
+           "dest_rank": (11, torch.int32), "dest_row": (12, torch.int32), "slot_pos": (13, torch.int32),
+           "pilot_mask": (14, torch.uint8)}
+_TDT = {F64: torch.float64, BF16: torch.bfloat16, F32: torch.float32}
 
 
 class XmoeError(RuntimeError):
@@ -106,6 +116,21 @@ def lib():
         L.xmoe_grouped_wgrad_bf16.argtypes = [p, p, p, i64, p, i64, i64, i64, p, p]
         L.xmoe_wgrad_split_bf16.argtypes = [p, p, p, i64, i64, i64, i64, p, p]
         L.xmoe_layer_grads.argtypes = [p] + [C.POINTER(p)] * 5
+        L.xmoe_layer_inspect.argtypes = [p, i32, i32, C.POINTER(p), C.POINTER(i64)]
+        L.xmoe_layer_status.argtypes = [p]
+        L.xmoe_layer_set_weights.argtypes = [p, p, p, p, p, p, p]
+        L.xmoe_rng_uniform.argtypes = [p, C.c_uint64, C.c_uint64, i64, C.c_double, C.c_double, C.c_double, i32, p, p]
+        L.xmoe_salt_seed.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
+        L.xmoe_salt_seed.restype = C.c_uint64
+        L.xmoe_make_layer_weights.argtypes = [p, C.c_uint64, C.c_uint64, i64, i64, i64, i64, i64, C.c_double, i32,
+                                              p, p, p, p]
+        pp = C.POINTER(p)
+        L.xmoe_pf_dispatch.argtypes = [p, i32, i64, i64, pp, pp, p, p, pp, p, pp, pp, pp, p]
+        L.xmoe_pf_combine.argtypes = [p, i32, i64, i64, pp, p, pp, pp, pp, p, p, pp, p]
+        L.xmoe_select_pilots.argtypes = [p, i64, p, p, i64, i64, i64, i64, i64, C.c_uint64, p, p, p]
+        L.xmoe_rbd_dispatch.argtypes = [p, i32, i64, i64, i64, pp, pp, pp, p, p, i64, p, pp, pp, p, pp, pp, pp, p]
+        L.xmoe_rbd_combine.argtypes = [p, i32, i64, pp, i64, p, p, p, p, p, p, p, p, pp, pp, p, p, pp, p]
+        L.xmoe_route_pairs.argtypes = [p, i64, p, p, p, i64, i64, i64, i64, C.POINTER(i64), C.POINTER(i64), p]
         _LIB = L
     return _LIB
 
@@ -117,6 +142,25 @@ def _check(rc: int):
 
 def _ptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _parr(ts):
+    """Host array of device pointers (None -> NULL)."""
+    arr = (C.c_void_p * max(1, len(ts)))()
+    for i, t in enumerate(ts):
+        arr[i] = None if t is None else t.data_ptr()
+    return arr
+
+
+def _i64arr(v):
+    import numpy as np
+    a = np.ascontiguousarray(v, dtype=np.int64)
+    return a, a.ctypes.data_as(C.c_void_p)
+
+
+def salt_seed(seed: int, a: int, b: int = 0) -> int:
+    """moesim::salt_seed (rng.hpp:17-19)."""
+    return int(lib().xmoe_salt_seed(seed, a, b))
 
 
 def _stream():
@@ -249,6 +293,106 @@ class Context:
                                       _ptr(out), _stream()))
         return out
 
+    # ------------------------------------------------------------ synthetic inputs
+    def rng_uniform(self, seed, offset, n, lo, hi, grid=0.0, dtype=F64, out=None):
+        """Outputs [offset, offset+n) of Rng(seed).uniform(lo, hi) on the device."""
+        out = torch.empty(n, dtype=_TDT[dtype], device="cuda") if out is None else out
+        _check(lib().xmoe_rng_uniform(self.h, seed, offset, n, lo, hi, grid, dtype, _ptr(out), _stream()))
+        return out
+
+    def make_layer_weights(self, seed, E, H, F, first_expert=0, n_experts=None, offset=0, gate_grid=0.0,
+                           dtype=F64, gate=True):
+        """moesim::make_layer_weights(Rng(seed)) on the device: gate [H,E] and
+        experts [first, first+n) of w1 [.,H,F], w2 [.,F,H]."""
+        n = E - first_expert if n_experts is None else n_experts
+        t = _TDT[dtype]
+        g = torch.empty((H, E), dtype=t, device="cuda") if gate else None
+        w1 = torch.empty((n, H, F), dtype=t, device="cuda")
+        w2 = torch.empty((n, F, H), dtype=t, device="cuda")
+        _check(lib().xmoe_make_layer_weights(self.h, seed, offset, E, H, F, first_expert, n, gate_grid, dtype,
+                                             _ptr(g), _ptr(w1), _ptr(w2), _stream()))
+        return g, w1, w2
+
+    # ------------------------------------------------------------ split EP operators (SPMD shape)
+    def pf_dispatch(self, dtype, H, E, packed, expert_ids, tpe, want_arrival=True):
+        """xmoe_pf_dispatch: per-worker packed rows / expert ids (device
+        tensors), tpe [W,E] int32 device.  Returns (expert_input list,
+        recv_per_expert [W,El], dest_rank list, dest_row list, arrival list)."""
+        W = len(packed)
+        El = E // W
+        th = tpe.cpu().numpy().reshape(W, E)
+        n_own = [int(th[:, j * El:(j + 1) * El].sum()) for j in range(W)]
+        dt = packed[0].dtype
+        ei = [torch.empty((max(n, 1), H), dtype=dt, device="cuda") for n in n_own]
+        rpe = torch.empty((W, El), dtype=torch.int32, device="cuda")
+        dr = [torch.empty(max(1, p.shape[0]), dtype=torch.int32, device="cuda") for p in packed]
+        dw = [torch.empty(max(1, p.shape[0]), dtype=torch.int32, device="cuda") for p in packed]
+        a2g = [torch.empty(max(n, 1), dtype=torch.int32, device="cuda") for n in n_own] if want_arrival else None
+        B, Bp = _i64arr([p.shape[0] for p in packed])
+        _check(lib().xmoe_pf_dispatch(self.h, dtype, H, E, _parr(packed), _parr(expert_ids), Bp, _ptr(tpe),
+                                      _parr(ei), _ptr(rpe), _parr(dr), _parr(dw),
+                                      _parr(a2g) if want_arrival else None, _stream()))
+        return ([e[:n] for e, n in zip(ei, n_own)], rpe, dr, dw,
+                [a[:n] for a, n in zip(a2g, n_own)] if want_arrival else None)
+
+    def pf_combine(self, dtype, H, E, expert_out, tpe, token_ids, expert_ids, cw, seq_lens):
+        W = len(expert_out)
+        out = [torch.empty((max(S, 1), H), dtype=expert_out[0].dtype, device="cuda") for S in seq_lens]
+        B, Bp = _i64arr([t.shape[0] for t in token_ids])
+        Sl, Sp = _i64arr(seq_lens)
+        eo = [e if e.numel() else torch.empty((1, H), dtype=expert_out[0].dtype, device="cuda") for e in expert_out]
+        _check(lib().xmoe_pf_combine(self.h, dtype, H, E, _parr(eo), _ptr(tpe), _parr(token_ids),
+                                     _parr(expert_ids), _parr(cw), Bp, Sp, _parr(out), _stream()))
+        return [o[:S] for o, S in zip(out, seq_lens)]
+
+    def select_pilots(self, token_ids, expert_ids, S, k, E, W, gpus_per_node, seed):
+        B = token_ids.shape[0]
+        mask = torch.zeros(max(B, 1), dtype=torch.uint8, device="cuda")
+        pof = torch.empty(max(B, 1), dtype=torch.int32, device="cuda")
+        _check(lib().xmoe_select_pilots(self.h, B, _ptr(token_ids), _ptr(expert_ids), S, k, E, W, gpus_per_node,
+                                        seed, _ptr(mask), _ptr(pof), _stream()))
+        return mask[:B], pof[:B]
+
+    def rbd_dispatch(self, dtype, H, E, gpus_per_node, packed, token_ids, expert_ids, seq_lens, k, tpe, masks):
+        W = len(packed)
+        El = E // W
+        th = tpe.cpu().numpy().reshape(W, E)
+        n_own = [int(th[:, j * El:(j + 1) * El].sum()) for j in range(W)]
+        dt = packed[0].dtype
+        ei = [torch.empty((max(n, 1), H), dtype=dt, device="cuda") for n in n_own]
+        rpe = torch.empty((W, El), dtype=torch.int32, device="cuda")
+        mk = lambda: [torch.empty(max(1, p.shape[0]), dtype=torch.int32, device="cuda") for p in packed]  # noqa
+        dr, dw, pof = mk(), mk(), mk()
+        B, Bp = _i64arr([p.shape[0] for p in packed])
+        Sl, Sp = _i64arr(seq_lens)
+        _check(lib().xmoe_rbd_dispatch(self.h, dtype, H, E, gpus_per_node, _parr(packed), _parr(token_ids),
+                                       _parr(expert_ids), Bp, Sp, k, _ptr(tpe), _parr(masks), _parr(ei), _ptr(rpe),
+                                       _parr(dr), _parr(dw), _parr(pof), _stream()))
+        return [e[:n] for e, n in zip(ei, n_own)], rpe, dr, dw, pof
+
+    def rbd_combine(self, dtype, H, expert_out, flat, seq_lens):
+        """flat: dict of device tensors land_of, land_pos, land_multi, land_w,
+        ent_ptr, ent_owner, ent_pos, ent_w, flat_scale and per-source lists
+        src_ptr, src_flat (see xmoe.h)."""
+        P = int(flat["land_of"].shape[0])
+        out = [torch.empty((max(S, 1), H), dtype=expert_out[0].dtype, device="cuda") for S in seq_lens]
+        Sl, Sp = _i64arr(seq_lens)
+        eo = [e if e.numel() else torch.empty((1, H), dtype=expert_out[0].dtype, device="cuda") for e in expert_out]
+        f = flat
+        _check(lib().xmoe_rbd_combine(self.h, dtype, H, _parr(eo), P, _ptr(f["land_of"]), _ptr(f["land_pos"]),
+                                      _ptr(f["land_multi"]), _ptr(f["land_w"]), _ptr(f["ent_ptr"]),
+                                      _ptr(f["ent_owner"]), _ptr(f["ent_pos"]), _ptr(f["ent_w"]),
+                                      _parr(f["src_ptr"]), _parr(f["src_flat"]), _ptr(f["flat_scale"]), Sp,
+                                      _parr(out), _stream()))
+        return [o[:S] for o, S in zip(out, seq_lens)]
+
+    def route_pairs(self, token, expert, expert_node, nodes, tokens, skip_node=-1):
+        c, g = C.c_int64(), C.c_int64()
+        _check(lib().xmoe_route_pairs(self.h, token.shape[0], _ptr(token), _ptr(expert), _ptr(expert_node),
+                                      expert_node.shape[0], nodes, tokens, skip_node, C.byref(c), C.byref(g),
+                                      _stream()))
+        return int(c.value), int(g.value)
+
     def grouped_gemm_bf16(self, A, rows_per_group, B, N, relu=False, out=None):
         rows, K = A.shape
         G = rows_per_group.shape[0]
@@ -334,6 +478,31 @@ class Layer:
             out["sw1"] = view(ptrs[3], (H, sh["ns"] * sh["Fs"]))
             out["sw2"] = view(ptrs[4], (sh["ns"] * sh["Fs"], H))
         return out
+
+    def inspect(self, what: str, worker: int = 0):
+        """Copy of one internal array of the last forward (xmoe_layer_inspect)."""
+        code, dt = INSPECT[what]
+        if dt is None:
+            dt = _TDT[self.dtype]
+        p, n = C.c_void_p(), C.c_int64()
+        _check(lib().xmoe_layer_inspect(self.h, worker, code, C.byref(p), C.byref(n)))
+        if n.value == 0 or not p.value:
+            return torch.empty(0, dtype=dt, device="cuda")
+        typestr = {torch.int32: "<i4", torch.float64: "<f8", torch.uint8: "|u1", torch.float32: "<f4",
+                   torch.bfloat16: "<i2"}[dt]
+
+        class _Dev:
+            __cuda_array_interface__ = {"shape": (n.value,), "typestr": typestr, "data": (p.value, False),
+                                        "version": 3}
+        t = torch.as_tensor(_Dev(), device="cuda").clone()
+        return t.view(torch.bfloat16) if dt == torch.bfloat16 else t
+
+    def status(self):
+        _check(lib().xmoe_layer_status(self.h))
+
+    def set_weights(self, gate, w1, w2, sw1=None, sw2=None):
+        _check(lib().xmoe_layer_set_weights(self.h, _ptr(gate), _ptr(w1), _ptr(w2), _ptr(sw1), _ptr(sw2),
+                                            _stream()))
 
     def ssmb_forward(self, x_full, out=None):
         S = x_full.shape[0]

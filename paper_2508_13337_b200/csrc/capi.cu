@@ -35,19 +35,6 @@ std::atomic<unsigned long long> g_kernel_launches{0};
             ::xmoe::fail(XMOE_ERR_NCCL, std::string(#expr ": ") + ncclGetErrorString(_r)); \
     } while (0)
 
-template <class F>
-static int guarded(F&& f) {
-    try {
-        f();
-        return XMOE_OK;
-    } catch (const Error& e) {
-        g_last_error = e.what();
-        return e.code;
-    } catch (const std::exception& e) {
-        g_last_error = e.what();
-        return XMOE_ERR_INTERNAL;
-    }
-}
 
 static size_t elem_size(int dtype) {
     if (dtype == XMOE_F64) return 8;
@@ -84,12 +71,6 @@ Ctx::~Ctx() {
 
 using namespace xmoe;
 
-struct xmoe_ctx {
-    Ctx c;
-};
-struct xmoe_layer {
-    Layer l;
-};
 
 extern "C" {
 
@@ -324,7 +305,108 @@ int xmoe_layer_create(xmoe_ctx* ctx, const xmoe_layer_desc* desc, const void* ga
 }
 
 int xmoe_layer_destroy(xmoe_layer* layer) {
-    return guarded([&] { delete layer; });
+    return guarded([&] {
+        if (!layer) return;
+        std::unique_ptr<xmoe_layer> own(layer);
+        own->l.quiesce();  // peers may still read this rank's symmetric region
+    });
+}
+
+int xmoe_layer_set_weights(xmoe_layer* layer, const void* gate, const void* w1, const void* w2, const void* sw1,
+                           const void* sw2, void* stream) {
+    return guarded([&] {
+        Layer& L = layer->l;
+        require(gate && w1 && w2, XMOE_ERR_VALIDATION, "gate, w1 and w2 are required");
+        require(L.Fs == 0 || (sw1 && sw2), XMOE_ERR_VALIDATION, "shared expert weights missing");
+        layer_load_weights(L, gate, w1, w2, sw1, sw2, static_cast<cudaStream_t>(stream));
+        // captured forwards read the weight buffers in place: still valid
+    });
+}
+
+int xmoe_layer_inspect(xmoe_layer* layer, int worker, int what, const void** ptr, int64_t* count) {
+    return guarded([&] {
+        Layer& L = layer->l;
+        require(ptr && count, XMOE_ERR_VALIDATION, "null output");
+        require(worker >= 0 && worker < L.nl, XMOE_ERR_VALIDATION, "worker out of range");
+        Worker& w = L.workers[worker];
+        XMOE_CUDA(cudaDeviceSynchronize());
+        int32_t B = 0;
+        XMOE_CUDA(cudaMemcpy(&B, w.B_dev, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        const long long S = L.last_S, Sk = S * L.k;
+        const void* p = nullptr;
+        long long n = 0;
+        switch (what) {
+            case XMOE_INSPECT_TOP_EXPERTS: p = w.top; n = Sk; break;
+            case XMOE_INSPECT_WEIGHTS: p = w.wts; n = Sk; break;
+            case XMOE_INSPECT_TOKEN_IDS: p = w.token_ids; n = B; break;
+            case XMOE_INSPECT_EXPERT_IDS: p = w.expert_ids; n = B; break;
+            case XMOE_INSPECT_COMBINE_WEIGHTS: p = w.cw; n = B; break;
+            case XMOE_INSPECT_TOKENS_PER_EXPERT: p = w.tpe; n = L.E; break;
+            case XMOE_INSPECT_TPE_ALL: p = L.tpe_all; n = static_cast<long long>(L.W) * L.E; break;
+            case XMOE_INSPECT_EXPERT_INPUT: p = w.recv; n = L.R_max * L.H; break;
+            case XMOE_INSPECT_EXPERT_OUTPUT: p = w.eout; n = L.R_max * L.H; break;
+            case XMOE_INSPECT_RECV_PER_EXPERT:
+                require(L.nchunks == 1, XMOE_ERR_VALIDATION, "chunked layers keep per-chunk regions (XMOE_INSPECT_TPE_CHUNKS)");
+                p = w.rpe; n = L.El; break;
+            case XMOE_INSPECT_TPE_CHUNKS:
+                require(L.nchunks > 1, XMOE_ERR_VALIDATION, "layer is not chunked");
+                p = L.tpe_c_all; n = static_cast<long long>(L.W) * L.nchunks * L.E; break;
+            case XMOE_INSPECT_DEST_RANK: p = w.dest_rank; n = B; break;
+            case XMOE_INSPECT_DEST_ROW: p = w.dest_row; n = B; break;
+            case XMOE_INSPECT_SLOT_POS: p = w.slot_pos; n = Sk; break;
+            case XMOE_INSPECT_PILOT_MASK: {
+                require(L.d.dispatch_mode == XMOE_DISPATCH_RBD, XMOE_ERR_VALIDATION, "not a redundancy-bypassing layer");
+                if (!L.dbg_mask) L.dbg_mask = static_cast<uint8_t*>(L.alloc(static_cast<size_t>(L.S_max) * L.k + 16));
+                XMOE_CUDA(cudaMemset(L.dbg_mask, 0, static_cast<size_t>(L.S_max) * L.k + 16));
+                launch_mask_from_groups(w.rbd, w.slot_pos, L.k, Sk, L.dbg_mask, nullptr, nullptr);
+                XMOE_CUDA(cudaDeviceSynchronize());
+                p = L.dbg_mask; n = B; break;
+            }
+            default: fail(XMOE_ERR_VALIDATION, "unknown inspect item");
+        }
+        *ptr = p;
+        *count = n;
+    });
+}
+
+int xmoe_rng_uniform(xmoe_ctx* ctx, uint64_t seed, uint64_t offset, int64_t n, double lo, double hi, double grid,
+                     int dtype, void* out, void* stream) {
+    return guarded([&] {
+        (void)ctx;
+        require(dtype == XMOE_F64 || dtype == XMOE_F32 || dtype == XMOE_BF16, XMOE_ERR_VALIDATION, "unknown dtype");
+        launch_rng_uniform(seed, offset, n, lo, hi, grid, dtype, out, static_cast<cudaStream_t>(stream));
+    });
+}
+
+uint64_t xmoe_salt_seed(uint64_t seed, uint64_t a, uint64_t b) { return salt_seed_host(seed, a, b); }
+
+int xmoe_make_layer_weights(xmoe_ctx* ctx, uint64_t seed, uint64_t offset, int64_t E, int64_t H, int64_t F,
+                            int64_t first_expert, int64_t n_experts, double gate_grid, int dtype, void* gate,
+                            void* w1, void* w2, void* stream) {
+    return guarded([&] {
+        require(E >= 1 && H >= 1 && F >= 1, XMOE_ERR_VALIDATION, "dims must be >= 1");
+        require(first_expert >= 0 && n_experts >= 0 && first_expert + n_experts <= E, XMOE_ERR_VALIDATION,
+                "expert slice out of range");
+        require(dtype == XMOE_F64 || dtype == XMOE_F32 || dtype == XMOE_BF16, XMOE_ERR_VALIDATION, "unknown dtype");
+        (void)ctx;
+        auto st = static_cast<cudaStream_t>(stream);
+        const size_t es = dtype == XMOE_F64 ? 8 : dtype == XMOE_F32 ? 4 : 2;
+        const unsigned long long hf = static_cast<unsigned long long>(H) * F;
+        // make_layer_weights draw order (padded_pipeline.cpp:13-27, gating.cpp:59-63):
+        // gate [H,E], then per expert w1 [H,F] and w2 [F,H], all uniform(-0.1, 0.1)
+        if (gate) launch_rng_uniform(seed, offset, H * E, -0.1, 0.1, gate_grid, dtype, gate, st);
+        for (int64_t i = 0; i < n_experts; ++i) {
+            const unsigned long long o = offset + static_cast<unsigned long long>(H) * E + 2 * hf * (first_expert + i);
+            if (w1) launch_rng_uniform(seed, o, static_cast<long long>(hf), -0.1, 0.1, 0.0, dtype,
+                                       static_cast<char*>(w1) + i * hf * es, st);
+            if (w2) launch_rng_uniform(seed, o + hf, static_cast<long long>(hf), -0.1, 0.1, 0.0, dtype,
+                                       static_cast<char*>(w2) + i * hf * es, st);
+        }
+    });
+}
+
+int xmoe_layer_status(xmoe_layer* layer) {
+    return guarded([&] { layer->l.check_peers(); });
 }
 
 int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S, void* out,
@@ -375,6 +457,17 @@ int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S,
         L.graphs.push_back({x, out, S, exec, kernels});
         XMOE_CUDA(cudaGraphLaunch(exec, st));
         g_kernel_launches.fetch_add(kernels, std::memory_order_relaxed);
+    });
+}
+
+int xmoe_moe_forward_v(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, const int64_t* S_per_worker, void* out,
+                       void* stream) {
+    return guarded([&] {
+        require(layer->l.ctx == &ctx->c, XMOE_ERR_VALIDATION, "layer belongs to another context");
+        require(S_per_worker != nullptr, XMOE_ERR_VALIDATION, "null token counts");
+        Layer& L = layer->l;
+        std::vector<long long> Sw(S_per_worker, S_per_worker + L.nl);
+        layer_forward_v(L, x, Sw.data(), out, static_cast<cudaStream_t>(stream));
     });
 }
 

@@ -14,6 +14,8 @@
 // region instead of NCCL all-reduces: flag[phase][c][src] on every owner,
 // written with st.release.sys by the source after its phase-c work, polled
 // with ld.acquire.sys by the consumer.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -94,6 +96,41 @@ __global__ void dispatch_dest_chunked_kernel(const int32_t* __restrict__ expert_
     }
 }
 
+// Peer-flag wait with a bounded spin.  A peer that never arrives (rank
+// skew beyond the timeout, a dead process) must not kill the CUDA context:
+// the waiter records the failed slot in the layer's host-mapped error word
+// and returns; the host turns it into XMOE_ERR_PEER_TIMEOUT on the next call
+// (xmoe_layer_status).  Once the word is set every later wait returns at once.
+// The timeout is XMOE_PEER_TIMEOUT_S (default 300 s), read once per process.
+__device__ __forceinline__ void wait_flag(const unsigned* f, unsigned e, unsigned long long timeout_ns, int slot,
+                                          int* err, unsigned ns) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        unsigned v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (static_cast<int>(v - e) >= 0) return;
+        if (*reinterpret_cast<volatile int*>(err) != 0) return;
+        __nanosleep(ns);
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > timeout_ns) {
+            atomicCAS(err, 0, 0x100 | slot);
+            __threadfence_system();
+            return;
+        }
+    }
+}
+
+unsigned long long peer_timeout_ns() {
+    static const unsigned long long ns = [] {
+        const char* e = std::getenv("XMOE_PEER_TIMEOUT_S");
+        const double s = e ? std::atof(e) : 300.0;
+        return static_cast<unsigned long long>((s > 0 ? s : 300.0) * 1e9);
+    }();
+    return ns;
+}
+
 __global__ void forward_begin_kernel(int32_t* s_rows, int S, unsigned* epoch) {
     if (threadIdx.x == 0) {
         *s_rows = S;
@@ -112,23 +149,9 @@ __global__ void flag_signal_kernel(unsigned* const* __restrict__ flag_tab, int W
 }
 
 __global__ void flag_wait_kernel(const unsigned* __restrict__ flags, int W, int slot,
-                                 const unsigned* __restrict__ epoch) {
+                                 const unsigned* __restrict__ epoch, unsigned long long tmo, int* err) {
     const int s = threadIdx.x;
-    if (s < W) {
-        const unsigned e = *epoch;
-        const unsigned* f = flags + static_cast<size_t>(slot) * W + s;
-        unsigned long long t0;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        for (;;) {
-            unsigned v;
-            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-            if (static_cast<int>(v - e) >= 0) break;
-            __nanosleep(100);
-            unsigned long long t1;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            if (t1 - t0 > 20000000000ull) __trap();  // a peer never arrived: fail, do not hang
-        }
-    }
+    if (s < W) wait_flag(flags + static_cast<size_t>(slot) * W + s, *epoch, tmo, slot, err, 100);
     __syncthreads();
 }
 
@@ -141,7 +164,7 @@ __global__ void flag_wait_kernel(const unsigned* __restrict__ flags, int W, int 
 __global__ void counts_exchange_kernel(CountSegs segs, int32_t* const* __restrict__ area_tab, int area_ints,
                                        int me, int W, unsigned* const* __restrict__ flag_tab,
                                        const unsigned* __restrict__ my_flags, int slot,
-                                       const unsigned* __restrict__ epoch) {
+                                       const unsigned* __restrict__ epoch, unsigned long long tmo, int* err) {
     const unsigned e = *epoch;
     const int par = static_cast<int>(e & 1u);
     for (int p = 0; p < W; ++p) {
@@ -158,18 +181,7 @@ __global__ void counts_exchange_kernel(CountSegs segs, int32_t* const* __restric
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag_tab[t] + static_cast<size_t>(slot) * W + me),
                      "r"(e)
                      : "memory");
-        const unsigned* f = my_flags + static_cast<size_t>(slot) * W + t;
-        unsigned long long t0;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        for (;;) {
-            unsigned v;
-            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-            if (static_cast<int>(v - e) >= 0) break;
-            __nanosleep(64);
-            unsigned long long t1;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            if (t1 - t0 > 20000000000ull) __trap();
-        }
+        wait_flag(my_flags + static_cast<size_t>(slot) * W + t, e, tmo, slot, err, 64);
     }
     __syncthreads();
     const int32_t* mine = area_tab[me] + static_cast<size_t>(par) * area_ints;
@@ -182,7 +194,8 @@ __global__ void counts_exchange_kernel(CountSegs segs, int32_t* const* __restric
 // Cross-GPU barrier on one flag slot (every rank's previous kernels on this
 // stream are complete and their peer stores visible when it passes).
 __global__ void flag_barrier_kernel(unsigned* const* __restrict__ flag_tab, const unsigned* __restrict__ my_flags,
-                                    int W, int me, int slot, const unsigned* __restrict__ epoch) {
+                                    int W, int me, int slot, const unsigned* __restrict__ epoch,
+                                    unsigned long long tmo, int* err) {
     const unsigned e = *epoch;
     const int t = threadIdx.x;
     __threadfence_system();
@@ -191,32 +204,23 @@ __global__ void flag_barrier_kernel(unsigned* const* __restrict__ flag_tab, cons
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag_tab[t] + static_cast<size_t>(slot) * W + me),
                      "r"(e)
                      : "memory");
-        const unsigned* f = my_flags + static_cast<size_t>(slot) * W + t;
-        unsigned long long t0;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        for (;;) {
-            unsigned v;
-            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-            if (static_cast<int>(v - e) >= 0) break;
-            __nanosleep(64);
-            unsigned long long t1;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            if (t1 - t0 > 20000000000ull) __trap();
-        }
+        wait_flag(my_flags + static_cast<size_t>(slot) * W + t, e, tmo, slot, err, 64);
     }
     __syncthreads();
 }
 
 void launch_counts_exchange(const CountSegs& segs, int32_t* const* area_tab, int area_ints, int me, int W,
                             unsigned* const* flag_tab, const unsigned* my_flags, int slot, const unsigned* epoch,
-                            cudaStream_t st) {
-    counts_exchange_kernel<<<1, 256, 0, st>>>(segs, area_tab, area_ints, me, W, flag_tab, my_flags, slot, epoch);
+                            int* err, cudaStream_t st) {
+    counts_exchange_kernel<<<1, 256, 0, st>>>(segs, area_tab, area_ints, me, W, flag_tab, my_flags, slot, epoch,
+                                              peer_timeout_ns(), err);
     XMOE_LAUNCH_CHECK();
 }
 
 void launch_flag_barrier(unsigned* const* flag_tab, const unsigned* my_flags, int W, int me, int slot,
-                         const unsigned* epoch, cudaStream_t st) {
-    flag_barrier_kernel<<<1, 32 * ((W + 31) / 32), 0, st>>>(flag_tab, my_flags, W, me, slot, epoch);
+                         const unsigned* epoch, int* err, cudaStream_t st) {
+    flag_barrier_kernel<<<1, 32 * ((W + 31) / 32), 0, st>>>(flag_tab, my_flags, W, me, slot, epoch,
+                                                            peer_timeout_ns(), err);
     XMOE_LAUNCH_CHECK();
 }
 
@@ -256,8 +260,8 @@ void launch_flag_signal(unsigned* const* flag_tab, int W, int me, int slot, cons
     XMOE_LAUNCH_CHECK();
 }
 
-void launch_flag_wait(const unsigned* flags, int W, int slot, const unsigned* epoch, cudaStream_t st) {
-    flag_wait_kernel<<<1, 32 * ((W + 31) / 32), 0, st>>>(flags, W, slot, epoch);
+void launch_flag_wait(const unsigned* flags, int W, int slot, const unsigned* epoch, int* err, cudaStream_t st) {
+    flag_wait_kernel<<<1, 32 * ((W + 31) / 32), 0, st>>>(flags, W, slot, epoch, peer_timeout_ns(), err);
     XMOE_LAUNCH_CHECK();
 }
 

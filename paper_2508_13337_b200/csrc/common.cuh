@@ -24,6 +24,23 @@ inline void require(bool ok, int code, const char* m) {
     if (!ok) fail(code, m);
 }
 
+// C-ABI wrapper: runs f, maps typed failures to status codes and keeps the
+// message for xmoe_last_error() (thread-local).
+extern thread_local std::string g_last_error;
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return XMOE_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return XMOE_ERR_INTERNAL;
+    }
+}
+
 #define XMOE_CUDA(expr)                                                               \
     do {                                                                              \
         cudaError_t _e = (expr);                                                      \

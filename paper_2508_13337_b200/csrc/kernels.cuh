@@ -136,14 +136,17 @@ void launch_dispatch_dest_chunked(const int32_t* expert_ids, const int32_t* toke
 void launch_forward_begin(int32_t* s_rows, int S, unsigned* epoch, cudaStream_t st);
 void launch_flag_signal(unsigned* const* flag_tab, int W, int me, int slot, const unsigned* epoch,
                         cudaStream_t st);
-void launch_flag_wait(const unsigned* flags, int W, int slot, const unsigned* epoch, cudaStream_t st);
+// waits give up after XMOE_PEER_TIMEOUT_S (default 300 s) and record the slot
+// in *err (the layer's host-mapped error word) instead of trapping
+void launch_flag_wait(const unsigned* flags, int W, int slot, const unsigned* epoch, int* err, cudaStream_t st);
 // flag slots per rank: [0, kMaxChunks) chunk dispatch, [kMaxChunks, 2 kMaxChunks)
 // chunk combine, then the count exchange, the unchunked forward's barriers
 // and the backward's two barriers (same epoch as the forward they follow)
 constexpr int kSlotCounts = 2 * kMaxChunks;
 constexpr int kSlotBar = 2 * kMaxChunks + 1;     // + 0..3
 constexpr int kSlotBwdBar = 2 * kMaxChunks + 5;  // + 0..1
-constexpr int kFlagSlots = 2 * kMaxChunks + 7;
+constexpr int kSlotQuiesce = 2 * kMaxChunks + 7;  // layer teardown
+constexpr int kFlagSlots = 2 * kMaxChunks + 8;
 struct CountSeg {
     const int32_t* src;  // my row
     int row;             // ints per rank row
@@ -156,8 +159,8 @@ struct CountSegs {
 };
 void launch_counts_exchange(const CountSegs& segs, int32_t* const* area_tab, int area_ints, int me, int W,
                             unsigned* const* flag_tab, const unsigned* my_flags, int slot, const unsigned* epoch,
-                            cudaStream_t st);
+                            int* err, cudaStream_t st);
 void launch_flag_barrier(unsigned* const* flag_tab, const unsigned* my_flags, int W, int me, int slot,
-                         const unsigned* epoch, cudaStream_t st);
+                         const unsigned* epoch, int* err, cudaStream_t st);
 
 }  // namespace xmoe

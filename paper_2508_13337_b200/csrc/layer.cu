@@ -69,6 +69,26 @@ Layer::~Layer() {
     for (void* p : peer_maps) cudaIpcCloseMemHandle(p);
     for (void* p : allocs) cudaFree(p);
     for (auto& e : events) cudaEventDestroy(e);
+    if (peer_err_h) cudaFreeHost(peer_err_h);
+}
+
+// Cross-rank quiesce before the symmetric region is unmapped and freed: a
+// peer's last combine may still be reading this rank's expert outputs over
+// NVLink.  One flag barrier on a dedicated slot (same epoch on every rank:
+// every rank ran the same forwards), then a local synchronise.
+void Layer::quiesce() {
+    if (!(distributed && p2p) || !flag_tab || !epoch) return;
+    XMOE_CUDA(cudaDeviceSynchronize());  // this rank's own passes are done
+    launch_flag_barrier(flag_tab, workers[0].flags, W, workers[0].rank, kSlotQuiesce, epoch, peer_err_d, cap_stream);
+    XMOE_CUDA(cudaStreamSynchronize(cap_stream));
+}
+
+// XMOE_ERR_PEER_TIMEOUT when a peer-flag wait of an earlier pass gave up
+void Layer::check_peers() const {
+    if (peer_err_h && *reinterpret_cast<volatile int*>(peer_err_h) != 0)
+        fail(XMOE_ERR_PEER_TIMEOUT, "a peer rank did not reach flag slot " +
+                                        std::to_string(*peer_err_h & 0xff) +
+                                        " within XMOE_PEER_TIMEOUT_S; the layer's exchange state is invalid");
 }
 
 void* Layer::alloc(size_t bytes) {
@@ -92,6 +112,58 @@ long long Layer::C(int s, int d) const {
     return a;
 }
 
+// Weights in, from the reference layouts (moe_instance.hpp:17-21): F64 keeps
+// them; BF16 goes K-major (gate [E,H], w1 [El,F,H], w2 [El,H,F], merged
+// shared [ns*Fs,H] / [H,ns*Fs]); training layers also refresh their
+// reference-layout copies (the dgrad B operands).  Stream-ordered on st.
+void layer_load_weights(Layer& L, const void* gate, const void* w1, const void* w2, const void* sw1, const void* sw2,
+                        cudaStream_t st) {
+    const int H = L.H, F = L.F, E = L.E;
+    const size_t es = L.es;
+    const bool bf = L.d.dtype == XMOE_BF16;
+    const size_t ew = static_cast<size_t>(L.E_held) * H * F;
+    const auto cp = [&](void* d, const void* s, size_t b) {
+        XMOE_CUDA(cudaMemcpyAsync(d, s, b, cudaMemcpyDeviceToDevice, st));
+    };
+    if (!bf) {
+        cp(L.gate, gate, static_cast<size_t>(H) * E * es);
+        cp(L.w1, w1, ew * es);
+        cp(L.w2, w2, ew * es);
+    } else {
+        launch_transpose(XMOE_BF16, gate, 1, H, E, XMOE_BF16, L.gate, st);       // [E,H]
+        launch_transpose(XMOE_BF16, w1, L.E_held, H, F, XMOE_BF16, L.w1, st);    // [El,F,H]
+        launch_transpose(XMOE_BF16, w2, L.E_held, F, H, XMOE_BF16, L.w2, st);    // [El,H,F]
+    }
+    const int ns = static_cast<int>(L.d.n_shared), Fs1 = static_cast<int>(L.d.shared_ffn_dim);
+    // merged shared FFN (moe_oracle.shared_expert_forward): W1cat [H, ns*Fs], W2cat [ns*Fs, H]
+    const auto cat_w1 = [&](void* dst) {
+        for (int s = 0; s < ns; ++s)
+            XMOE_CUDA(cudaMemcpy2DAsync(static_cast<char*>(dst) + static_cast<size_t>(s) * Fs1 * es,
+                                        static_cast<size_t>(L.Fs) * es,
+                                        static_cast<const char*>(sw1) + static_cast<size_t>(s) * H * Fs1 * es,
+                                        static_cast<size_t>(Fs1) * es, static_cast<size_t>(Fs1) * es, H,
+                                        cudaMemcpyDeviceToDevice, st));
+    };
+    if (L.Fs > 0) {
+        if (!bf) {
+            cat_w1(L.sw1);
+            cp(L.sw2, sw2, static_cast<size_t>(H) * L.Fs * es);
+        } else {
+            launch_transpose(XMOE_BF16, sw1, ns, H, Fs1, XMOE_BF16, L.sw1, st);  // [ns*Fs, H]
+            launch_transpose(XMOE_BF16, sw2, 1, L.Fs, H, XMOE_BF16, L.sw2, st);  // [H, ns*Fs]
+        }
+    }
+    if (L.train) {
+        cp(L.w1r, w1, ew * es);
+        cp(L.w2r, w2, ew * es);
+        cp(L.gater, gate, static_cast<size_t>(H) * E * es);
+        if (L.Fs > 0) {
+            cat_w1(L.sw1r);
+            cp(L.sw2r, sw2, static_cast<size_t>(H) * L.Fs * es);
+        }
+    }
+}
+
 // ---------------------------------------------------------------- creation
 void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const void* w1,
                   const void* w2, const void* sw1, const void* sw2, Layer& L) {
@@ -104,6 +176,10 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     require(d.num_experts % W == 0, XMOE_ERR_VALIDATION,
             "num_experts must be divisible by the worker-group size");
     require(d.model_dim >= 1 && d.ffn_dim >= 1, XMOE_ERR_VALIDATION, "dims must be >= 1");
+    // kernel limits checked up front, so a layer never fails half-way through a pass
+    require(d.num_experts <= 1024, XMOE_ERR_VALIDATION, "num_experts must be <= 1024");
+    require(!(d.flags & XMOE_LAYER_TRAIN) || (d.num_experts <= 256 && d.top_k <= 32), XMOE_ERR_VALIDATION,
+            "training layers support num_experts <= 256 and top_k <= 32");
     require(d.dispatch_mode == XMOE_DISPATCH_NAIVE || d.dispatch_mode == XMOE_DISPATCH_RBD,
             XMOE_ERR_VALIDATION, "unknown dispatch mode");
     const bool bf = d.dtype == XMOE_BF16;
@@ -159,35 +235,12 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     L.gate = L.alloc(static_cast<size_t>(H) * E * es);
     L.w1 = L.alloc(static_cast<size_t>(L.E_held) * H * F * es);
     L.w2 = L.alloc(static_cast<size_t>(L.E_held) * H * F * es);
-    if (!bf) {
-        XMOE_CUDA(cudaMemcpy(L.gate, gate, static_cast<size_t>(H) * E * es, cudaMemcpyDeviceToDevice));
-        XMOE_CUDA(cudaMemcpy(L.w1, w1, static_cast<size_t>(L.E_held) * H * F * es, cudaMemcpyDeviceToDevice));
-        XMOE_CUDA(cudaMemcpy(L.w2, w2, static_cast<size_t>(L.E_held) * H * F * es, cudaMemcpyDeviceToDevice));
-    } else {
-        launch_transpose(XMOE_BF16, gate, 1, H, E, XMOE_BF16, L.gate, st);       // [E,H]
-        launch_transpose(XMOE_BF16, w1, L.E_held, H, F, XMOE_BF16, L.w1, st);    // [El,F,H]
-        launch_transpose(XMOE_BF16, w2, L.E_held, F, H, XMOE_BF16, L.w2, st);    // [El,H,F]
-    }
     if (L.Fs > 0) {
         require(sw1 && sw2, XMOE_ERR_VALIDATION, "shared expert weights missing");
-        const int ns = static_cast<int>(d.n_shared), Fs1 = static_cast<int>(d.shared_ffn_dim);
         L.sw1 = L.alloc(static_cast<size_t>(H) * L.Fs * es);
         L.sw2 = L.alloc(static_cast<size_t>(H) * L.Fs * es);
-        // merged shared FFN (moe_oracle.shared_expert_forward): W1cat [H, ns*Fs], W2cat [ns*Fs, H]
-        if (!bf) {
-            for (int s = 0; s < ns; ++s)
-                XMOE_CUDA(cudaMemcpy2D(static_cast<char*>(L.sw1) + static_cast<size_t>(s) * Fs1 * es,
-                                       static_cast<size_t>(L.Fs) * es,
-                                       static_cast<const char*>(sw1) + static_cast<size_t>(s) * H * Fs1 * es,
-                                       static_cast<size_t>(Fs1) * es, static_cast<size_t>(Fs1) * es, H,
-                                       cudaMemcpyDeviceToDevice));
-            XMOE_CUDA(cudaMemcpy(L.sw2, sw2, static_cast<size_t>(H) * L.Fs * es, cudaMemcpyDeviceToDevice));
-        } else {
-            launch_transpose(XMOE_BF16, sw1, ns, H, Fs1, XMOE_BF16, L.sw1, st);  // [ns*Fs, H]
-            launch_transpose(XMOE_BF16, sw2, 1, L.Fs, H, XMOE_BF16, L.sw2, st);  // [H, ns*Fs]
-        }
     }
-
+    (void)st;
     // ---- per-rank workspace
     const long long S = d.max_tokens;
     require(S >= 1, XMOE_ERR_VALIDATION, "max_tokens must be >= 1");
@@ -427,6 +480,9 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     L.recv_tab = table(t_recv);
     L.flag_tab = reinterpret_cast<unsigned**>(table(t_flags));
     L.cnt_tab = reinterpret_cast<int32_t**>(table(t_counts));
+    XMOE_CUDA(cudaHostAlloc(&L.peer_err_h, sizeof(int), cudaHostAllocMapped));
+    *L.peer_err_h = 0;
+    XMOE_CUDA(cudaHostGetDevicePointer(&L.peer_err_d, L.peer_err_h, 0));
     L.epoch = static_cast<unsigned*>(L.alloc(sizeof(unsigned)));
     XMOE_CUDA(cudaMemset(L.epoch, 0, sizeof(unsigned)));
     L.eout_tab = table(t_eout);
@@ -441,23 +497,12 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         L.w1r = L.alloc(ew * es);
         L.w2r = L.alloc(ew * es);
         L.gater = L.alloc(static_cast<size_t>(H) * E * es);
-        XMOE_CUDA(cudaMemcpy(L.w1r, w1, ew * es, cudaMemcpyDeviceToDevice));
-        XMOE_CUDA(cudaMemcpy(L.w2r, w2, ew * es, cudaMemcpyDeviceToDevice));
-        XMOE_CUDA(cudaMemcpy(L.gater, gate, static_cast<size_t>(H) * E * es, cudaMemcpyDeviceToDevice));
         L.dgate = static_cast<float*>(L.alloc(sizeof(float) * H * E));
         L.dw1 = static_cast<float*>(L.alloc(sizeof(float) * ew));
         L.dw2 = static_cast<float*>(L.alloc(sizeof(float) * ew));
         if (L.Fs > 0) {
-            const int ns = static_cast<int>(d.n_shared), Fs1 = static_cast<int>(d.shared_ffn_dim);
             L.sw1r = L.alloc(static_cast<size_t>(H) * L.Fs * es);
             L.sw2r = L.alloc(static_cast<size_t>(H) * L.Fs * es);
-            for (int s2 = 0; s2 < ns; ++s2)  // W1cat [H, ns*Fs]
-                XMOE_CUDA(cudaMemcpy2D(static_cast<char*>(L.sw1r) + static_cast<size_t>(s2) * Fs1 * es,
-                                       static_cast<size_t>(L.Fs) * es,
-                                       static_cast<const char*>(sw1) + static_cast<size_t>(s2) * H * Fs1 * es,
-                                       static_cast<size_t>(Fs1) * es, static_cast<size_t>(Fs1) * es, H,
-                                       cudaMemcpyDeviceToDevice));
-            XMOE_CUDA(cudaMemcpy(L.sw2r, sw2, static_cast<size_t>(H) * L.Fs * es, cudaMemcpyDeviceToDevice));
             L.dsw1 = static_cast<float*>(L.alloc(sizeof(float) * H * L.Fs));
             L.dsw2 = static_cast<float*>(L.alloc(sizeof(float) * H * L.Fs));
         }
@@ -471,6 +516,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         L.jumps = static_cast<uint64_t*>(L.alloc(sizeof(uint64_t) * jt.size()));
         XMOE_CUDA(cudaMemcpy(L.jumps, jt.data(), sizeof(uint64_t) * jt.size(), cudaMemcpyHostToDevice));
     }
+    layer_load_weights(L, gate, w1, w2, sw1, sw2, nullptr);
     L.events.resize(kNumEvents);
     for (auto& e : L.events) XMOE_CUDA(cudaEventCreate(&e));
     if (L.train) {
@@ -528,7 +574,7 @@ static void exchange_counts(Layer& L, cudaStream_t st) {
         sg.s[sg.n++] = CountSeg{L.G_all + static_cast<size_t>(w.rank) * W, W, W * E + W * C * E, L.G_all};
         sg.s[sg.n++] = CountSeg{w.rbd.gd_own, 2 * W * C, W * E + W * C * E + W * W, L.gd_all};
     }
-    launch_counts_exchange(sg, L.cnt_tab, L.area_ints, w.rank, W, L.flag_tab, w.flags, kSlotCounts, L.epoch, st);
+    launch_counts_exchange(sg, L.cnt_tab, L.area_ints, w.rank, W, L.flag_tab, w.flags, kSlotCounts, L.epoch, L.peer_err_d, st);
 }
 
 // ---------------------------------------------------------------- chunked forward
@@ -656,7 +702,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     }
     for (int c = 0; c < C; ++c) {
         XMOE_CUDA(cudaStreamWaitEvent(st, L.evA[c], 0));
-        if (dist) launch_flag_wait(L.workers[0].flags, W, slot_A(c), L.epoch, st);
+        if (dist) launch_flag_wait(L.workers[0].flags, W, slot_A(c), L.epoch, L.peer_err_d, st);
         if (L.timing) XMOE_CUDA(cudaEventRecord(L.tl[4 * c + 1], st));
         const size_t r0 = static_cast<size_t>(c) * L.Rc;
         g_copy_blocks = 0;
@@ -690,7 +736,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     for (int c = 0; c < C; ++c) {
         g_copy_blocks = c == C - 1 ? 0 : blk_combine;  // the last combine runs alone
         XMOE_CUDA(cudaStreamWaitEvent(cm, L.evB[c], 0));
-        if (dist) launch_flag_wait(L.workers[0].flags, W, slot_B(c), L.epoch, cm);
+        if (dist) launch_flag_wait(L.workers[0].flags, W, slot_B(c), L.epoch, L.peer_err_d, cm);
         if (c == C - 1) L.mark(kEvReturn, cm);
         const int t0 = t0_of(c), n = t0_of(c + 1) - t0;
         if (n == 0) continue;
@@ -719,16 +765,42 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
 // ---------------------------------------------------------------- forward
 // x/out: [nl, S, H] (nl = ranks this process drives).
 void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t st) {
-    Ctx& ctx = *L.ctx;
+    L.check_peers();
     require(S >= 0 && S <= L.S_max, XMOE_ERR_VALIDATION, "sequence longer than the layer's max_tokens");
     L.last_ssmb = false;
     g_copy_blocks = 0;  // launch-shaping globals start clean even after an aborted forward
     g_copy_smem = 0;
     g_gemm_sm_limit = 0;
-    if (L.nchunks > 1 && S > 0) {
+    // A distributed layer takes the same path on every rank whatever its own
+    // S: the chunked and unchunked forwards use different peer-flag slots, so
+    // a rank with no tokens (S == 0) must still run the chunked protocol.
+    if (L.nchunks > 1 && (S > 0 || L.distributed)) {
+        L.last_Sw.assign(L.nl, S);
         layer_forward_chunked(L, x, S, out, st);
         return;
     }
+    std::vector<long long> Sw(L.nl, S);
+    layer_forward_v(L, x, Sw.data(), out, st);
+}
+
+// Per-worker token counts (rank == -1 contexts: the reference's MoeInstance
+// allows a different S_w per worker, moe_instance.hpp:27): x/out are the
+// workers' [S_w, H] blocks back to back.  Always the unchunked pipeline.
+void layer_forward_v(Layer& L, const void* x, const long long* Sw, void* out, cudaStream_t st) {
+    Ctx& ctx = *L.ctx;
+    L.check_peers();
+    long long Smax = 0;
+    std::vector<long long> xoff(L.nl + 1, 0);
+    for (int i = 0; i < L.nl; ++i) {
+        require(Sw[i] >= 0 && Sw[i] <= L.S_max, XMOE_ERR_VALIDATION, "sequence longer than the layer's max_tokens");
+        Smax = std::max(Smax, Sw[i]);
+        xoff[i + 1] = xoff[i] + Sw[i];
+    }
+    L.last_ssmb = false;
+    L.last_Sw.assign(Sw, Sw + L.nl);
+    g_copy_blocks = 0;
+    g_copy_smem = 0;
+    g_gemm_sm_limit = 0;
     const int W = L.W, E = L.E, H = L.H, F = L.F, k = L.k;
     const int dt = L.d.dtype;
     const size_t row_bytes = static_cast<size_t>(H) * L.es;
@@ -740,21 +812,21 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     const bool token_major = dt == XMOE_BF16 && (row_bytes & 15) == 0 && k <= 32;
     const char* xb = static_cast<const char*>(x);
     char* ob = static_cast<char*>(out);
-    const long long nk = S * k;
-    auto x_of = [&](int i) { return xb + static_cast<size_t>(i) * S * row_bytes; };
-    auto o_of = [&](int i) { return ob + static_cast<size_t>(i) * S * row_bytes; };
+    auto x_of = [&](int i) { return xb + static_cast<size_t>(xoff[i]) * row_bytes; };
+    auto o_of = [&](int i) { return ob + static_cast<size_t>(xoff[i]) * row_bytes; };
 
     L.mark(kEvStart, st);
     for (int i = 0; i < nl; ++i)  // one dense group of S rows; the forward's epoch
-        launch_forward_begin(L.workers[i].s_rows, static_cast<int>(S), i == 0 ? L.epoch : nullptr, st);
+        launch_forward_begin(L.workers[i].s_rows, static_cast<int>(Sw[i]), i == 0 ? L.epoch : nullptr, st);
     const int me = L.workers[0].rank;
     auto fbar = [&](int j) {  // cross-rank barrier of the peer transport
-        if (L.p2p) launch_flag_barrier(L.flag_tab, L.workers[0].flags, W, me, kSlotBar + j, L.epoch, st);
+        if (L.p2p) launch_flag_barrier(L.flag_tab, L.workers[0].flags, W, me, kSlotBar + j, L.epoch, L.peer_err_d, st);
         else L.barrier(st);
     };
     // 1. gate (gating.cpp:14-57)
     for (int i = 0; i < nl; ++i) {
         Worker& w = L.workers[i];
+        const long long S = Sw[i];
         if (dt == XMOE_F64) {
             launch_gate_logits_f64(reinterpret_cast<const double*>(x_of(i)), static_cast<const double*>(L.gate),
                                    S, H, E, w.logits, st);
@@ -774,6 +846,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     auto issue_shared = [&](cudaStream_t ss) {
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
+            const long long S = Sw[i];
             run_gemm(dt, x_of(i), S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, ss, w.smbits);
             run_gemm(dt, w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, w.sout, 0, ss);
         }
@@ -800,6 +873,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     // 2. padding-free token buffer (pft.cpp:12-60) [+ RBD groups and pilots, rbd.cpp:26-81]
     for (int i = 0; i < nl; ++i) {
         Worker& w = L.workers[i];
+        const long long S = Sw[i], nk = S * k;
         launch_pft(w.top, w.wts, S, k, E, static_cast<int>(std::min<long long>(L.d.max_token_count, 0x7fffffff)),
                    w.token_ids, w.expert_ids, w.cw, w.tpe, w.slot_pos, w.B_dev, w.pft_ws, st);
         if (rbd) {
@@ -827,15 +901,15 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     //    position) layout (pf_pipeline.cpp:47-73), then the rows themselves
     for (int i = 0; i < nl; ++i) {
         Worker& w = L.workers[i];
-        launch_dispatch_dest(L.tpe_all, W, E, w.rank, w.expert_ids, w.B_dev, nk, w.dest_rank, w.dest_row, st);
+        launch_dispatch_dest(L.tpe_all, W, E, w.rank, w.expert_ids, w.B_dev, Sw[i] * k, w.dest_rank, w.dest_row, st);
         if (rbd) launch_rbd_offsets(L.gd_all, W, w.rank, w.rbd, st);
     }
     L.mark(kEvCounts, st);  // counts + destinations; rows_moved is the row kernel alone
     if (rbd) {
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
-            launch_rbd_pack(x_of(i), static_cast<int>(row_bytes), w.rbd, W, 0, nk, w.slot_pos, k, w.dest_row,
-                            w.cw, L.recv_tab, L.desc_tab, st, static_cast<int>(S), w.expert_ids, L.El);
+            launch_rbd_pack(x_of(i), static_cast<int>(row_bytes), w.rbd, W, 0, Sw[i] * k, w.slot_pos, k, w.dest_row,
+                            w.cw, L.recv_tab, L.desc_tab, st, static_cast<int>(Sw[i]), w.expert_ids, L.El);
         }
         L.mark(kEvMoved, st);
         if (dist) fbar(0);
@@ -849,17 +923,17 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             if (token_major)
-                launch_scatter_tokens(x_of(i), static_cast<int>(row_bytes), static_cast<int>(S), k, w.slot_pos,
+                launch_scatter_tokens(x_of(i), static_cast<int>(row_bytes), static_cast<int>(Sw[i]), k, w.slot_pos,
                                       w.dest_rank, w.dest_row, w.cw, L.recv_tab, L.eout_tab, w.slot_src, w.slot_w, st);
             else
-                launch_scatter_rows(x_of(i), static_cast<int>(row_bytes), w.token_ids, w.B_dev, nk, w.dest_rank,
+                launch_scatter_rows(x_of(i), static_cast<int>(row_bytes), w.token_ids, w.B_dev, Sw[i] * k, w.dest_rank,
                                     w.dest_row, L.recv_tab, st);
         }
         L.mark(kEvMoved, st);
         if (dist) fbar(0);
     } else {
         Worker& w = L.workers[0];
-        launch_gather_rows(xb, S, static_cast<int>(row_bytes), w.token_ids, nk, w.B_dev, w.send, nullptr, st);
+        launch_gather_rows(xb, Sw[0], static_cast<int>(row_bytes), w.token_ids, Sw[0] * k, w.B_dev, w.send, nullptr, st);
         L.h_tpe.resize(static_cast<size_t>(W) * E);
         XMOE_CUDA(cudaMemcpyAsync(L.h_tpe.data(), L.tpe_all, sizeof(int32_t) * W * E, cudaMemcpyDeviceToHost, st));
         XMOE_CUDA(cudaStreamSynchronize(st));
@@ -894,14 +968,14 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             if (i == 0 && dist && L.gpn > 1) fbar(2);  // replicas' outputs are read from their owners
-            launch_rbd_merge(dt, L.eout_tab, H, w.desc_recv, w.gstart, w.rbd, 0, static_cast<long long>(W) * S,
+            launch_rbd_merge(dt, L.eout_tab, H, w.desc_recv, w.gstart, w.rbd, 0, static_cast<long long>(W) * Smax,
                              w.back_u, st);
         }
         if (dist) fbar(3);
         L.mark(kEvReturn, st);
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
-            launch_rbd_combine(dt, L.back_tab, H, static_cast<int>(S), w.rbd, 0, w.cw,
+            launch_rbd_combine(dt, L.back_tab, H, static_cast<int>(Sw[i]), w.rbd, 0, w.cw,
                                L.Fs > 0 ? w.sout : nullptr, o_of(i), st);
         }
     } else if (tables) {
@@ -910,21 +984,21 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             if (token_major)
-                launch_combine_slots(w.slot_src, w.slot_w, k, H, static_cast<int>(S), L.Fs > 0 ? w.sout : nullptr,
+                launch_combine_slots(w.slot_src, w.slot_w, k, H, static_cast<int>(Sw[i]), L.Fs > 0 ? w.sout : nullptr,
                                      o_of(i), st);
             else
-                launch_combine(dt, nullptr, H, nullptr, w.slot_pos, k, w.cw, static_cast<int>(S),
+                launch_combine(dt, nullptr, H, nullptr, w.slot_pos, k, w.cw, static_cast<int>(Sw[i]),
                                L.Fs > 0 ? w.sout : nullptr, o_of(i), st, L.eout_tab, w.dest_rank, w.dest_row);
         }
     } else {
         L.exchange_nccl(/*forward=*/false, st);
         L.mark(kEvReturn, st);
         Worker& w = L.workers[0];
-        launch_combine(dt, w.back, H, nullptr, w.slot_pos, k, w.cw, static_cast<int>(S),
+        launch_combine(dt, w.back, H, nullptr, w.slot_pos, k, w.cw, static_cast<int>(Sw[0]),
                        L.Fs > 0 ? w.sout : nullptr, ob, st);
     }
     L.mark(kEvCombine, st);
-    L.last_S = S;
+    L.last_S = Sw[0];
     L.bwd_pending = true;
 }
 
@@ -977,6 +1051,7 @@ void Layer::exchange_nccl(bool forward, cudaStream_t st) {
 //      + gate parts
 void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* dx, cudaStream_t st) {
     require(L.train, XMOE_ERR_VALIDATION, "layer was not created with XMOE_LAYER_TRAIN");
+    L.check_peers();
     require(S == L.last_S, XMOE_ERR_VALIDATION, "backward must follow a forward of the same sequence");
     // one backward per forward: the cross-rank barriers are keyed by the forward's epoch
     require(L.bwd_pending, XMOE_ERR_VALIDATION, "backward must follow a forward (one backward per forward)");
@@ -1042,7 +1117,7 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
     // SM's shared memory — it waited for them, 0.1 ms at N=4)
     const int me_rank = L.workers[0].rank;
     auto bbar = [&](int j) {
-        launch_flag_barrier(L.flag_tab, L.workers[0].flags, W, me_rank, kSlotBwdBar + j, L.epoch, st);
+        launch_flag_barrier(L.flag_tab, L.workers[0].flags, W, me_rank, kSlotBwdBar + j, L.epoch, L.peer_err_d, st);
     };
     if (dist) bbar(0);
     bmark(kBwScatter);

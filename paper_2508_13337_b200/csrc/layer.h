@@ -119,6 +119,7 @@ struct Layer {
     std::vector<void*> peer_maps;
     size_t es = 2;
     long long R_max = 0, S_max = 0, last_S = 0;
+    std::vector<long long> last_Sw;  // per-worker token counts of the last forward
     bool bwd_pending = false;  // a forward ran since the last backward (one backward per forward)
     void* gate = nullptr;  // F64 [H,E]; BF16 [E,H]
     void* w1 = nullptr;    // F64 [E_held,H,F]; BF16 [E_held,F,H]
@@ -185,6 +186,11 @@ struct Layer {
     std::vector<cudaEvent_t> tl;   // timing: per chunk scatter end, GEMM start, GEMM end, combine end
     std::vector<cudaEvent_t> bev;  // timing: backward stage boundaries (kBwdEvents)
     cudaEvent_t ev_done = nullptr;
+    // peer-wait failures (chunk.cu wait_flag): host-mapped word, 0 = healthy,
+    // 0x100 | slot = a peer never raised that flag within XMOE_PEER_TIMEOUT_S
+    uint8_t* dbg_mask = nullptr;  // xmoe_layer_inspect: RBD pilot mask of the last forward
+    int* peer_err_h = nullptr;
+    int* peer_err_d = nullptr;
 
     void* alloc(size_t bytes);
     void mark(int ev, cudaStream_t st);
@@ -192,6 +198,8 @@ struct Layer {
     void barrier(cudaStream_t st);
     long long C(int s, int d) const;  // copies source s -> dest d (needs h_tpe)
     void ledger(uint64_t* out, int n);
+    void quiesce();            // cross-rank barrier before teardown (p2p layers)
+    void check_peers() const;  // throws XMOE_ERR_PEER_TIMEOUT after a failed peer wait
     // reference-schema ledger (ledger.cpp)
     bool last_ssmb = false;             // last forward was ssmb_forward
     std::vector<long long> ssmb_rows;   // its shard lengths
@@ -204,8 +212,19 @@ struct Layer {
 
 void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const void* w1,
                   const void* w2, const void* sw1, const void* sw2, Layer& L);
+void layer_load_weights(Layer& L, const void* gate, const void* w1, const void* w2, const void* sw1, const void* sw2,
+                        cudaStream_t st);
 void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t st);
+void layer_forward_v(Layer& L, const void* x, const long long* Sw, void* out, cudaStream_t st);
 void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* dx, cudaStream_t st);
 void ssmb_forward(Ctx& ctx, Layer& L, const void* x_full, long long S, void* out_full, cudaStream_t st);
 
 }  // namespace xmoe
+
+// C-ABI handles (xmoe.h)
+struct xmoe_ctx {
+    xmoe::Ctx c;
+};
+struct xmoe_layer {
+    xmoe::Layer l;
+};

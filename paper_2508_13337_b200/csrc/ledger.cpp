@@ -35,7 +35,7 @@ void Layer::ledger(uint64_t* out, int n) {
         if (W > 1) v[2] += static_cast<uint64_t>(W - 1) * E * sizeof(int32_t);  // count all-gather
         // distinct (token, destination rank) groups leaving the rank: the rows
         // the redundancy bypass sends (rbd.cpp:427-442 with node_of = rank)
-        const long long S = last_S;
+        const long long S = last_Sw.empty() ? last_S : last_Sw[static_cast<size_t>(&w - workers.data())];
         if (S > 0) {
             std::vector<int32_t> slot(static_cast<size_t>(S) * k), eid(static_cast<size_t>(S) * k);
             XMOE_CUDA(cudaMemcpy(slot.data(), w.slot_pos, sizeof(int32_t) * slot.size(), cudaMemcpyDeviceToHost));
@@ -210,7 +210,7 @@ void Layer::ledger_entries(const xmoe_topology& topo, std::vector<xmoe_ledger_en
         // rbd.cpp:130-233, 300-345: per (token, node) group of source s
         int32_t G = 0;
         XMOE_CUDA(cudaMemcpy(&G, w.rbd.G_dev, sizeof(int32_t), cudaMemcpyDeviceToHost));
-        const long long S = last_S;
+        const long long S = last_Sw.empty() ? last_S : last_Sw[static_cast<size_t>(&w - workers.data())];
         std::vector<int32_t> tok(G), dst(G), first(G), n(G), pilot(G);
         if (G > 0) {
             XMOE_CUDA(cudaMemcpy(tok.data(), w.rbd.g.token, sizeof(int32_t) * G, cudaMemcpyDeviceToHost));

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) scatter_rows_kernel(
     const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
     for (long long r = warp; r < B; r += nwarps) {
-        const int t = token_ids[r];
+        const long long t = token_ids ? token_ids[r] : r;  // null: x is already packed
         char* dst = dest_bufs[dest_rank[r]] + static_cast<size_t>(dest_row[r]) * row_bytes;
         warp_copy_row(x + static_cast<size_t>(t) * row_bytes, dst, row_bytes, lane);
     }
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(32 * kTmaWarps) scatter_rows_tma_kernel(
         char* slot = my + static_cast<size_t>(q) * row_bytes;
         if (i >= kTmaSlots)  // the store that last read this slot must be done reading
             asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTmaSlots - 1) : "memory");
-        const char* src = x + static_cast<size_t>(token_ids[r]) * row_bytes;
+        const char* src = x + static_cast<size_t>(token_ids ? token_ids[r] : r) * row_bytes;
         char* dst = dest_bufs[dest_rank[r]] + static_cast<size_t>(dest_row[r]) * row_bytes;
         const uint32_t bar = smem_addr(&bars[wl][q]);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(row_bytes) : "memory");

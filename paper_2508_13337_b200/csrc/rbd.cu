@@ -86,8 +86,8 @@ void rng_state_from_seed(uint64_t seed, uint64_t out[4]) {
     for (int i = 0; i < 4; ++i) out[i] = x = splitmix64(x);
 }
 
-// Jump matrices J_k = T^(kRbdChunk * 2^k), T = one xoshiro step.
-void rbd_jump_tables(std::vector<uint64_t>& out) {
+// Jump matrices J_k = T^(2^log2_chunk * 2^k), k < count, T = one xoshiro step.
+void gf2_jump_tables(int log2_chunk, int count, std::vector<uint64_t>& out) {
     Mat T;
     for (int j = 0; j < 256; ++j) {  // column j = T(e_j)
         uint64_t s[4] = {0, 0, 0, 0};
@@ -99,17 +99,23 @@ void rbd_jump_tables(std::vector<uint64_t>& out) {
         }
     }
     Mat P = T, tmp;
-    for (int c = 1; c < kRbdChunk; c <<= 1) {  // T^kRbdChunk by squaring
+    for (int c = 0; c < log2_chunk; ++c) {
         mat_mul(P, P, tmp);
         P = tmp;
     }
-    out.assign(static_cast<size_t>(kRbdJumps) * 256 * 4, 0);
-    for (int k = 0; k < kRbdJumps; ++k) {
+    out.assign(static_cast<size_t>(count) * 256 * 4, 0);
+    for (int k = 0; k < count; ++k) {
         for (int i = 0; i < 256; ++i)
             for (int w = 0; w < 4; ++w) out[(static_cast<size_t>(k) * 256 + i) * 4 + w] = P.r[i][w];
         mat_mul(P, P, tmp);
         P = tmp;
     }
+}
+
+// Jump matrices J_k = T^(kRbdChunk * 2^k), T = one xoshiro step.
+void rbd_jump_tables(std::vector<uint64_t>& out) {
+    static_assert(kRbdChunk == 256, "chunk is 2^8 outputs");
+    gf2_jump_tables(8, kRbdJumps, out);
 }
 
 // One CTA per chunk of kRbdChunk groups: jump the seed state to the chunk
@@ -148,6 +154,88 @@ __global__ void __launch_bounds__(256) rbd_draw_kernel(uint64_t s0, uint64_t s1,
         const int n = min(kRbdChunk, G - c * kRbdChunk);
         for (int j = 0; j < n; ++j) draws[c * kRbdChunk + j] = xoshiro_next(s);
     }
+}
+
+// ---------------------------------------------------------------- synthetic inputs
+// The reference generator on the device (rng.hpp:24-47): outputs
+// [offset, offset + n) of Rng(seed)'s uniform(lo, hi) stream.  The stream is
+// cut into chains of kRngChain outputs; one CTA per chain jumps the seed
+// state to the chain start (GF(2) powers T^(kRngChain * 2^k), bit-parallel
+// over the 256 threads) and one thread then steps through the chain.
+// value = lo + (hi - lo) * ((x >> 11) * 2^-53) in fp64 (separate mul/add,
+// as the reference), optionally snapped to multiples of 1/grid
+// (round-half-even), stored as f64, f32 or bf16 (round to nearest even).
+constexpr int kRngLog2Chain = 16;
+constexpr long long kRngChain = 1LL << kRngLog2Chain;
+constexpr int kRngJumps = 40;
+
+__global__ void __launch_bounds__(256) rng_fill_kernel(uint64_t s0, uint64_t s1, uint64_t s2, uint64_t s3,
+                                                      const uint64_t* __restrict__ jumps, unsigned long long offset,
+                                                      long long n, double lo, double hi, double grid, int dtype,
+                                                      void* __restrict__ out) {
+    __shared__ uint64_t st[4];
+    __shared__ uint32_t bits[8];
+    const unsigned long long c = offset / kRngChain + blockIdx.x;  // global chain index
+    if (threadIdx.x == 0) {
+        st[0] = s0;
+        st[1] = s1;
+        st[2] = s2;
+        st[3] = s3;
+    }
+    __syncthreads();
+    const int i = threadIdx.x;
+    for (int k = 0; k < kRngJumps && (c >> k); ++k) {
+        if (!((c >> k) & 1)) continue;
+        const uint64_t* row = jumps + (static_cast<size_t>(k) * 256 + i) * 4;
+        const int par = (__popcll(row[0] & st[0]) + __popcll(row[1] & st[1]) + __popcll(row[2] & st[2]) +
+                         __popcll(row[3] & st[3])) & 1;
+        const unsigned b = __ballot_sync(0xffffffffu, par);
+        if ((i & 31) == 0) bits[i >> 5] = b;
+        __syncthreads();
+        if (i < 4) st[i] = static_cast<uint64_t>(bits[2 * i]) | (static_cast<uint64_t>(bits[2 * i + 1]) << 32);
+        __syncthreads();
+    }
+    if (i != 0) return;
+    uint64_t s[4] = {st[0], st[1], st[2], st[3]};
+    const unsigned long long g0 = c * kRngChain;                    // first output of the chain
+    const unsigned long long a = g0 < offset ? offset : g0;         // first one we keep
+    const unsigned long long e = min(g0 + kRngChain, offset + static_cast<unsigned long long>(n));
+    for (unsigned long long q = g0; q < a; ++q) xoshiro_next(s);
+    const double span = hi - lo;
+    for (unsigned long long q = a; q < e; ++q) {
+        const double u = static_cast<double>(xoshiro_next(s) >> 11) * 0x1.0p-53;
+        double v = __dadd_rn(lo, __dmul_rn(span, u));
+        if (grid > 0) v = __ddiv_rn(rint(__dmul_rn(v, grid)), grid);
+        const size_t o = static_cast<size_t>(q - offset);
+        if (dtype == XMOE_F64) static_cast<double*>(out)[o] = v;
+        else if (dtype == XMOE_F32) static_cast<float*>(out)[o] = __double2float_rn(v);
+        else static_cast<__nv_bfloat16*>(out)[o] = __double2bfloat16(v);
+    }
+}
+
+void launch_rng_uniform(uint64_t seed, unsigned long long offset, long long n, double lo, double hi, double grid,
+                        int dtype, void* out, cudaStream_t st) {
+    if (n <= 0) return;
+    static uint64_t* d_jumps = nullptr;
+    static int d_dev = -1;
+    int dev = 0;
+    XMOE_CUDA(cudaGetDevice(&dev));
+    if (!d_jumps || d_dev != dev) {  // per process and device; tables are ~320 KB
+        std::vector<uint64_t> jt;
+        gf2_jump_tables(kRngLog2Chain, kRngJumps, jt);
+        XMOE_CUDA(cudaMalloc(&d_jumps, jt.size() * sizeof(uint64_t)));
+        XMOE_CUDA(cudaMemcpy(d_jumps, jt.data(), jt.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+        d_dev = dev;
+    }
+    uint64_t s[4];
+    rng_state_from_seed(seed, s);
+    const unsigned long long c0 = offset / kRngChain;
+    const unsigned long long c1 = (offset + static_cast<unsigned long long>(n) - 1) / kRngChain;
+    const unsigned long long chains = c1 - c0 + 1;
+    require(chains < (1ull << 31), XMOE_ERR_VALIDATION, "rng_uniform: too many outputs");
+    rng_fill_kernel<<<static_cast<unsigned>(chains), 256, 0, st>>>(s[0], s[1], s[2], s[3], d_jumps, offset, n, lo,
+                                                                   hi, grid, dtype, out);
+    XMOE_LAUNCH_CHECK();
 }
 
 // ---------------------------------------------------------------- groups

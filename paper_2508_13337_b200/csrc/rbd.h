@@ -66,6 +66,10 @@ struct RbdWork {
 uint64_t salt_seed_host(uint64_t seed, uint64_t a, uint64_t b);
 void rng_state_from_seed(uint64_t seed, uint64_t out[4]);
 void rbd_jump_tables(std::vector<uint64_t>& out);
+void gf2_jump_tables(int log2_chunk, int count, std::vector<uint64_t>& out);
+// outputs [offset, offset + n) of Rng(seed).uniform(lo, hi) (rng.hpp:24-47)
+void launch_rng_uniform(uint64_t seed, unsigned long long offset, long long n, double lo, double hi, double grid,
+                        int dtype, void* out, cudaStream_t st);
 
 void launch_rbd_groups(const int32_t* slot_pos, const int32_t* expert_ids, int S, int k, int El,
                        const uint64_t state[4], const uint64_t* jumps, RbdWork& wk, cudaStream_t st);
@@ -91,6 +95,10 @@ void launch_rbd_merge(int dtype, const char* const* eout_tab, int H, const RbdDe
                       const RbdWork& wk, int c, long long max_groups, void* back_u, cudaStream_t st);
 void launch_rbd_combine(int dtype, const char* const* back_tab, int H, int S, const RbdWork& wk, int c,
                         const double* cw, const void* addend, void* out, cudaStream_t st);
+
+// ep.cu: pilot mask [B] (and each copy's pilot row) of the drawn groups
+void launch_mask_from_groups(const RbdWork& wk, const int32_t* slot_pos, int k, long long max_groups, uint8_t* mask,
+                             int32_t* pilot_of, cudaStream_t st);
 
 // pft.cu: stable CSR with the item count on the device (bound n_max).
 void launch_stable_csr_dev(const int32_t* keys, const int32_t* n_dev, int n_max, int K, int32_t* ptr,

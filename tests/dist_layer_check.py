@@ -175,6 +175,30 @@ def main():
         dist.barrier()
     if rank == 0:
         print("ragged / empty sequences checked", flush=True)
+    # unequal S per rank with one idle rank (S == 0): every rank must take the
+    # same (chunked or unchunked) protocol whatever its own S
+    for mode, chunks in ((capi.NAIVE, 0), (capi.NAIVE, 4), (capi.RBD, 0), (capi.RBD, 2)):
+        layer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=4096 * k,
+                           max_tokens=4096, dtype=capi.BF16, gate=bv(gate), w1=bv(w1[rank * el:(rank + 1) * el]),
+                           w2=bv(w2[rank * el:(rank + 1) * el]), dispatch_mode=mode, seed=5, chunks=chunks)
+        for it, Ss in enumerate(([0] + [4096 - 37 * r for r in range(1, world)],
+                                 [300 + r for r in range(world - 1)] + [0])):
+            xs = [grid_tokens(np.random.default_rng(900 + 10 * it + r), Ss[r], H) for r in range(world)]
+            o = layer.forward(bv(xs[rank])).float().cpu().numpy()
+            got = [None] * world
+            dist.all_gather_object(got, o)
+            if rank == 0:
+                Wt = O.LayerWeights(gate, w1, w2)
+                want = O.pf_moe_forward(xs, Wt, E, k, 4096 * k, exact=False) if mode == capi.NAIVE else \
+                    O.rbd_moe_forward(xs, Wt, E, k, 4096 * k, 5, exact=False)
+                errs = [norm_rel(got[r], want[r]) for r in range(world) if Ss[r] > 0]
+                shapes_ok = all(got[r].shape[0] == Ss[r] for r in range(world))
+                print(f"idle-rank case mode={mode} chunks={layer.chunks()} S={Ss} err={max(errs):.2e}", flush=True)
+                if max(errs) > 1e-2 or not shapes_ok:
+                    failures.append(("idle-rank", mode, chunks, Ss, errs))
+        layer.status()  # no peer wait timed out
+        del layer
+        dist.barrier()
     # backward over the peer transport (bf16, dropless): dx per rank, expert
     # grads of each rank's block, gate grads summed over ranks
     from oracle import moe_grad as Gr
