@@ -249,6 +249,11 @@ int xmoe_route_pairs(xmoe_ctx* ctx, int64_t n, const int32_t* token, const int32
  * GF(2) jump-ahead: any offset, no host draws. */
 int xmoe_rng_uniform(xmoe_ctx* ctx, uint64_t seed, uint64_t offset, int64_t n, double lo, double hi, double grid,
                      int dtype, void* out, void* stream);
+/* The same from an explicit generator state (moesim::Rng's four words), and
+ * a host-side jump of such a state by n outputs. */
+int xmoe_rng_uniform_state(xmoe_ctx* ctx, const uint64_t* state, uint64_t offset, int64_t n, double lo, double hi,
+                           double grid, int dtype, void* out, void* stream);
+int xmoe_rng_advance(uint64_t* state, uint64_t n);
 /* moesim::salt_seed (rng.hpp:17-19). */
 uint64_t xmoe_salt_seed(uint64_t seed, uint64_t a, uint64_t b);
 /* moesim::make_layer_weights (padded_pipeline.cpp:13-27) on the device for
@@ -364,6 +369,7 @@ int xmoe_layer_set_weights(xmoe_layer* layer, const void* gate, const void* w1, 
 #define XMOE_INSPECT_DEST_ROW 12         /* int32 [B] its grouped row at the owner */
 #define XMOE_INSPECT_SLOT_POS 13         /* int32 [S,k] packed rows of each token's kept copies */
 #define XMOE_INSPECT_PILOT_MASK 14       /* uint8 [B] RbdPlan::pilot_mask (rbd.hpp:28-41) */
+#define XMOE_INSPECT_SSMB_KEPT 15        /* int32 [G] kept copies per shard of the last ssmb_forward */
 int xmoe_layer_inspect(xmoe_layer* layer, int worker, int what, const void** ptr, int64_t* count);
 
 /* Byte ledger of the last forward on this layer (collectives.hpp:31-49):

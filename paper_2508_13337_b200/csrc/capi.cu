@@ -354,6 +354,9 @@ int xmoe_layer_inspect(xmoe_layer* layer, int worker, int what, const void** ptr
             case XMOE_INSPECT_DEST_RANK: p = w.dest_rank; n = B; break;
             case XMOE_INSPECT_DEST_ROW: p = w.dest_row; n = B; break;
             case XMOE_INSPECT_SLOT_POS: p = w.slot_pos; n = Sk; break;
+            case XMOE_INSPECT_SSMB_KEPT:
+                require(L.last_ssmb, XMOE_ERR_VALIDATION, "last forward was not ssmb_forward");
+                p = L.ssmb_B; n = static_cast<long long>(L.ssmb_rows.size()); break;
             case XMOE_INSPECT_PILOT_MASK: {
                 require(L.d.dispatch_mode == XMOE_DISPATCH_RBD, XMOE_ERR_VALIDATION, "not a redundancy-bypassing layer");
                 if (!L.dbg_mask) L.dbg_mask = static_cast<uint8_t*>(L.alloc(static_cast<size_t>(L.S_max) * L.k + 16));
@@ -379,6 +382,23 @@ int xmoe_rng_uniform(xmoe_ctx* ctx, uint64_t seed, uint64_t offset, int64_t n, d
 }
 
 uint64_t xmoe_salt_seed(uint64_t seed, uint64_t a, uint64_t b) { return salt_seed_host(seed, a, b); }
+
+int xmoe_rng_uniform_state(xmoe_ctx* ctx, const uint64_t* state, uint64_t offset, int64_t n, double lo, double hi,
+                           double grid, int dtype, void* out, void* stream) {
+    return guarded([&] {
+        (void)ctx;
+        require(state != nullptr, XMOE_ERR_VALIDATION, "null generator state");
+        require(dtype == XMOE_F64 || dtype == XMOE_F32 || dtype == XMOE_BF16, XMOE_ERR_VALIDATION, "unknown dtype");
+        launch_rng_uniform_state(state, offset, n, lo, hi, grid, dtype, out, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int xmoe_rng_advance(uint64_t* state, uint64_t n) {
+    return guarded([&] {
+        require(state != nullptr, XMOE_ERR_VALIDATION, "null generator state");
+        rng_advance(state, n);
+    });
+}
 
 int xmoe_make_layer_weights(xmoe_ctx* ctx, uint64_t seed, uint64_t offset, int64_t E, int64_t H, int64_t F,
                             int64_t first_expert, int64_t n_experts, double gate_grid, int dtype, void* gate,

@@ -213,29 +213,58 @@ __global__ void __launch_bounds__(256) rng_fill_kernel(uint64_t s0, uint64_t s1,
     }
 }
 
-void launch_rng_uniform(uint64_t seed, unsigned long long offset, long long n, double lo, double hi, double grid,
-                        int dtype, void* out, cudaStream_t st) {
-    if (n <= 0) return;
-    static uint64_t* d_jumps = nullptr;
-    static int d_dev = -1;
+static const uint64_t* rng_jumps_dev() {
+    static uint64_t* d_jumps[64] = {};
     int dev = 0;
     XMOE_CUDA(cudaGetDevice(&dev));
-    if (!d_jumps || d_dev != dev) {  // per process and device; tables are ~320 KB
+    require(dev >= 0 && dev < 64, XMOE_ERR_CUDA, "device index out of range");
+    if (!d_jumps[dev]) {  // per process and device; tables are ~320 KB
         std::vector<uint64_t> jt;
         gf2_jump_tables(kRngLog2Chain, kRngJumps, jt);
-        XMOE_CUDA(cudaMalloc(&d_jumps, jt.size() * sizeof(uint64_t)));
-        XMOE_CUDA(cudaMemcpy(d_jumps, jt.data(), jt.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
-        d_dev = dev;
+        XMOE_CUDA(cudaMalloc(&d_jumps[dev], jt.size() * sizeof(uint64_t)));
+        XMOE_CUDA(cudaMemcpy(d_jumps[dev], jt.data(), jt.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
     }
-    uint64_t s[4];
-    rng_state_from_seed(seed, s);
+    return d_jumps[dev];
+}
+
+void launch_rng_uniform_state(const uint64_t s[4], unsigned long long offset, long long n, double lo, double hi,
+                              double grid, int dtype, void* out, cudaStream_t st) {
+    if (n <= 0) return;
+    const uint64_t* jumps = rng_jumps_dev();
     const unsigned long long c0 = offset / kRngChain;
     const unsigned long long c1 = (offset + static_cast<unsigned long long>(n) - 1) / kRngChain;
     const unsigned long long chains = c1 - c0 + 1;
-    require(chains < (1ull << 31), XMOE_ERR_VALIDATION, "rng_uniform: too many outputs");
-    rng_fill_kernel<<<static_cast<unsigned>(chains), 256, 0, st>>>(s[0], s[1], s[2], s[3], d_jumps, offset, n, lo,
-                                                                   hi, grid, dtype, out);
+    require(chains < (1ull << 31) && c1 < (1ull << kRngJumps), XMOE_ERR_VALIDATION, "rng_uniform: too many outputs");
+    rng_fill_kernel<<<static_cast<unsigned>(chains), 256, 0, st>>>(s[0], s[1], s[2], s[3], jumps, offset, n, lo, hi,
+                                                                   grid, dtype, out);
     XMOE_LAUNCH_CHECK();
+}
+
+void launch_rng_uniform(uint64_t seed, unsigned long long offset, long long n, double lo, double hi, double grid,
+                        int dtype, void* out, cudaStream_t st) {
+    uint64_t s[4];
+    rng_state_from_seed(seed, s);
+    launch_rng_uniform_state(s, offset, n, lo, hi, grid, dtype, out, st);
+}
+
+// Host: advance a generator state by n outputs (jump tables for whole chains,
+// single steps for the rest).
+void rng_advance(uint64_t s[4], unsigned long long n) {
+    static std::vector<uint64_t> jt;
+    if (jt.empty()) gf2_jump_tables(kRngLog2Chain, kRngJumps, jt);
+    const unsigned long long c = n >> kRngLog2Chain;
+    for (int k = 0; k < kRngJumps && (c >> k); ++k) {
+        if (!((c >> k) & 1)) continue;
+        uint64_t o[4] = {0, 0, 0, 0};
+        for (int i = 0; i < 256; ++i) {
+            const uint64_t* row = jt.data() + (static_cast<size_t>(k) * 256 + i) * 4;
+            const int par = (__builtin_popcountll(row[0] & s[0]) + __builtin_popcountll(row[1] & s[1]) +
+                             __builtin_popcountll(row[2] & s[2]) + __builtin_popcountll(row[3] & s[3])) & 1;
+            if (par) o[i >> 6] |= 1ull << (i & 63);
+        }
+        for (int w = 0; w < 4; ++w) s[w] = o[w];
+    }
+    for (unsigned long long q = 0; q < (n & (kRngChain - 1)); ++q) xoshiro_next(s);
 }
 
 // ---------------------------------------------------------------- groups

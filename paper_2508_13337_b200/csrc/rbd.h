@@ -70,6 +70,9 @@ void gf2_jump_tables(int log2_chunk, int count, std::vector<uint64_t>& out);
 // outputs [offset, offset + n) of Rng(seed).uniform(lo, hi) (rng.hpp:24-47)
 void launch_rng_uniform(uint64_t seed, unsigned long long offset, long long n, double lo, double hi, double grid,
                         int dtype, void* out, cudaStream_t st);
+void launch_rng_uniform_state(const uint64_t s[4], unsigned long long offset, long long n, double lo, double hi,
+                              double grid, int dtype, void* out, cudaStream_t st);
+void rng_advance(uint64_t s[4], unsigned long long n);
 
 void launch_rbd_groups(const int32_t* slot_pos, const int32_t* expert_ids, int S, int k, int El,
                        const uint64_t state[4], const uint64_t* jumps, RbdWork& wk, cudaStream_t st);
