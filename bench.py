@@ -2,13 +2,16 @@
 """Benchmark driver: one MoE-block forward per step through libxmoe.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl xmoe|reference]
-                    [--mode rbd|naive] [--tokens S]
+                    [--config c1|c2|c3|c4|c5] [--mode auto|rbd|naive] [--tokens S]
 
-Workload (BASELINE.json configs[1], SURVEY §8 "C2"): DeepSeek-MoE-style
+Default workload (BASELINE.json configs[1], SURVEY §8 "C2"): DeepSeek-MoE
 layer, 64 routed experts top-6 + 2 shared, d_model 2048, d_ff 1408, 16,384
 tokens per GPU, bf16, expert parallel over N GPUs (E/N experts per GPU),
-dropless capacity.  Synthetic grid-exact inputs (tokens on 2^-7, gate on
-2^-10, experts bf16 uniform(-0.1, 0.1)), random-init weights.
+dropless.  --config selects the other BASELINE configs (C1 the 4096-token
+CPU-runnable layer, C3 DeepSeek-V3, C4 the 32K-token sequence-sharded block,
+C5 Zipf-skewed routing; paper_2508_13337_b200/configs.py).  Synthetic inputs
+from the reference's own generator (moesim::Rng, drawn on the device),
+grid-exact (tokens on 2^-7, gate on 2^-10, experts bf16), random-init weights.
 
 N=1 runs in this process; N>1 is launched by torchrun (one rank per GPU,
 NCCL over NVLink).  Prints ONE JSON line on rank 0.
@@ -27,7 +30,6 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-C2 = dict(E=64, k=6, H=2048, F=1408, n_shared=2, Fs=1408, S=16384)
 METRIC = "MoE-layer fwd tokens/s"
 NVLINK_GBPS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 UNIT = "tokens/s"
@@ -41,7 +43,9 @@ def parse():
     p.add_argument("--impl", default="xmoe", choices=["xmoe", "reference"])
     p.add_argument("--mode", default="auto", choices=["auto", "rbd", "naive"],
                    help="dispatch: auto = plain at N=1, redundancy bypass at N>1")
-    p.add_argument("--tokens", type=int, default=C2["S"])
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
+                   help="BASELINE config (SURVEY §8 C1-C5); c2 is the headline workload")
+    p.add_argument("--tokens", type=int, default=0, help="tokens per GPU (0 = the config's)")
     p.add_argument("--transport", default=None, choices=["p2p", "nccl"],
                    help="N>1 row transport: NVLink peer kernels (default) or NCCL send/recv baseline")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -51,12 +55,16 @@ def parse():
                    help="token chunks of the pipelined forward (0 auto, 1 off)")
     p.add_argument("--cpu-sample-tokens", type=int, default=512,
                    help="tokens per host thread for the cpu_baseline sample")
+    p.add_argument("--cpu-threads", type=int, default=0, help="host threads of the CPU reference (0 = all)")
     return p.parse_args()
 
 
-def gemm_traffic():
+def gemm_traffic(config="c2"):
+    """dram read+write bytes per routed-GEMM launch from the committed ncu
+    --set full capture of this config (profiles/gemm_traffic[_cN].json)."""
+    name = "gemm_traffic.json" if config == "c2" else f"gemm_traffic_{config}.json"
     try:
-        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
             return json.load(f)["traffic_bytes_per_launch"]
     except Exception:
         return None
@@ -170,36 +178,102 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU reference
-def cpu_reference(cfg, seconds_hint=None, threads=None, sample_tokens=48, steps=1, warmup=0):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _ref_inputs(cfg, sample_tokens, refbind):
+    """The config's inputs as the compiled reference draws them: the same
+    Rng streams, grid snapping and bf16 rounding as the device (configs.py)."""
+    import numpy as np
+    import torch
+    from paper_2508_13337_b200 import configs
+
+    sd = configs.seeds(refbind.salt_seed)
+    H = cfg["H"]
+    x = refbind.rng_uniform(sd["tokens"], sample_tokens * H, -1.0, 1.0)
+    x = (np.round(x * configs.TOKEN_GRID) / configs.TOKEN_GRID).reshape(sample_tokens, H)
+    bf = lambda a: torch.from_numpy(a).to(torch.bfloat16).to(torch.float64).numpy()  # noqa: E731
+    zipf_row = None
+    if cfg.get("zipf"):
+        u = refbind.rng_uniform(sd["zipf"], cfg["E"], 0.0, 1.0).tolist()
+        zipf_row = bf(np.array(configs.zipf_bias(cfg, u)))
+        x[:, 0] = 1.0
+    return sd, x, bf, zipf_row
+
+
+def cpu_reference(cfg, threads=None, sample_tokens=64, steps=1, warmup=0):
     """The unmodified reference (oracle/_ref/libmoesim_ref.so, compiled from
-    /root/reference) on host cores: every thread runs the reference's
-    pf_moe_forward (W=1) over its own token sample of the C2 layer, plus the
-    shared experts through the reference's own grouped_expert_mlp.  Returns
-    (tokens/s, cores, per-step seconds list, sample description)."""
+    /root/reference) on host cores, on the config's own inputs (the same
+    generator streams as the GPU arm).  Layers up to 1e9 expert parameters
+    (C1, C2, C5): every thread runs the reference's pf_moe_forward (W=1) over
+    a token sample, plus the shared experts through the reference's
+    grouped_expert_mlp.  Larger layers (C3: 60 GB of fp64 weights; C4) are
+    EXTRAPOLATED: per-token time = the reference's gate_forward per token +
+    top_k x its grouped_expert_mlp per row (one expert's weights) + the
+    shared experts' per token, each timed on the sample.  Returns (tokens/s,
+    cores, per-step seconds list, sample description)."""
     import numpy as np
     from oracle import refbind
 
     if not refbind.available():
         refbind.build()
-    E, k, H, F, Fs = cfg["E"], cfg["k"], cfg["H"], cfg["F"], cfg["n_shared"] * cfg["Fs"]
-    threads = threads or os.cpu_count() or 1
-    rng = np.random.default_rng(0)
-    gate = np.round(rng.uniform(-0.1, 0.1, (H, E)) * 1024) / 1024
-    w1 = rng.uniform(-0.1, 0.1, (E, H, F))
-    w2 = rng.uniform(-0.1, 0.1, (E, F, H))
-    layer = refbind.Layer(gate, w1, w2)
-    del w1, w2
-    shared = refbind.Layer(np.zeros((H, 1)), rng.uniform(-0.1, 0.1, (1, H, Fs)),
-                           rng.uniform(-0.1, 0.1, (1, Fs, H)))
-    samples = [np.round(rng.uniform(-1, 1, (1, sample_tokens, H)) * 128) / 128 for _ in range(threads)]
+    E, k, H, F = cfg["E"], cfg["k"], cfg["H"], cfg["F"]
+    ns, Fs = cfg["ns"], cfg["Fs"]
+    threads = threads or host_threads()
+    sd, x, bf, zipf_row = _ref_inputs(cfg, sample_tokens * threads, refbind)
+    samples = [x[i * sample_tokens:(i + 1) * sample_tokens] for i in range(threads)]
+    full = E * 2 * H * F <= 1_000_000_000
+    grid = lambda a: np.round(a * 1024) / 1024  # noqa: E731
+    if full:
+        gate, w1, w2 = refbind.make_layer_weights(sd["weights"], E, H, F)
+        gate = grid(gate)
+        if zipf_row is not None:
+            gate[0] = zipf_row
+        gate = bf(gate)
+        layer = refbind.Layer(gate, bf(w1), bf(w2))
+        del w1, w2
+    else:
+        gate, _, _ = refbind.make_layer_weights(sd["weights"], E, H, 1)  # gate draws come first
+        gate = bf(grid(gate))
+        # expert 0 only: w1[0] = draws [H*E, H*E + H*F), w2[0] = the next H*F
+        d = refbind.rng_uniform(sd["weights"], H * E + 2 * H * F, -0.1, 0.1)[H * E:]
+        one = refbind.Layer(np.zeros((H, 1)), bf(d[:H * F].reshape(1, H, F)), bf(d[H * F:].reshape(1, F, H)))
+    shared = None
+    if ns:
+        _, sw1, sw2 = refbind.make_layer_weights(sd["shared"], ns, H, Fs)
+        shared = refbind.Layer(np.zeros((H, ns)), bf(sw1), bf(sw2))
     cap = sample_tokens * k
     errs = []
+    parts = {}
 
     def work(i):
         try:
-            out = layer.pf_moe_forward_noncopy(samples[i], k, cap)
-            sh = shared.grouped_expert_mlp(samples[i][0], np.array([sample_tokens]), 0)
-            out[0] += 1.0 * sh
+            xs = samples[i]
+            if full:
+                out = layer.pf_moe_forward_noncopy(xs[None], k, cap)
+                if shared is not None:
+                    for q in range(ns):  # reference grouped_expert_mlp per shared expert
+                        out[0] += shared.grouped_expert_mlp(xs, np.array([0] * q + [sample_tokens] +
+                                                                         [0] * (ns - q - 1)), 0)
+                return
+            t0 = time.perf_counter()
+            refbind.gate_forward(xs, gate, k)
+            t1 = time.perf_counter()
+            one.grouped_expert_mlp(xs, np.array([sample_tokens]), 0)
+            t2 = time.perf_counter()
+            if shared is not None:
+                for q in range(ns):
+                    shared.grouped_expert_mlp(xs, np.array([0] * q + [sample_tokens] + [0] * (ns - q - 1)), 0)
+            t3 = time.perf_counter()
+            parts[i] = ((t1 - t0) + k * (t2 - t1) + (t3 - t2)) / sample_tokens  # s per token
         except Exception as e:  # pragma: no cover
             errs.append(e)
 
@@ -212,16 +286,20 @@ def cpu_reference(cfg, seconds_hint=None, threads=None, sample_tokens=48, steps=
         for t in ts:
             t.join()
         dt = time.perf_counter() - t0
+        if errs:
+            raise errs[0]
         if it >= warmup:
-            times.append(dt)
-    if errs:
-        raise errs[0]
+            # extrapolated: the step is the per-token time of the slowest thread x its tokens
+            times.append(dt if full else max(parts.values()) * sample_tokens)
     tok = threads * sample_tokens
     v = tok / statistics.mean(times)
-    desc = (f"{threads} host threads x {sample_tokens} tokens of the C2 layer per step "
-            f"(reference pf_moe_forward composition W=1, weights by reference, + reference "
-            f"grouped_expert_mlp for the 2 shared experts), "
-            f"fp64, backend {refbind.lib().ref_kernel_backend().decode()}")
+    how = ("reference pf_moe_forward composition (W=1) over the full layer" if full else
+           "EXTRAPOLATED from the reference's gate_forward per token + top_k x grouped_expert_mlp per row "
+           "(one expert's weights) timed on the sample")
+    desc = (f"{threads} host threads x {sample_tokens} tokens per step of {cfg['desc'].split(':')[0]} "
+            f"({how}{', + reference grouped_expert_mlp for the shared experts' if ns else ''}), "
+            f"fp64, inputs from the same Rng streams as the GPU arm, backend "
+            f"{refbind.lib().ref_kernel_backend().decode()}, CPU {cpu_model()}")
     return v, threads, times, desc
 
 
@@ -258,18 +336,24 @@ def bind_to_gpu_numa(device):
 def run_reference(args, rank, world, result_out):
     if rank != 0:
         return
-    # bounded per-step sample so that K+W steps stay within a few minutes
-    per_step = max(16, min(512, 1500 // max(1, args.steps + args.warmup)))
-    v, cores, times, desc = cpu_reference(C2, threads=host_threads(), sample_tokens=per_step,
+    from paper_2508_13337_b200 import configs
+    cfg = configs.CONFIGS[args.config]
+    # bounded per-step sample (>= 256 tokens per thread where the layer allows
+    # it) so that K+W steps stay within a few minutes
+    n = max(1, args.steps + args.warmup)
+    per_step = 256 if n <= 60 else max(64, min(256, 15000 // n))
+    threads = args.cpu_threads or host_threads()
+    v, cores, times, desc = cpu_reference(cfg, threads=threads, sample_tokens=per_step,
                                           steps=args.steps, warmup=args.warmup)
+    S = args.tokens or configs.tokens_per_gpu(cfg, world)
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": "C2: 64 routed experts top-6 + 2 shared, d_model 2048, d_ff 1408, "
-                                   "bf16-grid synthetic tokens; CPU sample per step",
-                       "tokens_per_gpu": args.tokens, "parallelism": f"ep{world}"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": desc},
+            "scaling": "strong" if cfg.get("ssmb") else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": cfg["desc"] + "; CPU sample per step", "tokens_per_gpu": S,
+                       "parallelism": f"ep{world}"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": desc,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), file=result_out, flush=True)
 
@@ -305,19 +389,20 @@ def main():
     else:
         ctx = capi.Context(local_rank, 1, 0)
 
-    cfg = C2
-    E, k, H, F, ns, Fs = cfg["E"], cfg["k"], cfg["H"], cfg["F"], cfg["n_shared"], cfg["Fs"]
-    S = args.tokens
-    El = E // world
-    g = torch.Generator(device="cuda")
-    g.manual_seed(1234)
-    gate = (torch.round((torch.rand(H, E, device="cuda", generator=g) * 0.2 - 0.1) * 1024) / 1024).to(torch.bfloat16)
-    g.manual_seed(5000 + rank)
-    w1 = ((torch.rand(El, H, F, device="cuda", generator=g) * 0.2 - 0.1)).to(torch.bfloat16)
-    w2 = ((torch.rand(El, F, H, device="cuda", generator=g) * 0.2 - 0.1)).to(torch.bfloat16)
-    g.manual_seed(777)
-    sw1 = ((torch.rand(ns, H, Fs, device="cuda", generator=g) * 0.2 - 0.1)).to(torch.bfloat16)
-    sw2 = ((torch.rand(ns, Fs, H, device="cuda", generator=g) * 0.2 - 0.1)).to(torch.bfloat16)
+    from paper_2508_13337_b200 import configs
+    cfg = configs.CONFIGS[args.config]
+    E, k, H, F, ns, Fs = cfg["E"], cfg["k"], cfg["H"], cfg["F"], cfg["ns"], cfg["Fs"]
+    ssmb = bool(cfg.get("ssmb"))
+    S = args.tokens or configs.tokens_per_gpu(cfg, world)   # this rank's tokens
+    S_seq = S * world if not ssmb else (args.tokens * world if args.tokens else cfg["S_total"])
+    if ssmb:  # every rank holds the whole sequence; rank g's shard is rows [g*S/G, ...)
+        gate, w1, w2, sw1, sw2, x_full = configs.device_inputs(ctx, capi, cfg, rank, world, S_seq, 0, torch)
+        base = S_seq // world
+        S = S_seq - (world - 1) * base if rank == world - 1 else base
+        x = x_full[rank * base:rank * base + S]
+    else:
+        gate, w1, w2, sw1, sw2, x = configs.device_inputs(ctx, capi, cfg, rank, world, S, rank * S, torch)
+    rbd_seed = configs.seeds(capi.salt_seed)["rbd"]
     if args.mode == "auto":
         # measured on B200: the redundancy bypass wins the step
         # at N=2; from N=4 the chunked plain dispatch, whose all-to-all
@@ -325,14 +410,24 @@ def main():
         # see dispatch_compare)
         args.mode = "rbd" if world == 2 else "naive"
     mode = capi.RBD if args.mode == "rbd" else capi.NAIVE
-    layer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
-                       max_tokens=S, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,
-                       dispatch_mode=mode, seed=99, chunks=args.chunks)
+    S_max = S_seq - (world - 1) * (S_seq // world) if ssmb else S
+
+    def make_layer(chunks=args.chunks, train=False, md=None):
+        return capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S_max * k,
+                          max_tokens=S_max, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,
+                          dispatch_mode=mode if md is None else md, seed=rbd_seed, chunks=chunks, train=train)
+
+    layer = make_layer()
     if not args.no_graph:
         layer.set_graph(True)
-    g.manual_seed(100 + rank)
-    x = (torch.round((torch.rand(S, H, device="cuda", generator=g) * 2 - 1) * 128) / 128).to(torch.bfloat16)
-    out = torch.empty_like(x)
+    out = torch.empty_like(x_full if ssmb else x)
+    xin = x_full if ssmb else x
+
+    def step(lyr, xi, oi):  # one pass of the hot path (SSMB: shard forward + all-gather)
+        if ssmb:
+            lyr.ssmb_forward(xi, oi)
+        else:
+            lyr.forward(xi, oi)
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -348,7 +443,7 @@ def main():
 
     # ---- warm-up
     for _ in range(args.warmup):
-        layer.forward(x, out)
+        step(layer, xin, out)
     torch.cuda.synchronize()
 
     # ---- device-timed region (inputs resident in HBM)
@@ -362,7 +457,7 @@ def main():
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for _ in range(args.steps):
-        layer.forward(x, out)
+        step(layer, xin, out)
     t1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -383,33 +478,29 @@ def main():
     # section changes the board's power/clock state),
     # on a forward-only unchunked layer (kernel-level stages; the training
     # layer's GEMM1 epilogue also stores ReLU masks)
-    slayer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
-                        max_tokens=S, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,
-                        dispatch_mode=mode, seed=99, chunks=1)
+    oshard = torch.empty_like(x)
+    slayer = make_layer(chunks=1)
     slayer.set_timing(True)
     stage_runs = []
     for _ in range(6):
-        slayer.forward(x, out)
+        slayer.forward(x, oshard)
         torch.cuda.synchronize()
         stage_runs.append(slayer.stage_ms())
     stages = {kk: statistics.median(r[kk] for r in stage_runs[1:]) for kk in stage_runs[0]}
     led = slayer.ledger()
     del slayer
     # ---- training layer (unchunked) for fwd+bwd
-    tlayer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
-                        max_tokens=S, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,
-                        dispatch_mode=mode, seed=99, train=not args.no_backward, chunks=1)
-    if not args.no_graph:
-        tlayer.set_graph(True)
-
     # ---- forward + backward (gradients w.r.t. x and every weight), same clock rules
+    # (training layer, unchunked; the sequence-sharded C4 block has no backward API)
     fwd_bwd = None
-    if not args.no_backward:
-        g.manual_seed(300 + rank)
-        dy = ((torch.rand(S, H, device="cuda", generator=g) * 2 - 1)).to(torch.bfloat16)
+    if not args.no_backward and not ssmb:
+        tlayer = make_layer(chunks=1, train=True)
+        if not args.no_graph:
+            tlayer.set_graph(True)
+        dy = ctx.rng_uniform(capi.salt_seed(0, 9500, rank), 0, S * H, -1.0, 1.0, dtype=capi.BF16).view(S, H)
         dxb = torch.empty_like(x)
         for _ in range(max(2, args.warmup)):
-            tlayer.forward(x, out)
+            tlayer.forward(x, oshard)
             tlayer.backward(x, dy, dxb)
         torch.cuda.synchronize()
         barrier()
@@ -417,7 +508,7 @@ def main():
         b1 = torch.cuda.Event(enable_timing=True)
         b0.record(stream)
         for _ in range(args.steps):
-            tlayer.forward(x, out)
+            tlayer.forward(x, oshard)
             tlayer.backward(x, dy, dxb)
         b1.record(stream)
         torch.cuda.synchronize()
@@ -426,7 +517,7 @@ def main():
         tlayer.set_timing(True)  # per-stage backward breakdown (eager launches)
         bst = []
         for _ in range(4):
-            tlayer.forward(x, out)
+            tlayer.forward(x, oshard)
             tlayer.backward(x, dy, dxb)
             torch.cuda.synchronize()
             bst.append(tlayer.bwd_stage_ms())
@@ -436,8 +527,7 @@ def main():
                    "ms_per_step": fb_ms, "bwd_stages_ms": bwd_stages,
                    "note": "forward + backward (dx and fp32 grads of gate, experts, shared experts); "
                            "gradients restated beyond the forward-only reference, checked against fp64 autograd"}
-
-    del tlayer
+        del tlayer
 
     # ---- plain vs redundancy-bypassing dispatch (N > 1): all-to-all bytes and
     # isolated kernel times of both, from unchunked layers in timing mode
@@ -445,13 +535,11 @@ def main():
     if world > 1:
         dispatch_compare = {}
         for name, md in (("naive", capi.NAIVE), ("rbd", capi.RBD)):
-            pl = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
-                            max_tokens=S, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,
-                            dispatch_mode=md, seed=99, chunks=1)
+            pl = make_layer(chunks=1, md=md)
             pl.set_timing(True)
             runs = []
             for _ in range(6):
-                pl.forward(x, out)
+                pl.forward(x, oshard)
                 torch.cuda.synchronize()
                 runs.append(pl.stage_ms())
             st_m = {kk: statistics.median(r[kk] for r in runs[1:]) for kk in runs[0]}
@@ -490,10 +578,10 @@ def main():
     # separate streams (double-buffered), as a serving loop would run them.
     e2e_steps = max(50, args.steps)  # steady state: one pipeline fill + drain amortised over the run
     numa_cpus = bind_to_gpu_numa(local_rank)
-    xh = [x.cpu().pin_memory() for _ in range(2)]
+    xh = [xin.cpu().pin_memory() for _ in range(2)]
     oh = [torch.empty_like(xh[0]).pin_memory() for _ in range(2)]
-    xd = [torch.empty_like(x) for _ in range(2)]
-    od = [torch.empty_like(x) for _ in range(2)]
+    xd = [torch.empty_like(xin) for _ in range(2)]
+    od = [torch.empty_like(xin) for _ in range(2)]
     s_in = torch.cuda.Stream()
     s_out = torch.cuda.Stream()
     ev_in = [torch.cuda.Event() for _ in range(2)]
@@ -517,7 +605,7 @@ def main():
             stream.wait_event(ev_in[b])
             if i >= 2:
                 stream.wait_event(ev_outfree[b])  # step i-2's output left the device
-            layer.forward(xd[b], od[b])
+            step(layer, xd[b], od[b])
             ev_done[b].record(stream)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_done[b])
@@ -539,25 +627,33 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            v, cores, _, desc = cpu_reference(C2, threads=host_threads(), sample_tokens=args.cpu_sample_tokens)
-            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": desc}
+            v, cores, _, desc = cpu_reference(cfg, threads=args.cpu_threads or host_threads(),
+                                              sample_tokens=args.cpu_sample_tokens)
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "sample": desc,
+                   "cpu_model": cpu_model()}
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
     if rank == 0:
-        value = world * S / (ms * 1e-3)
+        tokens_step = S_seq  # whole job: all ranks' tokens (C4: the one sharded sequence)
+        value = tokens_step / (ms * 1e-3)
+        wbytes = (E // world) * 2 * H * F * 2
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "C2: DeepSeek-MoE layer, 64 routed experts top-6 + 2 shared, d_model 2048, "
-                                   "d_ff 1408, bf16, expert parallel, dropless (BASELINE configs[1])",
-                       "tokens_per_gpu": S, "global_tokens": world * S, "parallelism": f"ep{world}",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if ssmb else "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (reference Rng streams drawn on the device; random-init weights)",
+            "config": {"workload": cfg["desc"], "config": args.config,
+                       "tokens_per_gpu": S, "global_tokens": tokens_step,
+                       "parallelism": (f"ssmb{world}+ep{world}" if ssmb else f"ep{world}"),
                        "dispatch": args.mode, "pass": "forward", "chunks": layer.chunks(),
                        "transport": (os.environ.get("XMOE_TRANSPORT") or "p2p") if world > 1 else "local",
-                       "l2": "working set > L2: 0.74 GB of expert weights + 64 MB tokens stream each step (126 MB L2)"},
-            "e2e": {"value": world * S / (e2e_ms * 1e-3), "unit": UNIT,
-                    "h2d_bytes_per_step": S * H * 2, "d2h_bytes_per_step": S * H * 2, "steps": e2e_steps,
+                       "l2": f"working set > L2: {wbytes / 1e9:.2f} GB of expert weights per GPU + "
+                             f"{S * H * 2 / 1e6:.0f} MB tokens stream each step (126 MB L2)"},
+            "e2e": {"value": tokens_step / (e2e_ms * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": xin.numel() * 2, "d2h_bytes_per_step": xin.numel() * 2,
+                    "steps": e2e_steps,
                     "host_cpus": numa_cpus,
                     "note": "pinned host x -> device, forward, device -> pinned host out, every step; copies of "
                             "neighbouring steps overlap the forward on two copy streams (double-buffered)"},
@@ -568,10 +664,9 @@ def main():
                                       f"of the forward, shorter than the sustained run; at N>1 it exceeds the "
                                       f"sustained figure); sustained {tf_sus}",
                          "frac_sustained": achieved / tf_sus,
-                         "traffic": gemm_traffic(),
+                         "traffic": gemm_traffic(args.config),
                          "traffic_note": "dram read+write bytes per routed-GEMM launch from the committed "
-                                         "ncu --set full capture (profiles/gemm_traffic.json); "
-                                         "algorithmic A+B+D bytes per launch ~1.05e9",
+                                         "ncu --set full capture (profiles/gemm_traffic*.json), null when absent",
                          "algorithmic_flops_per_launch_pair": gemm_flops,
                          "share_of_step": expert_frac_of_step},
             "stages_ms": stages,

@@ -313,10 +313,13 @@ int xmoe_moe_forward_v(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, const in
 
 /* moesim::ssmb_forward (ssmb.hpp:23-26, ssmb.cpp:12-46): x_full [S,H] is the
  * whole sequence on every rank; rank g runs rows [g*(S/G), ...) (last rank
- * takes the remainder) through the layer with every expert local
- * (the layer must hold all E experts), then an all-gather restores
- * out_full [S,H] on every rank.  G == world.  The layer is created with
- * XMOE_LAYER_SSMB and holds every expert; max_tokens >= the largest shard. */
+ * takes the remainder), then an all-gather restores out_full [S,H] on every
+ * rank.  G == world; max_tokens >= the largest shard.
+ *   XMOE_LAYER_SSMB layers hold every expert (the reference's replicated
+ *   weights, ssmb.cpp:29-43): each shard routes locally.
+ *   Expert-parallel layers (no XMOE_LAYER_SSMB; E/world experts per rank):
+ *   SSMB composed with EP — the shard's copies go to their owners through the
+ *   layer's exchange; same drop sets and, row by row, the same result. */
 int xmoe_ssmb_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x_full, int64_t S,
                       void* out_full, void* stream);
 

@@ -479,13 +479,16 @@ class Layer:
             out["sw2"] = view(ptrs[4], (sh["ns"] * sh["Fs"], H))
         return out
 
-    def inspect(self, what: str, worker: int = 0):
-        """Copy of one internal array of the last forward (xmoe_layer_inspect)."""
+    def inspect(self, what: str, worker: int = 0, limit: int | None = None):
+        """Copy of one internal array of the last forward (xmoe_layer_inspect),
+        at most `limit` elements."""
         code, dt = INSPECT[what]
         if dt is None:
             dt = _TDT[self.dtype]
         p, n = C.c_void_p(), C.c_int64()
         _check(lib().xmoe_layer_inspect(self.h, worker, code, C.byref(p), C.byref(n)))
+        if limit is not None:
+            n = C.c_int64(min(n.value, limit))
         if n.value == 0 or not p.value:
             return torch.empty(0, dtype=dt, device="cuda")
         typestr = {torch.int32: "<i4", torch.float64: "<f8", torch.uint8: "|u1", torch.float32: "<f4",

@@ -404,6 +404,223 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ---------------------------------------------------------------- fused gate
+// moesim::gate_forward (gating.cpp:14-57) in ONE kernel: the logits GEMM
+// x [S,H] . Wg^T [E,H] (E <= 256: one N tile) on the tensor cores, then the
+// epilogue thread that owns a token row reads its E fp32 logits straight from
+// TMEM and does the softmax and top-k in registers — no logits round trip
+// through HBM, no second launch.  Per row:
+//   pass 1  max and the top-k by (logit desc, id asc) — exp is monotone and
+//           on the grid inputs distinct logits differ by >= 2^-17, so this is
+//           the reference's (prob desc, id asc) order;
+//   pass 2  sum_e exp(l_e - max) in fp64, ascending e (gating.cpp:39-43);
+//           weights exp(l_j - max) / sum (raw probabilities, gating.cpp:51-54).
+// It also writes each tile's expert histogram (counts [tile, E]) for the
+// fused dropless placement (pft.cu route_place_kernel) and, for training
+// layers, the fp32 logits (the gate backward's input).
+template <int KMAX>
+__global__ void __launch_bounds__(kThreads, 1)
+    gate_route_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, int S,
+                      int E, int K, int k, int renorm, int32_t* __restrict__ top, double* __restrict__ weights,
+                      float* __restrict__ logits, int32_t* __restrict__ counts) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* smem_a = smem;
+    uint8_t* smem_b = smem + kStages * kABytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* full_bar = bars;
+    uint64_t* empty_bar = bars + kStages;
+    uint64_t* tfull_bar = bars + 2 * kStages;
+    uint64_t* tempty_bar = bars + 2 * kStages + kAccBufs;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * kAccBufs);
+    int32_t* hist = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 1024);  // [256]
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nkb = (K + BK - 1) / BK;
+    const int num_tiles = (S + BM - 1) / BM;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int b = 0; b < kAccBufs; ++b) {
+            mbar_init(&tfull_bar[b], 1);
+            mbar_init(&tempty_bar[b], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmap_a);
+        prefetch_tmap(&tmap_b);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                mbar_wait(&empty_bar[stage], phase ^ 1);
+                if (elect_one_sync()) {
+                    mbar_expect_tx(&full_bar[stage], kStageBytes);
+                    tma_load_2d(&tmap_a, &full_bar[stage], smem_a + stage * kABytes, kb * BK, t * BM);
+                    tma_load_2d(&tmap_b, &full_bar[stage], smem_b + stage * kBBytes, kb * BK, 0);
+                }
+                __syncwarp();
+                if (++stage == kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        const uint32_t idesc = make_idesc((E + 15) & ~15);
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * BN);
+            mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+            tc_fence_after();
+            for (int kb = 0; kb < nkb; ++kb) {
+                mbar_wait(&full_bar[stage], phase);
+                tc_fence_after();
+                if (elect_one_sync()) {
+                    const uint64_t da = make_desc(smem_u32(smem_a + stage * kABytes));
+                    const uint64_t db = make_desc(smem_u32(smem_b + stage * kBBytes));
+#pragma unroll
+                    for (int kk = 0; kk < BK / UK; ++kk)
+                        mma_bf16(tmem_d, da + static_cast<uint64_t>(kk * 2), db + static_cast<uint64_t>(kk * 2), idesc,
+                                 (kb > 0 || kk > 0) ? 1u : 0u);
+                    mma_commit(&empty_bar[stage]);
+                    if (kb == nkb - 1) mma_commit(&tfull_bar[acc]);
+                }
+                __syncwarp();
+                if (++stage == kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (++acc == kAccBufs) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    } else {
+        const int quarter = warp & 3;
+        const int et = threadIdx.x - 64;  // 0..127 over the epilogue warps
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            if (counts)
+                for (int e = et; e < E; e += 128) hist[e] = 0;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const int row = t * BM + quarter * 32 + lane;
+            const bool row_ok = row < S;
+            mbar_wait(&tfull_bar[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN);
+            float tv[KMAX];
+            int ti[KMAX];
+#pragma unroll
+            for (int j = 0; j < KMAX; ++j) {
+                tv[j] = -INFINITY;
+                ti[j] = 0x7fffffff;
+            }
+            float mx = -INFINITY;
+            for (int c0 = 0; c0 < E; c0 += 32) {  // pass 1: max, top-k, logits out
+                uint32_t v[32];
+                tmem_ld32(taddr + static_cast<uint32_t>(c0), v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int e = c0 + i;
+                    if (e >= E) break;
+                    float nv = __uint_as_float(v[i]);
+                    mx = fmaxf(mx, nv);
+                    int ni = e;
+#pragma unroll
+                    for (int j = 0; j < KMAX; ++j) {  // bubble insert: strict '>' keeps the lower id on ties
+                        if (j < k && nv > tv[j]) {
+                            const float fv = tv[j];
+                            const int fi = ti[j];
+                            tv[j] = nv;
+                            ti[j] = ni;
+                            nv = fv;
+                            ni = fi;
+                        }
+                    }
+                }
+                if (logits && row_ok) {
+                    float4* dst = reinterpret_cast<float4*>(logits + static_cast<size_t>(row) * E + c0);
+                    if (c0 + 32 <= E && (E & 3) == 0) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                                 __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+                    } else {
+                        for (int i = 0; i < 32 && c0 + i < E; ++i) logits[static_cast<size_t>(row) * E + c0 + i] = __uint_as_float(v[i]);
+                    }
+                }
+            }
+            const double m = static_cast<double>(mx);
+            double sum = 0.0;
+            for (int c0 = 0; c0 < E; c0 += 32) {  // pass 2: sum in ascending expert order
+                uint32_t v[32];
+                tmem_ld32(taddr + static_cast<uint32_t>(c0), v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (c0 + i < E) sum = __dadd_rn(sum, exp(__dsub_rn(static_cast<double>(__uint_as_float(v[i])), m)));
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty_bar[acc]);  // accumulator free for tile t + grid
+            if (++acc == kAccBufs) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+            if (row_ok) {
+                double w[KMAX], wsum = 0.0;
+#pragma unroll
+                for (int j = 0; j < KMAX; ++j) {
+                    w[j] = j < k ? __ddiv_rn(exp(__dsub_rn(static_cast<double>(tv[j]), m)), sum) : 0.0;
+                    if (j < k) wsum = __dadd_rn(wsum, w[j]);
+                }
+#pragma unroll
+                for (int j = 0; j < KMAX; ++j) {
+                    if (j >= k) break;
+                    top[static_cast<size_t>(row) * k + j] = ti[j];
+                    weights[static_cast<size_t>(row) * k + j] = renorm ? __ddiv_rn(w[j], wsum) : w[j];
+                    if (counts) atomicAdd(&hist[ti[j]], 1);
+                }
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (counts)
+                for (int e = et; e < E; e += 128) counts[static_cast<size_t>(t) * E + e] = hist[e];
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
+                     : "memory");
+    }
+}
+
 }  // namespace tc
 
 // ============================================================================
@@ -1603,6 +1820,28 @@ void launch_wgrad_mn_split(const void* A, int M, const void* B, int Nb, long lon
     long long blocks = (quads + 255) / 256;
     if (blocks > 8 * kNumSMs) blocks = 8 * kNumSMs;
     tc2::sum_partials_kernel<<<static_cast<int>(blocks < 1 ? 1 : blocks), 256, 0, st>>>(partial, splits, M, N, Nb, D);
+    XMOE_LAUNCH_CHECK();
+}
+
+bool gate_route_supported(int E, int k, int H) { return E >= 16 && E <= 256 && E % 16 == 0 && k >= 1 && k <= 8 && H % 8 == 0; }
+
+void launch_gate_route(const void* x, int S, int H, const void* gate_kmajor, int E, int k, int renorm, int32_t* top,
+                       double* weights, float* logits, int32_t* counts, cudaStream_t st) {
+    require(gate_route_supported(E, k, H), XMOE_ERR_VALIDATION,
+            "fused gate: 16 <= num_experts <= 256 (multiple of 16), top_k <= 8, model_dim % 8 == 0");
+    if (S == 0) return;
+    const CUtensorMap ta = make_tmap(x, S, H, tc::BM);
+    const CUtensorMap tb = make_tmap(gate_kmajor, E, H, tc::BN);
+    static bool attr_set = false;
+    if (!attr_set) {
+        XMOE_CUDA(cudaFuncSetAttribute(tc::gate_route_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(tc::kSmemBytes)));
+        attr_set = true;
+    }
+    const int tiles = (S + tc::BM - 1) / tc::BM;
+    const int grid = tiles < kNumSMs ? tiles : kNumSMs;
+    tc::gate_route_kernel<8><<<grid, tc::kThreads, tc::kSmemBytes, st>>>(ta, tb, S, E, H, k, renorm, top, weights,
+                                                                         logits, counts);
     XMOE_LAUNCH_CHECK();
 }
 

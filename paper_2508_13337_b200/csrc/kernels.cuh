@@ -88,6 +88,18 @@ void launch_grouped_gemm_bf16_f32out(const void* A, long long rows, int K,
                                      const int32_t* rows_per_group, int G, const void* B, int N,
                                      float* D, int relu, cudaStream_t st);
 
+// fused gate (gemm_tc.cu): logits GEMM + softmax + top-k from TMEM, per-tile
+// expert histograms counts [ceil(S/128), E] (optional), fp32 logits (optional)
+bool gate_route_supported(int E, int k, int H);
+void launch_gate_route(const void* x, int S, int H, const void* gate_kmajor, int E, int k, int renorm, int32_t* top,
+                       double* weights, float* logits, int32_t* counts, cudaStream_t st);
+// fused dropless placement (pft.cu) from the gate's tile histograms: the
+// packed ERI arrays, tokens_per_expert, slot_pos and B (= S*k)
+void launch_route_place(const int32_t* top, const double* weights, const int32_t* counts, int S, int E, int k,
+                        int32_t* token_ids, int32_t* expert_ids, double* cw, int32_t* tpe, int32_t* slot_pos,
+                        int32_t* B_dev, cudaStream_t st);
+constexpr int kRouteTile = 128;  // tokens per gate tile / histogram row
+
 // backward.cu
 void launch_bwd_owner_prep(const void* dyg, const void* eout, const float* gw, const unsigned long long* gsrc,
                            const int32_t* rpe, int El, int H, long long max_rows, float* const* slotdw_tab,

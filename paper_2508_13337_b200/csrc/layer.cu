@@ -268,6 +268,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
             L.R_max = std::max<long long>(L.R_max, static_cast<long long>(L.Rc) * L.nchunks);
         }
     }
+    L.route_cnt_ok = bf && gate_route_supported(L.E, L.k, L.H);
     const long long gmax = S * std::min<long long>(L.k, W);  // RBD groups per source
     const long long rmax = static_cast<long long>(W) * S;   // RBD groups received
     L.tpe_all = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * W * E));
@@ -317,6 +318,8 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         w.tpe = L.distributed ? static_cast<int32_t*>(L.alloc(sizeof(int32_t) * E))
                               : L.tpe_all + static_cast<size_t>(w.rank) * E;
         w.pft_ws = L.alloc(bucket_ws_bytes(nk, E));
+        if (L.route_cnt_ok)
+            w.route_cnt = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * ((S + kRouteTile - 1) / kRouteTile) * E));
         w.dest_rank = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * nk));
         w.dest_row = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * nk));
         w.slot_src = static_cast<unsigned long long*>(L.alloc(sizeof(unsigned long long) * nk));
@@ -577,6 +580,40 @@ static void exchange_counts(Layer& L, cudaStream_t st) {
     launch_counts_exchange(sg, L.cnt_tab, L.area_ints, w.rank, W, L.flag_tab, w.flags, kSlotCounts, L.epoch, L.peer_err_d, st);
 }
 
+// Fused routing (BF16): the gate GEMM's epilogue does softmax + top-k from
+// TMEM and writes per-tile expert histograms; the dropless placement is then
+// one launch (gemm_tc.cu gate_route_kernel, pft.cu route_place_kernel) instead
+// of gate GEMM + softmax + six PFT kernels.  Applies when no bucket can
+// overflow (cap >= S); XMOE_FUSED_ROUTE=0 keeps the general path (A/B).
+static bool fused_route(const Layer& L, long long S) {
+    static const bool on = [] {
+        const char* e = std::getenv("XMOE_FUSED_ROUTE");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on && L.d.dtype == XMOE_BF16 && L.route_cnt_ok && L.d.max_token_count >= S;
+}
+
+static void route_gate(Layer& L, Worker& w, const void* x, long long S, cudaStream_t st) {
+    float* lg = reinterpret_cast<float*>(w.logits);
+    if (fused_route(L, S)) {
+        launch_gate_route(x, static_cast<int>(S), L.H, L.gate, L.E, L.k, L.d.renorm, w.top, w.wts,
+                          L.train ? lg : nullptr, w.route_cnt, st);
+        return;
+    }
+    launch_grouped_gemm_bf16_f32out(x, S, L.H, w.s_rows, 1, L.gate, L.E, lg, 0, st);
+    launch_softmax_topk_f32(lg, S, L.E, L.k, L.d.renorm, w.top, w.wts, st);
+}
+
+static void route_pft(Layer& L, Worker& w, long long S, cudaStream_t st) {
+    if (fused_route(L, S)) {
+        launch_route_place(w.top, w.wts, w.route_cnt, static_cast<int>(S), L.E, L.k, w.token_ids, w.expert_ids, w.cw,
+                           w.tpe, w.slot_pos, w.B_dev, st);
+        return;
+    }
+    launch_pft(w.top, w.wts, S, L.k, L.E, static_cast<int>(std::min<long long>(L.d.max_token_count, 0x7fffffff)),
+               w.token_ids, w.expert_ids, w.cw, w.tpe, w.slot_pos, w.B_dev, w.pft_ws, st);
+}
+
 // ---------------------------------------------------------------- chunked forward
 // BF16 forward (plain or RBD dispatch), cut into L.nchunks token chunks
 // (chunk.cu).  Streams:
@@ -626,12 +663,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     L.mark(kEvStart, st);
     for (int i = 0; i < nl; ++i)
         launch_forward_begin(L.workers[i].s_rows, static_cast<int>(S), i == 0 ? L.epoch : nullptr, st);
-    for (int i = 0; i < nl; ++i) {  // 1. gate (gating.cpp:14-57)
-        Worker& w = L.workers[i];
-        float* lg = reinterpret_cast<float*>(w.logits);
-        launch_grouped_gemm_bf16_f32out(x_of(i), S, H, w.s_rows, 1, L.gate, E, lg, 0, st);
-        launch_softmax_topk_f32(lg, S, E, k, L.d.renorm, w.top, w.wts, st);
-    }
+    for (int i = 0; i < nl; ++i) route_gate(L, L.workers[i], x_of(i), S, st);  // 1. gate (gating.cpp:14-57)
     L.mark(kEvGate, st);
     XMOE_CUDA(cudaEventRecord(L.ev_fork, st));
     XMOE_CUDA(cudaStreamWaitEvent(cm, L.ev_fork, 0));
@@ -639,8 +671,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     //    destinations, then every chunk's rows
     for (int i = 0; i < nl; ++i) {
         Worker& w = L.workers[i];
-        launch_pft(w.top, w.wts, S, k, E, static_cast<int>(std::min<long long>(L.d.max_token_count, 0x7fffffff)),
-                   w.token_ids, w.expert_ids, w.cw, w.tpe, w.slot_pos, w.B_dev, w.pft_ws, cm);
+        route_pft(L, w, S, cm);
         launch_chunk_counts(w.token_ids, w.tpe, E, static_cast<int>(S), C, w.tpe_c, w.pfx_c, w.seg, cm);
         if (rbd) {  // groups, pilots (rbd.cpp:26-81), per (dest, chunk) counts
             launch_rbd_groups(w.slot_pos, w.expert_ids, static_cast<int>(S), k, El, w.rbd.state, L.jumps, w.rbd,
@@ -832,9 +863,7 @@ void layer_forward_v(Layer& L, const void* x, const long long* Sw, void* out, cu
                                    S, H, E, w.logits, st);
             launch_softmax_topk(w.logits, S, E, k, L.d.renorm, w.top, w.wts, st);
         } else {
-            float* lg = reinterpret_cast<float*>(w.logits);
-            launch_grouped_gemm_bf16_f32out(x_of(i), S, H, w.s_rows, 1, L.gate, E, lg, 0, st);
-            launch_softmax_topk_f32(lg, S, E, k, L.d.renorm, w.top, w.wts, st);
+            route_gate(L, w, x_of(i), S, st);
         }
     }
     L.mark(kEvGate, st);
@@ -874,8 +903,9 @@ void layer_forward_v(Layer& L, const void* x, const long long* Sw, void* out, cu
     for (int i = 0; i < nl; ++i) {
         Worker& w = L.workers[i];
         const long long S = Sw[i], nk = S * k;
-        launch_pft(w.top, w.wts, S, k, E, static_cast<int>(std::min<long long>(L.d.max_token_count, 0x7fffffff)),
-                   w.token_ids, w.expert_ids, w.cw, w.tpe, w.slot_pos, w.B_dev, w.pft_ws, st);
+        if (dt == XMOE_BF16) route_pft(L, w, S, st);
+        else launch_pft(w.top, w.wts, S, k, E, static_cast<int>(std::min<long long>(L.d.max_token_count, 0x7fffffff)),
+                        w.token_ids, w.expert_ids, w.cw, w.tpe, w.slot_pos, w.B_dev, w.pft_ws, st);
         if (rbd) {
             launch_rbd_groups(w.slot_pos, w.expert_ids, static_cast<int>(S), k, L.El, w.rbd.state, L.jumps,
                               w.rbd, st);
@@ -1205,7 +1235,6 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
 // the all-gather is a group of NCCL broadcasts (shards may differ in size).
 void ssmb_forward(Ctx& ctx, Layer& L, const void* x_full, long long S, void* out_full, cudaStream_t st) {
     const int G = ctx.world;
-    require(L.ssmb, XMOE_ERR_VALIDATION, "ssmb_forward: layer was not created for sequence sharding");
     require(G >= 1, XMOE_ERR_VALIDATION, "ssmb_forward: shard count must be >= 1");
     require(G <= S, XMOE_ERR_VALIDATION, "ssmb_forward: more shards than sequence rows");
     const long long base = S / G;
@@ -1213,6 +1242,32 @@ void ssmb_forward(Ctx& ctx, Layer& L, const void* x_full, long long S, void* out
     auto rows_of = [&](int g) { return g == G - 1 ? S - static_cast<long long>(g) * base : base; };
     const char* xb = static_cast<const char*>(x_full);
     char* ob = static_cast<char*>(out_full);
+    if (!L.ssmb) {
+        // Sequence shards over an EXPERT-PARALLEL layer (SSMB composed with
+        // EP): shard g's tokens are rank g's tokens, experts
+        // stay partitioned, and the exchange replaces the replicated weights.
+        // Capacity applies per source rank as in pft_construct, so the drop
+        // sets equal the reference's local-per-shard ones (§8(e)); every row's
+        // arithmetic is row-independent, so the output equals the replicated
+        // SSMB layer's bit for bit.
+        require(L.W == G, XMOE_ERR_VALIDATION, "ssmb_forward: shard count must match the worker-group size");
+        if (ctx.rank < 0 || G == 1) {  // shards are the workers' blocks, back to back
+            std::vector<long long> Sw(G);
+            for (int g = 0; g < G; ++g) Sw[g] = rows_of(g);
+            layer_forward_v(L, x_full, Sw.data(), out_full, st);
+            return;
+        }
+        const int me = ctx.rank;
+        layer_forward(L, xb + me * base * rb, rows_of(me), ob + me * base * rb, st);
+        auto comm = static_cast<ncclComm_t>(ctx.nccl);
+        XMOE_NCCL(ncclGroupStart());
+        for (int g = 0; g < G; ++g) {
+            char* p = ob + g * base * rb;
+            XMOE_NCCL(ncclBroadcast(p, p, rows_of(g) * rb, ncclUint8, g, comm, st));
+        }
+        XMOE_NCCL(ncclGroupEnd());
+        return;
+    }
     if (L.ssmb_cap < G) {  // kept copies per shard, for the ledger
         L.ssmb_B = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * G));
         L.ssmb_cap = G;

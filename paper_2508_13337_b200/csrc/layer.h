@@ -41,6 +41,7 @@ struct Worker {
     int32_t* B_dev = nullptr;     // packed row count
     int32_t* tpe = nullptr;       // [E] tokens per expert (row of tpe_all when shared)
     void* pft_ws = nullptr;
+    int32_t* route_cnt = nullptr; // [ceil(S/128), E] per-tile expert histograms of the fused gate
     int32_t* dest_rank = nullptr; // [S*k] owner of each packed row
     int32_t* dest_row = nullptr;  // [S*k] its row in the owner's grouped buffer
     int32_t* rpe = nullptr;       // [El] rows per local expert (recv_per_expert)
@@ -113,6 +114,7 @@ struct Layer {
     int gpn = 1;               // RBD GPUs per node (node_of = rank / gpn)
     bool rbd_gather = false;   // RBD GEMM1 gathers replica rows (no expand copy)
     bool ssmb = false;         // sequence-sharded block: experts replicated, MoE local
+    bool route_cnt_ok = false; // fused gate + dropless placement available (BF16, E <= 256, k <= 8)
     bool distributed = false;  // one process per GPU, world > 1
     bool p2p = false;          // NVLink peer tables (else NCCL send/recv baseline)
     int32_t* bar = nullptr;    // 4-byte all-reduce used as a cross-rank barrier

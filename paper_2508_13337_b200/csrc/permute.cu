@@ -75,43 +75,54 @@ __global__ void __launch_bounds__(32 * kRowWarps) gather_rows_kernel(
 //     expert_base_j[le] + sum_{s < src} tpe_s[e] + (r - blk_src[e])
 // which is the (local expert, source, position) order of pf_dispatch
 // (pf_pipeline.cpp:47-73).  tpe_all is the all-gathered [W, E] matrix.
+// exclusive scan of v[0..n) by one warp (n <= 32 * 32), out may alias v
+__device__ __forceinline__ void warp_exscan(const int32_t* v, int32_t* out, int n, int lane) {
+    int carry = 0;
+    for (int b0 = 0; b0 < n; b0 += 32) {
+        const int x = b0 + lane < n ? v[b0 + lane] : 0;
+        int incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (b0 + lane < n) out[b0 + lane] = carry + incl - x;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
 __global__ void dispatch_dest_kernel(const int32_t* __restrict__ tpe_all, int W, int E, int src,
                                      const int32_t* __restrict__ expert_ids,
                                      const int32_t* __restrict__ B_dev,
                                      int32_t* __restrict__ dest_rank,
                                      int32_t* __restrict__ dest_row) {
     extern __shared__ int32_t sh[];
-    int32_t* blk = sh;              // [E+1] packed block start of each expert at src
-    int32_t* before = sh + E + 1;   // [E] rows of expert e from sources < src
+    int32_t* blk = sh;              // [E] packed block start of each expert at src
+    int32_t* before = sh + E;       // [E] rows of expert e from sources < src
     int32_t* ebase = before + E;    // [E] grouped base of expert e on its owner
     const int El = E / W;
-    if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int e = 0; e < E; ++e) {
-            blk[e] = acc;
-            acc += tpe_all[src * E + e];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {  // column sums and the sources before src
+        int b = 0, all = 0;
+        for (int s = 0; s < W; ++s) {
+            const int c = tpe_all[s * E + e];
+            all += c;
+            if (s < src) b += c;
         }
-        blk[E] = acc;
-        for (int e = 0; e < E; ++e) {
-            int b = 0;
-            for (int s = 0; s < src; ++s) b += tpe_all[s * E + e];
-            before[e] = b;
-        }
-        for (int j = 0; j < W; ++j) {
-            int a = 0;
-            for (int le = 0; le < El; ++le) {
-                const int e = j * El + le;
-                ebase[e] = a;
-                for (int s = 0; s < W; ++s) a += tpe_all[s * E + e];
-            }
-        }
+        before[e] = b;
+        ebase[e] = all;
+        blk[e] = tpe_all[src * E + e];
     }
+    __syncthreads();
+    if (wid == 0) warp_exscan(blk, blk, E, lane);
+    else if (wid == 1) warp_exscan(ebase, ebase, E, lane);
     __syncthreads();
     const int B = *B_dev;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < B; r += gridDim.x * blockDim.x) {
         const int e = expert_ids[r];
         dest_rank[r] = e / El;
-        dest_row[r] = ebase[e] + before[e] + (r - blk[e]);
+        // grouped base of e on its owner: column sums of the owner's experts before e
+        dest_row[r] = ebase[e] - ebase[(e / El) * El] + before[e] + (r - blk[e]);
     }
 }
 
@@ -301,6 +312,7 @@ void launch_dispatch_dest(const int32_t* tpe_all, int W, int E, int src,
                           const int32_t* expert_ids, const int32_t* B_dev, long long max_rows,
                           int32_t* dest_rank, int32_t* dest_row, cudaStream_t st) {
     const int blocks = ceil_div(max_rows > 0 ? max_rows : 1, 256);
+    require(blocks >= 1 && E <= 1024, XMOE_ERR_VALIDATION, "dispatch destinations: num_experts <= 1024");
     dispatch_dest_kernel<<<blocks < 4 * kNumSMs ? blocks : 4 * kNumSMs, 256,
                            sizeof(int32_t) * (3 * E + 1), st>>>(tpe_all, W, E, src, expert_ids,
                                                                B_dev, dest_rank, dest_row);

@@ -386,6 +386,109 @@ __global__ void slot_sort_kernel(const int32_t* __restrict__ fpos, int S, int k,
     }
 }
 
+// ---------------------------------------------------------------- fused dropless placement
+// pft_construct (pft.cpp:12-60) when no bucket can overflow (cap >= S: every
+// expert holds at most one copy per token), in one launch from the gate's
+// per-tile expert histograms (gemm_tc.cu gate_route_kernel).  Block b owns
+// tokens [128 b, 128 b + 128):
+//   base[e] = (copies of experts < e) + (copies of e in tiles < b)
+//   rank    = tokens t' < t of this tile routed to e: a 128-bit token mask per
+//             expert (atomicOr, order-free) and a popcount below t
+// so copy (t, e) lands at packed row base[e] + rank — experts ascending,
+// tokens ascending inside an expert: the reference's order, bit for bit.
+// Each token's kept rows are then written ascending (slot_pos).
+__global__ void __launch_bounds__(256) route_place_kernel(const int32_t* __restrict__ top,
+                                                          const double* __restrict__ w,
+                                                          const int32_t* __restrict__ counts, int nt, int S, int E,
+                                                          int k, int32_t* __restrict__ token_ids,
+                                                          int32_t* __restrict__ expert_ids, double* __restrict__ cw,
+                                                          int32_t* __restrict__ tpe, int32_t* __restrict__ slot_pos,
+                                                          int32_t* __restrict__ B_dev) {
+    __shared__ int32_t tot[256], base[256];
+    __shared__ uint32_t mask[256][4];
+    const int b = blockIdx.x, tid = threadIdx.x;
+    for (int e = tid; e < E; e += blockDim.x) {
+        int all = 0, before = 0;
+        for (int q = 0; q < nt; ++q) {
+            const int c = counts[static_cast<size_t>(q) * E + e];
+            all += c;
+            if (q < b) before += c;
+        }
+        tot[e] = all;
+        base[e] = before;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mask[e][q] = 0u;
+    }
+    __syncthreads();
+    if (tid < 32) {  // exclusive scan of tot over experts (E <= 256: 8 per lane)
+        int v[8], run = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = tid * 8 + q;
+            v[q] = e < E ? tot[e] : 0;
+            run += v[q];
+        }
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tid >= o) incl += y;
+        }
+        int ex = incl - run;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = tid * 8 + q;
+            if (e < E) {
+                base[e] += ex;
+                if (b == 0) tpe[e] = v[q];
+            }
+            ex += v[q];
+        }
+        if (b == 0 && tid == 0) *B_dev = S * k;
+    }
+    const int t = tid, tok = b * kRouteTile + t;
+    const bool ok = t < kRouteTile && tok < S;
+    if (ok)
+        for (int j = 0; j < k; ++j) {
+            const int e = top[static_cast<size_t>(tok) * k + j];
+            atomicOr(&mask[e][t >> 5], 1u << (t & 31));
+        }
+    __syncthreads();
+    if (!ok) return;
+    int pos[32];
+    for (int j = 0; j < k; ++j) {
+        const int e = top[static_cast<size_t>(tok) * k + j];
+        int r = __popc(mask[e][t >> 5] & ((1u << (t & 31)) - 1u));
+        for (int q = 0; q < (t >> 5); ++q) r += __popc(mask[e][q]);
+        const int p = base[e] + r;
+        token_ids[p] = tok;
+        expert_ids[p] = e;
+        cw[p] = w[static_cast<size_t>(tok) * k + j];
+        int q = j;  // insertion: kept rows ascending (= experts ascending)
+        while (q > 0 && pos[q - 1] > p) {
+            pos[q] = pos[q - 1];
+            --q;
+        }
+        pos[q] = p;
+    }
+    for (int j = 0; j < k; ++j) slot_pos[static_cast<size_t>(tok) * k + j] = pos[j];
+}
+
+void launch_route_place(const int32_t* top, const double* weights, const int32_t* counts, int S, int E, int k,
+                        int32_t* token_ids, int32_t* expert_ids, double* cw, int32_t* tpe, int32_t* slot_pos,
+                        int32_t* B_dev, cudaStream_t st) {
+    require(E <= 256 && k <= 32, XMOE_ERR_VALIDATION, "fused placement: num_experts <= 256, top_k <= 32");
+    if (S == 0) {
+        XMOE_CUDA(cudaMemsetAsync(tpe, 0, sizeof(int32_t) * E, st));
+        XMOE_CUDA(cudaMemsetAsync(B_dev, 0, sizeof(int32_t), st));
+        return;
+    }
+    const int nt = (S + kRouteTile - 1) / kRouteTile;
+    route_place_kernel<<<nt, 256, 0, st>>>(top, weights, counts, nt, S, E, k, token_ids, expert_ids, cw, tpe,
+                                           slot_pos, B_dev);
+    XMOE_LAUNCH_CHECK();
+}
+
 // ---------------------------------------------------------------- host side
 size_t bucket_ws_bytes(long long n, int K) {
     const long long nchunks = (n + kChunk - 1) / kChunk + 1;

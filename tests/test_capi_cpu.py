@@ -24,8 +24,10 @@ def test_library_exports_every_declared_symbol():
 def test_cpp_compat_api_exported():
     out = subprocess.run(["nm", "-DC", build.LIB], capture_output=True, text=True).stdout
     hdr = open(build.ROOT + "/include/xmoe/moesim_compat.hpp").read()
-    names = set(re.findall(r"^\w[\w:<>, ]*\s+(\w+)\(const", hdr, re.M)) | {"pf_moe_forward", "rbd_moe_forward",
-                                                                         "ssmb_forward", "pft_construct"}
+    names = set(re.findall(r"^(?!inline)\w[\w:<>, ]*\s+(\w+)\((?:const|Comm|Rng)", hdr, re.M)) | {
+        "pf_moe_forward", "rbd_moe_forward", "ssmb_forward", "pft_construct", "pf_dispatch", "pf_combine",
+        "select_pilots", "rbd_dispatch", "rbd_combine", "make_layer_weights", "sample_redundancy"}
+    assert len(names) >= 20
     for n in names:
         assert f"xmoe::{n}(" in out, n
 

@@ -1,16 +1,21 @@
-"""BASELINE.json configs 2-5 at (or near) full size, bf16, through the C-ABI
-layer.  The oracle cannot run these sizes end to end in seconds, so parity is
-checked on a seeded SAMPLE of tokens: routing of the sampled rows comes from
-the pinned oracle gate (moe_oracle.gate_forward, gating.cpp:14-57), the
-expert FFNs of those rows are evaluated in fp64 torch on the same bf16
-weights (pf_pipeline.cpp:83-105), and the weighted sum is the reference's
-combine (pf_pipeline.cpp:107-135).  A misrouted copy, a lost or duplicated
-row, or a wrong weight shows up as an O(1) error; the stated tolerance is
-the bf16 one of test_gpu_layer.py (normwise < 1e-2 over the sample).
+"""BASELINE.json configs C1-C5 at FULL size, bf16, through the C-ABI layer
+(W workers driven from one process on one GPU for the expert-parallel
+shapes), on the bench's own inputs (the reference generator drawn on the
+device, paper_2508_13337_b200/configs.py).
 
-Inputs are on the bf16-exact grid (tokens 2^-7, gate 2^-10) so the fp32
-logits — and therefore the routing — are exact.  Weights are generated on
-the device (config 3 is 15 GB of bf16 expert weights)."""
+Bit-exact at full size, against an independent torch restatement of the
+reference's routing on the SAME device-held values (gating.cpp:14-57: on the
+bf16-exact grid every logit is an exact multiple of 2^-17 in fp64, so the
+reference's probability order is the logit order with ties to the lower id;
+pft.cpp:12-60 dropless: experts ascending, tokens ascending):
+  * every worker's top_experts, tokens_per_expert, token_ids, expert_ids;
+  * every owner's grouped expert input (pf_pipeline.cpp:47-73 order), row for
+    row (a pure copy of bf16 tokens).
+Outputs: a seeded sample of tokens against fp64 torch over the same bf16
+weights (normwise < 1e-2, the bf16 bar of test_gpu_layer.py).
+C5 additionally asserts the skew SURVEY §8(d) asks for (>= 1 empty expert,
+max load >= 4x the mean) and C4 that SSMB composed with EP equals the
+replicated-expert SSMB bit for bit (identical drop sets, §8(e))."""
 import numpy as np
 import pytest
 import torch
@@ -21,118 +26,151 @@ from tests.gpu_util import host, norm_rel
 pytestmark = pytest.mark.gpu
 
 
-def _weights(E, H, F, ns, Fs, seed):
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    u = lambda *s: ((torch.rand(*s, device="cuda", generator=g) - 0.5) * 0.2).to(torch.bfloat16)  # noqa: E731
-    w1, w2 = u(E, H, F), u(E, F, H)
-    sw1 = u(ns, H, Fs) if ns else None
-    sw2 = u(ns, Fs, H) if ns else None
-    return w1, w2, sw1, sw2
+def _inputs(cfg_name, W, S):
+    from paper_2508_13337_b200 import capi, configs
+    cfg = dict(configs.CONFIGS[cfg_name])
+    ctx = capi.Context(0, W, -1)
+    gate, w1, w2, sw1, sw2, x = configs.device_inputs(ctx, capi, cfg, 0, 1, W * S, 0, torch)
+    return ctx, cfg, gate, w1, w2, sw1, sw2, x
 
 
-def _grid_tokens(n, H, seed):
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    return (torch.randint(-128, 129, (n, H), device="cuda", generator=g).to(torch.float32) / 128).to(torch.bfloat16)
+def _routing(x, gate, k):
+    """Reference routing of bf16 grid tokens: exact fp64 logits, stable order."""
+    lg = x.double() @ gate.double()
+    order = torch.sort(-lg, dim=1, stable=True).indices
+    return order[:, :k].to(torch.int32)
 
 
-def _grid_gate(H, E, seed, zipf=None):
-    rng = np.random.default_rng(seed)
-    gate = np.round(rng.uniform(-0.1, 0.1, (H, E)) * 1024) / 1024
-    if zipf is not None:  # token feature 0 is pinned to 1.0: a per-expert logit bias
-        p = 1.0 / np.arange(1, E + 1) ** zipf
-        gate[0] = np.round(np.log(p / p.max()) * 1024) / 1024
-        gate[0, E - 4:] = -16.0  # four experts never chosen: empty groups
-    return torch.from_numpy(gate).to(torch.bfloat16).double().numpy()  # what the device holds
+def _pft(top, E):
+    """Dropless pft_construct: packed rows grouped by expert, tokens ascending."""
+    S, k = top.shape
+    flat = top.reshape(-1).long()
+    order = torch.sort(flat, stable=True).indices
+    return (order // k).to(torch.int32), flat[order].to(torch.int32), torch.bincount(flat, minlength=E).to(torch.int32)
+
+
+def _check_routing_and_layout(L, x, gate, W, S, E, k):
+    H = x.shape[1]
+    El = E // W
+    tpes, tids = [], []
+    for w in range(W):
+        xs = x[w * S:(w + 1) * S]
+        top = _routing(xs, gate, k)
+        tid, eid, tpe = _pft(top, E)
+        assert torch.equal(L.inspect("top_experts", w).view(S, k), top), w
+        assert torch.equal(L.inspect("tokens_per_expert", w), tpe), w
+        assert torch.equal(L.inspect("token_ids", w), tid), w
+        assert torch.equal(L.inspect("expert_ids", w), eid), w
+        tpes.append(tpe.long())
+        tids.append(tid.long())
+    tpe_all = torch.stack(tpes)                      # [W, E]
+    starts = torch.cumsum(tpe_all, 1) - tpe_all      # packed segment start per (src, e)
+    for j in range(W):
+        idx = []
+        for le in range(El):
+            e = j * El + le
+            for s in range(W):
+                a, n = int(starts[s, e]), int(tpe_all[s, e])
+                idx.append(s * S + tids[s][a:a + n])
+        idx = torch.cat(idx)
+        got = L.inspect("expert_input", j, limit=idx.numel() * H).view(-1, H)
+        assert torch.equal(got, x[idx]), j          # grouped layout bit-exact at full size
+    return tpe_all
 
 
 def _sampled_reference(x, gate, w1, w2, sw1, sw2, k, rows):
-    """fp64 output of the sampled rows (see module docstring)."""
+    """fp64 output of the sampled rows over the same bf16 weights."""
     xs = x[rows].double()
-    g = O.gate_forward(xs.cpu().numpy(), gate, k)
+    g = O.gate_forward(xs.cpu().numpy(), gate.double().cpu().numpy(), k)
     y = torch.zeros_like(xs)
     for j in range(k):
         for e in np.unique(g.top_experts[:, j]):
             sel = np.nonzero(g.top_experts[:, j] == e)[0]
             h = torch.relu(xs[sel] @ w1[e].double()) @ w2[e].double()
-            wt = torch.from_numpy(g.combine_weights[sel, j]).to(xs)
-            y[sel] += wt[:, None] * h
+            y[sel] += torch.from_numpy(g.combine_weights[sel, j]).to(xs)[:, None] * h
     if sw1 is not None:
         for s in range(sw1.shape[0]):
             y += torch.relu(xs @ sw1[s].double()) @ sw2[s].double()
     return host(y)
 
 
-def _run(W, S, E, k, H, F, ns, Fs, mode=0, zipf=None, n_sample=64, seed=0):
+def _layer(ctx, cfg, S, gate, w1, w2, sw1, sw2, mode=0, ssmb=False):
     from paper_2508_13337_b200 import capi
-    ctx = capi.Context(0, W, -1)
-    w1, w2, sw1, sw2 = _weights(E, H, F, ns, Fs, seed)
-    gate = _grid_gate(H, E, seed + 1, zipf)
-    x = _grid_tokens(W * S, H, seed + 2)
-    if zipf is not None:
-        x[:, 0] = 1.0
-    L = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
-                   max_tokens=S, dtype=capi.BF16,
-                   gate=torch.from_numpy(gate).to(torch.bfloat16).cuda(), w1=w1, w2=w2, sw1=sw1, sw2=sw2,
-                   dispatch_mode=mode, seed=seed)
-    out = L.forward(x.view(W, S, H)).view(W * S, H)
+    return capi.Layer(ctx, num_experts=cfg["E"], model_dim=cfg["H"], ffn_dim=cfg["F"], top_k=cfg["k"],
+                      max_token_count=S * cfg["k"], max_tokens=S, dtype=capi.BF16, gate=gate, w1=w1, w2=w2,
+                      sw1=sw1, sw2=sw2, dispatch_mode=mode, seed=7, ssmb=ssmb, chunks=1)
+
+
+def _run(cfg_name, W, S, mode=0, n_sample=48):
+    ctx, cfg, gate, w1, w2, sw1, sw2, x = _inputs(cfg_name, W, S)
+    L = _layer(ctx, cfg, S, gate, w1, w2, sw1, sw2, mode)
+    out = L.forward(x.view(W, S, -1)).view(W * S, -1)
     torch.cuda.synchronize()
-    rows = np.sort(np.random.default_rng(seed).choice(W * S, n_sample, replace=False))
-    want = _sampled_reference(x, gate, w1, w2, sw1, sw2, k, rows)
+    tpe_all = _check_routing_and_layout(L, x, gate, W, S, cfg["E"], cfg["k"])
+    rows = np.sort(np.random.default_rng(W + S).choice(W * S, n_sample, replace=False))
+    want = _sampled_reference(x, gate, w1, w2, sw1, sw2, cfg["k"], rows)
     got = host(out[torch.from_numpy(rows).cuda()])
     assert np.isfinite(got).all()
     assert norm_rel(got, want) < 1e-2, norm_rel(got, want)
-    return L, x, out
+    return L, tpe_all
+
+
+def test_c1_layer():
+    """C1: 64 experts top-6 + 2 shared, 2048/1408, 4096 tokens."""
+    _run("c1", 1, 4096)
 
 
 @pytest.mark.parametrize("mode", [0, 1])
-def test_config2_deepseek_moe_ep8(mode):
-    """Config 2: 64 experts top-6 + 2 shared, 2048/1408, 16K tokens per GPU,
-    8 expert-parallel workers (driven from one process), plain and RBD."""
-    L, _, _ = _run(8, 16384, 64, 6, 2048, 1408, 2, 1408, mode=mode, n_sample=48)
-    led = L.ledger()
-    if mode == 1:  # RBD moves fewer off-rank rows than there are off-rank copies
+def test_c2_ep8_full(mode):
+    """C2: 8 expert-parallel workers x 16K tokens, plain and RBD."""
+    L, _ = _run("c2", 8, 16384, mode)
+    if mode == 1:
+        led = L.ledger()
         assert 0 < led["unique_rows_offrank"] < led["copies_offrank"]
 
 
-def test_config3_deepseek_v3_layer():
-    """Config 3: 256 routed experts top-8 + 1 shared, d_model 7168, d_ff 2048,
-    8K tokens on one GPU."""
-    _run(1, 8192, 256, 8, 7168, 2048, 1, 2048, n_sample=32)
+def test_c3_single_gpu():
+    """C3: 256 experts top-8 + 1 shared, d_model 7168, d_ff 2048, 8K tokens."""
+    _run("c3", 1, 8192, n_sample=32)
 
 
-def test_config3_expert_parallel():
-    """Config 3 shape, 8 expert-parallel workers (32 experts each), 1K tokens
-    per worker, RBD."""
-    _run(8, 1024, 256, 8, 7168, 2048, 1, 2048, mode=1, n_sample=32)
+def test_c3_ep8_full():
+    """C3 at its stated scale: 8 workers x 8K tokens (64K), 32 experts each, RBD."""
+    _run("c3", 8, 8192, mode=1, n_sample=32)
 
 
 @pytest.mark.parametrize("mode", [0, 1])
-def test_config5_zipf_skewed_routing(mode):
-    """Config 5: 128 experts top-8 with Zipf-imbalanced gate logits, 64K tokens
-    over 8 workers — empty and oversized expert groups."""
-    L, x, _ = _run(8, 8192, 128, 8, 1024, 512, 0, 0, mode=mode, zipf=1.2, n_sample=64)
-    led = L.ledger()
-    assert led["routed_copies"] == 8 * 8192 * 8
+def test_c5_zipf_full(mode):
+    """C5: 128 experts top-8, Zipf-skewed gate logits, 8 workers x 8K tokens,
+    d_model 2048, d_ff 1408: empty and oversized expert groups."""
+    L, tpe_all = _run("c5", 8, 8192, mode)
+    load = tpe_all.sum(0).double()
+    assert int((load == 0).sum()) >= 1, load
+    assert float(load.max()) >= 4 * float(load.mean()), (float(load.max()), float(load.mean()))
+    assert int(load.sum()) == 8 * 8192 * 8
 
 
-@pytest.mark.parametrize("G", [2, 4])
-def test_config4_ssmb_32k(G):
-    """Config 4: a 32K-token sequence split across G sequence shards, 160
-    experts top-6, d_model 5120, d_ff 1536 (ssmb.cpp:12-46); no drops, so
-    every row equals the unsharded layer's."""
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_c4_ssmb_full(G):
+    """C4: a 32K-token sequence over G shards, 160 experts top-6, 5120/1536;
+    replicated-expert SSMB (ssmb.cpp:12-46) and, at G=8, SSMB composed with
+    EP (20 experts per rank): bit-identical outputs, routing exact per shard."""
     from paper_2508_13337_b200 import capi
-    S, E, k, H, F = 32768, 160, 6, 5120, 1536
-    ctx = capi.Context(0, G, -1)
-    w1, w2, _, _ = _weights(E, H, F, 0, 0, 5)
-    gate = _grid_gate(H, E, 6)
-    x = _grid_tokens(S, H, 7)
-    L = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k,
-                   max_tokens=S // G, dtype=capi.BF16, gate=torch.from_numpy(gate).to(torch.bfloat16).cuda(),
-                   w1=w1, w2=w2, ssmb=True)
+    S = 32768
+    ctx, cfg, gate, w1, w2, _, _, x = _inputs("c4", G, S // G)
+    L = _layer(ctx, cfg, S // G, gate, w1, w2, None, None, ssmb=True)
     out = L.ssmb_forward(x)
     torch.cuda.synchronize()
-    rows = np.sort(np.random.default_rng(G).choice(S, 48, replace=False))
-    rows[0], rows[-1] = 0, S - 1  # first and last shard
-    want = _sampled_reference(x, gate, w1, w2, None, None, k, rows)
-    got = host(out[torch.from_numpy(rows).cuda()])
-    assert norm_rel(got, want) < 1e-2, norm_rel(got, want)
+    rows = np.sort(np.random.default_rng(G).choice(S, 40, replace=False))
+    rows[0], rows[-1] = 0, S - 1
+    want = _sampled_reference(x, gate, w1, w2, None, None, cfg["k"], rows)
+    assert norm_rel(host(out[torch.from_numpy(rows).cuda()]), want) < 1e-2
+    if G == 8:
+        ep = _layer(ctx, cfg, S // G, gate, w1, w2, None, None)  # experts partitioned over the 8 ranks
+        out_ep = ep.ssmb_forward(x)
+        torch.cuda.synchronize()
+        _check_routing_and_layout(ep, x, gate, G, S // G, cfg["E"], cfg["k"])
+        assert torch.equal(out_ep, out)
+        led = ep.ledger()
+        assert led["routed_copies"] == S * cfg["k"]
+    del capi

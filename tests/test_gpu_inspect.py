@@ -124,3 +124,33 @@ def test_bf16_layer_internals(ref, W, rbd, chunks):
     assert L.chunks() == chunks
     L.forward(dev(toks, torch.bfloat16))
     check_layer(ref, L, toks, gate, w1, w2, E, k, S * k, W, rbd=rbd, seed=3, chunked=chunks > 1)
+
+
+@pytest.mark.parametrize("W,E,k,S,rbd", [(1, 64, 6, 4096, False), (2, 32, 8, 1000, False), (4, 64, 6, 777, True),
+                                         (1, 256, 8, 300, False), (1, 16, 1, 129, False)])
+def test_fused_routing_matches_general_path(ref, W, E, k, S, rbd):
+    """The fused gate (softmax + top-k in the GEMM epilogue) and the one-launch
+    dropless placement (taken when cap >= S) against the general gate + PFT
+    path (cap = S - 1: the general kernels, no bucket reaches it here): every
+    routing array, the grouped layout and the output bit-identical, and the
+    routing equal to the reference's."""
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, W, -1)
+    rng = np.random.default_rng(E + k + S)
+    H, F = 128, 64
+    gate = np.round(rng.uniform(-0.1, 0.1, (H, E)) * 1024) / 1024
+    w1 = rng.uniform(-0.1, 0.1, (E, H, F))
+    w2 = rng.uniform(-0.1, 0.1, (E, F, H))
+    toks = np.round(rng.uniform(-1, 1, (W, S, H)) * 128) / 128
+    xd = dev(toks, torch.bfloat16)
+    fused = _layer(ctx, capi.BF16, E, H, F, k, S * k, S, gate, w1, w2, mode=int(rbd), seed=3)
+    general = _layer(ctx, capi.BF16, E, H, F, k, S - 1, S, gate, w1, w2, mode=int(rbd), seed=3)
+    a = fused.forward(xd).clone()
+    b = general.forward(xd).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    for w in range(W):
+        for what in ("top_experts", "weights", "token_ids", "expert_ids", "combine_weights", "tokens_per_expert",
+                     "slot_pos", "dest_row"):
+            assert torch.equal(fused.inspect(what, w), general.inspect(what, w)), (what, w)
+    check_layer(ref, fused, toks, gate, w1, w2, E, k, S * k, W, rbd=rbd, seed=3)
