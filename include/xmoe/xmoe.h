@@ -12,6 +12,9 @@
  *   - ids are int32; combine weights are float64 (the reference's `double`);
  *   - XMOE_F64 operands use the reference layouts and reproduce its
  *     arithmetic order bit for bit (parity mode);
+ *   - XMOE_F32 is the same instantiation in single precision (fp32 storage,
+ *     the reference's operation order with fp32 rounding; the fp32 bar is the
+ *     reference's own max_rel_diff <= 1e-5, verify.cpp:117);
  *   - XMOE_BF16 operands are the performance path: bf16 storage, fp32
  *     accumulation on tcgen05 tensor cores, weights in the K-major B200
  *     layout documented per call;

@@ -172,6 +172,8 @@ def _dtype_code(t: torch.Tensor) -> int:
         return F64
     if t.dtype == torch.bfloat16:
         return BF16
+    if t.dtype == torch.float32:
+        return F32
     raise XmoeError(2, f"unsupported dtype {t.dtype}")
 
 
@@ -243,7 +245,7 @@ class Context:
     # ------------------------------------------------------------ operators
     def gate_forward(self, x, wg, k, renorm=False, want_logits=False):
         S, H = x.shape
-        E = wg.shape[1] if x.dtype == torch.float64 else wg.shape[0]
+        E = wg.shape[0] if x.dtype == torch.bfloat16 else wg.shape[1]
         top = torch.empty((S, k), dtype=torch.int32, device=x.device)
         w = torch.empty((S, k), dtype=torch.float64, device=x.device)
         lg = torch.empty((S, E), dtype=torch.float64, device=x.device) if want_logits else None
@@ -286,7 +288,7 @@ class Context:
         """F64: w1 [G,H,F], w2 [G,F,H]; BF16: w1 [G,F,H], w2 [G,H,F] (K-major)."""
         rows, H = inp.shape
         G = rows_per_expert.shape[0]
-        F = w1.shape[2] if inp.dtype == torch.float64 else w1.shape[1]
+        F = w1.shape[1] if inp.dtype == torch.bfloat16 else w1.shape[2]
         out = torch.empty_like(inp)
         _check(lib().xmoe_grouped_mlp(self.h, _dtype_code(inp), _ptr(inp), rows,
                                       _ptr(rows_per_expert), G, _ptr(w1), _ptr(w2), H, F,

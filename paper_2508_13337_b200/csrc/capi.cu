@@ -38,6 +38,7 @@ std::atomic<unsigned long long> g_kernel_launches{0};
 
 static size_t elem_size(int dtype) {
     if (dtype == XMOE_F64) return 8;
+    if (dtype == XMOE_F32) return 4;
     if (dtype == XMOE_BF16) return 2;
     fail(XMOE_ERR_VALIDATION, "unknown dtype");
 }
@@ -131,6 +132,11 @@ int xmoe_gate_forward(xmoe_ctx* ctx, int dtype, const void* x, const void* wg, i
             launch_gate_logits_f64(static_cast<const double*>(x), static_cast<const double*>(wg),
                                    S, H, E, lg, st);
             launch_softmax_topk(lg, S, E, k, renorm, top, weights, st);
+        } else if (dtype == XMOE_F32) {  // single-precision instantiation of the reference order
+            float* lg = reinterpret_cast<float*>(ws);
+            launch_gate_logits_f32(static_cast<const float*>(x), static_cast<const float*>(wg), S, H, E, lg, st);
+            launch_softmax_topk_f32(lg, S, E, k, renorm, top, weights, st);
+            if (logits) launch_f32_to_f64(lg, static_cast<long long>(S) * E, logits, st);
         } else if (dtype == XMOE_BF16) {
             require(E % 16 == 0 && H % 8 == 0, XMOE_ERR_VALIDATION,
                     "bf16 gate requires num_experts % 16 == 0 and model_dim % 8 == 0");
@@ -235,6 +241,11 @@ int xmoe_grouped_mlp(xmoe_ctx* ctx, int dtype, const void* in, int64_t rows,
                                     static_cast<const double*>(w1), F, static_cast<double*>(mid), 1, st);
             launch_grouped_gemm_f64(static_cast<const double*>(mid), rows, F, rows_per_expert, G,
                                     static_cast<const double*>(w2), H, static_cast<double*>(out), 0, st);
+        } else if (dtype == XMOE_F32) {
+            launch_grouped_gemm_f32(static_cast<const float*>(in), rows, H, rows_per_expert, G,
+                                    static_cast<const float*>(w1), F, static_cast<float*>(mid), 1, st);
+            launch_grouped_gemm_f32(static_cast<const float*>(mid), rows, F, rows_per_expert, G,
+                                    static_cast<const float*>(w2), H, static_cast<float*>(out), 0, st);
         } else {
             launch_grouped_gemm_bf16(in, rows, H, rows_per_expert, G, w1, F, mid, 1, st);
             launch_grouped_gemm_bf16(mid, rows, F, rows_per_expert, G, w2, H, out, 0, st);

@@ -43,20 +43,25 @@ struct CopyList {
     }
 };
 
-__global__ void __launch_bounds__(32 * kCombWarps) combine_f64_kernel(
-    const double* __restrict__ rows, int H, CopyList cl, const double* __restrict__ w, int S,
-    const double* __restrict__ addend, double* __restrict__ out) {
+template <typename T>
+__global__ void __launch_bounds__(32 * kCombWarps) combine_simt_kernel(
+    const T* __restrict__ rows, int H, CopyList cl, const double* __restrict__ w, int S,
+    const T* __restrict__ addend, T* __restrict__ out) {
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (t >= S) return;
     const int n = cl.count(t);
     for (int h = lane; h < H; h += 32) {
-        double acc = 0.0;
+        T acc = 0;
         for (int j = 0; j < n; ++j) {
             const int c = cl.at(t, j);
-            acc = __dadd_rn(acc, __dmul_rn(w[c], cl.row(rows, c, H)[h]));
+            if constexpr (sizeof(T) == 8) acc = __dadd_rn(acc, __dmul_rn(w[c], cl.row(rows, c, H)[h]));
+            else acc = __fadd_rn(acc, __fmul_rn(static_cast<float>(w[c]), cl.row(rows, c, H)[h]));
         }
-        if (addend) acc = __dadd_rn(acc, addend[static_cast<size_t>(t) * H + h]);
+        if (addend) {
+            if constexpr (sizeof(T) == 8) acc = __dadd_rn(acc, addend[static_cast<size_t>(t) * H + h]);
+            else acc = __fadd_rn(acc, addend[static_cast<size_t>(t) * H + h]);
+        }
         out[static_cast<size_t>(t) * H + h] = acc;
     }
 }
@@ -292,9 +297,13 @@ void launch_combine(int dtype, const void* rows, int H, const int32_t* ptr, cons
     CopyList cl{ptr, idx, k, tab, drank, drow};
     const int blocks = ceil_div(S, kCombWarps);
     if (dtype == XMOE_F64) {
-        combine_f64_kernel<<<blocks, 32 * kCombWarps, 0, st>>>(
+        combine_simt_kernel<double><<<blocks, 32 * kCombWarps, 0, st>>>(
             static_cast<const double*>(rows), H, cl, w, S, static_cast<const double*>(addend),
             static_cast<double*>(out));
+    } else if (dtype == XMOE_F32) {
+        combine_simt_kernel<float><<<blocks, 32 * kCombWarps, 0, st>>>(
+            static_cast<const float*>(rows), H, cl, w, S, static_cast<const float*>(addend),
+            static_cast<float*>(out));
     } else {
         require(H % 8 == 0, XMOE_ERR_VALIDATION, "bf16 path requires model_dim % 8 == 0");
         const long long warps = static_cast<long long>(S) * ((H + kSegCols - 1) / kSegCols);

@@ -179,6 +179,14 @@ __global__ void __launch_bounds__(32 * kEpWarps) rbd_merge_flat_kernel(
                     acc = __dadd_rn(acc, __dmul_rn(ent_w[e], y));
                 }
                 merged[static_cast<size_t>(p) * H + h] = acc;
+            } else if constexpr (sizeof(T) == 4) {
+                float acc = y0[h];
+                if (multi) acc = __fmul_rn(acc, static_cast<float>(land_w[p]));
+                for (int e = e0; e < e1; ++e) {
+                    const float y = reinterpret_cast<const float*>(eout_tab[ent_owner[e]])[static_cast<size_t>(ent_pos[e]) * H + h];
+                    acc = __fadd_rn(acc, __fmul_rn(static_cast<float>(ent_w[e]), y));
+                }
+                merged[static_cast<size_t>(p) * H + h] = acc;
             } else {
                 float acc = __bfloat162float(y0[h]);
                 if (multi) acc *= static_cast<float>(land_w[p]);
@@ -234,6 +242,7 @@ struct Carve {
 
 size_t elem_bytes(int dtype) {
     if (dtype == XMOE_F64) return 8;
+    if (dtype == XMOE_F32) return 4;
     if (dtype == XMOE_BF16) return 2;
     fail(XMOE_ERR_VALIDATION, "unknown dtype");
 }
@@ -509,6 +518,10 @@ int xmoe_rbd_combine(xmoe_ctx* ctx, int dtype, int64_t H, const void* const* exp
                 rbd_merge_flat_kernel<double><<<blocks, 32 * kEpWarps, 0, st>>>(
                     tab, static_cast<int>(H), static_cast<int>(P), land_of, land_pos, land_multi, land_w, ent_ptr,
                     ent_owner, ent_pos, ent_w, static_cast<double*>(merged));
+            else if (dtype == XMOE_F32)
+                rbd_merge_flat_kernel<float><<<blocks, 32 * kEpWarps, 0, st>>>(
+                    tab, static_cast<int>(H), static_cast<int>(P), land_of, land_pos, land_multi, land_w, ent_ptr,
+                    ent_owner, ent_pos, ent_w, static_cast<float*>(merged));
             else
                 rbd_merge_flat_kernel<__nv_bfloat16><<<blocks, 32 * kEpWarps, 0, st>>>(
                     tab, static_cast<int>(H), static_cast<int>(P), land_of, land_pos, land_multi, land_w, ent_ptr,

@@ -12,18 +12,24 @@
 
 namespace xmoe {
 
-// ---------------------------------------------------------------- F64 logits
+// ---------------------------------------------------------------- F64 / F32 logits
 // One thread per (token, expert); the warp spans experts so Wg rows are
-// coalesced and the token value is a broadcast.
-__global__ void gate_logits_f64_kernel(const double* __restrict__ x,
-                                       const double* __restrict__ wg, int S, int H, int E,
-                                       double* __restrict__ logits) {
+// coalesced and the token value is a broadcast.  Ascending h, separately
+// rounded multiply and add (kernels_scalar.cpp:11-23, -ffp-contract=off):
+// bit-exact to the reference in F64, the same order in single precision
+// for the F32 instantiation.
+template <typename T>
+__global__ void gate_logits_kernel(const T* __restrict__ x, const T* __restrict__ wg, int S, int H, int E,
+                                   T* __restrict__ logits) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     const int t = blockIdx.y;
     if (e >= E || t >= S) return;
-    const double* xr = x + static_cast<size_t>(t) * H;
-    double acc = 0.0;
-    for (int h = 0; h < H; ++h) acc = __dadd_rn(acc, __dmul_rn(xr[h], wg[static_cast<size_t>(h) * E + e]));
+    const T* xr = x + static_cast<size_t>(t) * H;
+    T acc = 0;
+    for (int h = 0; h < H; ++h) {
+        if constexpr (sizeof(T) == 8) acc = __dadd_rn(acc, __dmul_rn(xr[h], wg[static_cast<size_t>(h) * E + e]));
+        else acc = __fadd_rn(acc, __fmul_rn(xr[h], wg[static_cast<size_t>(h) * E + e]));
+    }
     logits[static_cast<size_t>(t) * E + e] = acc;
 }
 
@@ -59,22 +65,14 @@ __global__ void __launch_bounds__(256) softmax_topk_kernel(const LT* __restrict_
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
 #pragma unroll
     for (int i = 0; i < PER; ++i) p[i] = (lane + 32 * i < E) ? exp(__dsub_rn(p[i], mx)) : 0.0;
+    // sequential ascending-e sum, exactly as the reference accumulates
+    // (gating.cpp:42) — also for fp32 logits, so the BF16 weights equal the
+    // fused gate's (gemm_tc.cu gate_route_kernel) bit for bit
     double sum = 0.0;
-    if constexpr (sizeof(LT) == 8) {
-        // F64 parity: sequential ascending-e sum, exactly as the reference
-        // accumulates (gating.cpp:42)
 #pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const int lim = min(32, E - 32 * i);
-            for (int l = 0; l < lim; ++l) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, p[i], l));
-        }
-    } else {
-        // BF16 path: tree sum (weights within a few fp64 ulp of the reference;
-        // the top-k order depends on the logits alone, so routing is unchanged)
-#pragma unroll
-        for (int i = 0; i < PER; ++i) sum += p[i];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    for (int i = 0; i < PER; ++i) {
+        const int lim = min(32, E - 32 * i);
+        for (int l = 0; l < lim; ++l) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, p[i], l));
     }
 #pragma unroll
     for (int i = 0; i < PER; ++i) p[i] = (lane + 32 * i < E) ? __ddiv_rn(p[i], sum) : -1.0;
@@ -121,7 +119,14 @@ void launch_gate_logits_f64(const double* x, const double* wg, int S, int H, int
                             double* logits, cudaStream_t st) {
     if (S == 0) return;
     dim3 grid(ceil_div(E, 128), S);
-    gate_logits_f64_kernel<<<grid, 128, 0, st>>>(x, wg, S, H, E, logits);
+    gate_logits_kernel<double><<<grid, 128, 0, st>>>(x, wg, S, H, E, logits);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_gate_logits_f32(const float* x, const float* wg, int S, int H, int E, float* logits, cudaStream_t st) {
+    if (S == 0) return;
+    dim3 grid(ceil_div(E, 128), S);
+    gate_logits_kernel<float><<<grid, 128, 0, st>>>(x, wg, S, H, E, logits);
     XMOE_LAUNCH_CHECK();
 }
 

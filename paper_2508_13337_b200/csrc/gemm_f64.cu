@@ -1,4 +1,4 @@
-// FP64 parity instantiation of the grouped expert FFN — reproduces
+// FP64 parity (and F32) instantiations of the grouped expert FFN — reproduces
 // moesim::grouped_expert_mlp (/root/reference/proj/src/pf_pipeline.cpp:83-105)
 // bit for bit: each output is sum_p a[i,p]*b[p,j] accumulated in ascending p
 // with separately rounded multiply and add (kernels_scalar.cpp:11-23,
@@ -12,10 +12,9 @@
 
 namespace xmoe {
 
-__global__ void grouped_gemm_f64_kernel(const double* __restrict__ A, int K,
-                                        const int32_t* __restrict__ rows_per_group, int G,
-                                        const double* __restrict__ B, int N,
-                                        double* __restrict__ D, int relu) {
+template <typename T>
+__global__ void grouped_gemm_simt_kernel(const T* __restrict__ A, int K, const int32_t* __restrict__ rows_per_group,
+                                         int G, const T* __restrict__ B, int N, T* __restrict__ D, int relu) {
     extern __shared__ int32_t pre[];  // [G+1] row prefix
     if (threadIdx.x == 0) {
         int a = 0;
@@ -35,11 +34,14 @@ __global__ void grouped_gemm_f64_kernel(const double* __restrict__ A, int K,
         if (pre[mid] <= row) lo = mid;
         else hi = mid - 1;
     }
-    const double* a = A + static_cast<size_t>(row) * K;
-    const double* b = B + static_cast<size_t>(lo) * K * N + col;
-    double acc = 0.0;
-    for (int p = 0; p < K; ++p) acc = __dadd_rn(acc, __dmul_rn(a[p], b[static_cast<size_t>(p) * N]));
-    if (relu) acc = acc > 0.0 ? acc : 0.0;
+    const T* a = A + static_cast<size_t>(row) * K;
+    const T* b = B + static_cast<size_t>(lo) * K * N + col;
+    T acc = 0;
+    for (int p = 0; p < K; ++p) {
+        if constexpr (sizeof(T) == 8) acc = __dadd_rn(acc, __dmul_rn(a[p], b[static_cast<size_t>(p) * N]));
+        else acc = __fadd_rn(acc, __fmul_rn(a[p], b[static_cast<size_t>(p) * N]));
+    }
+    if (relu) acc = acc > T(0) ? acc : T(0);
     D[static_cast<size_t>(row) * N + col] = acc;
 }
 
@@ -49,8 +51,20 @@ void launch_grouped_gemm_f64(const double* A, long long rows_bound, int K,
     if (rows_bound == 0 || N == 0) return;
     require(rows_bound < (1ll << 31), XMOE_ERR_VALIDATION, "too many rows");
     dim3 grid(static_cast<unsigned>(rows_bound), ceil_div(N, 128));
-    grouped_gemm_f64_kernel<<<grid, 128, sizeof(int32_t) * (G + 1), st>>>(A, K, rows_per_group,
-                                                                         G, B, N, D, relu);
+    grouped_gemm_simt_kernel<double><<<grid, 128, sizeof(int32_t) * (G + 1), st>>>(A, K, rows_per_group, G, B, N,
+                                                                                  D, relu);
+    XMOE_LAUNCH_CHECK();
+}
+
+// F32 instantiation: the reference's order (ascending p, separate multiply
+// and add) in single precision.
+void launch_grouped_gemm_f32(const float* A, long long rows_bound, int K, const int32_t* rows_per_group, int G,
+                             const float* B, int N, float* D, int relu, cudaStream_t st) {
+    if (rows_bound == 0 || N == 0) return;
+    require(rows_bound < (1ll << 31), XMOE_ERR_VALIDATION, "too many rows");
+    dim3 grid(static_cast<unsigned>(rows_bound), ceil_div(N, 128));
+    grouped_gemm_simt_kernel<float><<<grid, 128, sizeof(int32_t) * (G + 1), st>>>(A, K, rows_per_group, G, B, N, D,
+                                                                                 relu);
     XMOE_LAUNCH_CHECK();
 }
 

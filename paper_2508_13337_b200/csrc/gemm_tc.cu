@@ -553,8 +553,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mx = fmaxf(mx, nv);
                     int ni = e;
 #pragma unroll
-                    for (int j = 0; j < KMAX; ++j) {  // bubble insert: strict '>' keeps the lower id on ties
-                        if (j < k && nv > tv[j]) {
+                    for (int j = 0; j < KMAX; ++j) {  // bubble insert by (logit desc, id asc): an
+                        // element pushed down must still pass equal logits of higher ids
+                        if (j < k && (nv > tv[j] || (nv == tv[j] && ni < ti[j]))) {
                             const float fv = tv[j];
                             const int fi = ti[j];
                             tv[j] = nv;

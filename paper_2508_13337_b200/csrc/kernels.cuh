@@ -11,6 +11,7 @@ namespace xmoe {
 // gate.cu
 void launch_gate_logits_f64(const double* x, const double* wg, int S, int H, int E,
                             double* logits, cudaStream_t st);
+void launch_gate_logits_f32(const float* x, const float* wg, int S, int H, int E, float* logits, cudaStream_t st);
 void launch_softmax_topk(const double* logits, int S, int E, int k, int renorm, int32_t* top,
                          double* weights, cudaStream_t st);
 void launch_softmax_topk_f32(const float* logits, int S, int E, int k, int renorm, int32_t* top,
@@ -59,6 +60,9 @@ void launch_combine(int dtype, const void* rows, int H, const int32_t* ptr, cons
 void launch_grouped_gemm_f64(const double* A, long long rows_bound, int K,
                              const int32_t* rows_per_group, int G, const double* B, int N,
                              double* D, int relu, cudaStream_t st);
+
+void launch_grouped_gemm_f32(const float* A, long long rows_bound, int K, const int32_t* rows_per_group, int G,
+                             const float* B, int N, float* D, int relu, cudaStream_t st);
 
 // gemm_tc.cu
 // mbits_out (ReLU GEMMs, training layers): bit i of word [row][c/32] = (y[row][c] != 0)

@@ -53,7 +53,7 @@ static int wgrad_splits(long long M, long long N, long long rows) {
     return s;
 }
 
-static size_t elem_size_of(int dtype) { return dtype == XMOE_F64 ? 8 : 2; }
+static size_t elem_size_of(int dtype) { return dtype == XMOE_F64 ? 8 : dtype == XMOE_F32 ? 4 : 2; }
 
 Layer::~Layer() {
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
@@ -183,7 +183,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     require(d.dispatch_mode == XMOE_DISPATCH_NAIVE || d.dispatch_mode == XMOE_DISPATCH_RBD,
             XMOE_ERR_VALIDATION, "unknown dispatch mode");
     const bool bf = d.dtype == XMOE_BF16;
-    require(bf || d.dtype == XMOE_F64, XMOE_ERR_VALIDATION, "unknown dtype");
+    require(bf || d.dtype == XMOE_F64 || d.dtype == XMOE_F32, XMOE_ERR_VALIDATION, "unknown dtype");
     if (bf) {
         require(d.num_experts % 16 == 0, XMOE_ERR_VALIDATION,
                 "bf16 path requires num_experts to be a multiple of 16");
@@ -560,6 +560,9 @@ static void run_gemm(int dtype, const void* A, long long rows_bound, int K, cons
     if (dtype == XMOE_F64)
         launch_grouped_gemm_f64(static_cast<const double*>(A), rows_bound, K, rpg, G,
                                 static_cast<const double*>(B), N, static_cast<double*>(D), relu, st);
+    else if (dtype == XMOE_F32)
+        launch_grouped_gemm_f32(static_cast<const float*>(A), rows_bound, K, rpg, G, static_cast<const float*>(B), N,
+                                static_cast<float*>(D), relu, st);
     else
         launch_grouped_gemm_bf16(A, rows_bound, K, rpg, G, B, N, D, relu, st, mbits_out);
 }
@@ -862,6 +865,11 @@ void layer_forward_v(Layer& L, const void* x, const long long* Sw, void* out, cu
             launch_gate_logits_f64(reinterpret_cast<const double*>(x_of(i)), static_cast<const double*>(L.gate),
                                    S, H, E, w.logits, st);
             launch_softmax_topk(w.logits, S, E, k, L.d.renorm, w.top, w.wts, st);
+        } else if (dt == XMOE_F32) {
+            float* lg = reinterpret_cast<float*>(w.logits);
+            launch_gate_logits_f32(reinterpret_cast<const float*>(x_of(i)), static_cast<const float*>(L.gate), S, H, E,
+                                   lg, st);
+            launch_softmax_topk_f32(lg, S, E, k, L.d.renorm, w.top, w.wts, st);
         } else {
             route_gate(L, w, x_of(i), S, st);
         }
@@ -1041,7 +1049,7 @@ void Layer::exchange_nccl(bool forward, cudaStream_t st) {
     const int me = w.rank;
     const size_t rb = static_cast<size_t>(H) * es;
     auto comm = static_cast<ncclComm_t>(ctx->nccl);
-    const ncclDataType_t ty = d.dtype == XMOE_F64 ? ncclFloat64 : ncclBfloat16;
+    const ncclDataType_t ty = d.dtype == XMOE_F64 ? ncclFloat64 : d.dtype == XMOE_F32 ? ncclFloat32 : ncclBfloat16;
     std::vector<int64_t> send_off(E + 1), recv_off(static_cast<size_t>(W) * El);
     if (xmoe_plan_dispatch(W, E, h_tpe.data(), me, send_off.data(), recv_off.data(), nullptr) != XMOE_OK)
         fail(XMOE_ERR_VALIDATION, "num_experts must be divisible by the worker-group size");

@@ -707,6 +707,14 @@ __global__ void __launch_bounds__(256) rbd_merge_kernel(const char* const* __res
                     acc = __dadd_rn(acc, __dmul_rn(md.w, static_cast<double>(row_of(md)[h])));
                 }
                 out[h] = static_cast<T>(acc);
+            } else if constexpr (sizeof(T) == 4) {  // F32: the reference's scale / axpy order in single precision
+                float acc = __fmul_rn(static_cast<float>(row_of(pd)[h]), static_cast<float>(pd.w));
+                for (int m = 0; m < n; ++m) {
+                    if (m == pm) continue;
+                    const RbdDesc md = desc[c0 + m];
+                    acc = __fadd_rn(acc, __fmul_rn(static_cast<float>(md.w), static_cast<float>(row_of(md)[h])));
+                }
+                out[h] = static_cast<T>(acc);
             } else {
                 float acc = __bfloat162float(row_of(pd)[h]) * static_cast<float>(pd.w);
                 for (int m = 0; m < n; ++m) {
@@ -763,6 +771,15 @@ __global__ void __launch_bounds__(256) rbd_combine_kernel(const char* const* __r
                 acc = __dadd_rn(acc, __dmul_rn(sc, static_cast<double>(rowp[i][h])));
             }
             if (addend) acc = __dadd_rn(acc, static_cast<double>(addend[static_cast<size_t>(t) * H + h]));
+            out[static_cast<size_t>(t) * H + h] = static_cast<T>(acc);
+        } else if constexpr (sizeof(T) == 4) {
+            float acc = 0.f;
+            for (int i = 0; i < nn; ++i) {
+                const int gid = b + order[i];
+                const float sc = g.n[gid] > 1 ? 1.f : static_cast<float>(cw[g.pilot[gid]]);
+                acc = __fadd_rn(acc, __fmul_rn(sc, static_cast<float>(rowp[i][h])));
+            }
+            if (addend) acc = __fadd_rn(acc, static_cast<float>(addend[static_cast<size_t>(t) * H + h]));
             out[static_cast<size_t>(t) * H + h] = static_cast<T>(acc);
         } else {
             float acc = 0.f;
@@ -1012,6 +1029,9 @@ void launch_rbd_merge(int dtype, const char* const* eout_tab, int H, const RbdDe
     if (dtype == XMOE_F64)
         rbd_merge_kernel<double><<<cap(warp_grid(per)), 256, 0, st>>>(eout_tab, H, desc, gstart, wk.rx, wk.C, c,
                                                                      static_cast<double*>(back_u));
+    else if (dtype == XMOE_F32)
+        rbd_merge_kernel<float><<<cap(warp_grid(per)), 256, 0, st>>>(eout_tab, H, desc, gstart, wk.rx, wk.C, c,
+                                                                    static_cast<float*>(back_u));
     else if (H % 8 == 0)
         rbd_merge_bf16_kernel<<<cap(warp_grid(per * ((H + 511) / 512))), 256, 0, st>>>(
             eout_tab, H, desc, gstart, wk.rx, wk.C, c, static_cast<__nv_bfloat16*>(back_u));
@@ -1029,6 +1049,10 @@ void launch_rbd_combine(int dtype, const char* const* back_tab, int H, int S, co
         rbd_combine_kernel<double><<<ceil_div(nt, 8), 256, 0, st>>>(
             back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru, wk.gpos, wk.C, c, wk.dptr, cw,
             static_cast<const double*>(addend), static_cast<double*>(out));
+    else if (dtype == XMOE_F32)
+        rbd_combine_kernel<float><<<ceil_div(nt, 8), 256, 0, st>>>(
+            back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru, wk.gpos, wk.C, c, wk.dptr, cw,
+            static_cast<const float*>(addend), static_cast<float*>(out));
     else if (H % 8 == 0)
         rbd_combine_bf16_kernel<<<ceil_div(static_cast<long long>(nt) * ((H + 511) / 512), 8), 256, 0, st>>>(
             back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru, wk.gpos, wk.C, c, wk.dptr, cw,
