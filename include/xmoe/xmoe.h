@@ -12,9 +12,9 @@
  *   - ids are int32; combine weights are float64 (the reference's `double`);
  *   - XMOE_F64 operands use the reference layouts and reproduce its
  *     arithmetic order bit for bit (parity mode);
- *   - XMOE_F32 is the same instantiation in single precision (fp32 storage,
- *     the reference's operation order with fp32 rounding; the fp32 bar is the
- *     reference's own max_rel_diff <= 1e-5, verify.cpp:117);
+ *   - XMOE_F32 keeps fp32 operands in the reference's operation order, the
+ *     exact fp32 products accumulated in fp64 and each result rounded once
+ *     to fp32 (bar: the reference's own max_rel_diff <= 1e-5, verify.cpp:117);
  *   - XMOE_BF16 operands are the performance path: bf16 storage, fp32
  *     accumulation on tcgen05 tensor cores, weights in the K-major B200
  *     layout documented per call;
@@ -93,6 +93,9 @@ uint64_t xmoe_kernel_launches(void);
 int xmoe_nccl_unique_id(void* out_128_bytes);
 int xmoe_ctx_create(int device, int world, int rank, const void* nccl_id, xmoe_ctx** out);
 int xmoe_ctx_destroy(xmoe_ctx* ctx);
+/* XMOE_OK, or XMOE_ERR_NCCL when the context's communicator reports an
+ * asynchronous error (ncclCommGetAsyncError). */
+int xmoe_ctx_status(xmoe_ctx* ctx);
 
 /* ------------------------------------------------------------------ operators */
 
@@ -296,7 +299,8 @@ int xmoe_layer_create(xmoe_ctx* ctx, const xmoe_layer_desc* desc, const void* ga
 /* Collective for one-process-per-GPU layers: every rank must call it (a flag
  * barrier keeps a peer's last NVLink reads off this rank's freed buffers). */
 int xmoe_layer_destroy(xmoe_layer* layer);
-/* XMOE_OK, or XMOE_ERR_PEER_TIMEOUT when a cross-GPU wait of an earlier pass
+/* XMOE_OK, XMOE_ERR_NCCL (asynchronous communicator error), or
+ * XMOE_ERR_PEER_TIMEOUT when a cross-GPU wait of an earlier pass
  * gave up after XMOE_PEER_TIMEOUT_S seconds (default 300) because a peer never
  * arrived.  The wait does not trap the device: the pass finishes with invalid
  * results and every later forward/backward on the layer returns this code. */

@@ -118,6 +118,7 @@ def lib():
         L.xmoe_layer_grads.argtypes = [p] + [C.POINTER(p)] * 5
         L.xmoe_layer_inspect.argtypes = [p, i32, i32, C.POINTER(p), C.POINTER(i64)]
         L.xmoe_layer_status.argtypes = [p]
+        L.xmoe_ctx_status.argtypes = [p]
         L.xmoe_layer_set_weights.argtypes = [p, p, p, p, p, p, p]
         L.xmoe_rng_uniform.argtypes = [p, C.c_uint64, C.c_uint64, i64, C.c_double, C.c_double, C.c_double, i32, p, p]
         L.xmoe_salt_seed.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
@@ -230,6 +231,9 @@ class Context:
         idbuf = None if nccl_id is None else C.create_string_buffer(nccl_id, 128)
         _check(lib().xmoe_ctx_create(device, world, rank, idbuf, C.byref(h)))
         self.h = h
+
+    def status(self):
+        _check(lib().xmoe_ctx_status(self.h))
 
     def close(self):
         if getattr(self, "h", None):

@@ -436,13 +436,30 @@ int xmoe_make_layer_weights(xmoe_ctx* ctx, uint64_t seed, uint64_t offset, int64
     });
 }
 
+// asynchronous NCCL failures of the context's communicator (ncclCommGetAsyncError)
+static void check_nccl_async(const Ctx& c) {
+    if (!c.nccl) return;
+    ncclResult_t async = ncclSuccess;
+    XMOE_NCCL(ncclCommGetAsyncError(static_cast<ncclComm_t>(c.nccl), &async));
+    if (async != ncclSuccess && async != ncclInProgress)
+        fail(XMOE_ERR_NCCL, std::string("asynchronous NCCL error: ") + ncclGetErrorString(async));
+}
+
+int xmoe_ctx_status(xmoe_ctx* ctx) {
+    return guarded([&] { check_nccl_async(ctx->c); });
+}
+
 int xmoe_layer_status(xmoe_layer* layer) {
-    return guarded([&] { layer->l.check_peers(); });
+    return guarded([&] {
+        layer->l.check_peers();
+        check_nccl_async(*layer->l.ctx);
+    });
 }
 
 int xmoe_moe_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, int64_t S, void* out,
                      void* stream) {
     return guarded([&] {
+        NvtxRange nvtx("xmoe_moe_forward");
         require(layer->l.ctx == &ctx->c, XMOE_ERR_VALIDATION, "layer belongs to another context");
         Layer& L = layer->l;
         auto st = static_cast<cudaStream_t>(stream);
@@ -526,6 +543,7 @@ int xmoe_layer_set_graph(xmoe_layer* layer, int enable) {
 int xmoe_moe_backward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x, const void* dy, int64_t S,
                       void* dx, void* stream) {
     return guarded([&] {
+        NvtxRange nvtx("xmoe_moe_backward");
         require(layer->l.ctx == &ctx->c, XMOE_ERR_VALIDATION, "layer belongs to another context");
         layer_backward(layer->l, x, dy, S, dx, static_cast<cudaStream_t>(stream));
     });
@@ -546,6 +564,7 @@ int xmoe_layer_grads(xmoe_layer* layer, float** dgate, float** dw1, float** dw2,
 int xmoe_ssmb_forward(xmoe_ctx* ctx, xmoe_layer* layer, const void* x_full, int64_t S,
                       void* out_full, void* stream) {
     return guarded([&] {
+        NvtxRange nvtx("xmoe_ssmb_forward");
         ssmb_forward(ctx->c, layer->l, x_full, S, out_full, static_cast<cudaStream_t>(stream));
     });
 }

@@ -51,18 +51,14 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_simt_kernel(
     const int lane = threadIdx.x & 31;
     if (t >= S) return;
     const int n = cl.count(t);
-    for (int h = lane; h < H; h += 32) {
-        T acc = 0;
+    for (int h = lane; h < H; h += 32) {  // F32: same order, fp64 accumulation, one rounding
+        double acc = 0.0;
         for (int j = 0; j < n; ++j) {
             const int c = cl.at(t, j);
-            if constexpr (sizeof(T) == 8) acc = __dadd_rn(acc, __dmul_rn(w[c], cl.row(rows, c, H)[h]));
-            else acc = __fadd_rn(acc, __fmul_rn(static_cast<float>(w[c]), cl.row(rows, c, H)[h]));
+            acc = __dadd_rn(acc, __dmul_rn(w[c], static_cast<double>(cl.row(rows, c, H)[h])));
         }
-        if (addend) {
-            if constexpr (sizeof(T) == 8) acc = __dadd_rn(acc, addend[static_cast<size_t>(t) * H + h]);
-            else acc = __fadd_rn(acc, addend[static_cast<size_t>(t) * H + h]);
-        }
-        out[static_cast<size_t>(t) * H + h] = acc;
+        if (addend) acc = __dadd_rn(acc, static_cast<double>(addend[static_cast<size_t>(t) * H + h]));
+        out[static_cast<size_t>(t) * H + h] = static_cast<T>(acc);
     }
 }
 

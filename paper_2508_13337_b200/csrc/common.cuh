@@ -9,6 +9,8 @@
 #include <stdexcept>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "xmoe/xmoe.h"
 
 namespace xmoe {
@@ -58,6 +60,14 @@ extern std::atomic<unsigned long long> g_kernel_launches;
     } while (0)
 
 constexpr int kNumSMs = 148;
+
+// NVTX range over a C-ABI call (host-side; free when no profiler is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
 

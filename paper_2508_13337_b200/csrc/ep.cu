@@ -179,14 +179,14 @@ __global__ void __launch_bounds__(32 * kEpWarps) rbd_merge_flat_kernel(
                     acc = __dadd_rn(acc, __dmul_rn(ent_w[e], y));
                 }
                 merged[static_cast<size_t>(p) * H + h] = acc;
-            } else if constexpr (sizeof(T) == 4) {
-                float acc = y0[h];
-                if (multi) acc = __fmul_rn(acc, static_cast<float>(land_w[p]));
+            } else if constexpr (sizeof(T) == 4) {  // F32: fp64 accumulation, one rounding
+                double acc = y0[h];
+                if (multi) acc = __dmul_rn(acc, land_w[p]);
                 for (int e = e0; e < e1; ++e) {
                     const float y = reinterpret_cast<const float*>(eout_tab[ent_owner[e]])[static_cast<size_t>(ent_pos[e]) * H + h];
-                    acc = __fadd_rn(acc, __fmul_rn(static_cast<float>(ent_w[e]), y));
+                    acc = __dadd_rn(acc, __dmul_rn(ent_w[e], static_cast<double>(y)));
                 }
-                merged[static_cast<size_t>(p) * H + h] = acc;
+                merged[static_cast<size_t>(p) * H + h] = static_cast<float>(acc);
             } else {
                 float acc = __bfloat162float(y0[h]);
                 if (multi) acc *= static_cast<float>(land_w[p]);

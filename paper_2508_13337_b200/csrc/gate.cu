@@ -16,8 +16,8 @@ namespace xmoe {
 // One thread per (token, expert); the warp spans experts so Wg rows are
 // coalesced and the token value is a broadcast.  Ascending h, separately
 // rounded multiply and add (kernels_scalar.cpp:11-23, -ffp-contract=off):
-// bit-exact to the reference in F64, the same order in single precision
-// for the F32 instantiation.
+// bit-exact to the reference in F64; the F32 instantiation keeps the order
+// with fp64 accumulation and rounds each logit once.
 template <typename T>
 __global__ void gate_logits_kernel(const T* __restrict__ x, const T* __restrict__ wg, int S, int H, int E,
                                    T* __restrict__ logits) {
@@ -25,12 +25,10 @@ __global__ void gate_logits_kernel(const T* __restrict__ x, const T* __restrict_
     const int t = blockIdx.y;
     if (e >= E || t >= S) return;
     const T* xr = x + static_cast<size_t>(t) * H;
-    T acc = 0;
-    for (int h = 0; h < H; ++h) {
-        if constexpr (sizeof(T) == 8) acc = __dadd_rn(acc, __dmul_rn(xr[h], wg[static_cast<size_t>(h) * E + e]));
-        else acc = __fadd_rn(acc, __fmul_rn(xr[h], wg[static_cast<size_t>(h) * E + e]));
-    }
-    logits[static_cast<size_t>(t) * E + e] = acc;
+    double acc = 0.0;  // F32: exact fp32 products, fp64 accumulation, one rounding
+    for (int h = 0; h < H; ++h)
+        acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(xr[h]), static_cast<double>(wg[static_cast<size_t>(h) * E + e])));
+    logits[static_cast<size_t>(t) * E + e] = static_cast<T>(acc);
 }
 
 // ---------------------------------------------------------------- BF16 logits

@@ -36,13 +36,13 @@ __global__ void grouped_gemm_simt_kernel(const T* __restrict__ A, int K, const i
     }
     const T* a = A + static_cast<size_t>(row) * K;
     const T* b = B + static_cast<size_t>(lo) * K * N + col;
-    T acc = 0;
-    for (int p = 0; p < K; ++p) {
-        if constexpr (sizeof(T) == 8) acc = __dadd_rn(acc, __dmul_rn(a[p], b[static_cast<size_t>(p) * N]));
-        else acc = __fadd_rn(acc, __fmul_rn(a[p], b[static_cast<size_t>(p) * N]));
-    }
-    if (relu) acc = acc > T(0) ? acc : T(0);
-    D[static_cast<size_t>(row) * N + col] = acc;
+    // F64: the reference's order and rounding; F32: the same order with the
+    // exact fp32 products accumulated in fp64, rounded once to fp32
+    double acc = 0.0;
+    for (int p = 0; p < K; ++p)
+        acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(a[p]), static_cast<double>(b[static_cast<size_t>(p) * N])));
+    if (relu) acc = acc > 0.0 ? acc : 0.0;
+    D[static_cast<size_t>(row) * N + col] = static_cast<T>(acc);
 }
 
 void launch_grouped_gemm_f64(const double* A, long long rows_bound, int K,
@@ -56,8 +56,8 @@ void launch_grouped_gemm_f64(const double* A, long long rows_bound, int K,
     XMOE_LAUNCH_CHECK();
 }
 
-// F32 instantiation: the reference's order (ascending p, separate multiply
-// and add) in single precision.
+// F32 instantiation: fp32 operands, the reference's order (ascending p,
+// separate multiply and add) with fp64 accumulation, one rounding to fp32.
 void launch_grouped_gemm_f32(const float* A, long long rows_bound, int K, const int32_t* rows_per_group, int G,
                              const float* B, int N, float* D, int relu, cudaStream_t st) {
     if (rows_bound == 0 || N == 0) return;

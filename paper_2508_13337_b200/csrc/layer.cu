@@ -98,8 +98,17 @@ void* Layer::alloc(size_t bytes) {
     return p;
 }
 
+// Stage boundary: a CUDA event in timing mode, and always an NVTX range per
+// stage (gate, pft, dispatch, experts, shared, combine) for nsys/ncu timelines.
 void Layer::mark(int ev, cudaStream_t st) {
     if (timing) XMOE_CUDA(cudaEventRecord(events[ev], st));
+    static const char* const kNames[kNumEvents] = {"xmoe.gate", "xmoe.pft", "xmoe.dispatch", "xmoe.experts",
+                                                   "xmoe.shared", "xmoe.combine", nullptr, nullptr,
+                                                   nullptr, nullptr};
+    if (ev == kEvCounts || ev == kEvMoved || ev == kEvReturn) return;  // sub-stage markers
+    if (nvtx_open) nvtxRangePop();
+    nvtx_open = ev != kEvCombine && kNames[ev] != nullptr;
+    if (nvtx_open) nvtxRangePushA(kNames[ev]);
 }
 
 void Layer::barrier(cudaStream_t st) {

@@ -161,6 +161,7 @@ struct Layer {
     std::vector<void*> allocs;
     std::vector<cudaEvent_t> events;
     bool timing = false;
+    bool nvtx_open = false;  // an NVTX stage range is pushed (Layer::mark)
     bool use_graph = false;
     struct GraphEntry {
         const void* x;

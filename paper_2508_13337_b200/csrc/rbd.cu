@@ -707,12 +707,12 @@ __global__ void __launch_bounds__(256) rbd_merge_kernel(const char* const* __res
                     acc = __dadd_rn(acc, __dmul_rn(md.w, static_cast<double>(row_of(md)[h])));
                 }
                 out[h] = static_cast<T>(acc);
-            } else if constexpr (sizeof(T) == 4) {  // F32: the reference's scale / axpy order in single precision
-                float acc = __fmul_rn(static_cast<float>(row_of(pd)[h]), static_cast<float>(pd.w));
+            } else if constexpr (sizeof(T) == 4) {  // F32: the reference's scale / axpy order, fp64 accumulation
+                double acc = __dmul_rn(static_cast<double>(row_of(pd)[h]), pd.w);
                 for (int m = 0; m < n; ++m) {
                     if (m == pm) continue;
                     const RbdDesc md = desc[c0 + m];
-                    acc = __fadd_rn(acc, __fmul_rn(static_cast<float>(md.w), static_cast<float>(row_of(md)[h])));
+                    acc = __dadd_rn(acc, __dmul_rn(md.w, static_cast<double>(row_of(md)[h])));
                 }
                 out[h] = static_cast<T>(acc);
             } else {
@@ -772,14 +772,14 @@ __global__ void __launch_bounds__(256) rbd_combine_kernel(const char* const* __r
             }
             if (addend) acc = __dadd_rn(acc, static_cast<double>(addend[static_cast<size_t>(t) * H + h]));
             out[static_cast<size_t>(t) * H + h] = static_cast<T>(acc);
-        } else if constexpr (sizeof(T) == 4) {
-            float acc = 0.f;
+        } else if constexpr (sizeof(T) == 4) {  // F32: fp64 accumulation, one rounding
+            double acc = 0.0;
             for (int i = 0; i < nn; ++i) {
                 const int gid = b + order[i];
-                const float sc = g.n[gid] > 1 ? 1.f : static_cast<float>(cw[g.pilot[gid]]);
-                acc = __fadd_rn(acc, __fmul_rn(sc, static_cast<float>(rowp[i][h])));
+                const double sc = g.n[gid] > 1 ? 1.0 : cw[g.pilot[gid]];
+                acc = __dadd_rn(acc, __dmul_rn(sc, static_cast<double>(rowp[i][h])));
             }
-            if (addend) acc = __fadd_rn(acc, static_cast<float>(addend[static_cast<size_t>(t) * H + h]));
+            if (addend) acc = __dadd_rn(acc, static_cast<double>(addend[static_cast<size_t>(t) * H + h]));
             out[static_cast<size_t>(t) * H + h] = static_cast<T>(acc);
         } else {
             float acc = 0.f;

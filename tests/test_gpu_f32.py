@@ -1,7 +1,7 @@
-"""The F32 instantiation (fp32 storage and arithmetic in the reference's
-operation order: ascending-h logits, ascending-p expert GEMMs and ascending
-copies in the combine, each multiply and add separately rounded) against the
-fp64 oracle, at the fp32 bar the reference itself uses between pipelines:
+"""The F32 instantiation (fp32 operands in the reference's operation order:
+ascending-h logits, ascending-p expert GEMMs, ascending copies in the
+combine; exact fp32 products accumulated in fp64, each result rounded once to
+fp32) against the fp64 oracle, at the fp32 bar the reference itself uses between pipelines:
 max_rel_diff (floor 1, matrix.hpp:47-62) <= 1e-5 (verify.cpp:117).  Inputs
 on the bf16-exact grid, so fp32 logits — and routing — are exact."""
 import numpy as np
