@@ -10,6 +10,9 @@
 //   BF16: fp32 accumulation of bf16 rows, 16-byte vectors, bf16 out.
 // An optional dense addend (the shared-expert output, weight 1.0) is added
 // after the routed copies.  HBM-bound: bytes per token = (copies+1)*H*2 + H*2.
+#include <cstdlib>
+#include <string>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -272,10 +275,111 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_slots_bf16_kernel(
     }
 }
 
+// Variant: one CTA per token (XMOE_COMBINE=cta): every copy's whole row is
+// read contiguously by the CTA (thread i owns 16-byte chunk i), the k loads
+// of a thread issued together, the slot list fetched once per token into
+// shared memory.  Same fp32 accumulation order per element as the warp
+// kernel (copies ascending, then the addends), so the output is identical.
+constexpr int kCtaThreads = 256;
+__global__ void __launch_bounds__(kCtaThreads, 4) combine_rows_cta_kernel(
+    const unsigned long long* __restrict__ slot_src, const float* __restrict__ slot_w, int k, int H, int S,
+    const __nv_bfloat16* __restrict__ addend, __nv_bfloat16* __restrict__ out, long long src_delta,
+    const __nv_bfloat16* __restrict__ addend2) {
+    __shared__ unsigned long long sp[2][32];
+    __shared__ float sw[2][32];
+    __shared__ int sn[2];
+    const int nchunk = H >> 3;
+    int buf = 0;
+    for (int t = blockIdx.x; t < S; t += gridDim.x, buf ^= 1) {
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            unsigned long long rp = 0;
+            float wv = 0.f;
+            if (lane < k) {
+                rp = slot_src[static_cast<size_t>(t) * k + lane];
+                wv = slot_w ? slot_w[static_cast<size_t>(t) * k + lane] : 1.f;
+            }
+            const int n = __popc(__ballot_sync(0xffffffffu, lane < k && rp != 0));
+            sp[buf][lane] = rp ? rp + static_cast<unsigned long long>(src_delta) : 0ull;
+            sw[buf][lane] = wv;
+            if (lane == 0) sn[buf] = n;
+        }
+        __syncthreads();  // double-buffered: token t+1's list goes to the other half
+        const int n = sn[buf];
+        for (int c = threadIdx.x; c < nchunk; c += blockDim.x) {
+            int4 a4 = make_int4(0, 0, 0, 0), b4 = make_int4(0, 0, 0, 0);
+            if (addend) a4 = ld_nc_v4(reinterpret_cast<const int4*>(addend + static_cast<size_t>(t) * H) + c);
+            if (addend2) b4 = ld_nc_v4(reinterpret_cast<const int4*>(addend2 + static_cast<size_t>(t) * H) + c);
+            float acc[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+            for (int j0 = 0; j0 < n; j0 += kBatch) {
+                int4 r[kBatch];
+#pragma unroll
+                for (int b = 0; b < kBatch; ++b)
+                    if (j0 + b < n) r[b] = ld_nc_v4(reinterpret_cast<const int4*>(sp[buf][j0 + b]) + c);
+#pragma unroll
+                for (int b = 0; b < kBatch; ++b) {
+                    if (j0 + b >= n) break;
+                    const float wj = sw[buf][j0 + b];
+                    const uint32_t u[4] = {static_cast<uint32_t>(r[b].x), static_cast<uint32_t>(r[b].y),
+                                           static_cast<uint32_t>(r[b].z), static_cast<uint32_t>(r[b].w)};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        acc[2 * q] = fmaf(wj, bf16_lo(u[q]), acc[2 * q]);
+                        acc[2 * q + 1] = fmaf(wj, bf16_hi(u[q]), acc[2 * q + 1]);
+                    }
+                }
+            }
+            if (addend) {
+                const uint32_t u[4] = {static_cast<uint32_t>(a4.x), static_cast<uint32_t>(a4.y),
+                                       static_cast<uint32_t>(a4.z), static_cast<uint32_t>(a4.w)};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    acc[2 * q] += bf16_lo(u[q]);
+                    acc[2 * q + 1] += bf16_hi(u[q]);
+                }
+            }
+            if (addend2) {
+                const uint32_t u[4] = {static_cast<uint32_t>(b4.x), static_cast<uint32_t>(b4.y),
+                                       static_cast<uint32_t>(b4.z), static_cast<uint32_t>(b4.w)};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    acc[2 * q] += bf16_lo(u[q]);
+                    acc[2 * q + 1] += bf16_hi(u[q]);
+                }
+            }
+            int4 o;
+            o.x = static_cast<int>(pack_bf16(acc[0], acc[1]));
+            o.y = static_cast<int>(pack_bf16(acc[2], acc[3]));
+            o.z = static_cast<int>(pack_bf16(acc[4], acc[5]));
+            o.w = static_cast<int>(pack_bf16(acc[6], acc[7]));
+            st_na_v4(reinterpret_cast<int4*>(out + static_cast<size_t>(t) * H) + c, o);
+        }
+    }
+}
+
+static int combine_variant() {
+    static const int v = [] {
+        const char* e = std::getenv("XMOE_COMBINE");
+        return (e && std::string(e) == "cta") ? 1 : 0;
+    }();
+    return v;
+}
+
 void launch_combine_slots(const unsigned long long* slot_src, const float* slot_w, int k, int H, int S,
                           const void* addend, void* out, cudaStream_t st, long long src_delta, const void* addend2) {
     if (S == 0) return;
     require(H % 8 == 0 && k <= 32, XMOE_ERR_VALIDATION, "slot combine needs model_dim % 8 == 0, k <= 32");
+    if (combine_variant() == 1) {
+        int blocks = S < 8 * kNumSMs ? S : 8 * kNumSMs;
+        if (g_copy_blocks > 0 && blocks > g_copy_blocks) blocks = g_copy_blocks;
+        combine_rows_cta_kernel<<<blocks, kCtaThreads, g_copy_smem, st>>>(
+            slot_src, slot_w, k, H, S, static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out),
+            src_delta, static_cast<const __nv_bfloat16*>(addend2));
+        XMOE_LAUNCH_CHECK();
+        return;
+    }
     const long long warps = static_cast<long long>(S) * ((H + kSegCols - 1) / kSegCols);
     long long blocks = ceil_div(warps, kCombWarps);
     if (g_copy_blocks > 0 && blocks > g_copy_blocks) blocks = g_copy_blocks;

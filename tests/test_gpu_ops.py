@@ -3,7 +3,9 @@ pinned oracle (oracle/moe_oracle.py) on identical inputs.
 
 Bars: integer/index outputs and F64 arithmetic bit-exact; softmax weights
 within 4 ulp-level (1e-15 rel, CUDA vs glibc exp); bf16 GEMM against a torch
-fp32 reference of the same bf16 operands within 2e-2 normwise."""
+fp32 reference of the same bf16 operands within the bf16 output rounding
+(normwise 3e-3, elementwise 2^-8 relative); bf16 combine within fp32
+accumulation + one bf16 rounding of the output."""
 import numpy as np
 import pytest
 import torch
@@ -184,7 +186,8 @@ def test_scatter_combine_bf16(ctx):
     w = rng.uniform(0, 1, n)
     got = ctx.scatter_combine(dev(rows, torch.bfloat16), dev(tid, torch.int32), dev(w), S)
     want = O.scatter_combine(rows, tid, w, S)
-    np.testing.assert_allclose(host(got), want, rtol=1e-2, atol=2e-2)
+    # fp32 sums of <= ~12 copies, one bf16 rounding: 2^-8 relative + fp32 noise
+    np.testing.assert_allclose(host(got), want, rtol=2.0 ** -8, atol=1e-5)
 
 
 # ---------------------------------------------------------------- expert FFN
@@ -233,6 +236,7 @@ def test_grouped_gemm_bf16_tcgen05(ctx, seg, K, N):
         D = ctx.grouped_gemm_bf16(A, segt, B, N, relu=relu)
         ref = _torch_grouped_gemm(A, segt, B, N, relu)
         err = (D.float() - ref).norm() / ref.norm().clamp_min(1e-30)
-        assert err < 2e-2, float(err)
-        # bf16 rounding of the fp32 accumulator is the only error
-        assert torch.allclose(D.float(), ref, rtol=1.6e-2, atol=1e-2)
+        # bf16 rounding of the fp32 accumulator is the only error: at most half
+        # a bf16 ulp (2^-9 relative) per element, ~1e-3 normwise
+        assert err < 3e-3, float(err)
+        assert torch.allclose(D.float(), ref, rtol=2.0 ** -8, atol=1e-4)
