@@ -578,10 +578,15 @@ def main():
     # separate streams (double-buffered), as a serving loop would run them.
     e2e_steps = max(50, args.steps)  # steady state: one pipeline fill + drain amortised over the run
     numa_cpus = bind_to_gpu_numa(local_rank)
-    xh = [xin.cpu().pin_memory() for _ in range(2)]
-    oh = [torch.empty_like(xh[0]).pin_memory() for _ in range(2)]
-    xd = [torch.empty_like(xin) for _ in range(2)]
+    # SSMB (C4): every rank holds the whole sequence buffer but reads only its
+    # shard, so only the shard crosses PCIe; the all-gathered output comes back whole
+    x_lo = (rank * (S_seq // world)) if ssmb else 0
+    xh = [x.cpu().pin_memory() for _ in range(2)]
+    oh = [torch.empty_like(xin.cpu()).pin_memory() for _ in range(2)]
+    xd = [xin.clone() for _ in range(2)]
     od = [torch.empty_like(xin) for _ in range(2)]
+    h2d_bytes = x.numel() * 2
+    d2h_bytes = xin.numel() * 2
     s_in = torch.cuda.Stream()
     s_out = torch.cuda.Stream()
     ev_in = [torch.cuda.Event() for _ in range(2)]
@@ -592,7 +597,7 @@ def main():
         if t0 is not None:
             t0.record(s_in)
         with torch.cuda.stream(s_in):
-            xd[0].copy_(xh[0], non_blocking=True)
+            xd[0][x_lo:x_lo + S].copy_(xh[0], non_blocking=True)
             ev_in[0].record(s_in)
         for i in range(n):
             b, nb = i % 2, (i + 1) % 2
@@ -600,7 +605,7 @@ def main():
                 with torch.cuda.stream(s_in):
                     if i >= 1:
                         s_in.wait_event(ev_done[nb])  # step i-1 finished reading xd[nb]
-                    xd[nb].copy_(xh[nb], non_blocking=True)
+                    xd[nb][x_lo:x_lo + S].copy_(xh[nb], non_blocking=True)
                     ev_in[nb].record(s_in)
             stream.wait_event(ev_in[b])
             if i >= 2:
@@ -652,7 +657,7 @@ def main():
                        "l2": f"working set > L2: {wbytes / 1e9:.2f} GB of expert weights per GPU + "
                              f"{S * H * 2 / 1e6:.0f} MB tokens stream each step (126 MB L2)"},
             "e2e": {"value": tokens_step / (e2e_ms * 1e-3), "unit": UNIT,
-                    "h2d_bytes_per_step": xin.numel() * 2, "d2h_bytes_per_step": xin.numel() * 2,
+                    "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
                     "steps": e2e_steps,
                     "host_cpus": numa_cpus,
                     "note": "pinned host x -> device, forward, device -> pinned host out, every step; copies of "

@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_slots_bf16_kernel(
     }
 }
 
-// Variant: one CTA per token (XMOE_COMBINE=cta): every copy's whole row is
+// One CTA per token (default on a full grid): every copy's whole row is
 // read contiguously by the CTA (thread i owns 16-byte chunk i), the k loads
 // of a thread issued together, the slot list fetched once per token into
 // shared memory.  Same fp32 accumulation order per element as the warp
@@ -359,12 +359,19 @@ __global__ void __launch_bounds__(kCtaThreads, 4) combine_rows_cta_kernel(
     }
 }
 
+// CTA-per-token variant on a full grid (measured on B200, C2 N=1: combine
+// 0.104-0.118 -> 0.097 ms, 0.70-0.79 -> 0.85 of HBM); the warp kernel when the
+// grid is capped to run beside GEMMs (chunked forward: its per-warp items keep
+// more rows in flight per block there; the CTA variant measured 40 -> 32 M
+// tokens/s at N=4).  XMOE_COMBINE=warp|cta forces one (A/B).
 static int combine_variant() {
     static const int v = [] {
         const char* e = std::getenv("XMOE_COMBINE");
-        return (e && std::string(e) == "cta") ? 1 : 0;
+        if (e && std::string(e) == "cta") return 1;
+        if (e && std::string(e) == "warp") return 2;
+        return 0;
     }();
-    return v;
+    return v == 0 ? (g_copy_blocks == 0 ? 1 : 0) : (v == 1 ? 1 : 0);
 }
 
 void launch_combine_slots(const unsigned long long* slot_src, const float* slot_w, int k, int H, int S,

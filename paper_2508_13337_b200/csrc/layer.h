@@ -201,6 +201,8 @@ struct Layer {
     void barrier(cudaStream_t st);
     long long C(int s, int d) const;  // copies source s -> dest d (needs h_tpe)
     void ledger(uint64_t* out, int n);
+    unsigned long long* led_cnt = nullptr;  // device ledger counters (rbd.cu ledger_counts_kernel)
+    std::vector<uint64_t> device_counts(const Worker& w, long long S, bool groups);
     void quiesce();            // cross-rank barrier before teardown (p2p layers)
     void check_peers() const;  // throws XMOE_ERR_PEER_TIMEOUT after a failed peer wait
     // reference-schema ledger (ledger.cpp)

@@ -7,7 +7,6 @@
 
 #include <algorithm>
 #include <cstring>
-#include <set>
 #include <string>
 #include <utility>
 #include <vector>
@@ -16,6 +15,17 @@
 #include "layer.h"
 
 namespace xmoe {
+
+// the device ledger counters of worker w's last forward (rbd.cu layout)
+std::vector<uint64_t> Layer::device_counts(const Worker& w, long long S, bool groups) {
+    const int ncnt = 1 + 3 * W + W * W;
+    if (!led_cnt) led_cnt = static_cast<unsigned long long*>(alloc(sizeof(unsigned long long) * ncnt));
+    launch_ledger_counts(w.slot_pos, static_cast<int>(S), k, w.expert_ids, El, w.rank, groups ? &w.rbd : nullptr, W,
+                         led_cnt, nullptr);
+    std::vector<uint64_t> h(ncnt, 0);
+    XMOE_CUDA(cudaMemcpy(h.data(), led_cnt, sizeof(uint64_t) * ncnt, cudaMemcpyDeviceToHost));
+    return h;
+}
 
 void Layer::ledger(uint64_t* out, int n) {
     std::vector<int32_t> tpe(static_cast<size_t>(W) * E);
@@ -34,26 +44,10 @@ void Layer::ledger(uint64_t* out, int n) {
         }
         if (W > 1) v[2] += static_cast<uint64_t>(W - 1) * E * sizeof(int32_t);  // count all-gather
         // distinct (token, destination rank) groups leaving the rank: the rows
-        // the redundancy bypass sends (rbd.cpp:427-442 with node_of = rank)
+        // the redundancy bypass sends (rbd.cpp:427-442 with node_of = rank),
+        // counted on the device
         const long long S = last_Sw.empty() ? last_S : last_Sw[static_cast<size_t>(&w - workers.data())];
-        if (S > 0) {
-            std::vector<int32_t> slot(static_cast<size_t>(S) * k), eid(static_cast<size_t>(S) * k);
-            XMOE_CUDA(cudaMemcpy(slot.data(), w.slot_pos, sizeof(int32_t) * slot.size(), cudaMemcpyDeviceToHost));
-            int32_t B = 0;
-            XMOE_CUDA(cudaMemcpy(&B, w.B_dev, sizeof(int32_t), cudaMemcpyDeviceToHost));
-            std::vector<int32_t> ex(B > 0 ? B : 1);
-            if (B > 0) XMOE_CUDA(cudaMemcpy(ex.data(), w.expert_ids, sizeof(int32_t) * B, cudaMemcpyDeviceToHost));
-            for (long long t = 0; t < S; ++t) {
-                std::set<int> dests;
-                for (int j = 0; j < k; ++j) {
-                    const int p = slot[static_cast<size_t>(t) * k + j];
-                    if (p < 0) break;
-                    const int d = ex[p] / El;
-                    if (d != w.rank) dests.insert(d);
-                }
-                v[6] += dests.size();
-            }
-        }
+        v[6] += device_counts(w, S, false)[0];
     }
     if (d.dispatch_mode == XMOE_DISPATCH_RBD) {
         h_G.resize(static_cast<size_t>(W) * W);
@@ -207,38 +201,20 @@ void Layer::ledger_entries(const xmoe_topology& topo, std::vector<xmoe_ledger_en
             }
             continue;
         }
-        // rbd.cpp:130-233, 300-345: per (token, node) group of source s
-        int32_t G = 0;
-        XMOE_CUDA(cudaMemcpy(&G, w.rbd.G_dev, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        // rbd.cpp:130-233, 300-345: per (token, node) group of source s, from
+        // the device counters (rbd.cu ledger_counts_kernel)
         const long long S = last_Sw.empty() ? last_S : last_Sw[static_cast<size_t>(&w - workers.data())];
-        std::vector<int32_t> tok(G), dst(G), first(G), n(G), pilot(G);
-        if (G > 0) {
-            XMOE_CUDA(cudaMemcpy(tok.data(), w.rbd.g.token, sizeof(int32_t) * G, cudaMemcpyDeviceToHost));
-            XMOE_CUDA(cudaMemcpy(dst.data(), w.rbd.g.dest, sizeof(int32_t) * G, cudaMemcpyDeviceToHost));
-            XMOE_CUDA(cudaMemcpy(first.data(), w.rbd.g.first_slot, sizeof(int32_t) * G, cudaMemcpyDeviceToHost));
-            XMOE_CUDA(cudaMemcpy(n.data(), w.rbd.g.n, sizeof(int32_t) * G, cudaMemcpyDeviceToHost));
-            XMOE_CUDA(cudaMemcpy(pilot.data(), w.rbd.g.pilot, sizeof(int32_t) * G, cudaMemcpyDeviceToHost));
-        }
-        std::vector<int32_t> slot(static_cast<size_t>(S) * k);
-        if (!slot.empty())
-            XMOE_CUDA(cudaMemcpy(slot.data(), w.slot_pos, sizeof(int32_t) * slot.size(), cudaMemcpyDeviceToHost));
-        int32_t B = 0;
-        XMOE_CUDA(cudaMemcpy(&B, w.B_dev, sizeof(int32_t), cudaMemcpyDeviceToHost));
-        std::vector<int32_t> ex(B > 0 ? B : 1);
-        if (B > 0) XMOE_CUDA(cudaMemcpy(ex.data(), w.expert_ids, sizeof(int32_t) * B, cudaMemcpyDeviceToHost));
-        for (int g = 0; g < G; ++g) {
-            const int L = dst[g];
-            at(2, s, L) += rbytes;  // rows1: the pilot row
-            at(6, L, s) += rbytes;  // combine rows1: one merged row home
-            if (n[g] > 1) at(1, s, L) += db;  // the pilot's weight rides along
-            for (int m = 0; m < n[g]; ++m) {
-                const int p = slot[static_cast<size_t>(tok[g]) * k + first[g] + m];
-                if (p == pilot[g]) continue;
-                const int owner = ex[p] / El;
-                at(1, s, L) += 3 * 8 + db;  // replica descriptor + weight
-                at(3, L, owner) += 3 * 8;   // stage-2 descriptor
-                at(4, L, owner) += rbytes;  // stage-2 row
-                at(5, owner, L) += rbytes;  // reverse stage 2
+        const std::vector<uint64_t> c = device_counts(w, S, true);
+        for (int L = 0; L < W; ++L) {
+            const uint64_t pil = c[1 + L], multi = c[1 + W + L], reps = c[1 + 2 * W + L];
+            at(2, s, L) += pil * rbytes;                   // rows1: the pilot rows
+            at(6, L, s) += pil * rbytes;                   // combine rows1: one merged row home
+            at(1, s, L) += multi * db + reps * (3 * 8 + db);  // weights + replica descriptors
+            for (int o = 0; o < W; ++o) {
+                const uint64_t r2 = c[1 + 3 * W + static_cast<size_t>(L) * W + o];
+                at(3, L, o) += r2 * 3 * 8;  // stage-2 descriptors
+                at(4, L, o) += r2 * rbytes;  // stage-2 rows
+                at(5, o, L) += r2 * rbytes;  // reverse stage 2
             }
         }
     }

@@ -28,6 +28,7 @@
 //            (rbd.cpp:318-336); singletons return raw
 //   combine  source adds its groups in pilot order with scale 1 (merged) or
 //            the pilot weight (singleton) (rbd.cpp:343-356).
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -945,6 +946,74 @@ __global__ void __launch_bounds__(256) rbd_combine_bf16_kernel(
         o.w = static_cast<int>(pack_bf16(acc[6], acc[7]));
         st_na_v4(reinterpret_cast<int4*>(out + static_cast<size_t>(t) * H) + c, o);
     }
+}
+
+// ---------------------------------------------------------------- byte ledger counts
+// Device counters behind the byte ledger of the last forward (ledger.cpp):
+//   out[0]                       (token, destination rank != me) groups: the rows
+//                                the redundancy bypass sends off-rank (rbd.cpp:427-442)
+//   out[1 + L]                   pilots landing at L (stage-1 rows, merged rows home)
+//   out[1 + W + L]               ... of groups with replicas (their weight rides along)
+//   out[1 + 2W + L]              replicas whose descriptors ride to L
+//   out[1 + 3W + L * W + o]      replicas forwarded by L to owner o (stage 2)
+// Block-level counts in shared memory, one global atomic per nonzero counter.
+__global__ void __launch_bounds__(256) ledger_counts_kernel(const int32_t* __restrict__ slot_pos, int S, int k,
+                                                            const int32_t* __restrict__ expert_ids, int El, int me,
+                                                            RbdGroups g, const int32_t* __restrict__ G_dev, int W,
+                                                            unsigned long long* __restrict__ out) {
+    extern __shared__ unsigned int cnt[];
+    const int ncnt = 1 + 3 * W + W * W;
+    for (int i = threadIdx.x; i < ncnt; i += blockDim.x) cnt[i] = 0u;
+    __syncthreads();
+    const int G = (G_dev && g.pilot) ? *G_dev : 0;
+    const int n_items = S > G ? S : G;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_items; i += gridDim.x * blockDim.x) {
+        if (i < S) {  // distinct off-rank destinations of token i (slots ascending = dests ascending)
+            int last = -1, nd = 0;
+            for (int j = 0; j < k; ++j) {
+                const int p = slot_pos[static_cast<size_t>(i) * k + j];
+                if (p < 0) break;
+                const int d = expert_ids[p] / El;
+                if (d != me && d != last) ++nd;
+                last = d;
+            }
+            if (nd) atomicAdd(&cnt[0], static_cast<unsigned>(nd));
+        }
+        if (i < G) {
+            const int L = g.dest[i], n = g.n[i], t = g.token[i], f = g.first_slot[i], pl = g.pilot[i];
+            atomicAdd(&cnt[1 + L], 1u);
+            if (n > 1) atomicAdd(&cnt[1 + W + L], 1u);
+            for (int m = 0; m < n; ++m) {
+                const int p = slot_pos[static_cast<size_t>(t) * k + f + m];
+                if (p == pl) continue;
+                atomicAdd(&cnt[1 + 2 * W + L], 1u);
+                atomicAdd(&cnt[1 + 3 * W + L * W + expert_ids[p] / El], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ncnt; i += blockDim.x)
+        if (cnt[i]) atomicAdd(&out[i], static_cast<unsigned long long>(cnt[i]));
+}
+
+void launch_ledger_counts(const int32_t* slot_pos, int S, int k, const int32_t* expert_ids, int El, int me,
+                          const RbdWork* wk, int W, unsigned long long* out, cudaStream_t st) {
+    const int ncnt = 1 + 3 * W + W * W;
+    require(ncnt * 4 <= 48 * 1024, XMOE_ERR_VALIDATION, "ledger counters: world too large");
+    XMOE_CUDA(cudaMemsetAsync(out, 0, sizeof(unsigned long long) * ncnt, st));
+    RbdGroups g{};
+    const int32_t* G_dev = nullptr;
+    long long items = S;
+    if (wk) {
+        g = wk->g;
+        G_dev = wk->G_dev;
+        items = std::max<long long>(S, static_cast<long long>(S) * k);
+    }
+    if (items == 0) return;
+    const long long blocks = std::min<long long>((items + 255) / 256, 4LL * kNumSMs);
+    ledger_counts_kernel<<<static_cast<int>(blocks), 256, sizeof(unsigned) * ncnt, st>>>(
+        slot_pos, S, k, expert_ids, El, me, g, G_dev, W, out);
+    XMOE_LAUNCH_CHECK();
 }
 
 // ---------------------------------------------------------------- launchers

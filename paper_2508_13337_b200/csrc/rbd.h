@@ -103,6 +103,11 @@ void launch_rbd_combine(int dtype, const char* const* back_tab, int H, int S, co
 void launch_mask_from_groups(const RbdWork& wk, const int32_t* slot_pos, int k, long long max_groups, uint8_t* mask,
                              int32_t* pilot_of, cudaStream_t st);
 
+// rbd.cu: device counters of the byte ledger (layout in rbd.cu); wk == null:
+// only out[0] (off-rank (token, destination) groups)
+void launch_ledger_counts(const int32_t* slot_pos, int S, int k, const int32_t* expert_ids, int El, int me,
+                          const RbdWork* wk, int W, unsigned long long* out, cudaStream_t st);
+
 // pft.cu: stable CSR with the item count on the device (bound n_max).
 void launch_stable_csr_dev(const int32_t* keys, const int32_t* n_dev, int n_max, int K, int32_t* ptr,
                            int32_t* perm, void* ws, cudaStream_t st);
