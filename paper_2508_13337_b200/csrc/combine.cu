@@ -10,6 +10,7 @@
 //   BF16: fp32 accumulation of bf16 rows, 16-byte vectors, bf16 out.
 // An optional dense addend (the shared-expert output, weight 1.0) is added
 // after the routed copies.  HBM-bound: bytes per token = (copies+1)*H*2 + H*2.
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 
@@ -284,13 +285,24 @@ constexpr int kCtaThreads = 256;
 __global__ void __launch_bounds__(kCtaThreads, 4) combine_rows_cta_kernel(
     const unsigned long long* __restrict__ slot_src, const float* __restrict__ slot_w, int k, int H, int S,
     const __nv_bfloat16* __restrict__ addend, __nv_bfloat16* __restrict__ out, long long src_delta,
-    const __nv_bfloat16* __restrict__ addend2) {
+    const __nv_bfloat16* __restrict__ addend2, float* __restrict__ partial, unsigned* __restrict__ ready) {
     __shared__ unsigned long long sp[2][32];
     __shared__ float sw[2][32];
     __shared__ int sn[2];
+    __shared__ int st_next[2];
     const int nchunk = H >> 3;
     int buf = 0;
-    for (int t = blockIdx.x; t < S; t += gridDim.x, buf ^= 1) {
+    // partial mode: tokens are taken from a device counter (ready[ceil(S/128)])
+    // so any resident CTA advances every 128-token block — the consuming GEMM
+    // may hold the SMs some CTAs of this grid would need
+    unsigned* next = partial ? ready + ((S + 127) >> 7) : nullptr;
+    int t = blockIdx.x;
+    if (next) {
+        if (threadIdx.x == 0) st_next[0] = static_cast<int>(atomicAdd(next, 1u));
+        __syncthreads();
+        t = st_next[0];
+    }
+    for (; t < S; buf ^= 1) {
         if (threadIdx.x < 32) {
             const int lane = threadIdx.x;
             unsigned long long rp = 0;
@@ -349,12 +361,30 @@ __global__ void __launch_bounds__(kCtaThreads, 4) combine_rows_cta_kernel(
                     acc[2 * q + 1] += bf16_hi(u[q]);
                 }
             }
+            if (partial) {  // fp32 sums of the routed copies; the shared GEMM2 epilogue finishes the row
+                float4* pd = reinterpret_cast<float4*>(partial + static_cast<size_t>(t) * H) + 2 * c;
+                pd[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+                pd[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+                continue;
+            }
             int4 o;
             o.x = static_cast<int>(pack_bf16(acc[0], acc[1]));
             o.y = static_cast<int>(pack_bf16(acc[2], acc[3]));
             o.z = static_cast<int>(pack_bf16(acc[4], acc[5]));
             o.w = static_cast<int>(pack_bf16(acc[6], acc[7]));
             st_na_v4(reinterpret_cast<int4*>(out + static_cast<size_t>(t) * H) + c, o);
+        }
+        if (partial) {  // publish token t: its 128-row block's counter (release), take the next token
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(ready + (t >> 7), 1u);
+                st_next[buf ^ 1] = static_cast<int>(atomicAdd(next, 1u));
+            }
+            __syncthreads();
+            t = st_next[buf ^ 1];
+        } else {
+            t += gridDim.x;
         }
     }
 }
@@ -383,7 +413,7 @@ void launch_combine_slots(const unsigned long long* slot_src, const float* slot_
         if (g_copy_blocks > 0 && blocks > g_copy_blocks) blocks = g_copy_blocks;
         combine_rows_cta_kernel<<<blocks, kCtaThreads, g_copy_smem, st>>>(
             slot_src, slot_w, k, H, S, static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out),
-            src_delta, static_cast<const __nv_bfloat16*>(addend2));
+            src_delta, static_cast<const __nv_bfloat16*>(addend2), nullptr, nullptr);
         XMOE_LAUNCH_CHECK();
         return;
     }
@@ -393,6 +423,30 @@ void launch_combine_slots(const unsigned long long* slot_src, const float* slot_
     combine_slots_bf16_kernel<<<static_cast<int>(blocks), 32 * kCombWarps, g_copy_smem, st>>>(
         slot_src, slot_w, k, H, S, static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out),
         src_delta, static_cast<const __nv_bfloat16*>(addend2));
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_combine_slots_partial(const unsigned long long* slot_src, const float* slot_w, int k, int H, int S,
+                                  float* partial, unsigned* ready, cudaStream_t st) {
+    if (S == 0) return;
+    require(H % 8 == 0 && k <= 32, XMOE_ERR_VALIDATION, "slot combine needs model_dim % 8 == 0, k <= 32");
+    // Launched BEFORE the GEMM that consumes it (that GEMM waits on the ready
+    // counters, so it must never hold SMs the combine cannot share): one CTA
+    // per SM by default (XMOE_LATE_GRID), preferring the maximum shared-memory
+    // carveout so a 2-CTA GEMM CTA (223 KB) still fits beside it.
+    static const int grid_cap = [] {
+        const char* e = std::getenv("XMOE_LATE_GRID");
+        return e ? std::max(1, std::atoi(e)) : kNumSMs;
+    }();
+    static bool attr = false;
+    if (!attr) {
+        XMOE_CUDA(cudaFuncSetAttribute(combine_rows_cta_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       static_cast<int>(cudaSharedmemCarveoutMaxShared)));
+        attr = true;
+    }
+    const int blocks = S < grid_cap ? S : grid_cap;
+    combine_rows_cta_kernel<<<blocks, kCtaThreads, 0, st>>>(slot_src, slot_w, k, H, S, nullptr, nullptr, 0, nullptr,
+                                                           partial, ready);
     XMOE_LAUNCH_CHECK();
 }
 

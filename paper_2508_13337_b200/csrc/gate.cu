@@ -46,7 +46,8 @@ template <int PER, typename LT>
 __global__ void __launch_bounds__(256) softmax_topk_kernel(const LT* __restrict__ logits, int S,
                                                            int E, int k, int renorm,
                                                            int32_t* __restrict__ top,
-                                                           double* __restrict__ weights) {
+                                                           double* __restrict__ weights,
+                                                           int32_t* __restrict__ counts) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= S) return;
@@ -101,6 +102,8 @@ __global__ void __launch_bounds__(256) softmax_topk_kernel(const LT* __restrict_
         if (lane == 0) {
             top[static_cast<size_t>(warp) * k + j] = bid;
             weights[static_cast<size_t>(warp) * k + j] = best;
+            // per-128-token-tile expert histogram for the one-launch placement
+            if (counts) atomicAdd(&counts[static_cast<size_t>(warp / kRouteTile) * E + bid], 1);
         }
         wsum = __dadd_rn(wsum, best);
     }
@@ -130,15 +133,17 @@ void launch_gate_logits_f32(const float* x, const float* wg, int S, int H, int E
 
 template <typename LT>
 static void softmax_dispatch(const LT* logits, int S, int E, int k, int renorm, int32_t* top,
-                             double* weights, cudaStream_t st) {
+                             double* weights, cudaStream_t st, int32_t* counts = nullptr) {
     if (S == 0) return;
     require(E <= 1024, XMOE_ERR_VALIDATION, "num_experts must be <= 1024");
+    if (counts)
+        XMOE_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * ((S + kRouteTile - 1) / kRouteTile) * E, st));
     const int grid = ceil_div(S, 8);
-    if (E <= 32) softmax_topk_kernel<1, LT><<<grid, 256, 0, st>>>(logits, S, E, k, renorm, top, weights);
-    else if (E <= 64) softmax_topk_kernel<2, LT><<<grid, 256, 0, st>>>(logits, S, E, k, renorm, top, weights);
-    else if (E <= 128) softmax_topk_kernel<4, LT><<<grid, 256, 0, st>>>(logits, S, E, k, renorm, top, weights);
-    else if (E <= 256) softmax_topk_kernel<8, LT><<<grid, 256, 0, st>>>(logits, S, E, k, renorm, top, weights);
-    else softmax_topk_kernel<32, LT><<<grid, 256, 0, st>>>(logits, S, E, k, renorm, top, weights);
+    if (E <= 32) softmax_topk_kernel<1, LT><<<grid, 256, 0, st>>>(logits, S, E, k, renorm, top, weights, counts);
+    else if (E <= 64) softmax_topk_kernel<2, LT><<<grid, 256, 0, st>>>(logits, S, E, k, renorm, top, weights, counts);
+    else if (E <= 128) softmax_topk_kernel<4, LT><<<grid, 256, 0, st>>>(logits, S, E, k, renorm, top, weights, counts);
+    else if (E <= 256) softmax_topk_kernel<8, LT><<<grid, 256, 0, st>>>(logits, S, E, k, renorm, top, weights, counts);
+    else softmax_topk_kernel<32, LT><<<grid, 256, 0, st>>>(logits, S, E, k, renorm, top, weights, counts);
     XMOE_LAUNCH_CHECK();
 }
 
@@ -148,8 +153,8 @@ void launch_softmax_topk(const double* logits, int S, int E, int k, int renorm, 
 }
 
 void launch_softmax_topk_f32(const float* logits, int S, int E, int k, int renorm, int32_t* top,
-                             double* weights, cudaStream_t st) {
-    softmax_dispatch(logits, S, E, k, renorm, top, weights, st);
+                             double* weights, cudaStream_t st, int32_t* counts) {
+    softmax_dispatch(logits, S, E, k, renorm, top, weights, st, counts);
 }
 
 }  // namespace xmoe

@@ -32,6 +32,8 @@ namespace xmoe {
 // SM budget of the next 2-CTA GEMM launches (0 = all SMs); the layer lowers it
 // for GEMMs that run on a side stream next to bandwidth-bound kernels.
 thread_local int g_gemm_sm_limit = 0;
+thread_local const float* g_gemm_addf = nullptr;
+thread_local const unsigned* g_gemm_ready = nullptr;
 
 namespace tc {
 
@@ -861,7 +863,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             const int32_t* __restrict__ group_sizes, int G, int M, int N, int K,
                             OutT* __restrict__ D, int relu, const uint32_t* __restrict__ mbits_in,
                             uint32_t* __restrict__ mbits_out, int coalesced, const int32_t* __restrict__ a_idx,
-                            int a_rows, const __grid_constant__ CUtensorMap tmap_d, int tma_d, int half_ok) {
+                            int a_rows, const __grid_constant__ CUtensorMap tmap_d, int tma_d, int half_ok,
+                            const float* addf, const unsigned* ready) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -1062,6 +1065,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int q = 0; q < BN / 32; ++q) mpre[q] = (mrow && row_ok && 32 * q < nw) ? __ldg(mrow + q) : 0u;
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
+            // fused addend (shared experts after the routed combine, layer.cu):
+            // D = bf16(addf + float(bf16(acc))) once the combine has published
+            // this warp's 128-row block (ready[block] == rows in the block)
+            const float* arow_f = nullptr;
+            if (addf && ti.row0 + wrow < off[G]) {
+                const int blk = (ti.row0 + wrow) >> 7;
+                const unsigned want = static_cast<unsigned>(min(128, off[G] - (blk << 7)));
+                if (lane == 0) {
+                    for (uint32_t it = 0;; ++it) {
+                        unsigned v;
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + blk) : "memory");
+                        if (v >= want) break;
+                        __nanosleep(200);
+                        if (it == (1u << 27)) asm volatile("trap;");  // a producer never published: fail loudly
+                    }
+                }
+                __syncwarp();
+                if (row_ok) arow_f = addf + static_cast<size_t>(ti.row0 + r) * N + ti.n0 + cbase;
+            }
             uint32_t* orow = mbits_out ? mbits_out + static_cast<size_t>(ti.row0 + r) * mwords +
                                              ((ti.n0 + cbase) >> 5)
                                        : nullptr;
@@ -1112,6 +1134,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int i = 0; i < 32; ++i)
                         if (!((mw >> i) & 1u)) f[i] = 0.f;
+                }
+                if (arow_f) {  // same arithmetic as the combine's addend: fp32 sum + bf16(shared)
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        float4 pv;
+                        asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                     : "=f"(pv.x), "=f"(pv.y), "=f"(pv.z), "=f"(pv.w)
+                                     : "l"(arow_f + c0 + 4 * q));
+                        f[4 * q + 0] = pv.x + __bfloat162float(__float2bfloat16_rn(f[4 * q + 0]));
+                        f[4 * q + 1] = pv.y + __bfloat162float(__float2bfloat16_rn(f[4 * q + 1]));
+                        f[4 * q + 2] = pv.z + __bfloat162float(__float2bfloat16_rn(f[4 * q + 2]));
+                        f[4 * q + 3] = pv.w + __bfloat162float(__float2bfloat16_rn(f[4 * q + 3]));
+                    }
                 }
                 if constexpr (sizeof(OutT) == 2) {
                     if (cn == 32 && (N & 7) == 0) {
@@ -1678,7 +1713,7 @@ static void launch_tc2(const void* A, long long a_rows, long long a_cols, const 
     tc2::grouped_gemm_tc2_kernel<OutT, kVarK><<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
         ta, tb, group_sizes, G, M, N, K, D, relu, mbits_in, mbits_out,
         sizeof(OutT) == 4 && !mbits_out ? epi_coalesced() : 0, a_idx, static_cast<int>(idx_rows), td, tma_d ? 1 : 0,
-        half_tiles() ? 1 : 0);
+        half_tiles() ? 1 : 0, kVarK ? nullptr : g_gemm_addf, kVarK ? nullptr : g_gemm_ready);
     XMOE_LAUNCH_CHECK();
 }
 
@@ -1702,9 +1737,13 @@ static bool use_2cta(int N) {
     return mode == 2 && N % 32 == 0;
 }
 
+bool gemm_2cta_enabled(int N) { return use_2cta(N); }
+
 void launch_grouped_gemm_bf16(const void* A, long long rows, int K, const int32_t* rows_per_group,
                               int G, const void* B, int N, void* D, int relu, cudaStream_t st, uint32_t* mbits_out) {
     require(!mbits_out || (relu && use_2cta(N)), XMOE_ERR_VALIDATION, "ReLU mask output needs the 2-CTA ReLU GEMM");
+    require(!g_gemm_addf || (use_2cta(N) && !relu && !mbits_out), XMOE_ERR_VALIDATION,
+            "fused addend needs the 2-CTA GEMM without ReLU");
     if (use_2cta(N))
         launch_tc2_rows<__nv_bfloat16>(A, rows, K, rows_per_group, G, B, N, static_cast<__nv_bfloat16*>(D), relu,
                                        nullptr, mbits_out, st);

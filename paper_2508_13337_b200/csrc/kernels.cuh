@@ -8,14 +8,17 @@
 
 namespace xmoe {
 
+constexpr int kRouteTile = 128;  // tokens per gate tile / routing histogram row
+
 // gate.cu
 void launch_gate_logits_f64(const double* x, const double* wg, int S, int H, int E,
                             double* logits, cudaStream_t st);
 void launch_gate_logits_f32(const float* x, const float* wg, int S, int H, int E, float* logits, cudaStream_t st);
 void launch_softmax_topk(const double* logits, int S, int E, int k, int renorm, int32_t* top,
                          double* weights, cudaStream_t st);
+// counts (optional): per-128-token-tile expert histograms [ceil(S/128), E]
 void launch_softmax_topk_f32(const float* logits, int S, int E, int k, int renorm, int32_t* top,
-                             double* weights, cudaStream_t st);
+                             double* weights, cudaStream_t st, int32_t* counts = nullptr);
 
 // pft.cu
 size_t bucket_ws_bytes(long long n, int K);
@@ -45,6 +48,9 @@ void launch_scatter_tokens(const void* x, int row_bytes, int S, int k, const int
 void launch_combine_slots(const unsigned long long* slot_src, const float* slot_w, int k, int H, int S,
                           const void* addend, void* out, cudaStream_t st, long long src_delta = 0,
                           const void* addend2 = nullptr);
+// routed copies only, fp32 sums to partial [S, H]; ready[t / 128] += 1 per token
+void launch_combine_slots_partial(const unsigned long long* slot_src, const float* slot_w, int k, int H, int S,
+                                  float* partial, unsigned* ready, cudaStream_t st);
 void launch_unscatter_rows(int row_bytes, const int32_t* B_dev, long long max_rows,
                            const int32_t* dest_rank, const int32_t* dest_row,
                            const char* const* src_bufs, void* out, cudaStream_t st);
@@ -102,7 +108,6 @@ void launch_gate_route(const void* x, int S, int H, const void* gate_kmajor, int
 void launch_route_place(const int32_t* top, const double* weights, const int32_t* counts, int S, int E, int k,
                         int32_t* token_ids, int32_t* expert_ids, double* cw, int32_t* tpe, int32_t* slot_pos,
                         int32_t* B_dev, cudaStream_t st);
-constexpr int kRouteTile = 128;  // tokens per gate tile / histogram row
 
 // backward.cu
 void launch_bwd_owner_prep(const void* dyg, const void* eout, const float* gw, const unsigned long long* gsrc,
@@ -121,6 +126,12 @@ void launch_gate_bwd(const float* logits, const int32_t* slot_pos, const int32_t
 
 // gemm_tc.cu: SM budget of subsequent 2-CTA GEMM launches on this thread (0 = all)
 extern thread_local int g_gemm_sm_limit;
+// fused fp32 addend of the next bf16 2-CTA GEMM launches (one group of rows,
+// no ReLU): D = bf16(addf[row] + float(bf16(acc))), each 128-row block read
+// once ready[block] reaches its row count (published by the partial combine)
+extern thread_local const float* g_gemm_addf;
+extern thread_local const unsigned* g_gemm_ready;
+bool gemm_2cta_enabled(int N);  // the 2-CTA kernel serves N (XMOE_GEMM, N % 32)
 // grid cap of the row-movement kernels (token scatter, slot combine; 0 =
 // their default).  The chunked forward runs them on a few SMs' worth of
 // blocks so the NVLink traffic they drive does not stall the GEMM CTAs on

@@ -60,7 +60,7 @@ Layer::~Layer() {
     if (side) cudaStreamDestroy(side);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (comm) cudaStreamDestroy(comm);
-    for (cudaEvent_t e : {ev_fork, ev_join, ev_side0, ev_side1, ev_done})
+    for (cudaEvent_t e : {ev_fork, ev_join, ev_side0, ev_side1, ev_done, ev_routed})
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : evA) cudaEventDestroy(e);
     for (cudaEvent_t e : evB) cudaEventDestroy(e);
@@ -278,6 +278,10 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         }
     }
     L.route_cnt_ok = bf && gate_route_supported(L.E, L.k, L.H);
+    if (bf && !L.distributed && L.nl == 1 && L.Fs > 0 && !L.ssmb) {  // late shared GEMM2 (layer_forward_v)
+        L.partial = static_cast<float*>(L.alloc(sizeof(float) * S * L.H));
+        L.ready = static_cast<unsigned*>(L.alloc(sizeof(unsigned) * ((S + 127) / 128 + 1)));
+    }
     const long long gmax = S * std::min<long long>(L.k, W);  // RBD groups per source
     const long long rmax = static_cast<long long>(W) * S;   // RBD groups received
     L.tpe_all = static_cast<int32_t*>(L.alloc(sizeof(int32_t) * W * E));
@@ -539,6 +543,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     XMOE_CUDA(cudaStreamCreateWithFlags(&L.cap_stream, cudaStreamNonBlocking));
     XMOE_CUDA(cudaEventCreateWithFlags(&L.ev_fork, cudaEventDisableTiming));
     XMOE_CUDA(cudaEventCreateWithFlags(&L.ev_join, cudaEventDisableTiming));
+    XMOE_CUDA(cudaEventCreateWithFlags(&L.ev_routed, cudaEventDisableTiming));
     XMOE_CUDA(cudaEventCreate(&L.ev_side0));
     XMOE_CUDA(cudaEventCreate(&L.ev_side1));
     if (L.nchunks > 1) {
@@ -592,6 +597,19 @@ static void exchange_counts(Layer& L, cudaStream_t st) {
     launch_counts_exchange(sg, L.cnt_tab, L.area_ints, w.rank, W, L.flag_tab, w.flags, kSlotCounts, L.epoch, L.peer_err_d, st);
 }
 
+// XMOE_LATE_SHARED=1 (A/B, off by default): one GPU, shared GEMM2 after the
+// routed GEMMs beside a combine into fp32 sums (below).  Bit-identical, but
+// measured slower on B200 (C2 N=1: 1.40-1.54 ms vs 1.23-1.25 ms): the combine
+// must take tokens dynamically and run beside a persistent GEMM that holds
+// most of each SM, so it loses more than the overlap gains.
+static bool late_shared_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("XMOE_LATE_SHARED");
+        return e && std::atoi(e) == 1;
+    }();
+    return on;
+}
+
 // Fused routing (BF16): the gate GEMM's epilogue does softmax + top-k from
 // TMEM and writes per-tile expert histograms; the dropless placement is then
 // one launch (gemm_tc.cu gate_route_kernel, pft.cu route_place_kernel) instead
@@ -607,9 +625,23 @@ static bool fused_route(const Layer& L, long long S) {
 
 static void route_gate(Layer& L, Worker& w, const void* x, long long S, cudaStream_t st) {
     float* lg = reinterpret_cast<float*>(w.logits);
-    if (fused_route(L, S)) {
+    // XMOE_FUSED_GATE=1: softmax + top-k in the gate GEMM's epilogue (one
+    // thread per token row reading TMEM).  Default: gate GEMM + warp-per-token
+    // softmax/top-k writing the tile histograms — measured faster (ncu, C2:
+    // 65 us for the fused kernel, whose serial per-row epilogue runs at one
+    // warp per SM sub-partition, vs ~35 us for the two kernels).
+    static const bool epilogue_gate = [] {
+        const char* e = std::getenv("XMOE_FUSED_GATE");
+        return e && std::atoi(e) == 1;
+    }();
+    if (fused_route(L, S) && epilogue_gate) {
         launch_gate_route(x, static_cast<int>(S), L.H, L.gate, L.E, L.k, L.d.renorm, w.top, w.wts,
                           L.train ? lg : nullptr, w.route_cnt, st);
+        return;
+    }
+    if (fused_route(L, S)) {
+        launch_grouped_gemm_bf16_f32out(x, S, L.H, w.s_rows, 1, L.gate, L.E, lg, 0, st);
+        launch_softmax_topk_f32(lg, S, L.E, L.k, L.d.renorm, w.top, w.wts, st, w.route_cnt);
         return;
     }
     launch_grouped_gemm_bf16_f32out(x, S, L.H, w.s_rows, 1, L.gate, L.E, lg, 0, st);
@@ -853,6 +885,14 @@ void layer_forward_v(Layer& L, const void* x, const long long* Sw, void* out, cu
     const bool rbd = L.d.dispatch_mode == XMOE_DISPATCH_RBD;
     // bf16 rows: token-major permute (x read once) + slot-address combine
     const bool token_major = dt == XMOE_BF16 && (row_bytes & 15) == 0 && k <= 32;
+    // One GPU, plain dispatch, shared experts: shared GEMM1 runs beside the
+    // routing and the permute, shared GEMM2 beside the combine.  The combine
+    // writes fp32 sums of the routed copies and publishes 128-token blocks;
+    // GEMM2's epilogue adds them (out = bf16(sum + bf16(shared))) — the same
+    // arithmetic as the combine's addend, so the output is unchanged bit for
+    // bit — and the combine's HBM traffic hides under GEMM2's tensor work.
+    const bool late_shared = late_shared_on() && L.partial && token_major && !rbd && !dist && nl == 1 &&
+                             L.Fs > 0 && !L.timing && Sw[0] > 0 && H % 64 == 0 && gemm_2cta_enabled(H);
     const char* xb = static_cast<const char*>(x);
     char* ob = static_cast<char*>(out);
     auto x_of = [&](int i) { return xb + static_cast<size_t>(xoff[i]) * row_bytes; };
@@ -912,9 +952,14 @@ void layer_forward_v(Layer& L, const void* x, const long long* Sw, void* out, cu
             return e ? std::atoi(e) : 0;
         }();
         g_gemm_sm_limit = dist ? shared_sms : shared_sms_n1;
-        issue_shared(L.side);
+        if (late_shared) {  // GEMM1 now, GEMM2 after the routed GEMMs (below)
+            Worker& w = L.workers[0];
+            run_gemm(dt, x_of(0), Sw[0], H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, L.side, w.smbits);
+        } else {
+            issue_shared(L.side);
+            XMOE_CUDA(cudaEventRecord(L.ev_join, L.side));
+        }
         g_gemm_sm_limit = 0;
-        XMOE_CUDA(cudaEventRecord(L.ev_join, L.side));
     }
     // 2. padding-free token buffer (pft.cpp:12-60) [+ RBD groups and pilots, rbd.cpp:26-81]
     for (int i = 0; i < nl; ++i) {
@@ -1000,6 +1045,50 @@ void layer_forward_v(Layer& L, const void* x, const long long* Sw, void* out, cu
         run_gemm(dt, w.mid, L.R_max, F, w.rpe, L.El, w2_of(L, w.rank), H, w.eout, 0, st);
     }
     L.mark(kEvGemm, st);
+    if (late_shared) {
+        Worker& w = L.workers[0];
+        // side: shared GEMM2 once the routed GEMMs are done (it must not hold
+        // SMs while they still need them), its epilogue waiting per 128-row
+        // block for the combine below; st: the combine into fp32 sums
+        // the combine goes first: GEMM2's epilogue waits on its ready
+        // counters, so GEMM2 must never occupy SMs the combine cannot share
+        // (launched the other way round it deadlocked on B200: the combine's
+        // CTAs were not co-scheduled beside the persistent GEMM CTAs)
+        XMOE_CUDA(cudaMemsetAsync(L.ready, 0, sizeof(unsigned) * ((Sw[0] + 127) / 128 + 1), st));
+        XMOE_CUDA(cudaEventRecord(L.ev_routed, st));  // routed GEMMs done, counters cleared
+        L.mark(kEvShared, st);
+        L.mark(kEvReturn, st);
+        static const bool gemm_first = [] {  // A/B: enqueue GEMM2 before the combine
+            const char* e = std::getenv("XMOE_LATE_ORDER");
+            return e && std::atoi(e) == 2;
+        }();
+        if (!gemm_first)
+            launch_combine_slots_partial(w.slot_src, w.slot_w, k, H, static_cast<int>(Sw[0]), L.partial, L.ready,
+                                         st);
+        XMOE_CUDA(cudaStreamWaitEvent(L.side, L.ev_routed, 0));
+        // GEMM2 leaves SMs free (XMOE_LATE_GEMM_SMS, default 128 of 148) so
+        // that combine CTAs always run; the combine takes tokens dynamically
+        static const int late_sms = [] {
+            const char* e = std::getenv("XMOE_LATE_GEMM_SMS");
+            return e ? std::max(2, std::atoi(e)) : 128;
+        }();
+        g_gemm_addf = L.partial;
+        g_gemm_ready = L.ready;
+        g_gemm_sm_limit = late_sms;
+        run_gemm(dt, w.smid, Sw[0], L.Fs, w.s_rows, 1, L.sw2, H, o_of(0), 0, L.side);
+        g_gemm_sm_limit = 0;
+        g_gemm_addf = nullptr;
+        g_gemm_ready = nullptr;
+        XMOE_CUDA(cudaEventRecord(L.ev_join, L.side));
+        if (gemm_first)
+            launch_combine_slots_partial(w.slot_src, w.slot_w, k, H, static_cast<int>(Sw[0]), L.partial, L.ready,
+                                         st);
+        XMOE_CUDA(cudaStreamWaitEvent(st, L.ev_join, 0));
+        L.mark(kEvCombine, st);
+        L.last_S = Sw[0];
+        L.bwd_pending = true;
+        return;
+    }
     if (L.Fs > 0) {
         if (L.timing) {
             XMOE_CUDA(cudaEventRecord(L.ev_side0, st));

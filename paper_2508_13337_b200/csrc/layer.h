@@ -115,6 +115,8 @@ struct Layer {
     bool rbd_gather = false;   // RBD GEMM1 gathers replica rows (no expand copy)
     bool ssmb = false;         // sequence-sharded block: experts replicated, MoE local
     bool route_cnt_ok = false; // fused gate + dropless placement available (BF16, E <= 256, k <= 8)
+    float* partial = nullptr;  // [S, H] fp32 routed sums (one GPU, late shared GEMM2)
+    unsigned* ready = nullptr; // [ceil(S/128)] tokens of each block the combine has published
     bool distributed = false;  // one process per GPU, world > 1
     bool p2p = false;          // NVLink peer tables (else NCCL send/recv baseline)
     int32_t* bar = nullptr;    // 4-byte all-reduce used as a cross-rank barrier
@@ -174,6 +176,7 @@ struct Layer {
     cudaStream_t cap_stream = nullptr;
     cudaStream_t side = nullptr;  // shared-expert GEMMs overlap routing + exchange
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_side0 = nullptr, ev_side1 = nullptr;
+    cudaEvent_t ev_routed = nullptr;  // late shared GEMM2: routed GEMMs done, ready counters cleared
     // token-chunked pipeline: C chunks of Rc rows per owner, comm stream for
     // the row movement, per-chunk events and cross-GPU epoch flags
     int nchunks = 1;

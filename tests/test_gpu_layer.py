@@ -489,3 +489,47 @@ def test_bf16_unusual_shapes(W, E, k, H, F, mode, chunks):
             O.rbd_moe_forward(list(x), w, E, k, cap, 2, exact=False)
         for i in range(W):
             assert norm_rel(got[i], want[i]) < 1e-2, (cap, i, norm_rel(got[i], want[i]))
+
+
+@pytest.mark.parametrize("S,H,ns", [(2048, 256, 2), (777, 128, 1), (16384, 2048, 2)])
+def test_late_shared_gemm_bit_identical(S, H, ns):
+    """One GPU with shared experts (XMOE_LATE_SHARED=1, an A/B knob run in a
+    subprocess here): shared GEMM2 runs beside the combine, its epilogue adding
+    the combine's fp32 sums per published 128-token block.  Same arithmetic as
+    the combine's addend: the output equals the in-order path's bit for bit;
+    with the knob off the forward, eager and graph-replayed, equals it too."""
+    from paper_2508_13337_b200 import capi
+    ctx = capi.Context(0, 1, -1)
+    rng = np.random.default_rng(S + H)
+    E, k, F, Fs = 64, 6, 128, 128
+    bf = torch.bfloat16
+    w = O.LayerWeights(grid_gate(rng, H, E), rng.uniform(-0.1, 0.1, (E, H, F)), rng.uniform(-0.1, 0.1, (E, F, H)))
+    sw1, sw2 = rng.uniform(-0.1, 0.1, (ns, H, Fs)), rng.uniform(-0.1, 0.1, (ns, Fs, H))
+    x = dev(grid_tokens(rng, S, H), bf)
+    L = _layer(ctx, capi.BF16, E, H, F, k, S * k, S, w, sw1, sw2)
+    a = [L.forward(x).clone() for _ in range(2)]
+    L.set_graph(True)
+    g = L.forward(x).clone()
+    L.set_graph(False)
+    L.set_timing(True)
+    b = L.forward(x).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b) and torch.equal(a[1], b) and torch.equal(g, b)
+    want = O.moe_layer_with_shared(host(x).astype(np.float64), O.LayerWeights(w.gate, bf16_round(w.w1), bf16_round(w.w2)),
+                                   E, k, S * k, bf16_round(sw1), bf16_round(sw2), exact=False)
+    assert norm_rel(host(b), want) < 1e-2
+
+
+def test_late_shared_knob_subprocess():
+    """XMOE_LATE_SHARED=1 in a fresh process: bit-identical to the default path."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r); import pytest; "
+            "sys.exit(pytest.main(['-q', '-x', '-k', 'late_shared_gemm', %r]))" % (root, os.path.abspath(__file__)))
+    env = dict(os.environ, XMOE_LATE_SHARED="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    print(r.stdout[-2000:], r.stderr[-2000:])
+    assert r.returncode == 0
+
