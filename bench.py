@@ -403,25 +403,55 @@ def main():
     else:
         gate, w1, w2, sw1, sw2, x = configs.device_inputs(ctx, capi, cfg, rank, world, S, rank * S, torch)
     rbd_seed = configs.seeds(capi.salt_seed)["rbd"]
+    auto_mode = args.mode == "auto" and world > 1
     if args.mode == "auto":
-        # measured on B200: the redundancy bypass wins the step
-        # at N=2; from N=4 the chunked plain dispatch, whose all-to-all
-        # overlaps the expert GEMMs, is faster (RBD still moves fewer bytes:
-        # see dispatch_compare)
-        args.mode = "rbd" if world == 2 else "naive"
+        args.mode = "naive"  # N=1: no exchange; N>1: probed below
     mode = capi.RBD if args.mode == "rbd" else capi.NAIVE
     S_max = S_seq - (world - 1) * (S_seq // world) if ssmb else S
 
-    def make_layer(chunks=args.chunks, train=False, md=None):
+    def make_layer(chunks=None, train=False, md=None):
+        chunks = args.chunks if chunks is None else chunks
         return capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S_max * k,
                           max_tokens=S_max, dtype=capi.BF16, gate=gate, w1=w1, w2=w2, sw1=sw1, sw2=sw2,
                           dispatch_mode=mode if md is None else md, seed=rbd_seed, chunks=chunks, train=train)
 
+    out = torch.empty_like(x_full if ssmb else x)
+    xin = x_full if ssmb else x
+    auto_probe = None
+    if auto_mode:
+        # Dispatch auto-selection, measured on this box before the timed region
+        # (the same warm-up budget for both): the chunked plain dispatch hides
+        # its larger all-to-all under the expert GEMMs; the redundancy bypass
+        # moves 25-67 % fewer bytes.  Which wins depends on the link speed of
+        # the box (B200 measurements in DESIGN.md §8 go either way at N=4), so
+        # the faster one, max over ranks, is kept.
+        auto_probe = {}
+        for name, md, ch in (("naive", capi.NAIVE, args.chunks), ("rbd", capi.RBD, args.chunks or 2)):
+            pl = make_layer(chunks=ch, md=md)
+            if not args.no_graph:
+                pl.set_graph(True)
+            for _ in range(3):
+                (pl.ssmb_forward(xin, out) if ssmb else pl.forward(xin, out))
+            torch.cuda.synchronize()
+            dist.barrier()
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record()
+            for _ in range(10):
+                (pl.ssmb_forward(xin, out) if ssmb else pl.forward(xin, out))
+            p1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([p0.elapsed_time(p1) / 10], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            auto_probe[name] = {"ms": float(t.item()), "chunks": pl.chunks()}
+            dist.barrier()
+            del pl
+        args.mode = min(auto_probe, key=lambda n: auto_probe[n]["ms"])
+        mode = capi.RBD if args.mode == "rbd" else capi.NAIVE
+        if args.mode == "rbd" and not args.chunks:
+            args.chunks = auto_probe["rbd"]["chunks"]
     layer = make_layer()
     if not args.no_graph:
         layer.set_graph(True)
-    out = torch.empty_like(x_full if ssmb else x)
-    xin = x_full if ssmb else x
 
     def step(lyr, xi, oi):  # one pass of the hot path (SSMB: shard forward + all-gather)
         if ssmb:
@@ -652,7 +682,8 @@ def main():
             "config": {"workload": cfg["desc"], "config": args.config,
                        "tokens_per_gpu": S, "global_tokens": tokens_step,
                        "parallelism": (f"ssmb{world}+ep{world}" if ssmb else f"ep{world}"),
-                       "dispatch": args.mode, "pass": "forward", "chunks": layer.chunks(),
+                       "dispatch": args.mode, "dispatch_probe": auto_probe, "pass": "forward",
+                       "chunks": layer.chunks(),
                        "transport": (os.environ.get("XMOE_TRANSPORT") or "p2p") if world > 1 else "local",
                        "l2": f"working set > L2: {wbytes / 1e9:.2f} GB of expert weights per GPU + "
                              f"{S * H * 2 / 1e6:.0f} MB tokens stream each step (126 MB L2)"},
