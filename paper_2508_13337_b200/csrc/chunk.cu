@@ -86,14 +86,120 @@ __global__ void dispatch_dest_chunked_kernel(const int32_t* __restrict__ expert_
                                              const int32_t* __restrict__ B_dev, int S, int C, int E, int El,
                                              const int32_t* __restrict__ seg, const int32_t* __restrict__ pfx_c,
                                              const int32_t* __restrict__ base, int32_t* __restrict__ dest_rank,
-                                             int32_t* __restrict__ dest_row) {
+                                             int32_t* __restrict__ dest_row, int32_t* const* __restrict__ rsrc_tab,
+                                             int me) {
     const int B = *B_dev;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < B; r += gridDim.x * blockDim.x) {
         const int e = expert_ids[r];
-        const int c = chunk_of(token_ids[r], S, C);
-        dest_rank[r] = e / El;
-        dest_row[r] = base[c * E + e] + (r - seg[e]) - pfx_c[c * E + e];
+        const int t = token_ids[r];
+        const int c = chunk_of(t, S, C);
+        const int d = e / El;
+        const int row = base[c * E + e] + (r - seg[e]) - pfx_c[c * E + e];
+        dest_rank[r] = d;
+        dest_row[r] = row;
+        // pull dispatch: tell the owner which (source, token) fills that row
+        if (rsrc_tab) rsrc_tab[d][row] = (me << 24) | t;
     }
+}
+
+// Pull dispatch, per token: where the combine reads each kept copy's expert
+// output (the owner's eout row) and the copy's weight.
+__global__ void slot_addrs_kernel(const int32_t* __restrict__ slot_pos, int n, const int32_t* __restrict__ dest_rank,
+                                  const int32_t* __restrict__ dest_row, const double* __restrict__ cw,
+                                  char* const* __restrict__ eout_tab, int row_bytes,
+                                  unsigned long long* __restrict__ slot_src, float* __restrict__ slot_w) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int p = slot_pos[i];
+        unsigned long long a = 0;
+        float wv = 0.f;
+        if (p >= 0) {
+            a = reinterpret_cast<unsigned long long>(eout_tab[dest_rank[p]] +
+                                                     static_cast<size_t>(dest_row[p]) * row_bytes);
+            wv = static_cast<float>(cw[p]);
+        }
+        slot_src[i] = a;
+        slot_w[i] = wv;
+    }
+}
+
+// Pull dispatch, owner side: one warp per grouped row of chunk region c
+// copies the token row from its source's staged input (xs_tab[source], a
+// peer address over NVLink for other ranks) into the owner's grouped buffer.
+// Reading peers instead of storing to them keeps the NVLink traffic from
+// stalling the expert GEMMs that share the SMs (B200, 2 GPUs: a GEMM beside
+// an SM-driven peer store stream runs 1.2-1.8x slower, beside peer loads
+// 1.07x).  rows = sum of the region's per-expert counts.
+constexpr int kPullWarps = 8;
+constexpr int kPullVec = 8;  // int4 per lane in flight (4 KB rows in one pass)
+__global__ void __launch_bounds__(1024) pull_rows_kernel(const int32_t* __restrict__ rsrc,
+                                                                    const int32_t* __restrict__ rpe, int El,
+                                                                    char* const* __restrict__ xs_tab, int row_bytes,
+                                                                    char* __restrict__ recv) {
+    __shared__ int s_rows;
+    if (threadIdx.x < 32) {
+        int v = 0;
+        for (int i = threadIdx.x; i < El; i += 32) v += rpe[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) s_rows = v;
+    }
+    __syncthreads();
+    const int rows = s_rows;
+    const int lane = threadIdx.x & 31;
+    const int nvec = row_bytes >> 4;
+    const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    for (long long r = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarps) {
+        const unsigned e = static_cast<unsigned>(__ldg(rsrc + r));
+        const int4* src = reinterpret_cast<const int4*>(xs_tab[e >> 24] + static_cast<size_t>(e & 0xFFFFFFu) * row_bytes);
+        int4* dst = reinterpret_cast<int4*>(recv + static_cast<size_t>(r) * row_bytes);
+        for (int base = 0; base < nvec; base += 32 * kPullVec) {
+            int4 v[kPullVec];
+#pragma unroll
+            for (int u = 0; u < kPullVec; ++u) {
+                const int c = base + lane + 32 * u;
+                v[u] = c < nvec ? ld_nc_v4(src + c) : make_int4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < kPullVec; ++u) {
+                const int c = base + lane + 32 * u;
+                if (c < nvec) st_na_v4(dst + c, v[u]);
+            }
+        }
+    }
+}
+
+void launch_slot_addrs(const int32_t* slot_pos, long long n, const int32_t* dest_rank, const int32_t* dest_row,
+                       const double* cw, char* const* eout_tab, int row_bytes, unsigned long long* slot_src,
+                       float* slot_w, cudaStream_t st) {
+    if (n <= 0) return;
+    const long long blocks = (n + 255) / 256;
+    slot_addrs_kernel<<<static_cast<int>(blocks < 4 * kNumSMs ? blocks : 4 * kNumSMs), 256, 0, st>>>(
+        slot_pos, static_cast<int>(n), dest_rank, dest_row, cw, eout_tab, row_bytes, slot_src, slot_w);
+    XMOE_LAUNCH_CHECK();
+}
+
+void launch_pull_rows(const int32_t* rsrc, const int32_t* rpe, int El, char* const* xs_tab, int row_bytes,
+                      long long max_rows, void* recv, cudaStream_t st) {
+    require(row_bytes % 16 == 0, XMOE_ERR_VALIDATION, "pull dispatch needs 16-byte rows");
+    if (max_rows <= 0) return;
+    if (g_copy_fat > 0) {  // one 1024-thread block per SM (the shared reservation keeps others off it)
+        constexpr int kFatSmem = 120 * 1024;
+        static bool attr = false;
+        if (!attr) {
+            XMOE_CUDA(cudaFuncSetAttribute(pull_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFatSmem));
+            attr = true;
+        }
+        pull_rows_kernel<<<g_copy_fat, 1024, kFatSmem, st>>>(rsrc, rpe, El, xs_tab, row_bytes,
+                                                            static_cast<char*>(recv));
+        XMOE_LAUNCH_CHECK();
+        return;
+    }
+    long long blocks = (max_rows + kPullWarps - 1) / kPullWarps;
+    const long long cap = g_copy_blocks > 0 ? g_copy_blocks : 4 * kNumSMs;
+    if (blocks > cap) blocks = cap;
+    pull_rows_kernel<<<static_cast<int>(blocks), 32 * kPullWarps, 0, st>>>(rsrc, rpe, El, xs_tab, row_bytes,
+                                                                          static_cast<char*>(recv));
+    XMOE_LAUNCH_CHECK();
 }
 
 // Peer-flag wait with a bounded spin.  A peer that never arrives (rank
@@ -241,11 +347,11 @@ void launch_chunk_bases(const int32_t* T, int W, int C, int E, int me, int Rc, i
 void launch_dispatch_dest_chunked(const int32_t* expert_ids, const int32_t* token_ids, const int32_t* B_dev,
                                   long long max_rows, int S, int C, int E, int El, const int32_t* seg,
                                   const int32_t* pfx_c, const int32_t* base, int32_t* dest_rank,
-                                  int32_t* dest_row, cudaStream_t st) {
+                                  int32_t* dest_row, cudaStream_t st, int32_t* const* rsrc_tab, int me) {
     const long long blocks = (max_rows + 255) / 256;
     dispatch_dest_chunked_kernel<<<static_cast<int>(blocks < 4 * kNumSMs ? (blocks > 0 ? blocks : 1) : 4 * kNumSMs),
                                    256, 0, st>>>(expert_ids, token_ids, B_dev, S, C, E, El, seg, pfx_c, base,
-                                                 dest_rank, dest_row);
+                                                 dest_rank, dest_row, rsrc_tab, me);
     XMOE_LAUNCH_CHECK();
 }
 

@@ -175,7 +175,8 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_bf16_kernel(
 // scatter): lane j loads copy j's expert-output address and weight — the only
 // dependent load before the rows stream.  One warp per (token, 512-column
 // segment); rows may live in a peer GPU's memory (NVLink loads).
-__global__ void __launch_bounds__(32 * kCombWarps) combine_slots_bf16_kernel(
+template <int kWarps>
+__global__ void __launch_bounds__(32 * kWarps) combine_slots_bf16_kernel(
     const unsigned long long* __restrict__ slot_src, const float* __restrict__ slot_w, int k, int H, int S,
     const __nv_bfloat16* __restrict__ addend, __nv_bfloat16* __restrict__ out, long long src_delta,
     const __nv_bfloat16* __restrict__ addend2) {
@@ -418,9 +419,16 @@ void launch_combine_slots(const unsigned long long* slot_src, const float* slot_
         return;
     }
     const long long warps = static_cast<long long>(S) * ((H + kSegCols - 1) / kSegCols);
+    if (g_copy_fat > 0) {  // whole-SM blocks: 16 warps x 128 registers fill an SM's register file
+        combine_slots_bf16_kernel<16><<<g_copy_fat, 32 * 16, 0, st>>>(
+            slot_src, slot_w, k, H, S, static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out),
+            src_delta, static_cast<const __nv_bfloat16*>(addend2));
+        XMOE_LAUNCH_CHECK();
+        return;
+    }
     long long blocks = ceil_div(warps, kCombWarps);
     if (g_copy_blocks > 0 && blocks > g_copy_blocks) blocks = g_copy_blocks;
-    combine_slots_bf16_kernel<<<static_cast<int>(blocks), 32 * kCombWarps, g_copy_smem, st>>>(
+    combine_slots_bf16_kernel<kCombWarps><<<static_cast<int>(blocks), 32 * kCombWarps, g_copy_smem, st>>>(
         slot_src, slot_w, k, H, S, static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out),
         src_delta, static_cast<const __nv_bfloat16*>(addend2));
     XMOE_LAUNCH_CHECK();

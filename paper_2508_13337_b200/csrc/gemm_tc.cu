@@ -1709,6 +1709,11 @@ static void launch_tc2(const void* A, long long a_rows, long long a_cols, const 
     XMOE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     long long cap_pairs = sms / 2;
     if (g_gemm_sm_limit > 0 && g_gemm_sm_limit / 2 < cap_pairs) cap_pairs = g_gemm_sm_limit / 2;
+    static const int env_sms = [] {  // XMOE_GEMM_SMS: cap on every 2-CTA GEMM grid (A/B, SM partitions)
+        const char* e = std::getenv("XMOE_GEMM_SMS");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (env_sms > 0 && env_sms / 2 < cap_pairs) cap_pairs = env_sms / 2;
     const long long pairs = tile_bound < cap_pairs ? tile_bound : cap_pairs;
     tc2::grouped_gemm_tc2_kernel<OutT, kVarK><<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
         ta, tb, group_sizes, G, M, N, K, D, relu, mbits_in, mbits_out,

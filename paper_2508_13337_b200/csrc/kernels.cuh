@@ -140,6 +140,12 @@ extern thread_local int g_copy_blocks;
 // dynamic shared memory the row-movement kernels reserve (unused): large
 // enough, it keeps them off SMs that hold a GEMM CTA (SM partition)
 extern thread_local int g_copy_smem;
+// SM partition of the chunked forward (XMOE_COMM_SMS): when > 0 the row
+// pulls and combines that run beside the expert GEMMs launch as this many
+// whole-SM blocks (one per SM: 1024 threads + a large shared reservation, or
+// the full register file), and the GEMMs take the remaining SMs, so the row
+// traffic never shares an SM with a GEMM CTA.
+extern thread_local int g_copy_fat;
 
 // misc.cu
 void launch_recv_counts(const int32_t* tpe_all, int W, int E, int dst, int32_t* rpe,
@@ -159,7 +165,14 @@ void launch_chunk_bases(const int32_t* T, int W, int C, int E, int me, int Rc, i
 void launch_dispatch_dest_chunked(const int32_t* expert_ids, const int32_t* token_ids, const int32_t* B_dev,
                                   long long max_rows, int S, int C, int E, int El, const int32_t* seg,
                                   const int32_t* pfx_c, const int32_t* base, int32_t* dest_rank,
-                                  int32_t* dest_row, cudaStream_t st);
+                                  int32_t* dest_row, cudaStream_t st,
+                                  int32_t* const* rsrc_tab = nullptr, int me = 0);
+// pull dispatch (chunk.cu): combine addresses per token slot; owner-side row pull
+void launch_slot_addrs(const int32_t* slot_pos, long long n, const int32_t* dest_rank, const int32_t* dest_row,
+                       const double* cw, char* const* eout_tab, int row_bytes, unsigned long long* slot_src,
+                       float* slot_w, cudaStream_t st);
+void launch_pull_rows(const int32_t* rsrc, const int32_t* rpe, int El, char* const* xs_tab, int row_bytes,
+                      long long max_rows, void* recv, cudaStream_t st);
 void launch_forward_begin(int32_t* s_rows, int S, unsigned* epoch, cudaStream_t st);
 void launch_flag_signal(unsigned* const* flag_tab, int W, int me, int slot, const unsigned* epoch,
                         cudaStream_t st);

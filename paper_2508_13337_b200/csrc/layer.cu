@@ -277,6 +277,14 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
             L.R_max = std::max<long long>(L.R_max, static_cast<long long>(L.Rc) * L.nchunks);
         }
     }
+    // pull dispatch (default on the chunked plain path; XMOE_DISPATCH=push
+    // keeps the source-side stores, A/B)
+    {
+        const char* e = std::getenv("XMOE_DISPATCH");
+        L.pull = L.nchunks > 1 && !rbd && !(e && std::string(e) == "push");
+        require(!L.pull || (S < (1LL << 24) && W <= 255), XMOE_ERR_VALIDATION,
+                "pull dispatch: max_tokens < 2^24 and world <= 255");
+    }
     L.route_cnt_ok = bf && gate_route_supported(L.E, L.k, L.H);
     if (bf && !L.distributed && L.nl == 1 && L.Fs > 0 && !L.ssmb) {  // late shared GEMM2 (layer_forward_v)
         L.partial = static_cast<float*>(L.alloc(sizeof(float) * S * L.H));
@@ -306,7 +314,9 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     const size_t off_gw = off_dxc + (L.train ? up(static_cast<size_t>(L.R_max) * H * es) : 0);
     const size_t off_gsrc = off_gw + (L.train ? up(sizeof(float) * L.R_max) : 0);
     const size_t off_sdw = off_gsrc + (L.train ? up(sizeof(unsigned long long) * L.R_max) : 0);
-    const size_t off_flags = off_sdw + (L.train ? up(sizeof(float) * nk) : 0);
+    const size_t off_xs = off_sdw + (L.train ? up(sizeof(float) * nk) : 0);
+    const size_t off_rsrc = off_xs + (L.pull ? up(static_cast<size_t>(S) * H * es) : 0);
+    const size_t off_flags = off_rsrc + (L.pull ? up(sizeof(int32_t) * L.R_max) : 0);
     const size_t flag_bytes = sizeof(unsigned) * kFlagSlots * W;
     // count all-gather area (double-buffered): tpe [W,E] | tpe_c [W,C,E] | G [W,W] | gd [W,2,W,C]
     L.area_ints = W * E + W * L.nchunks * E + W * W + 2 * W * W * L.nchunks;
@@ -316,7 +326,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     L.off_dxc = static_cast<long long>(off_dxc);
     L.workers.resize(L.nl);
     std::vector<char*> t_recv(W), t_eout(W), t_recv_u(W), t_desc(W), t_back(W);
-    std::vector<char*> t_dyg(W), t_dxc(W), t_gw(W), t_gsrc(W), t_sdw(W), t_flags(W), t_counts(W);
+    std::vector<char*> t_dyg(W), t_dxc(W), t_gw(W), t_gsrc(W), t_sdw(W), t_flags(W), t_counts(W), t_xs(W), t_rsrc(W);
     for (int i = 0; i < L.nl; ++i) {
         Worker& w = L.workers[i];
         w.rank = ssmb ? 0 : ctx.rank_of(i);
@@ -352,6 +362,10 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         }
         w.recv = w.sym + off_recv;
         w.eout = w.sym + off_eout;
+        if (L.pull) {
+            w.xs = w.sym + off_xs;
+            w.rsrc = reinterpret_cast<int32_t*>(w.sym + off_rsrc);
+        }
         w.mid = L.alloc(static_cast<size_t>(L.R_max) * F * es);
         if (L.distributed && !L.p2p) {
             w.send = L.alloc(static_cast<size_t>(nk) * H * es);
@@ -456,6 +470,8 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         t_recv_u[w.rank] = static_cast<char*>(w.recv_u);
         t_desc[w.rank] = reinterpret_cast<char*>(w.desc_recv);
         t_back[w.rank] = static_cast<char*>(w.back_u);
+        t_xs[w.rank] = w.xs;
+        t_rsrc[w.rank] = reinterpret_cast<char*>(w.rsrc);
     }
     if (L.distributed && L.p2p) {
         // export my symmetric region, import every peer's (CUDA IPC over NVLink)
@@ -486,6 +502,8 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
             t_back[r] = b + off_back;
             t_flags[r] = b + off_flags;
             t_counts[r] = b + off_counts;
+            t_xs[r] = b + off_xs;
+            t_rsrc[r] = b + off_rsrc;
         }
     }
     auto table = [&](const std::vector<char*>& v) {
@@ -502,6 +520,10 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     L.epoch = static_cast<unsigned*>(L.alloc(sizeof(unsigned)));
     XMOE_CUDA(cudaMemset(L.epoch, 0, sizeof(unsigned)));
     L.eout_tab = table(t_eout);
+    if (L.pull) {
+        L.xs_tab = table(t_xs);
+        L.rsrc_tab = reinterpret_cast<int32_t**>(table(t_rsrc));
+    }
     if (L.train) {
         L.dyg_tab = table(t_dyg);
         L.dxc_tab = table(t_dxc);
@@ -701,16 +723,56 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
         return e ? std::atoi(e) : 0;
     }();
     const int copy_smem = part_sms > 0 ? 32 * 1024 : 0;
+    // SM partition (pull dispatch): XMOE_COMM_SMS whole SMs move rows, the
+    // GEMMs take the rest (measured on B200: a chunk GEMM beside SM-driven
+    // row copies on shared SMs runs 1.5x slower; on 124 SMs beside 24 copy
+    // SMs, 1.07-1.17x, the copies at 460-660 GB/s)
+    static const int comm_sms_env = [] {
+        const char* e = std::getenv("XMOE_COMM_SMS");
+        return e ? std::max(0, std::min(kNumSMs / 2, std::atoi(e))) : 24;
+    }();
+    const int comm_sms = L.pull ? comm_sms_env : 0;
+    const int gemm_sms = comm_sms > 0 ? kNumSMs - comm_sms : part_sms;
     auto slot_A = [](int c) { return c; };
     auto slot_B = [](int c) { return kMaxChunks + c; };
 
+    // XMOE_CHUNK_SHARED=side (A/B): the shared-expert GEMMs on the side
+    // stream (SM-limited, XMOE_SHARED_SMS) beside the routed chunks instead of
+    // ahead of them on st; the first combine waits for them
+    static const bool shared_side = [] {
+        const char* e = std::getenv("XMOE_CHUNK_SHARED");
+        return e && std::string(e) == "side";
+    }();
+    const bool sh_side = shared_side && L.Fs > 0;
     L.mark(kEvStart, st);
     for (int i = 0; i < nl; ++i)
         launch_forward_begin(L.workers[i].s_rows, static_cast<int>(S), i == 0 ? L.epoch : nullptr, st);
+    if (sh_side) {
+        XMOE_CUDA(cudaEventRecord(L.ev_fork, st));
+        XMOE_CUDA(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
+        if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side0, L.side));
+        static const int shared_sms = [] {
+            const char* e = std::getenv("XMOE_SHARED_SMS");
+            return e ? std::atoi(e) : 104;
+        }();
+        g_gemm_sm_limit = shared_sms;
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            launch_grouped_gemm_bf16(x_of(i), S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, L.side);
+            launch_grouped_gemm_bf16(w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, w.sout, 0, L.side);
+        }
+        g_gemm_sm_limit = 0;
+        if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side1, L.side));
+        XMOE_CUDA(cudaEventRecord(L.ev_join, L.side));
+    }
     for (int i = 0; i < nl; ++i) route_gate(L, L.workers[i], x_of(i), S, st);  // 1. gate (gating.cpp:14-57)
     L.mark(kEvGate, st);
     XMOE_CUDA(cudaEventRecord(L.ev_fork, st));
     XMOE_CUDA(cudaStreamWaitEvent(cm, L.ev_fork, 0));
+    if (L.pull)  // stage the input where the owners can read it (peers finished reading the last one)
+        for (int i = 0; i < nl; ++i)
+            XMOE_CUDA(cudaMemcpyAsync(L.workers[i].xs, x_of(i), static_cast<size_t>(S) * rb, cudaMemcpyDeviceToDevice,
+                                      cm));
     // 2. comm stream: PFT (pft.cpp:12-60), chunk counts, count all-gather,
     //    destinations, then every chunk's rows
     for (int i = 0; i < nl; ++i) {
@@ -732,11 +794,41 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
         Worker& w = L.workers[i];
         launch_chunk_bases(L.tpe_c_all, W, C, E, w.rank, L.Rc, w.cbase, w.rpe_c, cm);
         launch_dispatch_dest_chunked(w.expert_ids, w.token_ids, w.B_dev, nk, static_cast<int>(S), C, E, El, w.seg,
-                                     w.pfx_c, w.cbase, w.dest_rank, w.dest_row, cm);
+                                     w.pfx_c, w.cbase, w.dest_rank, w.dest_row, cm, L.pull ? L.rsrc_tab : nullptr,
+                                     w.rank);
+        if (L.pull)
+            launch_slot_addrs(w.slot_pos, nk, w.dest_rank, w.dest_row, w.cw, L.eout_tab, static_cast<int>(rb),
+                              w.slot_src, w.slot_w, cm);
         if (rbd) launch_rbd_offsets(L.gd_all, W, w.rank, w.rbd, cm);
     }
     g_copy_smem = copy_smem;
-    for (int c = 0; c < C; ++c) {
+    if (L.pull) {
+        // every source's row table and staged input complete, then each
+        // chunk region is pulled (chunk 0 on the full grid, later chunks on
+        // XMOE_PULL_BLOCKS blocks beside the GEMMs)
+        static const int blk_pull = [] {
+            const char* e = std::getenv("XMOE_PULL_BLOCKS");
+            return e ? std::max(1, std::atoi(e)) : kNumSMs;
+        }();
+        if (dist) {
+            launch_flag_signal(L.flag_tab, W, me, slot_A(0), L.epoch, cm);
+            launch_flag_wait(L.workers[0].flags, W, slot_A(0), L.epoch, L.peer_err_d, cm);
+        }
+        g_copy_fat = comm_sms;
+        for (int c = 0; c < C; ++c) {
+            g_copy_blocks = c == 0 ? 0 : blk_pull;
+            for (int i = 0; i < nl; ++i) {
+                Worker& w = L.workers[i];
+                const size_t r0 = static_cast<size_t>(c) * L.Rc;
+                launch_pull_rows(w.rsrc + r0, w.rpe_c + c * El, El, L.xs_tab, static_cast<int>(rb), L.Rc,
+                                 static_cast<char*>(w.recv) + r0 * rb, cm);
+            }
+            if (L.timing) XMOE_CUDA(cudaEventRecord(L.tl[4 * c], cm));
+            XMOE_CUDA(cudaEventRecord(L.evA[c], cm));
+        }
+        g_copy_fat = 0;
+    }
+    for (int c = 0; c < C && !L.pull; ++c) {
         // chunk 0 gates the first expert GEMM: full grid; later chunks run
         // beside the GEMMs on a bounded grid
         g_copy_blocks = c == 0 ? 0 : blk_scatter;
@@ -764,9 +856,9 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     L.mark(kEvDispatch, cm);
     // 3. st: shared experts (x only), then the routed experts chunk by chunk
     //    (pf_pipeline.cpp:83-105)
-    if (L.Fs > 0) {
+    if (L.Fs > 0 && !sh_side) {
         if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side0, st));
-        g_gemm_sm_limit = part_sms;
+        g_gemm_sm_limit = gemm_sms;
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             launch_grouped_gemm_bf16(x_of(i), S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, st);
@@ -777,11 +869,11 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     }
     for (int c = 0; c < C; ++c) {
         XMOE_CUDA(cudaStreamWaitEvent(st, L.evA[c], 0));
-        if (dist) launch_flag_wait(L.workers[0].flags, W, slot_A(c), L.epoch, L.peer_err_d, st);
+        if (dist && !L.pull) launch_flag_wait(L.workers[0].flags, W, slot_A(c), L.epoch, L.peer_err_d, st);
         if (L.timing) XMOE_CUDA(cudaEventRecord(L.tl[4 * c + 1], st));
         const size_t r0 = static_cast<size_t>(c) * L.Rc;
         g_copy_blocks = 0;
-        g_gemm_sm_limit = part_sms;
+        g_gemm_sm_limit = gemm_sms;
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             if (rbd)  // replicas read (gather) or copy the row from their pilot's slot
@@ -808,8 +900,10 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     L.mark(kEvShared, st);
     // 4. comm: each chunk's weighted combine as soon as every owner finished
     //    it (pf_pipeline.cpp:107-135)
+    if (sh_side) XMOE_CUDA(cudaStreamWaitEvent(cm, L.ev_join, 0));
     for (int c = 0; c < C; ++c) {
         g_copy_blocks = c == C - 1 ? 0 : blk_combine;  // the last combine runs alone
+        g_copy_fat = c == C - 1 ? 0 : comm_sms;
         XMOE_CUDA(cudaStreamWaitEvent(cm, L.evB[c], 0));
         if (dist) launch_flag_wait(L.workers[0].flags, W, slot_B(c), L.epoch, L.peer_err_d, cm);
         if (c == C - 1) L.mark(kEvReturn, cm);
@@ -830,6 +924,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     }
     g_copy_blocks = 0;
     g_copy_smem = 0;
+    g_copy_fat = 0;
     XMOE_CUDA(cudaEventRecord(L.ev_done, cm));
     XMOE_CUDA(cudaStreamWaitEvent(st, L.ev_done, 0));
     L.mark(kEvCombine, st);
@@ -845,6 +940,7 @@ void layer_forward(Layer& L, const void* x, long long S, void* out, cudaStream_t
     L.last_ssmb = false;
     g_copy_blocks = 0;  // launch-shaping globals start clean even after an aborted forward
     g_copy_smem = 0;
+    g_copy_fat = 0;
     g_gemm_sm_limit = 0;
     // A distributed layer takes the same path on every rank whatever its own
     // S: the chunked and unchunked forwards use different peer-flag slots, so

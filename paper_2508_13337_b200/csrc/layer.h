@@ -56,6 +56,8 @@ struct Worker {
     unsigned long long* slot_src = nullptr;  // [S*k] address of each copy's expert output
     float* slot_w = nullptr;                 // [S*k] its combine weight
     char* sym = nullptr;          // symmetric region: recv | eout | recv_u | desc_recv | back_u
+    char* xs = nullptr;           // pull dispatch: staged input [S_max, H] (symmetric region)
+    int32_t* rsrc = nullptr;      // pull dispatch: (source << 24 | token) of every grouped row
     // redundancy-bypassing dispatch (rbd.cu)
     RbdWork rbd{};
     void* recv_u = nullptr;       // [W*S, H] unique rows received from every source
@@ -132,6 +134,11 @@ struct Layer {
     void* sw2 = nullptr;   // F64 [Fs,H]; BF16 [H,Fs]
     int32_t* tpe_all = nullptr;  // [W, E]
     char** recv_tab = nullptr;   // device table: rank -> recv buffer (shared-device ranks)
+    // pull dispatch (chunked plain dispatch): owners copy their rows from the
+    // sources' staged inputs instead of the sources storing into the owners
+    bool pull = false;
+    char** xs_tab = nullptr;      // rank -> staged input [S_max, H] (symmetric region)
+    int32_t** rsrc_tab = nullptr; // rank -> [R_max] (source << 24 | token) of every grouped row
     char** eout_tab = nullptr;
     // training tables and weights in the reference layouts (dgrad B operands)
     bool train = false;

@@ -16,6 +16,7 @@ namespace xmoe {
 
 thread_local int g_copy_blocks = 0;
 thread_local int g_copy_smem = 0;
+thread_local int g_copy_fat = 0;
 
 constexpr int kRowWarps = 8;
 constexpr int kUnroll = 8;
