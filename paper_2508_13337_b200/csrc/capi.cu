@@ -9,6 +9,7 @@
 // rbd_moe_forward (rbd.cpp:360-386) and ssmb_forward (ssmb.cpp:12-46).
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -27,6 +28,23 @@ namespace xmoe {
 
 thread_local std::string g_last_error;
 std::atomic<unsigned long long> g_kernel_launches{0};
+
+bool sync_check_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("XMOE_SYNC_CHECK");
+        return e && std::atoi(e) == 1;
+    }();
+    return on;
+}
+
+void sync_check(const char* file, int line) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(cudaStreamLegacy, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) return;
+    const cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess)
+        fail(XMOE_ERR_CUDA, std::string("kernel launched at ") + file + ":" + std::to_string(line) + ": " +
+                                cudaGetErrorString(e));
+}
 
 #define XMOE_NCCL(expr)                                                                \
     do {                                                                               \

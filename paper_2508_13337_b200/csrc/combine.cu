@@ -175,11 +175,16 @@ __global__ void __launch_bounds__(32 * kCombWarps) combine_bf16_kernel(
 // scatter): lane j loads copy j's expert-output address and weight — the only
 // dependent load before the rows stream.  One warp per (token, 512-column
 // segment); rows may live in a peer GPU's memory (NVLink loads).
+// partial mode (partial != null): the fp32 sums of the routed copies go to
+// partial [S, H] and every (token, segment) item adds 1 to its 128-token
+// block's counter ready[(t_base + t) / 128] (release) — the shared-expert
+// GEMM2 epilogue finishes the rows (layer.cu, chunked forward).
 template <int kWarps>
 __global__ void __launch_bounds__(32 * kWarps) combine_slots_bf16_kernel(
     const unsigned long long* __restrict__ slot_src, const float* __restrict__ slot_w, int k, int H, int S,
     const __nv_bfloat16* __restrict__ addend, __nv_bfloat16* __restrict__ out, long long src_delta,
-    const __nv_bfloat16* __restrict__ addend2) {
+    const __nv_bfloat16* __restrict__ addend2, float* __restrict__ partial, unsigned* __restrict__ ready,
+    int t_base) {
     const int nseg = (H + kSegCols - 1) / kSegCols;
     const int lane = threadIdx.x & 31;
     const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
@@ -243,6 +248,22 @@ __global__ void __launch_bounds__(32 * kWarps) combine_slots_bf16_kernel(
                 }
             }
         }
+    }
+    if (partial) {
+        float4* pd = reinterpret_cast<float4*>(partial + static_cast<size_t>(t) * H);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = h ? c1 : c0;
+            if (!(h ? v1 : v0)) continue;
+            pd[2 * c] = make_float4(acc[8 * h + 0], acc[8 * h + 1], acc[8 * h + 2], acc[8 * h + 3]);
+            pd[2 * c + 1] = make_float4(acc[8 * h + 4], acc[8 * h + 5], acc[8 * h + 6], acc[8 * h + 7]);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicAdd(ready + ((t_base + t) >> 7), 1u);
+        }
+        continue;
     }
     int4* dst = reinterpret_cast<int4*>(out + static_cast<size_t>(t) * H);
 #pragma unroll
@@ -422,7 +443,7 @@ void launch_combine_slots(const unsigned long long* slot_src, const float* slot_
     if (g_copy_fat > 0) {  // whole-SM blocks: 16 warps x 128 registers fill an SM's register file
         combine_slots_bf16_kernel<16><<<g_copy_fat, 32 * 16, 0, st>>>(
             slot_src, slot_w, k, H, S, static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out),
-            src_delta, static_cast<const __nv_bfloat16*>(addend2));
+            src_delta, static_cast<const __nv_bfloat16*>(addend2), nullptr, nullptr, 0);
         XMOE_LAUNCH_CHECK();
         return;
     }
@@ -430,7 +451,27 @@ void launch_combine_slots(const unsigned long long* slot_src, const float* slot_
     if (g_copy_blocks > 0 && blocks > g_copy_blocks) blocks = g_copy_blocks;
     combine_slots_bf16_kernel<kCombWarps><<<static_cast<int>(blocks), 32 * kCombWarps, g_copy_smem, st>>>(
         slot_src, slot_w, k, H, S, static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out),
-        src_delta, static_cast<const __nv_bfloat16*>(addend2));
+        src_delta, static_cast<const __nv_bfloat16*>(addend2), nullptr, nullptr, 0);
+    XMOE_LAUNCH_CHECK();
+}
+
+int combine_segments(int H) { return (H + kSegCols - 1) / kSegCols; }
+
+void launch_combine_slots_seg_partial(const unsigned long long* slot_src, const float* slot_w, int k, int H, int S,
+                                      float* partial, unsigned* ready, int t_base, cudaStream_t st) {
+    if (S == 0) return;
+    require(H % 8 == 0 && k <= 32, XMOE_ERR_VALIDATION, "slot combine needs model_dim % 8 == 0, k <= 32");
+    if (g_copy_fat > 0) {
+        combine_slots_bf16_kernel<16><<<g_copy_fat, 32 * 16, 0, st>>>(slot_src, slot_w, k, H, S, nullptr, nullptr, 0,
+                                                                      nullptr, partial, ready, t_base);
+        XMOE_LAUNCH_CHECK();
+        return;
+    }
+    const long long warps = static_cast<long long>(S) * combine_segments(H);
+    long long blocks = ceil_div(warps, kCombWarps);
+    if (g_copy_blocks > 0 && blocks > g_copy_blocks) blocks = g_copy_blocks;
+    combine_slots_bf16_kernel<kCombWarps><<<static_cast<int>(blocks), 32 * kCombWarps, 0, st>>>(
+        slot_src, slot_w, k, H, S, nullptr, nullptr, 0, nullptr, partial, ready, t_base);
     XMOE_LAUNCH_CHECK();
 }
 

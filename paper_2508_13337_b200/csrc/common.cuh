@@ -52,11 +52,16 @@ int guarded(F&& f) {
 
 // Every kernel launch of the library passes through this check, which also
 // counts it (xmoe_kernel_launches()).
+// XMOE_SYNC_CHECK=1 (debugging): synchronise after every launch and name
+// the failing launch site.
 extern std::atomic<unsigned long long> g_kernel_launches;
+bool sync_check_enabled();
+void sync_check(const char* file, int line);
 #define XMOE_LAUNCH_CHECK()                                              \
     do {                                                                 \
         ::xmoe::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \
         XMOE_CUDA(cudaGetLastError());                                   \
+        if (::xmoe::sync_check_enabled()) ::xmoe::sync_check(__FILE__, __LINE__); \
     } while (0)
 
 constexpr int kNumSMs = 148;

@@ -34,6 +34,7 @@ namespace xmoe {
 thread_local int g_gemm_sm_limit = 0;
 thread_local const float* g_gemm_addf = nullptr;
 thread_local const unsigned* g_gemm_ready = nullptr;
+thread_local int g_gemm_ready_mult = 1;
 
 namespace tc {
 
@@ -864,7 +865,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             OutT* __restrict__ D, int relu, const uint32_t* __restrict__ mbits_in,
                             uint32_t* __restrict__ mbits_out, int coalesced, const int32_t* __restrict__ a_idx,
                             int a_rows, const __grid_constant__ CUtensorMap tmap_d, int tma_d, int half_ok,
-                            const float* addf, const unsigned* ready) {
+                            const float* addf, const unsigned* ready, int ready_mult) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -1071,7 +1072,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const float* arow_f = nullptr;
             if (addf && ti.row0 + wrow < off[G]) {
                 const int blk = (ti.row0 + wrow) >> 7;
-                const unsigned want = static_cast<unsigned>(min(128, off[G] - (blk << 7)));
+                const unsigned want = static_cast<unsigned>(min(128, off[G] - (blk << 7)) * ready_mult);
                 if (lane == 0) {
                     for (uint32_t it = 0;; ++it) {
                         unsigned v;
@@ -1718,7 +1719,7 @@ static void launch_tc2(const void* A, long long a_rows, long long a_cols, const 
     tc2::grouped_gemm_tc2_kernel<OutT, kVarK><<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
         ta, tb, group_sizes, G, M, N, K, D, relu, mbits_in, mbits_out,
         sizeof(OutT) == 4 && !mbits_out ? epi_coalesced() : 0, a_idx, static_cast<int>(idx_rows), td, tma_d ? 1 : 0,
-        half_tiles() ? 1 : 0, kVarK ? nullptr : g_gemm_addf, kVarK ? nullptr : g_gemm_ready);
+        half_tiles() ? 1 : 0, kVarK ? nullptr : g_gemm_addf, kVarK ? nullptr : g_gemm_ready, g_gemm_ready_mult);
     XMOE_LAUNCH_CHECK();
 }
 

@@ -51,6 +51,12 @@ void launch_combine_slots(const unsigned long long* slot_src, const float* slot_
 // routed copies only, fp32 sums to partial [S, H]; ready[t / 128] += 1 per token
 void launch_combine_slots_partial(const unsigned long long* slot_src, const float* slot_w, int k, int H, int S,
                                   float* partial, unsigned* ready, cudaStream_t st);
+// the same over the warp kernel (fat SM blocks when g_copy_fat > 0): tokens
+// t_base.. of a chunk; every (token, 512-column segment) item adds 1 to
+// ready[(t_base + t) / 128], so a block is complete at rows x combine_segments(H)
+void launch_combine_slots_seg_partial(const unsigned long long* slot_src, const float* slot_w, int k, int H, int S,
+                                      float* partial, unsigned* ready, int t_base, cudaStream_t st);
+int combine_segments(int H);
 void launch_unscatter_rows(int row_bytes, const int32_t* B_dev, long long max_rows,
                            const int32_t* dest_rank, const int32_t* dest_row,
                            const char* const* src_bufs, void* out, cudaStream_t st);
@@ -131,6 +137,7 @@ extern thread_local int g_gemm_sm_limit;
 // once ready[block] reaches its row count (published by the partial combine)
 extern thread_local const float* g_gemm_addf;
 extern thread_local const unsigned* g_gemm_ready;
+extern thread_local int g_gemm_ready_mult;  // publications per row the ready counters count (default 1)
 bool gemm_2cta_enabled(int N);  // the 2-CTA kernel serves N (XMOE_GEMM, N % 32)
 // grid cap of the row-movement kernels (token scatter, slot combine; 0 =
 // their default).  The chunked forward runs them on a few SMs' worth of

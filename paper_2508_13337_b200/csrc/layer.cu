@@ -365,6 +365,10 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         if (L.pull) {
             w.xs = w.sym + off_xs;
             w.rsrc = reinterpret_cast<int32_t*>(w.sym + off_rsrc);
+            if (L.Fs > 0) {  // late shared GEMM2 of the chunked forward
+                w.lpartial = static_cast<float*>(L.alloc(sizeof(float) * S * H));
+                w.lready = static_cast<unsigned*>(L.alloc(sizeof(unsigned) * ((S + 127) / 128 + 1)));
+            }
         }
         w.mid = L.alloc(static_cast<size_t>(L.R_max) * F * es);
         if (L.distributed && !L.p2p) {
@@ -733,6 +737,20 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     }();
     const int comm_sms = L.pull ? comm_sms_env : 0;
     const int gemm_sms = comm_sms > 0 ? kNumSMs - comm_sms : part_sms;
+    // Late shared GEMM2 (XMOE_CHUNK_LATE=1, A/B; SM partition only): the head
+    // runs shared GEMM1 alone, so the first routed chunk starts as soon as its
+    // rows land; every chunk's combine writes fp32 routed sums and publishes
+    // 128-token blocks; shared GEMM2 runs last, beside the final combine, its
+    // epilogue adding the published sums (the combine's own arithmetic:
+    // bit-identical output).  The combines keep their own SMs, so the
+    // epilogue's wait cannot starve them.  Measured slower on B200 (C2, N=4:
+    // 42.3 -> 40.7 M tok/s; N=2: 21.9 -> 17.9): the fp32 sums double the
+    // combine's writes and the last combine runs on the partition's SMs.
+    static const bool late_env = [] {
+        const char* e = std::getenv("XMOE_CHUNK_LATE");
+        return e && std::atoi(e) == 1;
+    }();
+    const bool late = late_env && comm_sms > 0 && L.Fs > 0 && L.workers[0].lpartial != nullptr;
     auto slot_A = [](int c) { return c; };
     auto slot_B = [](int c) { return kMaxChunks + c; };
 
@@ -773,6 +791,9 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
         for (int i = 0; i < nl; ++i)
             XMOE_CUDA(cudaMemcpyAsync(L.workers[i].xs, x_of(i), static_cast<size_t>(S) * rb, cudaMemcpyDeviceToDevice,
                                       cm));
+    if (late)  // the previous forward's GEMM2 (earlier on st) has read them
+        for (int i = 0; i < nl; ++i)
+            XMOE_CUDA(cudaMemsetAsync(L.workers[i].lready, 0, sizeof(unsigned) * ((S + 127) / 128 + 1), cm));
     // 2. comm stream: PFT (pft.cpp:12-60), chunk counts, count all-gather,
     //    destinations, then every chunk's rows
     for (int i = 0; i < nl; ++i) {
@@ -862,7 +883,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
         for (int i = 0; i < nl; ++i) {
             Worker& w = L.workers[i];
             launch_grouped_gemm_bf16(x_of(i), S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, st);
-            launch_grouped_gemm_bf16(w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, w.sout, 0, st);
+            if (!late) launch_grouped_gemm_bf16(w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, w.sout, 0, st);
         }
         g_gemm_sm_limit = 0;
         if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side1, st));
@@ -903,7 +924,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     if (sh_side) XMOE_CUDA(cudaStreamWaitEvent(cm, L.ev_join, 0));
     for (int c = 0; c < C; ++c) {
         g_copy_blocks = c == C - 1 ? 0 : blk_combine;  // the last combine runs alone
-        g_copy_fat = c == C - 1 ? 0 : comm_sms;
+        g_copy_fat = c == C - 1 && !late ? 0 : comm_sms;  // (late: beside shared GEMM2)
         XMOE_CUDA(cudaStreamWaitEvent(cm, L.evB[c], 0));
         if (dist) launch_flag_wait(L.workers[0].flags, W, slot_B(c), L.epoch, L.peer_err_d, cm);
         if (c == C - 1) L.mark(kEvReturn, cm);
@@ -916,6 +937,12 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
                                    L.Fs > 0 ? w.sout : nullptr, o_of(i), cm);
                 continue;
             }
+            if (late) {
+                launch_combine_slots_seg_partial(w.slot_src + static_cast<size_t>(t0) * k,
+                                                 w.slot_w + static_cast<size_t>(t0) * k, k, H, n,
+                                                 w.lpartial + static_cast<size_t>(t0) * H, w.lready, t0, cm);
+                continue;
+            }
             launch_combine_slots(w.slot_src + static_cast<size_t>(t0) * k, w.slot_w + static_cast<size_t>(t0) * k,
                                  k, H, n, L.Fs > 0 ? static_cast<const char*>(w.sout) + t0 * rb : nullptr,
                                  o_of(i) + static_cast<size_t>(t0) * rb, cm);
@@ -925,6 +952,24 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     g_copy_blocks = 0;
     g_copy_smem = 0;
     g_copy_fat = 0;
+    if (late) {
+        // shared GEMM2 finishing every row from the published routed sums.
+        // Enqueued after the combines it waits on: streams may share a
+        // hardware queue, and a spinning GEMM ahead of them in it would
+        // never let them start.
+        g_gemm_sm_limit = gemm_sms;
+        g_gemm_ready_mult = combine_segments(H);
+        for (int i = 0; i < nl; ++i) {
+            Worker& w = L.workers[i];
+            g_gemm_addf = w.lpartial;
+            g_gemm_ready = w.lready;
+            launch_grouped_gemm_bf16(w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, o_of(i), 0, st);
+        }
+        g_gemm_addf = nullptr;
+        g_gemm_ready = nullptr;
+        g_gemm_ready_mult = 1;
+        g_gemm_sm_limit = 0;
+    }
     XMOE_CUDA(cudaEventRecord(L.ev_done, cm));
     XMOE_CUDA(cudaStreamWaitEvent(st, L.ev_done, 0));
     L.mark(kEvCombine, st);

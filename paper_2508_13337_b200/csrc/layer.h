@@ -57,6 +57,8 @@ struct Worker {
     float* slot_w = nullptr;                 // [S*k] its combine weight
     char* sym = nullptr;          // symmetric region: recv | eout | recv_u | desc_recv | back_u
     char* xs = nullptr;           // pull dispatch: staged input [S_max, H] (symmetric region)
+    float* lpartial = nullptr;    // chunked late shared: fp32 routed sums [S_max, H]
+    unsigned* lready = nullptr;   // chunked late shared: per 128-token block publication counts
     int32_t* rsrc = nullptr;      // pull dispatch: (source << 24 | token) of every grouped row
     // redundancy-bypassing dispatch (rbd.cu)
     RbdWork rbd{};
