@@ -183,13 +183,13 @@ void launch_pull_rows(const int32_t* rsrc, const int32_t* rpe, int El, char* con
     require(row_bytes % 16 == 0, XMOE_ERR_VALIDATION, "pull dispatch needs 16-byte rows");
     if (max_rows <= 0) return;
     if (g_copy_fat > 0) {  // one 1024-thread block per SM (the shared reservation keeps others off it)
-        constexpr int kFatSmem = 120 * 1024;
         static bool attr = false;
         if (!attr) {
-            XMOE_CUDA(cudaFuncSetAttribute(pull_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFatSmem));
+            XMOE_CUDA(cudaFuncSetAttribute(pull_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kFatSmemBytes));
             attr = true;
         }
-        pull_rows_kernel<<<g_copy_fat, 1024, kFatSmem, st>>>(rsrc, rpe, El, xs_tab, row_bytes,
+        pull_rows_kernel<<<g_copy_fat, 1024, kFatSmemBytes, st>>>(rsrc, rpe, El, xs_tab, row_bytes,
                                                             static_cast<char*>(recv));
         XMOE_LAUNCH_CHECK();
         return;

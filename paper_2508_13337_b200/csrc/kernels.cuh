@@ -153,6 +153,7 @@ extern thread_local int g_copy_smem;
 // the full register file), and the GEMMs take the remaining SMs, so the row
 // traffic never shares an SM with a GEMM CTA.
 extern thread_local int g_copy_fat;
+constexpr int kFatSmemBytes = 120 * 1024;  // reservation that keeps one fat block per SM and GEMM CTAs off it
 
 // misc.cu
 void launch_recv_counts(const int32_t* tpe_all, int W, int E, int dst, int32_t* rpe,

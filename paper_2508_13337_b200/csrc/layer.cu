@@ -735,7 +735,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
         const char* e = std::getenv("XMOE_COMM_SMS");
         return e ? std::max(0, std::min(kNumSMs / 2, std::atoi(e))) : 24;
     }();
-    const int comm_sms = L.pull ? comm_sms_env : 0;
+    const int comm_sms = (L.pull || rbd) ? comm_sms_env : 0;
     const int gemm_sms = comm_sms > 0 ? kNumSMs - comm_sms : part_sms;
     // Late shared GEMM2 (XMOE_CHUNK_LATE=1, A/B; SM partition only): the head
     // runs shared GEMM1 alone, so the first routed chunk starts as soon as its
@@ -854,12 +854,15 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
         // beside the GEMMs on a bounded grid
         g_copy_blocks = c == 0 ? 0 : blk_scatter;
         const int t0 = t0_of(c), n = t0_of(c + 1) - t0;
-        if (rbd)  // each (token, dest) group's row once + a descriptor per copy
+        if (rbd) {  // each (token, dest) group's row once + a descriptor per copy
+            g_copy_fat = comm_sms;
             for (int i = 0; i < nl; ++i) {
                 Worker& w = L.workers[i];
                 launch_rbd_pack(x_of(i), static_cast<int>(rb), w.rbd, W, c, nk, w.slot_pos, k, w.dest_row, w.cw,
                                 L.recv_tab, L.desc_tab, cm, static_cast<int>(S), w.expert_ids, El);
             }
+            g_copy_fat = 0;
+        }
         else if (n > 0)
             for (int i = 0; i < nl; ++i) {
                 Worker& w = L.workers[i];

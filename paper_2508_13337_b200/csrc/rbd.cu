@@ -533,7 +533,7 @@ __global__ void rbd_offsets_kernel(const int32_t* __restrict__ gd_all, int W, in
 // lane l < kept(t) writes slot l's descriptor.  Same bytes as the
 // group-major pack, k-fold fewer dependent row loads per warp.
 constexpr int kPackVec = 8;  // int4 per lane per pass (4 KB rows in one pass)
-__global__ void __launch_bounds__(256) rbd_pack_tokens_kernel(
+__global__ void __launch_bounds__(512) rbd_pack_tokens_kernel(
     const char* __restrict__ x, int row_bytes, int S, int C, int c, int k, int El,
     const int32_t* __restrict__ slot_pos, const int32_t* __restrict__ expert_ids,
     const int32_t* __restrict__ dest_row, const double* __restrict__ cw, const int32_t* __restrict__ gbase,
@@ -877,7 +877,7 @@ __global__ void __launch_bounds__(256) rbd_merge_bf16_kernel(const char* const* 
 // BF16 source combine, vectorised: one warp per (token, 512-column segment).
 // Lane i < #groups resolves group i's merged-row address (peer or local);
 // the warp then permutes them into pilot order and streams the rows.
-__global__ void __launch_bounds__(256) rbd_combine_bf16_kernel(
+__global__ void __launch_bounds__(1024) rbd_combine_bf16_kernel(
     const char* const* __restrict__ back_tab, int H, int S, const int32_t* __restrict__ gbase,
     const int32_t* __restrict__ gcount, const RbdGroups g, const int32_t* __restrict__ ru,
     const int32_t* __restrict__ gpos, int C, int ck, const int32_t* __restrict__ dptr,
@@ -1074,9 +1074,22 @@ void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, int W, int
             "rbd pack needs 8-byte rows, top_k <= 32");
     const int nt = static_cast<int>(static_cast<long long>(c + 1) * S / wk.C - static_cast<long long>(c) * S / wk.C);
     if (nt == 0) return;
-    int tg = warp_grid(nt);
-    if (g_copy_blocks > 0 && tg > g_copy_blocks) tg = g_copy_blocks;
-    rbd_pack_tokens_kernel<<<tg, 256, 0, st>>>(static_cast<const char*>(x), row_bytes, S, wk.C, c, k, El, slot_pos,
+    int tg = warp_grid(nt), threads = 256;
+    size_t smem = 0;
+    if (g_copy_fat > 0) {  // whole-SM blocks of the SM partition (kernels.cuh g_copy_fat)
+        static bool attr = false;
+        if (!attr) {
+            XMOE_CUDA(cudaFuncSetAttribute(rbd_pack_tokens_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kFatSmemBytes));
+            attr = true;
+        }
+        tg = g_copy_fat;
+        threads = 512;
+        smem = kFatSmemBytes;
+    } else if (g_copy_blocks > 0 && tg > g_copy_blocks) {
+        tg = g_copy_blocks;
+    }
+    rbd_pack_tokens_kernel<<<tg, threads, smem, st>>>(static_cast<const char*>(x), row_bytes, S, wk.C, c, k, El, slot_pos,
                                                expert_ids, dest_row, cw, wk.gbase, wk.gcount, wk.g, wk.dptr, wk.coff,
                                                wk.gpos, wk.ru, wk.rd, wk.cs, recv_u_tab, desc_tab, wk.gpn);
     XMOE_LAUNCH_CHECK();
@@ -1122,7 +1135,17 @@ void launch_rbd_combine(int dtype, const char* const* back_tab, int H, int S, co
         rbd_combine_kernel<float><<<ceil_div(nt, 8), 256, 0, st>>>(
             back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru, wk.gpos, wk.C, c, wk.dptr, cw,
             static_cast<const float*>(addend), static_cast<float*>(out));
-    else if (H % 8 == 0)
+    else if (H % 8 == 0 && g_copy_fat > 0) {  // whole-SM blocks of the SM partition
+        static bool attr = false;
+        if (!attr) {
+            XMOE_CUDA(cudaFuncSetAttribute(rbd_combine_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kFatSmemBytes));
+            attr = true;
+        }
+        rbd_combine_bf16_kernel<<<g_copy_fat, 1024, kFatSmemBytes, st>>>(
+            back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru, wk.gpos, wk.C, c, wk.dptr, cw,
+            static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out));
+    } else if (H % 8 == 0)
         rbd_combine_bf16_kernel<<<ceil_div(static_cast<long long>(nt) * ((H + 511) / 512), 8), 256, 0, st>>>(
             back_tab, H, S, wk.gbase, wk.gcount, wk.g, wk.ru, wk.gpos, wk.C, c, wk.dptr, cw,
             static_cast<const __nv_bfloat16*>(addend), static_cast<__nv_bfloat16*>(out));
