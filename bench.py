@@ -609,21 +609,23 @@ def main():
     e2e_steps = max(50, args.steps)  # steady state: one pipeline fill + drain amortised over the run
     numa_cpus = bind_to_gpu_numa(local_rank)
     # SSMB (C4): every rank holds the whole sequence buffer but reads only its
-    # shard, so only the shard crosses PCIe; the all-gathered output comes back whole
+    # shard, so only the shard crosses PCIe
     x_lo = (rank * (S_seq // world)) if ssmb else 0
     xh = [x.cpu().pin_memory() for _ in range(2)]
-    oh = [torch.empty_like(xin.cpu()).pin_memory() for _ in range(2)]
+    # SSMB: every rank holds the all-gathered output; each reads back its own
+    # shard, so the job retrieves the sequence's output once
+    oh = [torch.empty_like(xin[x_lo:x_lo + S].cpu()).pin_memory() for _ in range(2)]
     xd = [xin.clone() for _ in range(2)]
     od = [torch.empty_like(xin) for _ in range(2)]
     h2d_bytes = x.numel() * 2
-    d2h_bytes = xin.numel() * 2
+    d2h_bytes = oh[0].numel() * 2
     s_in = torch.cuda.Stream()
     s_out = torch.cuda.Stream()
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_done = [torch.cuda.Event() for _ in range(2)]
     ev_outfree = [torch.cuda.Event() for _ in range(2)]
 
-    def e2e_run(n, t0=None, t1=None):
+    def e2e_run(n, t0=None, t1=None, compute=True):
         if t0 is not None:
             t0.record(s_in)
         with torch.cuda.stream(s_in):
@@ -640,11 +642,12 @@ def main():
             stream.wait_event(ev_in[b])
             if i >= 2:
                 stream.wait_event(ev_outfree[b])  # step i-2's output left the device
-            step(layer, xd[b], od[b])
+            if compute:
+                step(layer, xd[b], od[b])
             ev_done[b].record(stream)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_done[b])
-                oh[b].copy_(od[b], non_blocking=True)
+                oh[b].copy_(od[b][x_lo:x_lo + S], non_blocking=True)
                 ev_outfree[b].record(s_out)
         if t1 is not None:
             t1.record(s_out)
@@ -657,6 +660,13 @@ def main():
     e2e_run(e2e_steps, e0, e1)
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
+    # the same loop with the forward left out: the host-link bound of e2e on
+    # this box (PCIe and host memory, shared by the ranks of the node)
+    e2e_run(3, compute=False)
+    barrier()
+    e2e_run(e2e_steps, e0, e1, compute=False)
+    barrier()
+    copy_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
 
     # ---- CPU baseline (reference on host cores, rank 0 at N=1 only)
     cpu = None
@@ -691,8 +701,12 @@ def main():
                     "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
                     "steps": e2e_steps,
                     "host_cpus": numa_cpus,
+                    "copies_only": {"value": tokens_step / (copy_ms * 1e-3), "unit": UNIT,
+                                    "ms_per_step": copy_ms},
                     "note": "pinned host x -> device, forward, device -> pinned host out, every step; copies of "
-                            "neighbouring steps overlap the forward on two copy streams (double-buffered)"},
+                            "neighbouring steps overlap the forward on two copy streams (double-buffered); "
+                            "bytes per rank (each rank moves its own shard; SSMB: its shard of the gathered "
+                            "output); copies_only = the same loop without the forward (the host-link bound)"},
             "roofline": {"bound": "tensor", "kernel": "grouped_gemm_tc (routed experts, GEMM1+GEMM2)",
                          "achieved": achieved, "peak": tf_burst, "unit": "TFLOP/s",
                          "frac": achieved / tf_burst,
