@@ -735,7 +735,15 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
         const char* e = std::getenv("XMOE_COMM_SMS");
         return e ? std::max(0, std::min(kNumSMs / 2, std::atoi(e))) : 24;
     }();
-    const int comm_sms = (L.pull || rbd) ? comm_sms_env : 0;
+    // RBD on the partition (XMOE_RBD_PARTITION=1, A/B): pack and combine as
+    // whole-SM blocks.  Measured slower (C2 N=4, 2 chunks: 36.6 -> 33.5 M
+    // tokens/s): the RBD combine's per-token group ordering needs more than
+    // 24 SMs' issue rate.
+    static const bool rbd_part = [] {
+        const char* e = std::getenv("XMOE_RBD_PARTITION");
+        return e && std::atoi(e) == 1;
+    }();
+    const int comm_sms = (L.pull || (rbd && rbd_part)) ? comm_sms_env : 0;
     const int gemm_sms = comm_sms > 0 ? kNumSMs - comm_sms : part_sms;
     // Late shared GEMM2 (XMOE_CHUNK_LATE=1, A/B; SM partition only): the head
     // runs shared GEMM1 alone, so the first routed chunk starts as soon as its

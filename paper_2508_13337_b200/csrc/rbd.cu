@@ -884,9 +884,11 @@ __global__ void __launch_bounds__(1024) rbd_combine_bf16_kernel(
     const double* __restrict__ cw, const __nv_bfloat16* __restrict__ addend, __nv_bfloat16* __restrict__ out) {
     const int nseg = (H + 511) / 512;
     const int t0 = rbd_chunk_t0(ck, S, C), nt = rbd_chunk_t0(ck + 1, S, C) - t0;
-    const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (gw >= static_cast<long long>(nt) * nseg) return;
+    const long long nw = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+    // grid-stride: the whole-SM launch of the SM partition has fewer warps than items
+    for (long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+         gw < static_cast<long long>(nt) * nseg; gw += nw) {
     const int t = t0 + static_cast<int>(gw / nseg), seg = static_cast<int>(gw % nseg);
     const int b = gbase[t], n = min(gcount[t], 32);
     int key = 0x7fffffff;
@@ -945,6 +947,7 @@ __global__ void __launch_bounds__(1024) rbd_combine_bf16_kernel(
         o.z = static_cast<int>(pack_bf16(acc[4], acc[5]));
         o.w = static_cast<int>(pack_bf16(acc[6], acc[7]));
         st_na_v4(reinterpret_cast<int4*>(out + static_cast<size_t>(t) * H) + c, o);
+    }
     }
 }
 

@@ -107,7 +107,8 @@ def main():
     # to the unchunked layer, eager and graph-replayed, over repeated forwards
     for ci, (S, cap_f, chunks, mode) in enumerate([(1000, None, 3, capi.NAIVE), (777, 0.6, 4, capi.NAIVE),
                                                    (4096, None, 0, capi.NAIVE), (1000, None, 3, capi.RBD),
-                                                   (777, 0.6, 4, capi.RBD), (4096, None, 0, capi.RBD)]):
+                                                   (777, 0.6, 4, capi.RBD), (4096, None, 0, capi.RBD),
+                                                   (4096, None, 2, capi.RBD), (8192, None, 4, capi.NAIVE)]):
         E, k, H, F = 16 * world, 6, 256, 128
         el = E // world
         rng = np.random.default_rng(300 + ci)

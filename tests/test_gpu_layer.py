@@ -298,12 +298,14 @@ def test_graph_replay_matches_eager(mode):
 @pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("W,S,chunks,cap_factor,shared", [(1, 1000, 2, None, True), (1, 4096, 8, None, True),
                                                           (4, 333, 3, None, False), (4, 512, 4, 0.5, True),
-                                                          (2, 3, 4, None, False), (8, 700, 5, None, True)])
+                                                          (2, 3, 4, None, False), (8, 700, 5, None, True),
+                                                          (2, 6144, 2, None, True)])
 def test_chunked_forward_bit_identical(W, S, chunks, cap_factor, shared, mode):
     """The token-chunked pipelined forward (chunk.cu), plain and
     redundancy-bypassing, is bit-identical to the unchunked one — ragged
-    chunks, capacity drops, more chunks than tokens — and matches the fp64
-    oracle at the bf16 tolerance."""
+    chunks, capacity drops, more chunks than tokens, and chunks with more
+    rows than the SM partition's whole-SM copy kernels have warps — and
+    matches the fp64 oracle at the bf16 tolerance."""
     from paper_2508_13337_b200 import capi
     ctx = capi.Context(0, W, -1)
     rng = np.random.default_rng(S + 17 * W)
