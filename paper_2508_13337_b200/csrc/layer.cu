@@ -264,7 +264,13 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         const int req = XMOE_LAYER_CHUNKS_OF(d.flags);
         require(req <= kMaxChunks, XMOE_ERR_VALIDATION, "at most 8 token chunks");
         const bool can = bf && !L.train && (!L.distributed || L.p2p) && L.k <= 32 && L.gpn == 1;
-        int C = req > 0 ? req : (S >= 4096 && L.distributed && !rbd ? std::min(4, W) : 1);
+        // default: up to min(4, W) chunks, keeping >= 512 rows per local
+        // expert per chunk on average (W*S*k/E per expert and forward): below
+        // that the chunk GEMMs pay padding tiles for the overlap (B200, N=4:
+        // C3 / C4 are fastest at 2 chunks, C2 / C5 at 4)
+        const long long rows_pe = static_cast<long long>(W) * S * L.k / std::max(1, L.E);
+        const int C_auto = static_cast<int>(std::max<long long>(1, std::min<long long>(std::min(4, W), rows_pe / 512)));
+        int C = req > 0 ? req : (S >= 4096 && L.distributed && !rbd ? C_auto : 1);
         if (const char* e = std::getenv("XMOE_CHUNKS")) C = std::max(1, std::min(kMaxChunks, std::atoi(e)));
         L.nchunks = can ? static_cast<int>(std::max<long long>(1, std::min<long long>(C, S))) : 1;
         if (L.nchunks > 1) {
