@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256) bwd_owner_prep_kernel(
 // bits.  Algorithmic bytes at W = 1: dy once, y and dz once per copy.
 constexpr int kBsVec = 8;  // int4 per lane per pass (4 KB rows in one pass)
 
-__global__ void __launch_bounds__(256) bwd_scatter_dy_kernel(
+__global__ void __launch_bounds__(512) bwd_scatter_dy_kernel(
     const char* __restrict__ dy, int H, int S, int k, const int32_t* __restrict__ slot_pos,
     const int32_t* __restrict__ dest_rank, const int32_t* __restrict__ dest_row, const double* __restrict__ cw,
     int me, char* __restrict__ dz, char* const* __restrict__ eout_tab, char* const* __restrict__ dyg_tab,
@@ -314,7 +314,20 @@ void launch_bwd_scatter_dy(const void* dy, int H, int S, int k, const int32_t* s
     long long blocks = (static_cast<long long>(S) + 7) / 8;
     if (blocks > 8LL * kNumSMs) blocks = 8LL * kNumSMs;
     if (g_copy_blocks > 0 && blocks > g_copy_blocks) blocks = g_copy_blocks;
-    bwd_scatter_dy_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(
+    int threads = 256;
+    size_t smem = 0;
+    if (g_copy_fat > 0) {  // whole-SM blocks of the SM partition (kernels.cuh g_copy_fat)
+        static bool attr = false;
+        if (!attr) {
+            XMOE_CUDA(cudaFuncSetAttribute(bwd_scatter_dy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kFatSmemBytes));
+            attr = true;
+        }
+        blocks = g_copy_fat;
+        threads = 512;
+        smem = kFatSmemBytes;
+    }
+    bwd_scatter_dy_kernel<<<static_cast<int>(blocks), threads, smem, st>>>(
         static_cast<const char*>(dy), H, S, k, slot_pos, dest_rank, dest_row, cw, me, static_cast<char*>(dz),
         eout_tab, dyg_tab, dxc_tab, gw_tab, gsrc_tab, slot_dw, bslot_src);
     XMOE_LAUNCH_CHECK();

@@ -1826,7 +1826,9 @@ static void wgrad_mn_impl(const void* A, int M, const void* B, int N, int b_cols
     int sms = 0;
     XMOE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const long long tiles = static_cast<long long>(G) * ((M + tc2::BM - 1) / tc2::BM) * ((N + tc2::BN - 1) / tc2::BN);
-    const long long pairs = tiles < sms / 2 ? tiles : sms / 2;
+    long long cap_pairs = sms / 2;
+    if (g_gemm_sm_limit > 0 && g_gemm_sm_limit / 2 < cap_pairs) cap_pairs = g_gemm_sm_limit / 2;
+    const long long pairs = tiles < cap_pairs ? tiles : cap_pairs;
     tc2::grouped_wgrad_mn_kernel<<<static_cast<int>(2 * pairs), tc2::kThreads, tc2::kSmemBytes, st>>>(
         ta, tb, tat, tbt, group_rows, G, M, N, D, epi_coalesced(), td, tma_store ? 1 : 0, transpose_out ? 1 : 0);
     XMOE_LAUNCH_CHECK();

@@ -1351,6 +1351,7 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
     require(L.bwd_pending, XMOE_ERR_VALIDATION, "backward must follow a forward (one backward per forward)");
     L.bwd_pending = false;
     g_copy_blocks = 0;  // launch-shaping globals start clean even after an aborted call
+    g_copy_fat = 0;
     g_gemm_sm_limit = 0;
     Ctx& ctx = *L.ctx;
     const int W = L.W, E = L.E, H = L.H, F = L.F, k = L.k, El = L.El;
@@ -1388,6 +1389,17 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
         return e ? std::max(0, std::atoi(e)) : 128;
     }();
     const int copy_cap = dist && !L.timing ? bwd_copy_blocks : 0;
+    // SM partition (as the chunked forward's; XMOE_BWD_COMM_SMS=n, A/B, off
+    // by default): the dy scatter and the dx combine run as whole-SM blocks
+    // on n SMs, the GEMMs beside them on the rest.  Measured neutral to
+    // slightly slower on B200 (C2 fwd+bwd, N=4: 12.93 M tokens/s off, 12.64
+    // at 24 SMs, 12.99 at 32; N=2: 7.32 off, 7.07 at 24)
+    static const int bwd_comm_env = [] {
+        const char* e = std::getenv("XMOE_BWD_COMM_SMS");
+        return e ? std::max(0, std::min(kNumSMs / 2, std::atoi(e))) : 0;
+    }();
+    const int bwd_comm = dist && !L.timing ? bwd_comm_env : 0;
+    const int bwd_gemm_sms = bwd_comm > 0 ? kNumSMs - bwd_comm : 0;
     if (!L.timing) {
         XMOE_CUDA(cudaEventRecord(L.ev_fork, st));
         XMOE_CUDA(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
@@ -1395,11 +1407,12 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
             const char* e = std::getenv("XMOE_BWD_SIDE_SMS");
             return e ? std::atoi(e) : 0;
         }();
-        g_gemm_sm_limit = side_sms;
+        g_gemm_sm_limit = bwd_gemm_sms > 0 ? bwd_gemm_sms : side_sms;
         token_level(L.side);
         g_gemm_sm_limit = 0;
     }
     g_copy_blocks = copy_cap;
+    g_copy_fat = bwd_comm;
     for (int i = 0; i < L.nl; ++i) {  // B1
         Worker& w = L.workers[i];
         launch_bwd_scatter_dy(xo(dy, i), H, static_cast<int>(S), k, w.slot_pos, w.dest_rank, w.dest_row, w.cw,
@@ -1413,6 +1426,7 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
     auto bbar = [&](int j) {
         launch_flag_barrier(L.flag_tab, L.workers[0].flags, W, me_rank, kSlotBwdBar + j, L.epoch, L.peer_err_d, st);
     };
+    g_copy_fat = 0;
     if (dist) bbar(0);
     bmark(kBwScatter);
     for (int i = 0; i < L.nl; ++i) {  // B2-B3 at the owner
@@ -1456,8 +1470,10 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
         for (int i = 0; i < L.nl; ++i) {
             Worker& w = L.workers[i];
             g_copy_blocks = copy_cap;
+            g_copy_fat = bwd_comm;
             launch_combine_slots(w.bslot_src, nullptr, k, H, static_cast<int>(S), L.Fs > 0 ? w.dxs : nullptr,
                                  static_cast<char*>(dx) + static_cast<size_t>(i) * S * rb, gs, 0, w.dxg);
+            g_copy_fat = 0;
             g_copy_blocks = 0;
         }
     };
@@ -1468,8 +1484,10 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
         XMOE_CUDA(cudaStreamWaitEvent(L.side, L.ev_fork, 0));  // side: token level, then the dx combine
         dx_combine(L.side);
         XMOE_CUDA(cudaEventRecord(L.ev_join, L.side));
+        g_gemm_sm_limit = bwd_gemm_sms;  // beside the dx combine's SMs
         gate_wgrad(st);
     }
+    g_gemm_sm_limit = bwd_gemm_sms;
     for (int i = 0; i < L.nl; ++i) {  // B4 wgrad straight on the grouped activations (MN-major operands)
         Worker& w = L.workers[i];
         const size_t go = dist ? 0 : static_cast<size_t>(w.rank) * El * H * F;
@@ -1477,6 +1495,7 @@ void layer_backward(Layer& L, const void* x, const void* dy, long long S, void* 
         // dW2_e [F, H] as (dz_e^T mid_e)^T: M = H fills whole 256-row tiles
         launch_grouped_wgrad_mn_t(w.dz, H, w.mid, F, L.R_max, w.rpe, El, w.tail_a, w.tail_b, L.dw2 + go, st);
     }
+    g_gemm_sm_limit = 0;
     bmark(kBwWgrad);
     if (L.timing) {
         token_level(st);

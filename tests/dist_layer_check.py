@@ -201,37 +201,39 @@ def main():
         del layer
         dist.barrier()
     # backward over the peer transport (bf16, dropless): dx per rank, expert
-    # grads of each rank's block, gate grads summed over ranks
+    # grads of each rank's block, gate grads summed over ranks; 2048 tokens:
+    # more rows than the SM partition's whole-SM blocks have warps
     from oracle import moe_grad as Gr
-    S, E, k, H, F = 256, 16 * world, 4, 128, 128
-    el = E // world
-    rng = np.random.default_rng(55)
-    gate = grid_gate(rng, H, E)
-    w1 = bf16_round(rng.uniform(-0.1, 0.1, (E, H, F)))
-    w2 = bf16_round(rng.uniform(-0.1, 0.1, (E, F, H)))
-    x = grid_tokens(rng, world, S, H)
-    dy = bf16_round(rng.uniform(-1, 1, (world, S, H)))
-    bv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).cuda()  # noqa: E731
-    layer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k, max_tokens=S,
-                       dtype=capi.BF16, gate=bv(gate), w1=bv(w1[rank * el:(rank + 1) * el]),
-                       w2=bv(w2[rank * el:(rank + 1) * el]), train=True)
-    xd = bv(x[rank])
-    layer.forward(xd)
-    dxr = layer.backward(xd, bv(dy[rank])).float().cpu().numpy()
-    gr = {n: (v.cpu().numpy() if v is not None else None) for n, v in layer.grads().items()}
-    got = [None] * world
-    dist.all_gather_object(got, (dxr, gr))
-    if rank == 0:
-        want = Gr.moe_grads(x.reshape(world * S, H), gate, w1, w2, dy.reshape(world * S, H), k, world * S * k)
-        errs = [norm_rel(np.concatenate([g[0] for g in got]), want["x"]),
-                norm_rel(sum(g[1]["gate"] for g in got), want["gate"]),
-                norm_rel(np.concatenate([g[1]["w1"] for g in got]), want["w1"]),
-                norm_rel(np.concatenate([g[1]["w2"] for g in got]), want["w2"])]
-        print("backward normwise errors dx/gate/w1/w2:", errs, flush=True)
-        if max(errs) > 3e-2:
-            failures.append(("backward", errs))
-    del layer
-    dist.barrier()
+    for S in (256, 2048):
+        E, k, H, F = 16 * world, 4, 128, 128
+        el = E // world
+        rng = np.random.default_rng(55)
+        gate = grid_gate(rng, H, E)
+        w1 = bf16_round(rng.uniform(-0.1, 0.1, (E, H, F)))
+        w2 = bf16_round(rng.uniform(-0.1, 0.1, (E, F, H)))
+        x = grid_tokens(rng, world, S, H)
+        dy = bf16_round(rng.uniform(-1, 1, (world, S, H)))
+        bv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).cuda()  # noqa: E731
+        layer = capi.Layer(ctx, num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=S * k, max_tokens=S,
+                           dtype=capi.BF16, gate=bv(gate), w1=bv(w1[rank * el:(rank + 1) * el]),
+                           w2=bv(w2[rank * el:(rank + 1) * el]), train=True)
+        xd = bv(x[rank])
+        layer.forward(xd)
+        dxr = layer.backward(xd, bv(dy[rank])).float().cpu().numpy()
+        gr = {n: (v.cpu().numpy() if v is not None else None) for n, v in layer.grads().items()}
+        got = [None] * world
+        dist.all_gather_object(got, (dxr, gr))
+        if rank == 0:
+            want = Gr.moe_grads(x.reshape(world * S, H), gate, w1, w2, dy.reshape(world * S, H), k, world * S * k)
+            errs = [norm_rel(np.concatenate([g[0] for g in got]), want["x"]),
+                    norm_rel(sum(g[1]["gate"] for g in got), want["gate"]),
+                    norm_rel(np.concatenate([g[1]["w1"] for g in got]), want["w1"]),
+                    norm_rel(np.concatenate([g[1]["w2"] for g in got]), want["w2"])]
+            print(f"backward S={S} normwise errors dx/gate/w1/w2:", errs, flush=True)
+            if max(errs) > 3e-2:
+                failures.append(("backward", S, errs))
+        del layer
+        dist.barrier()
     # sequence-sharded block across the ranks (ssmb.cpp:12-46)
     S, E, k, H, F = 101, 8, 2, 16, 8
     rng = np.random.default_rng(77)
