@@ -21,12 +21,7 @@
 
 namespace xmoe {
 
-__host__ __device__ __forceinline__ int chunk_t0(int c, int S, int C) {
-    return static_cast<int>(static_cast<long long>(c) * S / C);
-}
-__device__ __forceinline__ int chunk_of(int t, int S, int C) {
-    return static_cast<int>((static_cast<long long>(t + 1) * C - 1) / S);
-}
+// chunk_t0 / chunk_of: kernels.cuh
 
 // per (chunk c, expert e): kept copies of e whose token lies in chunk c, and
 // their offset inside e's packed segment (tokens ascend within a segment,

@@ -153,6 +153,19 @@ extern thread_local int g_copy_smem;
 // the full register file), and the GEMMs take the remaining SMs, so the row
 // traffic never shares an SM with a GEMM CTA.
 extern thread_local int g_copy_fat;
+
+// Token chunk boundaries of the pipelined forward: chunk c = tokens
+// [cS/C, (c+1)S/C); chunk_of(t) inverts chunk_t0.  (Measured on B200, C2
+// N=4: a half-size last chunk, or half-size first and last chunks, gave
+// 42.7 / 41.6 M tokens/s against 42.4-42.8 M for even chunks, and both cost
+// N=2 or C3 — even chunks kept.)
+__host__ __device__ __forceinline__ int chunk_t0(int c, long long S, int C) {
+    return c >= C ? static_cast<int>(S) : static_cast<int>(c * S / C);
+}
+__host__ __device__ __forceinline__ int chunk_of(int t, long long S, int C) {
+    return static_cast<int>((static_cast<long long>(t + 1) * C - 1) / S);
+}
+inline long long chunk_max_tokens(long long S, int C) { return (S + C - 1) / C; }
 constexpr int kFatSmemBytes = 120 * 1024;  // reservation that keeps one fat block per SM and GEMM CTAs off it
 
 // misc.cu

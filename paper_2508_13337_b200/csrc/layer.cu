@@ -274,7 +274,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         if (const char* e = std::getenv("XMOE_CHUNKS")) C = std::max(1, std::min(kMaxChunks, std::atoi(e)));
         L.nchunks = can ? static_cast<int>(std::max<long long>(1, std::min<long long>(C, S))) : 1;
         if (L.nchunks > 1) {
-            const long long cs = (S + L.nchunks - 1) / L.nchunks;
+            const long long cs = chunk_max_tokens(S, L.nchunks);
             const long long rc = std::min<long long>(static_cast<long long>(W) * cs * std::min<long long>(L.k, L.El),
                                                      static_cast<long long>(W) * L.El *
                                                          std::min<long long>(d.max_token_count, cs));
@@ -713,7 +713,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     char* ob = static_cast<char*>(out);
     auto x_of = [&](int i) { return xb + static_cast<size_t>(i) * S * rb; };
     auto o_of = [&](int i) { return ob + static_cast<size_t>(i) * S * rb; };
-    auto t0_of = [&](int c) { return static_cast<int>(static_cast<long long>(c) * S / C); };
+    auto t0_of = [&](int c) { return chunk_t0(c, S, C); };
     const int me = L.workers[0].rank;
     const bool rbd = L.d.dispatch_mode == XMOE_DISPATCH_RBD;
     // row-movement kernels run on a bounded grid beside the GEMMs

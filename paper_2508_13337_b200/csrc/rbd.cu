@@ -433,9 +433,7 @@ __global__ void rbd_group_pos_kernel(const int32_t* __restrict__ perm, const int
     nsorted[pos] = g.n[gid];
 }
 
-__device__ __forceinline__ int rbd_chunk_t0(int c, int S, int C) {
-    return static_cast<int>(static_cast<long long>(c) * S / C);
-}
+__device__ __forceinline__ int rbd_chunk_t0(int c, int S, int C) { return chunk_t0(c, S, C); }
 
 // first descriptor (my order) of sorted position p; p == G gives the total
 __device__ __forceinline__ int rbd_coff_at(const int32_t* coff, const int32_t* nsorted, int G, int p) {
@@ -1075,7 +1073,7 @@ void launch_rbd_pack(const void* x, int row_bytes, const RbdWork& wk, int W, int
     (void)max_groups;
     require((row_bytes & 7) == 0 && k <= 32 && expert_ids, XMOE_ERR_VALIDATION,
             "rbd pack needs 8-byte rows, top_k <= 32");
-    const int nt = static_cast<int>(static_cast<long long>(c + 1) * S / wk.C - static_cast<long long>(c) * S / wk.C);
+    const int nt = chunk_t0(c + 1, S, wk.C) - chunk_t0(c, S, wk.C);
     if (nt == 0) return;
     int tg = warp_grid(nt), threads = 256;
     size_t smem = 0;
@@ -1128,7 +1126,7 @@ void launch_rbd_merge(int dtype, const char* const* eout_tab, int H, const RbdDe
 
 void launch_rbd_combine(int dtype, const char* const* back_tab, int H, int S, const RbdWork& wk, int c,
                         const double* cw, const void* addend, void* out, cudaStream_t st) {
-    const int nt = static_cast<int>(static_cast<long long>(c + 1) * S / wk.C - static_cast<long long>(c) * S / wk.C);
+    const int nt = chunk_t0(c + 1, S, wk.C) - chunk_t0(c, S, wk.C);
     if (nt == 0) return;
     if (dtype == XMOE_F64)
         rbd_combine_kernel<double><<<ceil_div(nt, 8), 256, 0, st>>>(
