@@ -679,6 +679,21 @@ def main():
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
+    # whole-step roofline per GPU (B200_PROFILING.md: the slower of the tensor
+    # work at the measured bf16 peak and the bytes that must cross NVLink at
+    # the measured 770 GB/s per direction): routed + shared expert FFNs + gate
+    shared_flops = 4.0 * S * H * ns * Fs
+    gate_flops = 2.0 * S * H * E
+    step_flops = gemm_flops + shared_flops + gate_flops
+    nvl_bytes = (led.get("dispatch_rows_offrank", 0) + led.get("combine_rows_offrank", 0)) if world > 1 else 0
+    t_tensor = step_flops / (tf_burst * 1e12) * 1e3
+    t_nvl = nvl_bytes / (NVLINK_GBPS * 1e9) * 1e3
+    step_roofline = {"tensor_ms": t_tensor, "nvlink_ms": t_nvl, "bound_ms": max(t_tensor, t_nvl),
+                     "bound": "tensor" if t_tensor >= t_nvl else "nvlink", "frac": max(t_tensor, t_nvl) / ms,
+                     "flops_per_gpu": step_flops, "nvlink_bytes_per_gpu_per_direction": nvl_bytes,
+                     "note": "per GPU: (routed + shared expert FFN + gate) FLOPs at the measured burst bf16 peak vs "
+                             "this rank's off-rank dispatch + combine row bytes (ledger) at 770 GB/s per direction; "
+                             "frac = bound / ms_per_step"}
     if rank == 0:
         tokens_step = S_seq  # whole job: all ranks' tokens (C4: the one sharded sequence)
         value = tokens_step / (ms * 1e-3)
@@ -730,6 +745,7 @@ def main():
                             "combine_frac": comb_bytes / (stages["combine_kernel"] * 1e-3) / 1e9 / hbm
                             if world == 1 and stages.get("combine_kernel") else None},
             "ledger": led,
+            "step_roofline": step_roofline,
             "a2a": None if world == 1 else {
                 "bound": "nvlink", "unit": "GB/s", "peak": NVLINK_GBPS,
                 "bytes_offrank_per_gpu": dispatch_compare[args.mode]["offrank_bytes_dispatch"],
