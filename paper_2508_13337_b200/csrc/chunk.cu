@@ -95,6 +95,7 @@ __global__ void dispatch_dest_chunked_kernel(const int32_t* __restrict__ expert_
         // pull dispatch: tell the owner which (source, token) fills that row
         if (rsrc_tab) rsrc_tab[d][row] = (me << 24) | t;
     }
+    if (rsrc_tab) __threadfence_system();  // peer stores visible before the flag that follows
 }
 
 // Pull dispatch, per token: where the combine reads each kept copy's expert
