@@ -710,6 +710,10 @@ def main():
                        "dispatch": args.mode, "dispatch_probe": auto_probe, "pass": "forward",
                        "chunks": layer.chunks(),
                        "transport": (os.environ.get("XMOE_TRANSPORT") or "p2p") if world > 1 else "local",
+                       "row_movement": (("owner-side pull" if os.environ.get("XMOE_DISPATCH", "pull") == "pull"
+                                         else "source-side push") +
+                                        f", {os.environ.get('XMOE_COMM_SMS', '24')} whole SMs beside GEMMs on the rest"
+                                        if world > 1 and layer.chunks() > 1 and args.mode == "naive" else None),
                        "l2": f"working set > L2: {wbytes / 1e9:.2f} GB of expert weights per GPU + "
                              f"{S * H * 2 / 1e6:.0f} MB tokens stream each step (126 MB L2)"},
             "e2e": {"value": tokens_step / (e2e_ms * 1e-3), "unit": UNIT,
