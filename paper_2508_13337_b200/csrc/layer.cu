@@ -263,7 +263,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     {
         const int req = XMOE_LAYER_CHUNKS_OF(d.flags);
         require(req <= kMaxChunks, XMOE_ERR_VALIDATION, "at most 8 token chunks");
-        const bool can = bf && !L.train && (!L.distributed || L.p2p) && L.k <= 32 && L.gpn == 1;
+        const bool can = bf && !L.train && (!L.distributed || L.p2p) && L.k <= 32 && L.gpn == 1 && L.H % 8 == 0;
         // default: up to min(4, W) chunks, keeping >= 512 rows per local
         // expert per chunk on average (W*S*k/E per expert and forward): below
         // that the chunk GEMMs pay padding tiles for the overlap (B200, N=4:
@@ -287,7 +287,7 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
     // keeps the source-side stores, A/B)
     {
         const char* e = std::getenv("XMOE_DISPATCH");
-        L.pull = L.nchunks > 1 && !rbd && !(e && std::string(e) == "push");
+        L.pull = L.nchunks > 1 && !rbd && H % 8 == 0 && !(e && std::string(e) == "push");
         require(!L.pull || (S < (1LL << 24) && W <= 255), XMOE_ERR_VALIDATION,
                 "pull dispatch: max_tokens < 2^24 and world <= 255");
     }
