@@ -371,7 +371,8 @@ void layer_create(Ctx& ctx, const xmoe_layer_desc& d, const void* gate, const vo
         if (L.pull) {
             w.xs = w.sym + off_xs;
             w.rsrc = reinterpret_cast<int32_t*>(w.sym + off_rsrc);
-            if (L.Fs > 0) {  // late shared GEMM2 of the chunked forward
+            const char* le = std::getenv("XMOE_CHUNK_LATE");
+            if (L.Fs > 0 && le && std::atoi(le) == 1) {  // late shared GEMM2 of the chunked forward (A/B)
                 w.lpartial = static_cast<float*>(L.alloc(sizeof(float) * S * H));
                 w.lready = static_cast<unsigned*>(L.alloc(sizeof(unsigned) * ((S + 127) / 128 + 1)));
             }
