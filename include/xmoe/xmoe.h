@@ -95,7 +95,7 @@ int xmoe_ctx_create(int device, int world, int rank, const void* nccl_id, xmoe_c
 int xmoe_ctx_destroy(xmoe_ctx* ctx);
 /* XMOE_OK, or XMOE_ERR_NCCL when the context's communicator reports an
  * asynchronous error (ncclCommGetAsyncError). */
-int xmoe_ctx_status(xmoe_ctx* ctx);
+int xmoe_ctx_status(xmoe_ctx* ctx);  /* NCCL async errors; asynchronous checks (once) */
 
 /* ------------------------------------------------------------------ operators */
 
@@ -132,8 +132,10 @@ int xmoe_scatter_combine(xmoe_ctx* ctx, int dtype, const void* rows, int64_t n, 
 
 /* moesim::grouped_expert_mlp (pf_pipeline.hpp:38-39, pf_pipeline.cpp:83-105).
  * in [rows,H]; rows_per_expert [G] (device); expert i covers the next
- * rows_per_expert[i] rows.  `rows` bounds the buffer; the real total is
- * sum(rows_per_expert).  F64: w1 [G,H,F], w2 [G,F,H] (reference layout).
+ * rows_per_expert[i] rows and they must sum to `rows` (the reference's
+ * CountMismatch, checked on the device without a host sync: the GEMMs run on
+ * counts clamped to the buffer and xmoe_ctx_status reports the mismatch).
+ * F64: w1 [G,H,F], w2 [G,F,H] (reference layout).
  * BF16: w1 [G,F,H], w2 [G,H,F] (K-major; tcgen05 grouped GEMM). */
 int xmoe_grouped_mlp(xmoe_ctx* ctx, int dtype, const void* in, int64_t rows,
                      const int32_t* rows_per_expert, int64_t G, const void* w1, const void* w2,

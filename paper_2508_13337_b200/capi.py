@@ -288,8 +288,11 @@ class Context:
                                           _ptr(out), int(validate), _stream()))
         return out
 
-    def grouped_mlp(self, inp, rows_per_expert, w1, w2):
-        """F64: w1 [G,H,F], w2 [G,F,H]; BF16: w1 [G,F,H], w2 [G,H,F] (K-major)."""
+    def grouped_mlp(self, inp, rows_per_expert, w1, w2, validate=True):
+        """F64: w1 [G,H,F], w2 [G,F,H]; BF16: w1 [G,F,H], w2 [G,H,F] (K-major).
+        The C-ABI checks the counts on the device without a host sync;
+        validate=True waits for the stream and raises the reference's
+        CountMismatch (xmoe_ctx_status) here."""
         rows, H = inp.shape
         G = rows_per_expert.shape[0]
         F = w1.shape[1] if inp.dtype == torch.bfloat16 else w1.shape[2]
@@ -297,6 +300,9 @@ class Context:
         _check(lib().xmoe_grouped_mlp(self.h, _dtype_code(inp), _ptr(inp), rows,
                                       _ptr(rows_per_expert), G, _ptr(w1), _ptr(w2), H, F,
                                       _ptr(out), _stream()))
+        if validate:
+            torch.cuda.current_stream().synchronize()
+            self.status()
         return out
 
     # ------------------------------------------------------------ synthetic inputs

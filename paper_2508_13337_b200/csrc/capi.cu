@@ -83,6 +83,7 @@ int* Ctx::err_flag() {
 Ctx::~Ctx() {
     if (ws) cudaFree(ws);
     if (dflag) cudaFree(dflag);
+    if (async_err_h) cudaFreeHost(async_err_h);
     if (nccl) ncclCommDestroy(static_cast<ncclComm_t>(nccl));
 }
 
@@ -114,6 +115,9 @@ int xmoe_ctx_create(int device, int world, int rank, const void* nccl_id, xmoe_c
         XMOE_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
         require(major == 10, XMOE_ERR_CUDA, "xmoe requires an sm_100 (B200) device");
         auto* c = new xmoe_ctx;
+        XMOE_CUDA(cudaHostAlloc(&c->c.async_err_h, sizeof(int), cudaHostAllocMapped));
+        *c->c.async_err_h = 0;
+        XMOE_CUDA(cudaHostGetDevicePointer(&c->c.async_err_d, c->c.async_err_h, 0));
         c->c.device = device;
         c->c.world = world;
         c->c.rank = rank;
@@ -244,16 +248,17 @@ int xmoe_grouped_mlp(xmoe_ctx* ctx, int dtype, const void* in, int64_t rows,
                      int64_t H, int64_t F, void* out, void* stream) {
     return guarded([&] {
         auto st = static_cast<cudaStream_t>(stream);
-        // CountMismatch check (pf_pipeline.cpp:102-103): segment counts must
-        // cover the input exactly
-        std::vector<int32_t> h(G);
-        if (G) XMOE_CUDA(cudaMemcpyAsync(h.data(), rows_per_expert, sizeof(int32_t) * G, cudaMemcpyDeviceToHost, st));
-        XMOE_CUDA(cudaStreamSynchronize(st));
-        long long tot = 0;
-        for (auto v : h) tot += v;
-        if (tot != rows) fail(XMOE_ERR_COUNT_MISMATCH, "grouped_expert_mlp: segment counts disagree with input rows");
+        require(G >= 1, XMOE_ERR_VALIDATION, "grouped_expert_mlp: at least one expert");
+        // CountMismatch check (pf_pipeline.cpp:102-103) on the device, no host
+        // sync: the GEMMs run on counts clamped to the buffer and a mismatch
+        // is reported by xmoe_ctx_status
         const size_t es = elem_size(dtype);
-        void* mid = ctx->c.scratch(static_cast<size_t>(rows) * F * es + 256);
+        const size_t mid_bytes = (static_cast<size_t>(rows) * F * es + 255) & ~static_cast<size_t>(255);
+        char* scr = static_cast<char*>(ctx->c.scratch(mid_bytes + sizeof(int32_t) * G + 256));
+        void* mid = scr;
+        auto* counts = reinterpret_cast<int32_t*>(scr + mid_bytes);
+        launch_count_check(rows_per_expert, static_cast<int>(G), rows, counts, ctx->c.async_err_d, st);
+        rows_per_expert = counts;
         if (dtype == XMOE_F64) {
             launch_grouped_gemm_f64(static_cast<const double*>(in), rows, H, rows_per_expert, G,
                                     static_cast<const double*>(w1), F, static_cast<double*>(mid), 1, st);
@@ -464,7 +469,18 @@ static void check_nccl_async(const Ctx& c) {
 }
 
 int xmoe_ctx_status(xmoe_ctx* ctx) {
-    return guarded([&] { check_nccl_async(ctx->c); });
+    return guarded([&] {
+        check_nccl_async(ctx->c);
+        if (ctx->c.async_err_h) {
+            const int e = *reinterpret_cast<volatile int*>(ctx->c.async_err_h);
+            if (e != 0) {
+                *ctx->c.async_err_h = 0;  // reported once
+                if (e == XMOE_ERR_COUNT_MISMATCH)
+                    fail(e, "grouped_expert_mlp: segment counts disagree with input rows");
+                fail(e, "asynchronous check failed");
+            }
+        }
+    });
 }
 
 int xmoe_layer_status(xmoe_layer* layer) {

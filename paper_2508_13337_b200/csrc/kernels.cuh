@@ -139,6 +139,7 @@ extern thread_local const float* g_gemm_addf;
 extern thread_local const unsigned* g_gemm_ready;
 extern thread_local int g_gemm_ready_mult;  // publications per row the ready counters count (default 1)
 bool gemm_2cta_enabled(int N);  // the 2-CTA kernel serves N (XMOE_GEMM, N % 32)
+void launch_count_check(const int32_t* rpe, int G, long long rows, int32_t* clamped, int* err, cudaStream_t st);
 // grid cap of the row-movement kernels (token scatter, slot combine; 0 =
 // their default).  The chunked forward runs them on a few SMs' worth of
 // blocks so the NVLink traffic they drive does not stall the GEMM CTAs on

@@ -20,6 +20,8 @@ struct Ctx {
     void* ws = nullptr;     // grow-only scratch for the stateless operators
     size_t ws_bytes = 0;
     void* dflag = nullptr;  // device error flag
+    int* async_err_h = nullptr;  // sticky error of asynchronous checks (host-mapped; xmoe_ctx_status)
+    int* async_err_d = nullptr;
 
     int n_local() const { return rank < 0 ? world : 1; }
     int rank_of(int i) const { return rank < 0 ? i : rank; }

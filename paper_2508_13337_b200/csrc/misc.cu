@@ -16,6 +16,32 @@ __global__ void recv_counts_kernel(const int32_t* __restrict__ tpe_all, int W, i
     rpe[le] = a;
 }
 
+// CountMismatch check of a grouped FFN on the device (pf_pipeline.cpp:102-103):
+// the groups must cover exactly `rows` rows.  Writes the counts clamped so
+// that their running sum never passes `rows` (the GEMMs run on these: no
+// access past the buffers whatever the caller passed) and, on a mismatch,
+// records XMOE_ERR_COUNT_MISMATCH in the context's host-mapped error word
+// (xmoe_ctx_status reports it) — no host synchronisation.
+__global__ void count_check_kernel(const int32_t* __restrict__ rpe, int G, long long rows,
+                                   int32_t* __restrict__ clamped, int* err) {
+    if (threadIdx.x != 0) return;
+    long long run = 0;
+    bool bad = false;
+    for (int g = 0; g < G; ++g) {
+        const long long v = rpe[g];
+        bad |= v < 0;
+        const long long c = v < 0 ? 0 : (run + v > rows ? rows - run : v);
+        clamped[g] = static_cast<int32_t>(c);
+        run += v < 0 ? 0 : v;
+    }
+    if (bad || run != rows) atomicCAS(err, 0, XMOE_ERR_COUNT_MISMATCH);
+}
+
+void launch_count_check(const int32_t* rpe, int G, long long rows, int32_t* clamped, int* err, cudaStream_t st) {
+    count_check_kernel<<<1, 32, 0, st>>>(rpe, G, rows, clamped, err);
+    XMOE_LAUNCH_CHECK();
+}
+
 __global__ void fill_i32_kernel(int32_t* p, int n, int32_t v) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;

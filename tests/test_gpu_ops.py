@@ -209,6 +209,13 @@ def test_grouped_mlp_f64_bit_exact(ctx):
     with pytest.raises(XmoeError, match="segment counts disagree") as ei:
         ctx.grouped_mlp(dev(inp), dev(seg + 1, torch.int32), dev(w.w1), dev(w.w2))
     assert ei.value.kind == "CountMismatch"
+    # the C-ABI call itself does not wait: the device check is reported by
+    # xmoe_ctx_status once, and the clamped counts keep the GEMMs in bounds
+    ctx.grouped_mlp(dev(inp), dev(seg * 3, torch.int32), dev(w.w1), dev(w.w2), validate=False)
+    torch.cuda.synchronize()
+    with pytest.raises(XmoeError, match="segment counts disagree"):
+        ctx.status()
+    ctx.status()  # reported once
 
 
 def _torch_grouped_gemm(A, seg, B, N, relu):
