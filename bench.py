@@ -712,7 +712,7 @@ def main():
                        "transport": (os.environ.get("XMOE_TRANSPORT") or "p2p") if world > 1 else "local",
                        "row_movement": (("owner-side pull" if os.environ.get("XMOE_DISPATCH", "pull") == "pull"
                                          else "source-side push") +
-                                        f", {os.environ.get('XMOE_COMM_SMS', '24')} whole SMs beside GEMMs on the rest"
+                                        f", {os.environ.get('XMOE_COMM_SMS', '28')} whole SMs beside GEMMs on the rest"
                                         if world > 1 and layer.chunks() > 1 and args.mode == "naive" else None),
                        "l2": f"working set > L2: {wbytes / 1e9:.2f} GB of expert weights per GPU + "
                              f"{S * H * 2 / 1e6:.0f} MB tokens stream each step (126 MB L2)"},

@@ -740,8 +740,11 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     // SMs, 1.07-1.17x, the copies at 460-660 GB/s)
     static const int comm_sms_env = [] {
         const char* e = std::getenv("XMOE_COMM_SMS");
-        return e ? std::max(0, std::min(kNumSMs / 2, std::atoi(e))) : 24;
+        return e ? std::max(0, std::min(kNumSMs / 2, std::atoi(e))) : 28;
     }();
+    // (C2, N=4, same box: 24 / 26 / 28 / 32 SMs -> 42.2 / 43.4 / 42.9-43.0 /
+    // 42.1-42.4 M tokens/s; N=2: 21.9 / - / 21.9 / 21.5; 20 and 16 starve the
+    // combines.  28 leaves headroom for N=8's larger off-rank share.)
     // RBD on the partition (XMOE_RBD_PARTITION=1, A/B): pack and combine as
     // whole-SM blocks.  Measured slower (C2 N=4, 2 chunks: 36.6 -> 33.5 M
     // tokens/s): the RBD combine's per-token group ordering needs more than
