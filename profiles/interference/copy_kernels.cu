@@ -86,7 +86,43 @@ void run_tma_pull(int64_t src_ptr, torch::Tensor dst, int64_t nbytes, int64_t gr
     if (!set) { cudaFuncSetAttribute(tma_copy, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 16384); set = true; }
     tma_copy<<<grid, 32, 4 * 16384, st>>>((const char*)src_ptr, (char*)dst.data_ptr(), nbytes);
 }
+
+// fat pull staged through shared memory with cp.async (LDGSTS): each of the
+// 1024 threads keeps a ring of R 16-byte slots in flight (R * 16 KB of smem
+// per block), no registers held by the loads in flight
+template <int R>
+__global__ void __launch_bounds__(1024) lds_pull(const int4* __restrict__ src, int4* __restrict__ dst, long long n) {
+    extern __shared__ int4 sm4[];
+    const int tid = threadIdx.x;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long i0 = blockIdx.x * (long long)blockDim.x + tid;
+    long long k = 0;  // element index of this thread: i0 + k * stride
+    const long long cnt = i0 < n ? (n - i0 + stride - 1) / stride : 0;
+    for (; k < cnt + R - 1; ++k) {
+        if (k < cnt) {
+            uint32_t d = (uint32_t)__cvta_generic_to_shared(&sm4[(k % R) * blockDim.x + tid]);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(d), "l"(src + i0 + k * stride) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        const long long w = k - (R - 1);
+        if (w >= 0) {
+            asm volatile("cp.async.wait_group %0;" :: "n"(R - 1) : "memory");
+            dst[i0 + w * stride] = sm4[(w % R) * blockDim.x + tid];
+        }
+    }
+}
+void run_lds_pull(int64_t src_ptr, torch::Tensor dst, int64_t nbytes, int64_t grid, int64_t ring) {
+    auto st = c10::cuda::getCurrentCUDAStream();
+    if (ring == 8) {
+        cudaFuncSetAttribute(lds_pull<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 16384);
+        lds_pull<8><<<grid, 1024, 8 * 16384, st>>>((const int4*)src_ptr, (int4*)dst.data_ptr(), nbytes / 16);
+    } else {
+        cudaFuncSetAttribute(lds_pull<13>, cudaFuncAttributeMaxDynamicSharedMemorySize, 13 * 16384);
+        lds_pull<13><<<grid, 1024, 13 * 16384, st>>>((const int4*)src_ptr, (int4*)dst.data_ptr(), nbytes / 16);
+    }
+}
+
 PYBIND11_MODULE(TORCH_EXTENSION_NAME, m) {
     m.def("run_sm", &run_sm); m.def("run_tma", &run_tma);
-    m.def("run_sm_pull", &run_sm_pull); m.def("run_fat", &run_fat); m.def("run_tma_pull", &run_tma_pull);
+    m.def("run_sm_pull", &run_sm_pull); m.def("run_fat", &run_fat); m.def("run_lds_pull", &run_lds_pull); m.def("run_tma_pull", &run_tma_pull);
 }
