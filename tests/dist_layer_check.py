@@ -260,6 +260,39 @@ def main():
                 failures.append(("ssmb", r, max_rel_diff(got[r][0], want)))
         print("ssmb checked on", world, "ranks", flush=True)
     del layer
+    dist.barrier()
+    # SSMB composed with EP on the pull-dispatch chunked layer against the
+    # replicated-expert SSMB layer: bit-identical, ragged last shard
+    Ss = 4096
+    S = world * Ss + 37
+    E, k, H, F = 16 * world, 6, 256, 128
+    el = E // world
+    rng = np.random.default_rng(91)
+    gate = grid_gate(rng, H, E)
+    w1 = bf16_round(rng.uniform(-0.1, 0.1, (E, H, F)))
+    w2 = bf16_round(rng.uniform(-0.1, 0.1, (E, F, H)))
+    x = grid_tokens(rng, 1, S, H)[0]
+    bv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).cuda()  # noqa: E731
+    kw = dict(num_experts=E, model_dim=H, ffn_dim=F, top_k=k, max_token_count=(Ss + 37) * k, max_tokens=Ss + 37,
+              dtype=capi.BF16, gate=bv(gate))
+    rep = capi.Layer(ctx, w1=bv(w1), w2=bv(w2), ssmb=True, **kw)
+    out_rep = rep.ssmb_forward(bv(x)).clone()
+    del rep
+    dist.barrier()
+    ep = capi.Layer(ctx, w1=bv(w1[rank * el:(rank + 1) * el]), w2=bv(w2[rank * el:(rank + 1) * el]), **kw)
+    outs = [ep.ssmb_forward(bv(x)).clone() for _ in range(2)]
+    torch.cuda.synchronize()
+    same = all(torch.equal(o, out_rep) for o in outs)
+    got = [None] * world
+    dist.all_gather_object(got, (same, ep.chunks()))
+    if rank == 0:
+        print(f"ssmb+ep vs replicated: chunks={[g[1] for g in got]} bit-identical={[g[0] for g in got]}",
+              flush=True)
+        if not all(g[0] for g in got):
+            failures.append(("ssmb+ep", [g[0] for g in got]))
+    ep.status()
+    del ep
+    dist.barrier()
     if rank == 0:
         print("FAILURES", failures, flush=True)
     ok = torch.tensor([0 if not failures else 1])
