@@ -535,3 +535,22 @@ def test_late_shared_knob_subprocess():
     print(r.stdout[-2000:], r.stderr[-2000:])
     assert r.returncode == 0
 
+
+
+@pytest.mark.parametrize("knob", ["XMOE_CHUNK_LATE=1", "XMOE_DISPATCH=push", "XMOE_COMM_SMS=0"])
+def test_chunked_knobs_subprocess(knob):
+    """The chunked forward's A/B knobs (read once per process, so run in a
+    fresh one): late shared GEMM2 beside the final combine, source-side pushes,
+    no SM partition — each bit-identical to the unchunked forward."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r); import pytest; "
+            "sys.exit(pytest.main(['-q', '-x', '-k', 'chunked_forward_bit_identical', %r]))"
+            % (root, os.path.abspath(__file__)))
+    name, value = knob.split("=")
+    env = dict(os.environ, **{name: value})
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-2000:], r.stderr[-2000:])
+    assert r.returncode == 0
