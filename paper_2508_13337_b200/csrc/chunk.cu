@@ -14,6 +14,16 @@
 // region instead of NCCL all-reduces: flag[phase][c][src] on every owner,
 // written with st.release.sys by the source after its phase-c work, polled
 // with ld.acquire.sys by the consumer.
+//
+// Row movement (default): owners PULL.  Every source stages its tokens in
+// its symmetric region and writes, for each kept copy, (source, token) into
+// the owner's row table; one flag later each owner copies its chunk-c rows
+// over NVLink (pull_rows_kernel), and the combine reads the owners' expert
+// outputs the same way.  Beside the expert GEMMs these kernels run as
+// whole-SM blocks on XMOE_COMM_SMS SMs the GEMMs leave free (layer.cu):
+// SM-driven NVLink traffic on the GEMMs' own SMs slows them up to 1.6x
+// (profiles/interference/).  XMOE_DISPATCH=push keeps the source-side
+// scatter (scatter_tokens_kernel with peer stores, a flag per chunk).
 #include <cstdlib>
 
 #include "common.cuh"
