@@ -9,13 +9,15 @@
 // Row movement between ranks.  Ranks that share a device (rank == -1
 // contexts, or world 1) and ranks in separate processes with NVLink peer
 // access ("p2p") use the SAME kernels over device pointer tables: the
-// dispatch kernel gathers token rows and stores them straight into the
-// owner's grouped expert input (a peer address when the owner is another
-// GPU), and the combine kernel reads expert outputs straight out of the
-// owners' buffers while it reduces.  No host synchronisation: the count
-// all-gather and two 4-byte all-reduces order the ranks.  The NCCL
-// send/recv transport (XMOE_TRANSPORT=nccl, plain dispatch only) is kept as
-// the library-collective baseline it is measured against.
+// unchunked dispatch kernel gathers token rows and stores them straight into
+// the owner's grouped expert input (a peer address when the owner is another
+// GPU); the token-chunked pipeline (default at N > 1) has the owners pull
+// their rows instead, on SMs the expert GEMMs leave free (chunk.cu); the
+// combine kernel reads expert outputs straight out of the owners' buffers
+// while it reduces.  No host synchronisation: the count all-gather and epoch
+// flags in the symmetric regions order the ranks.  The NCCL send/recv
+// transport (XMOE_TRANSPORT=nccl, plain dispatch only) is kept as the
+// library-collective baseline it is measured against.
 #include <nccl.h>
 
 #include <algorithm>
