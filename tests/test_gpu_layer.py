@@ -299,7 +299,7 @@ def test_graph_replay_matches_eager(mode):
 @pytest.mark.parametrize("W,S,chunks,cap_factor,shared", [(1, 1000, 2, None, True), (1, 4096, 8, None, True),
                                                           (4, 333, 3, None, False), (4, 512, 4, 0.5, True),
                                                           (2, 3, 4, None, False), (8, 700, 5, None, True),
-                                                          (2, 6144, 2, None, True)])
+                                                          (2, 6144, 2, None, True), (8, 2048, 3, 0.5, True)])
 def test_chunked_forward_bit_identical(W, S, chunks, cap_factor, shared, mode):
     """The token-chunked pipelined forward (chunk.cu), plain and
     redundancy-bypassing, is bit-identical to the unchunked one — ragged
