@@ -774,35 +774,9 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     auto slot_A = [](int c) { return c; };
     auto slot_B = [](int c) { return kMaxChunks + c; };
 
-    // XMOE_CHUNK_SHARED=side (A/B): the shared-expert GEMMs on the side
-    // stream (SM-limited, XMOE_SHARED_SMS) beside the routed chunks instead of
-    // ahead of them on st; the first combine waits for them
-    static const bool shared_side = [] {
-        const char* e = std::getenv("XMOE_CHUNK_SHARED");
-        return e && std::string(e) == "side";
-    }();
-    const bool sh_side = shared_side && L.Fs > 0;
     L.mark(kEvStart, st);
     for (int i = 0; i < nl; ++i)
         launch_forward_begin(L.workers[i].s_rows, static_cast<int>(S), i == 0 ? L.epoch : nullptr, st);
-    if (sh_side) {
-        XMOE_CUDA(cudaEventRecord(L.ev_fork, st));
-        XMOE_CUDA(cudaStreamWaitEvent(L.side, L.ev_fork, 0));
-        if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side0, L.side));
-        static const int shared_sms = [] {
-            const char* e = std::getenv("XMOE_SHARED_SMS");
-            return e ? std::atoi(e) : 104;
-        }();
-        g_gemm_sm_limit = shared_sms;
-        for (int i = 0; i < nl; ++i) {
-            Worker& w = L.workers[i];
-            launch_grouped_gemm_bf16(x_of(i), S, H, w.s_rows, 1, L.sw1, L.Fs, w.smid, 1, L.side);
-            launch_grouped_gemm_bf16(w.smid, S, L.Fs, w.s_rows, 1, L.sw2, H, w.sout, 0, L.side);
-        }
-        g_gemm_sm_limit = 0;
-        if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side1, L.side));
-        XMOE_CUDA(cudaEventRecord(L.ev_join, L.side));
-    }
     for (int i = 0; i < nl; ++i) route_gate(L, L.workers[i], x_of(i), S, st);  // 1. gate (gating.cpp:14-57)
     L.mark(kEvGate, st);
     XMOE_CUDA(cudaEventRecord(L.ev_fork, st));
@@ -900,7 +874,7 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     L.mark(kEvDispatch, cm);
     // 3. st: shared experts (x only), then the routed experts chunk by chunk
     //    (pf_pipeline.cpp:83-105)
-    if (L.Fs > 0 && !sh_side) {
+    if (L.Fs > 0) {
         if (L.timing) XMOE_CUDA(cudaEventRecord(L.ev_side0, st));
         g_gemm_sm_limit = gemm_sms;
         for (int i = 0; i < nl; ++i) {
@@ -944,7 +918,6 @@ static void layer_forward_chunked(Layer& L, const void* x, long long S, void* ou
     L.mark(kEvShared, st);
     // 4. comm: each chunk's weighted combine as soon as every owner finished
     //    it (pf_pipeline.cpp:107-135)
-    if (sh_side) XMOE_CUDA(cudaStreamWaitEvent(cm, L.ev_join, 0));
     for (int c = 0; c < C; ++c) {
         g_copy_blocks = c == C - 1 ? 0 : blk_combine;  // the last combine runs alone
         g_copy_fat = c == C - 1 && !late ? 0 : comm_sms;  // (late: beside shared GEMM2)

@@ -537,11 +537,13 @@ def test_late_shared_knob_subprocess():
 
 
 
-@pytest.mark.parametrize("knob", ["XMOE_CHUNK_LATE=1", "XMOE_DISPATCH=push", "XMOE_COMM_SMS=0"])
+@pytest.mark.parametrize("knob", ["XMOE_CHUNK_LATE=1", "XMOE_DISPATCH=push", "XMOE_COMM_SMS=0",
+                                  "XMOE_RBD_PARTITION=1"])
 def test_chunked_knobs_subprocess(knob):
     """The chunked forward's A/B knobs (read once per process, so run in a
     fresh one): late shared GEMM2 beside the final combine, source-side pushes,
-    no SM partition — each bit-identical to the unchunked forward."""
+    no SM partition, RBD on the partition — each bit-identical to the
+    unchunked forward."""
     import os
     import subprocess
     import sys
